@@ -1,0 +1,234 @@
+/*
+ * switchback_b200.h — the C-ABI drop-in boundary of the B200 SwitchBack path.
+ *
+ * Plain pointers and sizes only (no torch, no C++ types). Device pointers
+ * unless an entry point says "host". Every call is stream-ordered on the
+ * handle's CUDA stream and returns as soon as the work is enqueued; device-side
+ * input errors (non-finite values, which the reference rejects up front) are
+ * latched in the handle and reported by sb_synchronize().
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj/core). The C++ shim in
+ * paper_2304_13013_b200/csrc/lowprec_shim.cpp re-exposes the reference's own
+ * lowprec:: signatures (host Matrix in, host Matrix out) on top of this ABI.
+ */
+#ifndef SWITCHBACK_B200_H
+#define SWITCHBACK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SB_ABI_VERSION 1
+
+typedef enum sb_status {
+  SB_OK = 0,
+  SB_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  SB_ERR_NONFINITE = 2,        /* "non-finite input" (quantize.cpp:11-14, linear.cpp:91-92) */
+  SB_ERR_CUDA = 3,
+  SB_ERR_UNSUPPORTED = 4
+} sb_status;
+
+typedef enum sb_dtype { SB_F32 = 0, SB_BF16 = 1, SB_I32 = 2, SB_I8 = 3, SB_U8 = 4, SB_I64 = 5 } sb_dtype;
+
+/* QuantAxis, quantize.hpp:12 */
+typedef enum sb_axis { SB_AXIS_ROW = 0, SB_AXIS_COLUMN = 1, SB_AXIS_TENSOR = 2 } sb_axis;
+
+/* Fp8Format::e4m3() / e5m2(), quantize.hpp:30-31 */
+typedef enum sb_fp8_format { SB_E4M3 = 0, SB_E5M2 = 1 } sb_fp8_format;
+
+/* LinearVariant, linear.hpp:23 */
+typedef enum sb_variant {
+  SB_STANDARD = 0,
+  SB_SWITCHBACK = 1,
+  SB_SWITCHBACK_M = 2,
+  SB_SWITCHBACK_Q = 3,
+  SB_ALLQUANT = 4
+} sb_variant;
+
+/* NumericFormat, linear.hpp:25 */
+typedef enum sb_numeric_format { SB_INT8 = 0, SB_FP8 = 1 } sb_numeric_format;
+
+/* State application of the int8 GEMM epilogue (linear.cpp:54-83). */
+typedef enum sb_scale_mode {
+  SB_SCALE_ROW_TENSOR = 0, /* int8_matmul_dequant: state_a[i] * state_b / 127^2 (linear.hpp:54) */
+  SB_SCALE_ROW_ROW = 1,    /* matmul_dequant_dual_rowwise: state_a[i] * state_b[j] / 127^2 (linear.hpp:58) */
+  SB_SCALE_NONE = 2        /* raw integer accumulators (out dtype SB_I32, or SB_I64 beyond k = 133144) */
+} sb_scale_mode;
+
+/* Clipping, optimizer.hpp:12-16 */
+typedef enum sb_clipping { SB_CLIP_NONE = 0, SB_CLIP_UPDATE = 1, SB_CLIP_GRAD = 2 } sb_clipping;
+
+typedef struct sb_handle_s* sb_handle;
+
+/* ------------------------------------------------------------ runtime -- */
+int sb_abi_version(void);
+/* Creates a handle bound to `device` (cudaSetDevice semantics) on the default stream. */
+sb_status sb_create(int device, sb_handle* out);
+sb_status sb_destroy(sb_handle h);
+/* `cuda_stream` is a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream). */
+sb_status sb_set_stream(sb_handle h, void* cuda_stream);
+/* Waits for the handle's stream; returns SB_ERR_NONFINITE (and clears the latch)
+ * when a kernel saw a NaN/Inf input since the last call. */
+sb_status sb_synchronize(sb_handle h);
+/* Non-blocking device error latch (device pointer to one uint32; bit 0 = non-finite). */
+uint32_t* sb_error_word(sb_handle h);
+/* "<op>: <reason>" — the reference's exception text for the last failure on this thread. */
+const char* sb_last_error(void);
+/* Kernel launches issued through this handle so far (launch accounting for bench.py). */
+uint64_t sb_launch_count(sb_handle h);
+
+/* ----------------------------------------------------------- quantize -- */
+/* quantize_rowwise, quantize.hpp:67 / quantize.cpp:131-133.
+ * x: rows x cols (leading dim ldx elements) of `dt` (SB_F32 or SB_BF16);
+ * q: int8 rows x cols (ldq); state: rows floats (absmax, 1.0 for all-zero rows). */
+sb_status sb_quantize_rowwise(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                              int8_t* q, int64_t ldq, float* state);
+
+/* quantize_columnwise, quantize.hpp:68 / quantize.cpp:135-137. q (rows x cols, ldq) and/or
+ * q_t (cols x rows, ldqt; = quantize_rowwise(x^T), the SwitchBackQ weight path linear.cpp:228-229)
+ * may be NULL; state: cols floats. */
+sb_status sb_quantize_columnwise(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                                 int8_t* q, int64_t ldq, int8_t* q_t, int64_t ldqt, float* state);
+
+/* quantize_tensorwise + quantize_tensorwise_transpose, quantize.hpp:69-71 /
+ * quantize.cpp:139-159: one absmax pass, one quantize pass writing q (rows x cols)
+ * and/or q_t (cols x rows) from a single read. state: 1 float. */
+sb_status sb_quantize_tensorwise(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                                 int8_t* q, int64_t ldq, int8_t* q_t, int64_t ldqt, float* state);
+
+/* dequantize (int8 branch), quantize.hpp:76 / quantize.cpp:178-197:
+ * y = float(double(p) * double(state) / 127). y dtype SB_F32 (bit-exact) or SB_BF16. */
+sb_status sb_dequantize(sb_handle h, const int8_t* q, int64_t rows, int64_t cols, int64_t ldq, const float* state,
+                        sb_axis axis, void* y, sb_dtype ydt, int64_t ldy);
+
+/* quantize_fp8, quantize.hpp:73 / quantize.cpp:161-176: payload = snap(x / state) with
+ * ties to the smaller magnitude, stored as e4m3 / e5m2 bytes (decode = the reference's
+ * payload_fp8 value). state: rows / cols / 1 floats per axis. */
+sb_status sb_quantize_fp8(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                          sb_fp8_format fmt, sb_axis axis, uint8_t* q, int64_t ldq, float* state);
+
+/* dequantize (fp8 branch), quantize.cpp:185-189: y = float(double(value(p)) * double(state)). */
+sb_status sb_dequantize_fp8(sb_handle h, const uint8_t* q, int64_t rows, int64_t cols, int64_t ldq, sb_fp8_format fmt,
+                            const float* state, sb_axis axis, void* y, sb_dtype ydt, int64_t ldy);
+
+/* --------------------------------------------------------------- GEMM -- */
+/* int8_matmul_dequant / matmul_dequant_dual_rowwise, linear.hpp:54-58 / linear.cpp:39-83.
+ * out[M x N] (ld N) = (qa[M x K] . qb[N x K]^T) with the state epilogue of `mode`.
+ * Both operands K-major (row-major, leading dim K). Output dtype:
+ *   SB_F32 + exact=1 : float(double(acc) * sa_i * sb_j / 16129.0), bit-identical to linear.cpp:49
+ *   SB_F32 + exact=0 : same formula in fp32
+ *   SB_BF16          : fp32 formula rounded to bf16 (the performance path)
+ *   SB_I32 / SB_I64  : raw accumulators (mode must be SB_SCALE_NONE) */
+sb_status sb_gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* qb, const float* sb,
+                     sb_scale_mode mode, int64_t M, int64_t N, int64_t K, void* out, sb_dtype out_dt, int exact);
+
+/* matmul, matrix.hpp:51 / matrix.cpp:53-68: y[r x c] = a[r x k] . bt[c x k]^T with a strictly
+ * sequential fp32 reduction per output and no FMA — bit-identical to the reference. */
+sb_status sb_matmul_f32(sb_handle h, const float* a, const float* bt, int64_t r, int64_t c, int64_t k, float* y);
+
+/* wgrad_full_precision, linear.cpp:193-195: dw[m x n] (+)= g[b x m]^T . x[b x n].
+ *   exact=1 (SB_F32 in): sequential fp32 over the b tokens, bit-identical to the reference.
+ *   exact=0 (SB_BF16 in): bf16 tcgen05 GEMM reading g and x in place (MN-major), fp32 out.
+ * accumulate=1 adds into dw (fp32) instead of overwriting. */
+sb_status sb_wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m, int64_t n,
+                   float* dw, int exact, int accumulate);
+
+/* fp8 GEMM (the SwitchBack fp8 simulation, linear.cpp:148-153 / :250-266): out = (qa . qb^T)
+ * * sa_i * sb_j with qa/qb e4m3|e5m2 bytes, K-major; states per row (row axis) or broadcast
+ * (tensor axis). Tensor-core accumulation (fp32) — tolerance parity. */
+sb_status sb_gemm_fp8(sb_handle h, const uint8_t* qa, sb_fp8_format fa, const float* sa, sb_axis axa,
+                      const uint8_t* qb, sb_fp8_format fb, const float* sb, sb_axis axb, int64_t M, int64_t N,
+                      int64_t K, void* out, sb_dtype out_dt);
+
+/* ------------------------------------------------------------- layer ---- */
+/* LinearMode, linear.hpp:30-35. exact = 1 selects the reference-bit-exact numerics
+ * (fp32 I/O, fp64 dequant epilogue, sequential fp32 weight gradient); exact = 0 is the
+ * B200 performance path (bf16 I/O, tcgen05 int8 + bf16 GEMMs, fp32 dW). */
+typedef struct sb_linear_mode {
+  int32_t variant;      /* sb_variant */
+  int32_t format;       /* sb_numeric_format */
+  int32_t fp8_forward;  /* sb_fp8_format, default SB_E4M3 */
+  int32_t fp8_gradient; /* sb_fp8_format, default SB_E5M2 */
+  int32_t exact;
+} sb_linear_mode;
+
+/* LinearContext, linear.hpp:39-48. Filled by sb_linear_forward; consumed by
+ * sb_linear_backward. Unlike the reference (deep copies, linear.cpp:140-143) it
+ * references the caller's x and w, which must stay alive and unmodified until
+ * the backward; quantized tensors live in the caller's workspace. */
+typedef struct sb_linear_ctx {
+  sb_linear_mode mode;
+  int64_t b, n, m;
+  sb_dtype dt;
+  const void* x; /* b x n */
+  const void* w; /* m x n */
+  int8_t* w_q_t; /* cached W_int8^T (n x m, tensor-wise), reused by the backward */
+  float* w_state;
+  int8_t* x_q; /* SwitchBackM: saved X_int8 (b x n) + row states */
+  float* x_state;
+  void* workspace;
+  size_t workspace_bytes;
+  int32_t valid;
+} sb_linear_ctx;
+
+/* Workspace the forward+backward pair needs (caller allocates once, reuses). */
+sb_status sb_linear_workspace_size(const sb_linear_mode* mode, int64_t b, int64_t n, int64_t m, size_t* bytes);
+
+/* linear_forward, linear.hpp:62-63 / linear.cpp:113-164: y[b x m] = X W^T through the
+ * variant's quantized path. x/w/y are `dt` (SB_F32 or SB_BF16). ctx may be NULL. */
+sb_status sb_linear_forward(sb_handle h, const sb_linear_mode* mode, const void* x, const void* w, sb_dtype dt,
+                            int64_t b, int64_t n, int64_t m, void* y, sb_linear_ctx* ctx, void* workspace,
+                            size_t workspace_bytes);
+
+/* linear_backward, linear.hpp:66-67 / linear.cpp:199-278: {dx [b x n] (dt), dw [m x n] (fp32)}.
+ * dw_accumulate = 1 adds into dw (gradient accumulation / DP bucket). */
+sb_status sb_linear_backward(sb_handle h, const sb_linear_mode* mode, const sb_linear_ctx* ctx, const void* g,
+                             void* dx, float* dw, int dw_accumulate);
+
+/* The reference bench's `switchback_fwd_bwd` unit (bench.cpp:75-81) over HOST buffers:
+ * copies x (b x n), w (m x n), g (b x m) in, runs forward + backward, copies y, dx, dw
+ * out. Token rows are pipelined in chunks across two streams so PCIe copies overlap
+ * the kernels. dt applies to x, w, g, y, dx; dw is fp32. Host buffers should be pinned. */
+sb_status sb_switchback_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, const void* x, const void* w,
+                                     const void* g, sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y, void* dx,
+                                     float* dw);
+
+/* --------------------------------------------------------- optimizer ---- */
+/* TensorRef, optimizer.hpp:74-79 (device pointers, fp32, numel elements each). */
+typedef struct sb_adamw_tensor {
+  float* theta;
+  const float* grad;
+  float* v;
+  float* u;
+  int64_t numel;
+} sb_adamw_tensor;
+
+/* OptimizerHyperparams, optimizer.hpp:21-33, with alpha = lr_schedule(t) evaluated by the
+ * caller (the reference evaluates its host std::function, optimizer.cpp:114). */
+typedef struct sb_adamw_hparams {
+  double alpha;
+  double beta1;
+  double beta2;
+  double beta2_warmup_lambda; /* > 0 selects beta2_warmup (optimizer.cpp:44-49) */
+  double eps;
+  double weight_decay;
+  double max_grad_norm; /* kGradClip only */
+  int32_t clipping;     /* sb_clipping */
+} sb_adamw_hparams;
+
+sb_status sb_stableadamw_workspace_size(const sb_adamw_tensor* tensors, int ntensors, size_t* bytes);
+
+/* optimizer_step, optimizer.hpp:85-86 / optimizer.cpp:102-172. `tensors` is a HOST array.
+ * rms_out / eta_out: DEVICE arrays of ntensors doubles (TensorStepInfo, optimizer.hpp:69-72),
+ * may be NULL. Element math in fp64 mirroring optimizer.cpp:142-146,162-167. */
+sb_status sb_stableadamw_step(sb_handle h, const sb_adamw_tensor* tensors, int ntensors, const sb_adamw_hparams* hp,
+                              int64_t t, double* rms_out, double* eta_out, void* workspace, size_t workspace_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWITCHBACK_B200_H */

@@ -1,0 +1,683 @@
+// capi.cu — the extern "C" boundary (include/switchback_b200.h).
+//
+// Argument checks reproduce the reference's std::invalid_argument conditions and
+// messages ("<op>: <reason>", quantize.cpp:11-14, linear.cpp:55,73-74,80-81,87-93,
+// 201-208, optimizer.cpp:104-112) as sb_status codes + sb_last_error() text.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "sb_internal.h"
+
+namespace sb {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+sb_status fail(sb_status st, const char* op, const char* reason) {
+  g_last_error = std::string(op) + ": " + reason;
+  return st;
+}
+
+sb_status cuda_fail(const char* op, cudaError_t e) {
+  g_last_error = std::string(op) + ": CUDA error: " + cudaGetErrorString(e);
+  return SB_ERR_CUDA;
+}
+
+unsigned int* scratch(sb_handle h, size_t words) {
+  const size_t bytes = words * sizeof(unsigned int);
+  if (bytes > h->scratch_bytes) {
+    if (h->d_scratch) {
+      cudaStreamSynchronize(h->stream);
+      cudaFree(h->d_scratch);
+    }
+    h->d_scratch = nullptr;
+    h->scratch_bytes = 0;
+    size_t want = std::max<size_t>(bytes, 4096);
+    if (cudaMalloc(&h->d_scratch, want) != cudaSuccess) return nullptr;
+    h->scratch_bytes = want;
+  }
+  return h->d_scratch;
+}
+
+}  // namespace sb
+
+namespace {
+
+// Device constant 1.0f used as the "no scale" state of plain bf16 GEMMs.
+__device__ float g_one = 1.0f;
+
+struct Carve {
+  uint8_t* base;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+// Workspace carve-up shared by sb_linear_workspace_size / forward / backward.
+struct LinearWs {
+  int8_t* x_q;
+  float* x_state;
+  int8_t* w_q;
+  int8_t* w_qt;
+  float* w_state;  // 1 (tensor) or m (row-wise W, SwitchBackQ forward)
+  float* wt_state; // n (column-wise W = rows of W^T, SwitchBackQ backward)
+  unsigned int* words;  // absmax words: max(m, n, b) + 1
+  int8_t* g_q;
+  float* g_state;
+  void* deq;       // SwitchBackM / fp8: dequantized operand buffer (b x n, dt)
+  void* deq2;      // fp8 AllQuant: snapped G (b x m, dt)
+  int8_t* gt_q;    // AllQuant int8: quantize_rowwise(G^T)  m x b
+  float* gt_state;
+  int8_t* xt_q;    // AllQuant int8: quantize_rowwise(X^T)  n x b
+  float* xt_state;
+  size_t total;
+};
+
+LinearWs carve(const sb_linear_mode& md, int64_t b, int64_t n, int64_t m, sb_dtype dt, void* base) {
+  Carve c{static_cast<uint8_t*>(base)};
+  LinearWs w{};
+  const size_t es = dt == SB_BF16 ? 2 : 4;
+  w.x_q = c.take<int8_t>(b * n);
+  w.x_state = c.take<float>(b);
+  w.w_q = c.take<int8_t>(m * n);
+  w.w_qt = c.take<int8_t>(m * n);
+  w.w_state = c.take<float>(std::max<int64_t>(m, 1));
+  w.wt_state = c.take<float>(std::max<int64_t>(n, 1));
+  w.words = c.take<unsigned int>(std::max(std::max(m, n), b) + 1);
+  w.g_q = c.take<int8_t>(b * m);
+  w.g_state = c.take<float>(b);
+  const bool need_deq = md.variant == SB_SWITCHBACK_M || md.format == SB_FP8;
+  w.deq = need_deq ? static_cast<void*>(c.take<uint8_t>(b * n * es)) : nullptr;
+  w.deq2 = (md.format == SB_FP8 && md.variant == SB_ALLQUANT) ? static_cast<void*>(c.take<uint8_t>(b * m * es)) : nullptr;
+  if (md.format == SB_INT8 && md.variant == SB_ALLQUANT) {
+    w.gt_q = c.take<int8_t>(m * b);
+    w.gt_state = c.take<float>(m);
+    w.xt_q = c.take<int8_t>(n * b);
+    w.xt_state = c.take<float>(n);
+  }
+  w.total = c.off + 256;
+  return w;
+}
+
+#define SB_TRY(expr)                       \
+  do {                                     \
+    sb_status _s = (expr);                 \
+    if (_s != SB_OK) return _s;            \
+  } while (0)
+#define SB_TRYC(op, expr) SB_CUDA_CHECK(op, (expr))
+
+__global__ void k_transpose_u8(const uint8_t* __restrict__ in, int64_t rows, int64_t cols, uint8_t* __restrict__ out) {
+  __shared__ uint8_t t[32][33];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32, c0 = static_cast<int64_t>(blockIdx.x) * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) t[i][threadIdx.x] = in[r * cols + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[c * rows + r] = t[threadIdx.x][i];
+  }
+}
+
+sb_status transpose_u8(sb_handle h, const void* in, int64_t rows, int64_t cols, void* out) {
+  const dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+  h->launches++;
+  k_transpose_u8<<<grid, dim3(32, 8), 0, h->stream>>>(static_cast<const uint8_t*>(in), rows, cols,
+                                                        static_cast<uint8_t*>(out));
+  SB_LAUNCH_CHECK("transpose");
+  return SB_OK;
+}
+
+bool float_dtype(sb_dtype dt) { return dt == SB_F32 || dt == SB_BF16; }
+
+sb_status check_h(sb_handle h, const char* op) {
+  if (!h) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "null handle");
+  cudaSetDevice(h->device);
+  return SB_OK;
+}
+
+// ------------------------------------------------------------ quantize ops
+sb_status q_tensorwise(sb_handle h, const void* x, sb_dtype dt, int64_t r, int64_t c, int64_t ldx, int8_t* q,
+                       int64_t ldq, int8_t* qt, int64_t ldqt, float* state, unsigned int* word) {
+  SB_TRYC("quantize_tensorwise", sb::launch_absmax_tensor(h, x, dt, r, c, ldx, word));
+  SB_TRYC("quantize_tensorwise", sb::launch_quantize_from_words(h, x, dt, r, c, ldx, word, 0, q, ldq, qt, ldqt, state));
+  return SB_OK;
+}
+
+sb_status q_columnwise(sb_handle h, const void* x, sb_dtype dt, int64_t r, int64_t c, int64_t ldx, int8_t* q,
+                       int64_t ldq, int8_t* qt, int64_t ldqt, float* state, unsigned int* words) {
+  SB_TRYC("quantize_columnwise", sb::launch_absmax_columns(h, x, dt, r, c, ldx, words));
+  SB_TRYC("quantize_columnwise", sb::launch_quantize_from_words(h, x, dt, r, c, ldx, words, 1, q, ldq, qt, ldqt, state));
+  return SB_OK;
+}
+
+sb_status q_fp8(sb_handle h, const void* x, sb_dtype dt, int64_t r, int64_t c, int64_t ldx, int fmt, int axis,
+                uint8_t* q, int64_t ldq, float* state, unsigned int* words) {
+  const char* op = "quantize_fp8";
+  if (axis == SB_AXIS_ROW) {
+    SB_TRYC(op, sb::launch_absmax_rows(h, x, dt, r, c, ldx, words));
+  } else if (axis == SB_AXIS_COLUMN) {
+    SB_TRYC(op, sb::launch_absmax_columns(h, x, dt, r, c, ldx, words));
+  } else {
+    SB_TRYC(op, sb::launch_absmax_tensor(h, x, dt, r, c, ldx, words));
+  }
+  SB_TRYC(op, sb::launch_quantize_fp8(h, x, dt, r, c, ldx, fmt, axis, words, q, ldq, state));
+  return SB_OK;
+}
+
+// --------------------------------------------------------- plain bf16 GEMM
+// (Standard-mode linear, fast path). a: [M x K] K-major or [K x M] MN-major, b likewise.
+sb_status gemm_bf16(sb_handle h, const void* a, bool a_mn, const void* b, bool b_mn, int64_t M, int64_t N, int64_t K,
+                    void* out, sb_dtype out_dt);
+
+}  // namespace
+
+// ======================================================================
+extern "C" {
+
+int sb_abi_version(void) { return SB_ABI_VERSION; }
+
+sb_status sb_create(int device, sb_handle* out) {
+  if (!out) return sb::fail(SB_ERR_INVALID_ARGUMENT, "sb_create", "null out");
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) return sb::fail(SB_ERR_CUDA, "sb_create", "no CUDA device");
+  if (device < 0 || device >= count) return sb::fail(SB_ERR_INVALID_ARGUMENT, "sb_create", "bad device");
+  SB_CUDA_CHECK("sb_create", cudaSetDevice(device));
+  cudaDeviceProp prop;
+  SB_CUDA_CHECK("sb_create", cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return sb::fail(SB_ERR_UNSUPPORTED, "sb_create", "requires an sm_100 (B200) device");
+  sb_handle h = new sb_handle_s();
+  h->device = device;
+  h->num_sms = prop.multiProcessorCount;
+  if (cudaMalloc(&h->d_err, sizeof(uint32_t)) != cudaSuccess) {
+    delete h;
+    return sb::fail(SB_ERR_CUDA, "sb_create", "allocation failed");
+  }
+  cudaMemset(h->d_err, 0, sizeof(uint32_t));
+  cudaDeviceSynchronize();
+  *out = h;
+  return SB_OK;
+}
+
+sb_status sb_destroy(sb_handle h) {
+  if (!h) return SB_OK;
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  if (h->d_err) cudaFree(h->d_err);
+  if (h->d_scratch) cudaFree(h->d_scratch);
+  if (h->dev_pool) cudaFree(h->dev_pool);
+  delete h;
+  return SB_OK;
+}
+
+sb_status sb_set_stream(sb_handle h, void* s) {
+  if (!h) return sb::fail(SB_ERR_INVALID_ARGUMENT, "sb_set_stream", "null handle");
+  h->stream = static_cast<cudaStream_t>(s);
+  return SB_OK;
+}
+
+sb_status sb_synchronize(sb_handle h) {
+  SB_TRY(check_h(h, "sb_synchronize"));
+  SB_CUDA_CHECK("sb_synchronize", cudaStreamSynchronize(h->stream));
+  uint32_t flags = 0;
+  SB_CUDA_CHECK("sb_synchronize", cudaMemcpy(&flags, h->d_err, sizeof(flags), cudaMemcpyDeviceToHost));
+  if (flags) {
+    cudaMemset(h->d_err, 0, sizeof(uint32_t));
+    return sb::fail(SB_ERR_NONFINITE, "switchback", "non-finite input");
+  }
+  return SB_OK;
+}
+
+uint32_t* sb_error_word(sb_handle h) { return h ? h->d_err : nullptr; }
+
+const char* sb_last_error(void) { return sb::g_last_error.c_str(); }
+
+uint64_t sb_launch_count(sb_handle h) { return h ? h->launches : 0; }
+
+// ------------------------------------------------------------ quantize --
+sb_status sb_quantize_rowwise(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                              int8_t* q, int64_t ldq, float* state) {
+  const char* op = "quantize_rowwise";
+  SB_TRY(check_h(h, op));
+  if (rows <= 0 || cols <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty matrix");
+  if (!float_dtype(dt) || !x || !q || !state || ldx < cols || ldq < cols)
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  SB_TRYC(op, sb::launch_quantize_rowwise(h, x, dt, rows, cols, ldx, q, ldq, state));
+  return SB_OK;
+}
+
+sb_status sb_quantize_columnwise(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                                 int8_t* q, int64_t ldq, int8_t* q_t, int64_t ldqt, float* state) {
+  const char* op = "quantize_columnwise";
+  SB_TRY(check_h(h, op));
+  if (rows <= 0 || cols <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty matrix");
+  if (!float_dtype(dt) || !x || (!q && !q_t) || !state || ldx < cols) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  unsigned int* words = sb::scratch(h, cols + 1);
+  if (!words) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed");
+  return q_columnwise(h, x, dt, rows, cols, ldx, q, ldq, q_t, ldqt, state, words);
+}
+
+sb_status sb_quantize_tensorwise(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                                 int8_t* q, int64_t ldq, int8_t* q_t, int64_t ldqt, float* state) {
+  const char* op = q ? "quantize_tensorwise" : "quantize_tensorwise_transpose";
+  SB_TRY(check_h(h, op));
+  if (rows <= 0 || cols <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty matrix");
+  if (!float_dtype(dt) || !x || (!q && !q_t) || !state || ldx < cols) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  unsigned int* words = sb::scratch(h, 1);
+  if (!words) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed");
+  return q_tensorwise(h, x, dt, rows, cols, ldx, q, ldq, q_t, ldqt, state, words);
+}
+
+sb_status sb_dequantize(sb_handle h, const int8_t* q, int64_t rows, int64_t cols, int64_t ldq, const float* state,
+                        sb_axis axis, void* y, sb_dtype ydt, int64_t ldy) {
+  const char* op = "dequantize";
+  SB_TRY(check_h(h, op));
+  if (!q || !state || !y || !float_dtype(ydt) || axis < 0 || axis > 2)
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "state length does not match axis");
+  if (rows == 0 || cols == 0) return SB_OK;
+  SB_TRYC(op, sb::launch_dequantize(h, q, rows, cols, ldq, state, axis, y, ydt, ldy));
+  return SB_OK;
+}
+
+sb_status sb_quantize_fp8(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                          sb_fp8_format fmt, sb_axis axis, uint8_t* q, int64_t ldq, float* state) {
+  const char* op = "quantize_fp8";
+  SB_TRY(check_h(h, op));
+  if (rows <= 0 || cols <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty matrix");
+  if (!float_dtype(dt) || !x || !q || !state || (fmt != SB_E4M3 && fmt != SB_E5M2) || axis < 0 || axis > 2)
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  unsigned int* words = sb::scratch(h, std::max(rows, cols) + 1);
+  if (!words) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed");
+  return q_fp8(h, x, dt, rows, cols, ldx, fmt, axis, q, ldq, state, words);
+}
+
+sb_status sb_dequantize_fp8(sb_handle h, const uint8_t* q, int64_t rows, int64_t cols, int64_t ldq, sb_fp8_format fmt,
+                            const float* state, sb_axis axis, void* y, sb_dtype ydt, int64_t ldy) {
+  const char* op = "dequantize";
+  SB_TRY(check_h(h, op));
+  if (!q || !state || !y || !float_dtype(ydt)) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  if (rows == 0 || cols == 0) return SB_OK;
+  SB_TRYC(op, sb::launch_dequantize_fp8(h, q, rows, cols, ldq, fmt, state, axis, y, ydt, ldy));
+  return SB_OK;
+}
+
+// ---------------------------------------------------------------- GEMM --
+sb_status sb_gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* qb, const float* sbp,
+                     sb_scale_mode mode, int64_t M, int64_t N, int64_t K, void* out, sb_dtype out_dt, int exact) {
+  const char* op = mode == SB_SCALE_ROW_ROW ? "matmul_dequant_dual_rowwise" : "int8_matmul_dequant";
+  SB_TRY(check_h(h, op));
+  if (M < 0 || N < 0 || K < 0 || !qa || !qb || !out) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  if (mode != SB_SCALE_NONE && (!sa || !sbp)) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "missing states");
+  if (M == 0 || N == 0) return SB_OK;
+  return sb::gemm_i8(h, qa, sa, qb, sbp, mode, M, N, K, out, out_dt, exact);
+}
+
+sb_status sb_matmul_f32(sb_handle h, const float* a, const float* bt, int64_t r, int64_t c, int64_t k, float* y) {
+  const char* op = "matmul";
+  SB_TRY(check_h(h, op));
+  if (!a || !bt || !y || r < 0 || c < 0 || k < 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "inner dimension mismatch");
+  if (r == 0 || c == 0) return SB_OK;
+  return sb::matmul_f32_seq(h, a, k, 1, bt, k, 1, r, c, k, y, 0);
+}
+
+sb_status sb_wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m, int64_t n, float* dw,
+                   int exact, int accumulate) {
+  const char* op = "linear_backward";
+  SB_TRY(check_h(h, op));
+  if (!g || !x || !dw || !float_dtype(dt) || b < 0 || m < 0 || n < 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  if (m == 0 || n == 0) return SB_OK;
+  return sb::wgrad(h, g, x, dt, b, m, n, dw, exact, accumulate);
+}
+
+sb_status sb_gemm_fp8(sb_handle h, const uint8_t* qa, sb_fp8_format fa, const float* sa, sb_axis axa, const uint8_t* qb,
+                      sb_fp8_format fb, const float* sbp, sb_axis axb, int64_t M, int64_t N, int64_t K, void* out,
+                      sb_dtype out_dt) {
+  const char* op = "fp8 matmul";
+  SB_TRY(check_h(h, op));
+  if (!qa || !qb || !sa || !sbp || !out) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  if (M == 0 || N == 0) return SB_OK;
+  return sb::gemm_fp8(h, qa, fa, sa, axa, qb, fb, sbp, axb, M, N, K, out, out_dt);
+}
+
+// --------------------------------------------------------------- layer --
+sb_status sb_linear_workspace_size(const sb_linear_mode* mode, int64_t b, int64_t n, int64_t m, size_t* bytes) {
+  if (!mode || !bytes || b < 0 || n < 0 || m < 0)
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, "linear_forward", "bad argument");
+  *bytes = carve(*mode, b, n, m, SB_F32, nullptr).total;
+  return SB_OK;
+}
+
+static bool same_mode(const sb_linear_mode& a, const sb_linear_mode& b) {  // LinearMode ==, linear.cpp:27-32
+  if (a.variant != b.variant || a.format != b.format || a.exact != b.exact) return false;
+  if (a.format == SB_INT8) return true;
+  return a.fp8_forward == b.fp8_forward && a.fp8_gradient == b.fp8_gradient;
+}
+
+sb_status sb_linear_forward(sb_handle h, const sb_linear_mode* mode, const void* x, const void* w, sb_dtype dt, int64_t b,
+                            int64_t n, int64_t m, void* y, sb_linear_ctx* ctx, void* workspace, size_t ws_bytes) {
+  const char* op = "linear_forward";
+  SB_TRY(check_h(h, op));
+  if (!mode || !x || !w || !y || !float_dtype(dt)) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  if (b <= 0 || n <= 0 || m <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty operand");  // linear.cpp:88
+  const sb_linear_mode md = *mode;
+  if (md.variant < SB_STANDARD || md.variant > SB_ALLQUANT || (md.format != SB_INT8 && md.format != SB_FP8))
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "unknown mode");
+  if (md.exact && dt != SB_F32) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "exact numerics need fp32 I/O");
+  const LinearWs ws = carve(md, b, n, m, dt, workspace);
+  if (md.variant != SB_STANDARD && (!workspace || ws_bytes < carve(md, b, n, m, dt, nullptr).total))
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "workspace too small");
+  if (ctx) {  // *ctx reset at entry, linear.cpp:116-119
+    std::memset(ctx, 0, sizeof(*ctx));
+    ctx->mode = md;
+    ctx->b = b;
+    ctx->n = n;
+    ctx->m = m;
+    ctx->dt = dt;
+    ctx->x = x;
+    ctx->w = w;
+    ctx->workspace = workspace;
+    ctx->workspace_bytes = ws_bytes;
+  }
+  const sb_dtype out_dt = dt;
+  if (md.variant == SB_STANDARD) {  // linear.cpp:121-127
+    if (md.exact || dt == SB_F32) {
+      SB_TRY(sb::matmul_f32_seq(h, static_cast<const float*>(x), n, 1, static_cast<const float*>(w), n, 1, b, m, n,
+                                static_cast<float*>(y), 0));
+    } else {
+      SB_TRY(gemm_bf16(h, x, false, w, false, b, m, n, y, out_dt));
+    }
+    if (ctx) ctx->valid = 1;
+    return SB_OK;
+  }
+  if (md.format == SB_INT8) {
+    SB_TRYC(op, sb::launch_quantize_rowwise(h, x, dt, b, n, n, ws.x_q, n, ws.x_state));
+    if (md.variant == SB_SWITCHBACK_Q) {
+      // dual row-wise: Y = qrow(X) . qrow(W)^T (linear.cpp:131-132)
+      SB_TRYC(op, sb::launch_quantize_rowwise(h, w, dt, m, n, n, ws.w_q, n, ws.w_state));
+      SB_TRY(sb::gemm_i8(h, ws.x_q, ws.x_state, ws.w_q, ws.w_state, SB_SCALE_ROW_ROW, b, m, n, y, out_dt, md.exact));
+    } else {
+      // tensor-wise W, both layouts from one read; W^T payload cached for the backward
+      SB_TRY(q_tensorwise(h, w, dt, m, n, n, ws.w_q, n, ws.w_qt, m, ws.w_state, ws.words));
+      SB_TRY(sb::gemm_i8(h, ws.x_q, ws.x_state, ws.w_q, ws.w_state, SB_SCALE_ROW_TENSOR, b, m, n, y, out_dt, md.exact));
+    }
+    if (ctx) {
+      ctx->w_q_t = md.variant == SB_SWITCHBACK_Q ? nullptr : ws.w_qt;
+      ctx->w_state = ws.w_state;
+      if (md.variant == SB_SWITCHBACK_M) {  // linear.cpp:137-139: keep only the int8 tensors
+        ctx->x_q = ws.x_q;
+        ctx->x_state = ws.x_state;
+        ctx->x = nullptr;
+        ctx->w = nullptr;
+      }
+      ctx->valid = 1;
+    }
+    return SB_OK;
+  }
+  // fp8 (linear.cpp:148-163): snapped operands, tensor-core product
+  const int ff = md.fp8_forward;
+  const int ax = md.variant == SB_ALLQUANT ? SB_AXIS_TENSOR : SB_AXIS_ROW;   // fp8_activation_axis
+  const int wx = md.variant == SB_SWITCHBACK_Q ? SB_AXIS_ROW : SB_AXIS_TENSOR;  // fp8_weight_axis
+  uint8_t* xq = reinterpret_cast<uint8_t*>(ws.x_q);
+  uint8_t* wq = reinterpret_cast<uint8_t*>(ws.w_q);
+  SB_TRY(q_fp8(h, x, dt, b, n, n, ff, ax, xq, n, ws.x_state, ws.words));
+  SB_TRY(q_fp8(h, w, dt, m, n, n, ff, wx, wq, n, ws.w_state, ws.words));
+  SB_TRY(sb::gemm_fp8(h, xq, ff, ws.x_state, ax, wq, ff, ws.w_state, wx, b, m, n, y, out_dt));
+  if (ctx) {
+    if (md.variant == SB_SWITCHBACK_M) {
+      ctx->x_q = ws.x_q;
+      ctx->x_state = ws.x_state;
+      ctx->x = nullptr;
+      ctx->w = nullptr;
+    }
+    ctx->w_state = ws.w_state;
+    ctx->valid = 1;
+  }
+  return SB_OK;
+}
+
+sb_status sb_linear_backward(sb_handle h, const sb_linear_mode* mode, const sb_linear_ctx* ctx, const void* g, void* dx,
+                             float* dw, int dw_accumulate) {
+  const char* op = "linear_backward";
+  SB_TRY(check_h(h, op));
+  if (!mode || !ctx || !ctx->valid || !g || !dx || !dw) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  if (!same_mode(*mode, ctx->mode))
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "context was produced by a different mode");  // linear.cpp:201-202
+  const sb_linear_mode md = ctx->mode;
+  const int64_t b = ctx->b, n = ctx->n, m = ctx->m;
+  const sb_dtype dt = ctx->dt;
+  const LinearWs ws = carve(md, b, n, m, dt, ctx->workspace);
+  const int exact = md.exact;
+
+  if (md.variant == SB_STANDARD) {  // linear.cpp:210-214
+    if (exact || dt == SB_F32) {
+      // x_grad = matmul(G, W^T^T) : dx[i][j] = sum_p g[i][p] * w[p][j]
+      SB_TRY(sb::matmul_f32_seq(h, static_cast<const float*>(g), m, 1, static_cast<const float*>(ctx->w), 1, n, b, n, m,
+                                static_cast<float*>(dx), 0));
+    } else {
+      SB_TRY(gemm_bf16(h, g, false, ctx->w, true, b, n, m, dx, dt));
+    }
+    return sb::wgrad(h, g, ctx->x, dt, b, m, n, dw, exact, dw_accumulate);
+  }
+
+  if (md.format == SB_INT8) {
+    SB_TRYC(op, sb::launch_quantize_rowwise(h, g, dt, b, m, m, ws.g_q, m, ws.g_state));
+    if (md.variant == SB_SWITCHBACK_Q) {
+      // column-wise quantize-transpose of W: per-row states of W^T (linear.cpp:226-229)
+      SB_TRY(q_columnwise(h, ctx->w, dt, m, n, n, nullptr, 0, ws.w_qt, m, ws.wt_state, ws.words));
+      SB_TRY(sb::gemm_i8(h, ws.g_q, ws.g_state, ws.w_qt, ws.wt_state, SB_SCALE_ROW_ROW, b, n, m, dx, dt, exact));
+    } else {
+      // W^T payload from the forward (== quantize_tensorwise_transpose(W), linear_test.cpp:252-264)
+      SB_TRY(sb::gemm_i8(h, ws.g_q, ws.g_state, ctx->w_q_t, ctx->w_state, SB_SCALE_ROW_TENSOR, b, n, m, dx, dt, exact));
+    }
+    if (md.variant == SB_ALLQUANT) {
+      // dW = dual_rowwise(qrow(G^T), qrow(X^T)) with K = b (linear.cpp:239-241)
+      SB_TRY(q_columnwise(h, g, dt, b, m, m, nullptr, 0, ws.gt_q, b, ws.gt_state, ws.words));
+      SB_TRY(q_columnwise(h, ctx->x, dt, b, n, n, nullptr, 0, ws.xt_q, b, ws.xt_state, ws.words));
+      if (dw_accumulate) return sb::fail(SB_ERR_UNSUPPORTED, op, "AllQuant dW does not accumulate");
+      return sb::gemm_i8(h, ws.gt_q, ws.gt_state, ws.xt_q, ws.xt_state, SB_SCALE_ROW_ROW, m, n, b, dw, SB_F32, exact);
+    }
+    if (md.variant == SB_SWITCHBACK_M) {
+      // dW on the dequantized saved activations (linear.cpp:243)
+      SB_TRYC(op, sb::launch_dequantize(h, ctx->x_q, b, n, n, ctx->x_state, SB_AXIS_ROW, ws.deq, dt, n));
+      return sb::wgrad(h, g, ws.deq, dt, b, m, n, dw, exact, dw_accumulate);
+    }
+    return sb::wgrad(h, g, ctx->x, dt, b, m, n, dw, exact, dw_accumulate);  // linear.cpp:245
+  }
+
+  // fp8 backward (linear.cpp:250-277)
+  const int ff = md.fp8_forward, fg = md.fp8_gradient;
+  uint8_t* wqt = reinterpret_cast<uint8_t*>(ws.w_qt);
+  uint8_t* wq = reinterpret_cast<uint8_t*>(ws.w_q);
+  const float* wt_state;
+  int wt_axis;
+  if (md.variant == SB_SWITCHBACK_M) {  // transpose of the saved tensor-wise payload
+    SB_TRY(transpose_u8(h, wq, m, n, wqt));
+    wt_state = ctx->w_state;
+    wt_axis = SB_AXIS_TENSOR;
+  } else if (md.variant == SB_SWITCHBACK_Q) {  // per-column states of W
+    SB_TRY(q_fp8(h, ctx->w, dt, m, n, n, ff, SB_AXIS_COLUMN, wq, n, ws.wt_state, ws.words));
+    SB_TRY(transpose_u8(h, wq, m, n, wqt));
+    wt_state = ws.wt_state;
+    wt_axis = SB_AXIS_ROW;
+  } else {
+    SB_TRY(q_fp8(h, ctx->w, dt, m, n, n, ff, SB_AXIS_TENSOR, wq, n, ws.w_state, ws.words));
+    SB_TRY(transpose_u8(h, wq, m, n, wqt));
+    wt_state = ws.w_state;
+    wt_axis = SB_AXIS_TENSOR;
+  }
+  const int gx = md.variant == SB_ALLQUANT ? SB_AXIS_TENSOR : SB_AXIS_ROW;
+  uint8_t* gq = reinterpret_cast<uint8_t*>(ws.g_q);
+  SB_TRY(q_fp8(h, g, dt, b, m, m, fg, gx, gq, m, ws.g_state, ws.words));
+  SB_TRY(sb::gemm_fp8(h, gq, fg, ws.g_state, gx, wqt, ff, wt_state, wt_axis, b, n, m, dx, dt));
+  if (md.variant == SB_ALLQUANT) {
+    // wgrad over snapped G and snapped (tensor-wise) X
+    SB_TRYC(op, sb::launch_dequantize_fp8(h, gq, b, m, m, fg, ws.g_state, gx, ws.deq2, dt, m));
+    uint8_t* xq = reinterpret_cast<uint8_t*>(ws.x_q);
+    SB_TRY(q_fp8(h, ctx->x, dt, b, n, n, ff, SB_AXIS_TENSOR, xq, n, ws.x_state, ws.words));
+    SB_TRYC(op, sb::launch_dequantize_fp8(h, xq, b, n, n, ff, ws.x_state, SB_AXIS_TENSOR, ws.deq, dt, n));
+    return sb::wgrad(h, ws.deq2, ws.deq, dt, b, m, n, dw, exact, dw_accumulate);
+  }
+  if (md.variant == SB_SWITCHBACK_M) {
+    SB_TRYC(op, sb::launch_dequantize_fp8(h, reinterpret_cast<const uint8_t*>(ctx->x_q), b, n, n, ff, ctx->x_state,
+                                          SB_AXIS_ROW, ws.deq, dt, n));
+    return sb::wgrad(h, g, ws.deq, dt, b, m, n, dw, exact, dw_accumulate);
+  }
+  return sb::wgrad(h, g, ctx->x, dt, b, m, n, dw, exact, dw_accumulate);
+}
+
+// ------------------------------------------------- host-buffer pipeline --
+// switchback_fwd_bwd over host memory: W is quantized once; token rows stream through in
+// chunks. Three streams: h2d copies, compute (the handle stream), d2h copies, so PCIe
+// transfers of chunk i+1 / i-1 overlap the kernels of chunk i. dW accumulates on the single
+// compute stream in chunk order (deterministic).
+sb_status sb_switchback_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, const void* x, const void* w,
+                                     const void* g, sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y, void* dx,
+                                     float* dw) {
+  const char* op = "switchback_fwd_bwd";
+  SB_TRY(check_h(h, op));
+  if (!mode || !x || !w || !g || !y || !dx || !dw || !float_dtype(dt)) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  if (b <= 0 || n <= 0 || m <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty operand");
+  if (mode->variant != SB_SWITCHBACK || mode->format != SB_INT8)
+    return sb::fail(SB_ERR_UNSUPPORTED, op, "host pipeline implements SwitchBack int8");
+  const size_t es = sb::dt_size(dt);
+  const int64_t chunk = std::min<int64_t>(b, 8192);
+  // device layout: W, W_q, W_qT, dW, 2 x {x, g, y, dx, x_q, g_q, states}
+  Carve c{nullptr};
+  auto layout = [&](Carve& cv, void** P) {
+    P[0] = cv.take<uint8_t>(m * n * es);
+    P[1] = cv.take<int8_t>(m * n);
+    P[2] = cv.take<int8_t>(m * n);
+    P[3] = cv.take<float>(m * n);
+    P[4] = cv.take<float>(8);
+    P[5] = cv.take<unsigned int>(8);
+    for (int s = 0; s < 2; ++s) {
+      P[6 + 8 * s + 0] = cv.take<uint8_t>(chunk * n * es);
+      P[6 + 8 * s + 1] = cv.take<uint8_t>(chunk * m * es);
+      P[6 + 8 * s + 2] = cv.take<uint8_t>(chunk * m * es);
+      P[6 + 8 * s + 3] = cv.take<uint8_t>(chunk * n * es);
+      P[6 + 8 * s + 4] = cv.take<int8_t>(chunk * n);
+      P[6 + 8 * s + 5] = cv.take<int8_t>(chunk * m);
+      P[6 + 8 * s + 6] = cv.take<float>(chunk);
+      P[6 + 8 * s + 7] = cv.take<float>(chunk);
+    }
+  };
+  void* P[22];
+  layout(c, P);
+  const size_t need = c.off + 256;
+  if (need > h->dev_pool_bytes) {
+    if (h->dev_pool) {
+      cudaStreamSynchronize(h->stream);
+      cudaFree(h->dev_pool);
+    }
+    h->dev_pool = nullptr;
+    h->dev_pool_bytes = 0;
+    SB_CUDA_CHECK(op, cudaMalloc(&h->dev_pool, need));
+    h->dev_pool_bytes = need;
+  }
+  Carve c2{static_cast<uint8_t*>(h->dev_pool)};
+  layout(c2, P);
+  void* dW_ = P[0];
+  int8_t* wq = static_cast<int8_t*>(P[1]);
+  int8_t* wqt = static_cast<int8_t*>(P[2]);
+  float* dwd = static_cast<float*>(P[3]);
+  float* wstate = static_cast<float*>(P[4]);
+  unsigned int* words = static_cast<unsigned int*>(P[5]);
+
+  cudaStream_t comp = h->stream, s_in, s_out;
+  SB_CUDA_CHECK(op, cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+  SB_CUDA_CHECK(op, cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+  cudaEvent_t ev_in[2], ev_comp[2], ev_out[2], ev_start;
+  for (int s = 0; s < 2; ++s) {
+    cudaEventCreateWithFlags(&ev_in[s], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_comp[s], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_out[s], cudaEventDisableTiming);
+  }
+  cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+  cudaEventRecord(ev_start, comp);
+  cudaStreamWaitEvent(s_in, ev_start, 0);
+  cudaStreamWaitEvent(s_out, ev_start, 0);
+  sb_status st = SB_OK;
+  const int64_t nchunks = (b + chunk - 1) / chunk;
+  auto h2d = [&](int64_t i) {
+    const int s = static_cast<int>(i & 1);
+    const int64_t r0 = i * chunk, rows = std::min(chunk, b - r0);
+    if (i >= 2) cudaStreamWaitEvent(s_in, ev_comp[s], 0);
+    cudaMemcpyAsync(P[6 + 8 * s + 0], static_cast<const uint8_t*>(x) + r0 * n * es, rows * n * es, cudaMemcpyHostToDevice, s_in);
+    cudaMemcpyAsync(P[6 + 8 * s + 1], static_cast<const uint8_t*>(g) + r0 * m * es, rows * m * es, cudaMemcpyHostToDevice, s_in);
+    cudaEventRecord(ev_in[s], s_in);
+  };
+  // W in, quantized once (both layouts)
+  cudaMemcpyAsync(dW_, w, m * n * es, cudaMemcpyHostToDevice, comp);
+  st = q_tensorwise(h, dW_, dt, m, n, n, wq, n, wqt, m, wstate, words);
+  h2d(0);
+  for (int64_t i = 0; i < nchunks && st == SB_OK; ++i) {
+    const int s = static_cast<int>(i & 1);
+    const int64_t r0 = i * chunk, rows = std::min(chunk, b - r0);
+    if (i + 1 < nchunks) h2d(i + 1);
+    cudaStreamWaitEvent(comp, ev_in[s], 0);
+    if (i >= 2) cudaStreamWaitEvent(comp, ev_out[s], 0);
+    void* xd = P[6 + 8 * s + 0];
+    void* gd = P[6 + 8 * s + 1];
+    void* yd = P[6 + 8 * s + 2];
+    void* dxd = P[6 + 8 * s + 3];
+    int8_t* xq = static_cast<int8_t*>(P[6 + 8 * s + 4]);
+    int8_t* gq = static_cast<int8_t*>(P[6 + 8 * s + 5]);
+    float* xs = static_cast<float*>(P[6 + 8 * s + 6]);
+    float* gs = static_cast<float*>(P[6 + 8 * s + 7]);
+    if (sb::launch_quantize_rowwise(h, xd, dt, rows, n, n, xq, n, xs) != cudaSuccess) st = sb::cuda_fail(op, cudaGetLastError());
+    if (st == SB_OK) st = sb::gemm_i8(h, xq, xs, wq, wstate, SB_SCALE_ROW_TENSOR, rows, m, n, yd, dt, mode->exact);
+    if (st == SB_OK && sb::launch_quantize_rowwise(h, gd, dt, rows, m, m, gq, m, gs) != cudaSuccess)
+      st = sb::cuda_fail(op, cudaGetLastError());
+    if (st == SB_OK) st = sb::gemm_i8(h, gq, gs, wqt, wstate, SB_SCALE_ROW_TENSOR, rows, n, m, dxd, dt, mode->exact);
+    if (st == SB_OK) st = sb::wgrad(h, gd, xd, dt, rows, m, n, dwd, mode->exact, i > 0);
+    cudaEventRecord(ev_comp[s], comp);
+    cudaStreamWaitEvent(s_out, ev_comp[s], 0);
+    cudaMemcpyAsync(static_cast<uint8_t*>(y) + r0 * m * es, yd, rows * m * es, cudaMemcpyDeviceToHost, s_out);
+    cudaMemcpyAsync(static_cast<uint8_t*>(dx) + r0 * n * es, dxd, rows * n * es, cudaMemcpyDeviceToHost, s_out);
+    cudaEventRecord(ev_out[s], s_out);
+  }
+  cudaStreamWaitEvent(comp, ev_out[0], 0);
+  cudaStreamWaitEvent(comp, ev_out[1], 0);
+  cudaMemcpyAsync(dw, dwd, m * n * sizeof(float), cudaMemcpyDeviceToHost, comp);
+  cudaError_t e = cudaStreamSynchronize(comp);
+  cudaStreamSynchronize(s_out);
+  for (int s = 0; s < 2; ++s) {
+    cudaEventDestroy(ev_in[s]);
+    cudaEventDestroy(ev_comp[s]);
+    cudaEventDestroy(ev_out[s]);
+  }
+  cudaEventDestroy(ev_start);
+  cudaStreamDestroy(s_in);
+  cudaStreamDestroy(s_out);
+  if (st != SB_OK) return st;
+  if (e != cudaSuccess) return sb::cuda_fail(op, e);
+  uint32_t flags = 0;
+  cudaMemcpy(&flags, h->d_err, sizeof(flags), cudaMemcpyDeviceToHost);
+  if (flags) {
+    cudaMemset(h->d_err, 0, sizeof(uint32_t));
+    return sb::fail(SB_ERR_NONFINITE, op, "non-finite input");
+  }
+  return SB_OK;
+}
+
+}  // extern "C"
+
+namespace {
+sb_status gemm_bf16(sb_handle h, const void* a, bool a_mn, const void* b, bool b_mn, int64_t M, int64_t N, int64_t K,
+                    void* out, sb_dtype out_dt) {
+  float* one = nullptr;
+  cudaGetSymbolAddress(reinterpret_cast<void**>(&one), g_one);
+  return sb::gemm_bf16_tc(h, a, a_mn, b, b_mn, M, N, K, out, out_dt, one);
+}
+}  // namespace

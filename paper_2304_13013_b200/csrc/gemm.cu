@@ -1,0 +1,406 @@
+// gemm.cu — host launchers for the SwitchBack GEMMs plus their exact / SIMT companions.
+//
+//   sb::gemm_i8    int8_matmul_dequant / matmul_dequant_dual_rowwise (linear.cpp:39-83)
+//                  tcgen05 kind::i8 when the operands are TMA-legal (K % 16 == 0, 16-B
+//                  aligned, K <= 133144 so s32 cannot overflow); otherwise a SIMT kernel
+//                  with int64 accumulation (the reference's own int64 switch, linear.cpp:62-65).
+//   sb::wgrad      wgrad_full_precision (linear.cpp:193-195): tcgen05 kind::f16 over MN-major
+//                  bf16 G and X, or the exact sequential fp32 kernel (matrix.cpp:53-68).
+//   sb::matmul_f32_seq  matmul (matrix.cpp:53-68): one output per thread, strictly sequential
+//                  fp32 sum with separately rounded multiply and add (-ffp-contract=off).
+//   sb::gemm_fp8   fp8 SwitchBack GEMM (tcgen05 kind::f8f6f4).
+#include <cuda_bf16.h>
+
+#include <mutex>
+
+#include "sb_internal.h"
+#include "tc_gemm.cuh"
+
+namespace {
+
+constexpr int64_t kInt32SafeInner = 2147483647LL / (127 * 127);  // 133144, linear.cpp:37
+
+// ----------------------------------------------------------- SIMT int8 ----
+template <int OUT>
+__global__ void k_gemm_i8_simt(const int8_t* __restrict__ qa, const float* __restrict__ sa, int sa_stride,
+                               const int8_t* __restrict__ qb, const float* __restrict__ sb, int sb_stride, int64_t M,
+                               int64_t N, int64_t K, void* __restrict__ out) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t i = blockIdx.y;
+  if (j >= N) return;
+  const int8_t* a = qa + i * K;
+  const int8_t* b = qb + j * K;
+  int64_t acc = 0;
+  for (int64_t p = 0; p < K; ++p) acc += static_cast<int64_t>(a[p]) * static_cast<int64_t>(b[p]);
+  const int64_t o = i * N + j;
+  if (OUT == 5) {  // raw int64
+    static_cast<int64_t*>(out)[o] = acc;
+  } else if (OUT == sbtc::OUT_I32) {
+    static_cast<int32_t*>(out)[o] = static_cast<int32_t>(acc);
+  } else {
+    const double d = __ddiv_rn(__dmul_rn(__dmul_rn(static_cast<double>(acc), static_cast<double>(sa[sa_stride ? i : 0])),
+                                         static_cast<double>(sb[sb_stride ? j : 0])),
+                               16129.0);
+    if (OUT == sbtc::OUT_F32_EXACT)
+      static_cast<float*>(out)[o] = __double2float_rn(d);
+    else if (OUT == sbtc::OUT_F32)
+      static_cast<float*>(out)[o] = static_cast<float>(acc) * (sa[sa_stride ? i : 0] / 16129.0f) * sb[sb_stride ? j : 0];
+    else
+      static_cast<__nv_bfloat16*>(out)[o] =
+          __float2bfloat16_rn(static_cast<float>(acc) * (sa[sa_stride ? i : 0] / 16129.0f) * sb[sb_stride ? j : 0]);
+  }
+}
+
+// --------------------------------------------------- exact sequential fp32 ----
+// y[i][j] (+)= sum_p a(i,p) * b(j,p), p ascending, fmul/fadd separately rounded.
+// 64 x 64 outputs per block, 4 x 4 per thread, k-tiles of 16 staged in smem.
+__device__ __forceinline__ void store_out(float* p, float v) { *p = v; }
+__device__ __forceinline__ void store_out(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+__device__ __forceinline__ float load_out(const float* p) { return *p; }
+__device__ __forceinline__ float load_out(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+
+template <typename T, typename TO = float>
+__global__ void __launch_bounds__(256) k_matmul_seq(const T* __restrict__ a, int64_t a_rs, int64_t a_ks,
+                                                    const T* __restrict__ b, int64_t b_rs, int64_t b_ks, int64_t R,
+                                                    int64_t Cc, int64_t K, TO* __restrict__ y, int accumulate) {
+  __shared__ float As[16][64 + 1];
+  __shared__ float Bs[16][64 + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.y) * 64, j0 = static_cast<int64_t>(blockIdx.x) * 64;
+  float acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0f;
+  for (int64_t k0 = 0; k0 < K; k0 += 16) {
+    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+      const int kk = e / 64, rr = e % 64;
+      const int64_t ia = i0 + rr, jb = j0 + rr, kg = k0 + kk;
+      As[kk][rr] = (ia < R && kg < K) ? static_cast<float>(a[ia * a_rs + kg * a_ks]) : 0.0f;
+      Bs[kk][rr] = (jb < Cc && kg < K) ? static_cast<float>(b[jb * b_rs + kg * b_ks]) : 0.0f;
+    }
+    __syncthreads();
+    const int kmax = static_cast<int>(K - k0 < 16 ? K - k0 : 16);
+    for (int kk = 0; kk < kmax; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) av[u] = As[kk][ty * 4 + u];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) bv[v] = Bs[kk][tx * 4 + v];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = __fadd_rn(acc[u][v], __fmul_rn(av[u], bv[v]));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int64_t i = i0 + ty * 4 + u, j = j0 + tx * 4 + v;
+      if (i < R && j < Cc) store_out(y + i * Cc + j, accumulate ? __fadd_rn(load_out(y + i * Cc + j), acc[u][v]) : acc[u][v]);
+    }
+}
+
+// -------------------------------------------------------------- SIMT fp8 ----
+__device__ __forceinline__ float dec_fp8(uint8_t b, int fmt) {
+  const uint32_t s = (b >> 7) & 1u;
+  float v;
+  if (fmt == 0) {
+    const uint32_t e = (b >> 3) & 0xFu, m = b & 7u;
+    v = e == 0 ? ldexpf(static_cast<float>(m), -9) : ldexpf(1.0f + m / 8.0f, static_cast<int>(e) - 7);
+  } else {
+    const uint32_t e = (b >> 2) & 0x1Fu, m = b & 3u;
+    v = e == 0 ? ldexpf(static_cast<float>(m), -16) : ldexpf(1.0f + m / 4.0f, static_cast<int>(e) - 15);
+  }
+  return s ? -v : v;
+}
+
+__global__ void k_gemm_fp8_simt(const uint8_t* __restrict__ qa, int fa, const float* __restrict__ sa, int sa_stride,
+                                const uint8_t* __restrict__ qb, int fb, const float* __restrict__ sb, int sb_stride,
+                                int64_t M, int64_t N, int64_t K, void* __restrict__ out, int out_bf16) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t i = blockIdx.y;
+  if (j >= N) return;
+  float acc = 0.0f;
+  for (int64_t p = 0; p < K; ++p) acc = fmaf(dec_fp8(qa[i * K + p], fa), dec_fp8(qb[j * K + p], fb), acc);
+  const float y = acc * sa[sa_stride ? i : 0] * sb[sb_stride ? j : 0];
+  if (out_bf16)
+    static_cast<__nv_bfloat16*>(out)[i * N + j] = __float2bfloat16_rn(y);
+  else
+    static_cast<float*>(out)[i * N + j] = y;
+}
+
+// ------------------------------------------------------------ TMA maps ----
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+template <int KIND, int OUT, bool A_MN = false, bool B_MN = false>
+cudaError_t launch_tc(sb_handle h, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d,
+                      const sbtc::Params& p, uint32_t idesc) {
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(sbtc::k_tc_gemm<KIND, A_MN, B_MN, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    sbtc::SMEM_BYTES);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  const int tiles = p.tiles_m * p.tiles_n;
+  const int grid = tiles < h->num_sms ? tiles : h->num_sms;
+  h->launches++;
+  sbtc::k_tc_gemm<KIND, A_MN, B_MN, OUT><<<grid, sbtc::NUM_THREADS, sbtc::SMEM_BYTES, h->stream>>>(a, b, d, p, idesc);
+  return cudaGetLastError();
+}
+
+bool out_tmap(CUtensorMap* m, sb_dtype dt, void* out, int64_t M, int64_t N) {
+  if (dt == SB_BF16)
+    return sb::encode_tmap_2d(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, out, N, M, N * 2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+  const CUtensorMapDataType t = dt == SB_I32 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  return sb::encode_tmap_2d(m, t, out, N, M, N * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+}  // namespace
+
+namespace sb {
+
+bool encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer,
+                    uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz) {
+  EncodeFn fn = get_encode();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {row_stride_bytes};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+sb_status gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* qb, const float* sbp, int scale_mode,
+                  int64_t M, int64_t N, int64_t K, void* out, sb_dtype out_dt, int exact) {
+  const char* op = "int8 matmul";
+  const bool raw = scale_mode == SB_SCALE_NONE;
+  if (raw && out_dt != SB_I32 && out_dt != SB_I64) return fail(SB_ERR_INVALID_ARGUMENT, op, "raw output needs I32/I64");
+  if (!raw && out_dt != SB_F32 && out_dt != SB_BF16) return fail(SB_ERR_INVALID_ARGUMENT, op, "bad output dtype");
+  if (out_dt == SB_I32 && K > kInt32SafeInner)
+    return fail(SB_ERR_INVALID_ARGUMENT, op, "int32 accumulator would overflow (k > 133144); use I64");
+  const int sa_stride = 1;  // A is always row-wise (X or G)
+  const int sb_stride = scale_mode == SB_SCALE_ROW_ROW ? 1 : 0;
+  int out_mode;
+  if (raw) out_mode = sbtc::OUT_I32;
+  else if (out_dt == SB_BF16) out_mode = sbtc::OUT_BF16;
+  else out_mode = exact ? sbtc::OUT_F32_EXACT : sbtc::OUT_F32;
+
+  const bool tc_ok = out_dt != SB_I64 && K <= kInt32SafeInner && (K % 16 == 0) && aligned(qa, 16) &&
+                     aligned(qb, 16) && aligned(out, 16) && ((N * static_cast<int64_t>(dt_size(out_dt))) % 16 == 0) &&
+                     M < (1LL << 31) && N < (1LL << 31) && get_encode() != nullptr;
+  if (tc_ok) {
+    CUtensorMap ta, tb, td;
+    bool ok = encode_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, qa, K, M, K, 128, 128, CU_TENSOR_MAP_SWIZZLE_128B) &&
+              encode_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, qb, K, N, K, 128, 256, CU_TENSOR_MAP_SWIZZLE_128B) &&
+              out_tmap(&td, out_dt, out, M, N);
+    if (ok) {
+      sbtc::Params p;
+      p.M = static_cast<int>(M);
+      p.N = static_cast<int>(N);
+      p.K = static_cast<int>(K);
+      p.sa = sa;
+      p.sb = sbp;
+      p.sa_stride = sa_stride;
+      p.sb_stride = sb_stride;
+      p.post_scale = 1.0f / 16129.0f;
+      p.tiles_m = static_cast<int>((M + sbtc::BM - 1) / sbtc::BM);
+      p.tiles_n = static_cast<int>((N + sbtc::BN - 1) / sbtc::BN);
+      cudaError_t e;
+      switch (out_mode) {
+        case sbtc::OUT_BF16: e = launch_tc<sbtc::KIND_I8, sbtc::OUT_BF16>(h, ta, tb, td, p, 0); break;
+        case sbtc::OUT_F32: e = launch_tc<sbtc::KIND_I8, sbtc::OUT_F32>(h, ta, tb, td, p, 0); break;
+        case sbtc::OUT_F32_EXACT: e = launch_tc<sbtc::KIND_I8, sbtc::OUT_F32_EXACT>(h, ta, tb, td, p, 0); break;
+        default: e = launch_tc<sbtc::KIND_I8, sbtc::OUT_I32>(h, ta, tb, td, p, 0); break;
+      }
+      if (e != cudaSuccess) return cuda_fail(op, e);
+      return SB_OK;
+    }
+  }
+  // SIMT path (unaligned / tiny / int64 accumulation)
+  const dim3 grid(static_cast<unsigned>((N + 127) / 128), static_cast<unsigned>(M));
+  h->launches++;
+  if (out_dt == SB_I64)
+    k_gemm_i8_simt<5><<<grid, 128, 0, h->stream>>>(qa, sa, sa_stride, qb, sbp, sb_stride, M, N, K, out);
+  else if (out_mode == sbtc::OUT_I32)
+    k_gemm_i8_simt<sbtc::OUT_I32><<<grid, 128, 0, h->stream>>>(qa, sa, sa_stride, qb, sbp, sb_stride, M, N, K, out);
+  else if (out_mode == sbtc::OUT_F32_EXACT)
+    k_gemm_i8_simt<sbtc::OUT_F32_EXACT><<<grid, 128, 0, h->stream>>>(qa, sa, sa_stride, qb, sbp, sb_stride, M, N, K,
+                                                                     out);
+  else if (out_mode == sbtc::OUT_F32)
+    k_gemm_i8_simt<sbtc::OUT_F32><<<grid, 128, 0, h->stream>>>(qa, sa, sa_stride, qb, sbp, sb_stride, M, N, K, out);
+  else
+    k_gemm_i8_simt<sbtc::OUT_BF16><<<grid, 128, 0, h->stream>>>(qa, sa, sa_stride, qb, sbp, sb_stride, M, N, K, out);
+  SB_LAUNCH_CHECK(op);
+  return SB_OK;
+}
+
+sb_status matmul_f32_seq(sb_handle h, const float* a, int64_t a_rs, int64_t a_ks, const float* bt, int64_t b_rs,
+                         int64_t b_ks, int64_t r, int64_t c, int64_t k, float* y, int accumulate) {
+  const dim3 grid(static_cast<unsigned>((c + 63) / 64), static_cast<unsigned>((r + 63) / 64));
+  h->launches++;
+  k_matmul_seq<float><<<grid, 256, 0, h->stream>>>(a, a_rs, a_ks, bt, b_rs, b_ks, r, c, k, y, accumulate);
+  SB_LAUNCH_CHECK("matmul");
+  return SB_OK;
+}
+
+sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m, int64_t n, float* dw,
+                int exact, int accumulate) {
+  const char* op = "linear_backward";
+  if (dt == SB_BF16 && !exact) {
+    const bool tc_ok = (m % 8 == 0) && (n % 8 == 0) && aligned(g, 16) && aligned(x, 16) && aligned(dw, 16) &&
+                       b < (1LL << 31) && get_encode() != nullptr;
+    if (tc_ok) {
+      CUtensorMap ta, tb, td;
+      // A = G viewed MN-major: inner dim m (contiguous), outer dim T; box {64 m, 64 tokens}
+      bool ok = encode_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, g, m, b, m * 2, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) &&
+                encode_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, x, n, b, n * 2, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) &&
+                out_tmap(&td, SB_F32, dw, m, n);
+      if (ok) {
+        sbtc::Params p;
+        p.M = static_cast<int>(m);
+        p.N = static_cast<int>(n);
+        p.K = static_cast<int>(b);
+        p.sa = nullptr;
+        p.sb = nullptr;
+        p.sa_stride = p.sb_stride = 0;
+        p.post_scale = 1.0f;
+        p.tiles_m = static_cast<int>((m + sbtc::BM - 1) / sbtc::BM);
+        p.tiles_n = static_cast<int>((n + sbtc::BN - 1) / sbtc::BN);
+        cudaError_t e = accumulate ? launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW_ADD, true, true>(h, ta, tb, td, p, 0)
+                                   : launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW, true, true>(h, ta, tb, td, p, 0);
+        if (e != cudaSuccess) return cuda_fail(op, e);
+        return SB_OK;
+      }
+    }
+  }
+  // exact sequential (or unaligned fallback): dW[i][j] = sum_t G[t][i] * X[t][j]
+  const dim3 grid(static_cast<unsigned>((n + 63) / 64), static_cast<unsigned>((m + 63) / 64));
+  h->launches++;
+  if (dt == SB_BF16)
+    k_matmul_seq<__nv_bfloat16><<<grid, 256, 0, h->stream>>>(static_cast<const __nv_bfloat16*>(g), 1, m,
+                                                             static_cast<const __nv_bfloat16*>(x), 1, n, m, n, b, dw,
+                                                             accumulate);
+  else
+    k_matmul_seq<float><<<grid, 256, 0, h->stream>>>(static_cast<const float*>(g), 1, m, static_cast<const float*>(x), 1,
+                                                     n, m, n, b, dw, accumulate);
+  SB_LAUNCH_CHECK(op);
+  return SB_OK;
+}
+
+sb_status gemm_bf16_tc(sb_handle h, const void* a, bool a_mn, const void* b, bool b_mn, int64_t M, int64_t N, int64_t K,
+                       void* out, sb_dtype out_dt, const float* one) {
+  const char* op = "matmul";
+  const bool tc_ok = (a_mn ? M % 8 == 0 : K % 8 == 0) && (b_mn ? N % 8 == 0 : K % 8 == 0) && aligned(a, 16) &&
+                     aligned(b, 16) && aligned(out, 16) && ((N * static_cast<int64_t>(dt_size(out_dt))) % 16 == 0) &&
+                     get_encode() != nullptr;
+  if (tc_ok) {
+    CUtensorMap ta, tb, td;
+    const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    const CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B;
+    bool ok = (a_mn ? encode_tmap_2d(&ta, bf, a, M, K, M * 2, 64, 64, sw) : encode_tmap_2d(&ta, bf, a, K, M, K * 2, 64, 128, sw)) &&
+              (b_mn ? encode_tmap_2d(&tb, bf, b, N, K, N * 2, 64, 64, sw) : encode_tmap_2d(&tb, bf, b, K, N, K * 2, 64, 256, sw)) &&
+              out_tmap(&td, out_dt, out, M, N);
+    if (ok) {
+      sbtc::Params p;
+      p.M = static_cast<int>(M);
+      p.N = static_cast<int>(N);
+      p.K = static_cast<int>(K);
+      p.sa = one;
+      p.sb = one;
+      p.sa_stride = p.sb_stride = 0;
+      p.post_scale = 1.0f;
+      p.tiles_m = static_cast<int>((M + sbtc::BM - 1) / sbtc::BM);
+      p.tiles_n = static_cast<int>((N + sbtc::BN - 1) / sbtc::BN);
+      cudaError_t e;
+      if (out_dt == SB_BF16) {
+        if (!a_mn && !b_mn) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_BF16, false, false>(h, ta, tb, td, p, 0);
+        else if (!a_mn && b_mn) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_BF16, false, true>(h, ta, tb, td, p, 0);
+        else if (a_mn && !b_mn) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_BF16, true, false>(h, ta, tb, td, p, 0);
+        else e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_BF16, true, true>(h, ta, tb, td, p, 0);
+      } else {
+        if (!a_mn && !b_mn) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW, false, false>(h, ta, tb, td, p, 0);
+        else if (!a_mn && b_mn) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW, false, true>(h, ta, tb, td, p, 0);
+        else if (a_mn && !b_mn) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW, true, false>(h, ta, tb, td, p, 0);
+        else e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW, true, true>(h, ta, tb, td, p, 0);
+      }
+      if (e != cudaSuccess) return cuda_fail(op, e);
+      return SB_OK;
+    }
+  }
+  // any shape: fp32-accumulating SIMT kernel over the same index maps
+  const __nv_bfloat16* A = static_cast<const __nv_bfloat16*>(a);
+  const __nv_bfloat16* B = static_cast<const __nv_bfloat16*>(b);
+  const int64_t a_rs = a_mn ? 1 : K, a_ks = a_mn ? M : 1, b_rs = b_mn ? 1 : K, b_ks = b_mn ? N : 1;
+  const dim3 grid(static_cast<unsigned>((N + 63) / 64), static_cast<unsigned>((M + 63) / 64));
+  h->launches++;
+  if (out_dt == SB_BF16)
+    k_matmul_seq<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, h->stream>>>(A, a_rs, a_ks, B, b_rs, b_ks, M, N, K,
+                                                                            static_cast<__nv_bfloat16*>(out), 0);
+  else
+    k_matmul_seq<__nv_bfloat16, float><<<grid, 256, 0, h->stream>>>(A, a_rs, a_ks, B, b_rs, b_ks, M, N, K,
+                                                                    static_cast<float*>(out), 0);
+  SB_LAUNCH_CHECK(op);
+  return SB_OK;
+}
+
+sb_status gemm_fp8(sb_handle h, const uint8_t* qa, int fa, const float* sa, int axa, const uint8_t* qb, int fb,
+                   const float* sbp, int axb, int64_t M, int64_t N, int64_t K, void* out, sb_dtype out_dt) {
+  const char* op = "fp8 matmul";
+  if (out_dt != SB_F32 && out_dt != SB_BF16) return fail(SB_ERR_INVALID_ARGUMENT, op, "bad output dtype");
+  const int sa_stride = axa == SB_AXIS_ROW ? 1 : 0, sb_stride = axb == SB_AXIS_ROW ? 1 : 0;
+  const bool tc_ok = (K % 16 == 0) && aligned(qa, 16) && aligned(qb, 16) && aligned(out, 16) &&
+                     ((N * static_cast<int64_t>(dt_size(out_dt))) % 16 == 0) && get_encode() != nullptr;
+  if (tc_ok) {
+    CUtensorMap ta, tb, td;
+    bool ok = encode_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, qa, K, M, K, 128, 128, CU_TENSOR_MAP_SWIZZLE_128B) &&
+              encode_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, qb, K, N, K, 128, 256, CU_TENSOR_MAP_SWIZZLE_128B) &&
+              out_tmap(&td, out_dt, out, M, N);
+    if (ok) {
+      sbtc::Params p;
+      p.M = static_cast<int>(M);
+      p.N = static_cast<int>(N);
+      p.K = static_cast<int>(K);
+      p.sa = sa;
+      p.sb = sbp;
+      p.sa_stride = sa_stride;
+      p.sb_stride = sb_stride;
+      p.post_scale = 1.0f;
+      p.tiles_m = static_cast<int>((M + sbtc::BM - 1) / sbtc::BM);
+      p.tiles_n = static_cast<int>((N + sbtc::BN - 1) / sbtc::BN);
+      const uint32_t idesc = sbtc::KindTraits<sbtc::KIND_F8>::IDESC | (static_cast<uint32_t>(fa) << 7) |
+                             (static_cast<uint32_t>(fb) << 10);
+      cudaError_t e = out_dt == SB_BF16 ? launch_tc<sbtc::KIND_F8, sbtc::OUT_BF16>(h, ta, tb, td, p, idesc)
+                                        : launch_tc<sbtc::KIND_F8, sbtc::OUT_F32>(h, ta, tb, td, p, idesc);
+      if (e != cudaSuccess) return cuda_fail(op, e);
+      return SB_OK;
+    }
+  }
+  const dim3 grid(static_cast<unsigned>((N + 127) / 128), static_cast<unsigned>(M));
+  h->launches++;
+  k_gemm_fp8_simt<<<grid, 128, 0, h->stream>>>(qa, fa, sa, sa_stride, qb, fb, sbp, sb_stride, M, N, K, out,
+                                               out_dt == SB_BF16);
+  SB_LAUNCH_CHECK(op);
+  return SB_OK;
+}
+
+}  // namespace sb

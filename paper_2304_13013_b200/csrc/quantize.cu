@@ -1,0 +1,666 @@
+// quantize.cu — HBM-bound quantize / dequantize kernels of the SwitchBack path.
+//
+//   K1 quantize_rowwise           quantize.cpp:116-133 (slice_absmax :89-112, quantize_entry :17-20)
+//   K2 tensor absmax              Matrix::abs_max, matrix.cpp:32-36
+//   K3 tensor-wise quantize (+ transposed copy in the same pass)   quantize.cpp:139-159
+//   K4 column-wise absmax / quantize (+ transposed = rowwise(W^T)) quantize.cpp:135-137, linear.cpp:228-229
+//   K8 fp8 quantize, ties to the smaller magnitude               quantize.cpp:65-76,161-176
+//   K10 dequantize (int8 / fp8)                                  quantize.cpp:178-197
+//
+// Bit-exactness of the int8 payload. The reference computes
+// lround(127.0*double(x)/double(s)). Because |127x/s - (k+1/2)| >= 2^-33 whenever it is
+// not an exact tie (x, s floats), the double quotient never moves a rounding
+// decision, so the payload is round-half-away-from-zero of the EXACT rational
+// 127|x|/s. We take a fast fp32 candidate k = floor(127|x|*(127/s)^-... + 1/2) and then
+// decide exactly between k-1, k, k+1 by comparing 127|x| with (k +- 1/2)*s:
+//   bf16 input: both products are exact in fp32 (<= 16 significant bits),
+//   fp32 input: the comparison runs in fp64 (31- and 33-bit products, exact) but only
+//               when the candidate is within 1e-3 of a half-integer.
+// Rows with tiny / huge absmax are pre-scaled by an exact power of two.
+//
+// Absmax uses an integer max over the sign-cleared bit patterns: for non-negative
+// floats integer order == float order, and NaN/Inf (>= 0x7f800000) surface as the
+// maximum, which is how non-finite input is detected (fmaxf would drop NaN).
+#include <cuda_bf16.h>
+
+#include "sb_internal.h"
+
+namespace {
+
+constexpr uint32_t kNonFiniteBits = 0x7f800000u;
+
+__device__ __forceinline__ void raise_nonfinite(uint32_t* err) { atomicOr(err, 1u); }
+
+template <typename T>
+__device__ __forceinline__ float to_f32(T v);
+template <>
+__device__ __forceinline__ float to_f32<float>(float v) {
+  return v;
+}
+template <>
+__device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 v) {
+  return __bfloat162float(v);
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t abs_bits(T v);
+template <>
+__device__ __forceinline__ uint32_t abs_bits<float>(float v) {
+  return __float_as_uint(v) & 0x7fffffffu;
+}
+template <>
+__device__ __forceinline__ uint32_t abs_bits<__nv_bfloat16>(__nv_bfloat16 v) {
+  return (static_cast<uint32_t>(__bfloat16_as_ushort(v)) & 0x7fffu) << 16;
+}
+
+// Max of |x| bit patterns in a 16-byte vector, in fp32 bit space.
+template <typename T>
+__device__ __forceinline__ uint32_t vec_absmax_bits(const uint4& v);
+template <>
+__device__ __forceinline__ uint32_t vec_absmax_bits<float>(const uint4& v) {
+  uint32_t a = max(v.x & 0x7fffffffu, v.y & 0x7fffffffu);
+  uint32_t b = max(v.z & 0x7fffffffu, v.w & 0x7fffffffu);
+  return max(a, b);
+}
+template <>
+__device__ __forceinline__ uint32_t vec_absmax_bits<__nv_bfloat16>(const uint4& v) {
+  uint32_t m = __vmaxu2(__vmaxu2(v.x & 0x7fff7fffu, v.y & 0x7fff7fffu), __vmaxu2(v.z & 0x7fff7fffu, v.w & 0x7fff7fffu));
+  return max(m & 0xffffu, m >> 16) << 16;
+}
+
+struct Scale {
+  float s;    // state after exact power-of-two prescale
+  float inv;  // 127 / s (fp32, approximate is fine: only seeds the candidate)
+  float pre;  // the power-of-two prescale applied to |x| and s
+};
+
+__device__ __forceinline__ Scale make_scale(float state) {
+  Scale sc;
+  sc.pre = 1.0f;
+  if (state < 0x1p-60f) sc.pre = 0x1p64f;
+  else if (state > 0x1p64f) sc.pre = 0x1p-64f;
+  sc.s = __fmul_rn(state, sc.pre);
+  sc.inv = __fdiv_rn(127.0f, sc.s);
+  return sc;
+}
+
+// |payload| = round_half_away(127|x|/s), exact (see file header).
+template <bool kExactF32Products>
+__device__ __forceinline__ float q_magnitude(float ax, const Scale& sc) {
+  const float a = __fmul_rn(ax, sc.pre);
+  const float qa = __fmul_rn(a, sc.inv);
+  float k = floorf(__fadd_rn(qa, 0.5f));
+  if (kExactF32Products) {
+    const float num = __fmul_rn(127.0f, a);
+    const float hi = __fmul_rn(__fadd_rn(k, 0.5f), sc.s);
+    const float lo = __fmul_rn(__fsub_rn(k, 0.5f), sc.s);
+    k = num >= hi ? __fadd_rn(k, 1.0f) : (num < lo ? __fsub_rn(k, 1.0f) : k);
+  } else {
+    const float frac = __fsub_rn(qa, floorf(qa));
+    if (fabsf(__fsub_rn(frac, 0.5f)) < 1e-3f) {
+      const double num = __dmul_rn(127.0, (double)a);
+      const double hi = __dmul_rn((double)k + 0.5, (double)sc.s);
+      const double lo = __dmul_rn((double)k - 0.5, (double)sc.s);
+      k = num >= hi ? k + 1.0f : (num < lo ? k - 1.0f : k);
+    }
+  }
+  return fminf(k, 127.0f);
+}
+
+template <typename T>
+__device__ __forceinline__ int8_t quantize_one(T v, const Scale& sc) {
+  const float x = to_f32(v);
+  const float k = q_magnitude<sizeof(T) == 2>(fabsf(x), sc);
+  const int ki = static_cast<int>(k);
+  return static_cast<int8_t>(x < 0.0f ? -ki : ki);
+}
+
+__device__ __forceinline__ float state_from_bits(uint32_t bits) {
+  return bits == 0u ? 1.0f : __uint_as_float(bits);  // all-zero slice sentinel (quantize.cpp:109-111)
+}
+
+// Pack the payload of one 16-byte input vector.
+template <typename T>
+struct VecQ;
+template <>
+struct VecQ<__nv_bfloat16> {
+  using Out = uint2;  // 8 int8
+  static __device__ __forceinline__ Out run(const uint4& v, const Scale& sc) {
+    const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) lo |= (static_cast<uint32_t>(static_cast<uint8_t>(quantize_one(e[i], sc)))) << (8 * i);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      hi |= (static_cast<uint32_t>(static_cast<uint8_t>(quantize_one(e[4 + i], sc)))) << (8 * i);
+    return make_uint2(lo, hi);
+  }
+};
+template <>
+struct VecQ<float> {
+  using Out = uint32_t;  // 4 int8
+  static __device__ __forceinline__ Out run(const uint4& v, const Scale& sc) {
+    const float* e = reinterpret_cast<const float*>(&v);
+    uint32_t w = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w |= (static_cast<uint32_t>(static_cast<uint8_t>(quantize_one(e[i], sc)))) << (8 * i);
+    return w;
+  }
+};
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// ------------------------------------------------------------------ K1 ----
+// One warp per row; 16-byte vector loads; the row stays in registers (NC vectors per
+// lane) between the absmax and the quantize pass, so HBM sees exactly one read of X.
+template <typename T, int NC>
+__global__ void __launch_bounds__(256) k_quantize_rowwise_vec(const T* __restrict__ x, int64_t rows, int64_t cols,
+                                                               int64_t ldx, int8_t* __restrict__ q, int64_t ldq,
+                                                               float* __restrict__ state, uint32_t* err) {
+  constexpr int VEC = 16 / sizeof(T);
+  using Out = typename VecQ<T>::Out;
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * ldx);
+  Out* qr = reinterpret_cast<Out*>(q + row * ldq);
+  const int nvec = static_cast<int>(cols / VEC);
+
+  uint4 buf[NC];
+  uint32_t amax = 0;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int v = c * 32 + lane;
+    if (v < nvec) {
+      buf[c] = ld_stream(xr + v);
+      amax = max(amax, vec_absmax_bits<T>(buf[c]));
+    }
+  }
+  amax = __reduce_max_sync(0xffffffffu, amax);
+  if (amax >= kNonFiniteBits) {
+    if (lane == 0) {
+      raise_nonfinite(err);
+      state[row] = __uint_as_float(amax);
+    }
+    return;
+  }
+  const float s = state_from_bits(amax);
+  if (lane == 0) state[row] = s;
+  const Scale sc = make_scale(s);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int v = c * 32 + lane;
+    if (v < nvec) qr[v] = VecQ<T>::run(buf[c], sc);
+  }
+}
+
+// Rows longer than the register budget: same algorithm, second pass re-reads (L2 hit).
+template <typename T>
+__global__ void __launch_bounds__(256) k_quantize_rowwise_stream(const T* __restrict__ x, int64_t rows, int64_t cols,
+                                                                  int64_t ldx, int8_t* __restrict__ q, int64_t ldq,
+                                                                  float* __restrict__ state, uint32_t* err) {
+  constexpr int VEC = 16 / sizeof(T);
+  using Out = typename VecQ<T>::Out;
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * ldx);
+  Out* qr = reinterpret_cast<Out*>(q + row * ldq);
+  const int64_t nvec = cols / VEC;
+  uint32_t amax = 0;
+  for (int64_t v = lane; v < nvec; v += 32) amax = max(amax, vec_absmax_bits<T>(__ldg(xr + v)));
+  amax = __reduce_max_sync(0xffffffffu, amax);
+  if (amax >= kNonFiniteBits) {
+    if (lane == 0) {
+      raise_nonfinite(err);
+      state[row] = __uint_as_float(amax);
+    }
+    return;
+  }
+  const float s = state_from_bits(amax);
+  if (lane == 0) state[row] = s;
+  const Scale sc = make_scale(s);
+  for (int64_t v = lane; v < nvec; v += 32) qr[v] = VecQ<T>::run(__ldg(xr + v), sc);
+}
+
+// Any shape / alignment: scalar element access.
+template <typename T>
+__global__ void __launch_bounds__(256) k_quantize_rowwise_scalar(const T* __restrict__ x, int64_t rows, int64_t cols,
+                                                                  int64_t ldx, int8_t* __restrict__ q, int64_t ldq,
+                                                                  float* __restrict__ state, uint32_t* err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const T* xr = x + row * ldx;
+  uint32_t amax = 0;
+  for (int64_t j = lane; j < cols; j += 32) amax = max(amax, abs_bits<T>(xr[j]));
+  amax = __reduce_max_sync(0xffffffffu, amax);
+  if (amax >= kNonFiniteBits) {
+    if (lane == 0) {
+      raise_nonfinite(err);
+      state[row] = __uint_as_float(amax);
+    }
+    return;
+  }
+  const float s = state_from_bits(amax);
+  if (lane == 0) state[row] = s;
+  const Scale sc = make_scale(s);
+  for (int64_t j = lane; j < cols; j += 32) q[row * ldq + j] = quantize_one(xr[j], sc);
+}
+
+template <typename T>
+cudaError_t rowwise_impl(sb_handle h, const T* x, int64_t rows, int64_t cols, int64_t ldx, int8_t* q, int64_t ldq,
+                         float* state) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int OUTB = VEC;  // bytes of payload per vector
+  const dim3 block(256);
+  const dim3 grid(static_cast<unsigned>((rows + 7) / 8));
+  const bool vec_ok = (cols % VEC == 0) && (ldx % VEC == 0) && sb::aligned(x, 16) && (ldq % OUTB == 0) &&
+                      sb::aligned(q, OUTB);
+  h->launches++;
+  if (!vec_ok) {
+    k_quantize_rowwise_scalar<T><<<grid, block, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
+    return cudaGetLastError();
+  }
+  const int64_t nvec = cols / VEC;
+  const int64_t per_lane = (nvec + 31) / 32;
+  if (per_lane <= 4)
+    k_quantize_rowwise_vec<T, 4><<<grid, block, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
+  else if (per_lane <= 8)
+    k_quantize_rowwise_vec<T, 8><<<grid, block, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
+  else if (per_lane <= 16)
+    k_quantize_rowwise_vec<T, 16><<<grid, block, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
+  else if (per_lane <= 24)
+    k_quantize_rowwise_vec<T, 24><<<grid, block, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
+  else
+    k_quantize_rowwise_stream<T><<<grid, block, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K2 ----
+// Tensor absmax: grid-stride over rows (warp per row), block max, one atomicMax per block.
+template <typename T>
+__global__ void __launch_bounds__(256) k_absmax_tensor(const T* __restrict__ x, int64_t rows, int64_t cols,
+                                                        int64_t ldx, unsigned int* word) {
+  __shared__ uint32_t wmax[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t m = 0;
+  const bool vec = (cols % (16 / sizeof(T)) == 0) && (ldx % (16 / sizeof(T)) == 0) && sb::aligned(x, 16);
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + warp; r < rows; r += static_cast<int64_t>(gridDim.x) * 8) {
+    const T* xr = x + r * ldx;
+    if (vec) {
+      const uint4* xv = reinterpret_cast<const uint4*>(xr);
+      const int64_t nvec = cols / (16 / sizeof(T));
+      for (int64_t v = lane; v < nvec; v += 32) m = max(m, vec_absmax_bits<T>(__ldg(xv + v)));
+    } else {
+      for (int64_t j = lane; j < cols; j += 32) m = max(m, abs_bits<T>(xr[j]));
+    }
+  }
+  m = __reduce_max_sync(0xffffffffu, m);
+  if (lane == 0) wmax[warp] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t b = 0;
+    for (int i = 0; i < 8; ++i) b = max(b, wmax[i]);
+    atomicMax(word, b);
+  }
+}
+
+// Row absmax only (fp8 row axis): one warp per row.
+template <typename T>
+__global__ void __launch_bounds__(256) k_absmax_rows(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx,
+                                                      unsigned int* words) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const T* xr = x + row * ldx;
+  uint32_t m = 0;
+  for (int64_t j = lane; j < cols; j += 32) m = max(m, abs_bits<T>(xr[j]));
+  m = __reduce_max_sync(0xffffffffu, m);
+  if (lane == 0) words[row] = m;
+}
+
+// ------------------------------------------------------------------ K4 ----
+// Column absmax: block = 32 columns x 8 row-lanes; grid.y splits rows; atomicMax per column.
+template <typename T>
+__global__ void __launch_bounds__(256) k_absmax_columns(const T* __restrict__ x, int64_t rows, int64_t cols,
+                                                         int64_t ldx, unsigned int* words) {
+  __shared__ uint32_t part[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t col = static_cast<int64_t>(blockIdx.x) * 32 + tx;
+  uint32_t m = 0;
+  if (col < cols)
+    for (int64_t r = static_cast<int64_t>(blockIdx.y) * 8 + ty; r < rows; r += static_cast<int64_t>(gridDim.y) * 8)
+      m = max(m, abs_bits<T>(x[r * ldx + col]));
+  part[ty][tx] = m;
+  __syncthreads();
+  if (ty == 0 && col < cols) {
+    for (int i = 1; i < 8; ++i) m = max(m, part[i][tx]);
+    atomicMax(words + col, m);
+  }
+}
+
+// ------------------------------------------------------------------ K3 ----
+// Quantize with tensor (one word) or per-column states. 64x64 tile per block: the
+// row-major payload is written straight out, the transposed payload goes through a
+// shared-memory tile so both layouts come from a single read of x (quantize.cpp:154-157).
+template <typename T>
+__global__ void __launch_bounds__(256) k_quantize_from_words(const T* __restrict__ x, int64_t rows, int64_t cols,
+                                                              int64_t ldx, const unsigned int* __restrict__ words,
+                                                              int per_column, int8_t* __restrict__ q, int64_t ldq,
+                                                              int8_t* __restrict__ qt, int64_t ldqt,
+                                                              float* __restrict__ state, uint32_t* err) {
+  __shared__ int8_t tile[64][64 + 4];
+  const int tx = threadIdx.x & 15;  // 4 columns each
+  const int ty = threadIdx.x >> 4;  // 16 rows per pass
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 64, c0 = static_cast<int64_t>(blockIdx.x) * 64;
+  // tensor state (or this thread's 4 column states)
+  uint32_t wb[4];
+  float st[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t c = c0 + tx * 4 + i;
+    wb[i] = per_column ? (c < cols ? words[c] : 0u) : words[0];
+    st[i] = state_from_bits(wb[i]);
+  }
+  const bool bad = (wb[0] >= kNonFiniteBits) || (wb[1] >= kNonFiniteBits) || (wb[2] >= kNonFiniteBits) ||
+                   (wb[3] >= kNonFiniteBits);
+  if (bad) raise_nonfinite(err);
+  // publish states once
+  if (blockIdx.y == 0) {
+    if (per_column) {
+      if (ty == 0)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t c = c0 + tx * 4 + i;
+          if (c < cols) state[c] = wb[i] >= kNonFiniteBits ? __uint_as_float(wb[i]) : st[i];
+        }
+    } else if (blockIdx.x == 0 && threadIdx.x == 0) {
+      state[0] = wb[0] >= kNonFiniteBits ? __uint_as_float(wb[0]) : st[0];
+    }
+  }
+  Scale sc[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) sc[i] = make_scale(st[i]);
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int lr = p * 16 + ty;
+    const int64_t r = r0 + lr;
+    uint32_t packed = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t c = c0 + tx * 4 + i;
+      int8_t v = 0;
+      if (r < rows && c < cols) v = quantize_one(x[r * ldx + c], sc[i]);
+      tile[lr][tx * 4 + i] = v;
+      packed |= static_cast<uint32_t>(static_cast<uint8_t>(v)) << (8 * i);
+    }
+    if (q && r < rows) {
+      const int64_t c = c0 + tx * 4;
+      if (c + 3 < cols && ((ldq & 3) == 0) && sb::aligned(q, 4)) {
+        *reinterpret_cast<uint32_t*>(q + r * ldq + c) = packed;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (c + i < cols) q[r * ldq + c + i] = tile[lr][tx * 4 + i];
+      }
+    }
+  }
+  if (!qt) return;
+  __syncthreads();
+  // transposed: qt[c][r] = tile[r][c]; thread handles 4 consecutive r of one c
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int lc = p * 16 + ty;
+    const int64_t c = c0 + lc;
+    if (c >= cols) continue;
+    const int64_t r = r0 + tx * 4;
+    if (r + 3 < rows && ((ldqt & 3) == 0) && sb::aligned(qt, 4)) {
+      uint32_t packed = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) packed |= static_cast<uint32_t>(static_cast<uint8_t>(tile[tx * 4 + i][lc])) << (8 * i);
+      *reinterpret_cast<uint32_t*>(qt + c * ldqt + r) = packed;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (r + i < rows) qt[c * ldqt + r + i] = tile[tx * 4 + i][lc];
+    }
+  }
+}
+
+// ----------------------------------------------------------------- K10 ----
+template <typename TO>
+__device__ __forceinline__ TO from_f32(float v);
+template <>
+__device__ __forceinline__ float from_f32<float>(float v) {
+  return v;
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+
+template <typename TO>
+__global__ void k_dequantize(const int8_t* __restrict__ q, int64_t rows, int64_t cols, int64_t ldq,
+                             const float* __restrict__ state, int axis, TO* __restrict__ y, int64_t ldy) {
+  const int64_t n = rows * cols;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    const float s = axis == 0 ? state[r] : axis == 1 ? state[c] : state[0];
+    // float(double(p) * double(s) / 127.0), quantize.cpp:191-194
+    const double d = __ddiv_rn(__dmul_rn(static_cast<double>(q[r * ldq + c]), static_cast<double>(s)), 127.0);
+    y[r * ldy + c] = from_f32<TO>(__double2float_rn(d));
+  }
+}
+
+// ------------------------------------------------------------------ K8 ----
+// fp8 snap with ties to the smaller magnitude and saturation at the set edges; returns
+// the e4m3 (bias 7, max 448, S.1111.111 = NaN) / e5m2 (bias 15, max 57344) byte.
+template <int MB, int BIAS>
+__device__ __forceinline__ uint8_t fp8_snap_encode(float r, float maxv, uint32_t maxcode) {
+  const uint32_t sign = (__float_as_uint(r) >> 31) << 7;
+  const float a = fabsf(r);
+  uint32_t code;
+  if (a >= maxv) {
+    code = maxcode;
+  } else if (a < __uint_as_float(static_cast<uint32_t>(128 - BIAS) << 23)) {  // below 2^(1-BIAS): denormal grid
+    const float n = __fmul_rn(a, __uint_as_float(static_cast<uint32_t>(127 + BIAS + MB - 1) << 23));  // exact
+    const float fl = floorf(n);
+    code = static_cast<uint32_t>(fl) + (__fsub_rn(n, fl) > 0.5f ? 1u : 0u);
+  } else {
+    constexpr uint32_t drop = 23 - MB;
+    const uint32_t bits = __float_as_uint(a);
+    const uint32_t rnd = (bits + (1u << (drop - 1)) - 1u) >> drop;  // round half toward zero
+    const uint32_t e32 = rnd >> MB, m = rnd & ((1u << MB) - 1u);
+    code = ((e32 - 127u + BIAS) << MB) | m;
+  }
+  return static_cast<uint8_t>(sign | code);
+}
+
+__device__ __forceinline__ float fp8_decode(uint8_t b, int fmt) {
+  const uint32_t s = (b >> 7) & 1u;
+  float v;
+  if (fmt == 0) {  // e4m3
+    const uint32_t e = (b >> 3) & 0xFu, m = b & 7u;
+    v = e == 0 ? ldexpf(static_cast<float>(m), -9) : ldexpf(1.0f + m / 8.0f, static_cast<int>(e) - 7);
+  } else {  // e5m2
+    const uint32_t e = (b >> 2) & 0x1Fu, m = b & 3u;
+    v = e == 0 ? ldexpf(static_cast<float>(m), -16) : ldexpf(1.0f + m / 4.0f, static_cast<int>(e) - 15);
+  }
+  return s ? -v : v;
+}
+
+template <typename T>
+__global__ void k_quantize_fp8(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx, int fmt, int axis,
+                               const unsigned int* __restrict__ words, uint8_t* __restrict__ q, int64_t ldq,
+                               float* __restrict__ state, uint32_t* err) {
+  const int64_t n = rows * cols;
+  const int64_t nstate = axis == 0 ? rows : axis == 1 ? cols : 1;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (int64_t i = tid; i < nstate; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t w = words[i];
+    if (w >= kNonFiniteBits) raise_nonfinite(err);
+    state[i] = w >= kNonFiniteBits ? __uint_as_float(w) : state_from_bits(w);
+  }
+  for (int64_t i = tid; i < n; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    const uint32_t w = words[axis == 0 ? r : axis == 1 ? c : 0];
+    const float s = state_from_bits(w);
+    // f32(double(x)/double(s)) == __fdiv_rn(x, s) (innocuous double rounding, 53 >= 2*24+2)
+    const float ratio = __fdiv_rn(to_f32(x[r * ldx + c]), s);
+    q[r * ldq + c] = fmt == 0 ? fp8_snap_encode<3, 7>(ratio, 448.0f, 0x7Eu)
+                              : fp8_snap_encode<2, 15>(ratio, 57344.0f, 0x7Bu);
+  }
+}
+
+template <typename TO>
+__global__ void k_dequantize_fp8(const uint8_t* __restrict__ q, int64_t rows, int64_t cols, int64_t ldq, int fmt,
+                                 const float* __restrict__ state, int axis, TO* __restrict__ y, int64_t ldy) {
+  const int64_t n = rows * cols;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    const float s = axis == 0 ? state[r] : axis == 1 ? state[c] : state[0];
+    // float(double(v) * double(s)) == __fmul_rn(v, s): the double product is exact
+    y[r * ldy + c] = from_f32<TO>(__fmul_rn(fp8_decode(q[r * ldq + c], fmt), s));
+  }
+}
+
+template <typename TI, typename TO>
+__global__ void k_convert(const TI* __restrict__ x, TO* __restrict__ y, int64_t n) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[i] = from_f32<TO>(to_f32(x[i]));
+}
+
+unsigned grid_for(int64_t n, int per_block, int num_sms) {
+  int64_t g = (n + per_block - 1) / per_block;
+  const int64_t cap = static_cast<int64_t>(num_sms) * 32;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<unsigned>(g);
+}
+
+}  // namespace
+
+namespace sb {
+
+cudaError_t launch_quantize_rowwise(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                                    int8_t* q, int64_t ldq, float* state) {
+  if (dt == SB_BF16)
+    return rowwise_impl(h, static_cast<const __nv_bfloat16*>(x), rows, cols, ldx, q, ldq, state);
+  return rowwise_impl(h, static_cast<const float*>(x), rows, cols, ldx, q, ldq, state);
+}
+
+cudaError_t launch_absmax_tensor(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                                 unsigned int* word) {
+  cudaError_t e = cudaMemsetAsync(word, 0, sizeof(unsigned int), h->stream);
+  if (e != cudaSuccess) return e;
+  const unsigned grid = grid_for(rows, 8, h->num_sms);
+  h->launches++;
+  if (dt == SB_BF16)
+    k_absmax_tensor<<<grid, 256, 0, h->stream>>>(static_cast<const __nv_bfloat16*>(x), rows, cols, ldx, word);
+  else
+    k_absmax_tensor<<<grid, 256, 0, h->stream>>>(static_cast<const float*>(x), rows, cols, ldx, word);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_absmax_rows(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                               unsigned int* words) {
+  const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
+  h->launches++;
+  if (dt == SB_BF16)
+    k_absmax_rows<<<grid, 256, 0, h->stream>>>(static_cast<const __nv_bfloat16*>(x), rows, cols, ldx, words);
+  else
+    k_absmax_rows<<<grid, 256, 0, h->stream>>>(static_cast<const float*>(x), rows, cols, ldx, words);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_absmax_columns(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                                  unsigned int* words) {
+  cudaError_t e = cudaMemsetAsync(words, 0, sizeof(unsigned int) * cols, h->stream);
+  if (e != cudaSuccess) return e;
+  const unsigned gx = static_cast<unsigned>((cols + 31) / 32);
+  int64_t gy = (rows + 63) / 64;
+  const int64_t cap = (static_cast<int64_t>(h->num_sms) * 8 + gx - 1) / gx;
+  if (gy > cap) gy = cap;
+  if (gy < 1) gy = 1;
+  h->launches++;
+  const dim3 grid(gx, static_cast<unsigned>(gy));
+  if (dt == SB_BF16)
+    k_absmax_columns<<<grid, 256, 0, h->stream>>>(static_cast<const __nv_bfloat16*>(x), rows, cols, ldx, words);
+  else
+    k_absmax_columns<<<grid, 256, 0, h->stream>>>(static_cast<const float*>(x), rows, cols, ldx, words);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quantize_from_words(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols,
+                                       int64_t ldx, const unsigned int* words, int per_column, int8_t* q, int64_t ldq,
+                                       int8_t* q_t, int64_t ldqt, float* state) {
+  const dim3 grid(static_cast<unsigned>((cols + 63) / 64), static_cast<unsigned>((rows + 63) / 64));
+  h->launches++;
+  if (dt == SB_BF16)
+    k_quantize_from_words<<<grid, 256, 0, h->stream>>>(static_cast<const __nv_bfloat16*>(x), rows, cols, ldx, words,
+                                                       per_column, q, ldq, q_t, ldqt, state, h->d_err);
+  else
+    k_quantize_from_words<<<grid, 256, 0, h->stream>>>(static_cast<const float*>(x), rows, cols, ldx, words,
+                                                       per_column, q, ldq, q_t, ldqt, state, h->d_err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dequantize(sb_handle h, const int8_t* q, int64_t rows, int64_t cols, int64_t ldq,
+                              const float* state, int axis, void* y, sb_dtype ydt, int64_t ldy) {
+  const unsigned grid = grid_for(rows * cols, 256 * 4, h->num_sms);
+  h->launches++;
+  if (ydt == SB_BF16)
+    k_dequantize<<<grid, 256, 0, h->stream>>>(q, rows, cols, ldq, state, axis, static_cast<__nv_bfloat16*>(y), ldy);
+  else
+    k_dequantize<<<grid, 256, 0, h->stream>>>(q, rows, cols, ldq, state, axis, static_cast<float*>(y), ldy);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quantize_fp8(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                                int fmt, int axis, const unsigned int* words, uint8_t* q, int64_t ldq, float* state) {
+  const unsigned grid = grid_for(rows * cols, 256 * 4, h->num_sms);
+  h->launches++;
+  if (dt == SB_BF16)
+    k_quantize_fp8<<<grid, 256, 0, h->stream>>>(static_cast<const __nv_bfloat16*>(x), rows, cols, ldx, fmt, axis,
+                                                words, q, ldq, state, h->d_err);
+  else
+    k_quantize_fp8<<<grid, 256, 0, h->stream>>>(static_cast<const float*>(x), rows, cols, ldx, fmt, axis, words, q,
+                                                ldq, state, h->d_err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dequantize_fp8(sb_handle h, const uint8_t* q, int64_t rows, int64_t cols, int64_t ldq, int fmt,
+                                  const float* state, int axis, void* y, sb_dtype ydt, int64_t ldy) {
+  const unsigned grid = grid_for(rows * cols, 256 * 4, h->num_sms);
+  h->launches++;
+  if (ydt == SB_BF16)
+    k_dequantize_fp8<<<grid, 256, 0, h->stream>>>(q, rows, cols, ldq, fmt, state, axis,
+                                                  static_cast<__nv_bfloat16*>(y), ldy);
+  else
+    k_dequantize_fp8<<<grid, 256, 0, h->stream>>>(q, rows, cols, ldq, fmt, state, axis, static_cast<float*>(y), ldy);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_convert(sb_handle h, const void* x, sb_dtype xdt, void* y, sb_dtype ydt, int64_t n) {
+  const unsigned grid = grid_for(n, 256 * 4, h->num_sms);
+  h->launches++;
+  if (xdt == SB_F32 && ydt == SB_BF16)
+    k_convert<<<grid, 256, 0, h->stream>>>(static_cast<const float*>(x), static_cast<__nv_bfloat16*>(y), n);
+  else if (xdt == SB_BF16 && ydt == SB_F32)
+    k_convert<<<grid, 256, 0, h->stream>>>(static_cast<const __nv_bfloat16*>(x), static_cast<float*>(y), n);
+  else
+    return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+}  // namespace sb

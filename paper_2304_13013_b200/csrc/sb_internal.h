@@ -1,0 +1,102 @@
+// sb_internal.h — shared host-side plumbing for the C-ABI implementation.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/switchback_b200.h"
+
+struct sb_handle_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  uint32_t* d_err = nullptr;       // device error latch (bit 0: non-finite input seen)
+  unsigned int* d_scratch = nullptr;  // small scratch (tensor absmax words etc.)
+  size_t scratch_bytes = 0;
+  uint64_t launches = 0;
+  // host-buffer pipeline (sb_switchback_fwd_bwd_host)
+  cudaStream_t aux_stream = nullptr;
+  void* dev_pool = nullptr;
+  size_t dev_pool_bytes = 0;
+};
+
+namespace sb {
+
+// Thread-local "<op>: <reason>" error text (sb_last_error).
+void set_error(const std::string& msg);
+sb_status fail(sb_status st, const char* op, const char* reason);
+sb_status cuda_fail(const char* op, cudaError_t e);
+
+#define SB_CUDA_CHECK(op, expr)                    \
+  do {                                             \
+    cudaError_t _e = (expr);                       \
+    if (_e != cudaSuccess) return sb::cuda_fail(op, _e); \
+  } while (0)
+
+#define SB_LAUNCH_CHECK(op)                                 \
+  do {                                                      \
+    cudaError_t _e = cudaGetLastError();                    \
+    if (_e != cudaSuccess) return sb::cuda_fail(op, _e);    \
+  } while (0)
+
+inline size_t dt_size(sb_dtype dt) {
+  switch (dt) {
+    case SB_F32: return 4;
+    case SB_BF16: return 2;
+    case SB_I32: return 4;
+    case SB_I8: return 1;
+    case SB_U8: return 1;
+    case SB_I64: return 8;
+  }
+  return 0;
+}
+__host__ __device__ inline bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+// Scratch words (device, unsigned) owned by the handle; grows on demand (not on hot path
+// after the first call at a given size).
+unsigned int* scratch(sb_handle h, size_t words);
+
+// TMA tensor-map encoding through the driver entry point (no -lcuda link).
+bool encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer,
+                    uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz);
+
+// ----------------------------------------------------------- launchers ----
+// quantize.cu
+cudaError_t launch_quantize_rowwise(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                                    int8_t* q, int64_t ldq, float* state);
+cudaError_t launch_absmax_tensor(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                                 unsigned int* word);
+cudaError_t launch_absmax_columns(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                                  unsigned int* words);
+// Quantize with states from absmax words (tensor: one word; column: cols words);
+// writes q and/or q_t; also writes the float states (sentinel applied).
+cudaError_t launch_quantize_from_words(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols,
+                                       int64_t ldx, const unsigned int* words, int per_column, int8_t* q, int64_t ldq,
+                                       int8_t* q_t, int64_t ldqt, float* state);
+cudaError_t launch_dequantize(sb_handle h, const int8_t* q, int64_t rows, int64_t cols, int64_t ldq,
+                              const float* state, int axis, void* y, sb_dtype ydt, int64_t ldy);
+cudaError_t launch_quantize_fp8(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                                int fmt, int axis, const unsigned int* words, uint8_t* q, int64_t ldq, float* state);
+cudaError_t launch_absmax_rows(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                               unsigned int* words);
+cudaError_t launch_dequantize_fp8(sb_handle h, const uint8_t* q, int64_t rows, int64_t cols, int64_t ldq, int fmt,
+                                  const float* state, int axis, void* y, sb_dtype ydt, int64_t ldy);
+cudaError_t launch_convert(sb_handle h, const void* x, sb_dtype xdt, void* y, sb_dtype ydt, int64_t n);
+
+// gemm_i8.cu
+sb_status gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* qb, const float* sb, int scale_mode,
+                  int64_t M, int64_t N, int64_t K, void* out, sb_dtype out_dt, int exact);
+// gemm_bf16.cu
+sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m, int64_t n, float* dw,
+                int exact, int accumulate);
+sb_status matmul_f32_seq(sb_handle h, const float* a, int64_t a_rs, int64_t a_ks, const float* bt, int64_t b_rs,
+                         int64_t b_ks, int64_t r, int64_t c, int64_t k, float* y, int accumulate);
+sb_status gemm_bf16_tc(sb_handle h, const void* a, bool a_mn, const void* b, bool b_mn, int64_t M, int64_t N, int64_t K,
+                       void* out, sb_dtype out_dt, const float* one);
+// gemm_fp8
+sb_status gemm_fp8(sb_handle h, const uint8_t* qa, int fa, const float* sa, int axa, const uint8_t* qb, int fb,
+                   const float* sb, int axb, int64_t M, int64_t N, int64_t K, void* out, sb_dtype out_dt);
+
+}  // namespace sb

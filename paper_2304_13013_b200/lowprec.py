@@ -1,0 +1,432 @@
+"""Python face of the reference's ``lowprec`` operator API, on B200 device tensors.
+
+Same names, argument meaning and error behaviour as the C++ reference
+(proj/core/include/lowprec/{quantize,linear,optimizer}.hpp), so parity tests read
+like the reference's own tests. Tensors are torch CUDA tensors (plumbing only:
+device memory and the current stream); every operation is a call through the
+C-ABI (include/switchback_b200.h) into hand-written sm_100a kernels.
+
+Differences from the reference, by design:
+  * the performance path keeps bf16 activations/weights (exact=False); exact=True
+    reproduces the reference's fp32 numerics bit for bit (fp64 dequant epilogue,
+    sequential fp32 weight gradient),
+  * non-finite inputs are detected on the device; with ``check=True`` (default for the
+    drop-in API) the call synchronizes and raises InvalidArgument("<op>: non-finite input").
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _capi as A
+from ._capi import InvalidArgument, SBError  # noqa: F401  (re-exported)
+
+ROW, COLUMN, TENSOR = A.SB_AXIS_ROW, A.SB_AXIS_COLUMN, A.SB_AXIS_TENSOR
+E4M3, E5M2 = A.SB_E4M3, A.SB_E5M2
+
+_VARIANTS = ["Standard", "SwitchBack", "SwitchBackM", "SwitchBackQ", "AllQuant"]  # linear.cpp:8-25
+
+
+def to_string(variant: int) -> str:
+    return _VARIANTS[variant]
+
+
+def parse_linear_variant(name: str) -> int:
+    if name not in _VARIANTS:
+        raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, f"unknown linear variant: {name}")
+    return _VARIANTS.index(name)
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return A.SB_F32
+    if t.dtype == torch.bfloat16:
+        return A.SB_BF16
+    raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, f"unsupported dtype {t.dtype}")
+
+
+def _p(t: torch.Tensor | None) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr() if t is not None else 0)
+
+
+def _need_cuda(*ts: torch.Tensor) -> None:
+    for t in ts:
+        if not t.is_cuda:
+            raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "switchback_b200: tensors must live on the B200")
+
+
+def _check_nonfinite(h: A.Handle, check: bool) -> None:
+    if check:
+        h.synchronize()
+
+
+@dataclass
+class QuantizedMatrix:
+    """quantize.hpp:48-65. payload int8 (or uint8 fp8 bytes) row-major; state per axis."""
+    payload: torch.Tensor
+    state: torch.Tensor
+    axis: int
+    fp8: bool = False
+    fmt: int = E4M3
+
+    @property
+    def rows(self) -> int:
+        return self.payload.shape[0]
+
+    @property
+    def cols(self) -> int:
+        return self.payload.shape[1]
+
+
+# ------------------------------------------------------------------ quantize
+def quantize_rowwise(x: torch.Tensor, check: bool = True) -> QuantizedMatrix:
+    """quantize.cpp:131-133."""
+    _need_cuda(x)
+    x = x.contiguous()
+    r, c = x.shape
+    q = torch.empty((r, c), dtype=torch.int8, device=x.device)
+    st = torch.empty(r, dtype=torch.float32, device=x.device)
+    h = A.handle(x.device.index)
+    A.check(h.lib.sb_quantize_rowwise(h.h, _p(x), _dt(x), r, c, c, _p(q), c, _p(st)))
+    try:
+        _check_nonfinite(h, check)
+    except InvalidArgument:
+        raise InvalidArgument(A.SB_ERR_NONFINITE, "quantize_rowwise: non-finite input") from None
+    return QuantizedMatrix(q, st, ROW)
+
+
+def quantize_columnwise(x: torch.Tensor, check: bool = True, transposed: bool = False) -> QuantizedMatrix:
+    """quantize.cpp:135-137. transposed=True returns quantize_rowwise(x^T) (linear.cpp:228-229)."""
+    _need_cuda(x)
+    x = x.contiguous()
+    r, c = x.shape
+    st = torch.empty(c, dtype=torch.float32, device=x.device)
+    h = A.handle(x.device.index)
+    if transposed:
+        qt = torch.empty((c, r), dtype=torch.int8, device=x.device)
+        A.check(h.lib.sb_quantize_columnwise(h.h, _p(x), _dt(x), r, c, c, _p(None), 0, _p(qt), r, _p(st)))
+        out = QuantizedMatrix(qt, st, ROW)
+    else:
+        q = torch.empty((r, c), dtype=torch.int8, device=x.device)
+        A.check(h.lib.sb_quantize_columnwise(h.h, _p(x), _dt(x), r, c, c, _p(q), c, _p(None), 0, _p(st)))
+        out = QuantizedMatrix(q, st, COLUMN)
+    try:
+        _check_nonfinite(h, check)
+    except InvalidArgument:
+        raise InvalidArgument(A.SB_ERR_NONFINITE, "quantize_columnwise: non-finite input") from None
+    return out
+
+
+def quantize_tensorwise(x: torch.Tensor, check: bool = True, with_transpose: bool = False):
+    """quantize.cpp:139-141. with_transpose=True also returns the transposed payload
+    from the same pass (quantize.cpp:143-159) -> (q, q_t)."""
+    _need_cuda(x)
+    x = x.contiguous()
+    r, c = x.shape
+    q = torch.empty((r, c), dtype=torch.int8, device=x.device)
+    qt = torch.empty((c, r), dtype=torch.int8, device=x.device) if with_transpose else None
+    st = torch.empty(1, dtype=torch.float32, device=x.device)
+    h = A.handle(x.device.index)
+    A.check(h.lib.sb_quantize_tensorwise(h.h, _p(x), _dt(x), r, c, c, _p(q), c, _p(qt), r, _p(st)))
+    try:
+        _check_nonfinite(h, check)
+    except InvalidArgument:
+        raise InvalidArgument(A.SB_ERR_NONFINITE, "quantize_tensorwise: non-finite input") from None
+    if with_transpose:
+        return QuantizedMatrix(q, st, TENSOR), QuantizedMatrix(qt, st, TENSOR)
+    return QuantizedMatrix(q, st, TENSOR)
+
+
+def quantize_tensorwise_transpose(x: torch.Tensor, check: bool = True) -> QuantizedMatrix:
+    """quantize.cpp:143-159: == quantize_tensorwise(x^T), written transposed in one pass."""
+    _need_cuda(x)
+    x = x.contiguous()
+    r, c = x.shape
+    qt = torch.empty((c, r), dtype=torch.int8, device=x.device)
+    st = torch.empty(1, dtype=torch.float32, device=x.device)
+    h = A.handle(x.device.index)
+    A.check(h.lib.sb_quantize_tensorwise(h.h, _p(x), _dt(x), r, c, c, _p(None), 0, _p(qt), r, _p(st)))
+    try:
+        _check_nonfinite(h, check)
+    except InvalidArgument:
+        raise InvalidArgument(A.SB_ERR_NONFINITE, "quantize_tensorwise_transpose: non-finite input") from None
+    return QuantizedMatrix(qt, st, TENSOR)
+
+
+def quantize_fp8(x: torch.Tensor, fmt: int, axis: int, check: bool = True) -> QuantizedMatrix:
+    """quantize.cpp:161-176; payload stored as e4m3/e5m2 bytes (uint8)."""
+    _need_cuda(x)
+    x = x.contiguous()
+    r, c = x.shape
+    q = torch.empty((r, c), dtype=torch.uint8, device=x.device)
+    st = torch.empty(r if axis == ROW else c if axis == COLUMN else 1, dtype=torch.float32, device=x.device)
+    h = A.handle(x.device.index)
+    A.check(h.lib.sb_quantize_fp8(h.h, _p(x), _dt(x), r, c, c, fmt, axis, _p(q), c, _p(st)))
+    try:
+        _check_nonfinite(h, check)
+    except InvalidArgument:
+        raise InvalidArgument(A.SB_ERR_NONFINITE, "quantize_fp8: non-finite input") from None
+    return QuantizedMatrix(q, st, axis, fp8=True, fmt=fmt)
+
+
+def dequantize(q: QuantizedMatrix, dtype: torch.dtype = torch.float32) -> torch.Tensor:
+    """quantize.cpp:178-197."""
+    want = q.rows if q.axis == ROW else q.cols if q.axis == COLUMN else 1
+    if q.state.numel() != want:
+        raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "dequantize: state length does not match axis")
+    y = torch.empty((q.rows, q.cols), dtype=dtype, device=q.payload.device)
+    h = A.handle(q.payload.device.index)
+    if q.fp8:
+        A.check(h.lib.sb_dequantize_fp8(h.h, _p(q.payload), q.rows, q.cols, q.cols, q.fmt, _p(q.state), q.axis,
+                                        _p(y), _dt(y), q.cols))
+    else:
+        A.check(h.lib.sb_dequantize(h.h, _p(q.payload), q.rows, q.cols, q.cols, _p(q.state), q.axis, _p(y), _dt(y),
+                                    q.cols))
+    return y
+
+
+# -------------------------------------------------------------------- GEMMs
+def _int8_product(qa: QuantizedMatrix, qb: QuantizedMatrix, mode: int, out_dtype, exact: bool) -> torch.Tensor:
+    if qa.cols != qb.cols:
+        raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "int8 matmul: inner dimension mismatch")  # linear.cpp:55
+    M, K, N = qa.rows, qa.cols, qb.rows
+    dev = qa.payload.device
+    h = A.handle(dev.index)
+    if out_dtype == "raw":
+        out = torch.empty((M, N), dtype=torch.int64 if K > 133144 else torch.int32, device=dev)
+        odt = A.SB_I64 if K > 133144 else A.SB_I32
+        A.check(h.lib.sb_gemm_i8(h.h, _p(qa.payload), _p(None), _p(qb.payload), _p(None), A.SB_SCALE_NONE, M, N, K,
+                                 _p(out), odt, 0))
+        return out
+    out = torch.empty((M, N), dtype=out_dtype, device=dev)
+    A.check(h.lib.sb_gemm_i8(h.h, _p(qa.payload), _p(qa.state), _p(qb.payload), _p(qb.state), mode, M, N, K, _p(out),
+                             _dt(out), int(exact)))
+    return out
+
+
+def int8_matmul_dequant(qx: QuantizedMatrix, qw: QuantizedMatrix, out_dtype=torch.float32,
+                        exact: bool = True) -> torch.Tensor:
+    """linear.cpp:71-76: row-wise X against tensor-wise W, int32 accumulate, dequant epilogue.
+    out_dtype='raw' returns the integer accumulators."""
+    if qx.fp8 or qw.fp8:
+        raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "int8_matmul_dequant: fp8 operand")
+    if qx.axis != ROW or qw.axis != TENSOR:
+        raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "int8_matmul_dequant: need row-wise X and tensor-wise W")
+    return _int8_product(qx, qw, A.SB_SCALE_ROW_TENSOR, out_dtype, exact)
+
+
+def matmul_dequant_dual_rowwise(qa: QuantizedMatrix, qb: QuantizedMatrix, out_dtype=torch.float32,
+                                exact: bool = True) -> torch.Tensor:
+    """linear.cpp:78-83."""
+    if qa.fp8 or qb.fp8:
+        raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "matmul_dequant_dual_rowwise: fp8 operand")
+    if qa.axis != ROW or qb.axis != ROW:
+        raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT,
+                              "matmul_dequant_dual_rowwise: both operands must be row-wise")
+    return _int8_product(qa, qb, A.SB_SCALE_ROW_ROW, out_dtype, exact)
+
+
+def matmul(a: torch.Tensor, b_transposed: torch.Tensor) -> torch.Tensor:
+    """matrix.cpp:53-68: A . B^T, sequential fp32 reduction, bit-identical to the reference."""
+    _need_cuda(a, b_transposed)
+    if a.shape[1] != b_transposed.shape[1]:
+        raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "matmul: inner dimension mismatch")
+    a = a.contiguous().float()
+    b = b_transposed.contiguous().float()
+    y = torch.empty((a.shape[0], b.shape[0]), dtype=torch.float32, device=a.device)
+    h = A.handle(a.device.index)
+    A.check(h.lib.sb_matmul_f32(h.h, _p(a), _p(b), a.shape[0], b.shape[0], a.shape[1], _p(y)))
+    return y
+
+
+def wgrad(g: torch.Tensor, x: torch.Tensor, exact: bool | None = None, out: torch.Tensor | None = None,
+          accumulate: bool = False) -> torch.Tensor:
+    """wgrad_full_precision, linear.cpp:193-195: G^T X (fp32 out)."""
+    _need_cuda(g, x)
+    b, m = g.shape
+    n = x.shape[1]
+    if exact is None:
+        exact = g.dtype == torch.float32
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float32, device=g.device)
+    h = A.handle(g.device.index)
+    A.check(h.lib.sb_wgrad(h.h, _p(g), _p(x), _dt(g), b, m, n, _p(out), int(exact), int(accumulate)))
+    return out
+
+
+def gemm_fp8(qa: QuantizedMatrix, qb: QuantizedMatrix, out_dtype=torch.float32) -> torch.Tensor:
+    """fp8 SwitchBack product (linear.cpp:151-153): snapped operands, tensor-core accumulation."""
+    M, K, N = qa.rows, qa.cols, qb.rows
+    out = torch.empty((M, N), dtype=out_dtype, device=qa.payload.device)
+    h = A.handle(qa.payload.device.index)
+    A.check(h.lib.sb_gemm_fp8(h.h, _p(qa.payload), qa.fmt, _p(qa.state), qa.axis, _p(qb.payload), qb.fmt,
+                              _p(qb.state), qb.axis, M, N, K, _p(out), _dt(out)))
+    return out
+
+
+# -------------------------------------------------------------------- layer
+@dataclass
+class LinearMode:
+    """linear.hpp:30-35 (+ exact: reference-bit-exact numerics)."""
+    variant: int = A.SB_STANDARD
+    format: int = A.SB_INT8
+    fp8_forward: int = E4M3
+    fp8_gradient: int = E5M2
+    exact: bool = False
+
+    def c(self) -> A.LinearMode:
+        return A.LinearMode(self.variant, self.format, self.fp8_forward, self.fp8_gradient, int(self.exact))
+
+    def __eq__(self, o) -> bool:  # linear.cpp:27-32
+        if self.variant != o.variant or self.format != o.format or self.exact != o.exact:
+            return False
+        return self.format == A.SB_INT8 or (self.fp8_forward == o.fp8_forward and self.fp8_gradient == o.fp8_gradient)
+
+
+@dataclass
+class LinearContext:
+    """linear.hpp:39-48. Holds the device context plus the tensors it references."""
+    mode: LinearMode | None = None
+    raw: A.LinearCtx = field(default_factory=A.LinearCtx)
+    keep: tuple = ()
+    workspace: torch.Tensor | None = None
+
+
+def _workspace(mode: LinearMode, b: int, n: int, m: int, device) -> torch.Tensor:
+    nbytes = C.c_size_t()
+    A.check(A.load().sb_linear_workspace_size(C.byref(mode.c()), b, n, m, C.byref(nbytes)))
+    return torch.empty(nbytes.value, dtype=torch.uint8, device=device)
+
+
+def linear_forward(mode: LinearMode, x: torch.Tensor, w: torch.Tensor, ctx: LinearContext | None = None,
+                   workspace: torch.Tensor | None = None, check: bool = True) -> torch.Tensor:
+    """linear.cpp:113-164: Y = X W^T through the variant's quantized path."""
+    _need_cuda(x, w)
+    if x.dim() != 2 or w.dim() != 2 or x.numel() == 0 or w.numel() == 0:
+        raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "linear_forward: empty operand")
+    if x.shape[1] != w.shape[1]:
+        raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "linear_forward: X is b x n but W is not m x n")
+    if x.dtype != w.dtype:
+        raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "linear_forward: X and W dtypes differ")
+    x, w = x.contiguous(), w.contiguous()
+    b, n = x.shape
+    m = w.shape[0]
+    if workspace is None:
+        workspace = _workspace(mode, b, n, m, x.device)
+    y = torch.empty((b, m), dtype=x.dtype, device=x.device)
+    h = A.handle(x.device.index)
+    raw = A.LinearCtx()
+    st = h.lib.sb_linear_forward(h.h, C.byref(mode.c()), _p(x), _p(w), _dt(x), b, n, m, _p(y), C.byref(raw),
+                                 _p(workspace), workspace.numel())
+    A.check(st)
+    try:
+        _check_nonfinite(h, check)
+    except InvalidArgument:
+        raise InvalidArgument(A.SB_ERR_NONFINITE, "linear_forward: non-finite input") from None
+    if ctx is not None:
+        ctx.mode = mode
+        ctx.raw = raw
+        ctx.keep = (x, w) if mode.variant != A.SB_SWITCHBACK_M else ()
+        ctx.workspace = workspace
+    return y
+
+
+def linear_backward(mode: LinearMode, ctx: LinearContext, g: torch.Tensor, dw: torch.Tensor | None = None,
+                    dw_accumulate: bool = False, check: bool = True) -> tuple[torch.Tensor, torch.Tensor]:
+    """linear.cpp:199-278 -> (x_grad [b x n], w_grad [m x n] fp32)."""
+    if ctx.mode is None or not (mode == ctx.mode):
+        raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT,
+                              "linear_backward: context was produced by a different mode")
+    r = ctx.raw
+    if g.dim() != 2 or g.shape[0] != r.b or g.shape[1] != r.m:
+        raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "linear_backward: G must be b x m")
+    _need_cuda(g)
+    g = g.contiguous()
+    dx = torch.empty((r.b, r.n), dtype=g.dtype, device=g.device)
+    if dw is None:
+        dw = torch.empty((r.m, r.n), dtype=torch.float32, device=g.device)
+    h = A.handle(g.device.index)
+    A.check(h.lib.sb_linear_backward(h.h, C.byref(mode.c()), C.byref(r), _p(g), _p(dx), _p(dw), int(dw_accumulate)))
+    try:
+        _check_nonfinite(h, check)
+    except InvalidArgument:
+        raise InvalidArgument(A.SB_ERR_NONFINITE, "linear_backward: non-finite input") from None
+    return dx, dw
+
+
+def switchback_fwd_bwd_host(x, w, g, exact: bool = False):
+    """bench.cpp:75-81 over HOST tensors (pinned CPU torch tensors): returns (y, dx, dw) on the
+    host. Copies + kernels pipelined over token chunks inside the C-ABI call."""
+    b, n = x.shape
+    m = w.shape[0]
+    y = torch.empty((b, m), dtype=x.dtype, pin_memory=True)
+    dx = torch.empty((b, n), dtype=x.dtype, pin_memory=True)
+    dw = torch.empty((m, n), dtype=torch.float32, pin_memory=True)
+    h = A.handle()
+    md = LinearMode(A.SB_SWITCHBACK, A.SB_INT8, exact=exact)
+    A.check(h.lib.sb_switchback_fwd_bwd_host(h.h, C.byref(md.c()), _p(x), _p(w), _p(g), _dt(x), b, n, m, _p(y),
+                                             _p(dx), _p(dw)))
+    return y, dx, dw
+
+
+# ---------------------------------------------------------------- optimizer
+@dataclass
+class OptimizerHyperparams:
+    """optimizer.hpp:21-33; lr_schedule is a Python callable t -> alpha_t."""
+    lr_schedule: object = None
+    beta1: float = 0.9
+    beta2: float = 0.99
+    beta2_warmup_lambda: float = 0.0
+    eps: float = 1e-6
+    weight_decay: float = 0.0
+    clipping: int = A.SB_CLIP_NONE
+    max_grad_norm: float = 1.0
+
+
+@dataclass
+class TensorRef:
+    """optimizer.hpp:74-79 (fp32 device tensors, updated in place)."""
+    name: str
+    param: torch.Tensor
+    grad: torch.Tensor
+    v: torch.Tensor
+    u: torch.Tensor
+
+
+def optimizer_step(tensors: list[TensorRef], hp: OptimizerHyperparams, t: int,
+                   workspace: torch.Tensor | None = None, infos: bool = True):
+    """optimizer.cpp:102-172. Returns [(rms, eta)] per tensor (TensorStepInfo), or the
+    device tensor of shape [n, 2] when infos=False (no host sync)."""
+    if t < 1:
+        raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "optimizer_step: t must be >= 1")
+    if hp.lr_schedule is None:
+        raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "optimizer_step: lr_schedule not set")
+    for r in tensors:
+        if r.param is None or r.grad is None or r.v is None or r.u is None:
+            raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "optimizer_step: null tensor reference")
+        if not (r.param.shape == r.grad.shape == r.v.shape == r.u.shape):
+            raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, f"optimizer_step: shape mismatch for {r.name}")
+        for a in (r.param, r.grad, r.v, r.u):
+            if a.dtype != torch.float32 or not a.is_cuda or not a.is_contiguous():
+                raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "optimizer_step: tensors must be contiguous fp32 CUDA")
+    n = len(tensors)
+    arr = (A.AdamwTensor * max(n, 1))()
+    for i, r in enumerate(tensors):
+        arr[i] = A.AdamwTensor(r.param.data_ptr(), r.grad.data_ptr(), r.v.data_ptr(), r.u.data_ptr(), r.param.numel())
+    dev = tensors[0].param.device if n else torch.device("cuda")
+    if workspace is None:
+        nbytes = C.c_size_t()
+        A.check(A.load().sb_stableadamw_workspace_size(arr, n, C.byref(nbytes)))
+        workspace = torch.empty(nbytes.value, dtype=torch.uint8, device=dev)
+    out = torch.empty((2, max(n, 1)), dtype=torch.float64, device=dev)
+    hpc = A.AdamwHparams(float(hp.lr_schedule(t)), hp.beta1, hp.beta2, hp.beta2_warmup_lambda, hp.eps,
+                         hp.weight_decay, hp.max_grad_norm, int(hp.clipping))
+    h = A.handle(dev.index)
+    A.check(h.lib.sb_stableadamw_step(h.h, arr, n, C.byref(hpc), t, _p(out[0]), _p(out[1]), _p(workspace),
+                                      workspace.numel()))
+    if not infos:
+        return out
+    o = out.cpu()
+    return [(float(o[0, i]), float(o[1, i])) for i in range(n)]

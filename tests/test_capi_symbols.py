@@ -1,0 +1,48 @@
+"""CPU: the C-ABI library loads and exports every entry point include/switchback_b200.h declares;
+without a device the product path fails loudly (no CPU fallback)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from paper_2304_13013_b200 import _capi as A
+
+HDR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "switchback_b200.h")
+
+
+def declared_symbols():
+    text = open(HDR).read()
+    return sorted(set(re.findall(r"^\s*(?:[A-Za-z_][\w\s\*]*?\s\**)?(sb_[a-z0-9_]+)\s*\(", text, re.M)))
+
+
+def test_header_declares_expected_entry_points():
+    assert declared_symbols() == sorted(A.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    L = A.load()
+    for name in declared_symbols():
+        assert hasattr(L, name), name
+    assert L.sb_abi_version() == 1
+
+
+def test_library_is_sm100a():
+    import subprocess
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-lelf", A.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_device_fails_loudly():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a device is present")
+    L = A.load()
+    h = C.c_void_p()
+    st = L.sb_create(0, C.byref(h))
+    assert st != A.SB_OK
+    assert b"no CUDA device" in L.sb_last_error()
+    with pytest.raises(A.SBError):
+        A.handle(0)

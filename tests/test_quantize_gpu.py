@@ -1,0 +1,124 @@
+"""GPU parity: quantize kernels (K1-K4, K8, K10) vs the oracle — bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2304_13013_b200 import lowprec as L
+from tests._util import adversarial, bf16, dev, fp8_decode, host
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(1, 1), (3, 5), (13, 70), (7, 8), (64, 1024), (37, 1280), (33, 5120), (9, 8200), (5, 16384), (2, 40000)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_rowwise_bit_exact(shape, dtype):
+    x = adversarial(*shape, seed=sum(shape))
+    if dtype == torch.bfloat16:
+        x = bf16(x)
+    q = L.quantize_rowwise(dev(x, dtype))
+    qo, so = O.quantize(x, O.ROW)
+    assert np.array_equal(host(q.payload), qo)
+    assert np.array_equal(host(q.state), so)
+
+
+@pytest.mark.parametrize("scale", [1e-38, 1e-20, 1.0, 1e20, 3e38])
+def test_rowwise_random_scales_fp32(scale):
+    rng = np.random.default_rng(1)
+    x = (rng.standard_normal((257, 333)) * scale).astype(np.float32)
+    q = L.quantize_rowwise(dev(x))
+    qo, so = O.quantize(x, O.ROW)
+    assert np.array_equal(host(q.payload), qo) and np.array_equal(host(q.state), so)
+
+
+def test_rowwise_every_tie_exhaustive_bf16():
+    # all 2^16 bf16 bit patterns that are finite, against a row state of 2.0 (ties at p/2*2/127)
+    u = np.arange(0, 65536, dtype=np.uint32) << 16
+    v = u.view(np.float32)
+    v = v[np.isfinite(v) & (np.abs(v) <= 2.0)]
+    x = np.concatenate([v, [2.0]]).astype(np.float32)
+    pad = (-x.size) % 8
+    x = np.concatenate([x, np.zeros(pad, np.float32)]).reshape(1, -1)
+    q = L.quantize_rowwise(dev(x, torch.bfloat16))
+    qo, so = O.quantize(x, O.ROW)
+    assert np.array_equal(host(q.payload), qo) and np.array_equal(host(q.state), so)
+
+
+def test_rowwise_nonfinite_raises():
+    x = np.ones((4, 64), np.float32)
+    x[2, 5] = np.nan
+    with pytest.raises(L.InvalidArgument, match="quantize_rowwise: non-finite input"):
+        L.quantize_rowwise(dev(x))
+    x[2, 5] = np.inf
+    with pytest.raises(L.InvalidArgument, match="non-finite"):
+        L.quantize_rowwise(dev(x, torch.bfloat16))
+    L.quantize_rowwise(dev(np.ones((4, 64), np.float32)))  # latch cleared
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (3, 5), (13, 70), (64, 64), (130, 70), (1280, 5120), (5120, 1280)])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_tensorwise_and_transpose_bit_exact(shape, dtype):
+    x = adversarial(*shape, seed=3)
+    x[4:5] = 0 if shape[0] > 4 else x[4:5]  # keep one global absmax from the "huge" row out of the way
+    if dtype == torch.bfloat16:
+        x = bf16(x)
+    q, qt = L.quantize_tensorwise(dev(x, dtype), with_transpose=True)
+    qo, so = O.quantize(x, O.TENSOR)
+    qto, sto = O.quantize(x, O.TENSOR_T)
+    assert np.array_equal(host(q.payload), qo) and np.array_equal(host(q.state), so)
+    assert np.array_equal(host(qt.payload), qto)
+    q2 = L.quantize_tensorwise_transpose(dev(x, dtype))
+    assert np.array_equal(host(q2.payload), qto) and np.array_equal(host(q2.state), sto)
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (2, 3), (13, 70), (300, 77), (1280, 5120)])
+def test_columnwise_bit_exact(shape):
+    x = adversarial(*shape, seed=5).T.copy() if shape[0] > 7 else adversarial(*shape, seed=5)
+    q = L.quantize_columnwise(dev(x))
+    qo, so = O.quantize(x, O.COL)
+    assert np.array_equal(host(q.payload), qo) and np.array_equal(host(q.state), so)
+    qt = L.quantize_columnwise(dev(x), transposed=True)  # == quantize_rowwise(x^T)
+    qro, sro = O.quantize(x.T.copy(), O.ROW)
+    assert np.array_equal(host(qt.payload), qro) and np.array_equal(host(qt.state), sro)
+
+
+@pytest.mark.parametrize("axis", [L.ROW, L.COLUMN, L.TENSOR])
+def test_dequantize_bit_exact(axis):
+    x = adversarial(29, 77, seed=9)
+    ax = {L.ROW: O.ROW, L.COLUMN: O.COL, L.TENSOR: O.TENSOR}[axis]
+    qo, so = O.quantize(x, ax)
+    q = L.QuantizedMatrix(dev(qo, torch.int8), dev(so), axis)
+    assert np.array_equal(host(L.dequantize(q)), O.dequantize(qo, so, ax))
+
+
+@pytest.mark.parametrize("fmt", [L.E4M3, L.E5M2])
+@pytest.mark.parametrize("axis", [L.ROW, L.COLUMN, L.TENSOR])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_fp8_quantize_bit_exact(fmt, axis, dtype):
+    x = adversarial(41, 97, seed=fmt * 3 + axis)
+    x[4] = 0
+    if dtype == torch.bfloat16:
+        x = bf16(x)
+    q = L.quantize_fp8(dev(x, dtype), fmt, axis)
+    ofmt = O.E4M3 if fmt == L.E4M3 else O.E5M2
+    oax = {L.ROW: O.ROW, L.COLUMN: O.COL, L.TENSOR: O.TENSOR}[axis]
+    po, so = O.quantize_fp8(x, ofmt, oax)
+    assert np.array_equal(fp8_decode(host(q.payload), fmt), po)
+    assert np.array_equal(host(q.state), so)
+    y = L.dequantize(q)
+    want = (po.astype(np.float64) * (so[:, None] if oax == O.ROW else so[None, :] if oax == O.COL else so[0])).astype(np.float32)
+    assert np.array_equal(host(y), want)
+
+
+def test_golden_fixture_quantize(golden):
+    d = golden("quantize.npz")
+    for key, prefix in (("x_adv", ""), ("x_g", "g_")):
+        x = d[key]
+        assert np.array_equal(host(L.quantize_rowwise(dev(x)).payload), d[prefix + "q_row"])
+        assert np.array_equal(host(L.quantize_columnwise(dev(x)).payload), d[prefix + "q_col"])
+        assert np.array_equal(host(L.quantize_tensorwise(dev(x)).payload), d[prefix + "q_tensor"])
+        assert np.array_equal(host(L.quantize_tensorwise_transpose(dev(x)).payload), d[prefix + "q_tensor_t"])
+        p = L.quantize_fp8(dev(x), L.E4M3, L.ROW)
+        assert np.array_equal(fp8_decode(host(p.payload), 0), d[prefix + "fp8_e4m3_row"])
