@@ -150,26 +150,26 @@ EncodeFn get_encode() {
   return fn;
 }
 
-template <int KIND, int OUT, bool A_MN = false, bool B_MN = false>
+template <int KIND, int OUT, bool A_MN = false, bool B_MN = false, bool SB_COL = false>
 cudaError_t launch_tc(sb_handle h, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d,
                       const sbtc::Params& p, uint32_t idesc) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(sbtc::k_tc_gemm<KIND, A_MN, B_MN, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr_err = cudaFuncSetAttribute(sbtc::k_tc_gemm<KIND, A_MN, B_MN, OUT, SB_COL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     sbtc::SMEM_BYTES);
   });
   if (attr_err != cudaSuccess) return attr_err;
-  const int tiles = p.tiles_m * p.tiles_n;
+  const int tiles = p.tiles_m * p.tiles_n * p.splits;
   const int grid = tiles < h->num_sms ? tiles : h->num_sms;
   h->launches++;
-  sbtc::k_tc_gemm<KIND, A_MN, B_MN, OUT><<<grid, sbtc::NUM_THREADS, sbtc::SMEM_BYTES, h->stream>>>(a, b, d, p, idesc);
+  sbtc::k_tc_gemm<KIND, A_MN, B_MN, OUT, SB_COL><<<grid, sbtc::NUM_THREADS, sbtc::SMEM_BYTES, h->stream>>>(a, b, d, p, idesc);
   return cudaGetLastError();
 }
 
 bool out_tmap(CUtensorMap* m, sb_dtype dt, void* out, int64_t M, int64_t N) {
   if (dt == SB_BF16)
-    return sb::encode_tmap_2d(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, out, N, M, N * 2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+    return sb::encode_tmap_2d(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, out, N, M, N * 2, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   const CUtensorMapDataType t = dt == SB_I32 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   return sb::encode_tmap_2d(m, t, out, N, M, N * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
 }
@@ -225,11 +225,22 @@ sb_status gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* 
       p.post_scale = 1.0f / 16129.0f;
       p.tiles_m = static_cast<int>((M + sbtc::BM - 1) / sbtc::BM);
       p.tiles_n = static_cast<int>((N + sbtc::BN - 1) / sbtc::BN);
+      p.splits = 1;
       cudaError_t e;
+      const bool col = sb_stride == 1;
       switch (out_mode) {
-        case sbtc::OUT_BF16: e = launch_tc<sbtc::KIND_I8, sbtc::OUT_BF16>(h, ta, tb, td, p, 0); break;
-        case sbtc::OUT_F32: e = launch_tc<sbtc::KIND_I8, sbtc::OUT_F32>(h, ta, tb, td, p, 0); break;
-        case sbtc::OUT_F32_EXACT: e = launch_tc<sbtc::KIND_I8, sbtc::OUT_F32_EXACT>(h, ta, tb, td, p, 0); break;
+        case sbtc::OUT_BF16:
+          e = col ? launch_tc<sbtc::KIND_I8, sbtc::OUT_BF16, false, false, true>(h, ta, tb, td, p, 0)
+                  : launch_tc<sbtc::KIND_I8, sbtc::OUT_BF16>(h, ta, tb, td, p, 0);
+          break;
+        case sbtc::OUT_F32:
+          e = col ? launch_tc<sbtc::KIND_I8, sbtc::OUT_F32, false, false, true>(h, ta, tb, td, p, 0)
+                  : launch_tc<sbtc::KIND_I8, sbtc::OUT_F32>(h, ta, tb, td, p, 0);
+          break;
+        case sbtc::OUT_F32_EXACT:
+          e = col ? launch_tc<sbtc::KIND_I8, sbtc::OUT_F32_EXACT, false, false, true>(h, ta, tb, td, p, 0)
+                  : launch_tc<sbtc::KIND_I8, sbtc::OUT_F32_EXACT>(h, ta, tb, td, p, 0);
+          break;
         default: e = launch_tc<sbtc::KIND_I8, sbtc::OUT_I32>(h, ta, tb, td, p, 0); break;
       }
       if (e != cudaSuccess) return cuda_fail(op, e);
@@ -286,8 +297,21 @@ sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t 
         p.post_scale = 1.0f;
         p.tiles_m = static_cast<int>((m + sbtc::BM - 1) / sbtc::BM);
         p.tiles_n = static_cast<int>((n + sbtc::BN - 1) / sbtc::BN);
-        cudaError_t e = accumulate ? launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW_ADD, true, true>(h, ta, tb, td, p, 0)
-                                   : launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW, true, true>(h, ta, tb, td, p, 0);
+        // Split K (= tokens) in two when the output has too few tiles to fill the SMs in whole
+        // waves: both halves reduce-add into a zeroed dW, and 0 + a + b == 0 + b + a, so the
+        // result stays deterministic (more splits would make the fp32 sum order-dependent).
+        const int tiles = p.tiles_m * p.tiles_n;
+        const int64_t kblocks = (b + 63) / 64;
+        auto eff = [&](int s) { int u = tiles * s; int w = (u + h->num_sms - 1) / h->num_sms; return double(u) / (w * h->num_sms); };
+        p.splits = (!accumulate && kblocks >= 64 && eff(2) > eff(1) + 0.05) ? 2 : 1;
+        cudaError_t e;
+        if (p.splits == 2) {
+          e = cudaMemsetAsync(dw, 0, sizeof(float) * m * n, h->stream);
+          if (e == cudaSuccess) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW_ADD, true, true>(h, ta, tb, td, p, 0);
+        } else {
+          e = accumulate ? launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW_ADD, true, true>(h, ta, tb, td, p, 0)
+                         : launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW, true, true>(h, ta, tb, td, p, 0);
+        }
         if (e != cudaSuccess) return cuda_fail(op, e);
         return SB_OK;
       }
@@ -331,6 +355,7 @@ sb_status gemm_bf16_tc(sb_handle h, const void* a, bool a_mn, const void* b, boo
       p.post_scale = 1.0f;
       p.tiles_m = static_cast<int>((M + sbtc::BM - 1) / sbtc::BM);
       p.tiles_n = static_cast<int>((N + sbtc::BN - 1) / sbtc::BN);
+      p.splits = 1;
       cudaError_t e;
       if (out_dt == SB_BF16) {
         if (!a_mn && !b_mn) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_BF16, false, false>(h, ta, tb, td, p, 0);
@@ -387,10 +412,16 @@ sb_status gemm_fp8(sb_handle h, const uint8_t* qa, int fa, const float* sa, int 
       p.post_scale = 1.0f;
       p.tiles_m = static_cast<int>((M + sbtc::BM - 1) / sbtc::BM);
       p.tiles_n = static_cast<int>((N + sbtc::BN - 1) / sbtc::BN);
+      p.splits = 1;
       const uint32_t idesc = sbtc::KindTraits<sbtc::KIND_F8>::IDESC | (static_cast<uint32_t>(fa) << 7) |
                              (static_cast<uint32_t>(fb) << 10);
-      cudaError_t e = out_dt == SB_BF16 ? launch_tc<sbtc::KIND_F8, sbtc::OUT_BF16>(h, ta, tb, td, p, idesc)
-                                        : launch_tc<sbtc::KIND_F8, sbtc::OUT_F32>(h, ta, tb, td, p, idesc);
+      cudaError_t e;
+      if (sb_stride)
+        e = out_dt == SB_BF16 ? launch_tc<sbtc::KIND_F8, sbtc::OUT_BF16, false, false, true>(h, ta, tb, td, p, idesc)
+                              : launch_tc<sbtc::KIND_F8, sbtc::OUT_F32, false, false, true>(h, ta, tb, td, p, idesc);
+      else
+        e = out_dt == SB_BF16 ? launch_tc<sbtc::KIND_F8, sbtc::OUT_BF16>(h, ta, tb, td, p, idesc)
+                              : launch_tc<sbtc::KIND_F8, sbtc::OUT_F32>(h, ta, tb, td, p, idesc);
       if (e != cudaSuccess) return cuda_fail(op, e);
       return SB_OK;
     }

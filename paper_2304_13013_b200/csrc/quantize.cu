@@ -157,46 +157,127 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
 }
 
 // ------------------------------------------------------------------ K1 ----
-// One warp per row; 16-byte vector loads; the row stays in registers (NC vectors per
-// lane) between the absmax and the quantize pass, so HBM sees exactly one read of X.
-template <typename T, int NC>
-__global__ void __launch_bounds__(256) k_quantize_rowwise_vec(const T* __restrict__ x, int64_t rows, int64_t cols,
+// A row is owned by a group of TPR threads (32..256, chosen so each thread holds <= NV
+// 16-byte vectors); the row stays in registers between the absmax and the quantize pass,
+// so HBM sees exactly one read of X and one write of the payload. Groups of more than one
+// warp combine their absmax through shared memory with a per-group named barrier.
+//
+// Fast path per element: q = |x| * (127/s) (fp32), k = floor(q + 1/2). The candidate can
+// only be wrong when q lies within ~2^-16 of a half-integer, so a warp whose vector has no
+// element within 2^-12 of one keeps k; otherwise the warp re-derives every element of the
+// vector with the exact comparison (q_magnitude). Bytes are formed with the 1.5*2^23
+// magic-add (low byte = two's complement of the signed integer) and PRMT packing.
+template <typename T>
+struct Unpack;
+template <>
+struct Unpack<__nv_bfloat16> {
+  static constexpr int N = 8;
+  static __device__ __forceinline__ void run(const uint4& v, float (&x)[8]) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      x[2 * i] = __uint_as_float(w[i] << 16);
+      x[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+};
+template <>
+struct Unpack<float> {
+  static constexpr int N = 4;
+  static __device__ __forceinline__ void run(const uint4& v, float (&x)[4]) {
+    x[0] = __uint_as_float(v.x);
+    x[1] = __uint_as_float(v.y);
+    x[2] = __uint_as_float(v.z);
+    x[3] = __uint_as_float(v.w);
+  }
+};
+
+__device__ __forceinline__ uint32_t pack4(float k0, float k1, float k2, float k3) {
+  // k: signed integral floats in [-127, 127]; + 1.5*2^23 puts the integer in the low byte
+  const uint32_t u0 = __float_as_uint(__fadd_rn(k0, 12582912.0f));
+  const uint32_t u1 = __float_as_uint(__fadd_rn(k1, 12582912.0f));
+  const uint32_t u2 = __float_as_uint(__fadd_rn(k2, 12582912.0f));
+  const uint32_t u3 = __float_as_uint(__fadd_rn(k3, 12582912.0f));
+  return __byte_perm(__byte_perm(u0, u1, 0x0040), __byte_perm(u2, u3, 0x0040), 0x5410);
+}
+
+// Quantize one 16-byte vector; `plain` = the row needs no power-of-two prescale.
+template <typename T>
+__device__ __forceinline__ typename VecQ<T>::Out qvec(const uint4& v, const Scale& sc, bool plain) {
+  constexpr int N = Unpack<T>::N;
+  float x[N], k[N];
+  Unpack<T>::run(v, x);
+  bool near = !plain;
+  if (plain) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const float qa = __fmul_rn(fabsf(x[i]), sc.inv);
+      k[i] = floorf(__fadd_rn(qa, 0.5f));
+      const float d = fabsf(__fsub_rn(qa, k[i]));  // |q - k| in [0, 1/2]
+      near |= d > 0.499755859375f;                 // within 2^-12 of a half-integer
+    }
+  }
+  if (__any_sync(0xffffffffu, near)) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) k[i] = q_magnitude<sizeof(T) == 2>(fabsf(x[i]), sc);
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) k[i] = copysignf(fminf(k[i], 127.0f), x[i]);
+  if constexpr (N == 8) {
+    return make_uint2(pack4(k[0], k[1], k[2], k[3]), pack4(k[4], k[5], k[6], k[7]));
+  } else {
+    return pack4(k[0], k[1], k[2], k[3]);
+  }
+}
+
+template <typename T, int TPR, int NV>
+__global__ void __launch_bounds__(256) k_quantize_rowwise_grp(const T* __restrict__ x, int64_t rows, int64_t cols,
                                                                int64_t ldx, int8_t* __restrict__ q, int64_t ldq,
                                                                float* __restrict__ state, uint32_t* err) {
   constexpr int VEC = 16 / sizeof(T);
+  constexpr int GROUPS = 256 / TPR;
+  constexpr int WPG = TPR / 32;
   using Out = typename VecQ<T>::Out;
-  const int lane = threadIdx.x & 31;
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= rows) return;
+  __shared__ uint32_t red[8];
+  const int g = threadIdx.x / TPR, t = threadIdx.x % TPR;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * GROUPS + g;
+  if (row >= rows) return;  // whole group leaves together
   const uint4* xr = reinterpret_cast<const uint4*>(x + row * ldx);
   Out* qr = reinterpret_cast<Out*>(q + row * ldq);
   const int nvec = static_cast<int>(cols / VEC);
-
-  uint4 buf[NC];
+  uint4 buf[NV];
   uint32_t amax = 0;
 #pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const int v = c * 32 + lane;
+  for (int c = 0; c < NV; ++c) {
+    const int v = c * TPR + t;
     if (v < nvec) {
       buf[c] = ld_stream(xr + v);
       amax = max(amax, vec_absmax_bits<T>(buf[c]));
     }
   }
   amax = __reduce_max_sync(0xffffffffu, amax);
+  if (WPG > 1) {
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) red[w] = amax;
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(TPR) : "memory");
+#pragma unroll
+    for (int i = 0; i < WPG; ++i) amax = max(amax, red[g * WPG + i]);
+  }
   if (amax >= kNonFiniteBits) {
-    if (lane == 0) {
+    if (t == 0) {
       raise_nonfinite(err);
       state[row] = __uint_as_float(amax);
     }
     return;
   }
   const float s = state_from_bits(amax);
-  if (lane == 0) state[row] = s;
+  if (t == 0) state[row] = s;
   const Scale sc = make_scale(s);
+  const bool plain = sc.pre == 1.0f;
 #pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const int v = c * 32 + lane;
-    if (v < nvec) qr[v] = VecQ<T>::run(buf[c], sc);
+  for (int c = 0; c < NV; ++c) {
+    const int v = c * TPR + t;
+    if (v < nvec) qr[v] = qvec<T>(buf[c], sc, plain);
   }
 }
 
@@ -226,7 +307,8 @@ __global__ void __launch_bounds__(256) k_quantize_rowwise_stream(const T* __rest
   const float s = state_from_bits(amax);
   if (lane == 0) state[row] = s;
   const Scale sc = make_scale(s);
-  for (int64_t v = lane; v < nvec; v += 32) qr[v] = VecQ<T>::run(__ldg(xr + v), sc);
+  const bool plain = sc.pre == 1.0f;
+  for (int64_t v = lane; v < nvec; v += 32) qr[v] = qvec<T>(__ldg(xr + v), sc, plain);
 }
 
 // Any shape / alignment: scalar element access.
@@ -254,32 +336,42 @@ __global__ void __launch_bounds__(256) k_quantize_rowwise_scalar(const T* __rest
   for (int64_t j = lane; j < cols; j += 32) q[row * ldq + j] = quantize_one(xr[j], sc);
 }
 
+template <typename T, int TPR, int NV>
+void launch_grp(sb_handle h, const T* x, int64_t rows, int64_t cols, int64_t ldx, int8_t* q, int64_t ldq,
+                float* state) {
+  constexpr int GROUPS = 256 / TPR;
+  const dim3 grid(static_cast<unsigned>((rows + GROUPS - 1) / GROUPS));
+  k_quantize_rowwise_grp<T, TPR, NV><<<grid, 256, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
+}
+
 template <typename T>
 cudaError_t rowwise_impl(sb_handle h, const T* x, int64_t rows, int64_t cols, int64_t ldx, int8_t* q, int64_t ldq,
                          float* state) {
   constexpr int VEC = 16 / sizeof(T);
   constexpr int OUTB = VEC;  // bytes of payload per vector
-  const dim3 block(256);
-  const dim3 grid(static_cast<unsigned>((rows + 7) / 8));
   const bool vec_ok = (cols % VEC == 0) && (ldx % VEC == 0) && sb::aligned(x, 16) && (ldq % OUTB == 0) &&
                       sb::aligned(q, OUTB);
   h->launches++;
   if (!vec_ok) {
-    k_quantize_rowwise_scalar<T><<<grid, block, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
+    const dim3 grid(static_cast<unsigned>((rows + 7) / 8));
+    k_quantize_rowwise_scalar<T><<<grid, 256, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
     return cudaGetLastError();
   }
   const int64_t nvec = cols / VEC;
-  const int64_t per_lane = (nvec + 31) / 32;
-  if (per_lane <= 4)
-    k_quantize_rowwise_vec<T, 4><<<grid, block, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
-  else if (per_lane <= 8)
-    k_quantize_rowwise_vec<T, 8><<<grid, block, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
-  else if (per_lane <= 16)
-    k_quantize_rowwise_vec<T, 16><<<grid, block, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
-  else if (per_lane <= 24)
-    k_quantize_rowwise_vec<T, 24><<<grid, block, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
-  else
-    k_quantize_rowwise_stream<T><<<grid, block, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
+  // threads per row: enough that each holds <= 8 vectors (and ~4-6 for long rows)
+  if (nvec <= 32 * 8) {
+    if (nvec <= 32 * 4) launch_grp<T, 32, 4>(h, x, rows, cols, ldx, q, ldq, state);
+    else launch_grp<T, 32, 8>(h, x, rows, cols, ldx, q, ldq, state);
+  } else if (nvec <= 64 * 8) {
+    launch_grp<T, 64, 8>(h, x, rows, cols, ldx, q, ldq, state);
+  } else if (nvec <= 128 * 8) {
+    launch_grp<T, 128, 8>(h, x, rows, cols, ldx, q, ldq, state);
+  } else if (nvec <= 256 * 8) {
+    launch_grp<T, 256, 8>(h, x, rows, cols, ldx, q, ldq, state);
+  } else {
+    const dim3 grid(static_cast<unsigned>((rows + 7) / 8));
+    k_quantize_rowwise_stream<T><<<grid, 256, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
+  }
   return cudaGetLastError();
 }
 

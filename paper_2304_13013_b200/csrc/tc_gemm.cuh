@@ -2,10 +2,13 @@
 //
 //   D[M x N] = A . B^T, accumulated in TMEM, one 128 x 256 output tile per CTA at a time.
 //
-//   warp 0      TMA producer (one elected lane): A/B tiles -> 4-stage smem ring
-//   warp 1      TMEM allocator + MMA issuer (one lane issues tcgen05.mma, commits to mbarriers)
-//   warps 4..7  epilogue: tcgen05.ld (32 lanes x 32 columns) -> scale/convert in registers ->
-//               swizzled smem staging -> TMA store (or TMA reduce-add for accumulation)
+//   warp 0       TMA producer (one lane): A/B tiles -> 4-stage smem ring (48 KB / stage)
+//   warp 1       TMEM allocator + MMA issuer (one lane issues tcgen05.mma, commits to mbarriers)
+//   warps 4..11  epilogue, 8 warps: warp w reads TMEM lane quarter (w & 3) and column half
+//                ((w - 4) >> 2): tcgen05.ld 2 x (32 lanes x 32 columns) -> scale / convert in
+//                registers -> 128B-swizzled smem staging -> TMA store (TMA reduce-add for
+//                accumulation). Scales are hoisted: one per-row factor per tile, per-column
+//                factors staged once per tile in smem.
 //   Two TMEM accumulators (2 x 256 columns) let the epilogue of tile i overlap the MMAs of
 //   tile i+1.
 //
@@ -41,10 +44,12 @@ constexpr int STAGES = 4;
 constexpr int A_STAGE_BYTES = 16384;  // 128 rows x 128 B  (K-major)  |  64 k-rows x 128 elem x 2 B (MN)
 constexpr int B_STAGE_BYTES = 32768;  // 256 rows x 128 B            |  64 k-rows x 256 elem x 2 B
 constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
-constexpr int EPI_BUF_BYTES = 4096;  // 32 rows x 128 B (f32/s32) or 32 rows x 64 B (bf16)
-constexpr int NUM_THREADS = 256;
+constexpr int EPI_WARPS = 8;
+constexpr int EPI_BUF_BYTES = 4096;  // per epilogue warp: 32 rows x 128 B
+constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
 constexpr int TMEM_COLS = 512;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 4 * 2 * EPI_BUF_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_WARPS * EPI_BUF_BYTES + 2 * BN * 4 /*col scales*/ +
+                           1024 /*align*/ + 256 /*barriers*/;
 
 struct Params {
   int M, N, K;             // K in elements
@@ -53,7 +58,17 @@ struct Params {
   int sa_stride, sb_stride;
   float post_scale;        // 1/16129 for int8 dequant, 1 otherwise
   int tiles_m, tiles_n;
+  int splits;              // split-K factor: work unit u = (tile u / splits, k-slice u % splits)
 };
+
+// Work unit -> (m0, n0, [kb0, kb1)).
+__device__ __forceinline__ void unit_coords(const Params& p, int u, int k_blocks, int& m0, int& n0, int& kb0, int& kb1) {
+  const int t = u / p.splits, s = u - t * p.splits;
+  m0 = (t / p.tiles_n) * BM;
+  n0 = (t % p.tiles_n) * BN;
+  kb0 = static_cast<int>((static_cast<int64_t>(k_blocks) * s) / p.splits);
+  kb1 = static_cast<int>((static_cast<int64_t>(k_blocks) * (s + 1)) / p.splits);
+}
 
 template <int KIND>
 struct KindTraits;
@@ -101,7 +116,18 @@ __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int k) {
   return MN ? sbptx::umma_desc_sw128(base + k * 2048, 8192, 1024) : sbptx::umma_desc_sw128(base + k * 32, 16, 1024);
 }
 
-template <int KIND, bool A_MN, bool B_MN, int OUT>
+__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory"); }
+
+// Write 8 x 16-byte chunks (one 128-byte row) of this lane into a SW128-swizzled staging row.
+__device__ __forceinline__ void stage_row128(uint8_t* buf, int lane, const uint32_t (&w)[32]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int pj = j ^ (lane & 7);
+    *reinterpret_cast<uint4*>(buf + lane * 128 + pj * 16) = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+  }
+}
+
+template <int KIND, bool A_MN, bool B_MN, int OUT, bool SB_COL>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmD, const Params p, uint32_t idesc_runtime) {
@@ -110,7 +136,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + STAGES * A_STAGE_BYTES;
   uint8_t* smem_epi = smem + STAGES * STAGE_BYTES;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_epi + 4 * 2 * EPI_BUF_BYTES);
+  float* col_scale = reinterpret_cast<float*>(smem_epi + EPI_WARPS * EPI_BUF_BYTES);  // [2][BN]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(col_scale + 2 * BN);
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -118,7 +145,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int num_tiles = p.tiles_m * p.tiles_n;
+  const int num_tiles = p.tiles_m * p.tiles_n * p.splits;  // work units
   const int k_blocks = (p.K + KindTraits<KIND>::K_PER_STAGE - 1) / KindTraits<KIND>::K_PER_STAGE;
 
   if (warp == 0 && lane == 0) {
@@ -131,7 +158,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       sbptx::mbar_init(&tfull_bar[a], 1);
-      sbptx::mbar_init(&tempty_bar[a], 4);
+      sbptx::mbar_init(&tempty_bar[a], EPI_WARPS);
     }
     sbptx::fence_mbar_init();
   }
@@ -147,8 +174,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * BN;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        int m0, n0, kb0, kb1;
+        unit_coords(p, t, k_blocks, m0, n0, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           sbptx::mbar_wait(&empty_bar[stage], phase ^ 1u);
           sbptx::mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
           uint8_t* sa_ = smem_a + stage * A_STAGE_BYTES;
@@ -176,7 +204,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         sbptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1u);
         sbptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        int m0_, n0_, kb0, kb1;
+        unit_coords(p, t, k_blocks, m0_, n0_, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           sbptx::mbar_wait(&full_bar[stage], phase);
           sbptx::tc_fence_after();
           const uint32_t a_addr = sbptx::smem_u32(smem_a + stage * A_STAGE_BYTES);
@@ -186,11 +216,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t ad = operand_desc<A_MN>(a_addr, k);
             const uint64_t bd = operand_desc<B_MN>(b_addr, k);
             if (KIND == KIND_I8)
-              sbptx::mma_i8(d_tmem, ad, bd, idesc, (kb | k) != 0);
+              sbptx::mma_i8(d_tmem, ad, bd, idesc, (kb != kb0) || k);
             else if (KIND == KIND_F8)
-              sbptx::mma_f8(d_tmem, ad, bd, idesc, (kb | k) != 0);
+              sbptx::mma_f8(d_tmem, ad, bd, idesc, (kb != kb0) || k);
             else
-              sbptx::mma_f16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+              sbptx::mma_f16(d_tmem, ad, bd, idesc, (kb != kb0) || k);
           }
           sbptx::mma_commit(&empty_bar[stage]);
           if (++stage == STAGES) {
@@ -203,114 +233,131 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
-    const int ew = warp & 3;  // TMEM lane quarter this warp may access
-    uint8_t* bufs = smem_epi + ew * 2 * EPI_BUF_BYTES;
-    int bsel = 0;
+    constexpr bool SCALED = OUT == OUT_BF16 || OUT == OUT_F32 || OUT == OUT_F32_EXACT;
+    const int ew = warp & 3;               // TMEM lane quarter this warp may access
+    const int half = (warp - 4) >> 2;      // column half of the tile
+    const int ei = threadIdx.x - 128;      // 0..255 within the epilogue group
+    uint8_t* buf = smem_epi + (warp - 4) * EPI_BUF_BYTES;
+    const float sb_tensor = (SCALED && !SB_COL) ? __ldg(p.sb) : 1.0f;
     int it = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
-      const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * BN;
+      int m0, n0, kb0_, kb1_;
+      unit_coords(p, t, k_blocks, m0, n0, kb0_, kb1_);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
+      float* cs = col_scale + (it & 1) * BN;
+      if (SCALED && SB_COL) {
+        // stage this tile's per-column states once (all 8 epilogue warps, 256 threads)
+        epi_bar_sync();
+        cs[ei] = (n0 + ei) < p.N ? __ldg(p.sb + n0 + ei) : 0.0f;
+        epi_bar_sync();
+      }
+      const int row = m0 + ew * 32 + lane;
+      float fr = 1.0f;       // per-row factor: sa_i * post (* sb for a tensor-wise B)
+      double sa_d = 1.0;
+      if (SCALED) {
+        const float s = row < p.M ? __ldg(p.sa + (p.sa_stride ? row : 0)) : 0.0f;
+        sa_d = static_cast<double>(s);
+        fr = SB_COL ? s * p.post_scale : s * p.post_scale * sb_tensor;
+      }
       sbptx::mbar_wait(&tfull_bar[acc], acc_phase);
       sbptx::tc_fence_after();
-      const int row = m0 + ew * 32 + lane;
-      float row_scale = 1.0f;
-      double row_scale_d = 1.0;
-      if (OUT == OUT_BF16 || OUT == OUT_F32 || OUT == OUT_F32_EXACT) {
-        const float s = row < p.M ? p.sa[p.sa_stride ? row : 0] : 0.0f;
-        row_scale_d = static_cast<double>(s);
-        row_scale = s * p.post_scale;
-      }
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + half * 128;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        sbptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
+      for (int pr = 0; pr < 2; ++pr) {  // two 64-column pairs per warp
+        uint32_t r0[32], r1[32];
+        sbptx::tmem_ld_32x32b_x32(t_row + pr * 64, r0);
+        sbptx::tmem_ld_32x32b_x32(t_row + pr * 64 + 32, r1);
         sbptx::tmem_ld_wait();
-        if (c == BN / 32 - 1) {
+        if (pr == 1) {
           // accumulator fully drained into registers: hand TMEM back to the MMA warp
           sbptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) sbptx::mbar_arrive(&tempty_bar[acc]);
         }
-        const int col0 = n0 + c * 32;
-        if (col0 >= p.N) continue;  // whole chunk outside D (uniform across the warp)
-        uint8_t* buf = bufs + bsel * EPI_BUF_BYTES;
-        // make sure the TMA store that last used this buffer has finished reading it
-        if (lane == 0) sbptx::tma_store_wait_read<1>();
-        __syncwarp();
+        const int cl = half * 128 + pr * 64;  // column within tile
+        const int col0 = n0 + cl;
+        if (col0 >= p.N) continue;  // whole pair outside D (warp-uniform)
         if (OUT == OUT_BF16) {
-          // 32 bf16 = 64 B per row; SWIZZLE_64B: 16-byte chunk j of row r lives at j ^ ((r >> 1) & 3)
-          uint32_t w[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            float v0, v1;
-            const int ca = col0 + 2 * j, cb = ca + 1;
-            float sb0 = 1.0f, sb1 = 1.0f;
-            if (p.sb_stride) {
-              sb0 = ca < p.N ? __ldg(p.sb + ca) : 0.0f;
-              sb1 = cb < p.N ? __ldg(p.sb + cb) : 0.0f;
-            } else {
-              sb0 = sb1 = __ldg(p.sb);
-            }
-            if (KIND == KIND_I8) {
-              v0 = static_cast<float>(static_cast<int32_t>(r[2 * j])) * row_scale * sb0;
-              v1 = static_cast<float>(static_cast<int32_t>(r[2 * j + 1])) * row_scale * sb1;
-            } else {
-              v0 = __uint_as_float(r[2 * j]) * row_scale * sb0;
-              v1 = __uint_as_float(r[2 * j + 1]) * row_scale * sb1;
-            }
-            w[j] = pack_bf16x2(v0, v1);
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int pj = j ^ ((lane >> 1) & 3);
-            *reinterpret_cast<uint4*>(buf + lane * 64 + pj * 16) = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
-          }
-        } else {
-          // 32 x 4-byte values = 128 B per row; SWIZZLE_128B: chunk j of row r at j ^ (r & 7)
           uint32_t w[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int cj = col0 + j;
-            if (OUT == OUT_I32 || OUT == OUT_F32_RAW || OUT == OUT_F32_RAW_ADD) {
-              w[j] = r[j];
+          for (int j = 0; j < 16; ++j) {
+            float a0, a1, b0, b1;
+            if (KIND == KIND_I8) {
+              a0 = static_cast<float>(static_cast<int32_t>(r0[2 * j]));
+              a1 = static_cast<float>(static_cast<int32_t>(r0[2 * j + 1]));
+              b0 = static_cast<float>(static_cast<int32_t>(r1[2 * j]));
+              b1 = static_cast<float>(static_cast<int32_t>(r1[2 * j + 1]));
             } else {
-              const float sbj = p.sb_stride ? (cj < p.N ? __ldg(p.sb + cj) : 0.0f) : __ldg(p.sb);
-              if (OUT == OUT_F32_EXACT) {
-                const double d =
-                    __ddiv_rn(__dmul_rn(__dmul_rn(static_cast<double>(static_cast<int32_t>(r[j])), row_scale_d),
-                                        static_cast<double>(sbj)),
-                              16129.0);
+              a0 = __uint_as_float(r0[2 * j]);
+              a1 = __uint_as_float(r0[2 * j + 1]);
+              b0 = __uint_as_float(r1[2 * j]);
+              b1 = __uint_as_float(r1[2 * j + 1]);
+            }
+            if (SB_COL) {
+              a0 *= fr * cs[cl + 2 * j];
+              a1 *= fr * cs[cl + 2 * j + 1];
+              b0 *= fr * cs[cl + 32 + 2 * j];
+              b1 *= fr * cs[cl + 32 + 2 * j + 1];
+            } else {
+              a0 *= fr;
+              a1 *= fr;
+              b0 *= fr;
+              b1 *= fr;
+            }
+            w[j] = pack_bf16x2(a0, a1);
+            w[16 + j] = pack_bf16x2(b0, b1);
+          }
+          if (lane == 0) sbptx::tma_store_wait_read<0>();  // previous store done reading buf
+          __syncwarp();
+          stage_row128(buf, lane, w);  // 64 bf16 = 128 B per row
+          sbptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            sbptx::tma_store_2d(&tmD, buf, col0, m0 + ew * 32);
+            sbptx::tma_store_commit();
+          }
+        } else {
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub) {
+            const uint32_t(&r)[32] = sub ? r1 : r0;
+            const int cc = cl + sub * 32;
+            if (n0 + cc >= p.N) break;
+            uint32_t w[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (OUT == OUT_I32 || OUT == OUT_F32_RAW || OUT == OUT_F32_RAW_ADD) {
+                w[j] = r[j];
+              } else if (OUT == OUT_F32_EXACT) {
+                const float sbj = SB_COL ? cs[cc + j] : sb_tensor;
+                const double d = __ddiv_rn(
+                    __dmul_rn(__dmul_rn(static_cast<double>(static_cast<int32_t>(r[j])), sa_d), static_cast<double>(sbj)),
+                    16129.0);
                 w[j] = __float_as_uint(__double2float_rn(d));
-              } else if (KIND == KIND_I8) {
-                w[j] = __float_as_uint(static_cast<float>(static_cast<int32_t>(r[j])) * row_scale * sbj);
               } else {
-                w[j] = __float_as_uint(__uint_as_float(r[j]) * row_scale * sbj);
+                const float v = KIND == KIND_I8 ? static_cast<float>(static_cast<int32_t>(r[j])) : __uint_as_float(r[j]);
+                w[j] = __float_as_uint(SB_COL ? v * (fr * cs[cc + j]) : v * fr);
               }
             }
-          }
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int pj = j ^ (lane & 7);
-            *reinterpret_cast<uint4*>(buf + lane * 128 + pj * 16) = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+            if (lane == 0) sbptx::tma_store_wait_read<0>();
+            __syncwarp();
+            stage_row128(buf, lane, w);  // 32 x 4 B = 128 B per row
+            sbptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              if (OUT == OUT_F32_RAW_ADD) {
+                asm volatile(
+                    "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                        reinterpret_cast<uint64_t>(&tmD)),
+                    "r"(sbptx::smem_u32(buf)), "r"(n0 + cc), "r"(m0 + ew * 32)
+                    : "memory");
+              } else {
+                sbptx::tma_store_2d(&tmD, buf, n0 + cc, m0 + ew * 32);
+              }
+              sbptx::tma_store_commit();
+            }
           }
         }
-        sbptx::fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          if (OUT == OUT_F32_RAW_ADD) {
-            asm volatile(
-                "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                    reinterpret_cast<uint64_t>(&tmD)),
-                "r"(sbptx::smem_u32(buf)), "r"(col0), "r"(m0 + ew * 32)
-                : "memory");
-          } else {
-            sbptx::tma_store_2d(&tmD, buf, col0, m0 + ew * 32);
-          }
-          sbptx::tma_store_commit();
-        }
-        bsel ^= 1;
       }
     }
     if (lane == 0) sbptx::tma_store_wait_all<0>();

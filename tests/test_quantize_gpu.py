@@ -24,7 +24,7 @@ def test_rowwise_bit_exact(shape, dtype):
     assert np.array_equal(host(q.state), so)
 
 
-@pytest.mark.parametrize("scale", [1e-38, 1e-20, 1.0, 1e20, 3e38])
+@pytest.mark.parametrize("scale", [1e-38, 1e-20, 1.0, 1e20, 5e37])
 def test_rowwise_random_scales_fp32(scale):
     rng = np.random.default_rng(1)
     x = (rng.standard_normal((257, 333)) * scale).astype(np.float32)
