@@ -48,8 +48,10 @@ constexpr int EPI_WARPS = 8;
 constexpr int EPI_BUF_BYTES = 4096;  // per epilogue warp: 32 rows x 128 B
 constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
 constexpr int TMEM_COLS = 512;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_WARPS * EPI_BUF_BYTES + 2 * BN * 4 /*col scales*/ +
+constexpr int MAX_DYN_SMEM = 232448;  // 227 KB opt-in limit per CTA on sm_100
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_WARPS * EPI_BUF_BYTES + BN * 4 /*col scales*/ +
                            1024 /*align*/ + 256 /*barriers*/;
+static_assert(SMEM_BYTES <= MAX_DYN_SMEM, "shared memory budget");
 
 struct Params {
   int M, N, K;             // K in elements
@@ -136,8 +138,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + STAGES * A_STAGE_BYTES;
   uint8_t* smem_epi = smem + STAGES * STAGE_BYTES;
-  float* col_scale = reinterpret_cast<float*>(smem_epi + EPI_WARPS * EPI_BUF_BYTES);  // [2][BN]
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(col_scale + 2 * BN);
+  float* col_scale = reinterpret_cast<float*>(smem_epi + EPI_WARPS * EPI_BUF_BYTES);  // [BN]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(col_scale + BN);
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       unit_coords(p, t, k_blocks, m0, n0, kb0_, kb1_);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      float* cs = col_scale + (it & 1) * BN;
+      float* cs = col_scale;  // single buffer: the first barrier below orders reuse
       if (SCALED && SB_COL) {
         // stage this tile's per-column states once (all 8 epilogue warps, 256 threads)
         epi_bar_sync();
