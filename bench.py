@@ -158,6 +158,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     T = args.tokens
     mode = L.LinearMode(A.SB_SWITCHBACK, A.SB_INT8)
+    cmode = mode.c()
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
 
     def randn(*shape, scale=1.0):
@@ -167,57 +168,101 @@ def run_ours(args):
     for name, n, m in LAYERS:
         lay = {"name": name, "n": n, "m": m,
                "x": randn(T, n), "w": randn(m, n, scale=n ** -0.5), "g": randn(T, m),
-               "dw": torch.empty(m, n, device=dev, dtype=torch.float32), "ctx": L.LinearContext()}
+               "y": torch.empty(T, m, device=dev, dtype=torch.bfloat16),
+               "dx": torch.empty(T, n, device=dev, dtype=torch.bfloat16),
+               "gq": torch.empty(T, m, device=dev, dtype=torch.int8),
+               "gs": torch.empty(T, device=dev, dtype=torch.float32),
+               "dw": torch.empty(m, n, device=dev, dtype=torch.float32), "ctx": A.LinearCtx()}
         lay["ws"] = L._workspace(mode, T, n, m, dev)
         layers.append(lay)
-    ar = dp.GradAllReduce()
-    stream = torch.cuda.current_stream(dev)
     h = A.handle(local)
-    ev_dw = []  # (start, end) events around each dW GEMM inside the timed region
+    P = L._p
 
-    def step(record=False):
-        for lay in layers:
-            lay["y"] = L.linear_forward(mode, lay["x"], lay["w"], lay["ctx"], workspace=lay["ws"], check=False)
-        for lay in reversed(layers):
-            dx = lay.setdefault("dxbuf", torch.empty(T, lay["n"], device=dev, dtype=torch.bfloat16))
-            if record:
-                # same kernels as sb_linear_backward, with events around the dW GEMM (dominant kernel)
-                _backward_split(h, L, A, mode, lay, dx, ev_dw)
-            else:
-                A.check(h.lib.sb_linear_backward(h.h, C.byref(mode.c()), C.byref(lay["ctx"].raw), L._p(lay["g"]),
-                                                 L._p(dx), L._p(lay["dw"]), 0))
-            ar.launch(lay["dw"])
+    # The step's kernels, straight through the C-ABI (the same launches sb_linear_forward /
+    # sb_linear_backward issue; the backward is split so the dW GEMM can be timed alone).
+    def fwd(lay):
+        A.check(h.lib.sb_linear_forward(h.h, C.byref(cmode), P(lay["x"]), P(lay["w"]), A.SB_BF16, T, lay["n"],
+                                        lay["m"], P(lay["y"]), C.byref(lay["ctx"]), P(lay["ws"]), lay["ws"].numel()))
+
+    def bwd_dx(lay):
+        c = lay["ctx"]
+        A.check(h.lib.sb_quantize_rowwise(h.h, P(lay["g"]), A.SB_BF16, T, lay["m"], lay["m"], P(lay["gq"]), lay["m"],
+                                          P(lay["gs"])))
+        A.check(h.lib.sb_gemm_i8(h.h, P(lay["gq"]), P(lay["gs"]), C.c_void_p(c.w_q_t), C.c_void_p(c.w_state),
+                                 A.SB_SCALE_ROW_TENSOR, T, lay["n"], lay["m"], P(lay["dx"]), A.SB_BF16, 0))
+
+    def bwd_dw(lay):
+        A.check(h.lib.sb_wgrad(h.h, P(lay["g"]), P(lay["x"]), A.SB_BF16, T, lay["m"], lay["n"], P(lay["dw"]), 0, 0))
+
+    fc1, fc2 = layers
+    segments = [lambda: (fwd(fc1), fwd(fc2), bwd_dx(fc2)), lambda: bwd_dw(fc2), lambda: bwd_dx(fc1),
+                lambda: bwd_dw(fc1)]
+    stream = torch.cuda.current_stream(dev)
+    ar = dp.GradAllReduce()
+
+    # warmup (eager), counting launches of one step
+    for i in range(max(1, args.warmup)):
+        l0 = h.launches()
+        h.bind_stream(stream.cuda_stream)
+        for seg in segments:
+            seg()
+        launches_per_step = h.launches() - l0
+    torch.cuda.synchronize()
+    graphs = None
+    if not args.no_graph:
+        graphs = []
+        for seg in segments:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                h.bind_stream(torch.cuda.current_stream(dev).cuda_stream)
+                seg()
+            graphs.append(g)
+        h.bind_stream(stream.cuda_stream)
+        for g in graphs:
+            g.replay()
+        torch.cuda.synchronize()
+
+    run = [g.replay for g in graphs] if graphs else segments
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+
+    def step(e):
+        run[0]()
+        e[0].record(stream)
+        run[1]()          # dW fc2
+        e[1].record(stream)
+        ar.launch(fc2["dw"])
+        run[2]()
+        e[2].record(stream)
+        run[3]()          # dW fc1
+        e[3].record(stream)
+        ar.launch(fc1["dw"])
         ar.wait()
 
-    # warmup
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    launches0 = h.launches()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
         start.record(stream)
-        for _ in range(args.steps):
-            step(record=True)
+        for i in range(args.steps):
+            step(ev[i])
         end.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    launches = h.launches() - launches0
     ms = start.elapsed_time(end) / args.steps
     ms = dp.max_over_ranks(ms, dev)
     value = T * world / (ms / 1000.0)
+    launches = launches_per_step * args.steps
 
-    # dominant kernel: the bf16 dW GEMM (2*m*n*T flops per launch)
-    dw_times = [s.elapsed_time(e) for s, e in ev_dw]
+    # dominant kernel: the bf16 dW GEMM (2*m*n*T flops per launch), timed by the events
+    # bracketing its graph segment inside the timed region
+    dw_times = [e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3]) for e in ev]
     pk = peaks()
-    dw_flops = [2.0 * lay["m"] * lay["n"] * T for lay in layers] * args.steps
-    achieved = sum(dw_flops) / (sum(dw_times) / 1000.0) / 1e12
+    flops_step = sum(2.0 * lay["m"] * lay["n"] * T for lay in layers)
+    achieved = flops_step * args.steps / (sum(dw_times) / 1000.0) / 1e12
     peak = pk["bf16_tflops_sustained"]
     traffic = None
     prof = os.path.join(ROOT, "profiles", "dw_gemm_traffic.json")
@@ -225,15 +270,12 @@ def run_ours(args):
         with open(prof) as f:
             traffic = json.load(f).get("bytes_per_launch")
     share = sum(dw_times) / (ms * args.steps)
+    int8_ops_step = sum(4.0 * lay["m"] * lay["n"] * T for lay in layers)
 
-    # e2e through the C-ABI host-buffer entry (pinned host memory, copies inside the timed region)
     e2e = None
     if rank == 0 and not args.no_e2e:
         e2e = e2e_host(args, L, torch)
-
-    # yardstick: bf16 cuBLAS linear (torch.matmul) fwd + dX + dW on the same shapes
     yard = cublas_yardstick(torch, layers, T, args) if rank == 0 else None
-
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         r, cores, sample, kind = cpu_reference_rate(budget_s=args.ref_budget)
@@ -245,39 +287,19 @@ def run_ours(args):
                 "vs_baseline": None, "dtype": "int8 (fwd, dX) + bf16 (dW), fp32 accumulate", "data": "synthetic",
                 "config": {"workload": WORKLOAD, "tokens_per_gpu": T, "global_tokens": T * world,
                            "layers": [f"{n}->{m}" for _, n, m in LAYERS], "parallelism": f"dp{world} (token shards)",
-                           "l2": "inputs larger than L2 (X, G, H operands 168-673 MB each)"},
+                           "l2": "inputs larger than L2 (X, G, H operands 168-673 MB each)",
+                           "cuda_graphs": graphs is not None},
                 "gpu_launches": launches,
                 "roofline": {"bound": "tensor", "kernel": "bf16 dW GEMM (tcgen05 kind::f16, MN-major)",
                              "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                             "peak_source": f"{pk['source']} bf16 sustained", "traffic": traffic,
-                             "share_of_step": share,
-                             "flops_per_launch": [2 * lay["m"] * lay["n"] * T for lay in layers]},
+                             "peak_source": f"{pk['source']} bf16 sustained (MEASURED_PEAKS.json)", "traffic": traffic,
+                             "share_of_step": share, "flops_per_launch": [2 * lay["m"] * lay["n"] * T for lay in layers]},
+                "int8_tops_per_step": int8_ops_step / 1e12,
                 "clocks": clk.summary(),
                 "e2e": e2e, "cpu_baseline": cpu, "yardstick_cublas_bf16": yard}
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
-
-
-def _backward_split(h, L, A, mode, lay, dx, ev_dw):
-    """linear_backward with events around the dW GEMM: identical kernels to
-    sb_linear_backward (quantize G, int8 dX GEMM, bf16 dW GEMM)."""
-    import torch
-
-    c = lay["ctx"].raw
-    T, n, m = c.b, c.n, c.m
-    # quantize G + dX via the C-ABI pieces the layer call uses
-    ws = lay["ws"]
-    gq = lay.setdefault("gq", torch.empty(T, m, device=ws.device, dtype=torch.int8))
-    gs = lay.setdefault("gs", torch.empty(T, device=ws.device, dtype=torch.float32))
-    A.check(h.lib.sb_quantize_rowwise(h.h, L._p(lay["g"]), A.SB_BF16, T, m, m, L._p(gq), m, L._p(gs)))
-    A.check(h.lib.sb_gemm_i8(h.h, L._p(gq), L._p(gs), C.c_void_p(c.w_q_t), C.c_void_p(c.w_state),
-                             A.SB_SCALE_ROW_TENSOR, T, n, m, L._p(dx), A.SB_BF16, 0))
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    A.check(h.lib.sb_wgrad(h.h, L._p(lay["g"]), L._p(lay["x"]), A.SB_BF16, T, m, n, L._p(lay["dw"]), 0, 0))
-    e.record()
-    ev_dw.append((s, e))
 
 
 def e2e_host(args, L, torch):
@@ -341,6 +363,7 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

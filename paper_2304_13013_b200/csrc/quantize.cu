@@ -230,38 +230,35 @@ __device__ __forceinline__ typename VecQ<T>::Out qvec(const uint4& v, const Scal
   }
 }
 
-template <typename T, int TPR, int NV>
-__global__ void __launch_bounds__(256) k_quantize_rowwise_grp(const T* __restrict__ x, int64_t rows, int64_t cols,
-                                                               int64_t ldx, int8_t* __restrict__ q, int64_t ldq,
-                                                               float* __restrict__ state, uint32_t* err) {
-  constexpr int VEC = 16 / sizeof(T);
-  constexpr int GROUPS = 256 / TPR;
-  constexpr int WPG = TPR / 32;
-  using Out = typename VecQ<T>::Out;
-  __shared__ uint32_t red[8];
-  const int g = threadIdx.x / TPR, t = threadIdx.x % TPR;
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * GROUPS + g;
-  if (row >= rows) return;  // whole group leaves together
-  const uint4* xr = reinterpret_cast<const uint4*>(x + row * ldx);
-  Out* qr = reinterpret_cast<Out*>(q + row * ldq);
-  const int nvec = static_cast<int>(cols / VEC);
-  uint4 buf[NV];
-  uint32_t amax = 0;
+template <typename T, int NV>
+__device__ __forceinline__ void load_row(const uint4* xr, int nvec, int t, int tpr, uint4 (&buf)[NV]) {
 #pragma unroll
   for (int c = 0; c < NV; ++c) {
-    const int v = c * TPR + t;
-    if (v < nvec) {
-      buf[c] = ld_stream(xr + v);
-      amax = max(amax, vec_absmax_bits<T>(buf[c]));
-    }
+    const int v = c * tpr + t;
+    if (v < nvec) buf[c] = ld_stream(xr + v);
   }
+}
+
+// Persistent: each TPR-thread group walks rows g, g + G, g + 2G, ... and prefetches the
+// next row into a second register buffer before quantizing the current one, so HBM reads
+// stay in flight while the ALUs work (one read of X, one write of the payload).
+template <typename T, int TPR, int NV>
+__device__ __forceinline__ void quantize_row_regs(const uint4 (&buf)[NV], int64_t row, int nvec, int t, int g,
+                                                  uint32_t (&red)[2][8], int parity, int8_t* __restrict__ q,
+                                                  int64_t ldq, float* __restrict__ state, uint32_t* err) {
+  constexpr int WPG = TPR / 32;
+  using Out = typename VecQ<T>::Out;
+  uint32_t amax = 0;
+#pragma unroll
+  for (int c = 0; c < NV; ++c)
+    if (c * TPR + t < nvec) amax = max(amax, vec_absmax_bits<T>(buf[c]));
   amax = __reduce_max_sync(0xffffffffu, amax);
   if (WPG > 1) {
-    const int w = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0) red[w] = amax;
+    const int w = (threadIdx.x >> 5) & (WPG - 1);
+    if ((threadIdx.x & 31) == 0) red[parity][g * WPG + w] = amax;
     asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(TPR) : "memory");
 #pragma unroll
-    for (int i = 0; i < WPG; ++i) amax = max(amax, red[g * WPG + i]);
+    for (int i = 0; i < WPG; ++i) amax = max(amax, red[parity][g * WPG + i]);
   }
   if (amax >= kNonFiniteBits) {
     if (t == 0) {
@@ -274,10 +271,41 @@ __global__ void __launch_bounds__(256) k_quantize_rowwise_grp(const T* __restric
   if (t == 0) state[row] = s;
   const Scale sc = make_scale(s);
   const bool plain = sc.pre == 1.0f;
+  Out* qr = reinterpret_cast<Out*>(q + row * ldq);
 #pragma unroll
   for (int c = 0; c < NV; ++c) {
     const int v = c * TPR + t;
     if (v < nvec) qr[v] = qvec<T>(buf[c], sc, plain);
+  }
+}
+
+template <typename T, int TPR, int NV>
+__global__ void __launch_bounds__(256) k_quantize_rowwise_grp(const T* __restrict__ x, int64_t rows, int64_t cols,
+                                                               int64_t ldx, int8_t* __restrict__ q, int64_t ldq,
+                                                               float* __restrict__ state, uint32_t* err) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int GROUPS = 256 / TPR;
+  __shared__ uint32_t red[2][8];
+  const int g = threadIdx.x / TPR, t = threadIdx.x % TPR;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * GROUPS;
+  const int nvec = static_cast<int>(cols / VEC);
+  int64_t row = static_cast<int64_t>(blockIdx.x) * GROUPS + g;
+  if (row >= rows) return;  // whole group leaves together
+  uint4 b0[NV], b1[NV];
+  load_row<T, NV>(reinterpret_cast<const uint4*>(x + row * ldx), nvec, t, TPR, b0);
+  int parity = 0;
+  while (true) {
+    const int64_t r1 = row + stride;
+    if (r1 < rows) load_row<T, NV>(reinterpret_cast<const uint4*>(x + r1 * ldx), nvec, t, TPR, b1);
+    quantize_row_regs<T, TPR, NV>(b0, row, nvec, t, g, red, parity, q, ldq, state, err);
+    if (r1 >= rows) break;
+    parity ^= 1;
+    const int64_t r2 = r1 + stride;
+    if (r2 < rows) load_row<T, NV>(reinterpret_cast<const uint4*>(x + r2 * ldx), nvec, t, TPR, b0);
+    quantize_row_regs<T, TPR, NV>(b1, r1, nvec, t, g, red, parity, q, ldq, state, err);
+    if (r2 >= rows) break;
+    parity ^= 1;
+    row = r2;
   }
 }
 
@@ -340,7 +368,15 @@ template <typename T, int TPR, int NV>
 void launch_grp(sb_handle h, const T* x, int64_t rows, int64_t cols, int64_t ldx, int8_t* q, int64_t ldq,
                 float* state) {
   constexpr int GROUPS = 256 / TPR;
-  const dim3 grid(static_cast<unsigned>((rows + GROUPS - 1) / GROUPS));
+  static int per_sm = 0;  // resident blocks per SM for this instantiation (persistent grid)
+  if (per_sm == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantize_rowwise_grp<T, TPR, NV>, 256, 0);
+    if (per_sm < 1) per_sm = 1;
+  }
+  int64_t blocks = (rows + GROUPS - 1) / GROUPS;
+  const int64_t cap = static_cast<int64_t>(h->num_sms) * per_sm;
+  if (blocks > cap) blocks = cap;
+  const dim3 grid(static_cast<unsigned>(blocks));
   k_quantize_rowwise_grp<T, TPR, NV><<<grid, 256, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
 }
 
@@ -358,16 +394,28 @@ cudaError_t rowwise_impl(sb_handle h, const T* x, int64_t rows, int64_t cols, in
     return cudaGetLastError();
   }
   const int64_t nvec = cols / VEC;
-  // threads per row: enough that each holds <= 8 vectors (and ~4-6 for long rows)
-  if (nvec <= 32 * 8) {
-    if (nvec <= 32 * 4) launch_grp<T, 32, 4>(h, x, rows, cols, ldx, q, ldq, state);
-    else launch_grp<T, 32, 8>(h, x, rows, cols, ldx, q, ldq, state);
-  } else if (nvec <= 64 * 8) {
-    launch_grp<T, 64, 8>(h, x, rows, cols, ldx, q, ldq, state);
-  } else if (nvec <= 128 * 8) {
-    launch_grp<T, 128, 8>(h, x, rows, cols, ldx, q, ldq, state);
-  } else if (nvec <= 256 * 8) {
-    launch_grp<T, 256, 8>(h, x, rows, cols, ldx, q, ldq, state);
+  // threads per row: the smallest group that leaves each thread <= 6 vectors; NV rounded
+  // up to {2, 4, 5, 6} so registers match the row length (row 1280 bf16 -> 32 x 5,
+  // 5120 bf16 -> 128 x 5, 1024 bf16 -> 32 x 4)
+  auto pick = [&](int tpr) -> int {
+    const int64_t need = (nvec + tpr - 1) / tpr;
+    return need <= 2 ? 2 : need <= 4 ? 4 : need <= 5 ? 5 : need <= 6 ? 6 : 0;
+  };
+#define SB_QROW(TPR)                                                         \
+  switch (pick(TPR)) {                                                      \
+    case 2: launch_grp<T, TPR, 2>(h, x, rows, cols, ldx, q, ldq, state); break; \
+    case 4: launch_grp<T, TPR, 4>(h, x, rows, cols, ldx, q, ldq, state); break; \
+    case 5: launch_grp<T, TPR, 5>(h, x, rows, cols, ldx, q, ldq, state); break; \
+    default: launch_grp<T, TPR, 6>(h, x, rows, cols, ldx, q, ldq, state); break; \
+  }
+  if (pick(32)) {
+    SB_QROW(32)
+  } else if (pick(64)) {
+    SB_QROW(64)
+  } else if (pick(128)) {
+    SB_QROW(128)
+  } else if (pick(256)) {
+    SB_QROW(256)
   } else {
     const dim3 grid(static_cast<unsigned>((rows + 7) / 8));
     k_quantize_rowwise_stream<T><<<grid, 256, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
