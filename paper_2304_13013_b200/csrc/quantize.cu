@@ -23,7 +23,10 @@
 // maximum, which is how non-finite input is detected (fmaxf would drop NaN).
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include "sb_internal.h"
+#include "sb_ptx.cuh"
 
 namespace {
 
@@ -157,16 +160,19 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
 }
 
 // ------------------------------------------------------------------ K1 ----
-// A row is owned by a group of TPR threads (32..256, chosen so each thread holds <= NV
-// 16-byte vectors); the row stays in registers between the absmax and the quantize pass,
-// so HBM sees exactly one read of X and one write of the payload. Groups of more than one
-// warp combine their absmax through shared memory with a per-group named barrier.
+// TMA-fed row-wise quantizer. One producer lane streams whole rows of X with
+// cp.async.bulk (16-byte aligned rows) into a ring of smem slots (mbarrier full/empty
+// pairs); 8 consumer warps each own every 8th row of the block's share: absmax over the
+// row from smem (integer max of |x| bit patterns), then the quantize pass from smem, int8
+// payload written with coalesced 8-/4-byte stores. HBM sees one read of X and one write of
+// the payload; the ring keeps ~100 KB of reads in flight per block (2 blocks per SM).
 //
-// Fast path per element: q = |x| * (127/s) (fp32), k = floor(q + 1/2). The candidate can
-// only be wrong when q lies within ~2^-16 of a half-integer, so a warp whose vector has no
-// element within 2^-12 of one keeps k; otherwise the warp re-derives every element of the
-// vector with the exact comparison (q_magnitude). Bytes are formed with the 1.5*2^23
-// magic-add (low byte = two's complement of the signed integer) and PRMT packing.
+// Per element (fast path): qs = x * (127/s) (signed, fp32), m = qs + 1.5*2^23 rounds qs to
+// the nearest integer and leaves it (two's complement) in the low byte of m; the residual
+// r = qs - (m - 1.5*2^23) is exact. The candidate can only differ from the reference's
+// round-half-away of the exact 127x/s when |r| is within ~2^-16 of 1/2, so a warp with any
+// |r| > 1/2 - 2^-12 in the vector re-derives the vector with the exact comparison
+// (q_magnitude). Bytes are packed with PRMT.
 template <typename T>
 struct Unpack;
 template <>
@@ -192,12 +198,9 @@ struct Unpack<float> {
   }
 };
 
-__device__ __forceinline__ uint32_t pack4(float k0, float k1, float k2, float k3) {
-  // k: signed integral floats in [-127, 127]; + 1.5*2^23 puts the integer in the low byte
-  const uint32_t u0 = __float_as_uint(__fadd_rn(k0, 12582912.0f));
-  const uint32_t u1 = __float_as_uint(__fadd_rn(k1, 12582912.0f));
-  const uint32_t u2 = __float_as_uint(__fadd_rn(k2, 12582912.0f));
-  const uint32_t u3 = __float_as_uint(__fadd_rn(k3, 12582912.0f));
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+
+__device__ __forceinline__ uint32_t pack4u(uint32_t u0, uint32_t u1, uint32_t u2, uint32_t u3) {
   return __byte_perm(__byte_perm(u0, u1, 0x0040), __byte_perm(u2, u3, 0x0040), 0x5410);
 }
 
@@ -205,111 +208,107 @@ __device__ __forceinline__ uint32_t pack4(float k0, float k1, float k2, float k3
 template <typename T>
 __device__ __forceinline__ typename VecQ<T>::Out qvec(const uint4& v, const Scale& sc, bool plain) {
   constexpr int N = Unpack<T>::N;
-  float x[N], k[N];
+  float x[N];
+  uint32_t u[N];
   Unpack<T>::run(v, x);
-  bool near = !plain;
-  if (plain) {
+  float rmax = 0.0f;
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      const float qa = __fmul_rn(fabsf(x[i]), sc.inv);
-      k[i] = floorf(__fadd_rn(qa, 0.5f));
-      const float d = fabsf(__fsub_rn(qa, k[i]));  // |q - k| in [0, 1/2]
-      near |= d > 0.499755859375f;                 // within 2^-12 of a half-integer
-    }
+  for (int i = 0; i < N; ++i) {
+    const float qs = __fmul_rn(x[i], sc.inv);
+    const float m = __fadd_rn(qs, kMagic);
+    const float r = __fsub_rn(qs, __fsub_rn(m, kMagic));
+    rmax = fmaxf(rmax, fabsf(r));
+    u[i] = __float_as_uint(m);
   }
+  const bool near = !plain || rmax > 0.499755859375f;  // within 2^-12 of a half-integer
   if (__any_sync(0xffffffffu, near)) {
 #pragma unroll
-    for (int i = 0; i < N; ++i) k[i] = q_magnitude<sizeof(T) == 2>(fabsf(x[i]), sc);
+    for (int i = 0; i < N; ++i)
+      u[i] = __float_as_uint(__fadd_rn(copysignf(q_magnitude<sizeof(T) == 2>(fabsf(x[i]), sc), x[i]), kMagic));
   }
-#pragma unroll
-  for (int i = 0; i < N; ++i) k[i] = copysignf(fminf(k[i], 127.0f), x[i]);
   if constexpr (N == 8) {
-    return make_uint2(pack4(k[0], k[1], k[2], k[3]), pack4(k[4], k[5], k[6], k[7]));
+    return make_uint2(pack4u(u[0], u[1], u[2], u[3]), pack4u(u[4], u[5], u[6], u[7]));
   } else {
-    return pack4(k[0], k[1], k[2], k[3]);
+    return pack4u(u[0], u[1], u[2], u[3]);
   }
 }
 
-template <typename T, int NV>
-__device__ __forceinline__ void load_row(const uint4* xr, int nvec, int t, int tpr, uint4 (&buf)[NV]) {
-#pragma unroll
-  for (int c = 0; c < NV; ++c) {
-    const int v = c * tpr + t;
-    if (v < nvec) buf[c] = ld_stream(xr + v);
-  }
+constexpr int kQWarps = 8;                     // consumer warps per block
+constexpr int kQThreads = 32 * (kQWarps + 1);  // + 1 producer warp
+constexpr int kQRingBytes = 100 * 1024;
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   sbptx::smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(sbptx::smem_u32(bar))
+               : "memory");
 }
 
-// Persistent: each TPR-thread group walks rows g, g + G, g + 2G, ... and prefetches the
-// next row into a second register buffer before quantizing the current one, so HBM reads
-// stay in flight while the ALUs work (one read of X, one write of the payload).
-template <typename T, int TPR, int NV>
-__device__ __forceinline__ void quantize_row_regs(const uint4 (&buf)[NV], int64_t row, int nvec, int t, int g,
-                                                  uint32_t (&red)[2][8], int parity, int8_t* __restrict__ q,
-                                                  int64_t ldq, float* __restrict__ state, uint32_t* err) {
-  constexpr int WPG = TPR / 32;
+template <typename T>
+__global__ void __launch_bounds__(kQThreads) k_quantize_rowwise_tma(const T* __restrict__ x, int64_t rows, int64_t cols,
+                                                                   int64_t ldx, int8_t* __restrict__ q, int64_t ldq,
+                                                                   float* __restrict__ state, uint32_t* err,
+                                                                   int stages, int slot_bytes) {
+  constexpr int VEC = 16 / sizeof(T);
   using Out = typename VecQ<T>::Out;
-  uint32_t amax = 0;
-#pragma unroll
-  for (int c = 0; c < NV; ++c)
-    if (c * TPR + t < nvec) amax = max(amax, vec_absmax_bits<T>(buf[c]));
-  amax = __reduce_max_sync(0xffffffffu, amax);
-  if (WPG > 1) {
-    const int w = (threadIdx.x >> 5) & (WPG - 1);
-    if ((threadIdx.x & 31) == 0) red[parity][g * WPG + w] = amax;
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(TPR) : "memory");
-#pragma unroll
-    for (int i = 0; i < WPG; ++i) amax = max(amax, red[parity][g * WPG + i]);
+  extern __shared__ __align__(128) uint8_t qsmem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(qsmem + static_cast<size_t>(stages) * slot_bytes);
+  uint64_t* empty = full + stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t row_bytes = static_cast<uint32_t>(cols * sizeof(T));
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      sbptx::mbar_init(&full[s], 1);
+      sbptx::mbar_init(&empty[s], 1);
+    }
+    sbptx::fence_mbar_init();
   }
-  if (amax >= kNonFiniteBits) {
-    if (t == 0) {
-      raise_nonfinite(err);
-      state[row] = __uint_as_float(amax);
+  __syncthreads();
+  if (warp == kQWarps) {
+    if (lane == 0) {  // producer
+      int i = 0;
+      for (int64_t row = blockIdx.x; row < rows; row += gridDim.x, ++i) {
+        const int s = i % stages;
+        const uint32_t ph = static_cast<uint32_t>(i / stages) & 1u;
+        sbptx::mbar_wait(&empty[s], ph ^ 1u);
+        sbptx::mbar_arrive_expect_tx(&full[s], row_bytes);
+        bulk_load(qsmem + static_cast<size_t>(s) * slot_bytes, x + row * ldx, row_bytes, &full[s]);
+      }
     }
     return;
   }
-  const float s = state_from_bits(amax);
-  if (t == 0) state[row] = s;
-  const Scale sc = make_scale(s);
-  const bool plain = sc.pre == 1.0f;
-  Out* qr = reinterpret_cast<Out*>(q + row * ldq);
-#pragma unroll
-  for (int c = 0; c < NV; ++c) {
-    const int v = c * TPR + t;
-    if (v < nvec) qr[v] = qvec<T>(buf[c], sc, plain);
-  }
-}
-
-template <typename T, int TPR, int NV>
-__global__ void __launch_bounds__(256) k_quantize_rowwise_grp(const T* __restrict__ x, int64_t rows, int64_t cols,
-                                                               int64_t ldx, int8_t* __restrict__ q, int64_t ldq,
-                                                               float* __restrict__ state, uint32_t* err) {
-  constexpr int VEC = 16 / sizeof(T);
-  constexpr int GROUPS = 256 / TPR;
-  __shared__ uint32_t red[2][8];
-  const int g = threadIdx.x / TPR, t = threadIdx.x % TPR;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * GROUPS;
   const int nvec = static_cast<int>(cols / VEC);
-  int64_t row = static_cast<int64_t>(blockIdx.x) * GROUPS + g;
-  if (row >= rows) return;  // whole group leaves together
-  uint4 b0[NV], b1[NV];
-  load_row<T, NV>(reinterpret_cast<const uint4*>(x + row * ldx), nvec, t, TPR, b0);
-  int parity = 0;
-  while (true) {
-    const int64_t r1 = row + stride;
-    if (r1 < rows) load_row<T, NV>(reinterpret_cast<const uint4*>(x + r1 * ldx), nvec, t, TPR, b1);
-    quantize_row_regs<T, TPR, NV>(b0, row, nvec, t, g, red, parity, q, ldq, state, err);
-    if (r1 >= rows) break;
-    parity ^= 1;
-    const int64_t r2 = r1 + stride;
-    if (r2 < rows) load_row<T, NV>(reinterpret_cast<const uint4*>(x + r2 * ldx), nvec, t, TPR, b0);
-    quantize_row_regs<T, TPR, NV>(b1, r1, nvec, t, g, red, parity, q, ldq, state, err);
-    if (r2 >= rows) break;
-    parity ^= 1;
-    row = r2;
+  int i = warp;
+  for (int64_t row = blockIdx.x + static_cast<int64_t>(warp) * gridDim.x; row < rows;
+       row += static_cast<int64_t>(kQWarps) * gridDim.x, i += kQWarps) {
+    const int s = i % stages;
+    const uint32_t ph = static_cast<uint32_t>(i / stages) & 1u;
+    sbptx::mbar_wait(&full[s], ph);
+    const uint4* xs = reinterpret_cast<const uint4*>(qsmem + static_cast<size_t>(s) * slot_bytes);
+    uint32_t amax = 0;
+#pragma unroll 4
+    for (int v = lane; v < nvec; v += 32) amax = max(amax, vec_absmax_bits<T>(xs[v]));
+    amax = __reduce_max_sync(0xffffffffu, amax);
+    if (amax >= kNonFiniteBits) {
+      if (lane == 0) {
+        raise_nonfinite(err);
+        state[row] = __uint_as_float(amax);
+      }
+    } else {
+      const float st = state_from_bits(amax);
+      if (lane == 0) state[row] = st;
+      const Scale sc = make_scale(st);
+      const bool plain = sc.pre == 1.0f;
+      Out* qr = reinterpret_cast<Out*>(q + row * ldq);
+#pragma unroll 4
+      for (int v = lane; v < nvec; v += 32) qr[v] = qvec<T>(xs[v], sc, plain);
+    }
+    __syncwarp();
+    if (lane == 0) sbptx::mbar_arrive(&empty[s]);
   }
 }
 
-// Rows longer than the register budget: same algorithm, second pass re-reads (L2 hit).
+// Rows longer than a ring slot: one warp per row, second pass re-reads (L2 hit).
 template <typename T>
 __global__ void __launch_bounds__(256) k_quantize_rowwise_stream(const T* __restrict__ x, int64_t rows, int64_t cols,
                                                                   int64_t ldx, int8_t* __restrict__ q, int64_t ldq,
@@ -364,22 +363,6 @@ __global__ void __launch_bounds__(256) k_quantize_rowwise_scalar(const T* __rest
   for (int64_t j = lane; j < cols; j += 32) q[row * ldq + j] = quantize_one(xr[j], sc);
 }
 
-template <typename T, int TPR, int NV>
-void launch_grp(sb_handle h, const T* x, int64_t rows, int64_t cols, int64_t ldx, int8_t* q, int64_t ldq,
-                float* state) {
-  constexpr int GROUPS = 256 / TPR;
-  static int per_sm = 0;  // resident blocks per SM for this instantiation (persistent grid)
-  if (per_sm == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantize_rowwise_grp<T, TPR, NV>, 256, 0);
-    if (per_sm < 1) per_sm = 1;
-  }
-  int64_t blocks = (rows + GROUPS - 1) / GROUPS;
-  const int64_t cap = static_cast<int64_t>(h->num_sms) * per_sm;
-  if (blocks > cap) blocks = cap;
-  const dim3 grid(static_cast<unsigned>(blocks));
-  k_quantize_rowwise_grp<T, TPR, NV><<<grid, 256, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
-}
-
 template <typename T>
 cudaError_t rowwise_impl(sb_handle h, const T* x, int64_t rows, int64_t cols, int64_t ldx, int8_t* q, int64_t ldq,
                          float* state) {
@@ -393,29 +376,19 @@ cudaError_t rowwise_impl(sb_handle h, const T* x, int64_t rows, int64_t cols, in
     k_quantize_rowwise_scalar<T><<<grid, 256, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
     return cudaGetLastError();
   }
-  const int64_t nvec = cols / VEC;
-  // threads per row: the smallest group that leaves each thread <= 6 vectors; NV rounded
-  // up to {2, 4, 5, 6} so registers match the row length (row 1280 bf16 -> 32 x 5,
-  // 5120 bf16 -> 128 x 5, 1024 bf16 -> 32 x 4)
-  auto pick = [&](int tpr) -> int {
-    const int64_t need = (nvec + tpr - 1) / tpr;
-    return need <= 2 ? 2 : need <= 4 ? 4 : need <= 5 ? 5 : need <= 6 ? 6 : 0;
-  };
-#define SB_QROW(TPR)                                                         \
-  switch (pick(TPR)) {                                                      \
-    case 2: launch_grp<T, TPR, 2>(h, x, rows, cols, ldx, q, ldq, state); break; \
-    case 4: launch_grp<T, TPR, 4>(h, x, rows, cols, ldx, q, ldq, state); break; \
-    case 5: launch_grp<T, TPR, 5>(h, x, rows, cols, ldx, q, ldq, state); break; \
-    default: launch_grp<T, TPR, 6>(h, x, rows, cols, ldx, q, ldq, state); break; \
-  }
-  if (pick(32)) {
-    SB_QROW(32)
-  } else if (pick(64)) {
-    SB_QROW(64)
-  } else if (pick(128)) {
-    SB_QROW(128)
-  } else if (pick(256)) {
-    SB_QROW(256)
+  const int64_t row_bytes = cols * static_cast<int64_t>(sizeof(T));
+  const int slot = static_cast<int>((row_bytes + 127) / 128 * 128);
+  const int stages = static_cast<int>(std::min<int64_t>(32, kQRingBytes / std::max(slot, 1)));
+  if (stages >= 4) {
+    static bool attr = false;
+    const int smem = stages * slot + 2 * stages * 8;
+    if (!attr) {
+      cudaFuncSetAttribute(k_quantize_rowwise_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kQRingBytes + 1024);
+      attr = true;
+    }
+    int64_t blocks = std::min<int64_t>(rows, static_cast<int64_t>(h->num_sms) * 2);
+    k_quantize_rowwise_tma<T><<<static_cast<unsigned>(blocks), kQThreads, smem, h->stream>>>(
+        x, rows, cols, ldx, q, ldq, state, h->d_err, stages, slot);
   } else {
     const dim3 grid(static_cast<unsigned>((rows + 7) / 8));
     k_quantize_rowwise_stream<T><<<grid, 256, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
