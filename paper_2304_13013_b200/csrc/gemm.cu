@@ -15,6 +15,9 @@
 
 #include "sb_internal.h"
 #include "tc_gemm.cuh"
+#include "tc_gemm2.cuh"
+
+#include <cstdlib>
 
 namespace {
 
@@ -150,20 +153,66 @@ EncodeFn get_encode() {
   return fn;
 }
 
+// A GEMM operand as a 2-D row-major global tensor: `inner` contiguous elements per row,
+// `outer` rows. mn = the operand is MN-major (its contiguous dimension is M or N).
+struct Operand {
+  const void* ptr;
+  CUtensorMapDataType dt;
+  uint64_t inner, outer, stride_bytes;
+  bool mn;
+  uint32_t kbox;  // K-major: elements per 128-byte K slice (128 for 8-bit, 64 for bf16)
+};
+
+bool encode_operand(CUtensorMap* m, const Operand& o, uint32_t rows) {
+  if (o.mn) return sb::encode_tmap_2d(m, o.dt, o.ptr, o.inner, o.outer, o.stride_bytes, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B);
+  return sb::encode_tmap_2d(m, o.dt, o.ptr, o.inner, o.outer, o.stride_bytes, o.kbox, rows, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// 2-CTA (cta_group::2, 256 x 256 pair tiles) unless SB_GEMM_1CTA=1.
+bool use_2cta(sb_handle h) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("SB_GEMM_1CTA");
+    env = (e && e[0] == '1') ? 1 : 0;
+  }
+  return env == 0 && h->num_sms >= 2;
+}
+
 template <int KIND, int OUT, bool A_MN = false, bool B_MN = false, bool SB_COL = false>
-cudaError_t launch_tc(sb_handle h, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d,
-                      const sbtc::Params& p, uint32_t idesc) {
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(sbtc::k_tc_gemm<KIND, A_MN, B_MN, OUT, SB_COL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    sbtc::SMEM_BYTES);
-  });
-  if (attr_err != cudaSuccess) return attr_err;
-  const int tiles = p.tiles_m * p.tiles_n * p.splits;
-  const int grid = tiles < h->num_sms ? tiles : h->num_sms;
+cudaError_t launch_tc(sb_handle h, const Operand& A, const Operand& B, const CUtensorMap& d, sbtc::Params p,
+                      uint32_t idesc) {
+  const bool two = use_2cta(h);
+  CUtensorMap ta, tb;
+  if (!encode_operand(&ta, A, 128) || !encode_operand(&tb, B, two ? 128 : 256)) return cudaErrorInvalidValue;
+  p.tiles_m = static_cast<int>((p.M + (two ? sbtc2::BM2 : sbtc::BM) - 1) / (two ? sbtc2::BM2 : sbtc::BM));
+  p.tiles_n = static_cast<int>((p.N + sbtc::BN - 1) / sbtc::BN);
+  if (p.splits < 1) p.splits = 1;
+  const int units = p.tiles_m * p.tiles_n * p.splits;
   h->launches++;
-  sbtc::k_tc_gemm<KIND, A_MN, B_MN, OUT, SB_COL><<<grid, sbtc::NUM_THREADS, sbtc::SMEM_BYTES, h->stream>>>(a, b, d, p, idesc);
+  if (two) {
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [] {
+      attr_err = cudaFuncSetAttribute(sbtc2::k_tc_gemm2<KIND, A_MN, B_MN, OUT, SB_COL>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, sbtc2::SMEM2_BYTES);
+    });
+    if (attr_err != cudaSuccess) return attr_err;
+    const int pairs = h->num_sms / 2;
+    const int grid = 2 * (units < pairs ? units : pairs);
+    sbtc2::k_tc_gemm2<KIND, A_MN, B_MN, OUT, SB_COL><<<grid, sbtc::NUM_THREADS, sbtc2::SMEM2_BYTES, h->stream>>>(
+        ta, tb, d, p, idesc);
+    return cudaGetLastError();
+  }
+  static std::once_flag once1;
+  static cudaError_t attr_err1 = cudaSuccess;
+  std::call_once(once1, [] {
+    attr_err1 = cudaFuncSetAttribute(sbtc::k_tc_gemm<KIND, A_MN, B_MN, OUT, SB_COL>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, sbtc::SMEM_BYTES);
+  });
+  if (attr_err1 != cudaSuccess) return attr_err1;
+  const int grid = units < h->num_sms ? units : h->num_sms;
+  sbtc::k_tc_gemm<KIND, A_MN, B_MN, OUT, SB_COL><<<grid, sbtc::NUM_THREADS, sbtc::SMEM_BYTES, h->stream>>>(
+      ta, tb, d, p, idesc);
   return cudaGetLastError();
 }
 
@@ -208,44 +257,41 @@ sb_status gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* 
   const bool tc_ok = out_dt != SB_I64 && K <= kInt32SafeInner && (K % 16 == 0) && aligned(qa, 16) &&
                      aligned(qb, 16) && aligned(out, 16) && ((N * static_cast<int64_t>(dt_size(out_dt))) % 16 == 0) &&
                      M < (1LL << 31) && N < (1LL << 31) && get_encode() != nullptr;
-  if (tc_ok) {
-    CUtensorMap ta, tb, td;
-    bool ok = encode_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, qa, K, M, K, 128, 128, CU_TENSOR_MAP_SWIZZLE_128B) &&
-              encode_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, qb, K, N, K, 128, 256, CU_TENSOR_MAP_SWIZZLE_128B) &&
-              out_tmap(&td, out_dt, out, M, N);
-    if (ok) {
-      sbtc::Params p;
-      p.M = static_cast<int>(M);
-      p.N = static_cast<int>(N);
-      p.K = static_cast<int>(K);
-      p.sa = sa;
-      p.sb = sbp;
-      p.sa_stride = sa_stride;
-      p.sb_stride = sb_stride;
-      p.post_scale = 1.0f / 16129.0f;
-      p.tiles_m = static_cast<int>((M + sbtc::BM - 1) / sbtc::BM);
-      p.tiles_n = static_cast<int>((N + sbtc::BN - 1) / sbtc::BN);
-      p.splits = 1;
-      cudaError_t e;
-      const bool col = sb_stride == 1;
-      switch (out_mode) {
-        case sbtc::OUT_BF16:
-          e = col ? launch_tc<sbtc::KIND_I8, sbtc::OUT_BF16, false, false, true>(h, ta, tb, td, p, 0)
-                  : launch_tc<sbtc::KIND_I8, sbtc::OUT_BF16>(h, ta, tb, td, p, 0);
-          break;
-        case sbtc::OUT_F32:
-          e = col ? launch_tc<sbtc::KIND_I8, sbtc::OUT_F32, false, false, true>(h, ta, tb, td, p, 0)
-                  : launch_tc<sbtc::KIND_I8, sbtc::OUT_F32>(h, ta, tb, td, p, 0);
-          break;
-        case sbtc::OUT_F32_EXACT:
-          e = col ? launch_tc<sbtc::KIND_I8, sbtc::OUT_F32_EXACT, false, false, true>(h, ta, tb, td, p, 0)
-                  : launch_tc<sbtc::KIND_I8, sbtc::OUT_F32_EXACT>(h, ta, tb, td, p, 0);
-          break;
-        default: e = launch_tc<sbtc::KIND_I8, sbtc::OUT_I32>(h, ta, tb, td, p, 0); break;
-      }
-      if (e != cudaSuccess) return cuda_fail(op, e);
-      return SB_OK;
+  CUtensorMap td;
+  if (tc_ok && out_tmap(&td, out_dt, out, M, N)) {
+    const Operand A{qa, CU_TENSOR_MAP_DATA_TYPE_UINT8, static_cast<uint64_t>(K), static_cast<uint64_t>(M),
+                    static_cast<uint64_t>(K), false, 128};
+    const Operand B{qb, CU_TENSOR_MAP_DATA_TYPE_UINT8, static_cast<uint64_t>(K), static_cast<uint64_t>(N),
+                    static_cast<uint64_t>(K), false, 128};
+    sbtc::Params p{};
+    p.M = static_cast<int>(M);
+    p.N = static_cast<int>(N);
+    p.K = static_cast<int>(K);
+    p.sa = sa;
+    p.sb = sbp;
+    p.sa_stride = sa_stride;
+    p.sb_stride = sb_stride;
+    p.post_scale = 1.0f / 16129.0f;
+    p.splits = 1;
+    cudaError_t e;
+    const bool col = sb_stride == 1;
+    switch (out_mode) {
+      case sbtc::OUT_BF16:
+        e = col ? launch_tc<sbtc::KIND_I8, sbtc::OUT_BF16, false, false, true>(h, A, B, td, p, 0)
+                : launch_tc<sbtc::KIND_I8, sbtc::OUT_BF16>(h, A, B, td, p, 0);
+        break;
+      case sbtc::OUT_F32:
+        e = col ? launch_tc<sbtc::KIND_I8, sbtc::OUT_F32, false, false, true>(h, A, B, td, p, 0)
+                : launch_tc<sbtc::KIND_I8, sbtc::OUT_F32>(h, A, B, td, p, 0);
+        break;
+      case sbtc::OUT_F32_EXACT:
+        e = col ? launch_tc<sbtc::KIND_I8, sbtc::OUT_F32_EXACT, false, false, true>(h, A, B, td, p, 0)
+                : launch_tc<sbtc::KIND_I8, sbtc::OUT_F32_EXACT>(h, A, B, td, p, 0);
+        break;
+      default: e = launch_tc<sbtc::KIND_I8, sbtc::OUT_I32>(h, A, B, td, p, 0); break;
     }
+    if (e != cudaSuccess) return cuda_fail(op, e);
+    return SB_OK;
   }
   // SIMT path (unaligned / tiny / int64 accumulation)
   const dim3 grid(static_cast<unsigned>((N + 127) / 128), static_cast<unsigned>(M));
@@ -277,45 +323,43 @@ sb_status matmul_f32_seq(sb_handle h, const float* a, int64_t a_rs, int64_t a_ks
 sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m, int64_t n, float* dw,
                 int exact, int accumulate) {
   const char* op = "linear_backward";
-  if (dt == SB_BF16 && !exact) {
-    const bool tc_ok = (m % 8 == 0) && (n % 8 == 0) && aligned(g, 16) && aligned(x, 16) && aligned(dw, 16) &&
-                       b < (1LL << 31) && get_encode() != nullptr;
-    if (tc_ok) {
-      CUtensorMap ta, tb, td;
-      // A = G viewed MN-major: inner dim m (contiguous), outer dim T; box {64 m, 64 tokens}
-      bool ok = encode_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, g, m, b, m * 2, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) &&
-                encode_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, x, n, b, n * 2, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) &&
-                out_tmap(&td, SB_F32, dw, m, n);
-      if (ok) {
-        sbtc::Params p;
-        p.M = static_cast<int>(m);
-        p.N = static_cast<int>(n);
-        p.K = static_cast<int>(b);
-        p.sa = nullptr;
-        p.sb = nullptr;
-        p.sa_stride = p.sb_stride = 0;
-        p.post_scale = 1.0f;
-        p.tiles_m = static_cast<int>((m + sbtc::BM - 1) / sbtc::BM);
-        p.tiles_n = static_cast<int>((n + sbtc::BN - 1) / sbtc::BN);
-        // Split K (= tokens) in two when the output has too few tiles to fill the SMs in whole
-        // waves: both halves reduce-add into a zeroed dW, and 0 + a + b == 0 + b + a, so the
-        // result stays deterministic (more splits would make the fp32 sum order-dependent).
-        const int tiles = p.tiles_m * p.tiles_n;
-        const int64_t kblocks = (b + 63) / 64;
-        auto eff = [&](int s) { int u = tiles * s; int w = (u + h->num_sms - 1) / h->num_sms; return double(u) / (w * h->num_sms); };
-        p.splits = (!accumulate && kblocks >= 64 && eff(2) > eff(1) + 0.05) ? 2 : 1;
-        cudaError_t e;
-        if (p.splits == 2) {
-          e = cudaMemsetAsync(dw, 0, sizeof(float) * m * n, h->stream);
-          if (e == cudaSuccess) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW_ADD, true, true>(h, ta, tb, td, p, 0);
-        } else {
-          e = accumulate ? launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW_ADD, true, true>(h, ta, tb, td, p, 0)
-                         : launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW, true, true>(h, ta, tb, td, p, 0);
-        }
-        if (e != cudaSuccess) return cuda_fail(op, e);
-        return SB_OK;
-      }
+  CUtensorMap td;
+  if (dt == SB_BF16 && !exact && (m % 8 == 0) && (n % 8 == 0) && aligned(g, 16) && aligned(x, 16) && aligned(dw, 16) &&
+      b < (1LL << 31) && get_encode() != nullptr && out_tmap(&td, SB_F32, dw, m, n)) {
+    // A = G[T x m] and B = X[T x n] read in place as MN-major operands; K = T tokens
+    const Operand A{g, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, static_cast<uint64_t>(m), static_cast<uint64_t>(b),
+                    static_cast<uint64_t>(m * 2), true, 64};
+    const Operand B{x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, static_cast<uint64_t>(n), static_cast<uint64_t>(b),
+                    static_cast<uint64_t>(n * 2), true, 64};
+    sbtc::Params p{};
+    p.M = static_cast<int>(m);
+    p.N = static_cast<int>(n);
+    p.K = static_cast<int>(b);
+    p.post_scale = 1.0f;
+    // Split K (= tokens) in two when the output has too few tiles to fill the SMs (pairs) in
+    // whole waves: both halves reduce-add into a zeroed dW, and 0 + a + b == 0 + b + a, so the
+    // result stays deterministic (more splits would make the fp32 sum order-dependent).
+    const bool two = use_2cta(h);
+    const int tm = static_cast<int>((m + (two ? 256 : 128) - 1) / (two ? 256 : 128));
+    const int tiles = tm * static_cast<int>((n + 255) / 256);
+    const int slots = two ? h->num_sms / 2 : h->num_sms;
+    const int64_t kblocks = (b + 63) / 64;
+    auto eff = [&](int s) {
+      const int u = tiles * s;
+      const int w = (u + slots - 1) / slots;
+      return double(u) / (double(w) * slots);
+    };
+    p.splits = (!accumulate && kblocks >= 64 && eff(2) > eff(1) + 0.05) ? 2 : 1;
+    cudaError_t e;
+    if (p.splits == 2) {
+      e = cudaMemsetAsync(dw, 0, sizeof(float) * m * n, h->stream);
+      if (e == cudaSuccess) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW_ADD, true, true>(h, A, B, td, p, 0);
+    } else {
+      e = accumulate ? launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW_ADD, true, true>(h, A, B, td, p, 0)
+                     : launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW, true, true>(h, A, B, td, p, 0);
     }
+    if (e != cudaSuccess) return cuda_fail(op, e);
+    return SB_OK;
   }
   // exact sequential (or unaligned fallback): dW[i][j] = sum_t G[t][i] * X[t][j]
   const dim3 grid(static_cast<unsigned>((n + 63) / 64), static_cast<unsigned>((m + 63) / 64));
@@ -337,52 +381,47 @@ sb_status gemm_bf16_tc(sb_handle h, const void* a, bool a_mn, const void* b, boo
   const bool tc_ok = (a_mn ? M % 8 == 0 : K % 8 == 0) && (b_mn ? N % 8 == 0 : K % 8 == 0) && aligned(a, 16) &&
                      aligned(b, 16) && aligned(out, 16) && ((N * static_cast<int64_t>(dt_size(out_dt))) % 16 == 0) &&
                      get_encode() != nullptr;
-  if (tc_ok) {
-    CUtensorMap ta, tb, td;
+  CUtensorMap td;
+  if (tc_ok && out_tmap(&td, out_dt, out, M, N)) {
     const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-    const CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B;
-    bool ok = (a_mn ? encode_tmap_2d(&ta, bf, a, M, K, M * 2, 64, 64, sw) : encode_tmap_2d(&ta, bf, a, K, M, K * 2, 64, 128, sw)) &&
-              (b_mn ? encode_tmap_2d(&tb, bf, b, N, K, N * 2, 64, 64, sw) : encode_tmap_2d(&tb, bf, b, K, N, K * 2, 64, 256, sw)) &&
-              out_tmap(&td, out_dt, out, M, N);
-    if (ok) {
-      sbtc::Params p;
-      p.M = static_cast<int>(M);
-      p.N = static_cast<int>(N);
-      p.K = static_cast<int>(K);
-      p.sa = one;
-      p.sb = one;
-      p.sa_stride = p.sb_stride = 0;
-      p.post_scale = 1.0f;
-      p.tiles_m = static_cast<int>((M + sbtc::BM - 1) / sbtc::BM);
-      p.tiles_n = static_cast<int>((N + sbtc::BN - 1) / sbtc::BN);
-      p.splits = 1;
-      cudaError_t e;
-      if (out_dt == SB_BF16) {
-        if (!a_mn && !b_mn) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_BF16, false, false>(h, ta, tb, td, p, 0);
-        else if (!a_mn && b_mn) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_BF16, false, true>(h, ta, tb, td, p, 0);
-        else if (a_mn && !b_mn) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_BF16, true, false>(h, ta, tb, td, p, 0);
-        else e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_BF16, true, true>(h, ta, tb, td, p, 0);
-      } else {
-        if (!a_mn && !b_mn) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW, false, false>(h, ta, tb, td, p, 0);
-        else if (!a_mn && b_mn) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW, false, true>(h, ta, tb, td, p, 0);
-        else if (a_mn && !b_mn) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW, true, false>(h, ta, tb, td, p, 0);
-        else e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW, true, true>(h, ta, tb, td, p, 0);
-      }
-      if (e != cudaSuccess) return cuda_fail(op, e);
-      return SB_OK;
+    const Operand A = a_mn ? Operand{a, bf, static_cast<uint64_t>(M), static_cast<uint64_t>(K), static_cast<uint64_t>(M * 2), true, 64}
+                           : Operand{a, bf, static_cast<uint64_t>(K), static_cast<uint64_t>(M), static_cast<uint64_t>(K * 2), false, 64};
+    const Operand B = b_mn ? Operand{b, bf, static_cast<uint64_t>(N), static_cast<uint64_t>(K), static_cast<uint64_t>(N * 2), true, 64}
+                           : Operand{b, bf, static_cast<uint64_t>(K), static_cast<uint64_t>(N), static_cast<uint64_t>(K * 2), false, 64};
+    sbtc::Params p{};
+    p.M = static_cast<int>(M);
+    p.N = static_cast<int>(N);
+    p.K = static_cast<int>(K);
+    p.sa = one;
+    p.sb = one;
+    p.post_scale = 1.0f;
+    p.splits = 1;
+    cudaError_t e;
+    if (out_dt == SB_BF16) {
+      if (!a_mn && !b_mn) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_BF16, false, false>(h, A, B, td, p, 0);
+      else if (!a_mn && b_mn) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_BF16, false, true>(h, A, B, td, p, 0);
+      else if (a_mn && !b_mn) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_BF16, true, false>(h, A, B, td, p, 0);
+      else e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_BF16, true, true>(h, A, B, td, p, 0);
+    } else {
+      if (!a_mn && !b_mn) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW, false, false>(h, A, B, td, p, 0);
+      else if (!a_mn && b_mn) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW, false, true>(h, A, B, td, p, 0);
+      else if (a_mn && !b_mn) e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW, true, false>(h, A, B, td, p, 0);
+      else e = launch_tc<sbtc::KIND_BF16, sbtc::OUT_F32_RAW, true, true>(h, A, B, td, p, 0);
     }
+    if (e != cudaSuccess) return cuda_fail(op, e);
+    return SB_OK;
   }
   // any shape: fp32-accumulating SIMT kernel over the same index maps
-  const __nv_bfloat16* A = static_cast<const __nv_bfloat16*>(a);
-  const __nv_bfloat16* B = static_cast<const __nv_bfloat16*>(b);
+  const __nv_bfloat16* Ap = static_cast<const __nv_bfloat16*>(a);
+  const __nv_bfloat16* Bp = static_cast<const __nv_bfloat16*>(b);
   const int64_t a_rs = a_mn ? 1 : K, a_ks = a_mn ? M : 1, b_rs = b_mn ? 1 : K, b_ks = b_mn ? N : 1;
   const dim3 grid(static_cast<unsigned>((N + 63) / 64), static_cast<unsigned>((M + 63) / 64));
   h->launches++;
   if (out_dt == SB_BF16)
-    k_matmul_seq<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, h->stream>>>(A, a_rs, a_ks, B, b_rs, b_ks, M, N, K,
+    k_matmul_seq<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, h->stream>>>(Ap, a_rs, a_ks, Bp, b_rs, b_ks, M, N, K,
                                                                             static_cast<__nv_bfloat16*>(out), 0);
   else
-    k_matmul_seq<__nv_bfloat16, float><<<grid, 256, 0, h->stream>>>(A, a_rs, a_ks, B, b_rs, b_ks, M, N, K,
+    k_matmul_seq<__nv_bfloat16, float><<<grid, 256, 0, h->stream>>>(Ap, a_rs, a_ks, Bp, b_rs, b_ks, M, N, K,
                                                                     static_cast<float*>(out), 0);
   SB_LAUNCH_CHECK(op);
   return SB_OK;
@@ -395,36 +434,33 @@ sb_status gemm_fp8(sb_handle h, const uint8_t* qa, int fa, const float* sa, int 
   const int sa_stride = axa == SB_AXIS_ROW ? 1 : 0, sb_stride = axb == SB_AXIS_ROW ? 1 : 0;
   const bool tc_ok = (K % 16 == 0) && aligned(qa, 16) && aligned(qb, 16) && aligned(out, 16) &&
                      ((N * static_cast<int64_t>(dt_size(out_dt))) % 16 == 0) && get_encode() != nullptr;
-  if (tc_ok) {
-    CUtensorMap ta, tb, td;
-    bool ok = encode_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, qa, K, M, K, 128, 128, CU_TENSOR_MAP_SWIZZLE_128B) &&
-              encode_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, qb, K, N, K, 128, 256, CU_TENSOR_MAP_SWIZZLE_128B) &&
-              out_tmap(&td, out_dt, out, M, N);
-    if (ok) {
-      sbtc::Params p;
-      p.M = static_cast<int>(M);
-      p.N = static_cast<int>(N);
-      p.K = static_cast<int>(K);
-      p.sa = sa;
-      p.sb = sbp;
-      p.sa_stride = sa_stride;
-      p.sb_stride = sb_stride;
-      p.post_scale = 1.0f;
-      p.tiles_m = static_cast<int>((M + sbtc::BM - 1) / sbtc::BM);
-      p.tiles_n = static_cast<int>((N + sbtc::BN - 1) / sbtc::BN);
-      p.splits = 1;
-      const uint32_t idesc = sbtc::KindTraits<sbtc::KIND_F8>::IDESC | (static_cast<uint32_t>(fa) << 7) |
-                             (static_cast<uint32_t>(fb) << 10);
-      cudaError_t e;
-      if (sb_stride)
-        e = out_dt == SB_BF16 ? launch_tc<sbtc::KIND_F8, sbtc::OUT_BF16, false, false, true>(h, ta, tb, td, p, idesc)
-                              : launch_tc<sbtc::KIND_F8, sbtc::OUT_F32, false, false, true>(h, ta, tb, td, p, idesc);
-      else
-        e = out_dt == SB_BF16 ? launch_tc<sbtc::KIND_F8, sbtc::OUT_BF16>(h, ta, tb, td, p, idesc)
-                              : launch_tc<sbtc::KIND_F8, sbtc::OUT_F32>(h, ta, tb, td, p, idesc);
-      if (e != cudaSuccess) return cuda_fail(op, e);
-      return SB_OK;
-    }
+  CUtensorMap td;
+  if (tc_ok && out_tmap(&td, out_dt, out, M, N)) {
+    const Operand A{qa, CU_TENSOR_MAP_DATA_TYPE_UINT8, static_cast<uint64_t>(K), static_cast<uint64_t>(M),
+                    static_cast<uint64_t>(K), false, 128};
+    const Operand B{qb, CU_TENSOR_MAP_DATA_TYPE_UINT8, static_cast<uint64_t>(K), static_cast<uint64_t>(N),
+                    static_cast<uint64_t>(K), false, 128};
+    sbtc::Params p{};
+    p.M = static_cast<int>(M);
+    p.N = static_cast<int>(N);
+    p.K = static_cast<int>(K);
+    p.sa = sa;
+    p.sb = sbp;
+    p.sa_stride = sa_stride;
+    p.sb_stride = sb_stride;
+    p.post_scale = 1.0f;
+    p.splits = 1;
+    const uint32_t idesc = sbtc::KindTraits<sbtc::KIND_F8>::IDESC | (static_cast<uint32_t>(fa) << 7) |
+                           (static_cast<uint32_t>(fb) << 10);
+    cudaError_t e;
+    if (sb_stride)
+      e = out_dt == SB_BF16 ? launch_tc<sbtc::KIND_F8, sbtc::OUT_BF16, false, false, true>(h, A, B, td, p, idesc)
+                            : launch_tc<sbtc::KIND_F8, sbtc::OUT_F32, false, false, true>(h, A, B, td, p, idesc);
+    else
+      e = out_dt == SB_BF16 ? launch_tc<sbtc::KIND_F8, sbtc::OUT_BF16>(h, A, B, td, p, idesc)
+                            : launch_tc<sbtc::KIND_F8, sbtc::OUT_F32>(h, A, B, td, p, idesc);
+    if (e != cudaSuccess) return cuda_fail(op, e);
+    return SB_OK;
   }
   const dim3 grid(static_cast<unsigned>((N + 127) / 128), static_cast<unsigned>(M));
   h->launches++;

@@ -300,8 +300,13 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_rowwise_tma(const T* __r
       const Scale sc = make_scale(st);
       const bool plain = sc.pre == 1.0f;
       Out* qr = reinterpret_cast<Out*>(q + row * ldq);
+      // warp-uniform trip count: qvec() votes across the warp (__any_sync)
 #pragma unroll 4
-      for (int v = lane; v < nvec; v += 32) qr[v] = qvec<T>(xs[v], sc, plain);
+      for (int b = 0; b < nvec; b += 32) {
+        const int v = b + lane;
+        const Out o = qvec<T>(v < nvec ? xs[v] : make_uint4(0, 0, 0, 0), sc, plain);
+        if (v < nvec) qr[v] = o;
+      }
     }
     __syncwarp();
     if (lane == 0) sbptx::mbar_arrive(&empty[s]);
@@ -335,7 +340,11 @@ __global__ void __launch_bounds__(256) k_quantize_rowwise_stream(const T* __rest
   if (lane == 0) state[row] = s;
   const Scale sc = make_scale(s);
   const bool plain = sc.pre == 1.0f;
-  for (int64_t v = lane; v < nvec; v += 32) qr[v] = qvec<T>(__ldg(xr + v), sc, plain);
+  for (int64_t b = 0; b < nvec; b += 32) {  // warp-uniform trip count (qvec votes)
+    const int64_t v = b + lane;
+    const Out o = qvec<T>(v < nvec ? __ldg(xr + v) : make_uint4(0, 0, 0, 0), sc, plain);
+    if (v < nvec) qr[v] = o;
+  }
 }
 
 // Any shape / alignment: scalar element access.
