@@ -197,8 +197,29 @@ cudaError_t launch_tc(sb_handle h, const Operand& A, const Operand& B, const CUt
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, sbtc2::SMEM2_BYTES);
     });
     if (attr_err != cudaSuccess) return attr_err;
-    const int pairs = h->num_sms / 2;
-    const int grid = 2 * (units < pairs ? units : pairs);
+    // persistent grid: only as many CTA pairs as can be co-resident (a pair needs two SMs of
+    // one TPC); launching more would run the surplus as a second wave
+    static int max_pairs = 0;
+    if (max_pairs == 0) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(2 * (h->num_sms / 2));
+      cfg.blockDim = dim3(sbtc::NUM_THREADS);
+      cfg.dynamicSmemBytes = sbtc2::SMEM2_BYTES;
+      cudaLaunchAttribute attr;
+      attr.id = cudaLaunchAttributeClusterDimension;
+      attr.val.clusterDim.x = 2;
+      attr.val.clusterDim.y = 1;
+      attr.val.clusterDim.z = 1;
+      cfg.attrs = &attr;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, sbtc2::k_tc_gemm2<KIND, A_MN, B_MN, OUT, SB_COL>, &cfg) != cudaSuccess ||
+          n < 1)
+        n = h->num_sms / 2;
+      max_pairs = n;
+      cudaGetLastError();
+    }
+    const int grid = 2 * (units < max_pairs ? units : max_pairs);
     sbtc2::k_tc_gemm2<KIND, A_MN, B_MN, OUT, SB_COL><<<grid, sbtc::NUM_THREADS, sbtc2::SMEM2_BYTES, h->stream>>>(
         ta, tb, d, p, idesc);
     return cudaGetLastError();
