@@ -17,6 +17,7 @@
 #include "tc_gemm.cuh"
 #include "tc_gemm2.cuh"
 
+#include <cstdio>
 #include <cstdlib>
 
 namespace {
@@ -218,6 +219,7 @@ cudaError_t launch_tc(sb_handle h, const Operand& A, const Operand& B, const CUt
         n = h->num_sms / 2;
       max_pairs = n;
       cudaGetLastError();
+      if (getenv("SB_DEBUG")) fprintf(stderr, "[sb] 2-CTA GEMM: %d co-resident pairs\n", n);
     }
     const int grid = 2 * (units < max_pairs ? units : max_pairs);
     sbtc2::k_tc_gemm2<KIND, A_MN, B_MN, OUT, SB_COL><<<grid, sbtc::NUM_THREADS, sbtc2::SMEM2_BYTES, h->stream>>>(
