@@ -169,14 +169,16 @@ bool encode_operand(CUtensorMap* m, const Operand& o, uint32_t rows) {
   return sb::encode_tmap_2d(m, o.dt, o.ptr, o.inner, o.outer, o.stride_bytes, o.kbox, rows, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-// 2-CTA (cta_group::2, 256 x 256 pair tiles) unless SB_GEMM_1CTA=1.
+// 1-CTA 128 x 256 tiles by default; SB_GEMM_2CTA=1 selects the cta_group::2 256 x 256 kernel
+// (tc_gemm2.cuh: bit-exact, but its 2-SM TMA feed currently runs at ~half the 1-CTA rate —
+// see DESIGN.md "open items").
 bool use_2cta(sb_handle h) {
   static int env = -1;
   if (env < 0) {
-    const char* e = getenv("SB_GEMM_1CTA");
+    const char* e = getenv("SB_GEMM_2CTA");
     env = (e && e[0] == '1') ? 1 : 0;
   }
-  return env == 0 && h->num_sms >= 2;
+  return env == 1 && h->num_sms >= 2;
 }
 
 template <int KIND, int OUT, bool A_MN = false, bool B_MN = false, bool SB_COL = false>
