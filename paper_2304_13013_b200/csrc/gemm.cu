@@ -375,6 +375,9 @@ sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t 
       return double(u) / (double(w) * slots);
     };
     p.splits = (!accumulate && kblocks >= 64 && eff(2) > eff(1) + 0.05) ? 2 : 1;
+    // raster so the larger operand is streamed once: tiles sharing a block of it run
+    // concurrently (G^T X: walk M when X is the larger of the two)
+    p.m_fast = n > m ? 1 : 0;
     cudaError_t e;
     if (p.splits == 2) {
       e = cudaMemsetAsync(dw, 0, sizeof(float) * m * n, h->stream);

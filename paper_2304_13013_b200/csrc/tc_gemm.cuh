@@ -61,13 +61,14 @@ struct Params {
   float post_scale;        // 1/16129 for int8 dequant, 1 otherwise
   int tiles_m, tiles_n;
   int splits;              // split-K factor: work unit u = (tile u / splits, k-slice u % splits)
+  int m_fast;              // raster: 1 = consecutive tiles walk M (B tile reused), 0 = walk N (A reused)
 };
 
 // Work unit -> (m0, n0, [kb0, kb1)).
 __device__ __forceinline__ void unit_coords(const Params& p, int u, int k_blocks, int& m0, int& n0, int& kb0, int& kb1) {
   const int t = u / p.splits, s = u - t * p.splits;
-  m0 = (t / p.tiles_n) * BM;
-  n0 = (t % p.tiles_n) * BN;
+  m0 = (p.m_fast ? t % p.tiles_m : t / p.tiles_n) * BM;
+  n0 = (p.m_fast ? t / p.tiles_m : t % p.tiles_n) * BN;
   kb0 = static_cast<int>((static_cast<int64_t>(k_blocks) * s) / p.splits);
   kb1 = static_cast<int>((static_cast<int64_t>(k_blocks) * (s + 1)) / p.splits);
 }

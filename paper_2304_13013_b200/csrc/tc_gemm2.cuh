@@ -79,8 +79,8 @@ __device__ __forceinline__ void mma2(uint32_t d, uint64_t a, uint64_t b, uint32_
 // Work unit -> (m0 of the 256-row pair tile, n0, [kb0, kb1)).
 __device__ __forceinline__ void unit2(const Params& p, int u, int k_blocks, int& m0, int& n0, int& kb0, int& kb1) {
   const int t = u / p.splits, s = u - t * p.splits;
-  m0 = (t / p.tiles_n) * BM2;
-  n0 = (t % p.tiles_n) * BN;
+  m0 = (p.m_fast ? t % p.tiles_m : t / p.tiles_n) * BM2;
+  n0 = (p.m_fast ? t / p.tiles_m : t % p.tiles_n) * BN;
   kb0 = static_cast<int>((static_cast<int64_t>(k_blocks) * s) / p.splits);
   kb1 = static_cast<int>((static_cast<int64_t>(k_blocks) * (s + 1)) / p.splits);
 }
