@@ -81,6 +81,14 @@ const char* sb_last_error(void);
 /* Kernel launches issued through this handle so far (launch accounting for bench.py). */
 uint64_t sb_launch_count(sb_handle h);
 
+/* Device memory + synchronous copies on the handle's stream (for FFI callers without a CUDA runtime). */
+sb_status sb_device_alloc(sb_handle h, size_t bytes, void** out);
+sb_status sb_device_free(sb_handle h, void* ptr);
+sb_status sb_copy_to_device(sb_handle h, void* dst, const void* src, size_t bytes);
+sb_status sb_copy_to_host(sb_handle h, void* dst, const void* src, size_t bytes);
+/* Matrix::all_finite (matrix.cpp:22-26) as a device check: latches SB_ERR_NONFINITE for sb_synchronize. */
+sb_status sb_check_finite(sb_handle h, const void* x, sb_dtype dt, int64_t n);
+
 /* ----------------------------------------------------------- quantize -- */
 /* quantize_rowwise, quantize.hpp:67 / quantize.cpp:131-133.
  * x: rows x cols (leading dim ldx elements) of `dt` (SB_F32 or SB_BF16);
@@ -114,6 +122,18 @@ sb_status sb_quantize_fp8(sb_handle h, const void* x, sb_dtype dt, int64_t rows,
 /* dequantize (fp8 branch), quantize.cpp:185-189: y = float(double(value(p)) * double(state)). */
 sb_status sb_dequantize_fp8(sb_handle h, const uint8_t* q, int64_t rows, int64_t cols, int64_t ldq, sb_fp8_format fmt,
                             const float* state, sb_axis axis, void* y, sb_dtype ydt, int64_t ldy);
+
+/* fp8_cast, quantize.hpp:44 / quantize.cpp:78-84: y = nearest e4m3/e5m2 value of x, ties to the
+ * smaller magnitude, saturating at the format's largest finite value. */
+sb_status sb_fp8_cast(sb_handle h, const float* x, int64_t n, sb_fp8_format fmt, float* y);
+
+/* dequantize (fp8 branch) over DECODED payload values p (fp32 value-set members, the reference's
+ * payload_fp8 representation): y = float(double(p) * double(state)), quantize.cpp:185-189. */
+sb_status sb_dequantize_values(sb_handle h, const float* p, int64_t rows, int64_t cols, const float* state, sb_axis axis,
+                               float* y);
+
+/* transpose_tensorwise's payload move (linear.cpp:170-189): out[cols x rows] = in[rows x cols]^T. */
+sb_status sb_transpose_i8(sb_handle h, const int8_t* in, int64_t rows, int64_t cols, int8_t* out);
 
 /* --------------------------------------------------------------- GEMM -- */
 /* int8_matmul_dequant / matmul_dequant_dual_rowwise, linear.hpp:54-58 / linear.cpp:39-83.
@@ -227,6 +247,21 @@ sb_status sb_stableadamw_workspace_size(const sb_adamw_tensor* tensors, int nten
  * may be NULL. Element math in fp64 mirroring optimizer.cpp:142-146,162-167. */
 sb_status sb_stableadamw_step(sb_handle h, const sb_adamw_tensor* tensors, int ntensors, const sb_adamw_hparams* hp,
                               int64_t t, double* rms_out, double* eta_out, void* workspace, size_t workspace_bytes);
+
+/* compute_rms, optimizer.hpp:54 / optimizer.cpp:31-42: *out (DEVICE double) =
+ * sqrt(mean(g^2 / max(u, eps^2))), fp64, fixed-order reduction. */
+sb_status sb_compute_rms(sb_handle h, const float* g, const float* u, int64_t n, double eps, double* out);
+
+/* grad_clip_global_norm, optimizer.hpp:59 / optimizer.cpp:72-81: scales every gradient by
+ * max_norm / norm when the global L2 norm exceeds max_norm. `grads` / `numel` are HOST arrays
+ * of device pointers / sizes. */
+sb_status sb_grad_clip_global_norm(sb_handle h, float* const* grads, const int64_t* numel, int n, double max_norm);
+
+/* filter_nonfinite, optimizer.hpp:67 / optimizer.cpp:83-100: out_i = float(double(g_i) / scale);
+ * skipped[i] (DEVICE int32) = 1 when out_i has a non-finite entry; with per_tensor_skip = 0 any
+ * bad tensor marks all of them. */
+sb_status sb_filter_nonfinite(sb_handle h, const float* const* grads, float* const* out, const int64_t* numel, int n,
+                              double scale, int per_tensor_skip, int32_t* skipped);
 
 #ifdef __cplusplus
 }

@@ -30,6 +30,8 @@ EXPORTS = [
     "sb_quantize_tensorwise", "sb_dequantize", "sb_quantize_fp8", "sb_dequantize_fp8", "sb_gemm_i8",
     "sb_matmul_f32", "sb_wgrad", "sb_gemm_fp8", "sb_linear_workspace_size", "sb_linear_forward",
     "sb_linear_backward", "sb_switchback_fwd_bwd_host", "sb_stableadamw_workspace_size", "sb_stableadamw_step",
+    "sb_device_alloc", "sb_device_free", "sb_copy_to_device", "sb_copy_to_host", "sb_check_finite", "sb_fp8_cast",
+    "sb_transpose_i8", "sb_compute_rms", "sb_grad_clip_global_norm", "sb_filter_nonfinite", "sb_dequantize_values",
 ]
 
 
@@ -112,6 +114,17 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             "sb_stableadamw_workspace_size": ([C.POINTER(AdamwTensor), i32, C.POINTER(sz)], i32),
             "sb_stableadamw_step": ([v, C.POINTER(AdamwTensor), i32, C.POINTER(AdamwHparams), i64, v, v, v, sz],
                                     i32),
+            "sb_device_alloc": ([v, sz, C.POINTER(v)], i32),
+            "sb_device_free": ([v, v], i32),
+            "sb_copy_to_device": ([v, v, v, sz], i32),
+            "sb_copy_to_host": ([v, v, v, sz], i32),
+            "sb_check_finite": ([v, v, i32, i64], i32),
+            "sb_fp8_cast": ([v, v, i64, i32, v], i32),
+            "sb_transpose_i8": ([v, v, i64, i64, v], i32),
+            "sb_compute_rms": ([v, v, v, i64, C.c_double, v], i32),
+            "sb_grad_clip_global_norm": ([v, C.POINTER(v), C.POINTER(i64), i32, C.c_double], i32),
+            "sb_filter_nonfinite": ([v, C.POINTER(v), C.POINTER(v), C.POINTER(i64), i32, C.c_double, i32, v], i32),
+            "sb_dequantize_values": ([v, v, i64, i64, v, i32, v], i32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

@@ -74,7 +74,8 @@ struct LinearWs {
   int8_t* g_q;
   float* g_state;
   void* deq;       // SwitchBackM / fp8: dequantized operand buffer (b x n, dt)
-  void* deq2;      // fp8 AllQuant: snapped G (b x m, dt)
+  void* deq2;      // fp8 AllQuant / exact fp8: snapped G (b x m, dt)
+  float* wdeq;     // exact fp8: snapped W (m x n, fp32)
   int8_t* gt_q;    // AllQuant int8: quantize_rowwise(G^T)  m x b
   float* gt_state;
   int8_t* xt_q;    // AllQuant int8: quantize_rowwise(X^T)  n x b
@@ -97,7 +98,10 @@ LinearWs carve(const sb_linear_mode& md, int64_t b, int64_t n, int64_t m, sb_dty
   w.g_state = c.take<float>(b);
   const bool need_deq = md.variant == SB_SWITCHBACK_M || md.format == SB_FP8;
   w.deq = need_deq ? static_cast<void*>(c.take<uint8_t>(b * n * es)) : nullptr;
-  w.deq2 = (md.format == SB_FP8 && md.variant == SB_ALLQUANT) ? static_cast<void*>(c.take<uint8_t>(b * m * es)) : nullptr;
+  w.deq2 = (md.format == SB_FP8 && (md.variant == SB_ALLQUANT || md.exact)) ? static_cast<void*>(c.take<uint8_t>(b * m * es))
+                                                                           : nullptr;
+  // exact fp8: the reference multiplies the dequantized (snapped) operands in fp32
+  w.wdeq = (md.format == SB_FP8 && md.exact) ? c.take<float>(m * n) : nullptr;
   if (md.format == SB_INT8 && md.variant == SB_ALLQUANT) {
     w.gt_q = c.take<int8_t>(m * b);
     w.gt_state = c.take<float>(m);
@@ -432,7 +436,14 @@ sb_status sb_linear_forward(sb_handle h, const sb_linear_mode* mode, const void*
   uint8_t* wq = reinterpret_cast<uint8_t*>(ws.w_q);
   SB_TRY(q_fp8(h, x, dt, b, n, n, ff, ax, xq, n, ws.x_state, ws.words));
   SB_TRY(q_fp8(h, w, dt, m, n, n, ff, wx, wq, n, ws.w_state, ws.words));
-  SB_TRY(sb::gemm_fp8(h, xq, ff, ws.x_state, ax, wq, ff, ws.w_state, wx, b, m, n, y, out_dt));
+  if (md.exact) {  // matmul(dequantize(qx), dequantize(qw)), linear.cpp:151-153, sequential fp32
+    SB_TRYC(op, sb::launch_dequantize_fp8(h, xq, b, n, n, ff, ws.x_state, ax, ws.deq, SB_F32, n));
+    SB_TRYC(op, sb::launch_dequantize_fp8(h, wq, m, n, n, ff, ws.w_state, wx, ws.wdeq, SB_F32, n));
+    SB_TRY(sb::matmul_f32_seq(h, static_cast<const float*>(ws.deq), n, 1, ws.wdeq, n, 1, b, m, n,
+                              static_cast<float*>(y), 0));
+  } else {
+    SB_TRY(sb::gemm_fp8(h, xq, ff, ws.x_state, ax, wq, ff, ws.w_state, wx, b, m, n, y, out_dt));
+  }
   if (ctx) {
     if (md.variant == SB_SWITCHBACK_M) {
       ctx->x_q = ws.x_q;
@@ -519,7 +530,15 @@ sb_status sb_linear_backward(sb_handle h, const sb_linear_mode* mode, const sb_l
   const int gx = md.variant == SB_ALLQUANT ? SB_AXIS_TENSOR : SB_AXIS_ROW;
   uint8_t* gq = reinterpret_cast<uint8_t*>(ws.g_q);
   SB_TRY(q_fp8(h, g, dt, b, m, m, fg, gx, gq, m, ws.g_state, ws.words));
-  SB_TRY(sb::gemm_fp8(h, gq, fg, ws.g_state, gx, wqt, ff, wt_state, wt_axis, b, n, m, dx, dt));
+  if (exact) {  // x_grad = matmul(g_snap, w_snap_t), linear.cpp:266, sequential fp32
+    SB_TRYC(op, sb::launch_dequantize_fp8(h, gq, b, m, m, fg, ws.g_state, gx, ws.deq2, SB_F32, m));
+    SB_TRYC(op, sb::launch_dequantize_fp8(h, reinterpret_cast<const uint8_t*>(wqt), n, m, m, ff, wt_state, wt_axis,
+                                          ws.wdeq, SB_F32, m));
+    SB_TRY(sb::matmul_f32_seq(h, static_cast<const float*>(ws.deq2), m, 1, ws.wdeq, m, 1, b, n, m,
+                              static_cast<float*>(dx), 0));
+  } else {
+    SB_TRY(sb::gemm_fp8(h, gq, fg, ws.g_state, gx, wqt, ff, wt_state, wt_axis, b, n, m, dx, dt));
+  }
   if (md.variant == SB_ALLQUANT) {
     // wgrad over snapped G and snapped (tensor-wise) X
     SB_TRYC(op, sb::launch_dequantize_fp8(h, gq, b, m, m, fg, ws.g_state, gx, ws.deq2, dt, m));

@@ -655,6 +655,17 @@ __global__ void k_dequantize_fp8(const uint8_t* __restrict__ q, int64_t rows, in
   }
 }
 
+// fp8_cast (quantize.cpp:78-84): snap to the value set without a scale; non-finite -> latch.
+__global__ void k_fp8_cast(const float* __restrict__ x, int64_t n, int fmt, float* __restrict__ y, uint32_t* err) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float v = x[i];
+    if (!isfinite(v)) raise_nonfinite(err);
+    const uint8_t b = fmt == 0 ? fp8_snap_encode<3, 7>(v, 448.0f, 0x7Eu) : fp8_snap_encode<2, 15>(v, 57344.0f, 0x7Bu);
+    y[i] = fp8_decode(b, fmt);
+  }
+}
+
 template <typename TI, typename TO>
 __global__ void k_convert(const TI* __restrict__ x, TO* __restrict__ y, int64_t n) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -770,6 +781,13 @@ cudaError_t launch_dequantize_fp8(sb_handle h, const uint8_t* q, int64_t rows, i
                                                   static_cast<__nv_bfloat16*>(y), ldy);
   else
     k_dequantize_fp8<<<grid, 256, 0, h->stream>>>(q, rows, cols, ldq, fmt, state, axis, static_cast<float*>(y), ldy);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fp8_cast(sb_handle h, const float* x, int64_t n, int fmt, float* y) {
+  const unsigned grid = grid_for(n, 256 * 4, h->num_sms);
+  h->launches++;
+  k_fp8_cast<<<grid, 256, 0, h->stream>>>(x, n, fmt, y, h->d_err);
   return cudaGetLastError();
 }
 

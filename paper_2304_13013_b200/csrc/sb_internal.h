@@ -84,6 +84,7 @@ cudaError_t launch_absmax_rows(sb_handle h, const void* x, sb_dtype dt, int64_t 
 cudaError_t launch_dequantize_fp8(sb_handle h, const uint8_t* q, int64_t rows, int64_t cols, int64_t ldq, int fmt,
                                   const float* state, int axis, void* y, sb_dtype ydt, int64_t ldy);
 cudaError_t launch_convert(sb_handle h, const void* x, sb_dtype xdt, void* y, sb_dtype ydt, int64_t n);
+cudaError_t launch_fp8_cast(sb_handle h, const float* x, int64_t n, int fmt, float* y);
 
 // gemm_i8.cu
 sb_status gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* qb, const float* sb, int scale_mode,

@@ -46,3 +46,18 @@ def test_no_device_fails_loudly():
     assert b"no CUDA device" in L.sb_last_error()
     with pytest.raises(A.SBError):
         A.handle(0)
+
+
+def test_lowprec_shim_exports_reference_api():
+    """liblowprec_b200.so serves the reference's lowprec:: signatures (INTEGRATION.md option A)."""
+    import subprocess
+
+    shim = os.path.join(os.path.dirname(A.LIB_PATH), "liblowprec_b200.so")
+    if not os.path.exists(shim):
+        pytest.skip("shim not built")
+    syms = subprocess.run(["nm", "-DC", "--defined-only", shim], capture_output=True, text=True).stdout
+    for name in ["lowprec::quantize_rowwise(lowprec::Matrix const&)", "lowprec::quantize_tensorwise_transpose(",
+                 "lowprec::int8_matmul_dequant(", "lowprec::matmul_dequant_dual_rowwise(", "lowprec::linear_forward(",
+                 "lowprec::linear_backward(", "lowprec::optimizer_step(", "lowprec::dequantize(",
+                 "lowprec::quantize_fp8(", "lowprec::matmul("]:
+        assert name in syms, name
