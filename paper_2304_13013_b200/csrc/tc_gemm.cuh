@@ -92,6 +92,17 @@ struct KindTraits<KIND_BF16> {
   static constexpr int K_PER_STAGE = 64;  // 64 bf16 = 128 B of K per stage
 };
 
+#ifdef SB_GEMM_PROBE
+// Pipeline probe (tools/gemm_probe.cu only): per CTA {MMA waits on full, MMA waits on tempty,
+// MMA-loop cycles, producer waits on empty, epilogue waits on tfull, k-blocks}.
+extern __device__ unsigned long long g_probe[1024 * 6];  // defined in build/probe/probe_glue.cu
+#define SB_PROBE_T0() const long long sb_t0_ = clock64()
+#define SB_PROBE_ADD(slot) atomicAdd(&g_probe[blockIdx.x * 6 + (slot)], (unsigned long long)(clock64() - sb_t0_))
+#else
+#define SB_PROBE_T0()
+#define SB_PROBE_ADD(slot)
+#endif
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -180,7 +191,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int m0, n0, kb0, kb1;
         unit_coords(p, t, k_blocks, m0, n0, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
-          sbptx::mbar_wait(&empty_bar[stage], phase ^ 1u);
+          {
+            SB_PROBE_T0();
+            sbptx::mbar_wait(&empty_bar[stage], phase ^ 1u);
+            SB_PROBE_ADD(3);
+          }
           sbptx::mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
           uint8_t* sa_ = smem_a + stage * A_STAGE_BYTES;
           uint8_t* sb_ = smem_b + stage * B_STAGE_BYTES;
@@ -201,16 +216,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
+#ifdef SB_GEMM_PROBE
+      const long long sb_loop0 = clock64();
+#endif
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
-        sbptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1u);
+        {
+          SB_PROBE_T0();
+          sbptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1u);
+          SB_PROBE_ADD(1);
+        }
         sbptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         int m0_, n0_, kb0, kb1;
         unit_coords(p, t, k_blocks, m0_, n0_, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
-          sbptx::mbar_wait(&full_bar[stage], phase);
+          {
+            SB_PROBE_T0();
+            sbptx::mbar_wait(&full_bar[stage], phase);
+            SB_PROBE_ADD(0);
+          }
+#ifdef SB_GEMM_PROBE
+          atomicAdd(&g_probe[blockIdx.x * 6 + 5], 1ull);
+#endif
           sbptx::tc_fence_after();
           const uint32_t a_addr = sbptx::smem_u32(smem_a + stage * A_STAGE_BYTES);
           const uint32_t b_addr = sbptx::smem_u32(smem_b + stage * B_STAGE_BYTES);
@@ -233,6 +262,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         sbptx::mma_commit(&tfull_bar[acc]);
       }
+#ifdef SB_GEMM_PROBE
+      atomicAdd(&g_probe[blockIdx.x * 6 + 2], (unsigned long long)(clock64() - sb_loop0));
+#endif
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
@@ -263,7 +295,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         sa_d = static_cast<double>(s);
         fr = SB_COL ? s * p.post_scale : s * p.post_scale * sb_tensor;
       }
-      sbptx::mbar_wait(&tfull_bar[acc], acc_phase);
+      {
+        SB_PROBE_T0();
+        sbptx::mbar_wait(&tfull_bar[acc], acc_phase);
+        if (lane == 0 && warp == 4) SB_PROBE_ADD(4);
+      }
       sbptx::tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + half * 128;
 #pragma unroll 1

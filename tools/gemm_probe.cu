@@ -1,0 +1,66 @@
+// gemm_probe.cu — run one tcgen05 GEMM shape with the SB_GEMM_PROBE pipeline counters and print
+// where the MMA thread, the TMA producer and the epilogue spend their cycles.
+// build: see tools/build_probe.sh
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../include/switchback_b200.h"
+#include "../paper_2304_13013_b200/csrc/sb_internal.h"
+
+extern "C" void sb_probe_read(unsigned long long* out, int n);
+extern "C" void sb_probe_reset();
+
+int main(int argc, char** argv) {
+  const int64_t M = argc > 1 ? atoll(argv[1]) : 65792, N = argc > 2 ? atoll(argv[2]) : 5120,
+                K = argc > 3 ? atoll(argv[3]) : 1280;
+  const int kind = argc > 4 ? atoi(argv[4]) : 0;  // 0 int8 fwd, 1 bf16 dW (M=m, N=n, K=T)
+  sb_handle h;
+  if (sb_create(0, &h) != SB_OK) {
+    printf("no device: %s\n", sb_last_error());
+    return 1;
+  }
+  void *a, *b, *sa, *sbv, *out;
+  const size_t esz = kind == 0 ? 1 : 2;
+  cudaMalloc(&a, (kind == 0 ? M : K) * (kind == 0 ? K : M) * esz);
+  cudaMalloc(&b, (kind == 0 ? N : K) * (kind == 0 ? K : N) * esz);
+  cudaMalloc(&sa, M * 4);
+  cudaMalloc(&sbv, 4);
+  cudaMalloc(&out, M * N * 4);
+  cudaMemset(a, 1, (kind == 0 ? M * K : K * M) * esz);
+  cudaMemset(b, 1, (kind == 0 ? N * K : K * N) * esz);
+  std::vector<float> ones(M, 1.0f);
+  cudaMemcpy(sa, ones.data(), M * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(sbv, ones.data(), 4, cudaMemcpyHostToDevice);
+  auto run = [&] {
+    if (kind == 0)
+      return sb_gemm_i8(h, (int8_t*)a, (float*)sa, (int8_t*)b, (float*)sbv, SB_SCALE_ROW_TENSOR, M, N, K, out, SB_BF16, 0);
+    return sb_wgrad(h, a, b, SB_BF16, K, M, N, (float*)out, 0, 0);
+  };
+  for (int i = 0; i < 3; ++i) run();
+  cudaDeviceSynchronize();
+  sb_probe_reset();
+  cudaEvent_t s, e;
+  cudaEventCreate(&s);
+  cudaEventCreate(&e);
+  cudaEventRecord(s);
+  sb_status st = run();
+  cudaEventRecord(e);
+  cudaDeviceSynchronize();
+  float ms;
+  cudaEventElapsedTime(&ms, s, e);
+  std::vector<unsigned long long> p(148 * 6);
+  sb_probe_read(p.data(), 148 * 6);
+  double sums[6] = {0};
+  for (int c = 0; c < 148; ++c)
+    for (int j = 0; j < 6; ++j) sums[j] += p[c * 6 + j];
+  const double ops = 2.0 * M * N * K;
+  printf("M=%lld N=%lld K=%lld kind=%d status=%d  %.1f us  %.0f T(FL)OPS\n", (long long)M, (long long)N, (long long)K, kind,
+         st, ms * 1e3, ops / (ms * 1e-3) / 1e12);
+  printf("per CTA avg (cycles): mma-loop %.0f | mma wait full %.0f | mma wait tempty %.0f | producer wait empty %.0f |"
+         " epi(w4) wait tfull %.0f | k-blocks %.1f\n",
+         sums[2] / 148, sums[0] / 148, sums[1] / 148, sums[3] / 148, sums[4] / 148, sums[5] / 148);
+  printf("MMA busy fraction of loop ~ %.2f (ideal cycles = kblocks*4*128 = %.0f)\n",
+         (sums[5] / 148 * 512) / (sums[2] / 148), sums[5] / 148 * 512);
+  return 0;
+}
