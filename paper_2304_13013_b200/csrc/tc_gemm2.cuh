@@ -146,7 +146,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const int am0 = m0 + static_cast<int>(rank) * BM;         // this CTA's A rows
         const int bn0 = n0 + static_cast<int>(rank) * (BN / 2);   // this CTA's half of B
         for (int kb = kb0; kb < kb1; ++kb) {
-          sbptx::mbar_wait(&empty_bar[stage], phase ^ 1u);
+          { SB_PROBE_T0(); sbptx::mbar_wait(&empty_bar[stage], phase ^ 1u); SB_PROBE_ADD(3); }
           if (rank == 0)
             sbptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * STAGE2_BYTES);
           else
@@ -185,13 +185,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       for (int u = pair; u < num_units; u += npairs, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
-        sbptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1u);
+        { SB_PROBE_T0(); sbptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1u); SB_PROBE_ADD(1); }
         sbptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         int m0_, n0_, kb0, kb1;
         unit2(p, u, k_blocks, m0_, n0_, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
-          sbptx::mbar_wait(&full_bar[stage], phase);
+          { SB_PROBE_T0(); sbptx::mbar_wait(&full_bar[stage], phase); SB_PROBE_ADD(0); }
+#ifdef SB_GEMM_PROBE
+          atomicAdd(&g_probe[blockIdx.x * 6 + 5], 1ull);
+#endif
           sbptx::tc_fence_after();
           const uint32_t a_addr = sbptx::smem_u32(smem_a + stage * A2_BYTES);
           const uint32_t b_addr = sbptx::smem_u32(smem_b + stage * B2_BYTES);
@@ -236,7 +239,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         sa_d = static_cast<double>(s);
         fr = SB_COL ? s * p.post_scale : s * p.post_scale * sb_tensor;
       }
-      sbptx::mbar_wait(&tfull_bar[acc], acc_phase);
+      { SB_PROBE_T0(); sbptx::mbar_wait(&tfull_bar[acc], acc_phase); if (lane == 0 && warp == 4) SB_PROBE_ADD(4); }
       sbptx::tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + half * 128;
 #pragma unroll 1
