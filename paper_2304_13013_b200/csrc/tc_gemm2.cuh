@@ -26,7 +26,7 @@ constexpr int A2_BYTES = 16384;  // per CTA: 128 rows x 128 B (K-major) | 64 k-r
 constexpr int B2_BYTES = 16384;  // per CTA: half of B, same geometry
 constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
 constexpr int BM2 = 256;         // tile rows per CTA pair
-constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + EPI_WARPS * EPI_BUF_BYTES + BN * 4 + 1024 + 256;
+constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + EPI_WARPS * EPI_BUF_BYTES + BN * 4 + 1024 + 512;
 static_assert(SMEM2_BYTES <= MAX_DYN_SMEM, "shared memory budget");
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // clears the CTA-rank bit of a shared::cluster address
 
@@ -55,6 +55,16 @@ __device__ __forceinline__ void commit_mc(uint64_t* bar) {
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           sbptx::smem_u32(bar)),
       "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+// wait with cluster-scope acquire (the arrival comes from the peer CTA)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAITC_%=;\n\t}\n" ::"r"(sbptx::smem_u32(bar)),
+      "r"(parity)
       : "memory");
 }
 template <int KIND>
@@ -99,7 +109,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty_bar = full_bar + STAGES2;
   uint64_t* tfull_bar = empty_bar + STAGES2;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* pfull_bar = tempty_bar + 2;  // leader: "peer's stage landed" (relayed)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pfull_bar + STAGES2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -114,8 +125,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     sbptx::tma_prefetch_desc(&tmB);
     sbptx::tma_prefetch_desc(&tmD);
     for (int s = 0; s < STAGES2; ++s) {
-      sbptx::mbar_init(&full_bar[s], 2);
+      sbptx::mbar_init(&full_bar[s], 1);
       sbptx::mbar_init(&empty_bar[s], 1);
+      sbptx::mbar_init(&pfull_bar[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       sbptx::mbar_init(&tfull_bar[a], 1);
@@ -147,23 +159,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const int bn0 = n0 + static_cast<int>(rank) * (BN / 2);   // this CTA's half of B
         for (int kb = kb0; kb < kb1; ++kb) {
           { SB_PROBE_T0(); sbptx::mbar_wait(&empty_bar[stage], phase ^ 1u); SB_PROBE_ADD(3); }
-          if (rank == 0)
-            sbptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * STAGE2_BYTES);
-          else
-            arrive_leader(&full_bar[stage]);
+          // each CTA's loads complete on its OWN full barrier (plain 1-CTA TMA); the peer's
+          // warp 1 relays completion to the leader (pfull) with one remote arrive
+          sbptx::mbar_arrive_expect_tx(&full_bar[stage], STAGE2_BYTES);
           uint8_t* sa_ = smem_a + stage * A2_BYTES;
           uint8_t* sb_ = smem_b + stage * B2_BYTES;
           if (A_MN) {
-            tma_load_2sm(&tmA, &full_bar[stage], sa_, am0, kb * 64);
-            tma_load_2sm(&tmA, &full_bar[stage], sa_ + 8192, am0 + 64, kb * 64);
+            sbptx::tma_load_2d(&tmA, &full_bar[stage], sa_, am0, kb * 64);
+            sbptx::tma_load_2d(&tmA, &full_bar[stage], sa_ + 8192, am0 + 64, kb * 64);
           } else {
-            tma_load_2sm(&tmA, &full_bar[stage], sa_, kb * KPS, am0);
+            sbptx::tma_load_2d(&tmA, &full_bar[stage], sa_, kb * KPS, am0);
           }
           if (B_MN) {
-            tma_load_2sm(&tmB, &full_bar[stage], sb_, bn0, kb * 64);
-            tma_load_2sm(&tmB, &full_bar[stage], sb_ + 8192, bn0 + 64, kb * 64);
+            sbptx::tma_load_2d(&tmB, &full_bar[stage], sb_, bn0, kb * 64);
+            sbptx::tma_load_2d(&tmB, &full_bar[stage], sb_ + 8192, bn0 + 64, kb * 64);
           } else {
-            tma_load_2sm(&tmB, &full_bar[stage], sb_, kb * KPS, bn0);
+            sbptx::tma_load_2d(&tmB, &full_bar[stage], sb_, kb * KPS, bn0);
           }
           if (++stage == STAGES2) {
             stage = 0;
@@ -174,6 +185,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------- MMA issue (leader only)
+    if (rank == 1 && lane == 0) {
+      // relay: the peer's stage s landed -> arrive on the leader's pfull[s]
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = pair; u < num_units; u += npairs) {
+        int m0_, n0_, kb0, kb1;
+        unit2(p, u, k_blocks, m0_, n0_, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          sbptx::mbar_wait(&full_bar[stage], phase);
+          arrive_leader(&pfull_bar[stage]);
+          if (++stage == STAGES2) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
     if (rank == 0 && lane == 0) {
       const uint32_t base = KIND == KIND_F8 ? idesc_runtime : KindTraits<KIND>::IDESC;
       // M = 256 for the pair: m_dim field = 256 >> 4
@@ -191,7 +219,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         int m0_, n0_, kb0, kb1;
         unit2(p, u, k_blocks, m0_, n0_, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
-          { SB_PROBE_T0(); sbptx::mbar_wait(&full_bar[stage], phase); SB_PROBE_ADD(0); }
+          {
+            SB_PROBE_T0();
+            sbptx::mbar_wait(&full_bar[stage], phase);
+            mbar_wait_cluster(&pfull_bar[stage], phase);
+            SB_PROBE_ADD(0);
+          }
 #ifdef SB_GEMM_PROBE
           atomicAdd(&g_probe[blockIdx.x * 6 + 5], 1ull);
 #endif
