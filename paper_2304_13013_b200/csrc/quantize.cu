@@ -171,7 +171,7 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
 // the nearest integer and leaves it (two's complement) in the low byte of m; the residual
 // r = qs - (m - 1.5*2^23) is exact. The candidate can only differ from the reference's
 // round-half-away of the exact 127x/s when |r| is within ~2^-16 of 1/2, so a warp with any
-// |r| > 1/2 - 2^-12 in the vector re-derives the vector with the exact comparison
+// |r| > 1/2 - 2^-15 in the vector re-derives the vector with the exact comparison
 // (q_magnitude). Bytes are packed with PRMT.
 template <typename T>
 struct Unpack;
@@ -220,7 +220,8 @@ __device__ __forceinline__ typename VecQ<T>::Out qvec(const uint4& v, const Scal
     rmax = fmaxf(rmax, fabsf(r));
     u[i] = __float_as_uint(m);
   }
-  const bool near = !plain || rmax > 0.499755859375f;  // within 2^-12 of a half-integer
+  // |qs - 127x/s| <= 127 * 2^-23 < 2^-16: only residuals within 2^-15 of 1/2 can round differently
+  const bool near = !plain || rmax > 0.499969482421875f;  // 1/2 - 2^-15
   if (__any_sync(0xffffffffu, near)) {
 #pragma unroll
     for (int i = 0; i < N; ++i)
@@ -233,7 +234,7 @@ __device__ __forceinline__ typename VecQ<T>::Out qvec(const uint4& v, const Scal
   }
 }
 
-constexpr int kQWarps = 8;                     // consumer warps per block
+constexpr int kQWarps = 12;                    // consumer warps per block (2 blocks / SM)
 constexpr int kQThreads = 32 * (kQWarps + 1);  // + 1 producer warp
 constexpr int kQRingBytes = 100 * 1024;
 
