@@ -279,9 +279,13 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_rowwise_tma(const T* __r
     return;
   }
   const int nvec = static_cast<int>(cols / VEC);
+  // A consumer must never wait on a slot more than one phase ahead (try_wait.parity on the
+  // previous parity returns at once), so at most `stages` consumers take part.
+  const int active = kQWarps < stages ? kQWarps : stages;
+  if (warp >= active) return;
   int i = warp;
   for (int64_t row = blockIdx.x + static_cast<int64_t>(warp) * gridDim.x; row < rows;
-       row += static_cast<int64_t>(kQWarps) * gridDim.x, i += kQWarps) {
+       row += static_cast<int64_t>(active) * gridDim.x, i += active) {
     const int s = i % stages;
     const uint32_t ph = static_cast<uint32_t>(i / stages) & 1u;
     sbptx::mbar_wait(&full[s], ph);

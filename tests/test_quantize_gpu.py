@@ -9,7 +9,8 @@ from tests._util import adversarial, bf16, dev, fp8_decode, host
 
 pytestmark = pytest.mark.gpu
 
-SHAPES = [(1, 1), (3, 5), (13, 70), (7, 8), (64, 1024), (37, 1280), (33, 5120), (9, 8200), (5, 16384), (2, 40000)]
+SHAPES = [(1, 1), (3, 5), (13, 70), (7, 8), (64, 1024), (37, 1280), (33, 5120), (9, 8200), (5, 16384), (2, 40000),
+          (2000, 5120), (700, 10240), (4000, 1280)]  # many rows per block: ring wrap-around with few stages
 
 
 @pytest.mark.parametrize("shape", SHAPES)
