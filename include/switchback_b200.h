@@ -80,6 +80,11 @@ uint32_t* sb_error_word(sb_handle h);
 const char* sb_last_error(void);
 /* Kernel launches issued through this handle so far (launch accounting for bench.py). */
 uint64_t sb_launch_count(sb_handle h);
+/* Tensor-core GEMM tiling for this handle (no reference counterpart: a B200 tuning knob).
+ * SB_GEMM_AUTO: 2-CTA (cta_group::2) 256 x 256 tiles when the problem fills the SM pairs,
+ * else 1-CTA 128 x 256; the other values force one form (results are identical). */
+typedef enum sb_gemm_path { SB_GEMM_AUTO = 0, SB_GEMM_1CTA = 1, SB_GEMM_2CTA = 2 } sb_gemm_path;
+sb_status sb_set_gemm_path(sb_handle h, int path);
 
 /* Device memory + synchronous copies on the handle's stream (for FFI callers without a CUDA runtime). */
 sb_status sb_device_alloc(sb_handle h, size_t bytes, void** out);

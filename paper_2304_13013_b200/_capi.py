@@ -22,6 +22,7 @@ SB_STANDARD, SB_SWITCHBACK, SB_SWITCHBACK_M, SB_SWITCHBACK_Q, SB_ALLQUANT = rang
 SB_INT8, SB_FP8 = range(2)
 SB_SCALE_ROW_TENSOR, SB_SCALE_ROW_ROW, SB_SCALE_NONE = range(3)
 SB_CLIP_NONE, SB_CLIP_UPDATE, SB_CLIP_GRAD = range(3)
+SB_GEMM_AUTO, SB_GEMM_1CTA, SB_GEMM_2CTA = range(3)
 
 # every symbol include/switchback_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = [
@@ -32,6 +33,7 @@ EXPORTS = [
     "sb_linear_backward", "sb_switchback_fwd_bwd_host", "sb_stableadamw_workspace_size", "sb_stableadamw_step",
     "sb_device_alloc", "sb_device_free", "sb_copy_to_device", "sb_copy_to_host", "sb_check_finite", "sb_fp8_cast",
     "sb_transpose_i8", "sb_compute_rms", "sb_grad_clip_global_norm", "sb_filter_nonfinite", "sb_dequantize_values",
+    "sb_set_gemm_path",
 ]
 
 
@@ -96,6 +98,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             "sb_error_word": ([v], v),
             "sb_last_error": ([], C.c_char_p),
             "sb_launch_count": ([v], C.c_uint64),
+            "sb_set_gemm_path": ([v, i32], i32),
             "sb_quantize_rowwise": ([v, v, i32, i64, i64, i64, v, i64, v], i32),
             "sb_quantize_columnwise": ([v, v, i32, i64, i64, i64, v, i64, v, i64, v], i32),
             "sb_quantize_tensorwise": ([v, v, i32, i64, i64, i64, v, i64, v, i64, v], i32),
@@ -161,6 +164,10 @@ class Handle:
 
     def launches(self) -> int:
         return int(self.lib.sb_launch_count(self.h))
+
+    def set_gemm_path(self, path: int) -> None:
+        """SB_GEMM_AUTO / SB_GEMM_1CTA / SB_GEMM_2CTA (tiling only; results are identical)."""
+        check(self.lib.sb_set_gemm_path(self.h, path))
 
     def __del__(self):
         try:

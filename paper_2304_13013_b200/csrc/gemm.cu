@@ -164,29 +164,36 @@ struct Operand {
   uint32_t kbox;  // K-major: elements per 128-byte K slice (128 for 8-bit, 64 for bf16)
 };
 
-bool encode_operand(CUtensorMap* m, const Operand& o, uint32_t rows) {
-  if (o.mn) return sb::encode_tmap_2d(m, o.dt, o.ptr, o.inner, o.outer, o.stride_bytes, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B);
+// rows: box rows of a K-major operand; mn_krows: k-rows per box of an MN-major one.
+bool encode_operand(CUtensorMap* m, const Operand& o, uint32_t rows, uint32_t mn_krows) {
+  if (o.mn)
+    return sb::encode_tmap_2d(m, o.dt, o.ptr, o.inner, o.outer, o.stride_bytes, 64, mn_krows, CU_TENSOR_MAP_SWIZZLE_128B);
   return sb::encode_tmap_2d(m, o.dt, o.ptr, o.inner, o.outer, o.stride_bytes, o.kbox, rows, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-// 1-CTA 128 x 256 tiles by default; SB_GEMM_2CTA=1 selects the cta_group::2 256 x 256 kernel
-// (tc_gemm2.cuh: bit-exact, but its 2-SM TMA feed currently runs at ~half the 1-CTA rate —
-// see DESIGN.md "open items").
-bool use_2cta(sb_handle h) {
-  static int env = -1;
-  if (env < 0) {
+// 2-CTA (cta_group::2, 256 x 256 tiles, tc_gemm2.cuh) whenever the problem has at least one
+// 256-row tile per SM pair's worth of work; 1-CTA 128 x 256 (tc_gemm.cuh) for small M.
+// SB_GEMM_2CTA=0/1 in the environment overrides the AUTO choice; sb_set_gemm_path overrides both.
+bool use_2cta(sb_handle h, int64_t M, int64_t units256) {
+  if (h->gemm_path == SB_GEMM_1CTA || h->num_sms < 2) return false;
+  if (h->gemm_path == SB_GEMM_2CTA) return true;
+  static int env = -2;
+  if (env == -2) {
     const char* e = getenv("SB_GEMM_2CTA");
-    env = (e && e[0] == '1') ? 1 : 0;
+    env = e ? (e[0] == '1' ? 1 : 0) : -1;
   }
-  return env == 1 && h->num_sms >= 2;
+  if (env >= 0) return env == 1;
+  return M > 128 && units256 >= h->num_sms / 2;
 }
 
 template <int KIND, int OUT, bool A_MN = false, bool B_MN = false, bool SB_COL = false>
 cudaError_t launch_tc(sb_handle h, const Operand& A, const Operand& B, const CUtensorMap& d, sbtc::Params p,
                       uint32_t idesc) {
-  const bool two = use_2cta(h);
+  const int64_t units256 = ((p.M + 255) / 256) * ((p.N + sbtc::BN - 1) / sbtc::BN) * (p.splits < 1 ? 1 : p.splits);
+  const bool two = use_2cta(h, p.M, units256);
   CUtensorMap ta, tb;
-  if (!encode_operand(&ta, A, 128) || !encode_operand(&tb, B, two ? 128 : 256)) return cudaErrorInvalidValue;
+  if (!encode_operand(&ta, A, 128, two ? 128 : 64) || !encode_operand(&tb, B, two ? 128 : 256, two ? 128 : 64))
+    return cudaErrorInvalidValue;
   p.tiles_m = static_cast<int>((p.M + (two ? sbtc2::BM2 : sbtc::BM) - 1) / (two ? sbtc2::BM2 : sbtc::BM));
   p.tiles_n = static_cast<int>((p.N + sbtc::BN - 1) / sbtc::BN);
   if (p.splits < 1) p.splits = 1;
@@ -364,7 +371,7 @@ sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t 
     // Split K (= tokens) in two when the output has too few tiles to fill the SMs (pairs) in
     // whole waves: both halves reduce-add into a zeroed dW, and 0 + a + b == 0 + b + a, so the
     // result stays deterministic (more splits would make the fp32 sum order-dependent).
-    const bool two = use_2cta(h);
+    const bool two = use_2cta(h, m, ((m + 255) / 256) * ((n + 255) / 256));
     const int tm = static_cast<int>((m + (two ? 256 : 128) - 1) / (two ? 256 : 128));
     const int tiles = tm * static_cast<int>((n + 255) / 256);
     const int slots = two ? h->num_sms / 2 : h->num_sms;

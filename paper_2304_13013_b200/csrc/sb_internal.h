@@ -16,6 +16,7 @@ struct sb_handle_s {
   unsigned int* d_scratch = nullptr;  // small scratch (tensor absmax words etc.)
   size_t scratch_bytes = 0;
   uint64_t launches = 0;
+  int gemm_path = 0;  // sb_gemm_path
   // host-buffer pipeline (sb_switchback_fwd_bwd_host)
   cudaStream_t aux_stream = nullptr;
   void* dev_pool = nullptr;

@@ -141,6 +141,123 @@ __device__ __forceinline__ void stage_row128(uint8_t* buf, int lane, const uint3
   }
 }
 
+// Arrive on the cluster leader's copy of a barrier (the same smem offset in CTA rank 0).
+__device__ __forceinline__ void arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(sbptx::smem_u32(bar) & 0xFEFFFFFFu)
+               : "memory");
+}
+
+// Drain this CTA's 128 x 256 accumulator (TMEM lane quarter `ew`, column half `half`) to D:
+// tcgen05.ld -> scale / convert in registers -> SW128 smem staging -> TMA store (or reduce-add).
+// Rows [rm0, rm0 + 128) of D; the TMEM buffer is handed back (`tempty`, on the leader CTA's
+// barrier when TWO) as soon as it is drained into registers.
+template <int KIND, int OUT, bool SB_COL, bool TWO>
+__device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap* tmD, uint32_t t_row, uint64_t* tempty,
+                                              int rm0, int n0, int ew, int half, int lane, uint8_t* buf, const float* cs,
+                                              float fr, double sa_d, float sb_tensor) {
+#pragma unroll 1
+  for (int pr = 0; pr < 2; ++pr) {  // two 64-column pairs per warp
+    uint32_t r0[32], r1[32];
+    sbptx::tmem_ld_32x32b_x32(t_row + pr * 64, r0);
+    sbptx::tmem_ld_32x32b_x32(t_row + pr * 64 + 32, r1);
+    sbptx::tmem_ld_wait();
+    if (pr == 1) {
+      // accumulator fully drained into registers: hand TMEM back to the MMA warp
+      sbptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (TWO)
+          arrive_leader(tempty);
+        else
+          sbptx::mbar_arrive(tempty);
+      }
+    }
+    const int cl = half * 128 + pr * 64;  // column within tile
+    const int col0 = n0 + cl;
+    if (col0 >= p.N || rm0 >= p.M) continue;  // whole pair outside D (warp-uniform)
+    if (OUT == OUT_BF16) {
+      uint32_t w[32];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        float a0, a1, b0, b1;
+        if (KIND == KIND_I8) {
+          a0 = static_cast<float>(static_cast<int32_t>(r0[2 * j]));
+          a1 = static_cast<float>(static_cast<int32_t>(r0[2 * j + 1]));
+          b0 = static_cast<float>(static_cast<int32_t>(r1[2 * j]));
+          b1 = static_cast<float>(static_cast<int32_t>(r1[2 * j + 1]));
+        } else {
+          a0 = __uint_as_float(r0[2 * j]);
+          a1 = __uint_as_float(r0[2 * j + 1]);
+          b0 = __uint_as_float(r1[2 * j]);
+          b1 = __uint_as_float(r1[2 * j + 1]);
+        }
+        if (SB_COL) {
+          a0 *= fr * cs[cl + 2 * j];
+          a1 *= fr * cs[cl + 2 * j + 1];
+          b0 *= fr * cs[cl + 32 + 2 * j];
+          b1 *= fr * cs[cl + 32 + 2 * j + 1];
+        } else {
+          a0 *= fr;
+          a1 *= fr;
+          b0 *= fr;
+          b1 *= fr;
+        }
+        w[j] = pack_bf16x2(a0, a1);
+        w[16 + j] = pack_bf16x2(b0, b1);
+      }
+      if (lane == 0) sbptx::tma_store_wait_read<0>();  // previous store done reading buf
+      __syncwarp();
+      stage_row128(buf, lane, w);  // 64 bf16 = 128 B per row
+      sbptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        sbptx::tma_store_2d(tmD, buf, col0, rm0 + ew * 32);
+        sbptx::tma_store_commit();
+      }
+    } else {
+#pragma unroll
+      for (int sub = 0; sub < 2; ++sub) {
+        const uint32_t(&r)[32] = sub ? r1 : r0;
+        const int cc = cl + sub * 32;
+        if (n0 + cc >= p.N) break;
+        uint32_t w[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (OUT == OUT_I32 || OUT == OUT_F32_RAW || OUT == OUT_F32_RAW_ADD) {
+            w[j] = r[j];
+          } else if (OUT == OUT_F32_EXACT) {
+            const float sbj = SB_COL ? cs[cc + j] : sb_tensor;
+            const double d = __ddiv_rn(
+                __dmul_rn(__dmul_rn(static_cast<double>(static_cast<int32_t>(r[j])), sa_d), static_cast<double>(sbj)),
+                16129.0);
+            w[j] = __float_as_uint(__double2float_rn(d));
+          } else {
+            const float v = KIND == KIND_I8 ? static_cast<float>(static_cast<int32_t>(r[j])) : __uint_as_float(r[j]);
+            w[j] = __float_as_uint(SB_COL ? v * (fr * cs[cc + j]) : v * fr);
+          }
+        }
+        if (lane == 0) sbptx::tma_store_wait_read<0>();
+        __syncwarp();
+        stage_row128(buf, lane, w);  // 32 x 4 B = 128 B per row
+        sbptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (OUT == OUT_F32_RAW_ADD) {
+            asm volatile(
+                "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                    reinterpret_cast<uint64_t>(tmD)),
+                "r"(sbptx::smem_u32(buf)), "r"(n0 + cc), "r"(rm0 + ew * 32)
+                : "memory");
+          } else {
+            sbptx::tma_store_2d(tmD, buf, n0 + cc, rm0 + ew * 32);
+          }
+          sbptx::tma_store_commit();
+        }
+      }
+    }
+  }
+}
+
 template <int KIND, bool A_MN, bool B_MN, int OUT, bool SB_COL>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -302,102 +419,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       sbptx::tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + half * 128;
-#pragma unroll 1
-      for (int pr = 0; pr < 2; ++pr) {  // two 64-column pairs per warp
-        uint32_t r0[32], r1[32];
-        sbptx::tmem_ld_32x32b_x32(t_row + pr * 64, r0);
-        sbptx::tmem_ld_32x32b_x32(t_row + pr * 64 + 32, r1);
-        sbptx::tmem_ld_wait();
-        if (pr == 1) {
-          // accumulator fully drained into registers: hand TMEM back to the MMA warp
-          sbptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) sbptx::mbar_arrive(&tempty_bar[acc]);
-        }
-        const int cl = half * 128 + pr * 64;  // column within tile
-        const int col0 = n0 + cl;
-        if (col0 >= p.N) continue;  // whole pair outside D (warp-uniform)
-        if (OUT == OUT_BF16) {
-          uint32_t w[32];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            float a0, a1, b0, b1;
-            if (KIND == KIND_I8) {
-              a0 = static_cast<float>(static_cast<int32_t>(r0[2 * j]));
-              a1 = static_cast<float>(static_cast<int32_t>(r0[2 * j + 1]));
-              b0 = static_cast<float>(static_cast<int32_t>(r1[2 * j]));
-              b1 = static_cast<float>(static_cast<int32_t>(r1[2 * j + 1]));
-            } else {
-              a0 = __uint_as_float(r0[2 * j]);
-              a1 = __uint_as_float(r0[2 * j + 1]);
-              b0 = __uint_as_float(r1[2 * j]);
-              b1 = __uint_as_float(r1[2 * j + 1]);
-            }
-            if (SB_COL) {
-              a0 *= fr * cs[cl + 2 * j];
-              a1 *= fr * cs[cl + 2 * j + 1];
-              b0 *= fr * cs[cl + 32 + 2 * j];
-              b1 *= fr * cs[cl + 32 + 2 * j + 1];
-            } else {
-              a0 *= fr;
-              a1 *= fr;
-              b0 *= fr;
-              b1 *= fr;
-            }
-            w[j] = pack_bf16x2(a0, a1);
-            w[16 + j] = pack_bf16x2(b0, b1);
-          }
-          if (lane == 0) sbptx::tma_store_wait_read<0>();  // previous store done reading buf
-          __syncwarp();
-          stage_row128(buf, lane, w);  // 64 bf16 = 128 B per row
-          sbptx::fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            sbptx::tma_store_2d(&tmD, buf, col0, m0 + ew * 32);
-            sbptx::tma_store_commit();
-          }
-        } else {
-#pragma unroll
-          for (int sub = 0; sub < 2; ++sub) {
-            const uint32_t(&r)[32] = sub ? r1 : r0;
-            const int cc = cl + sub * 32;
-            if (n0 + cc >= p.N) break;
-            uint32_t w[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (OUT == OUT_I32 || OUT == OUT_F32_RAW || OUT == OUT_F32_RAW_ADD) {
-                w[j] = r[j];
-              } else if (OUT == OUT_F32_EXACT) {
-                const float sbj = SB_COL ? cs[cc + j] : sb_tensor;
-                const double d = __ddiv_rn(
-                    __dmul_rn(__dmul_rn(static_cast<double>(static_cast<int32_t>(r[j])), sa_d), static_cast<double>(sbj)),
-                    16129.0);
-                w[j] = __float_as_uint(__double2float_rn(d));
-              } else {
-                const float v = KIND == KIND_I8 ? static_cast<float>(static_cast<int32_t>(r[j])) : __uint_as_float(r[j]);
-                w[j] = __float_as_uint(SB_COL ? v * (fr * cs[cc + j]) : v * fr);
-              }
-            }
-            if (lane == 0) sbptx::tma_store_wait_read<0>();
-            __syncwarp();
-            stage_row128(buf, lane, w);  // 32 x 4 B = 128 B per row
-            sbptx::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              if (OUT == OUT_F32_RAW_ADD) {
-                asm volatile(
-                    "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                        reinterpret_cast<uint64_t>(&tmD)),
-                    "r"(sbptx::smem_u32(buf)), "r"(n0 + cc), "r"(m0 + ew * 32)
-                    : "memory");
-              } else {
-                sbptx::tma_store_2d(&tmD, buf, n0 + cc, m0 + ew * 32);
-              }
-              sbptx::tma_store_commit();
-            }
-          }
-        }
-      }
+      epilogue_tile<KIND, OUT, SB_COL, false>(p, &tmD, t_row, &tempty_bar[acc], m0, n0, ew, half, lane, buf, cs, fr,
+                                             sa_d, sb_tensor);
     }
     if (lane == 0) sbptx::tma_store_wait_all<0>();
   }

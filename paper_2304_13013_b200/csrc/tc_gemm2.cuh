@@ -1,16 +1,21 @@
-// tc_gemm2.cuh — the 2-CTA (cta_group::2) form of the persistent tcgen05 GEMM.
+// tc_gemm2.cuh — the 2-CTA (cta_group::2) form of the persistent tcgen05 GEMM, the default
+// for every GEMM big enough to fill the SM pairs.
 //
 // A cluster of two CTAs on one TPC computes a 256 x 256 tile: CTA r loads its 128 rows of A
 // and 128 of the 256 rows/cols of B; the leader (rank 0) issues tcgen05.mma.cta_group::2
 // (M = 256), which reads A and B from both CTAs' shared memory and writes rows 0-127 of the
-// accumulator to the leader's TMEM and rows 128-255 to the peer's. Per SM this halves the
-// shared-memory operand bytes per MMA and the L2->SM operand traffic per flop relative to
-// the 1-CTA 128 x 256 kernel (tc_gemm.cuh), and the 6-stage ring (32 KB / stage / CTA)
-// doubles the K-depth in flight.
+// accumulator to the leader's TMEM and rows 128-255 to the peer's. Per SM this cuts the
+// L2 -> SMEM operand bytes per MMA from 48 KB to 32 KB per 128-byte K slice.
+//
+// Stages are 256 bytes of K deep (int8: 256 elements, bf16: 128) = 64 KB per CTA, 3 stages.
+// The deep stage is the point: every stage costs the single producer / MMA threads a fixed
+// ~500-700 cycles of mbarrier + TMA-issue latency (measured, tools/feed_bench.cu), so a
+// 128-byte stage (512 MMA cycles) starves the tensor core while a 256-byte stage (1024 MMA
+// cycles) leaves it slack.
 //
 // Synchronisation (all mbarriers live at the same smem offsets in both CTAs):
-//   full[s]   leader-only: 2 arrivals (leader arrive.expect_tx of both CTAs' bytes + the
-//             peer's remote arrive); both CTAs' TMA loads complete_tx on the leader's copy.
+//   full[s]   leader-only: one arrival (the leader's arrive.expect_tx of BOTH CTAs' bytes);
+//             both CTAs' TMA loads (.cta_group::2) complete_tx on the leader's copy.
 //   empty[s]  per CTA: the leader's tcgen05.commit multicasts the arrival to both CTAs.
 //   tfull[a]  per CTA: commit multicast when accumulator a is complete.
 //   tempty[a] leader-only: 2 x 8 epilogue-warp arrivals (peer warps arrive remotely).
@@ -21,14 +26,33 @@ namespace sbtc2 {
 
 using namespace sbtc;
 
-constexpr int STAGES2 = 6;
-constexpr int A2_BYTES = 16384;  // per CTA: 128 rows x 128 B (K-major) | 64 k-rows x 128 elem x 2 B (MN)
-constexpr int B2_BYTES = 16384;  // per CTA: half of B, same geometry
+constexpr int STAGES2 = 3;
+constexpr int ATOM_BYTES = 16384;              // 128 rows x 128 B (one SW128 box)
+constexpr int A2_BYTES = 2 * ATOM_BYTES;       // per CTA: 128 rows x 256 B of K
+constexpr int B2_BYTES = 2 * ATOM_BYTES;       // per CTA: its 128-row half of B
 constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
-constexpr int BM2 = 256;         // tile rows per CTA pair
-constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + EPI_WARPS * EPI_BUF_BYTES + BN * 4 + 1024 + 512;
+constexpr int BM2 = 256;                       // tile rows per CTA pair
+constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + EPI_WARPS * EPI_BUF_BYTES + BN * 4 + 1024 + 256;
 static_assert(SMEM2_BYTES <= MAX_DYN_SMEM, "shared memory budget");
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // clears the CTA-rank bit of a shared::cluster address
+
+template <int KIND>
+struct Kind2;
+template <>
+struct Kind2<KIND_I8> {
+  static constexpr int KPS = 256;  // K elements per stage
+  static constexpr int KATOM = 128;  // K elements per 128-byte atom
+};
+template <>
+struct Kind2<KIND_F8> {
+  static constexpr int KPS = 256;
+  static constexpr int KATOM = 128;
+};
+template <>
+struct Kind2<KIND_BF16> {
+  static constexpr int KPS = 128;
+  static constexpr int KATOM = 64;
+};
 
 __device__ __forceinline__ uint32_t cta_rank() {
   uint32_t r;
@@ -38,11 +62,7 @@ __device__ __forceinline__ uint32_t cta_rank() {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// arrive on the leader CTA's copy of a barrier (works from either CTA)
-__device__ __forceinline__ void arrive_leader(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(sbptx::smem_u32(bar) & kPeerMask)
-               : "memory");
-}
+// TMA load into this CTA's smem, completion counted on the LEADER's barrier.
 __device__ __forceinline__ void tma_load_2sm(const CUtensorMap* m, uint64_t* bar, void* dst, int32_t c0, int32_t c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
@@ -57,7 +77,7 @@ __device__ __forceinline__ void commit_mc(uint64_t* bar) {
       "h"(static_cast<uint16_t>(3))
       : "memory");
 }
-// wait with cluster-scope acquire (the arrival comes from the peer CTA)
+// wait with cluster-scope acquire (the arrivals come from the peer CTA too)
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P;\n"
@@ -86,6 +106,29 @@ __device__ __forceinline__ void mma2(uint32_t d, uint64_t a, uint64_t b, uint32_
                  : "memory");
 }
 
+// Load one operand's share of a stage: 128 rows (or MN columns) x 256 bytes of K as two
+// 16 KB SW128 boxes. K-major: boxes {KATOM elements, 128 rows} side by side along K.
+// MN-major: boxes {64 MN elements, 128 k-rows}, one per 64-wide MN chunk.
+template <bool MN, int KATOM>
+__device__ __forceinline__ void load2(const CUtensorMap* tm, uint64_t* bar, uint8_t* dst, int r0, int kb) {
+  if (MN) {
+    tma_load_2sm(tm, bar, dst, r0, kb * 128);
+    tma_load_2sm(tm, bar, dst + ATOM_BYTES, r0 + 64, kb * 128);
+  } else {
+    tma_load_2sm(tm, bar, dst, (2 * kb) * KATOM, r0);
+    tma_load_2sm(tm, bar, dst + ATOM_BYTES, (2 * kb + 1) * KATOM, r0);
+  }
+}
+
+// UMMA descriptor for MMA step kk (of 8) within a stage (one MMA consumes 32 bytes of K).
+//   K-major: step kk lives in atom kk/4 at byte column 32*(kk%4); SBO = 8 rows (1 KB).
+//   MN-major: one MMA = 16 k-rows = 2 KB down both MN chunks; LBO = MN-chunk stride (16 KB).
+template <bool MN>
+__device__ __forceinline__ uint64_t desc2(uint32_t base, int kk) {
+  return MN ? sbptx::umma_desc_sw128(base + kk * 2048, ATOM_BYTES, 1024)
+            : sbptx::umma_desc_sw128(base + (kk >> 2) * ATOM_BYTES + (kk & 3) * 32, 16, 1024);
+}
+
 // Work unit -> (m0 of the 256-row pair tile, n0, [kb0, kb1)).
 __device__ __forceinline__ void unit2(const Params& p, int u, int k_blocks, int& m0, int& n0, int& kb0, int& kb1) {
   const int t = u / p.splits, s = u - t * p.splits;
@@ -109,15 +152,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty_bar = full_bar + STAGES2;
   uint64_t* tfull_bar = empty_bar + STAGES2;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint64_t* pfull_bar = tempty_bar + 2;  // leader: "peer's stage landed" (relayed)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pfull_bar + STAGES2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int num_units = p.tiles_m * p.tiles_n * p.splits;
-  constexpr int KPS = KindTraits<KIND>::K_PER_STAGE;
+  constexpr int KPS = Kind2<KIND>::KPS;
   const int k_blocks = (p.K + KPS - 1) / KPS;
 
   if (warp == 0 && lane == 0) {
@@ -127,7 +169,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     for (int s = 0; s < STAGES2; ++s) {
       sbptx::mbar_init(&full_bar[s], 1);
       sbptx::mbar_init(&empty_bar[s], 1);
-      sbptx::mbar_init(&pfull_bar[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       sbptx::mbar_init(&tfull_bar[a], 1);
@@ -155,27 +196,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       for (int u = pair; u < num_units; u += npairs) {
         int m0, n0, kb0, kb1;
         unit2(p, u, k_blocks, m0, n0, kb0, kb1);
-        const int am0 = m0 + static_cast<int>(rank) * BM;         // this CTA's A rows
-        const int bn0 = n0 + static_cast<int>(rank) * (BN / 2);   // this CTA's half of B
+        const int am0 = m0 + static_cast<int>(rank) * BM;        // this CTA's A rows
+        const int bn0 = n0 + static_cast<int>(rank) * (BN / 2);  // this CTA's half of B
         for (int kb = kb0; kb < kb1; ++kb) {
           { SB_PROBE_T0(); sbptx::mbar_wait(&empty_bar[stage], phase ^ 1u); SB_PROBE_ADD(3); }
-          // each CTA's loads complete on its OWN full barrier (plain 1-CTA TMA); the peer's
-          // warp 1 relays completion to the leader (pfull) with one remote arrive
-          sbptx::mbar_arrive_expect_tx(&full_bar[stage], STAGE2_BYTES);
-          uint8_t* sa_ = smem_a + stage * A2_BYTES;
-          uint8_t* sb_ = smem_b + stage * B2_BYTES;
-          if (A_MN) {
-            sbptx::tma_load_2d(&tmA, &full_bar[stage], sa_, am0, kb * 64);
-            sbptx::tma_load_2d(&tmA, &full_bar[stage], sa_ + 8192, am0 + 64, kb * 64);
-          } else {
-            sbptx::tma_load_2d(&tmA, &full_bar[stage], sa_, kb * KPS, am0);
-          }
-          if (B_MN) {
-            sbptx::tma_load_2d(&tmB, &full_bar[stage], sb_, bn0, kb * 64);
-            sbptx::tma_load_2d(&tmB, &full_bar[stage], sb_ + 8192, bn0 + 64, kb * 64);
-          } else {
-            sbptx::tma_load_2d(&tmB, &full_bar[stage], sb_, kb * KPS, bn0);
-          }
+          if (rank == 0) sbptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * STAGE2_BYTES);
+          load2<A_MN, Kind2<KIND>::KATOM>(&tmA, &full_bar[stage], smem_a + stage * A2_BYTES, am0, kb);
+          load2<B_MN, Kind2<KIND>::KATOM>(&tmB, &full_bar[stage], smem_b + stage * B2_BYTES, bn0, kb);
           if (++stage == STAGES2) {
             stage = 0;
             phase ^= 1u;
@@ -185,23 +212,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------- MMA issue (leader only)
-    if (rank == 1 && lane == 0) {
-      // relay: the peer's stage s landed -> arrive on the leader's pfull[s]
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = pair; u < num_units; u += npairs) {
-        int m0_, n0_, kb0, kb1;
-        unit2(p, u, k_blocks, m0_, n0_, kb0, kb1);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          sbptx::mbar_wait(&full_bar[stage], phase);
-          arrive_leader(&pfull_bar[stage]);
-          if (++stage == STAGES2) {
-            stage = 0;
-            phase ^= 1u;
-          }
-        }
-      }
-    }
     if (rank == 0 && lane == 0) {
       const uint32_t base = KIND == KIND_F8 ? idesc_runtime : KindTraits<KIND>::IDESC;
       // M = 256 for the pair: m_dim field = 256 >> 4
@@ -210,21 +220,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
+#ifdef SB_GEMM_PROBE
+      const long long sb_loop0 = clock64();
+#endif
       for (int u = pair; u < num_units; u += npairs, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
-        { SB_PROBE_T0(); sbptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1u); SB_PROBE_ADD(1); }
+        { SB_PROBE_T0(); mbar_wait_cluster(&tempty_bar[acc], acc_phase ^ 1u); SB_PROBE_ADD(1); }
         sbptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         int m0_, n0_, kb0, kb1;
         unit2(p, u, k_blocks, m0_, n0_, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
-          {
-            SB_PROBE_T0();
-            sbptx::mbar_wait(&full_bar[stage], phase);
-            mbar_wait_cluster(&pfull_bar[stage], phase);
-            SB_PROBE_ADD(0);
-          }
+          { SB_PROBE_T0(); sbptx::mbar_wait(&full_bar[stage], phase); SB_PROBE_ADD(0); }
 #ifdef SB_GEMM_PROBE
           atomicAdd(&g_probe[blockIdx.x * 6 + 5], 1ull);
 #endif
@@ -232,8 +240,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           const uint32_t a_addr = sbptx::smem_u32(smem_a + stage * A2_BYTES);
           const uint32_t b_addr = sbptx::smem_u32(smem_b + stage * B2_BYTES);
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            mma2<KIND>(d_tmem, operand_desc<A_MN>(a_addr, k), operand_desc<B_MN>(b_addr, k), idesc, (kb != kb0) || k);
+          for (int kk = 0; kk < 8; ++kk)
+            mma2<KIND>(d_tmem, desc2<A_MN>(a_addr, kk), desc2<B_MN>(b_addr, kk), idesc, (kb != kb0) || kk);
           commit_mc(&empty_bar[stage]);
           if (++stage == STAGES2) {
             stage = 0;
@@ -242,6 +250,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
         commit_mc(&tfull_bar[acc]);
       }
+#ifdef SB_GEMM_PROBE
+      atomicAdd(&g_probe[blockIdx.x * 6 + 2], (unsigned long long)(clock64() - sb_loop0));
+#endif
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue (both CTAs)
@@ -275,101 +286,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       { SB_PROBE_T0(); sbptx::mbar_wait(&tfull_bar[acc], acc_phase); if (lane == 0 && warp == 4) SB_PROBE_ADD(4); }
       sbptx::tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + half * 128;
-#pragma unroll 1
-      for (int pr = 0; pr < 2; ++pr) {
-        uint32_t r0[32], r1[32];
-        sbptx::tmem_ld_32x32b_x32(t_row + pr * 64, r0);
-        sbptx::tmem_ld_32x32b_x32(t_row + pr * 64 + 32, r1);
-        sbptx::tmem_ld_wait();
-        if (pr == 1) {
-          sbptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) arrive_leader(&tempty_bar[acc]);
-        }
-        const int cl = half * 128 + pr * 64;
-        const int col0 = n0 + cl;
-        if (col0 >= p.N || rm0 >= p.M) continue;
-        if (OUT == OUT_BF16) {
-          uint32_t w[32];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            float a0, a1, b0, b1;
-            if (KIND == KIND_I8) {
-              a0 = static_cast<float>(static_cast<int32_t>(r0[2 * j]));
-              a1 = static_cast<float>(static_cast<int32_t>(r0[2 * j + 1]));
-              b0 = static_cast<float>(static_cast<int32_t>(r1[2 * j]));
-              b1 = static_cast<float>(static_cast<int32_t>(r1[2 * j + 1]));
-            } else {
-              a0 = __uint_as_float(r0[2 * j]);
-              a1 = __uint_as_float(r0[2 * j + 1]);
-              b0 = __uint_as_float(r1[2 * j]);
-              b1 = __uint_as_float(r1[2 * j + 1]);
-            }
-            if (SB_COL) {
-              a0 *= fr * cs[cl + 2 * j];
-              a1 *= fr * cs[cl + 2 * j + 1];
-              b0 *= fr * cs[cl + 32 + 2 * j];
-              b1 *= fr * cs[cl + 32 + 2 * j + 1];
-            } else {
-              a0 *= fr;
-              a1 *= fr;
-              b0 *= fr;
-              b1 *= fr;
-            }
-            w[j] = pack_bf16x2(a0, a1);
-            w[16 + j] = pack_bf16x2(b0, b1);
-          }
-          if (lane == 0) sbptx::tma_store_wait_read<0>();
-          __syncwarp();
-          stage_row128(buf, lane, w);
-          sbptx::fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            sbptx::tma_store_2d(&tmD, buf, col0, rm0 + ew * 32);
-            sbptx::tma_store_commit();
-          }
-        } else {
-#pragma unroll
-          for (int sub = 0; sub < 2; ++sub) {
-            const uint32_t(&r)[32] = sub ? r1 : r0;
-            const int cc = cl + sub * 32;
-            if (n0 + cc >= p.N) break;
-            uint32_t w[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (OUT == OUT_I32 || OUT == OUT_F32_RAW || OUT == OUT_F32_RAW_ADD) {
-                w[j] = r[j];
-              } else if (OUT == OUT_F32_EXACT) {
-                const float sbj = SB_COL ? cs[cc + j] : sb_tensor;
-                const double d = __ddiv_rn(
-                    __dmul_rn(__dmul_rn(static_cast<double>(static_cast<int32_t>(r[j])), sa_d), static_cast<double>(sbj)),
-                    16129.0);
-                w[j] = __float_as_uint(__double2float_rn(d));
-              } else {
-                const float v = KIND == KIND_I8 ? static_cast<float>(static_cast<int32_t>(r[j])) : __uint_as_float(r[j]);
-                w[j] = __float_as_uint(SB_COL ? v * (fr * cs[cc + j]) : v * fr);
-              }
-            }
-            if (lane == 0) sbptx::tma_store_wait_read<0>();
-            __syncwarp();
-            stage_row128(buf, lane, w);
-            sbptx::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              if (OUT == OUT_F32_RAW_ADD) {
-                asm volatile(
-                    "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                        reinterpret_cast<uint64_t>(&tmD)),
-                    "r"(sbptx::smem_u32(buf)), "r"(n0 + cc), "r"(rm0 + ew * 32)
-                    : "memory");
-              } else {
-                sbptx::tma_store_2d(&tmD, buf, n0 + cc, rm0 + ew * 32);
-              }
-              sbptx::tma_store_commit();
-            }
-          }
-        }
-      }
+      epilogue_tile<KIND, OUT, SB_COL, true>(p, &tmD, t_row, &tempty_bar[acc], rm0, n0, ew, half, lane, buf, cs, fr,
+                                            sa_d, sb_tensor);
     }
     if (lane == 0) sbptx::tma_store_wait_all<0>();
   }
