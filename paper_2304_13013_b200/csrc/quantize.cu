@@ -72,9 +72,10 @@ __device__ __forceinline__ uint32_t vec_absmax_bits<__nv_bfloat16>(const uint4& 
 }
 
 struct Scale {
-  float s;    // state after exact power-of-two prescale
-  float inv;  // 127 / s (fp32, approximate is fine: only seeds the candidate)
-  float pre;  // the power-of-two prescale applied to |x| and s
+  float s;     // state after exact power-of-two prescale
+  float inv;   // 127 / s (fp32, approximate is fine: only seeds the candidate)
+  float pre;   // the power-of-two prescale applied to |x| and s
+  float inv2;  // 127 / s * (1 + [2^-23, 2^-20]): the bf16 one-FMA exact path (see qvec)
 };
 
 __device__ __forceinline__ Scale make_scale(float state) {
@@ -84,6 +85,7 @@ __device__ __forceinline__ Scale make_scale(float state) {
   else if (state > 0x1p64f) sc.pre = 0x1p-64f;
   sc.s = __fmul_rn(state, sc.pre);
   sc.inv = __fdiv_rn(127.0f, sc.s);
+  sc.inv2 = __fmul_ru(__fdiv_ru(127.0f, sc.s), 1.0f + 0x1p-22f);
   return sc;
 }
 
@@ -204,9 +206,31 @@ __device__ __forceinline__ uint32_t pack4u(uint32_t u0, uint32_t u1, uint32_t u2
   return __byte_perm(__byte_perm(u0, u1, 0x0040), __byte_perm(u2, u3, 0x0040), 0x5410);
 }
 
+// bf16 input, one FMA per element, exact without any tie check. x and s are bf16 values
+// (8 significant bits, s = max|x| >= |x|), so when 127|x|/s is not a half-integer it is at
+// least (127|x|/s) * 2^-16 away from one: with x = a 2^e (a < 256 integer) and s = b 2^f
+// (f >= e), 127|x|/s - (k + 1/2) = 2^e (254 a - (2k+1) b 2^(f-e)) / (2s), a nonzero multiple
+// of 2^e / (2s) = (127|x|/s) / (254 a). inv2 = 127/s (1 + d) with 2^-23 < d < 2^-20, so
+// x * inv2 (one rounding, fused with the magic add) moves the quotient by less than 2^-19 of
+// itself — never across a half-integer — and moves exact ties strictly AWAY from zero, where
+// round-to-nearest-even then lands on the reference's lround (round half away from zero).
+__device__ __forceinline__ uint2 qvec_bf16_fast(const uint4& v, float inv2) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  uint32_t u[8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    u[2 * i] = __float_as_uint(__fmaf_rn(__uint_as_float(w[i] << 16), inv2, kMagic));
+    u[2 * i + 1] = __float_as_uint(__fmaf_rn(__uint_as_float(w[i] & 0xffff0000u), inv2, kMagic));
+  }
+  return make_uint2(pack4u(u[0], u[1], u[2], u[3]), pack4u(u[4], u[5], u[6], u[7]));
+}
+
 // Quantize one 16-byte vector; `plain` = the row needs no power-of-two prescale.
 template <typename T>
 __device__ __forceinline__ typename VecQ<T>::Out qvec(const uint4& v, const Scale& sc, bool plain) {
+  if constexpr (sizeof(T) == 2) {
+    if (__all_sync(0xffffffffu, plain)) return qvec_bf16_fast(v, sc.inv2);
+  }
   constexpr int N = Unpack<T>::N;
   float x[N];
   uint32_t u[N];
@@ -280,7 +304,9 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_rowwise_tma(const T* __r
   }
   const int nvec = static_cast<int>(cols / VEC);
   // A consumer must never wait on a slot more than one phase ahead (try_wait.parity on the
-  // previous parity returns at once), so at most `stages` consumers take part.
+  // previous parity returns at once). The launcher makes `stages` a multiple of the active
+  // consumer count, so slot s only ever holds rows of consumer s % active: each consumer
+  // waits on its own slots' phases in order, having consumed the previous phase itself.
   const int active = kQWarps < stages ? kQWarps : stages;
   if (warp >= active) return;
   int i = warp;
@@ -377,6 +403,111 @@ __global__ void __launch_bounds__(256) k_quantize_rowwise_scalar(const T* __rest
   for (int64_t j = lane; j < cols; j += 32) q[row * ldq + j] = quantize_one(xr[j], sc);
 }
 
+// Register-resident row-wise quantizer: one warp owns a whole row (up to 32*VPL 16-byte
+// vectors). All of the row's loads are issued before the first use (VPL independent 16-byte
+// loads per lane in flight), the absmax is a warp reduction, and the payload is produced from
+// the same registers — one HBM read of X, one write of the payload, no shared memory. Enough
+// warps per SM stay resident (launch bounds) to keep ~100+ KB of reads in flight per SM.
+template <typename T, int VPL>
+__global__ void __launch_bounds__(256) k_quantize_rowwise_reg(const T* __restrict__ x, int64_t rows, int nvec,
+                                                              int64_t ldx, int8_t* __restrict__ q, int64_t ldq,
+                                                              float* __restrict__ state, uint32_t* err) {
+  using Out = typename VecQ<T>::Out;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+       row += warps) {
+    const uint4* xr = reinterpret_cast<const uint4*>(x + row * ldx);
+    uint4 v[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int i = j * 32 + lane;
+      v[j] = i < nvec ? ld_stream(xr + i) : make_uint4(0, 0, 0, 0);
+    }
+    uint32_t amax = 0;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) amax = max(amax, vec_absmax_bits<T>(v[j]));
+    amax = __reduce_max_sync(0xffffffffu, amax);
+    if (amax >= kNonFiniteBits) {
+      if (lane == 0) {
+        raise_nonfinite(err);
+        state[row] = __uint_as_float(amax);
+      }
+      continue;
+    }
+    const float st = state_from_bits(amax);
+    if (lane == 0) state[row] = st;
+    const Scale sc = make_scale(st);
+    const bool plain = sc.pre == 1.0f;
+    Out* qr = reinterpret_cast<Out*>(q + row * ldq);
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      if (j * 32 >= nvec) break;  // warp-uniform (qvec votes across the warp)
+      const int i = j * 32 + lane;
+      const Out o = qvec<T>(v[j], sc, plain);
+      if (i < nvec) qr[i] = o;
+    }
+  }
+}
+
+template <typename T, int VPL>
+void launch_reg(sb_handle h, const T* x, int64_t rows, int nvec, int64_t ldx, int8_t* q, int64_t ldq, float* state) {
+  static int blocks_per_sm = 0;
+  if (blocks_per_sm == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_quantize_rowwise_reg<T, VPL>, 256, 0) !=
+            cudaSuccess ||
+        blocks_per_sm < 1)
+      blocks_per_sm = 1;
+  }
+  const int64_t need = (rows + 7) / 8;
+  const int64_t blocks = std::min<int64_t>(need, static_cast<int64_t>(h->num_sms) * blocks_per_sm);
+  k_quantize_rowwise_reg<T, VPL><<<static_cast<unsigned>(blocks), 256, 0, h->stream>>>(x, rows, nvec, ldx, q, ldq,
+                                                                                      state, h->d_err);
+}
+
+// Dispatch on vectors-per-lane; false when the row is too long for registers.
+template <typename T>
+bool rowwise_reg(sb_handle h, const T* x, int64_t rows, int nvec, int64_t ldx, int8_t* q, int64_t ldq, float* state) {
+  const int vpl = (nvec + 31) / 32;
+  switch (vpl) {
+    case 1: launch_reg<T, 1>(h, x, rows, nvec, ldx, q, ldq, state); return true;
+    case 2: launch_reg<T, 2>(h, x, rows, nvec, ldx, q, ldq, state); return true;
+    case 3: launch_reg<T, 3>(h, x, rows, nvec, ldx, q, ldq, state); return true;
+    case 4: launch_reg<T, 4>(h, x, rows, nvec, ldx, q, ldq, state); return true;
+    case 5: launch_reg<T, 5>(h, x, rows, nvec, ldx, q, ldq, state); return true;
+    case 6: launch_reg<T, 6>(h, x, rows, nvec, ldx, q, ldq, state); return true;
+    case 7:
+    case 8: launch_reg<T, 8>(h, x, rows, nvec, ldx, q, ldq, state); return true;
+    case 9:
+    case 10: launch_reg<T, 10>(h, x, rows, nvec, ldx, q, ldq, state); return true;
+    case 11:
+    case 12: launch_reg<T, 12>(h, x, rows, nvec, ldx, q, ldq, state); return true;
+    case 13:
+    case 14:
+    case 15:
+    case 16: launch_reg<T, 16>(h, x, rows, nvec, ldx, q, ldq, state); return true;
+    case 17:
+    case 18:
+    case 19:
+    case 20: launch_reg<T, 20>(h, x, rows, nvec, ldx, q, ldq, state); return true;
+    case 21:
+    case 22:
+    case 23:
+    case 24: launch_reg<T, 24>(h, x, rows, nvec, ldx, q, ldq, state); return true;
+    default: return false;
+  }
+}
+
+// SB_QUANT_KERNEL=tma selects the smem-ring kernel (A/B measurements); default: registers.
+bool prefer_tma_ring() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SB_QUANT_KERNEL");
+    v = (e && e[0] == 't') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 template <typename T>
 cudaError_t rowwise_impl(sb_handle h, const T* x, int64_t rows, int64_t cols, int64_t ldx, int8_t* q, int64_t ldq,
                          float* state) {
@@ -390,9 +521,13 @@ cudaError_t rowwise_impl(sb_handle h, const T* x, int64_t rows, int64_t cols, in
     k_quantize_rowwise_scalar<T><<<grid, 256, 0, h->stream>>>(x, rows, cols, ldx, q, ldq, state, h->d_err);
     return cudaGetLastError();
   }
+  if (!prefer_tma_ring() && cols / VEC <= 32 * 24 && rows > 0 &&
+      rowwise_reg<T>(h, x, rows, static_cast<int>(cols / VEC), ldx, q, ldq, state))
+    return cudaGetLastError();
   const int64_t row_bytes = cols * static_cast<int64_t>(sizeof(T));
   const int slot = static_cast<int>((row_bytes + 127) / 128 * 128);
-  const int stages = static_cast<int>(std::min<int64_t>(32, kQRingBytes / std::max(slot, 1)));
+  int stages = static_cast<int>(std::min<int64_t>(32, kQRingBytes / std::max(slot, 1)));
+  if (stages > kQWarps) stages -= stages % kQWarps;  // slot ownership: see k_quantize_rowwise_tma
   if (stages >= 4) {
     static bool attr = false;
     const int smem = stages * slot + 2 * stages * 8;

@@ -6,9 +6,19 @@ import torch
 
 import oracle as O
 from paper_2304_13013_b200 import lowprec as L
+from paper_2304_13013_b200 import _capi as A
 from tests._util import bf16, dev, fp8_decode, host, rel_err
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(params=[A.SB_GEMM_1CTA, A.SB_GEMM_2CTA], ids=["1cta", "2cta"])
+def gemm_path(request):
+    """Run the test on both tensor-core tilings (1-CTA 128x256 and cta_group::2 256x256)."""
+    h = A.handle()
+    h.set_gemm_path(request.param)
+    yield request.param
+    h.set_gemm_path(A.SB_GEMM_AUTO)
 
 
 def rand_q(rng, r, c):
@@ -30,7 +40,7 @@ GEMM_SHAPES = [(128, 256, 128), (200, 300, 160), (1, 1, 16), (130, 520, 1024), (
 
 
 @pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
-def test_int8_raw_and_exact_dequant(M, N, K):
+def test_int8_raw_and_exact_dequant(M, N, K, gemm_path):
     rng = np.random.default_rng(M * 7 + N * 3 + K)
     qa, qb = rand_q(rng, M, K), rand_q(rng, N, K)
     sa = rng.uniform(0.1, 5, M).astype(np.float32)
@@ -47,7 +57,7 @@ def test_int8_raw_and_exact_dequant(M, N, K):
 
 
 @pytest.mark.parametrize("M,N,K", [(256, 512, 256), (77, 130, 48)])
-def test_int8_dual_rowwise(M, N, K):
+def test_int8_dual_rowwise(M, N, K, gemm_path):
     rng = np.random.default_rng(3)
     qa, qb = rand_q(rng, M, K), rand_q(rng, N, K)
     sa = rng.uniform(0.1, 5, M).astype(np.float32)
@@ -71,7 +81,7 @@ def test_int8_pinned_and_int64():  # linear_test.cpp:62-72, :97-105
         assert raw[0, 0] == 16129 * k
 
 
-def test_int8_full_size_sampled_rows():
+def test_int8_full_size_sampled_rows(gemm_path):
     """C2 fc1 forward shape: M=65792, N=5120, K=1280; sampled rows checked exactly."""
     M, N, K = 65792, 5120, 1280
     g = torch.Generator(device="cuda").manual_seed(0)
@@ -91,7 +101,7 @@ def test_int8_full_size_sampled_rows():
 
 
 @pytest.mark.parametrize("T,m,n", [(64, 128, 256), (8192, 256, 512), (1000, 384, 264), (100, 24, 40), (65792, 128, 256)])
-def test_wgrad_bf16_tensor_core(T, m, n):
+def test_wgrad_bf16_tensor_core(T, m, n, gemm_path):
     rng = np.random.default_rng(T)
     g = bf16(rng.standard_normal((T, m)).astype(np.float32))
     x = bf16(rng.standard_normal((T, n)).astype(np.float32))
@@ -125,7 +135,7 @@ def test_matmul_exact_bit_identical(r, c, k):
 
 @pytest.mark.parametrize("fa,fb", [(L.E4M3, L.E4M3), (L.E5M2, L.E4M3)])
 @pytest.mark.parametrize("M,N,K", [(256, 512, 256), (130, 300, 160)])
-def test_fp8_gemm(fa, fb, M, N, K):
+def test_fp8_gemm(fa, fb, M, N, K, gemm_path):
     rng = np.random.default_rng(11)
     a = rng.standard_normal((M, K)).astype(np.float32)
     b = rng.standard_normal((N, K)).astype(np.float32)

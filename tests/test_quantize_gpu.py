@@ -47,6 +47,67 @@ def test_rowwise_every_tie_exhaustive_bf16():
     assert np.array_equal(host(q.payload), qo) and np.array_equal(host(q.state), so)
 
 
+def _bf16_tie_rows(cols):
+    """One row per bf16 state mantissa (128 rows, state 1.xxx * 2^3): the row holds the state and
+    every bf16 magnitude in [state * 2^-9, state] of both signs (all inputs with a nonzero payload,
+    every exact half-integer tie 127|x|/s = k + 1/2 among them), then random fill <= state."""
+    rng = np.random.default_rng(0)
+    rows = []
+    for b in range(128, 256):
+        st = np.float32(b / 128.0 * 8.0)
+        u = np.arange(0, 1 << 15, dtype=np.uint32) << 16
+        v = u.view(np.float32)
+        v = v[(v <= st) & (v >= st * 2.0 ** -9)]
+        row = np.concatenate([[st], v, -v]).astype(np.float32)
+        assert row.size <= cols
+        fill = bf16((rng.uniform(-1, 1, cols - row.size) * st).astype(np.float32))
+        rows.append(np.concatenate([row, fill]))
+    return np.stack(rows).astype(np.float32)
+
+
+@pytest.mark.parametrize("cols", [4096, 5120, 6144])
+def test_rowwise_bf16_ties_every_state_mantissa(cols):
+    """The bf16 one-FMA path (qvec_bf16_fast) against the reference rounding for every state
+    mantissa, including 1.984375 (= 254/128, the mantissa with ties at every odd multiple)."""
+    x = _bf16_tie_rows(cols)
+    q = L.quantize_rowwise(dev(x, torch.bfloat16))
+    qo, so = O.quantize(x, O.ROW)
+    assert np.array_equal(host(q.state), so)
+    assert np.array_equal(host(q.payload), qo)
+
+
+def test_rowwise_smem_ring_kernel_subprocess():
+    """The TMA/smem-ring row kernel (SB_QUANT_KERNEL=tma) on shapes with many rows per block
+    and ring wrap-around, including the slot-ownership case (stages not a multiple of warps)."""
+    import subprocess
+    import sys
+    import textwrap
+
+    code = textwrap.dedent("""
+        import numpy as np, torch, sys
+        sys.path.insert(0, '.')
+        import oracle as O
+        from paper_2304_13013_b200 import lowprec as L
+        from tests._util import adversarial, bf16, dev, host
+        for shape in [(4000, 1280), (3000, 1024), (2000, 5120), (700, 10240), (513, 2000)]:
+            for dt in (torch.float32, torch.bfloat16):
+                x = adversarial(*shape, seed=sum(shape))
+                if dt == torch.bfloat16:
+                    x = bf16(x)
+                q = L.quantize_rowwise(dev(x, dt))
+                qo, so = O.quantize(x, O.ROW)
+                assert np.array_equal(host(q.payload), qo), (shape, dt)
+                assert np.array_equal(host(q.state), so), (shape, dt)
+        print("ok")
+    """)
+    import os
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, "SB_QUANT_KERNEL": "tma"},
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
 def test_rowwise_nonfinite_raises():
     x = np.ones((4, 64), np.float32)
     x[2, 5] = np.nan
