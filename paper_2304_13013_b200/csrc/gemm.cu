@@ -186,55 +186,72 @@ bool use_2cta(sb_handle h, int64_t M, int64_t units256) {
   return M > 128 && units256 >= h->num_sms / 2;
 }
 
+// 2-CTA launch of pipeline shape CFG (tc_gemm2.cuh Pipe2).
+template <int KIND, int OUT, bool A_MN, bool B_MN, bool SB_COL, int CFG>
+cudaError_t launch_2cta_cfg(sb_handle h, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& d,
+                            const sbtc::Params& p, uint32_t idesc, int units) {
+  auto kern = sbtc2::k_tc_gemm2<KIND, A_MN, B_MN, OUT, SB_COL, CFG>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  static int max_pairs = 0;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sbtc2::SMEM2_BYTES);
+    // persistent grid: only as many CTA pairs as can be co-resident (a pair needs two SMs of
+    // one TPC); launching more would run the surplus as a second wave
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * (h->num_sms / 2));
+    cfg.blockDim = dim3(sbtc::NUM_THREADS);
+    cfg.dynamicSmemBytes = sbtc2::SMEM2_BYTES;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 2;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (attr_err != cudaSuccess || cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1)
+      n = h->num_sms / 2;
+    max_pairs = n;
+    cudaGetLastError();
+    if (getenv("SB_DEBUG")) fprintf(stderr, "[sb] 2-CTA GEMM (cfg %d): %d co-resident pairs\n", CFG, n);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  const int grid = 2 * (units < max_pairs ? units : max_pairs);
+  kern<<<grid, sbtc::NUM_THREADS, sbtc2::SMEM2_BYTES, h->stream>>>(ta, tb, d, p, idesc);
+  return cudaGetLastError();
+}
+
+// SB_GEMM_CFG=0|1 picks the 2-CTA pipeline shape (default 0).
+int gemm2_cfg() {
+  static int c = -1;
+  if (c < 0) c = getenv("SB_GEMM_CFG") ? atoi(getenv("SB_GEMM_CFG")) : 0;
+  return c;
+}
+constexpr int kCfgMnKrows[2] = {64 * sbtc2::Pipe2<0>::ATOMS, 64 * sbtc2::Pipe2<1>::ATOMS};
+
+template <int KIND, int OUT, bool A_MN, bool B_MN, bool SB_COL>
+cudaError_t launch_2cta(sb_handle h, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& d,
+                        const sbtc::Params& p, uint32_t idesc, int units) {
+  if (gemm2_cfg() == 1) return launch_2cta_cfg<KIND, OUT, A_MN, B_MN, SB_COL, 1>(h, ta, tb, d, p, idesc, units);
+  return launch_2cta_cfg<KIND, OUT, A_MN, B_MN, SB_COL, 0>(h, ta, tb, d, p, idesc, units);
+}
+
 template <int KIND, int OUT, bool A_MN = false, bool B_MN = false, bool SB_COL = false>
 cudaError_t launch_tc(sb_handle h, const Operand& A, const Operand& B, const CUtensorMap& d, sbtc::Params p,
                       uint32_t idesc) {
   const int64_t units256 = ((p.M + 255) / 256) * ((p.N + sbtc::BN - 1) / sbtc::BN) * (p.splits < 1 ? 1 : p.splits);
   const bool two = use_2cta(h, p.M, units256);
   CUtensorMap ta, tb;
-  if (!encode_operand(&ta, A, 128, two ? 128 : 64) || !encode_operand(&tb, B, two ? 128 : 256, two ? 128 : 64))
+  const int mnk = two ? kCfgMnKrows[gemm2_cfg() == 1 ? 1 : 0] : 64;
+  if (!encode_operand(&ta, A, 128, mnk) || !encode_operand(&tb, B, two ? 128 : 256, mnk))
     return cudaErrorInvalidValue;
   p.tiles_m = static_cast<int>((p.M + (two ? sbtc2::BM2 : sbtc::BM) - 1) / (two ? sbtc2::BM2 : sbtc::BM));
   p.tiles_n = static_cast<int>((p.N + sbtc::BN - 1) / sbtc::BN);
   if (p.splits < 1) p.splits = 1;
   const int units = p.tiles_m * p.tiles_n * p.splits;
   h->launches++;
-  if (two) {
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [] {
-      attr_err = cudaFuncSetAttribute(sbtc2::k_tc_gemm2<KIND, A_MN, B_MN, OUT, SB_COL>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, sbtc2::SMEM2_BYTES);
-    });
-    if (attr_err != cudaSuccess) return attr_err;
-    // persistent grid: only as many CTA pairs as can be co-resident (a pair needs two SMs of
-    // one TPC); launching more would run the surplus as a second wave
-    static int max_pairs = 0;
-    if (max_pairs == 0) {
-      cudaLaunchConfig_t cfg{};
-      cfg.gridDim = dim3(2 * (h->num_sms / 2));
-      cfg.blockDim = dim3(sbtc::NUM_THREADS);
-      cfg.dynamicSmemBytes = sbtc2::SMEM2_BYTES;
-      cudaLaunchAttribute attr;
-      attr.id = cudaLaunchAttributeClusterDimension;
-      attr.val.clusterDim.x = 2;
-      attr.val.clusterDim.y = 1;
-      attr.val.clusterDim.z = 1;
-      cfg.attrs = &attr;
-      cfg.numAttrs = 1;
-      int n = 0;
-      if (cudaOccupancyMaxActiveClusters(&n, sbtc2::k_tc_gemm2<KIND, A_MN, B_MN, OUT, SB_COL>, &cfg) != cudaSuccess ||
-          n < 1)
-        n = h->num_sms / 2;
-      max_pairs = n;
-      cudaGetLastError();
-      if (getenv("SB_DEBUG")) fprintf(stderr, "[sb] 2-CTA GEMM: %d co-resident pairs\n", n);
-    }
-    const int grid = 2 * (units < max_pairs ? units : max_pairs);
-    sbtc2::k_tc_gemm2<KIND, A_MN, B_MN, OUT, SB_COL><<<grid, sbtc::NUM_THREADS, sbtc2::SMEM2_BYTES, h->stream>>>(
-        ta, tb, d, p, idesc);
-    return cudaGetLastError();
-  }
+  if (two) return launch_2cta<KIND, OUT, A_MN, B_MN, SB_COL>(h, ta, tb, d, p, idesc, units);
   static std::once_flag once1;
   static cudaError_t attr_err1 = cudaSuccess;
   std::call_once(once1, [] {

@@ -26,13 +26,21 @@ namespace sbtc2 {
 
 using namespace sbtc;
 
-constexpr int STAGES2 = 3;
-constexpr int ATOM_BYTES = 16384;              // 128 rows x 128 B (one SW128 box)
-constexpr int A2_BYTES = 2 * ATOM_BYTES;       // per CTA: 128 rows x 256 B of K
-constexpr int B2_BYTES = 2 * ATOM_BYTES;       // per CTA: its 128-row half of B
-constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
-constexpr int BM2 = 256;                       // tile rows per CTA pair
-constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + EPI_WARPS * EPI_BUF_BYTES + BN * 4 + 1024 + 256;
+constexpr int ATOM_BYTES = 16384;  // 128 rows x 128 B (one SW128 atom column)
+constexpr int BM2 = 256;           // tile rows per CTA pair
+constexpr int RING_BYTES = 196608;  // operand ring per CTA (192 KB)
+// Pipeline shapes (template CFG):
+//   0: 2 atoms (256 B of K) per stage, 3 stages, 1 producer thread
+//   1: 1 atom  (128 B of K) per stage, 6 stages, 2 producer threads (even / odd stages)
+template <int CFG>
+struct Pipe2 {
+  static constexpr int ATOMS = CFG == 0 ? 2 : 1;
+  static constexpr int NPROD = CFG == 0 ? 1 : 2;
+  static constexpr int OPB = ATOMS * ATOM_BYTES;  // bytes of one operand per stage per CTA
+  static constexpr int STAGE = 2 * OPB;
+  static constexpr int STAGES = RING_BYTES / STAGE;
+};
+constexpr int SMEM2_BYTES = RING_BYTES + EPI_WARPS * EPI_BUF_BYTES + BN * 4 + 1024 + 256;
 static_assert(SMEM2_BYTES <= MAX_DYN_SMEM, "shared memory budget");
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // clears the CTA-rank bit of a shared::cluster address
 
@@ -40,17 +48,14 @@ template <int KIND>
 struct Kind2;
 template <>
 struct Kind2<KIND_I8> {
-  static constexpr int KPS = 256;  // K elements per stage
   static constexpr int KATOM = 128;  // K elements per 128-byte atom
 };
 template <>
 struct Kind2<KIND_F8> {
-  static constexpr int KPS = 256;
   static constexpr int KATOM = 128;
 };
 template <>
 struct Kind2<KIND_BF16> {
-  static constexpr int KPS = 128;
   static constexpr int KATOM = 64;
 };
 
@@ -106,26 +111,26 @@ __device__ __forceinline__ void mma2(uint32_t d, uint64_t a, uint64_t b, uint32_
                  : "memory");
 }
 
-// Load one operand's share of a stage: 128 rows (or MN columns) x 256 bytes of K as two
-// 16 KB SW128 boxes. K-major: boxes {KATOM elements, 128 rows} side by side along K.
-// MN-major: boxes {64 MN elements, 128 k-rows}, one per 64-wide MN chunk.
-template <bool MN, int KATOM>
+// Load one operand's share of a stage: 128 rows (or MN columns) x ATOMS*128 bytes of K.
+// K-major: ATOMS boxes {KATOM elements, 128 rows} side by side along K.
+// MN-major: two boxes {64 MN elements, 64*ATOMS k-rows}, one per 64-wide MN chunk.
+template <bool MN, int KATOM, int ATOMS>
 __device__ __forceinline__ void load2(const CUtensorMap* tm, uint64_t* bar, uint8_t* dst, int r0, int kb) {
   if (MN) {
-    tma_load_2sm(tm, bar, dst, r0, kb * 128);
-    tma_load_2sm(tm, bar, dst + ATOM_BYTES, r0 + 64, kb * 128);
+    tma_load_2sm(tm, bar, dst, r0, kb * 64 * ATOMS);
+    tma_load_2sm(tm, bar, dst + ATOMS * 8192, r0 + 64, kb * 64 * ATOMS);
   } else {
-    tma_load_2sm(tm, bar, dst, (2 * kb) * KATOM, r0);
-    tma_load_2sm(tm, bar, dst + ATOM_BYTES, (2 * kb + 1) * KATOM, r0);
+#pragma unroll
+    for (int j = 0; j < ATOMS; ++j) tma_load_2sm(tm, bar, dst + j * ATOM_BYTES, (ATOMS * kb + j) * KATOM, r0);
   }
 }
 
-// UMMA descriptor for MMA step kk (of 8) within a stage (one MMA consumes 32 bytes of K).
+// UMMA descriptor for MMA step kk (of 4*ATOMS) within a stage (one MMA consumes 32 bytes of K).
 //   K-major: step kk lives in atom kk/4 at byte column 32*(kk%4); SBO = 8 rows (1 KB).
-//   MN-major: one MMA = 16 k-rows = 2 KB down both MN chunks; LBO = MN-chunk stride (16 KB).
-template <bool MN>
+//   MN-major: one MMA = 16 k-rows = 2 KB down both MN chunks; LBO = MN-chunk stride.
+template <bool MN, int ATOMS>
 __device__ __forceinline__ uint64_t desc2(uint32_t base, int kk) {
-  return MN ? sbptx::umma_desc_sw128(base + kk * 2048, ATOM_BYTES, 1024)
+  return MN ? sbptx::umma_desc_sw128(base + kk * 2048, ATOMS * 8192, 1024)
             : sbptx::umma_desc_sw128(base + (kk >> 2) * ATOM_BYTES + (kk & 3) * 32, 16, 1024);
 }
 
@@ -138,15 +143,17 @@ __device__ __forceinline__ void unit2(const Params& p, int u, int k_blocks, int&
   kb1 = static_cast<int>((static_cast<int64_t>(k_blocks) * (s + 1)) / p.splits);
 }
 
-template <int KIND, bool A_MN, bool B_MN, int OUT, bool SB_COL>
+template <int KIND, bool A_MN, bool B_MN, int OUT, bool SB_COL, int CFG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     k_tc_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmD, const Params p, uint32_t idesc_runtime) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  using PP = Pipe2<CFG>;
+  constexpr int STAGES2 = PP::STAGES;
   uint8_t* smem_a = smem;
-  uint8_t* smem_b = smem + STAGES2 * A2_BYTES;
-  uint8_t* smem_epi = smem + STAGES2 * STAGE2_BYTES;
+  uint8_t* smem_b = smem + STAGES2 * PP::OPB;
+  uint8_t* smem_epi = smem + RING_BYTES;
   float* col_scale = reinterpret_cast<float*>(smem_epi + EPI_WARPS * EPI_BUF_BYTES);
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(col_scale + BN);
   uint64_t* empty_bar = full_bar + STAGES2;
@@ -159,7 +166,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const uint32_t rank = cta_rank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int num_units = p.tiles_m * p.tiles_n * p.splits;
-  constexpr int KPS = Kind2<KIND>::KPS;
+  constexpr int KPS = Kind2<KIND>::KATOM * PP::ATOMS;
   const int k_blocks = (p.K + KPS - 1) / KPS;
 
   if (warp == 0 && lane == 0) {
@@ -188,26 +195,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   sbptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ producer (both CTAs)
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = pair; u < num_units; u += npairs) {
-        int m0, n0, kb0, kb1;
-        unit2(p, u, k_blocks, m0, n0, kb0, kb1);
-        const int am0 = m0 + static_cast<int>(rank) * BM;        // this CTA's A rows
-        const int bn0 = n0 + static_cast<int>(rank) * (BN / 2);  // this CTA's half of B
-        for (int kb = kb0; kb < kb1; ++kb) {
-          { SB_PROBE_T0(); sbptx::mbar_wait(&empty_bar[stage], phase ^ 1u); SB_PROBE_ADD(3); }
-          if (rank == 0) sbptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * STAGE2_BYTES);
-          load2<A_MN, Kind2<KIND>::KATOM>(&tmA, &full_bar[stage], smem_a + stage * A2_BYTES, am0, kb);
-          load2<B_MN, Kind2<KIND>::KATOM>(&tmB, &full_bar[stage], smem_b + stage * B2_BYTES, bn0, kb);
-          if (++stage == STAGES2) {
-            stage = 0;
-            phase ^= 1u;
-          }
-        }
+  if ((warp == 0 || (PP::NPROD == 2 && warp == 2)) && lane == 0) {
+    // ------------------------------------------------ producer(s) (both CTAs)
+    // With two producer threads, thread `pid` issues the stages of k-iterations i % 2 == pid,
+    // so the per-stage mbarrier + TMA-issue latency of the two chains overlaps.
+    const int pid = warp == 0 ? 0 : 1;
+    int i = 0;
+    for (int u = pair; u < num_units; u += npairs) {
+      int m0, n0, kb0, kb1;
+      unit2(p, u, k_blocks, m0, n0, kb0, kb1);
+      const int am0 = m0 + static_cast<int>(rank) * BM;        // this CTA's A rows
+      const int bn0 = n0 + static_cast<int>(rank) * (BN / 2);  // this CTA's half of B
+      for (int kb = kb0; kb < kb1; ++kb, ++i) {
+        if (PP::NPROD == 2 && (i & 1) != pid) continue;
+        const int stage = i % STAGES2;
+        const uint32_t phase = static_cast<uint32_t>(i / STAGES2) & 1u;
+        { SB_PROBE_T0(); sbptx::mbar_wait(&empty_bar[stage], phase ^ 1u); SB_PROBE_ADD(3); }
+        if (rank == 0) sbptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * PP::STAGE);
+        load2<A_MN, Kind2<KIND>::KATOM, PP::ATOMS>(&tmA, &full_bar[stage], smem_a + stage * PP::OPB, am0, kb);
+        load2<B_MN, Kind2<KIND>::KATOM, PP::ATOMS>(&tmB, &full_bar[stage], smem_b + stage * PP::OPB, bn0, kb);
       }
     }
   } else if (warp == 1) {
@@ -237,11 +243,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           atomicAdd(&g_probe[blockIdx.x * 6 + 5], 1ull);
 #endif
           sbptx::tc_fence_after();
-          const uint32_t a_addr = sbptx::smem_u32(smem_a + stage * A2_BYTES);
-          const uint32_t b_addr = sbptx::smem_u32(smem_b + stage * B2_BYTES);
+          const uint32_t a_addr = sbptx::smem_u32(smem_a + stage * PP::OPB);
+          const uint32_t b_addr = sbptx::smem_u32(smem_b + stage * PP::OPB);
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            mma2<KIND>(d_tmem, desc2<A_MN>(a_addr, kk), desc2<B_MN>(b_addr, kk), idesc, (kb != kb0) || kk);
+          for (int kk = 0; kk < 4 * PP::ATOMS; ++kk)
+            mma2<KIND>(d_tmem, desc2<A_MN, PP::ATOMS>(a_addr, kk), desc2<B_MN, PP::ATOMS>(b_addr, kk), idesc,
+                       (kb != kb0) || kk);
           commit_mc(&empty_bar[stage]);
           if (++stage == STAGES2) {
             stage = 0;
