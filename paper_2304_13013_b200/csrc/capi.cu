@@ -151,8 +151,14 @@ sb_status check_h(sb_handle h, const char* op) {
 }
 
 // ------------------------------------------------------------ quantize ops
+// `word` must hold 2 device words.
 sb_status q_tensorwise(sb_handle h, const void* x, sb_dtype dt, int64_t r, int64_t c, int64_t ldx, int8_t* q,
                        int64_t ldq, int8_t* qt, int64_t ldqt, float* state, unsigned int* word) {
+  cudaError_t fe = cudaSuccess;
+  if (sb::launch_quantize_tensorwise_fused(h, x, dt, r, c, ldx, q, ldq, qt, ldqt, state, word, &fe)) {
+    SB_TRYC("quantize_tensorwise", fe);
+    return SB_OK;
+  }
   SB_TRYC("quantize_tensorwise", sb::launch_absmax_tensor(h, x, dt, r, c, ldx, word));
   SB_TRYC("quantize_tensorwise", sb::launch_quantize_from_words(h, x, dt, r, c, ldx, word, 0, q, ldq, qt, ldqt, state));
   return SB_OK;
@@ -285,7 +291,7 @@ sb_status sb_quantize_tensorwise(sb_handle h, const void* x, sb_dtype dt, int64_
   SB_TRY(check_h(h, op));
   if (rows <= 0 || cols <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty matrix");
   if (!float_dtype(dt) || !x || (!q && !q_t) || !state || ldx < cols) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
-  unsigned int* words = sb::scratch(h, 1);
+  unsigned int* words = sb::scratch(h, 2);
   if (!words) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed");
   return q_tensorwise(h, x, dt, rows, cols, ldx, q, ldq, q_t, ldqt, state, words);
 }

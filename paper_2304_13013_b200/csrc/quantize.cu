@@ -696,6 +696,125 @@ __global__ void __launch_bounds__(256) k_quantize_from_words(const T* __restrict
   }
 }
 
+// ------------------------------------------------------------- K2+K3 fused ----
+// Tensor-wise quantize (+ transposed payload) in ONE launch: phase 1 reduces max|x| over a
+// grid-stride share of the 16-byte vectors (atomicMax of bit patterns into sync[0]); a
+// grid-wide arrival counter (sync[1]; all CTAs are co-resident by construction of the grid)
+// separates it from phase 2, which re-reads x (L2-resident: W is <= tens of MB) in 64 x 64
+// tiles and writes q and/or q_t from one read (quantize.cpp:139-159). bf16 input takes the
+// one-FMA exact path (qvec_bf16_fast: the tensor state is a bf16 value >= every |x|).
+// sync[0..1] must be zero at launch (the launcher memsets them).
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const unsigned int* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_quantize_tensorwise_fused(const T* __restrict__ x, int64_t rows, int64_t cols,
+                                                                    int64_t ldx, int8_t* __restrict__ q, int64_t ldq,
+                                                                    int8_t* __restrict__ qt, int64_t ldqt,
+                                                                    float* __restrict__ state, unsigned int* sync,
+                                                                    uint32_t* err) {
+  constexpr int VEC = 16 / sizeof(T);
+  __shared__ uint32_t red[8];
+  __shared__ __align__(16) int8_t tile[64][64 + 16];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t vpr = cols / VEC;  // vectors per row
+  const int64_t nvec = rows * vpr;
+  // ---- phase 1: absmax
+  uint32_t m = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nvec;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / vpr, v = i - r * vpr;
+    m = max(m, vec_absmax_bits<T>(ld_stream(reinterpret_cast<const uint4*>(x + r * ldx) + v)));
+  }
+  m = __reduce_max_sync(0xffffffffu, m);
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < 8; ++i) m = max(m, red[i]);
+    if (m) atomicMax(sync, m);
+    __threadfence();
+    atomicAdd(sync + 1, 1u);
+    while (ld_acquire_gpu(sync + 1) < gridDim.x) __nanosleep(64);
+    red[0] = ld_acquire_gpu(sync);
+  }
+  __syncthreads();
+  // ---- phase 2: quantize 64 x 64 tiles
+  const uint32_t wb = red[0];
+  if (wb >= kNonFiniteBits) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      raise_nonfinite(err);
+      state[0] = __uint_as_float(wb);
+    }
+    return;
+  }
+  const float st = state_from_bits(wb);
+  if (blockIdx.x == 0 && threadIdx.x == 0) state[0] = st;
+  const Scale sc = make_scale(st);
+  const bool fast = sizeof(T) == 2 && sc.pre == 1.0f;
+  const int64_t tr = (rows + 63) / 64, tc = (cols + 63) / 64;
+  for (int64_t t = blockIdx.x; t < tr * tc; t += gridDim.x) {
+    const int64_t r0 = (t / tc) * 64, c0 = (t % tc) * 64;
+    // 64 rows x 64 cols: thread -> (row lr = pass*32 + tid/8, 8-column group tid%8) for bf16,
+    // (row pass*16 + tid/16, 4-column group tid%16) for fp32
+    constexpr int GPR = 64 / VEC;          // vector groups per tile row
+    constexpr int RPP = 256 / GPR;         // rows per pass
+    const int g = threadIdx.x % GPR, lr0 = threadIdx.x / GPR;
+#pragma unroll
+    for (int pass = 0; pass < 64 / RPP; ++pass) {
+      const int lr = pass * RPP + lr0;
+      const int64_t r = r0 + lr, c = c0 + g * VEC;
+      uint32_t w0 = 0, w1 = 0;  // payload bytes of this vector (VEC <= 8)
+      if (r < rows && c < cols) {
+        const uint4 v = ld_stream(reinterpret_cast<const uint4*>(x + r * ldx + c));
+        if constexpr (sizeof(T) == 2) {
+          const uint2 o = fast ? qvec_bf16_fast(v, sc.inv2) : VecQ<T>::run(v, sc);
+          w0 = o.x;
+          w1 = o.y;
+        } else {
+          w0 = VecQ<T>::run(v, sc);
+        }
+        if (q) {
+          if constexpr (VEC == 8)
+            *reinterpret_cast<uint2*>(q + r * ldq + c) = make_uint2(w0, w1);
+          else
+            *reinterpret_cast<uint32_t*>(q + r * ldq + c) = w0;
+        }
+      }
+      if constexpr (VEC == 8)
+        *reinterpret_cast<uint2*>(&tile[lr][g * 8]) = make_uint2(w0, w1);
+      else
+        *reinterpret_cast<uint32_t*>(&tile[lr][g * 4]) = w0;
+    }
+    if (qt) {
+      __syncthreads();
+      // q_t[c][r0 .. r0+63]: thread -> column lc = tid / 4, 16 consecutive rows (tid % 4) * 16
+      const int lc = threadIdx.x >> 2, rq = (threadIdx.x & 3) * 16;
+      const int64_t c = c0 + lc;
+      if (c < cols) {
+        uint32_t wv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint32_t pk = 0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) pk |= static_cast<uint32_t>(static_cast<uint8_t>(tile[rq + 4 * k + i][lc])) << (8 * i);
+          wv[k] = pk;
+        }
+        const int64_t r = r0 + rq;
+        int8_t* dst = qt + c * ldqt + r;
+        if (r + 15 < rows && sb::aligned(dst, 16)) {
+          *reinterpret_cast<uint4*>(dst) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        } else {
+          for (int i = 0; i < 16 && r + i < rows; ++i) dst[i] = static_cast<int8_t>((wv[i >> 2] >> (8 * (i & 3))) & 0xff);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ----------------------------------------------------------------- K10 ----
 template <typename TO>
 __device__ __forceinline__ TO from_f32(float v);
@@ -843,6 +962,38 @@ cudaError_t launch_absmax_tensor(sb_handle h, const void* x, sb_dtype dt, int64_
   else
     k_absmax_tensor<<<grid, 256, 0, h->stream>>>(static_cast<const float*>(x), rows, cols, ldx, word);
   return cudaGetLastError();
+}
+
+// One-launch tensor-wise quantize when x is 16-byte vectorisable; false = use K2 + K3.
+bool launch_quantize_tensorwise_fused(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols,
+                                      int64_t ldx, int8_t* q, int64_t ldq, int8_t* q_t, int64_t ldqt, float* state,
+                                      unsigned int* sync, cudaError_t* err) {
+  const int vec = dt == SB_BF16 ? 8 : 4;
+  if (cols % vec || ldx % vec || !sb::aligned(x, 16) || rows <= 0 || cols <= 0) return false;
+  if (q && (ldq % vec || !sb::aligned(q, 8))) return false;
+  static int cap_bf16 = 0, cap_f32 = 0;
+  int& cap = dt == SB_BF16 ? cap_bf16 : cap_f32;
+  if (cap == 0) {
+    int b = 0;
+    if (dt == SB_BF16)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_quantize_tensorwise_fused<__nv_bfloat16>, 256, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_quantize_tensorwise_fused<float>, 256, 0);
+    cap = std::max(1, std::min(b, 4)) * h->num_sms;  // every CTA co-resident: the grid barrier needs it
+  }
+  const int64_t tiles = ((rows + 63) / 64) * ((cols + 63) / 64);
+  const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(tiles, cap)));
+  *err = cudaMemsetAsync(sync, 0, 2 * sizeof(unsigned int), h->stream);
+  if (*err != cudaSuccess) return true;
+  h->launches++;
+  if (dt == SB_BF16)
+    k_quantize_tensorwise_fused<<<grid, 256, 0, h->stream>>>(static_cast<const __nv_bfloat16*>(x), rows, cols, ldx, q,
+                                                             ldq, q_t, ldqt, state, sync, h->d_err);
+  else
+    k_quantize_tensorwise_fused<<<grid, 256, 0, h->stream>>>(static_cast<const float*>(x), rows, cols, ldx, q, ldq, q_t,
+                                                             ldqt, state, sync, h->d_err);
+  *err = cudaGetLastError();
+  return true;
 }
 
 cudaError_t launch_absmax_rows(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,

@@ -119,7 +119,8 @@ def test_rowwise_nonfinite_raises():
     L.quantize_rowwise(dev(np.ones((4, 64), np.float32)))  # latch cleared
 
 
-@pytest.mark.parametrize("shape", [(1, 1), (3, 5), (13, 70), (64, 64), (130, 70), (1280, 5120), (5120, 1280)])
+@pytest.mark.parametrize("shape", [(1, 1), (3, 5), (13, 70), (64, 64), (130, 70), (1280, 5120), (5120, 1280), (72, 136),
+                                   (3840, 1280), (1000, 8), (8, 1000)])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 def test_tensorwise_and_transpose_bit_exact(shape, dtype):
     x = adversarial(*shape, seed=3)
@@ -133,6 +134,33 @@ def test_tensorwise_and_transpose_bit_exact(shape, dtype):
     assert np.array_equal(host(qt.payload), qto)
     q2 = L.quantize_tensorwise_transpose(dev(x, dtype))
     assert np.array_equal(host(q2.payload), qto) and np.array_equal(host(q2.state), sto)
+
+
+@pytest.mark.parametrize("b", [128, 160, 201, 254, 255])
+def test_tensorwise_bf16_ties(b):
+    """Tensor state with mantissa b/128 and every bf16 magnitude below it (all exact ties) —
+    the fused one-launch tensor-wise kernel's one-FMA path against the reference rounding."""
+    st = np.float32(b / 128.0 * 4.0)
+    u = np.arange(0, 1 << 15, dtype=np.uint32) << 16
+    v = u.view(np.float32)
+    v = v[(v <= st) & (v >= st * 2.0 ** -9)]
+    row = np.concatenate([[st], v, -v]).astype(np.float32)
+    cols = 64
+    row = np.concatenate([row, np.zeros((-row.size) % cols, np.float32)])
+    x = row.reshape(-1, cols)
+    q, qt = L.quantize_tensorwise(dev(x, torch.bfloat16), with_transpose=True)
+    qo, so = O.quantize(x, O.TENSOR)
+    assert np.array_equal(host(q.payload), qo) and np.array_equal(host(q.state), so)
+    assert np.array_equal(host(qt.payload), qo.T)
+
+
+def test_tensorwise_nonfinite_raises():
+    x = np.ones((256, 512), np.float32)
+    x[100, 7] = np.inf
+    with pytest.raises(L.InvalidArgument, match="non-finite"):
+        L.quantize_tensorwise(dev(x, torch.bfloat16))
+    q = L.quantize_tensorwise(dev(np.ones((256, 512), np.float32), torch.bfloat16))  # latch cleared, words reset
+    assert host(q.state)[0] == 1.0 and (host(q.payload) == 127).all()
 
 
 @pytest.mark.parametrize("shape", [(1, 1), (2, 3), (13, 70), (300, 77), (1280, 5120)])
