@@ -31,6 +31,16 @@ T_PER_GPU = 256 * 257
 LAYERS = [("fc1", 1280, 5120), ("fc2", 5120, 1280)]  # (name, n = in_features, m = out_features)
 METRIC = "SwitchBack fwd+bwd tokens/s at ViT-H shapes (1/2/4/8 GPU); int8 TOPS % of peak"
 WORKLOAD = "CLIP ViT-Huge MLP block 1280->5120->1280, 256 images x 257 tokens, int8 fwd/dX + bf16 dW"
+# BASELINE.json configs as bench modes (--config); c2 is the headline line the driver runs.
+CONFIGS = {
+    "c2": (LAYERS, WORKLOAD, "switchback", "int8"),
+    "c3": ([("qkv", 1280, 3840), ("out", 1280, 1280), ("fc1", 1280, 5120), ("fc2", 5120, 1280)],
+           "All CLIP ViT-Huge linears of one block (qkv 1280->3840, out 1280->1280, fc1, fc2), 65792 tokens per GPU",
+           "switchback", "int8"),
+    "c4q": (LAYERS, "ViT-Huge MLP block, SwitchBackQ (row-wise W, row x row int8 dequant)", "switchback_q", "int8"),
+    "c4fp8": (LAYERS, "ViT-Huge MLP block, SwitchBack fp8 (e4m3 fwd, e5m2 grad, kind::f8f6f4)", "switchback", "fp8"),
+}
+INT8_PEAK_TOPS = 4500.0  # B200 dense int8 datasheet; tools/mma_rate.cu measures 4.47 POPS 2-CTA MMA issue
 
 
 def peaks():
@@ -153,19 +163,22 @@ def run_ours(args):
     from paper_2304_13013_b200 import dp
     from paper_2304_13013_b200 import lowprec as L
 
+    layers_cfg, workload, variant, fmt = CONFIGS[args.config]
     rank, world, local = dp.init_from_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     T = args.tokens
-    mode = L.LinearMode(A.SB_SWITCHBACK, A.SB_INT8)
+    mode = L.LinearMode({"switchback": A.SB_SWITCHBACK, "switchback_q": A.SB_SWITCHBACK_Q}[variant],
+                        A.SB_INT8 if fmt == "int8" else A.SB_FP8)
     cmode = mode.c()
+    plain = variant == "switchback" and fmt == "int8"  # the segmented SwitchBack int8 step
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
 
     def randn(*shape, scale=1.0):
         return (torch.randn(*shape, device=dev, generator=gen) * scale).to(torch.bfloat16)
 
     layers = []
-    for name, n, m in LAYERS:
+    for name, n, m in layers_cfg:
         lay = {"name": name, "n": n, "m": m,
                "x": randn(T, n), "w": randn(m, n, scale=n ** -0.5), "g": randn(T, m),
                "y": torch.empty(T, m, device=dev, dtype=torch.bfloat16),
@@ -179,7 +192,8 @@ def run_ours(args):
     P = L._p
 
     # The step's kernels, straight through the C-ABI (the same launches sb_linear_forward /
-    # sb_linear_backward issue; the backward is split so the dW GEMM can be timed alone).
+    # sb_linear_backward issue; for SwitchBack int8 the backward is split so the dW GEMM can
+    # be timed alone).
     def fwd(lay):
         A.check(h.lib.sb_linear_forward(h.h, C.byref(cmode), P(lay["x"]), P(lay["w"]), A.SB_BF16, T, lay["n"],
                                         lay["m"], P(lay["y"]), C.byref(lay["ctx"]), P(lay["ws"]), lay["ws"].numel()))
@@ -194,9 +208,28 @@ def run_ours(args):
     def bwd_dw(lay):
         A.check(h.lib.sb_wgrad(h.h, P(lay["g"]), P(lay["x"]), A.SB_BF16, T, lay["m"], lay["n"], P(lay["dw"]), 0, 0))
 
-    fc1, fc2 = layers
-    segments = [lambda: (fwd(fc1), fwd(fc2), bwd_dx(fc2)), lambda: bwd_dw(fc2), lambda: bwd_dx(fc1),
-                lambda: bwd_dw(fc1)]
+    def bwd_full(lay):
+        A.check(h.lib.sb_linear_backward(h.h, C.byref(cmode), C.byref(lay["ctx"]), P(lay["g"]), P(lay["dx"]),
+                                         P(lay["dw"]), 0))
+
+    # Segments (one CUDA graph each): forwards of all layers then, last layer first, the
+    # input-gradient work and the weight gradient of each layer. seg_dw marks dW segments.
+    segments, seg_dw = [], []
+    if plain:
+        segments.append(lambda: ([fwd(l) for l in layers], bwd_dx(layers[-1])))
+        seg_dw.append(False)
+        for i in range(len(layers) - 1, -1, -1):
+            segments.append(lambda l=layers[i]: bwd_dw(l))
+            seg_dw.append(True)
+            if i > 0:
+                segments.append(lambda l=layers[i - 1]: bwd_dx(l))
+                seg_dw.append(False)
+    else:
+        segments.append(lambda: [fwd(l) for l in layers])
+        seg_dw.append(False)
+        for i in range(len(layers) - 1, -1, -1):
+            segments.append(lambda l=layers[i]: bwd_full(l))
+            seg_dw.append(False)
     stream = torch.cuda.current_stream(dev)
     ar = dp.GradAllReduce()
 
@@ -223,19 +256,23 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     run = [g.replay for g in graphs] if graphs else segments
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    ns = len(run)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(ns + 1)] for _ in range(args.steps)]
+    # dW all-reduce issue points: after each layer's dW segment (or full backward)
+    ar_after = {}
+    k = 0
+    for j in range(1, ns):
+        if seg_dw[j] or not plain:
+            ar_after[j] = layers[len(layers) - 1 - k]["dw"]
+            k += 1
 
     def step(e):
-        run[0]()
         e[0].record(stream)
-        run[1]()          # dW fc2
-        e[1].record(stream)
-        ar.launch(fc2["dw"])
-        run[2]()
-        e[2].record(stream)
-        run[3]()          # dW fc1
-        e[3].record(stream)
-        ar.launch(fc1["dw"])
+        for j in range(ns):
+            run[j]()
+            e[j + 1].record(stream)
+            if j in ar_after:
+                ar.launch(ar_after[j])
         ar.wait()
 
     if world > 1:
@@ -257,49 +294,238 @@ def run_ours(args):
     value = T * world / (ms / 1000.0)
     launches = launches_per_step * args.steps
 
-    # dominant kernel: the bf16 dW GEMM (2*m*n*T flops per launch), timed by the events
-    # bracketing its graph segment inside the timed region
-    dw_times = [e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3]) for e in ev]
     pk = peaks()
-    flops_step = sum(2.0 * lay["m"] * lay["n"] * T for lay in layers)
-    achieved = flops_step * args.steps / (sum(dw_times) / 1000.0) / 1e12
-    peak = pk["bf16_tflops_sustained"]
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "dw_gemm_traffic.json")
-    if os.path.exists(prof):
-        with open(prof) as f:
-            traffic = json.load(f).get("bytes_per_launch")
-    share = sum(dw_times) / (ms * args.steps)
+    roof = None
+    if plain:
+        # dominant kernel: the bf16 dW GEMM (2*m*n*T flops per launch), timed by the events
+        # bracketing its graph segment inside the timed region
+        dw_ms = sum(e[j].elapsed_time(e[j + 1]) for e in ev for j in range(ns) if seg_dw[j])
+        flops_step = sum(2.0 * lay["m"] * lay["n"] * T for lay in layers)
+        achieved = flops_step * args.steps / (dw_ms / 1000.0) / 1e12
+        peak = pk["bf16_tflops"]
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "dw_gemm_traffic.json")
+        if os.path.exists(prof):
+            with open(prof) as f:
+                traffic = json.load(f).get("bytes_per_launch")
+        roof = {"bound": "tensor", "kernel": "bf16 dW GEMM (tcgen05 kind::f16 cta_group::2, MN-major operands)",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "peak_source": f"{pk['source']} bf16 burst (MEASURED_PEAKS.json bf16_tflops: the kernel is timed "
+                               f"inside a {ms * args.steps:.0f} ms region); sustained figure "
+                               f"{pk['bf16_tflops_sustained']}, datasheet dense 2250",
+                "traffic": traffic, "share_of_step": dw_ms / (ms * args.steps),
+                "flops_per_launch": [2 * lay["m"] * lay["n"] * T for lay in layers]}
     int8_ops_step = sum(4.0 * lay["m"] * lay["n"] * T for lay in layers)
 
     e2e = None
-    if rank == 0 and not args.no_e2e:
+    if rank == 0 and not args.no_e2e and args.config == "c2":
         e2e = e2e_host(args, L, torch)
     yard = cublas_yardstick(torch, layers, T, args) if rank == 0 else None
+    kern = kernel_rates(torch, A, h, layers, T, pk, fmt == "int8" and variant == "switchback") if rank == 0 else None
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and args.config == "c2":
         r, cores, sample, kind = cpu_reference_rate(budget_s=args.ref_budget)
         cpu = {"value": r, "unit": "tokens/s", "cores": cores, "kind": kind, "sample": sample}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "int8 (fwd, dX) + bf16 (dW), fp32 accumulate", "data": "synthetic",
-                "config": {"workload": WORKLOAD, "tokens_per_gpu": T, "global_tokens": T * world,
-                           "layers": [f"{n}->{m}" for _, n, m in LAYERS], "parallelism": f"dp{world} (token shards)",
-                           "l2": "inputs larger than L2 (X, G, H operands 168-673 MB each)",
+                "vs_baseline": None,
+                "dtype": ("int8 (fwd, dX) + bf16 (dW), fp32 accumulate" if fmt == "int8" else
+                          "fp8 e4m3/e5m2 (fwd, dX) + fp8-snapped dW, fp32 accumulate"),
+                "data": "synthetic",
+                "config": {"workload": workload, "config": args.config, "variant": variant, "format": fmt,
+                           "tokens_per_gpu": T, "global_tokens": T * world,
+                           "layers": [f"{n}->{m}" for _, n, m in layers_cfg], "parallelism": f"dp{world} (token shards)",
+                           "l2": "inputs larger than L2 (X, G operands 168-673 MB each)",
                            "cuda_graphs": graphs is not None},
                 "gpu_launches": launches,
-                "roofline": {"bound": "tensor", "kernel": "bf16 dW GEMM (tcgen05 kind::f16, MN-major)",
-                             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                             "peak_source": f"{pk['source']} bf16 sustained (MEASURED_PEAKS.json)", "traffic": traffic,
-                             "share_of_step": share, "flops_per_launch": [2 * lay["m"] * lay["n"] * T for lay in layers]},
+                "roofline": roof,
                 "int8_tops_per_step": int8_ops_step / 1e12,
+                "kernels": kern,
                 "clocks": clk.summary(),
                 "e2e": e2e, "cpu_baseline": cpu, "yardstick_cublas_bf16": yard}
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def run_c5(args):
+    """BASELINE.json configs[4]: one StableAdamW step (optimizer.cpp:102-172, update_clip,
+    beta1 0.9, beta2 0.99, eps 1e-6, weight decay 0.2) over the ~1.0e9 fp32 parameters of 51
+    ViT-H blocks {3840x1280, 1280x1280, 5120x1280, 1280x5120}, whole
+    tensors sharded round-robin over the ranks (strong scaling: total parameters fixed).
+    HBM-bound: 28 B/param (read theta, g, v, u; write theta, v, u)."""
+    import torch
+
+    from paper_2304_13013_b200 import _capi as A
+    from paper_2304_13013_b200 import dp
+
+    rank, world, local = dp.init_from_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    shapes = [(3840, 1280), (1280, 1280), (5120, 1280), (1280, 5120)] * 51
+    mine = [s for i, s in enumerate(shapes) if i % world == rank]
+    total_params = sum(a * b for a, b in shapes)
+    n_mine = sum(a * b for a, b in mine)
+    # one flat allocation per state array, tensors are views (as a trainer's flat buffers)
+    g = torch.Generator(device=dev).manual_seed(5 + rank)
+    flat = {k: torch.empty(n_mine, device=dev) for k in ("theta", "grad", "v", "u")}
+    flat["theta"].normal_(generator=g).mul_(0.02)
+    flat["grad"].normal_(generator=g).mul_(1e-3)
+    flat["v"].zero_()
+    flat["u"].zero_()
+    arr = (A.AdamwTensor * len(mine))()
+    off = 0
+    for i, (a, b) in enumerate(mine):
+        n = a * b
+        arr[i] = A.AdamwTensor(*(flat[k].data_ptr() + 4 * off for k in ("theta", "grad", "v", "u")), n)
+        off += n
+    lib = A.load()
+    nbytes = C.c_size_t()
+    A.check(lib.sb_stableadamw_workspace_size(arr, len(mine), C.byref(nbytes)))
+    ws = torch.empty(max(1, nbytes.value), dtype=torch.uint8, device=dev)
+    out = torch.empty((2, len(mine)), dtype=torch.float64, device=dev)
+    hp = A.AdamwHparams(1e-3, 0.9, 0.99, 0.0, 1e-6, 0.2, 1.0, A.SB_CLIP_UPDATE)
+    h = A.handle(local)
+    stream = torch.cuda.current_stream(dev)
+    h.bind_stream(stream.cuda_stream)
+    t = [0]
+
+    def step():
+        t[0] += 1
+        A.check(h.lib.sb_stableadamw_step(h.h, arr, len(mine), C.byref(hp), t[0], C.c_void_p(out[0].data_ptr()),
+                                          C.c_void_p(out[1].data_ptr()), C.c_void_p(ws.data_ptr()), ws.numel()))
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    l0 = h.launches()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        s_ev.record(stream)
+        for _ in range(args.steps):
+            step()
+        e_ev.record(stream)
+        torch.cuda.synchronize()
+    launches = h.launches() - l0
+    ms = dp.max_over_ranks(s_ev.elapsed_time(e_ev) / args.steps, dev)
+    pk = peaks()
+    achieved = 28.0 * n_mine / (ms / 1000.0) / 1e9
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_optimizer_rate()
+    if rank == 0:
+        line = {"metric": "StableAdamW step params/s over 1.0e9 ViT-H parameters (BASELINE.json configs[4])",
+                "value": total_params / (ms / 1000.0), "unit": "params/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64 math / f32 storage", "data": "synthetic",
+                "config": {"workload": "StableAdamW (update_clip) over 51 ViT-H blocks x 4 weight tensors",
+                           "config": "c5", "params_total": total_params, "params_per_rank": n_mine,
+                           "tensors_per_rank": len(mine), "parallelism": f"{world} ranks, whole tensors round-robin",
+                           "l2": "state (16 GB) far larger than L2"},
+                "gpu_launches": launches,
+                "roofline": {"bound": "hbm", "kernel": "StableAdamW phase 1 + 2 (csrc/optim.cu)", "achieved": achieved,
+                             "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
+                             "traffic": None, "bytes_per_param": 28},
+                "clocks": clk.summary(), "e2e": None, "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def cpu_optimizer_rate(budget_s: float = 10.0):
+    """The reference's optimizer_step (oracle/_ref, single-threaded as the reference) on a
+    bounded sample of the C5 tensors; params/s."""
+    import numpy as np
+
+    import oracle as O
+
+    if not O.ref_available():
+        return None
+    L = O.ref()
+    shapes = [(1280, 1280), (3840, 1280)]
+    rng = np.random.default_rng(0)
+    arrs = [[(rng.standard_normal(a * b) * s).astype(np.float32) for s in (0.02, 1e-3, 0.0, 0.0)] for a, b in shapes]
+    pp = C.POINTER(C.c_void_p)
+    mk = lambda k: (C.c_void_p * len(arrs))(*[x[k].ctypes.data for x in arrs])  # noqa: E731
+    numel = np.array([a * b for a, b in shapes], np.int64)
+    rms, eta = np.zeros(len(shapes)), np.zeros(len(shapes))
+    t0, n, t = time.perf_counter(), 0, 0
+    while time.perf_counter() - t0 < budget_s:
+        t += 1
+        rc = L.ref_optimizer_step(len(shapes), C.cast(mk(0), pp), C.cast(mk(1), pp), C.cast(mk(2), pp),
+                                  C.cast(mk(3), pp), numel, 1e-3, 0.9, 0.99, 0.0, 1e-6, 0.2, 1, 1.0, t, rms, eta)
+        assert rc == 0
+        n += int(numel.sum())
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "params/s", "cores": 1, "kind": "reference",
+            "sample": f"{t} optimizer_step calls over 1280x1280 + 3840x1280 fp32 tensors (6.55 M params each), "
+                      "lowprec::optimizer_step (single-threaded as the reference)"}
+
+
+def kernel_rates(torch, A, h, layers, T, pk, int8_path):
+    """Per-kernel rates measured after the timed region, each launch alone with CUDA events on
+    the launching stream (median of 5, inputs > L2): the int8 GEMMs (the metric's 'int8 TOPS %
+    of peak') and the row-wise quantizer (HBM-bound)."""
+    import ctypes as C
+
+    P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    stream = torch.cuda.current_stream()
+    h.bind_stream(stream.cuda_stream)
+
+    def timed(fn, reps=5):
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return sorted(ts)[len(ts) // 2] / 1000.0
+
+    out = {"int8_gemm": [], "quantize_rowwise": []}
+    if not int8_path:
+        return out
+    for lay in layers:
+        n, m = lay["n"], lay["m"]
+        xq = torch.empty(T, n, device="cuda", dtype=torch.int8)
+        xs = torch.empty(T, device="cuda")
+        A.check(h.lib.sb_quantize_rowwise(h.h, P(lay["x"]), A.SB_BF16, T, n, n, P(xq), n, P(xs)))
+        # forward Y = X_q W_q^T (M=T, N=m, K=n) and input gradient dX = G_q W_q (M=T, N=n, K=m)
+        wq = torch.empty(m, n, device="cuda", dtype=torch.int8)
+        wqt = torch.empty(n, m, device="cuda", dtype=torch.int8)
+        wst = torch.empty(1, device="cuda")
+        A.check(h.lib.sb_quantize_tensorwise(h.h, P(lay["w"]), A.SB_BF16, m, n, n, P(wq), n, P(wqt), m, P(wst)))
+        gq = torch.empty(T, m, device="cuda", dtype=torch.int8)
+        gs = torch.empty(T, device="cuda")
+        A.check(h.lib.sb_quantize_rowwise(h.h, P(lay["g"]), A.SB_BF16, T, m, m, P(gq), m, P(gs)))
+        fwd = lambda: A.check(h.lib.sb_gemm_i8(h.h, P(xq), P(xs), P(wq), P(wst), A.SB_SCALE_ROW_TENSOR,  # noqa: E731
+                                               T, m, n, P(lay["y"]), A.SB_BF16, 0))
+        dxg = lambda: A.check(h.lib.sb_gemm_i8(h.h, P(gq), P(gs), P(wqt), P(wst), A.SB_SCALE_ROW_TENSOR,  # noqa: E731
+                                               T, n, m, P(lay["dx"]), A.SB_BF16, 0))
+        for name, fn, N, K in (("fwd", fwd, m, n), ("dX", dxg, n, m)):
+            t = timed(fn)
+            tops = 2.0 * T * N * K / t / 1e12
+            out["int8_gemm"].append({"gemm": f"{lay['name']} {name} M={T} N={N} K={K}", "us": t * 1e6, "tops": tops,
+                                     "peak_tops": INT8_PEAK_TOPS, "frac": tops / INT8_PEAK_TOPS})
+        for src, cols in ((lay["x"], n), (lay["g"], m)):
+            q = torch.empty(T, cols, device="cuda", dtype=torch.int8)
+            st = torch.empty(T, device="cuda")
+            t = timed(lambda: A.check(h.lib.sb_quantize_rowwise(h.h, P(src), A.SB_BF16, T, cols, cols, P(q), cols,
+                                                                P(st))))
+            gbs = (T * cols * 3 + 4 * T) / t / 1e9
+            out["quantize_rowwise"].append({"shape": f"{T}x{cols} bf16", "us": t * 1e6, "gbs": gbs,
+                                            "peak_gbs": pk["hbm_gbs"], "frac": gbs / pk["hbm_gbs"]})
+    tot_ops = sum(2.0 * T * lay["n"] * lay["m"] * 2 for lay in layers)
+    tot_t = sum(k["us"] for k in out["int8_gemm"]) / 1e6
+    out["int8_summary"] = {"tops": tot_ops / tot_t / 1e12, "peak_tops": INT8_PEAK_TOPS,
+                           "frac": tot_ops / tot_t / 1e12 / INT8_PEAK_TOPS,
+                           "peak_source": "B200 dense int8 datasheet (4.5 POPS); MEASURED_PEAKS.json has no int8 entry"}
+    return out
 
 
 def e2e_host(args, L, torch):
@@ -359,6 +585,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c5"])
     ap.add_argument("--tokens", type=int, default=T_PER_GPU)
     ap.add_argument("--ref-budget", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
@@ -367,6 +594,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
+    elif args.config == "c5":
+        run_c5(args)
     else:
         run_ours(args)
 
