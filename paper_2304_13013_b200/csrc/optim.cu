@@ -22,9 +22,9 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kPerThread = 16;
-constexpr int kChunk = kThreads * kPerThread;  // elements per block
-constexpr int kMaxGroup = 96;                  // tensors per launch (kernel-parameter budget)
-constexpr size_t kGroupL2Bytes = 48ull << 20;  // v,u bytes per group kept L2-resident
+constexpr int kChunk = kThreads * kPerThread;  // elements per block task
+constexpr int kMaxGroup = 256;                 // tensors per launch (kernel parameters <= 32 KB)
+constexpr int kVecPerIter = 1;                 // float4 groups loaded per inner iteration (register budget)
 
 struct TensorDesc {
   float* theta;
@@ -32,15 +32,23 @@ struct TensorDesc {
   float* v;
   float* u;
   int64_t numel;
-  int64_t block0;  // first block of this tensor in the group launch
+  int64_t block0;  // first chunk of this tensor in the group (= index of its first partial)
   int64_t nblocks;
-  int32_t index;  // position in the caller's tensor list (rms/eta outputs)
+  int64_t task0;   // first phase-1 task (tasks [task0, task0 + nblocks))
+  int64_t task2;   // first phase-2 task
+  int32_t index;   // position in the caller's tensor list (rms/eta outputs)
+  int32_t vec;     // all four arrays 16-byte aligned and numel % 4 == 0: float4 path
 };
 
 struct Group {
   TensorDesc t[kMaxGroup];
+  // task segments in fetch order: phase 1 of tensor k+1 precedes phase 2 of tensor k, so a
+  // phase-2 task never waits on chunks still in flight (seg = 2*k + phase)
+  int64_t seg_start[2 * kMaxGroup];
+  int16_t seg_id[2 * kMaxGroup];
   int count;
   int64_t total_blocks;
+  int64_t total_tasks;
 };
 
 struct Coeffs {
@@ -50,14 +58,18 @@ struct Coeffs {
   int32_t update_clip;
 };
 
-__device__ __forceinline__ int find_tensor(const Group& g, int64_t blk) {
+template <typename F>
+__device__ __forceinline__ int find_by(const Group& g, F key, int64_t x) {
   int lo = 0, hi = g.count - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (g.t[mid].block0 <= blk) lo = mid;
+    if (key(g.t[mid]) <= x) lo = mid;
     else hi = mid - 1;
   }
   return lo;
+}
+__device__ __forceinline__ int find_tensor(const Group& g, int64_t blk) {
+  return find_by(g, [](const TensorDesc& d) { return d.block0; }, blk);
 }
 
 // Deterministic block sum: per-warp xor-tree, then warp 0 over the 8 warp sums.
@@ -70,68 +82,179 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   double s = 0.0;
   if (threadIdx.x == 0)
     for (int i = 0; i < kThreads / 32; ++i) s = __dadd_rn(s, red[i]);
+  __syncthreads();  // red reusable
   return s;
 }
 
-__global__ void __launch_bounds__(kThreads) k_adamw_phase1(const __grid_constant__ Group grp, Coeffs c,
-                                                           const double* __restrict__ clip_ptr,
-                                                           double* __restrict__ partials) {
-  __shared__ double red[kThreads / 32];
-  const int64_t blk = blockIdx.x;
-  const TensorDesc& d = grp.t[find_tensor(grp, blk)];
-  const int64_t base = (blk - d.block0) * kChunk;
-  const double clip = clip_ptr ? *clip_ptr : 1.0;
-  double acc = 0.0;
-#pragma unroll 4
-  for (int e = 0; e < kPerThread; ++e) {
-    const int64_t i = base + e * kThreads + threadIdx.x;
-    if (i < d.numel) {
-      const double g = __dmul_rn(static_cast<double>(d.grad[i]), clip);
-      const float vn = __double2float_rn(__dadd_rn(__dmul_rn(c.b1, static_cast<double>(d.v[i])), __dmul_rn(c.omb1, g)));
-      const float un =
-          __double2float_rn(__dadd_rn(__dmul_rn(c.b2, static_cast<double>(d.u[i])), __dmul_rn(__dmul_rn(c.omb2, g), g)));
-      d.v[i] = vn;
-      d.u[i] = un;
-      const double ud = static_cast<double>(un);
-      acc = __dadd_rn(acc, __ddiv_rn(__dmul_rn(g, g), ud > c.floor_ ? ud : c.floor_));
-    }
-  }
-  const double s = block_sum(acc, red);
-  if (threadIdx.x == 0) partials[blk] = s;
+__device__ __forceinline__ uint32_t ld_acquire(const unsigned int* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
-__global__ void __launch_bounds__(kThreads) k_adamw_phase2(const __grid_constant__ Group grp, Coeffs c,
-                                                           const double* __restrict__ partials, double* rms_out,
-                                                           double* eta_out) {
-  __shared__ double red[kThreads / 32];
-  __shared__ double eta_s;
-  const int64_t blk = blockIdx.x;
-  const TensorDesc& d = grp.t[find_tensor(grp, blk)];
-  // every block of the tensor reduces the same partials in the same order -> same eta
-  double s = 0.0;
-  for (int64_t j = threadIdx.x; j < d.nblocks; j += kThreads) s = __dadd_rn(s, partials[d.block0 + j]);
-  // fixed-order combine of the per-thread strided sums
-  const double tot = block_sum(s, red);
-  if (threadIdx.x == 0) {
-    const double rms = __dsqrt_rn(__ddiv_rn(tot, static_cast<double>(d.numel)));
-    const double eta = c.update_clip ? __ddiv_rn(c.alpha, rms > 1.0 ? rms : 1.0) : c.alpha;
-    eta_s = eta;
-    if (blk == d.block0) {
-      if (rms_out) rms_out[d.index] = rms;
-      if (eta_out) eta_out[d.index] = eta;
+// Moments of one element (optimizer.cpp:142-146) and its RMS term g^2 / max(u, eps^2) (:148-157).
+__device__ __forceinline__ double moments(const Coeffs& c, double g, float& v, float& u) {
+  v = __double2float_rn(__dadd_rn(__dmul_rn(c.b1, static_cast<double>(v)), __dmul_rn(c.omb1, g)));
+  u = __double2float_rn(__dadd_rn(__dmul_rn(c.b2, static_cast<double>(u)), __dmul_rn(__dmul_rn(c.omb2, g), g)));
+  const double ud = static_cast<double>(u);
+  return __ddiv_rn(__dmul_rn(g, g), ud > c.floor_ ? ud : c.floor_);
+}
+// Parameter update of one element (optimizer.cpp:162-167).
+__device__ __forceinline__ float update(const Coeffs& c, double eta, double eta_wd, float th_f, float v, float u) {
+  const double th = static_cast<double>(th_f);
+  const double upd = __ddiv_rn(static_cast<double>(v), __dadd_rn(__dsqrt_rn(static_cast<double>(u)), c.eps));
+  return __double2float_rn(__dsub_rn(__dsub_rn(th, __dmul_rn(eta_wd, th)), __dmul_rn(eta, upd)));
+}
+
+// Phase-1 work on chunk `blk` of tensor d: moments + partial RMS sum (fixed order).
+__device__ __forceinline__ double phase1_chunk(const TensorDesc& d, const Coeffs& c, double clip, int64_t blk) {
+  const int64_t base = blk * kChunk;
+  double acc = 0.0;
+  if (d.vec) {
+    // thread owns 4 float4 groups: elements base + (e*256 + tid)*4 .. +3 (coalesced 16 B),
+    // loaded two groups at a time (register budget for 2 blocks / SM)
+#pragma unroll
+    for (int hh = 0; hh < 4 / kVecPerIter; ++hh) {
+      float4 gv[kVecPerIter], vv[kVecPerIter], uv[kVecPerIter];
+#pragma unroll
+      for (int e = 0; e < kVecPerIter; ++e) {
+        const int64_t i = base + (static_cast<int64_t>(kVecPerIter * hh + e) * kThreads + threadIdx.x) * 4;
+        if (i < d.numel) {
+          gv[e] = __ldcs(reinterpret_cast<const float4*>(d.grad + i));
+          vv[e] = __ldcg(reinterpret_cast<const float4*>(d.v + i));
+          uv[e] = __ldcg(reinterpret_cast<const float4*>(d.u + i));
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < kVecPerIter; ++e) {
+        const int64_t i = base + (static_cast<int64_t>(kVecPerIter * hh + e) * kThreads + threadIdx.x) * 4;
+        if (i < d.numel) {
+          const float ga[4] = {gv[e].x, gv[e].y, gv[e].z, gv[e].w};
+          float va[4] = {vv[e].x, vv[e].y, vv[e].z, vv[e].w};
+          float ua[4] = {uv[e].x, uv[e].y, uv[e].z, uv[e].w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const double g = clip == 1.0 ? static_cast<double>(ga[k]) : __dmul_rn(static_cast<double>(ga[k]), clip);
+            acc = __dadd_rn(acc, moments(c, g, va[k], ua[k]));
+          }
+          *reinterpret_cast<float4*>(d.v + i) = make_float4(va[0], va[1], va[2], va[3]);
+          *reinterpret_cast<float4*>(d.u + i) = make_float4(ua[0], ua[1], ua[2], ua[3]);
+        }
+      }
+    }
+  } else {
+    for (int e = 0; e < kPerThread; ++e) {
+      const int64_t i = base + e * kThreads + threadIdx.x;
+      if (i < d.numel) {
+        const double g = __dmul_rn(static_cast<double>(d.grad[i]), clip);
+        float v = d.v[i], u = d.u[i];
+        acc = __dadd_rn(acc, moments(c, g, v, u));
+        d.v[i] = v;
+        d.u[i] = u;
+      }
     }
   }
-  __syncthreads();
-  const double eta = eta_s;
+  return acc;
+}
+
+__device__ __forceinline__ void phase2_chunk(const TensorDesc& d, const Coeffs& c, double eta, int64_t blk) {
   const double eta_wd = __dmul_rn(eta, c.wd);
-  const int64_t base = (blk - d.block0) * kChunk;
-#pragma unroll 4
-  for (int e = 0; e < kPerThread; ++e) {
-    const int64_t i = base + e * kThreads + threadIdx.x;
-    if (i < d.numel) {
-      const double th = static_cast<double>(d.theta[i]);
-      const double upd = __ddiv_rn(static_cast<double>(d.v[i]), __dadd_rn(__dsqrt_rn(static_cast<double>(d.u[i])), c.eps));
-      d.theta[i] = __double2float_rn(__dsub_rn(__dsub_rn(th, __dmul_rn(eta_wd, th)), __dmul_rn(eta, upd)));
+  const int64_t base = blk * kChunk;
+  if (d.vec) {
+#pragma unroll
+    for (int hh = 0; hh < 4 / kVecPerIter; ++hh) {
+      float4 tv[kVecPerIter], vv[kVecPerIter], uv[kVecPerIter];
+#pragma unroll
+      for (int e = 0; e < kVecPerIter; ++e) {
+        const int64_t i = base + (static_cast<int64_t>(kVecPerIter * hh + e) * kThreads + threadIdx.x) * 4;
+        if (i < d.numel) {
+          tv[e] = __ldcs(reinterpret_cast<const float4*>(d.theta + i));
+          vv[e] = __ldcs(reinterpret_cast<const float4*>(d.v + i));
+          uv[e] = __ldcs(reinterpret_cast<const float4*>(d.u + i));
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < kVecPerIter; ++e) {
+        const int64_t i = base + (static_cast<int64_t>(kVecPerIter * hh + e) * kThreads + threadIdx.x) * 4;
+        if (i < d.numel) {
+          float4 o;
+          o.x = update(c, eta, eta_wd, tv[e].x, vv[e].x, uv[e].x);
+          o.y = update(c, eta, eta_wd, tv[e].y, vv[e].y, uv[e].y);
+          o.z = update(c, eta, eta_wd, tv[e].z, vv[e].z, uv[e].z);
+          o.w = update(c, eta, eta_wd, tv[e].w, vv[e].w, uv[e].w);
+          __stcs(reinterpret_cast<float4*>(d.theta + i), o);
+        }
+      }
+    }
+  } else {
+    for (int e = 0; e < kPerThread; ++e) {
+      const int64_t i = base + e * kThreads + threadIdx.x;
+      if (i < d.numel) d.theta[i] = update(c, eta, eta_wd, d.theta[i], d.v[i], d.u[i]);
+    }
+  }
+}
+
+// Persistent multi-tensor StableAdamW. Tasks, fetched in order from an atomic counter:
+// for each tensor its phase-1 chunks, then its phase-2 chunks. A phase-2 task waits until
+// every phase-1 chunk of its tensor has published its partial (all of them were fetched
+// before it, by running blocks: no deadlock), reduces the tensor's partials in a fixed order
+// (same eta in every block), and updates theta while v, u of the tensor are still in L2.
+// No launch boundary between tensors: phase 1 of tensor i+1 overlaps the tail of tensor i.
+// sync[0] = task counter, sync[1 + k] = finished phase-1 chunks of group tensor k (zeroed
+// by the launcher).
+__global__ void __launch_bounds__(kThreads, 4) k_adamw_persistent(const __grid_constant__ Group grp, Coeffs c,
+                                                               const double* __restrict__ clip_ptr,
+                                                               double* __restrict__ partials,
+                                                               unsigned int* __restrict__ sync, double* rms_out,
+                                                               double* eta_out) {
+  __shared__ double red[kThreads / 32];
+  __shared__ int64_t s_task;
+  __shared__ double s_eta;
+  const double clip = clip_ptr ? *clip_ptr : 1.0;
+  for (;;) {
+    if (threadIdx.x == 0) s_task = atomicAdd(sync, 1u);
+    __syncthreads();
+    const int64_t task = s_task;
+    __syncthreads();
+    if (task >= grp.total_tasks) break;
+    int lo = 0, hi = 2 * grp.count - 1;  // segment containing `task`
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (grp.seg_start[mid] <= task) lo = mid;
+      else hi = mid - 1;
+    }
+    const int seg = grp.seg_id[lo];
+    const int ti = seg >> 1;
+    const TensorDesc& d = grp.t[ti];
+    const int64_t local = (seg & 1) ? d.nblocks + (task - d.task2) : task - d.task0;
+    if (local < d.nblocks) {
+      const double s = block_sum(phase1_chunk(d, c, clip, local), red);
+      if (threadIdx.x == 0) {
+        partials[d.block0 + local] = s;
+        __threadfence();
+        atomicAdd(sync + 1 + ti, 1u);
+      }
+    } else {
+      const int64_t blk = local - d.nblocks;
+      if (threadIdx.x == 0) {
+        while (ld_acquire(sync + 1 + ti) < static_cast<uint32_t>(d.nblocks)) __nanosleep(100);
+      }
+      __syncthreads();
+      // every block of the tensor reduces the same partials in the same order -> same eta
+      double s = 0.0;
+      for (int64_t j = threadIdx.x; j < d.nblocks; j += kThreads) s = __dadd_rn(s, __ldcg(partials + d.block0 + j));
+      const double tot = block_sum(s, red);
+      if (threadIdx.x == 0) {
+        const double rms = __dsqrt_rn(__ddiv_rn(tot, static_cast<double>(d.numel)));
+        const double eta = c.update_clip ? __ddiv_rn(c.alpha, rms > 1.0 ? rms : 1.0) : c.alpha;
+        s_eta = eta;
+        if (blk == 0) {
+          if (rms_out) rms_out[d.index] = rms;
+          if (eta_out) eta_out[d.index] = eta;
+        }
+      }
+      __syncthreads();
+      phase2_chunk(d, c, s_eta, blk);
     }
   }
 }
@@ -140,9 +263,9 @@ __global__ void __launch_bounds__(kThreads) k_adamw_phase2(const __grid_constant
 __global__ void __launch_bounds__(kThreads) k_sumsq(const __grid_constant__ Group grp, double* __restrict__ partials,
                                                     int64_t offset) {
   __shared__ double red[kThreads / 32];
-  const int64_t blk = blockIdx.x;
-  const TensorDesc& d = grp.t[find_tensor(grp, blk)];
-  const int64_t base = (blk - d.block0) * kChunk;
+  const int64_t gblk = offset + blockIdx.x;  // global chunk index (partials slot)
+  const TensorDesc& d = grp.t[find_tensor(grp, gblk)];
+  const int64_t base = (gblk - d.block0) * kChunk;
   double acc = 0.0;
   for (int e = 0; e < kPerThread; ++e) {
     const int64_t i = base + e * kThreads + threadIdx.x;
@@ -152,7 +275,7 @@ __global__ void __launch_bounds__(kThreads) k_sumsq(const __grid_constant__ Grou
     }
   }
   const double s = block_sum(acc, red);
-  if (threadIdx.x == 0) partials[offset + blk] = s;
+  if (threadIdx.x == 0) partials[gblk] = s;
 }
 
 __global__ void k_clip_factor(const double* __restrict__ partials, int64_t n, double max_norm, double* clip) {
@@ -181,15 +304,13 @@ double beta2_warmup(int64_t t, double lambda) {  // optimizer.cpp:44-49
 std::vector<Group> make_groups(const sb_adamw_tensor* ts, int n, int64_t* total_blocks) {
   std::vector<Group> groups;
   Group cur{};
-  size_t cur_bytes = 0;
   int64_t blocks_all = 0;
+  auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   for (int i = 0; i < n; ++i) {
     const int64_t nb = (ts[i].numel + kChunk - 1) / kChunk;
-    const size_t bytes = static_cast<size_t>(ts[i].numel) * 8;
-    if (cur.count > 0 && (cur.count == kMaxGroup || cur_bytes + bytes > kGroupL2Bytes)) {
+    if (cur.count == kMaxGroup) {
       groups.push_back(cur);
       cur = Group{};
-      cur_bytes = 0;
     }
     if (nb == 0) continue;
     TensorDesc& d = cur.t[cur.count++];
@@ -198,14 +319,32 @@ std::vector<Group> make_groups(const sb_adamw_tensor* ts, int n, int64_t* total_
     d.v = ts[i].v;
     d.u = ts[i].u;
     d.numel = ts[i].numel;
-    d.block0 = cur.total_blocks;
+    d.block0 = blocks_all;  // partials are global across groups (the grad-clip pass shares them)
     d.nblocks = nb;
     d.index = i;
+    d.vec = a16(d.theta) && a16(d.grad) && a16(d.v) && a16(d.u) && (d.numel % 4 == 0);
     cur.total_blocks += nb;
-    cur_bytes += bytes;
     blocks_all += nb;
   }
   if (cur.count > 0) groups.push_back(cur);
+  for (Group& g : groups) {  // fetch order: p1(0), p1(1), p2(0), p1(2), p2(1), ..., p2(last)
+    int64_t tk = 0;
+    int ns = 0;
+    auto seg = [&](int k, int phase) {
+      g.seg_start[ns] = tk;
+      g.seg_id[ns] = static_cast<int16_t>(2 * k + phase);
+      ++ns;
+      if (phase) g.t[k].task2 = tk;
+      else g.t[k].task0 = tk;
+      tk += g.t[k].nblocks;
+    };
+    for (int k = 0; k < g.count; ++k) {
+      seg(k, 0);
+      if (k > 0) seg(k - 1, 1);
+    }
+    if (g.count > 0) seg(g.count - 1, 1);
+    g.total_tasks = tk;
+  }
   *total_blocks = blocks_all;
   return groups;
 }
@@ -216,7 +355,9 @@ extern "C" sb_status sb_stableadamw_workspace_size(const sb_adamw_tensor* tensor
   if (!bytes || (ntensors > 0 && !tensors)) return sb::fail(SB_ERR_INVALID_ARGUMENT, "optimizer_step", "null argument");
   int64_t total = 0;
   for (int i = 0; i < ntensors; ++i) total += (tensors[i].numel + kChunk - 1) / kChunk;
-  *bytes = static_cast<size_t>(total + 16) * sizeof(double);
+  // partials (one double per chunk), the grad-clip factor, sync words (task counter +
+  // per-tensor phase-1 counts of the largest group)
+  *bytes = static_cast<size_t>(total + 2) * sizeof(double) + (kMaxGroup + 2) * sizeof(unsigned int) + 64;
   return SB_OK;
 }
 
@@ -263,11 +404,18 @@ extern "C" sb_status sb_stableadamw_step(sb_handle h, const sb_adamw_tensor* ten
     k_clip_factor<<<1, kThreads, 0, h->stream>>>(partials, off, hp->max_grad_norm, clip);
     SB_LAUNCH_CHECK(op);
   }
+  // persistent task-list kernel per group; sync words (task counter + per-tensor phase-1
+  // counts) zeroed once per step
+  unsigned int* sync = reinterpret_cast<unsigned int*>(clip + 1);
+  int blocks_per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_adamw_persistent, kThreads, 0);
+  blocks_per_sm = std::max(1, blocks_per_sm);
   for (const Group& g : groups) {
-    h->launches += 2;
-    k_adamw_phase1<<<static_cast<unsigned>(g.total_blocks), kThreads, 0, h->stream>>>(
-        g, c, hp->clipping == SB_CLIP_GRAD ? clip : nullptr, partials);
-    k_adamw_phase2<<<static_cast<unsigned>(g.total_blocks), kThreads, 0, h->stream>>>(g, c, partials, rms_out, eta_out);
+    SB_CUDA_CHECK(op, cudaMemsetAsync(sync, 0, sizeof(unsigned int) * (g.count + 1), h->stream));
+    const int64_t grid = std::min<int64_t>(g.total_tasks, static_cast<int64_t>(h->num_sms) * blocks_per_sm);
+    h->launches++;
+    k_adamw_persistent<<<static_cast<unsigned>(grid), kThreads, 0, h->stream>>>(
+        g, c, hp->clipping == SB_CLIP_GRAD ? clip : nullptr, partials, sync, rms_out, eta_out);
   }
   SB_LAUNCH_CHECK(op);
   return SB_OK;
