@@ -174,12 +174,21 @@ sb_status q_columnwise(sb_handle h, const void* x, sb_dtype dt, int64_t r, int64
 sb_status q_fp8(sb_handle h, const void* x, sb_dtype dt, int64_t r, int64_t c, int64_t ldx, int fmt, int axis,
                 uint8_t* q, int64_t ldq, float* state, unsigned int* words) {
   const char* op = "quantize_fp8";
+  cudaError_t fe = cudaSuccess;
+  if (sb::launch_quantize_fp8_fast(h, x, dt, r, c, ldx, fmt, axis, words, q, ldq, state, true, &fe)) {
+    SB_TRYC(op, fe);
+    return SB_OK;
+  }
   if (axis == SB_AXIS_ROW) {
     SB_TRYC(op, sb::launch_absmax_rows(h, x, dt, r, c, ldx, words));
   } else if (axis == SB_AXIS_COLUMN) {
     SB_TRYC(op, sb::launch_absmax_columns(h, x, dt, r, c, ldx, words));
   } else {
     SB_TRYC(op, sb::launch_absmax_tensor(h, x, dt, r, c, ldx, words));
+  }
+  if (sb::launch_quantize_fp8_fast(h, x, dt, r, c, ldx, fmt, axis, words, q, ldq, state, false, &fe)) {
+    SB_TRYC(op, fe);
+    return SB_OK;
   }
   SB_TRYC(op, sb::launch_quantize_fp8(h, x, dt, r, c, ldx, fmt, axis, words, q, ldq, state));
   return SB_OK;

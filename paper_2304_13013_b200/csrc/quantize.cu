@@ -901,6 +901,151 @@ __global__ void k_quantize_fp8(const T* __restrict__ x, int64_t rows, int64_t co
   }
 }
 
+
+// fp8 payload of one 16-byte input vector with a row / tensor state (8 bf16 -> 8 bytes, 4 f32 -> 4).
+// ratio = f32(double(x)/double(s)) == __fdiv_rn(x, s) (innocuous double rounding, 53 >= 2*24+2).
+template <typename T>
+__device__ __forceinline__ uint2 fp8_vec(const uint4& v, float s, int fmt) {
+  constexpr int N = Unpack<T>::N;
+  float x[N];
+  Unpack<T>::run(v, x);
+  uint32_t b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const float ratio = __fdiv_rn(x[i], s);
+    b[i] = fmt == 0 ? fp8_snap_encode<3, 7>(ratio, 448.0f, 0x7Eu) : fp8_snap_encode<2, 15>(ratio, 57344.0f, 0x7Bu);
+  }
+  return make_uint2(b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24), b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24));
+}
+
+// Row-axis fp8 quantize, one warp per row held in registers: absmax + state + payload in one
+// pass over x (the register-resident design of k_quantize_rowwise_reg).
+template <typename T, int VPL>
+__global__ void __launch_bounds__(256) k_quantize_fp8_rows_reg(const T* __restrict__ x, int64_t rows, int nvec,
+                                                               int64_t ldx, int fmt, uint8_t* __restrict__ q,
+                                                               int64_t ldq, float* __restrict__ state, uint32_t* err) {
+  constexpr int OUTB = 16 / sizeof(T);  // payload bytes per vector
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+       row += warps) {
+    const uint4* xr = reinterpret_cast<const uint4*>(x + row * ldx);
+    uint4 v[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int i = j * 32 + lane;
+      v[j] = i < nvec ? ld_stream(xr + i) : make_uint4(0, 0, 0, 0);
+    }
+    uint32_t amax = 0;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) amax = max(amax, vec_absmax_bits<T>(v[j]));
+    amax = __reduce_max_sync(0xffffffffu, amax);
+    if (amax >= kNonFiniteBits) {
+      if (lane == 0) {
+        raise_nonfinite(err);
+        state[row] = __uint_as_float(amax);
+      }
+      continue;
+    }
+    const float st = state_from_bits(amax);
+    if (lane == 0) state[row] = st;
+    uint8_t* qr = q + row * ldq;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int i = j * 32 + lane;
+      if (i < nvec) {
+        const uint2 o = fp8_vec<T>(v[j], st, fmt);
+        if (OUTB == 8)
+          *reinterpret_cast<uint2*>(qr + i * 8) = o;
+        else
+          *reinterpret_cast<uint32_t*>(qr + i * 4) = o.x;
+      }
+    }
+  }
+}
+
+// Tensor / column-axis fp8 quantize from absmax words, 16-byte vectors, rows grid-strided by
+// block, no per-element integer division.
+template <typename T>
+__global__ void __launch_bounds__(256) k_quantize_fp8_vec(const T* __restrict__ x, int64_t rows, int64_t cols,
+                                                          int64_t ldx, int fmt, int axis,
+                                                          const unsigned int* __restrict__ words,
+                                                          uint8_t* __restrict__ q, int64_t ldq,
+                                                          float* __restrict__ state, uint32_t* err) {
+  constexpr int VEC = 16 / sizeof(T);
+  const int64_t nstate = axis == 1 ? cols : 1;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nstate;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t w = words[i];
+    if (w >= kNonFiniteBits) raise_nonfinite(err);
+    state[i] = w >= kNonFiniteBits ? __uint_as_float(w) : state_from_bits(w);
+  }
+  const int64_t nv = cols / VEC;
+  const float st = axis == 1 ? 0.0f : state_from_bits(words[0]);
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const uint4* xr = reinterpret_cast<const uint4*>(x + r * ldx);
+    for (int64_t v = threadIdx.x; v < nv; v += blockDim.x) {
+      const uint4 xv = ld_stream(xr + v);
+      uint2 o;
+      if (axis == 1) {  // per-column states: VEC distinct divisors
+        constexpr int N = Unpack<T>::N;
+        float xs[N];
+        Unpack<T>::run(xv, xs);
+        uint32_t b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const float ratio = __fdiv_rn(xs[k], state_from_bits(__ldg(words + v * VEC + k)));
+          b[k] = fmt == 0 ? fp8_snap_encode<3, 7>(ratio, 448.0f, 0x7Eu) : fp8_snap_encode<2, 15>(ratio, 57344.0f, 0x7Bu);
+        }
+        o = make_uint2(b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24), b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24));
+      } else {
+        o = fp8_vec<T>(xv, st, fmt);
+      }
+      if (VEC == 8)
+        *reinterpret_cast<uint2*>(q + r * ldq + v * 8) = o;
+      else
+        *reinterpret_cast<uint32_t*>(q + r * ldq + v * 4) = o.x;
+    }
+  }
+}
+
+template <typename T>
+bool fp8_rows_reg(sb_handle h, const T* x, int64_t rows, int nvec, int64_t ldx, int fmt, uint8_t* q, int64_t ldq,
+                  float* state) {
+  const int vpl = (nvec + 31) / 32;
+  auto go = [&](auto kern) {
+    static int bps = 0;
+    if (bps == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, 0) != cudaSuccess || bps < 1))
+      bps = 1;
+    const int64_t blocks = std::min<int64_t>((rows + 7) / 8, static_cast<int64_t>(h->num_sms) * bps);
+    kern<<<static_cast<unsigned>(blocks), 256, 0, h->stream>>>(x, rows, nvec, ldx, fmt, q, ldq, state, h->d_err);
+    return true;
+  };
+  switch (vpl) {
+    case 1: return go(k_quantize_fp8_rows_reg<T, 1>);
+    case 2: return go(k_quantize_fp8_rows_reg<T, 2>);
+    case 3:
+    case 4: return go(k_quantize_fp8_rows_reg<T, 4>);
+    case 5:
+    case 6: return go(k_quantize_fp8_rows_reg<T, 6>);
+    case 7:
+    case 8: return go(k_quantize_fp8_rows_reg<T, 8>);
+    case 9:
+    case 10:
+    case 11:
+    case 12: return go(k_quantize_fp8_rows_reg<T, 12>);
+    case 13:
+    case 14:
+    case 15:
+    case 16: return go(k_quantize_fp8_rows_reg<T, 16>);
+    case 17:
+    case 18:
+    case 19:
+    case 20: return go(k_quantize_fp8_rows_reg<T, 20>);
+    default: return false;
+  }
+}
+
 template <typename TO>
 __global__ void k_dequantize_fp8(const uint8_t* __restrict__ q, int64_t rows, int64_t cols, int64_t ldq, int fmt,
                                  const float* __restrict__ state, int axis, TO* __restrict__ y, int64_t ldy) {
@@ -1048,6 +1193,42 @@ cudaError_t launch_dequantize(sb_handle h, const int8_t* q, int64_t rows, int64_
   else
     k_dequantize<<<grid, 256, 0, h->stream>>>(q, rows, cols, ldq, state, axis, static_cast<float*>(y), ldy);
   return cudaGetLastError();
+}
+
+// Fast fp8 paths (16-byte vectorisable x, q): row axis fused in one register-resident pass
+// (returns true, nothing else to launch); tensor / column axis after their absmax kernel.
+// Returns false when the generic kernels must run.
+bool launch_quantize_fp8_fast(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                              int fmt, int axis, const unsigned int* words, uint8_t* q, int64_t ldq, float* state,
+                              bool row_fused, cudaError_t* err) {
+  const int vec = dt == SB_BF16 ? 8 : 4;
+  if (cols % vec || ldx % vec || ldq % vec || !sb::aligned(x, 16) || !sb::aligned(q, vec) || rows <= 0 || cols <= 0)
+    return false;
+  if (row_fused) {
+    if (axis != SB_AXIS_ROW) return false;
+    h->launches++;
+    const bool ok = dt == SB_BF16 ? fp8_rows_reg(h, static_cast<const __nv_bfloat16*>(x), rows,
+                                                 static_cast<int>(cols / vec), ldx, fmt, q, ldq, state)
+                                  : fp8_rows_reg(h, static_cast<const float*>(x), rows, static_cast<int>(cols / vec),
+                                                 ldx, fmt, q, ldq, state);
+    if (!ok) {
+      h->launches--;
+      return false;
+    }
+    *err = cudaGetLastError();
+    return true;
+  }
+  if (axis == SB_AXIS_ROW) return false;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(rows, static_cast<int64_t>(h->num_sms) * 8));
+  h->launches++;
+  if (dt == SB_BF16)
+    k_quantize_fp8_vec<<<grid, 256, 0, h->stream>>>(static_cast<const __nv_bfloat16*>(x), rows, cols, ldx, fmt, axis,
+                                                    words, q, ldq, state, h->d_err);
+  else
+    k_quantize_fp8_vec<<<grid, 256, 0, h->stream>>>(static_cast<const float*>(x), rows, cols, ldx, fmt, axis, words, q,
+                                                    ldq, state, h->d_err);
+  *err = cudaGetLastError();
+  return true;
 }
 
 cudaError_t launch_quantize_fp8(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,

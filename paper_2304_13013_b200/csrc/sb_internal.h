@@ -83,6 +83,9 @@ cudaError_t launch_quantize_from_words(sb_handle h, const void* x, sb_dtype dt, 
                                        int8_t* q_t, int64_t ldqt, float* state);
 cudaError_t launch_dequantize(sb_handle h, const int8_t* q, int64_t rows, int64_t cols, int64_t ldq,
                               const float* state, int axis, void* y, sb_dtype ydt, int64_t ldy);
+bool launch_quantize_fp8_fast(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
+                              int fmt, int axis, const unsigned int* words, uint8_t* q, int64_t ldq, float* state,
+                              bool row_fused, cudaError_t* err);
 cudaError_t launch_quantize_fp8(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
                                 int fmt, int axis, const unsigned int* words, uint8_t* q, int64_t ldq, float* state);
 cudaError_t launch_absmax_rows(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,

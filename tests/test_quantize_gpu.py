@@ -183,11 +183,12 @@ def test_dequantize_bit_exact(axis):
     assert np.array_equal(host(L.dequantize(q)), O.dequantize(qo, so, ax))
 
 
+@pytest.mark.parametrize("shape", [(41, 97), (40, 96), (33, 5120), (300, 1280)])  # generic + vectorised kernels
 @pytest.mark.parametrize("fmt", [L.E4M3, L.E5M2])
 @pytest.mark.parametrize("axis", [L.ROW, L.COLUMN, L.TENSOR])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
-def test_fp8_quantize_bit_exact(fmt, axis, dtype):
-    x = adversarial(41, 97, seed=fmt * 3 + axis)
+def test_fp8_quantize_bit_exact(fmt, axis, dtype, shape):
+    x = adversarial(*shape, seed=fmt * 3 + axis)
     x[4] = 0
     if dtype == torch.bfloat16:
         x = bf16(x)
