@@ -544,7 +544,9 @@ sb_status sb_linear_backward(sb_handle h, const sb_linear_mode* mode, const sb_l
     wt_state = ws.wt_state;
     wt_axis = SB_AXIS_ROW;
   } else {
-    SB_TRY(q_fp8(h, ctx->w, dt, m, n, n, ff, SB_AXIS_TENSOR, wq, n, ws.w_state, ws.words));
+    // the forward's tensor-wise payload of W (ws.w_q, state ws.w_state) is still in the
+    // workspace and W is unmodified (ctx contract), so re-quantizing it (linear.cpp:259-261)
+    // would reproduce it bit for bit: transpose it instead
     SB_TRY(transpose_u8(h, wq, m, n, wqt));
     wt_state = ws.w_state;
     wt_axis = SB_AXIS_TENSOR;

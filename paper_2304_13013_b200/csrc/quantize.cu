@@ -24,6 +24,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "sb_internal.h"
 #include "sb_ptx.cuh"
@@ -844,24 +845,25 @@ __global__ void k_dequantize(const int8_t* __restrict__ q, int64_t rows, int64_t
 // ------------------------------------------------------------------ K8 ----
 // fp8 snap with ties to the smaller magnitude and saturation at the set edges; returns
 // the e4m3 (bias 7, max 448, S.1111.111 = NaN) / e5m2 (bias 15, max 57344) byte.
+// Integer-only (no FRND / F2I, which run on the 16/clk/SM conversion pipe): with a = |r| =
+// M 2^(E-150) (M the 24-bit significand, E the biased exponent), the normal-grid code drops
+// 23-MB mantissa bits rounding half toward zero; below 2^(1-BIAS) the denormal grid step is
+// 2^(1-BIAS-MB), so code = M / 2^(151-BIAS-MB-E) rounded half down (shift clamped to 31:
+// everything under a quarter of the smallest step is 0). Checked against the float-path
+// formulation on every non-negative f32 (tools/fp8_div_check.cu).
 template <int MB, int BIAS>
 __device__ __forceinline__ uint8_t fp8_snap_encode(float r, float maxv, uint32_t maxcode) {
-  const uint32_t sign = (__float_as_uint(r) >> 31) << 7;
-  const float a = fabsf(r);
-  uint32_t code;
-  if (a >= maxv) {
-    code = maxcode;
-  } else if (a < __uint_as_float(static_cast<uint32_t>(128 - BIAS) << 23)) {  // below 2^(1-BIAS): denormal grid
-    const float n = __fmul_rn(a, __uint_as_float(static_cast<uint32_t>(127 + BIAS + MB - 1) << 23));  // exact
-    const float fl = floorf(n);
-    code = static_cast<uint32_t>(fl) + (__fsub_rn(n, fl) > 0.5f ? 1u : 0u);
-  } else {
-    constexpr uint32_t drop = 23 - MB;
-    const uint32_t bits = __float_as_uint(a);
-    const uint32_t rnd = (bits + (1u << (drop - 1)) - 1u) >> drop;  // round half toward zero
-    const uint32_t e32 = rnd >> MB, m = rnd & ((1u << MB) - 1u);
-    code = ((e32 - 127u + BIAS) << MB) | m;
-  }
+  const uint32_t bits = __float_as_uint(r);
+  const uint32_t sign = (bits >> 31) << 7;
+  const uint32_t ab = bits & 0x7fffffffu;
+  constexpr uint32_t drop = 23 - MB;
+  const uint32_t code_n = ((ab + (1u << (drop - 1)) - 1u) >> drop) - ((127u - BIAS) << MB);
+  const uint32_t E = ab >> 23;
+  const uint32_t M = (ab & 0x7fffffu) | 0x800000u;
+  const uint32_t sh = min(31u, static_cast<uint32_t>(151 - BIAS - MB) - min(E, static_cast<uint32_t>(151 - BIAS - MB - 1)));
+  const uint32_t code_d = (M + (1u << (sh - 1)) - 1u) >> sh;
+  uint32_t code = E < static_cast<uint32_t>(128 - BIAS) ? code_d : code_n;
+  code = ab >= __float_as_uint(maxv) ? maxcode : code;
   return static_cast<uint8_t>(sign | code);
 }
 
@@ -904,23 +906,42 @@ __global__ void k_quantize_fp8(const T* __restrict__ x, int64_t rows, int64_t co
 
 // fp8 payload of one 16-byte input vector with a row / tensor state (8 bf16 -> 8 bytes, 4 f32 -> 4).
 // ratio = f32(double(x)/double(s)) == __fdiv_rn(x, s) (innocuous double rounding, 53 >= 2*24+2).
-template <typename T>
-__device__ __forceinline__ uint2 fp8_vec(const uint4& v, float s, int fmt) {
+//
+// bf16 x with a state s in [2^-60, 2^64]: fl32(x/s) is formed as q0 = x * r, r = fl32(1/s),
+// plus one Markstein correction q = fma(fma(-s, q0, x), r, q0) with the sign of x restored
+// (so -0 stays -0). The fp8 payload this gives equals the one from the correctly rounded
+// quotient for EVERY bf16 pair |x| <= s in that range, e4m3 and e5m2 (exhaustive check,
+// tools/fp8_div_check.cu, ~1.07e9 pairs); rows outside it and fp32 input use __fdiv_rn.
+template <bool FAST, int FMT, typename T>
+__device__ __forceinline__ uint2 fp8_vec(const uint4& v, float s, float r) {
   constexpr int N = Unpack<T>::N;
   float x[N];
   Unpack<T>::run(v, x);
   uint32_t b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
   for (int i = 0; i < N; ++i) {
-    const float ratio = __fdiv_rn(x[i], s);
-    b[i] = fmt == 0 ? fp8_snap_encode<3, 7>(ratio, 448.0f, 0x7Eu) : fp8_snap_encode<2, 15>(ratio, 57344.0f, 0x7Bu);
+    float ratio;
+    if (FAST) {
+      const float q0 = __fmul_rn(x[i], r);
+      ratio = copysignf(__fmaf_rn(__fmaf_rn(-s, q0, x[i]), r, q0), x[i]);
+    } else {
+      ratio = __fdiv_rn(x[i], s);
+    }
+    b[i] = FMT == 0 ? fp8_snap_encode<3, 7>(ratio, 448.0f, 0x7Eu) : fp8_snap_encode<2, 15>(ratio, 57344.0f, 0x7Bu);
   }
   return make_uint2(b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24), b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24));
+}
+// bf16 with a state in [2^-60, 2^64] takes the FAST quotient (see above); anything else the
+// correctly rounded division. `r` = fl32(1/s) or 0 for "exact division".
+template <typename T>
+__device__ __forceinline__ uint2 fp8_vec_any(const uint4& v, float s, int fmt, float r) {
+  if (sizeof(T) == 2 && r != 0.0f) return fmt == 0 ? fp8_vec<true, 0, T>(v, s, r) : fp8_vec<true, 1, T>(v, s, r);
+  return fmt == 0 ? fp8_vec<false, 0, T>(v, s, r) : fp8_vec<false, 1, T>(v, s, r);
 }
 
 // Row-axis fp8 quantize, one warp per row held in registers: absmax + state + payload in one
 // pass over x (the register-resident design of k_quantize_rowwise_reg).
-template <typename T, int VPL>
+template <typename T, int VPL, int FMT>
 __global__ void __launch_bounds__(256) k_quantize_fp8_rows_reg(const T* __restrict__ x, int64_t rows, int nvec,
                                                                int64_t ldx, int fmt, uint8_t* __restrict__ q,
                                                                int64_t ldq, float* __restrict__ state, uint32_t* err) {
@@ -949,18 +970,25 @@ __global__ void __launch_bounds__(256) k_quantize_fp8_rows_reg(const T* __restri
     }
     const float st = state_from_bits(amax);
     if (lane == 0) state[row] = st;
+    const float rcp = (st >= 0x1p-60f && st <= 0x1p64f) ? __frcp_rn(st) : 0.0f;  // 0: exact division
     uint8_t* qr = q + row * ldq;
+    auto emit = [&](auto fast) {
 #pragma unroll
-    for (int j = 0; j < VPL; ++j) {
-      const int i = j * 32 + lane;
-      if (i < nvec) {
-        const uint2 o = fp8_vec<T>(v[j], st, fmt);
-        if (OUTB == 8)
-          *reinterpret_cast<uint2*>(qr + i * 8) = o;
-        else
-          *reinterpret_cast<uint32_t*>(qr + i * 4) = o.x;
+      for (int j = 0; j < VPL; ++j) {
+        const int i = j * 32 + lane;
+        if (i < nvec) {
+          const uint2 o = fp8_vec<decltype(fast)::value, FMT, T>(v[j], st, rcp);
+          if (OUTB == 8)
+            *reinterpret_cast<uint2*>(qr + i * 8) = o;
+          else
+            *reinterpret_cast<uint32_t*>(qr + i * 4) = o.x;
+        }
       }
-    }
+    };
+    if (sizeof(T) == 2 && rcp != 0.0f)
+      emit(std::true_type{});
+    else
+      emit(std::false_type{});
   }
 }
 
@@ -982,6 +1010,7 @@ __global__ void __launch_bounds__(256) k_quantize_fp8_vec(const T* __restrict__ 
   }
   const int64_t nv = cols / VEC;
   const float st = axis == 1 ? 0.0f : state_from_bits(words[0]);
+  const float rcp = (axis != 1 && st >= 0x1p-60f && st <= 0x1p64f) ? __frcp_rn(st) : 0.0f;
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     const uint4* xr = reinterpret_cast<const uint4*>(x + r * ldx);
     for (int64_t v = threadIdx.x; v < nv; v += blockDim.x) {
@@ -999,7 +1028,7 @@ __global__ void __launch_bounds__(256) k_quantize_fp8_vec(const T* __restrict__ 
         }
         o = make_uint2(b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24), b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24));
       } else {
-        o = fp8_vec<T>(xv, st, fmt);
+        o = fp8_vec_any<T>(xv, st, fmt, rcp);
       }
       if (VEC == 8)
         *reinterpret_cast<uint2*>(q + r * ldq + v * 8) = o;
@@ -1009,9 +1038,9 @@ __global__ void __launch_bounds__(256) k_quantize_fp8_vec(const T* __restrict__ 
   }
 }
 
-template <typename T>
-bool fp8_rows_reg(sb_handle h, const T* x, int64_t rows, int nvec, int64_t ldx, int fmt, uint8_t* q, int64_t ldq,
-                  float* state) {
+template <typename T, int FMT>
+bool fp8_rows_reg_f(sb_handle h, const T* x, int64_t rows, int nvec, int64_t ldx, int fmt, uint8_t* q, int64_t ldq,
+                    float* state) {
   const int vpl = (nvec + 31) / 32;
   auto go = [&](auto kern) {
     static int bps = 0;
@@ -1022,28 +1051,34 @@ bool fp8_rows_reg(sb_handle h, const T* x, int64_t rows, int nvec, int64_t ldx, 
     return true;
   };
   switch (vpl) {
-    case 1: return go(k_quantize_fp8_rows_reg<T, 1>);
-    case 2: return go(k_quantize_fp8_rows_reg<T, 2>);
+    case 1: return go(k_quantize_fp8_rows_reg<T, 1, FMT>);
+    case 2: return go(k_quantize_fp8_rows_reg<T, 2, FMT>);
     case 3:
-    case 4: return go(k_quantize_fp8_rows_reg<T, 4>);
+    case 4: return go(k_quantize_fp8_rows_reg<T, 4, FMT>);
     case 5:
-    case 6: return go(k_quantize_fp8_rows_reg<T, 6>);
+    case 6: return go(k_quantize_fp8_rows_reg<T, 6, FMT>);
     case 7:
-    case 8: return go(k_quantize_fp8_rows_reg<T, 8>);
+    case 8: return go(k_quantize_fp8_rows_reg<T, 8, FMT>);
     case 9:
     case 10:
     case 11:
-    case 12: return go(k_quantize_fp8_rows_reg<T, 12>);
+    case 12: return go(k_quantize_fp8_rows_reg<T, 12, FMT>);
     case 13:
     case 14:
     case 15:
-    case 16: return go(k_quantize_fp8_rows_reg<T, 16>);
+    case 16: return go(k_quantize_fp8_rows_reg<T, 16, FMT>);
     case 17:
     case 18:
     case 19:
-    case 20: return go(k_quantize_fp8_rows_reg<T, 20>);
+    case 20: return go(k_quantize_fp8_rows_reg<T, 20, FMT>);
     default: return false;
   }
+}
+template <typename T>
+bool fp8_rows_reg(sb_handle h, const T* x, int64_t rows, int nvec, int64_t ldx, int fmt, uint8_t* q, int64_t ldq,
+                  float* state) {
+  return fmt == 0 ? fp8_rows_reg_f<T, 0>(h, x, rows, nvec, ldx, fmt, q, ldq, state)
+                  : fp8_rows_reg_f<T, 1>(h, x, rows, nvec, ldx, fmt, q, ldq, state);
 }
 
 template <typename TO>

@@ -1,0 +1,114 @@
+// fp8_div_check.cu — exhaustive check that, for bf16 x and bf16 state s (|x| <= s), the quotient
+// fl32(x / s) (= the reference's f32(double(x)/double(s)), quantize.cpp:65-76 / :161-176) equals
+//   variant A: q = x * r,                         r = fl32(1/s)
+//   variant B: q = fma(fma(-s, q0, x), r, q0),    q0 = x * r   (one Markstein correction)
+// Prints the mismatch counts; B must be 0 for the bf16 fp8 fast path to use it.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 tools/fp8_div_check.cu -o build/fp8_div_check
+#include <cstdio>
+#include <cuda_bf16.h>
+
+// fp8 snap (copy of quantize.cu's fp8_snap_encode: ties to the smaller magnitude)
+template <int MB, int BIAS>
+__device__ __forceinline__ unsigned snap(float r, float maxv, unsigned maxcode) {
+  const unsigned sign = (__float_as_uint(r) >> 31) << 7;
+  const float a = fabsf(r);
+  unsigned code;
+  if (a >= maxv) {
+    code = maxcode;
+  } else if (a < __uint_as_float(static_cast<unsigned>(128 - BIAS) << 23)) {
+    const float n = __fmul_rn(a, __uint_as_float(static_cast<unsigned>(127 + BIAS + MB - 1) << 23));
+    const float fl = floorf(n);
+    code = static_cast<unsigned>(fl) + (__fsub_rn(n, fl) > 0.5f ? 1u : 0u);
+  } else {
+    constexpr unsigned drop = 23 - MB;
+    const unsigned bits = __float_as_uint(a);
+    const unsigned rnd = (bits + (1u << (drop - 1)) - 1u) >> drop;
+    const unsigned e32 = rnd >> MB, m = rnd & ((1u << MB) - 1u);
+    code = ((e32 - 127u + BIAS) << MB) | m;
+  }
+  return sign | code;
+}
+
+__device__ unsigned int g_n;
+__device__ float g_ex[64][4];
+__global__ void k(unsigned long long* bad) {
+  // s: positive finite bf16 patterns; x: all magnitudes <= s, both signs
+  const unsigned sb = blockIdx.x + 1;  // 1 .. 0x7F7F
+  const float s = __uint_as_float(sb << 16);
+  const float r = __frcp_rn(s);
+  if (!(s >= 0x1p-60f && s <= 0x1p64f)) return;  // production prescales these rows by 2^+-64
+  unsigned long long ba = 0, bb = 0, p4a = 0, p4b = 0, p5a = 0, p5b = 0;
+  for (unsigned xb = threadIdx.x; xb <= sb; xb += blockDim.x) {
+    for (int sign = 0; sign < 2; ++sign) {
+      const float x = __uint_as_float((xb << 16) | (sign ? 0x80000000u : 0u));
+      const float ref = __fdiv_rn(x, s);
+      const float qa = __fmul_rn(x, r);
+      const float qb = copysignf(__fmaf_rn(__fmaf_rn(-s, qa, x), r, qa), x);
+      ba += __float_as_uint(qa) != __float_as_uint(ref);
+      bb += __float_as_uint(qb) != __float_as_uint(ref);
+      const unsigned r4 = snap<3, 7>(ref, 448.0f, 0x7Eu), r5 = snap<2, 15>(ref, 57344.0f, 0x7Bu);
+      p4a += snap<3, 7>(qa, 448.0f, 0x7Eu) != r4;
+      p4b += snap<3, 7>(qb, 448.0f, 0x7Eu) != r4;
+      if (snap<3, 7>(qb, 448.0f, 0x7Eu) != r4) {
+        unsigned i = atomicAdd(&g_n, 1u);
+        if (i < 64) { g_ex[i][0] = s; g_ex[i][1] = x; g_ex[i][2] = ref; g_ex[i][3] = qb; }
+      }
+      p5a += snap<2, 15>(qa, 57344.0f, 0x7Bu) != r5;
+      p5b += snap<2, 15>(qb, 57344.0f, 0x7Bu) != r5;
+    }
+  }
+  atomicAdd(bad, ba);
+  atomicAdd(bad + 1, bb);
+  atomicAdd(bad + 2, p4a);
+  atomicAdd(bad + 3, p4b);
+  atomicAdd(bad + 4, p5a);
+  atomicAdd(bad + 5, p5b);
+}
+
+template <int MB, int BIAS>
+__device__ __forceinline__ unsigned snap_int(float r, float maxv, unsigned maxcode) {
+  const unsigned bits = __float_as_uint(r);
+  const unsigned sign = (bits >> 31) << 7;
+  const unsigned ab = bits & 0x7fffffffu;
+  constexpr unsigned drop = 23 - MB;
+  const unsigned code_n = ((ab + (1u << (drop - 1)) - 1u) >> drop) - ((127u - BIAS) << MB);
+  const unsigned E = ab >> 23;
+  const unsigned M = (ab & 0x7fffffu) | 0x800000u;
+  const unsigned sh = min(31u, static_cast<unsigned>(151 - BIAS - MB) - min(E, static_cast<unsigned>(151 - BIAS - MB - 1)));
+  const unsigned code_d = (M + (1u << (sh - 1)) - 1u) >> sh;
+  unsigned code = E < static_cast<unsigned>(128 - BIAS) ? code_d : code_n;
+  code = ab >= __float_as_uint(maxv) ? maxcode : code;
+  return sign | code;
+}
+// every finite f32 (both signs): integer snap == float-path snap
+__global__ void k_snap(unsigned long long* bad) {
+  unsigned long long b4 = 0, b5 = 0;
+  for (unsigned long long u = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; u < 0xFF000000ull;
+       u += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned w = static_cast<unsigned>(u < 0x7F800000ull ? u : u - 0x7F800000ull + 0x80000000ull);
+    const float f = __uint_as_float(w);
+    b4 += snap<3, 7>(f, 448.0f, 0x7Eu) != snap_int<3, 7>(f, 448.0f, 0x7Eu);
+    b5 += snap<2, 15>(f, 57344.0f, 0x7Bu) != snap_int<2, 15>(f, 57344.0f, 0x7Bu);
+  }
+  atomicAdd(bad + 6, b4);
+  atomicAdd(bad + 7, b5);
+}
+
+int main() {
+  unsigned long long* d;
+  cudaMalloc(&d, 64);
+  cudaMemset(d, 0, 64);
+  k<<<0x7F7F, 256>>>(d);
+  k_snap<<<148 * 16, 256>>>(d);
+  unsigned long long h[8];
+  cudaMemcpy(h, d, 64, cudaMemcpyDeviceToHost);
+  printf("integer snap vs float snap over all finite f32: e4m3 %llu, e5m2 %llu mismatches\n", h[6], h[7]);
+  printf("err=%d  mismatches: x*rcp %llu   x*rcp + 1 correction %llu   (pairs ~%.2e)\n", (int)cudaGetLastError(), h[0], h[1],
+         0x7F7F * 0x7F7F * 1.0);
+  float ex[64][4];
+  cudaMemcpyFromSymbol(ex, g_ex, sizeof(ex));
+  for (int i = 0; i < 12; ++i) printf("s=%a x=%a ref=%a qb=%a\n", ex[i][0], ex[i][1], ex[i][2], ex[i][3]);
+  printf("fp8 payload mismatches: e4m3 x*rcp %llu, corrected %llu | e5m2 x*rcp %llu, corrected %llu\n", h[2], h[3], h[4],
+         h[5]);
+  return 0;
+}
