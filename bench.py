@@ -214,6 +214,8 @@ def run_ours(args):
 
     # Segments (one CUDA graph each): forwards of all layers then, last layer first, the
     # input-gradient work and the weight gradient of each layer. seg_dw marks dW segments.
+    # The first layer's dW runs before its dX so that, under DP, the last dW all-reduce
+    # overlaps that dX instead of being exposed at the end of the step.
     segments, seg_dw = [], []
     if plain:
         segments.append(lambda: ([fwd(l) for l in layers], bwd_dx(layers[-1])))
@@ -221,9 +223,11 @@ def run_ours(args):
         for i in range(len(layers) - 1, -1, -1):
             segments.append(lambda l=layers[i]: bwd_dw(l))
             seg_dw.append(True)
-            if i > 0:
+            if i > 1:
                 segments.append(lambda l=layers[i - 1]: bwd_dx(l))
                 seg_dw.append(False)
+        segments.append(lambda: bwd_dx(layers[0]))
+        seg_dw.append(False)
     else:
         segments.append(lambda: [fwd(l) for l in layers])
         seg_dw.append(False)
