@@ -312,7 +312,7 @@ def run_ours(args):
         if os.path.exists(prof):
             with open(prof) as f:
                 traffic = json.load(f).get("bytes_per_launch")
-        roof = {"bound": "tensor", "kernel": "bf16 dW GEMM (tcgen05 kind::f16 cta_group::2, MN-major operands)",
+        roof = {"bound": "tensor", "kernel": "bf16 dW GEMM (tcgen05 kind::f16 cta_group::2, 256x384 one-wave tiles, MN-major operands)",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "peak_source": f"{pk['source']} bf16 burst (MEASURED_PEAKS.json bf16_tflops: the kernel is timed "
                                f"inside a {ms * args.steps:.0f} ms region); sustained figure "

@@ -16,6 +16,7 @@
 #include "sb_internal.h"
 #include "tc_gemm.cuh"
 #include "tc_gemm2.cuh"
+#include "tc_dw_wide.cuh"
 
 #include <cstdio>
 #include <cstdlib>
@@ -265,6 +266,68 @@ cudaError_t launch_tc(sb_handle h, const Operand& A, const Operand& B, const CUt
   return cudaGetLastError();
 }
 
+// One-wave 256 x 384 dW (tc_dw_wide.cuh) when one orientation fits the SM pairs in a single
+// wave; cudaErrorNotSupported = use the 256 x 256 split-K path. G: A operand (MN-major, m
+// wide), X: B operand (n wide); TRANS runs C = X^T G and stores C^T.
+cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, const CUtensorMap& td, int64_t m, int64_t n,
+                           int64_t T) {
+  static int env = -1;
+  if (env < 0) env = getenv("SB_DW_WIDE") ? atoi(getenv("SB_DW_WIDE")) : 1;
+  if (!env || h->gemm_path == SB_GEMM_1CTA || h->num_sms < 2) return cudaErrorNotSupported;
+  static int max_pairs = 0;
+  static cudaError_t attr_err = cudaSuccess;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    for (auto kern : {sbdw::k_dw_wide<false>, sbdw::k_dw_wide<true>}) {
+      const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sbdw::SMEM_BYTES);
+      if (e != cudaSuccess) attr_err = e;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * (h->num_sms / 2));
+    cfg.blockDim = dim3(sbtc::NUM_THREADS);
+    cfg.dynamicSmemBytes = sbdw::SMEM_BYTES;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 2;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n_ = 0;
+    if (attr_err != cudaSuccess || cudaOccupancyMaxActiveClusters(&n_, sbdw::k_dw_wide<false>, &cfg) != cudaSuccess ||
+        n_ < 1)
+      n_ = h->num_sms / 2;
+    max_pairs = n_;
+    cudaGetLastError();
+  });
+  if (attr_err != cudaSuccess) return cudaErrorNotSupported;
+  const int64_t u_direct = ((m + sbdw::WM - 1) / sbdw::WM) * ((n + sbdw::WN - 1) / sbdw::WN);
+  const int64_t u_trans = ((n + sbdw::WM - 1) / sbdw::WM) * ((m + sbdw::WN - 1) / sbdw::WN);
+  const bool trans = u_direct > max_pairs;
+  if (trans && u_trans > max_pairs) return cudaErrorNotSupported;
+  // worth it only when the 256 x 256 tiling would leave a partial wave
+  const int64_t u256 = ((m + 255) / 256) * ((n + 255) / 256);
+  if (u256 % max_pairs == 0 || (trans ? u_trans : u_direct) * 4 < max_pairs * 3) return cudaErrorNotSupported;
+  const Operand& Aop = trans ? X : G;
+  const Operand& Bop = trans ? G : X;
+  CUtensorMap ta, tb;
+  if (!encode_operand(&ta, Aop, 128, 64) || !encode_operand(&tb, Bop, 128, 64)) return cudaErrorInvalidValue;
+  sbdw::WParams p{};
+  p.M = static_cast<int>(trans ? n : m);
+  p.N = static_cast<int>(trans ? m : n);
+  p.K = static_cast<int>(T);
+  p.tiles_m = static_cast<int>((p.M + sbdw::WM - 1) / sbdw::WM);
+  p.tiles_n = static_cast<int>((p.N + sbdw::WN - 1) / sbdw::WN);
+  const int units = p.tiles_m * p.tiles_n;
+  const int grid = 2 * (units < max_pairs ? units : max_pairs);
+  h->launches++;
+  if (trans)
+    sbdw::k_dw_wide<true><<<grid, sbtc::NUM_THREADS, sbdw::SMEM_BYTES, h->stream>>>(ta, tb, td, p);
+  else
+    sbdw::k_dw_wide<false><<<grid, sbtc::NUM_THREADS, sbdw::SMEM_BYTES, h->stream>>>(ta, tb, td, p);
+  return cudaGetLastError();
+}
+
 bool out_tmap(CUtensorMap* m, sb_dtype dt, void* out, int64_t M, int64_t N) {
   if (dt == SB_BF16)
     return sb::encode_tmap_2d(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, out, N, M, N * 2, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -380,6 +443,11 @@ sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t 
                     static_cast<uint64_t>(m * 2), true, 64};
     const Operand B{x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, static_cast<uint64_t>(n), static_cast<uint64_t>(b),
                     static_cast<uint64_t>(n * 2), true, 64};
+    if (!accumulate) {
+      const cudaError_t we = launch_dw_wide(h, A, B, td, m, n, b);
+      if (we == cudaSuccess) return SB_OK;
+      if (we != cudaErrorNotSupported) return cuda_fail(op, we);
+    }
     sbtc::Params p{};
     p.M = static_cast<int>(m);
     p.N = static_cast<int>(n);

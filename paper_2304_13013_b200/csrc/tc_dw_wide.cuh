@@ -1,0 +1,219 @@
+// tc_dw_wide.cuh — one-wave weight-gradient GEMM: dW = G^T X (linear.cpp:193-195) on
+// cta_group::2 with 256 x 384 pair tiles, bf16 MN-major operands read in place (K = T tokens),
+// fp32 raw accumulators stored once (no split-K, no memset, no reduce-add).
+//
+// Why: at the C2/C3 shapes the 256 x 256 tiling gives 100 tiles for 74 SM pairs, so the
+// 2-CTA GEMM needs split-K = 2 (200 units, 2.7 waves, 90% wave efficiency, a 26 MB memset and
+// fp32 reduce-adds). 256 x 384 tiles give 5 x 14 = 70 units: one wave, 95% of the pairs busy,
+// every output element written once. For dW [5120 x 1280] the GEMM is run transposed
+// (C = X^T G, M = n, N = m) and the epilogue writes C^T, so both MLP weight gradients map to
+// 70 tiles.
+//
+// Per k-step of 16 tokens the leader issues two MMAs into one 384-column TMEM accumulator:
+//   MMA a: N = 256 over B columns [0, 256)   (CTA r holds columns 128r .. 128r+127)
+//   MMA b: N = 128 over B columns [256, 384) (CTA r holds columns 256+64r .. 256+64r+63)
+// Stages hold 64 tokens: A 128 MN x 64 k (2 SW128 boxes), B 192 MN x 64 k (3 boxes) = 40 KB
+// per CTA, 4 stages. Synchronisation as tc_gemm2.cuh (leader-only full barrier with both
+// CTAs' bytes, multicast commits to both CTAs' empty barriers).
+#pragma once
+#include "tc_gemm2.cuh"
+
+namespace sbdw {
+
+using namespace sbtc;
+using sbtc2::cluster_sync;
+using sbtc2::commit_mc;
+using sbtc2::cta_rank;
+using sbtc2::mbar_wait_cluster;
+using sbtc2::tma_load_2sm;
+
+constexpr int WN = 384;          // pair tile columns
+constexpr int WM = 256;          // pair tile rows
+constexpr int KROWS = 64;        // tokens per stage
+constexpr int BOX = 8192;        // 64 MN x 64 k-rows bf16
+constexpr int A_BYTES = 2 * BOX;
+constexpr int B_BYTES = 3 * BOX;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int NSTAGES = 4;
+constexpr int SMEM_BYTES = NSTAGES * STAGE_BYTES + EPI_WARPS * EPI_BUF_BYTES + 1024 + 256;
+static_assert(SMEM_BYTES <= MAX_DYN_SMEM, "shared memory budget");
+
+struct WParams {
+  int M, N, K;  // GEMM shape (TRANS: M = n, N = m)
+  int tiles_m, tiles_n;
+};
+
+__device__ __forceinline__ void mma_f16_2(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+               "l"(a), "l"(b), "r"(idesc), "r"(acc)
+               : "memory");
+}
+
+// TRANS: the accumulator row (GEMM row = n index) / column (m index) block of 32 x 32 is
+// written to D[m][n] through a transposed staging tile: lane t (row t) stores its 32 values
+// down column t of a [32 m][32 n] fp32 tile (SW128 layout of the D tensor map; for a fixed
+// register index the 32 lanes fill one 128-byte row, so the stores are bank-conflict free).
+template <bool TRANS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    k_dw_wide(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmD, const WParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + NSTAGES * A_BYTES;
+  uint8_t* smem_epi = smem + NSTAGES * STAGE_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_epi + EPI_WARPS * EPI_BUF_BYTES);
+  uint64_t* empty_bar = full_bar + NSTAGES;
+  uint64_t* tfull_bar = empty_bar + NSTAGES;
+  uint64_t* tempty_bar = tfull_bar + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int num_units = p.tiles_m * p.tiles_n;
+  const int k_blocks = (p.K + KROWS - 1) / KROWS;
+
+  if (warp == 0 && lane == 0) {
+    sbptx::tma_prefetch_desc(&tmA);
+    sbptx::tma_prefetch_desc(&tmB);
+    sbptx::tma_prefetch_desc(&tmD);
+    for (int s = 0; s < NSTAGES; ++s) {
+      sbptx::mbar_init(&full_bar[s], 1);
+      sbptx::mbar_init(&empty_bar[s], 1);
+    }
+    sbptx::mbar_init(tfull_bar, 1);
+    sbptx::mbar_init(tempty_bar, 2 * EPI_WARPS);
+    sbptx::fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sbptx::smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  sbptx::tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  sbptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------------------------------------------------------- producer (both CTAs)
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = pair; u < num_units; u += npairs) {
+      const int m0 = (u % p.tiles_m) * WM, n0 = (u / p.tiles_m) * WN;
+      const int am0 = m0 + static_cast<int>(rank) * BM;
+      const int bn_a = n0 + static_cast<int>(rank) * 128;      // MMA a: 2 chunks of 64
+      const int bn_b = n0 + 256 + static_cast<int>(rank) * 64;  // MMA b: 1 chunk
+      for (int kb = 0; kb < k_blocks; ++kb) {
+        sbptx::mbar_wait(&empty_bar[stage], phase ^ 1u);
+        if (rank == 0) sbptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * STAGE_BYTES);
+        uint8_t* sa = smem_a + stage * A_BYTES;
+        uint8_t* sb = smem_b + stage * B_BYTES;
+        const int k0 = kb * KROWS;
+        tma_load_2sm(&tmA, &full_bar[stage], sa, am0, k0);
+        tma_load_2sm(&tmA, &full_bar[stage], sa + BOX, am0 + 64, k0);
+        tma_load_2sm(&tmB, &full_bar[stage], sb, bn_a, k0);
+        tma_load_2sm(&tmB, &full_bar[stage], sb + BOX, bn_a + 64, k0);
+        tma_load_2sm(&tmB, &full_bar[stage], sb + 2 * BOX, bn_b, k0);
+        if (++stage == NSTAGES) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // --------------------------------------------------------------- MMA issue (leader)
+    if (rank == 0 && lane == 0) {
+      // bf16 x bf16 -> f32, both operands MN-major, M = 256 (pair)
+      const uint32_t id_a = sbptx::make_idesc(1, 1, 1, 1, 1, WM, 256);
+      const uint32_t id_b = sbptx::make_idesc(1, 1, 1, 1, 1, WM, 128);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int u = pair; u < num_units; u += npairs, ++it) {
+        mbar_wait_cluster(tempty_bar, (it & 1) ^ 1u);
+        sbptx::tc_fence_after();
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          sbptx::mbar_wait(&full_bar[stage], phase);
+          sbptx::tc_fence_after();
+          const uint32_t a_addr = sbptx::smem_u32(smem_a + stage * A_BYTES);
+          const uint32_t b_addr = sbptx::smem_u32(smem_b + stage * B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < KROWS / 16; ++kk) {
+            const uint64_t ad = sbptx::umma_desc_sw128(a_addr + kk * 2048, BOX, 1024);
+            const uint32_t acc = (kb | kk) != 0;
+            mma_f16_2(tmem_base, ad, sbptx::umma_desc_sw128(b_addr + kk * 2048, BOX, 1024), id_a, acc);
+            mma_f16_2(tmem_base + 256, ad, sbptx::umma_desc_sw128(b_addr + 2 * BOX + kk * 2048, BOX, 1024), id_b,
+                      acc);
+          }
+          commit_mc(&empty_bar[stage]);
+          if (++stage == NSTAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        commit_mc(tfull_bar);
+      }
+    }
+  } else if (warp >= 4) {
+    // --------------------------------------------------------------- epilogue (both CTAs)
+    const int ew = warp & 3;             // TMEM lane quarter
+    const int half = (warp - 4) >> 2;    // column half: [192 half, 192 half + 192)
+    uint8_t* buf = smem_epi + (warp - 4) * EPI_BUF_BYTES;
+    int it = 0;
+    for (int u = pair; u < num_units; u += npairs, ++it) {
+      const int m0 = (u % p.tiles_m) * WM, n0 = (u / p.tiles_m) * WN;
+      const int rm0 = m0 + static_cast<int>(rank) * BM + ew * 32;  // this warp's 32 GEMM rows
+      sbptx::mbar_wait(tfull_bar, it & 1);
+      sbptx::tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + half * 192;
+#pragma unroll 1
+      for (int c = 0; c < 6; ++c) {  // 6 x 32 columns
+        uint32_t r[32];
+        sbptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
+        sbptx::tmem_ld_wait();
+        if (c == 5) {
+          sbptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) sbtc::arrive_leader(tempty_bar);
+        }
+        const int col0 = n0 + half * 192 + c * 32;  // GEMM column of r[0]
+        if (col0 >= p.N || rm0 >= p.M) continue;   // warp-uniform
+        if (lane == 0) sbptx::tma_store_wait_read<0>();
+        __syncwarp();
+        if (TRANS) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int chunk = (lane >> 2) ^ (j & 7);
+            *reinterpret_cast<uint32_t*>(buf + j * 128 + chunk * 16 + (lane & 3) * 4) = r[j];
+          }
+        } else {
+          stage_row128(buf, lane, r);
+        }
+        sbptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (TRANS)
+            sbptx::tma_store_2d(&tmD, buf, rm0, col0);  // D[m = col][n = row]
+          else
+            sbptx::tma_store_2d(&tmD, buf, col0, rm0);
+          sbptx::tma_store_commit();
+        }
+      }
+    }
+    if (lane == 0) sbptx::tma_store_wait_all<0>();
+  }
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    sbptx::tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS) : "memory");
+  }
+}
+
+}  // namespace sbdw

@@ -116,6 +116,26 @@ def test_wgrad_bf16_tensor_core(T, m, n, gemm_path):
     assert rel_err(host(dw2), 2 * want) < tol
 
 
+@pytest.mark.parametrize("T,m,n", [(1024, 1280, 5120), (1024, 5120, 1280), (640, 1024, 6144), (200, 1280, 4992),
+                                   (520, 4992, 1280)])
+def test_wgrad_one_wave_wide_tiles(T, m, n):
+    """The 256 x 384 one-wave dW kernel (tc_dw_wide.cuh), direct and transposed-store forms,
+    incl. partial last tiles; against fp64, and equal to the split-K 256 x 256 path within fp32."""
+    rng = np.random.default_rng(m + n + T)
+    g = bf16(rng.standard_normal((T, m)).astype(np.float32))
+    x = bf16(rng.standard_normal((T, n)).astype(np.float32))
+    want = g.astype(np.float64).T @ x.astype(np.float64)
+    dw = host(L.wgrad(dev(g, torch.bfloat16), dev(x, torch.bfloat16), exact=False))
+    assert rel_err(dw, want) < 2e-5
+    h = A.handle()
+    h.set_gemm_path(A.SB_GEMM_1CTA)
+    try:
+        dw1 = host(L.wgrad(dev(g, torch.bfloat16), dev(x, torch.bfloat16), exact=False))
+    finally:
+        h.set_gemm_path(A.SB_GEMM_AUTO)
+    assert rel_err(dw, dw1) < 2e-6
+
+
 @pytest.mark.parametrize("T,m,n", [(37, 29, 53), (256, 64, 96)])
 def test_wgrad_exact_bit_identical(T, m, n):
     rng = np.random.default_rng(5)

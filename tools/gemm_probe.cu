@@ -9,6 +9,18 @@
 #include "../paper_2304_13013_b200/csrc/sb_internal.h"
 
 extern "C" void sb_probe_read(unsigned long long* out, int n);
+
+// pseudo-random operand bytes (realistic tensor-core power: constant data under-reports it)
+__global__ void k_fill(uint8_t* p, size_t n, int bf16) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u ^ 0x9e3779b9u;
+    h ^= h >> 15;
+    h *= 2246822519u;
+    h ^= h >> 13;
+    // bf16: keep exponents near 1.0 (0x3f00..0x3fff | sign) in the high byte of each element
+    p[i] = bf16 ? ((i & 1) ? (uint8_t)(0x3f | (h & 0x80)) : (uint8_t)(h >> 8)) : (uint8_t)(h % 255 - 127 + 256);
+  }
+}
 extern "C" void sb_probe_reset();
 
 int main(int argc, char** argv) {
@@ -27,8 +39,8 @@ int main(int argc, char** argv) {
   cudaMalloc(&sa, M * 4);
   cudaMalloc(&sbv, 4);
   cudaMalloc(&out, M * N * 4);
-  cudaMemset(a, 1, (kind == 0 ? M * K : K * M) * esz);
-  cudaMemset(b, 1, (kind == 0 ? N * K : K * N) * esz);
+  k_fill<<<1184, 256>>>((uint8_t*)a, (kind == 0 ? M * K : K * M) * esz, kind);
+  k_fill<<<1184, 256>>>((uint8_t*)b, (kind == 0 ? N * K : K * N) * esz, kind);
   std::vector<float> ones(M, 1.0f);
   cudaMemcpy(sa, ones.data(), M * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(sbv, ones.data(), 4, cudaMemcpyHostToDevice);
