@@ -151,7 +151,7 @@ sb_status check_h(sb_handle h, const char* op) {
 }
 
 // ------------------------------------------------------------ quantize ops
-// `word` must hold 2 device words.
+// `word` must hold 4 device words.
 sb_status q_tensorwise(sb_handle h, const void* x, sb_dtype dt, int64_t r, int64_t c, int64_t ldx, int8_t* q,
                        int64_t ldq, int8_t* qt, int64_t ldqt, float* state, unsigned int* word) {
   cudaError_t fe = cudaSuccess;
@@ -300,7 +300,7 @@ sb_status sb_quantize_tensorwise(sb_handle h, const void* x, sb_dtype dt, int64_
   SB_TRY(check_h(h, op));
   if (rows <= 0 || cols <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty matrix");
   if (!float_dtype(dt) || !x || (!q && !q_t) || !state || ldx < cols) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
-  unsigned int* words = sb::scratch(h, 2);
+  unsigned int* words = sb::scratch(h, 4);
   if (!words) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed");
   return q_tensorwise(h, x, dt, rows, cols, ldx, q, ldq, q_t, ldqt, state, words);
 }

@@ -698,13 +698,15 @@ __global__ void __launch_bounds__(256) k_quantize_from_words(const T* __restrict
 }
 
 // ------------------------------------------------------------- K2+K3 fused ----
-// Tensor-wise quantize (+ transposed payload) in ONE launch: phase 1 reduces max|x| over a
-// grid-stride share of the 16-byte vectors (atomicMax of bit patterns into sync[0]); a
-// grid-wide arrival counter (sync[1]; all CTAs are co-resident by construction of the grid)
-// separates it from phase 2, which re-reads x (L2-resident: W is <= tens of MB) in 64 x 64
-// tiles and writes q and/or q_t from one read (quantize.cpp:139-159). bf16 input takes the
-// one-FMA exact path (qvec_bf16_fast: the tensor state is a bf16 value >= every |x|).
-// sync[0..1] must be zero at launch (the launcher memsets them).
+// Tensor-wise quantize (+ transposed payload) in ONE launch, as an ordered task list fetched
+// from an atomic counter: first the absmax tasks (64-row slabs, atomicMax of bit patterns
+// into sync[0], completion counted in sync[2]), then the 64 x 64 quantize tiles, which wait
+// for the count and re-read x from L2 (W is <= tens of MB), writing q and/or q_t from one read
+// (quantize.cpp:139-159). A tile task only ever waits on absmax tasks fetched before it by
+// running blocks, so no co-residency is assumed (safe next to other kernels on other streams).
+// bf16 input takes the one-FMA exact path (qvec_bf16_fast: the tensor state is a bf16 value
+// >= every |x|). sync[0..3] are zeroed by the launcher (sync[1] task counter, sync[3] "state
+// written" flag).
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const unsigned int* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -719,44 +721,71 @@ __global__ void __launch_bounds__(256) k_quantize_tensorwise_fused(const T* __re
                                                                     uint32_t* err) {
   constexpr int VEC = 16 / sizeof(T);
   __shared__ uint32_t red[8];
+  __shared__ int64_t s_task;
   __shared__ __align__(16) int8_t tile[64][64 + 16];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t vpr = cols / VEC;  // vectors per row
-  const int64_t nvec = rows * vpr;
-  // ---- phase 1: absmax
-  uint32_t m = 0;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nvec;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = i / vpr, v = i - r * vpr;
-    m = max(m, vec_absmax_bits<T>(ld_stream(reinterpret_cast<const uint4*>(x + r * ldx) + v)));
-  }
-  m = __reduce_max_sync(0xffffffffu, m);
-  if (lane == 0) red[warp] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int i = 1; i < 8; ++i) m = max(m, red[i]);
-    if (m) atomicMax(sync, m);
-    __threadfence();
-    atomicAdd(sync + 1, 1u);
-    while (ld_acquire_gpu(sync + 1) < gridDim.x) __nanosleep(64);
-    red[0] = ld_acquire_gpu(sync);
-  }
-  __syncthreads();
-  // ---- phase 2: quantize 64 x 64 tiles
-  const uint32_t wb = red[0];
-  if (wb >= kNonFiniteBits) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      raise_nonfinite(err);
-      state[0] = __uint_as_float(wb);
-    }
-    return;
-  }
-  const float st = state_from_bits(wb);
-  if (blockIdx.x == 0 && threadIdx.x == 0) state[0] = st;
-  const Scale sc = make_scale(st);
-  const bool fast = sizeof(T) == 2 && sc.pre == 1.0f;
+  const int vpr = static_cast<int>(cols / VEC);  // vectors per row
+  // phase-1 tasks: absmax over slabs of ~32 KB of whole rows
+  const int64_t slab_ = 32768 / (cols * static_cast<int64_t>(sizeof(T)));
+  const int slab = static_cast<int>(slab_ > 1 ? slab_ : 1);
+  const int64_t n_abs = (rows + slab - 1) / slab;
   const int64_t tr = (rows + 63) / 64, tc = (cols + 63) / 64;
-  for (int64_t t = blockIdx.x; t < tr * tc; t += gridDim.x) {
+  const int64_t n_tasks = n_abs + tr * tc;
+  bool have_state = false;
+  float st = 0.0f;
+  Scale sc{};
+  bool fast = false;
+  for (;;) {
+    if (threadIdx.x == 0) s_task = atomicAdd(sync + 1, 1u);
+    __syncthreads();
+    const int64_t task = s_task;
+    __syncthreads();
+    if (task >= n_tasks) break;
+    if (task < n_abs) {
+      // ---- phase 1 task: absmax of rows [slab task, slab task + slab)
+      const int64_t r0 = task * slab;
+      const int nr = static_cast<int>(rows - r0 < slab ? rows - r0 : slab);
+      uint32_t m = 0;
+      for (int i = threadIdx.x; i < nr * vpr; i += blockDim.x) {
+        const int r = i / vpr, v = i - r * vpr;
+        m = max(m, vec_absmax_bits<T>(ld_stream(reinterpret_cast<const uint4*>(x + (r0 + r) * ldx) + v)));
+      }
+      m = __reduce_max_sync(0xffffffffu, m);
+      if (lane == 0) red[warp] = m;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int i = 1; i < 8; ++i) m = max(m, red[i]);
+        if (m) atomicMax(sync, m);
+        __threadfence();
+        atomicAdd(sync + 2, 1u);
+      }
+      __syncthreads();
+      continue;
+    }
+    // ---- phase 2 task: one 64 x 64 tile; every phase-1 task was fetched before this one by
+    // a running block, so the wait below always ends (no co-residency assumption)
+    if (!have_state) {
+      if (threadIdx.x == 0) {
+        while (ld_acquire_gpu(sync + 2) < static_cast<uint32_t>(n_abs)) __nanosleep(64);
+        red[0] = ld_acquire_gpu(sync);
+      }
+      __syncthreads();
+      const uint32_t wb = red[0];
+      __syncthreads();
+      if (wb >= kNonFiniteBits) {
+        if (threadIdx.x == 0 && atomicOr(sync + 3, 1u) == 0u) {
+          raise_nonfinite(err);
+          state[0] = __uint_as_float(wb);
+        }
+        break;
+      }
+      st = state_from_bits(wb);
+      if (threadIdx.x == 0 && atomicOr(sync + 3, 1u) == 0u) state[0] = st;
+      sc = make_scale(st);
+      fast = sizeof(T) == 2 && sc.pre == 1.0f;
+      have_state = true;
+    }
+    const int64_t t = task - n_abs;
     const int64_t r0 = (t / tc) * 64, c0 = (t % tc) * 64;
     // 64 rows x 64 cols: thread -> (row lr = pass*32 + tid/8, 8-column group tid%8) for bf16,
     // (row pass*16 + tid/16, 4-column group tid%16) for fp32
@@ -1159,11 +1188,12 @@ bool launch_quantize_tensorwise_fused(sb_handle h, const void* x, sb_dtype dt, i
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_quantize_tensorwise_fused<__nv_bfloat16>, 256, 0);
     else
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_quantize_tensorwise_fused<float>, 256, 0);
-    cap = std::max(1, std::min(b, 4)) * h->num_sms;  // every CTA co-resident: the grid barrier needs it
+    cap = std::max(1, std::min(b, 4)) * h->num_sms;
   }
-  const int64_t tiles = ((rows + 63) / 64) * ((cols + 63) / 64);
-  const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(tiles, cap)));
-  *err = cudaMemsetAsync(sync, 0, 2 * sizeof(unsigned int), h->stream);
+  const int64_t slab = std::max<int64_t>(1, 32768 / (cols * static_cast<int64_t>(dt == SB_BF16 ? 2 : 4)));
+  const int64_t tasks = (rows + slab - 1) / slab + ((rows + 63) / 64) * ((cols + 63) / 64);
+  const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(tasks, cap)));
+  *err = cudaMemsetAsync(sync, 0, 4 * sizeof(unsigned int), h->stream);
   if (*err != cudaSuccess) return true;
   h->launches++;
   if (dt == SB_BF16)

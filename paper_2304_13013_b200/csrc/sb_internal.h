@@ -69,7 +69,7 @@ cudaError_t launch_quantize_rowwise(sb_handle h, const void* x, sb_dtype dt, int
                                     int8_t* q, int64_t ldq, float* state);
 cudaError_t launch_absmax_tensor(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ldx,
                                  unsigned int* word);
-// Tensor-wise quantize in one launch (absmax, grid barrier, quantize + transpose); sync = 2
+// Tensor-wise quantize in one launch (absmax tasks, then quantize + transpose tasks); sync = 4
 // device words. Returns false (nothing launched) when x is not 16-byte vectorisable.
 bool launch_quantize_tensorwise_fused(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols,
                                       int64_t ldx, int8_t* q, int64_t ldq, int8_t* q_t, int64_t ldqt, float* state,
