@@ -236,6 +236,13 @@ sb_status sb_destroy(sb_handle h) {
   if (h->d_err) cudaFree(h->d_err);
   if (h->d_scratch) cudaFree(h->d_scratch);
   if (h->dev_pool) cudaFree(h->dev_pool);
+  if (h->s_in) {
+    cudaStreamDestroy(h->s_in);
+    cudaStreamDestroy(h->s_out);
+    for (auto& row : h->hp_ev)
+      for (auto& e : row) cudaEventDestroy(e);
+    cudaEventDestroy(h->hp_start);
+  }
   delete h;
   return SB_OK;
 }
@@ -594,8 +601,13 @@ sb_status sb_switchback_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, co
   if (mode->variant != SB_SWITCHBACK || mode->format != SB_INT8)
     return sb::fail(SB_ERR_UNSUPPORTED, op, "host pipeline implements SwitchBack int8");
   const size_t es = sb::dt_size(dt);
-  const int64_t chunk = std::min<int64_t>(b, 8192);
-  // device layout: W, W_q, W_qT, dW, 2 x {x, g, y, dx, x_q, g_q, states}
+  // Token rows stream through NS slots of `chunk` rows: H2D of chunk i+2 | kernels of chunk i |
+  // D2H of chunk i-1 run concurrently; Y of a chunk is copied out as soon as its forward GEMM
+  // is done, dX after the backward. Small chunks keep the un-overlapped pipeline fill (first
+  // H2D) and drain (last D2H, the dW copy) short; 4096 rows still fill the SM pairs.
+  constexpr int NS = 3;
+  const int64_t chunk = std::min<int64_t>(b, 4096);
+  // device layout: W, W_q, W_qT, dW, states/words, NS x {x, g, y, dx, x_q, g_q, x states, g states}
   Carve c{nullptr};
   auto layout = [&](Carve& cv, void** P) {
     P[0] = cv.take<uint8_t>(m * n * es);
@@ -604,7 +616,7 @@ sb_status sb_switchback_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, co
     P[3] = cv.take<float>(m * n);
     P[4] = cv.take<float>(8);
     P[5] = cv.take<unsigned int>(8);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NS; ++s) {
       P[6 + 8 * s + 0] = cv.take<uint8_t>(chunk * n * es);
       P[6 + 8 * s + 1] = cv.take<uint8_t>(chunk * m * es);
       P[6 + 8 * s + 2] = cv.take<uint8_t>(chunk * m * es);
@@ -615,7 +627,7 @@ sb_status sb_switchback_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, co
       P[6 + 8 * s + 7] = cv.take<float>(chunk);
     }
   };
-  void* P[22];
+  void* P[6 + 8 * NS];
   layout(c, P);
   const size_t need = c.off + 256;
   if (need > h->dev_pool_bytes) {
@@ -628,6 +640,13 @@ sb_status sb_switchback_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, co
     SB_CUDA_CHECK(op, cudaMalloc(&h->dev_pool, need));
     h->dev_pool_bytes = need;
   }
+  if (!h->s_in) {
+    SB_CUDA_CHECK(op, cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
+    SB_CUDA_CHECK(op, cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
+    for (auto& row : h->hp_ev)
+      for (auto& e : row) SB_CUDA_CHECK(op, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    SB_CUDA_CHECK(op, cudaEventCreateWithFlags(&h->hp_start, cudaEventDisableTiming));
+  }
   Carve c2{static_cast<uint8_t*>(h->dev_pool)};
   layout(c2, P);
   void* dW_ = P[0];
@@ -636,40 +655,36 @@ sb_status sb_switchback_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, co
   float* dwd = static_cast<float*>(P[3]);
   float* wstate = static_cast<float*>(P[4]);
   unsigned int* words = static_cast<unsigned int*>(P[5]);
+  cudaEvent_t* ev_in = h->hp_ev[0];
+  cudaEvent_t* ev_y = h->hp_ev[1];
+  cudaEvent_t* ev_comp = h->hp_ev[2];
+  cudaEvent_t* ev_out = h->hp_ev[3];
 
-  cudaStream_t comp = h->stream, s_in, s_out;
-  SB_CUDA_CHECK(op, cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
-  SB_CUDA_CHECK(op, cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
-  cudaEvent_t ev_in[2], ev_comp[2], ev_out[2], ev_start;
-  for (int s = 0; s < 2; ++s) {
-    cudaEventCreateWithFlags(&ev_in[s], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev_comp[s], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev_out[s], cudaEventDisableTiming);
-  }
-  cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
-  cudaEventRecord(ev_start, comp);
-  cudaStreamWaitEvent(s_in, ev_start, 0);
-  cudaStreamWaitEvent(s_out, ev_start, 0);
+  cudaStream_t comp = h->stream, s_in = h->s_in, s_out = h->s_out;
+  cudaEventRecord(h->hp_start, comp);
+  cudaStreamWaitEvent(s_in, h->hp_start, 0);
+  cudaStreamWaitEvent(s_out, h->hp_start, 0);
   sb_status st = SB_OK;
   const int64_t nchunks = (b + chunk - 1) / chunk;
   auto h2d = [&](int64_t i) {
-    const int s = static_cast<int>(i & 1);
+    const int s = static_cast<int>(i % NS);
     const int64_t r0 = i * chunk, rows = std::min(chunk, b - r0);
-    if (i >= 2) cudaStreamWaitEvent(s_in, ev_comp[s], 0);
+    if (i >= NS) cudaStreamWaitEvent(s_in, ev_comp[s], 0);  // slot's x, g consumed by chunk i-NS
     cudaMemcpyAsync(P[6 + 8 * s + 0], static_cast<const uint8_t*>(x) + r0 * n * es, rows * n * es, cudaMemcpyHostToDevice, s_in);
     cudaMemcpyAsync(P[6 + 8 * s + 1], static_cast<const uint8_t*>(g) + r0 * m * es, rows * m * es, cudaMemcpyHostToDevice, s_in);
     cudaEventRecord(ev_in[s], s_in);
   };
-  // W in, quantized once (both layouts)
+  // W in, quantized once (both layouts), while the first chunks stream in
+  h2d(0);
   cudaMemcpyAsync(dW_, w, m * n * es, cudaMemcpyHostToDevice, comp);
   st = q_tensorwise(h, dW_, dt, m, n, n, wq, n, wqt, m, wstate, words);
-  h2d(0);
+  for (int64_t i = 1; i < std::min<int64_t>(NS - 1, nchunks); ++i) h2d(i);
   for (int64_t i = 0; i < nchunks && st == SB_OK; ++i) {
-    const int s = static_cast<int>(i & 1);
+    const int s = static_cast<int>(i % NS);
     const int64_t r0 = i * chunk, rows = std::min(chunk, b - r0);
-    if (i + 1 < nchunks) h2d(i + 1);
+    if (i + NS - 1 < nchunks) h2d(i + NS - 1);
     cudaStreamWaitEvent(comp, ev_in[s], 0);
-    if (i >= 2) cudaStreamWaitEvent(comp, ev_out[s], 0);
+    if (i >= NS) cudaStreamWaitEvent(comp, ev_out[s], 0);  // slot's y, dx copied out
     void* xd = P[6 + 8 * s + 0];
     void* gd = P[6 + 8 * s + 1];
     void* yd = P[6 + 8 * s + 2];
@@ -680,29 +695,23 @@ sb_status sb_switchback_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, co
     float* gs = static_cast<float*>(P[6 + 8 * s + 7]);
     if (sb::launch_quantize_rowwise(h, xd, dt, rows, n, n, xq, n, xs) != cudaSuccess) st = sb::cuda_fail(op, cudaGetLastError());
     if (st == SB_OK) st = sb::gemm_i8(h, xq, xs, wq, wstate, SB_SCALE_ROW_TENSOR, rows, m, n, yd, dt, mode->exact);
+    cudaEventRecord(ev_y[s], comp);
     if (st == SB_OK && sb::launch_quantize_rowwise(h, gd, dt, rows, m, m, gq, m, gs) != cudaSuccess)
       st = sb::cuda_fail(op, cudaGetLastError());
     if (st == SB_OK) st = sb::gemm_i8(h, gq, gs, wqt, wstate, SB_SCALE_ROW_TENSOR, rows, n, m, dxd, dt, mode->exact);
     if (st == SB_OK) st = sb::wgrad(h, gd, xd, dt, rows, m, n, dwd, mode->exact, i > 0);
     cudaEventRecord(ev_comp[s], comp);
-    cudaStreamWaitEvent(s_out, ev_comp[s], 0);
+    cudaStreamWaitEvent(s_out, ev_y[s], 0);
     cudaMemcpyAsync(static_cast<uint8_t*>(y) + r0 * m * es, yd, rows * m * es, cudaMemcpyDeviceToHost, s_out);
+    cudaStreamWaitEvent(s_out, ev_comp[s], 0);
     cudaMemcpyAsync(static_cast<uint8_t*>(dx) + r0 * n * es, dxd, rows * n * es, cudaMemcpyDeviceToHost, s_out);
     cudaEventRecord(ev_out[s], s_out);
   }
-  cudaStreamWaitEvent(comp, ev_out[0], 0);
-  cudaStreamWaitEvent(comp, ev_out[1], 0);
+  for (int s = 0; s < NS; ++s) cudaStreamWaitEvent(comp, ev_out[s], 0);
   cudaMemcpyAsync(dw, dwd, m * n * sizeof(float), cudaMemcpyDeviceToHost, comp);
   cudaError_t e = cudaStreamSynchronize(comp);
+  cudaStreamSynchronize(s_in);
   cudaStreamSynchronize(s_out);
-  for (int s = 0; s < 2; ++s) {
-    cudaEventDestroy(ev_in[s]);
-    cudaEventDestroy(ev_comp[s]);
-    cudaEventDestroy(ev_out[s]);
-  }
-  cudaEventDestroy(ev_start);
-  cudaStreamDestroy(s_in);
-  cudaStreamDestroy(s_out);
   if (st != SB_OK) return st;
   if (e != cudaSuccess) return sb::cuda_fail(op, e);
   uint32_t flags = 0;

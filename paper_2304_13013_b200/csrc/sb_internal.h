@@ -17,8 +17,10 @@ struct sb_handle_s {
   size_t scratch_bytes = 0;
   uint64_t launches = 0;
   int gemm_path = 0;  // sb_gemm_path
-  // host-buffer pipeline (sb_switchback_fwd_bwd_host)
-  cudaStream_t aux_stream = nullptr;
+  // host-buffer pipeline (sb_switchback_fwd_bwd_host): copy streams + events, created once
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t hp_ev[4][3] = {};  // [in, y, comp, out][slot]
+  cudaEvent_t hp_start = nullptr;
   void* dev_pool = nullptr;
   size_t dev_pool_bytes = 0;
 };
