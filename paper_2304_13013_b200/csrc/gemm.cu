@@ -219,7 +219,7 @@ cudaError_t launch_2cta_cfg(sb_handle h, const CUtensorMap& ta, const CUtensorMa
   });
   if (attr_err != cudaSuccess) return attr_err;
   const int grid = 2 * (units < max_pairs ? units : max_pairs);
-  kern<<<grid, sbtc::NUM_THREADS, sbtc2::SMEM2_BYTES, h->stream>>>(ta, tb, d, p, idesc);
+  sb::launch_pdl(kern, dim3(grid), dim3(sbtc::NUM_THREADS), sbtc2::SMEM2_BYTES, h->stream, ta, tb, d, p, idesc);
   return cudaGetLastError();
 }
 
@@ -322,9 +322,9 @@ cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, cons
   const int grid = 2 * (units < max_pairs ? units : max_pairs);
   h->launches++;
   if (trans)
-    sbdw::k_dw_wide<true><<<grid, sbtc::NUM_THREADS, sbdw::SMEM_BYTES, h->stream>>>(ta, tb, td, p);
+    sb::launch_pdl(sbdw::k_dw_wide<true>, dim3(grid), dim3(sbtc::NUM_THREADS), sbdw::SMEM_BYTES, h->stream, ta, tb, td, p);
   else
-    sbdw::k_dw_wide<false><<<grid, sbtc::NUM_THREADS, sbdw::SMEM_BYTES, h->stream>>>(ta, tb, td, p);
+    sb::launch_pdl(sbdw::k_dw_wide<false>, dim3(grid), dim3(sbtc::NUM_THREADS), sbdw::SMEM_BYTES, h->stream, ta, tb, td, p);
   return cudaGetLastError();
 }
 

@@ -416,6 +416,8 @@ __global__ void __launch_bounds__(256) k_quantize_rowwise_reg(const T* __restric
   using Out = typename VecQ<T>::Out;
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  sbptx::pdl_trigger();
+  sbptx::pdl_wait();
   for (int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
        row += warps) {
     const uint4* xr = reinterpret_cast<const uint4*>(x + row * ldx);
@@ -462,8 +464,8 @@ void launch_reg(sb_handle h, const T* x, int64_t rows, int nvec, int64_t ldx, in
   }
   const int64_t need = (rows + 7) / 8;
   const int64_t blocks = std::min<int64_t>(need, static_cast<int64_t>(h->num_sms) * blocks_per_sm);
-  k_quantize_rowwise_reg<T, VPL><<<static_cast<unsigned>(blocks), 256, 0, h->stream>>>(x, rows, nvec, ldx, q, ldq,
-                                                                                      state, h->d_err);
+  sb::launch_pdl(k_quantize_rowwise_reg<T, VPL>, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, h->stream, x, rows,
+                 nvec, ldx, q, ldq, state, h->d_err);
 }
 
 // Dispatch on vectors-per-lane; false when the row is too long for registers.
@@ -735,6 +737,8 @@ __global__ void __launch_bounds__(256) k_quantize_tensorwise_fused(const T* __re
   float st = 0.0f;
   Scale sc{};
   bool fast = false;
+  sbptx::pdl_trigger();
+  sbptx::pdl_wait();
   for (;;) {
     if (threadIdx.x == 0) s_task = atomicAdd(sync + 1, 1u);
     __syncthreads();
@@ -1197,11 +1201,11 @@ bool launch_quantize_tensorwise_fused(sb_handle h, const void* x, sb_dtype dt, i
   if (*err != cudaSuccess) return true;
   h->launches++;
   if (dt == SB_BF16)
-    k_quantize_tensorwise_fused<<<grid, 256, 0, h->stream>>>(static_cast<const __nv_bfloat16*>(x), rows, cols, ldx, q,
-                                                             ldq, q_t, ldqt, state, sync, h->d_err);
+    sb::launch_pdl(k_quantize_tensorwise_fused<__nv_bfloat16>, dim3(grid), dim3(256), 0, h->stream,
+                   static_cast<const __nv_bfloat16*>(x), rows, cols, ldx, q, ldq, q_t, ldqt, state, sync, h->d_err);
   else
-    k_quantize_tensorwise_fused<<<grid, 256, 0, h->stream>>>(static_cast<const float*>(x), rows, cols, ldx, q, ldq, q_t,
-                                                             ldqt, state, sync, h->d_err);
+    sb::launch_pdl(k_quantize_tensorwise_fused<float>, dim3(grid), dim3(256), 0, h->stream, static_cast<const float*>(x),
+                   rows, cols, ldx, q, ldq, q_t, ldqt, state, sync, h->d_err);
   *err = cudaGetLastError();
   return true;
 }

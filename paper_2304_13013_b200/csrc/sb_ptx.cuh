@@ -27,6 +27,14 @@ SB_DEV bool elect_one() {
   return pred != 0;
 }
 
+// ------------------------------------------- programmatic dependent launch ----
+// Kernels launched with sb::launch_pdl let the NEXT kernel in the stream start launching at
+// once (trigger) and wait for the previous kernel's completion + memory flush (wait) before
+// touching global memory: the prologue (barrier init, TMEM alloc, descriptor prefetch) and
+// the launch latency overlap the previous kernel's tail.
+SB_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+SB_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------- mbarrier ----
 SB_DEV void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));

@@ -99,6 +99,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   cluster_sync();
   sbptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  sbptx::pdl_trigger();
+  sbptx::pdl_wait();
 
   if (warp == 0 && lane == 0) {
     // ---------------------------------------------------------------- producer (both CTAs)

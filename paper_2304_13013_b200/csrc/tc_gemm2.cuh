@@ -194,6 +194,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   cluster_sync();  // barriers of both CTAs initialised before any remote arrive / complete_tx
   sbptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  sbptx::pdl_trigger();  // the prologue above overlapped the previous kernel's tail;
+  sbptx::pdl_wait();     // its outputs are visible from here on
 
   if ((warp == 0 || (PP::NPROD == 2 && warp == 2)) && lane == 0) {
     // ------------------------------------------------ producer(s) (both CTAs)

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // util.cu — the remaining C-ABI entries: device memory + copies for FFI callers, the
 // device finiteness check (Matrix::all_finite), fp8_cast, the int8 payload transpose, and the
 // optimizer helpers compute_rms / grad_clip_global_norm / filter_nonfinite
@@ -281,3 +282,14 @@ sb_status sb_filter_nonfinite(sb_handle h, const float* const* grads, float* con
 }
 
 }  // extern "C"
+
+namespace sb {
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SB_PDL");
+    v = (e && e[0] == '1') ? 1 : 0;  // default off: measured 1% slower on the C2 step
+  }
+  return v == 1;
+}
+}  // namespace sb
