@@ -321,11 +321,13 @@ def run_ours(args):
                 "flops_per_launch": [2 * lay["m"] * lay["n"] * T for lay in layers]}
     int8_ops_step = sum(4.0 * lay["m"] * lay["n"] * T for lay in layers)
 
+    # per-kernel rates right after the timed region (same thermal / power state), then the
+    # cuBLAS yardstick, then the host-buffer e2e pass and the CPU reference
+    kern = kernel_rates(torch, A, h, layers, T, pk, fmt == "int8" and variant == "switchback") if rank == 0 else None
+    yard = cublas_yardstick(torch, layers, T, args) if rank == 0 else None
     e2e = None
     if rank == 0 and not args.no_e2e and args.config == "c2":
         e2e = e2e_host(args, L, torch)
-    yard = cublas_yardstick(torch, layers, T, args) if rank == 0 else None
-    kern = kernel_rates(torch, A, h, layers, T, pk, fmt == "int8" and variant == "switchback") if rank == 0 else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and args.config == "c2":
         r, cores, sample, kind = cpu_reference_rate(budget_s=args.ref_budget)
