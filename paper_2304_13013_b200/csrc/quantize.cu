@@ -1071,6 +1071,51 @@ __global__ void __launch_bounds__(256) k_quantize_fp8_vec(const T* __restrict__ 
   }
 }
 
+// Long rows: two passes over the row per warp — absmax streaming (nothing kept), then reload
+// (an L2 hit: the row was just read) and quantize. ~40 registers instead of 4 per 16-byte
+// vector of the row, so 4x the resident warps hide the ALU-heavy snap's latency.
+template <typename T, int FMT>
+__global__ void __launch_bounds__(256) k_quantize_fp8_rows_2pass(const T* __restrict__ x, int64_t rows, int nvec,
+                                                                 int64_t ldx, uint8_t* __restrict__ q, int64_t ldq,
+                                                                 float* __restrict__ state, uint32_t* err) {
+  constexpr int OUTB = 16 / sizeof(T);
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+       row += warps) {
+    const uint4* xr = reinterpret_cast<const uint4*>(x + row * ldx);
+    uint32_t amax = 0;
+#pragma unroll 4
+    for (int i = lane; i < nvec; i += 32) amax = max(amax, vec_absmax_bits<T>(__ldcg(xr + i)));
+    amax = __reduce_max_sync(0xffffffffu, amax);
+    if (amax >= kNonFiniteBits) {
+      if (lane == 0) {
+        raise_nonfinite(err);
+        state[row] = __uint_as_float(amax);
+      }
+      continue;
+    }
+    const float st = state_from_bits(amax);
+    if (lane == 0) state[row] = st;
+    const float rcp = (st >= 0x1p-60f && st <= 0x1p64f) ? __frcp_rn(st) : 0.0f;
+    uint8_t* qr = q + row * ldq;
+    auto emit = [&](auto fast) {
+#pragma unroll 4
+      for (int i = lane; i < nvec; i += 32) {
+        const uint2 o = fp8_vec<decltype(fast)::value, FMT, T>(ld_stream(xr + i), st, rcp);
+        if (OUTB == 8)
+          *reinterpret_cast<uint2*>(qr + i * 8) = o;
+        else
+          *reinterpret_cast<uint32_t*>(qr + i * 4) = o.x;
+      }
+    };
+    if (sizeof(T) == 2 && rcp != 0.0f)
+      emit(std::true_type{});
+    else
+      emit(std::false_type{});
+  }
+}
+
 template <typename T, int FMT>
 bool fp8_rows_reg_f(sb_handle h, const T* x, int64_t rows, int nvec, int64_t ldx, int fmt, uint8_t* q, int64_t ldq,
                     float* state) {
@@ -1083,6 +1128,17 @@ bool fp8_rows_reg_f(sb_handle h, const T* x, int64_t rows, int nvec, int64_t ldx
     kern<<<static_cast<unsigned>(blocks), 256, 0, h->stream>>>(x, rows, nvec, ldx, fmt, q, ldq, state, h->d_err);
     return true;
   };
+  static int keep = -1;
+  if (keep < 0) keep = getenv("SB_FP8_KEEP") ? atoi(getenv("SB_FP8_KEEP")) : 0;
+  if (vpl > 6 && !keep) {
+    auto kern = k_quantize_fp8_rows_2pass<T, FMT>;
+    static int bps = 0;
+    if (bps == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, 0) != cudaSuccess || bps < 1))
+      bps = 1;
+    const int64_t blocks = std::min<int64_t>((rows + 7) / 8, static_cast<int64_t>(h->num_sms) * bps);
+    kern<<<static_cast<unsigned>(blocks), 256, 0, h->stream>>>(x, rows, nvec, ldx, q, ldq, state, h->d_err);
+    return true;
+  }
   switch (vpl) {
     case 1: return go(k_quantize_fp8_rows_reg<T, 1, FMT>);
     case 2: return go(k_quantize_fp8_rows_reg<T, 2, FMT>);
