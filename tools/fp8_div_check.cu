@@ -80,6 +80,32 @@ __device__ __forceinline__ unsigned snap_int(float r, float maxv, unsigned maxco
   code = ab >= __float_as_uint(maxv) ? maxcode : code;
   return sign | code;
 }
+template <int MB, int BIAS>
+__device__ __forceinline__ unsigned snap_unit(float r) {
+  const unsigned bits = __float_as_uint(r);
+  const unsigned ab = bits & 0x7fffffffu;
+  constexpr unsigned drop = 23 - MB;
+  const unsigned code_n = ((ab + (1u << (drop - 1)) - 1u) >> drop) - ((127u - BIAS) << MB);
+  const float n = __fmul_rn(__uint_as_float(ab), __uint_as_float(static_cast<unsigned>(127 + BIAS + MB - 1) << 23));
+  const float m = __fadd_rn(n, 12582912.0f);
+  const float rn = __fsub_rn(m, 12582912.0f);
+  const unsigned code_d = (__float_as_uint(m) - 0x4B400000u) - (__fsub_rn(n, rn) == -0.5f ? 1u : 0u);
+  const unsigned code = ab < (static_cast<unsigned>(128 - BIAS) << 23) ? code_d : code_n;
+  return ((bits >> 24) & 0x80u) | code;
+}
+// every f32 with |r| <= 1 (both signs): unit snap == float-path snap
+__global__ void k_snap_unit(unsigned long long* bad) {
+  unsigned long long b4 = 0, b5 = 0;
+  for (unsigned long long u = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; u <= 2ull * 0x3F800000ull + 1;
+       u += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned w = static_cast<unsigned>(u <= 0x3F800000ull ? u : (u - 0x3F800001ull) | 0x80000000ull);
+    const float f = __uint_as_float(w);
+    b4 += snap<3, 7>(f, 448.0f, 0x7Eu) != snap_unit<3, 7>(f);
+    b5 += snap<2, 15>(f, 57344.0f, 0x7Bu) != snap_unit<2, 15>(f);
+  }
+  atomicAdd(bad + 8, b4);
+  atomicAdd(bad + 9, b5);
+}
 // every finite f32 (both signs): integer snap == float-path snap
 __global__ void k_snap(unsigned long long* bad) {
   unsigned long long b4 = 0, b5 = 0;
@@ -96,12 +122,14 @@ __global__ void k_snap(unsigned long long* bad) {
 
 int main() {
   unsigned long long* d;
-  cudaMalloc(&d, 64);
-  cudaMemset(d, 0, 64);
+  cudaMalloc(&d, 80);
+  cudaMemset(d, 0, 80);
   k<<<0x7F7F, 256>>>(d);
   k_snap<<<148 * 16, 256>>>(d);
-  unsigned long long h[8];
-  cudaMemcpy(h, d, 64, cudaMemcpyDeviceToHost);
+  k_snap_unit<<<148 * 16, 256>>>(d);
+  unsigned long long h[10];
+  cudaMemcpy(h, d, 80, cudaMemcpyDeviceToHost);
+  printf("unit snap (|r| <= 1) vs float snap: e4m3 %llu, e5m2 %llu mismatches\n", h[8], h[9]);
   printf("integer snap vs float snap over all finite f32: e4m3 %llu, e5m2 %llu mismatches\n", h[6], h[7]);
   printf("err=%d  mismatches: x*rcp %llu   x*rcp + 1 correction %llu   (pairs ~%.2e)\n", (int)cudaGetLastError(), h[0], h[1],
          0x7F7F * 0x7F7F * 1.0);
