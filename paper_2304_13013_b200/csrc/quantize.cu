@@ -920,6 +920,19 @@ __device__ __forceinline__ uint32_t fp8_snap_unit(float r) {
   return ((bits >> 24) & 0x80u) | code;
 }
 
+// fp8_snap_unit without the sign: a = |ratio| >= 0.
+template <int MB, int BIAS>
+__device__ __forceinline__ uint32_t fp8_code_unit_abs(float a) {
+  const uint32_t ab = __float_as_uint(a);
+  constexpr uint32_t drop = 23 - MB;
+  const uint32_t code_n = ((ab + (1u << (drop - 1)) - 1u) >> drop) - ((127u - BIAS) << MB);
+  const float n = __fmul_rn(a, __uint_as_float(static_cast<uint32_t>(127 + BIAS + MB - 1) << 23));
+  const float m = __fadd_rn(n, 12582912.0f);
+  const float rn = __fsub_rn(m, 12582912.0f);
+  const uint32_t code_d = (__float_as_uint(m) - 0x4B400000u) - (__fsub_rn(n, rn) == -0.5f ? 1u : 0u);
+  return ab < (static_cast<uint32_t>(128 - BIAS) << 23) ? code_d : code_n;
+}
+
 __device__ __forceinline__ float fp8_decode(uint8_t b, int fmt) {
   const uint32_t s = (b >> 7) & 1u;
   float v;
@@ -965,8 +978,29 @@ __global__ void k_quantize_fp8(const T* __restrict__ x, int64_t rows, int64_t co
 // (so -0 stays -0). The fp8 payload this gives equals the one from the correctly rounded
 // quotient for EVERY bf16 pair |x| <= s in that range, e4m3 and e5m2 (exhaustive check,
 // tools/fp8_div_check.cu, ~1.07e9 pairs); rows outside it and fp32 input use __fdiv_rn.
+// bf16 fast path on magnitudes: the quotient of |x| (abs is a free operand modifier), the
+// magnitude code, and the 8 sign bits OR-ed in from the raw bf16 words at the end.
+template <int FMT>
+__device__ __forceinline__ uint2 fp8_vec_bf16_fast(const uint4& v, float s, float r) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  uint32_t c[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float ax = fabsf(__uint_as_float((i & 1) ? (w[i >> 1] & 0xffff0000u) : (w[i >> 1] << 16)));
+    const float q0 = __fmul_rn(ax, r);
+    const float a = __fmaf_rn(__fmaf_rn(-s, q0, ax), r, q0);
+    c[i] = FMT == 0 ? fp8_code_unit_abs<3, 7>(a) : fp8_code_unit_abs<2, 15>(a);
+  }
+  // sign of element 2k is bit 15 of w[k], of element 2k+1 bit 31
+  const uint32_t s0 = ((w[0] >> 8) & 0x80u) | ((w[0] >> 16) & 0x8000u) | ((w[1] << 8) & 0x800000u) | (w[1] & 0x80000000u);
+  const uint32_t s1 = ((w[2] >> 8) & 0x80u) | ((w[2] >> 16) & 0x8000u) | ((w[3] << 8) & 0x800000u) | (w[3] & 0x80000000u);
+  return make_uint2((c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24)) | s0,
+                    (c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24)) | s1);
+}
+
 template <bool FAST, int FMT, typename T>
 __device__ __forceinline__ uint2 fp8_vec(const uint4& v, float s, float r) {
+  if constexpr (FAST && sizeof(T) == 2) return fp8_vec_bf16_fast<FMT>(v, s, r);
   constexpr int N = Unpack<T>::N;
   float x[N];
   Unpack<T>::run(v, x);
