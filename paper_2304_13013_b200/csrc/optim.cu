@@ -195,21 +195,28 @@ __device__ __forceinline__ void phase2_chunk(const TensorDesc& d, const Coeffs& 
 }
 
 // Persistent multi-tensor StableAdamW. Tasks, fetched in order from an atomic counter:
-// for each tensor its phase-1 chunks, then its phase-2 chunks. A phase-2 task waits until
-// every phase-1 chunk of its tensor has published its partial (all of them were fetched
-// before it, by running blocks: no deadlock), reduces the tensor's partials in a fixed order
-// (same eta in every block), and updates theta while v, u of the tensor are still in L2.
-// No launch boundary between tensors: phase 1 of tensor i+1 overlaps the tail of tensor i.
-// sync[0] = task counter, sync[1 + k] = finished phase-1 chunks of group tensor k (zeroed
-// by the launcher).
+// phase-1 chunks of tensor k+1 precede phase-2 chunks of tensor k. The block that completes
+// a tensor's last phase-1 chunk reduces the tensor's partials in a fixed order (same sum
+// whichever block it is), computes RMS and eta once and publishes eta; a phase-2 chunk waits
+// for that flag (every phase-1 chunk of its tensor was fetched before it, by running blocks:
+// no deadlock) and updates theta while v, u of the tensor are still in L2. No launch
+// boundary between tensors: phase 1 of tensor k+1 overlaps the tail of tensor k.
+// sync[0] = task counter, sync[1 + 2k] = finished phase-1 chunks of group tensor k,
+// sync[2 + 2k] = its eta-ready flag (zeroed by the launcher); eta_buf[k] = its eta.
+__device__ __forceinline__ void st_release(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __global__ void __launch_bounds__(kThreads, 4) k_adamw_persistent(const __grid_constant__ Group grp, Coeffs c,
                                                                const double* __restrict__ clip_ptr,
                                                                double* __restrict__ partials,
-                                                               unsigned int* __restrict__ sync, double* rms_out,
+                                                               unsigned int* __restrict__ sync,
+                                                               double* __restrict__ eta_buf, double* rms_out,
                                                                double* eta_out) {
   __shared__ double red[kThreads / 32];
   __shared__ int64_t s_task;
   __shared__ double s_eta;
+  __shared__ int s_last;
   const double clip = clip_ptr ? *clip_ptr : 1.0;
   for (;;) {
     if (threadIdx.x == 0) s_task = atomicAdd(sync, 1u);
@@ -232,29 +239,34 @@ __global__ void __launch_bounds__(kThreads, 4) k_adamw_persistent(const __grid_c
       if (threadIdx.x == 0) {
         partials[d.block0 + local] = s;
         __threadfence();
-        atomicAdd(sync + 1 + ti, 1u);
-      }
-    } else {
-      const int64_t blk = local - d.nblocks;
-      if (threadIdx.x == 0) {
-        while (ld_acquire(sync + 1 + ti) < static_cast<uint32_t>(d.nblocks)) __nanosleep(100);
+        s_last = atomicAdd(sync + 1 + 2 * ti, 1u) == static_cast<unsigned int>(d.nblocks - 1);
       }
       __syncthreads();
-      // every block of the tensor reduces the same partials in the same order -> same eta
-      double s = 0.0;
-      for (int64_t j = threadIdx.x; j < d.nblocks; j += kThreads) s = __dadd_rn(s, __ldcg(partials + d.block0 + j));
-      const double tot = block_sum(s, red);
-      if (threadIdx.x == 0) {
-        const double rms = __dsqrt_rn(__ddiv_rn(tot, static_cast<double>(d.numel)));
-        const double eta = c.update_clip ? __ddiv_rn(c.alpha, rms > 1.0 ? rms : 1.0) : c.alpha;
-        s_eta = eta;
-        if (blk == 0) {
+      if (s_last) {
+        // the block that finished the tensor's last chunk reduces its partials in a fixed
+        // order (thread-strided, then the block tree: the same sum whichever block does it),
+        // computes RMS and eta once and publishes eta for the phase-2 chunks
+        __threadfence();
+        double sum = 0.0;
+        for (int64_t j = threadIdx.x; j < d.nblocks; j += kThreads) sum = __dadd_rn(sum, __ldcg(partials + d.block0 + j));
+        const double tot = block_sum(sum, red);
+        if (threadIdx.x == 0) {
+          const double rms = __dsqrt_rn(__ddiv_rn(tot, static_cast<double>(d.numel)));
+          const double eta = c.update_clip ? __ddiv_rn(c.alpha, rms > 1.0 ? rms : 1.0) : c.alpha;
+          eta_buf[ti] = eta;
           if (rms_out) rms_out[d.index] = rms;
           if (eta_out) eta_out[d.index] = eta;
+          __threadfence();
+          st_release(sync + 2 + 2 * ti, 1u);
         }
       }
+    } else {
+      if (threadIdx.x == 0) {
+        while (ld_acquire(sync + 2 + 2 * ti) == 0u) __nanosleep(100);
+        s_eta = __ldcg(eta_buf + ti);
+      }
       __syncthreads();
-      phase2_chunk(d, c, s_eta, blk);
+      phase2_chunk(d, c, s_eta, local - d.nblocks);
     }
   }
 }
@@ -355,9 +367,9 @@ extern "C" sb_status sb_stableadamw_workspace_size(const sb_adamw_tensor* tensor
   if (!bytes || (ntensors > 0 && !tensors)) return sb::fail(SB_ERR_INVALID_ARGUMENT, "optimizer_step", "null argument");
   int64_t total = 0;
   for (int i = 0; i < ntensors; ++i) total += (tensors[i].numel + kChunk - 1) / kChunk;
-  // partials (one double per chunk), the grad-clip factor, sync words (task counter +
-  // per-tensor phase-1 counts of the largest group)
-  *bytes = static_cast<size_t>(total + 2) * sizeof(double) + (kMaxGroup + 2) * sizeof(unsigned int) + 64;
+  // partials (one double per chunk), the grad-clip factor, eta per group tensor, sync words
+  // (task counter + per group tensor: finished phase-1 chunks, eta-ready flag)
+  *bytes = static_cast<size_t>(total + 2 + kMaxGroup) * sizeof(double) + (2 * kMaxGroup + 2) * sizeof(unsigned int) + 64;
   return SB_OK;
 }
 
@@ -406,16 +418,17 @@ extern "C" sb_status sb_stableadamw_step(sb_handle h, const sb_adamw_tensor* ten
   }
   // persistent task-list kernel per group; sync words (task counter + per-tensor phase-1
   // counts) zeroed once per step
-  unsigned int* sync = reinterpret_cast<unsigned int*>(clip + 1);
+  double* eta_buf = clip + 1;
+  unsigned int* sync = reinterpret_cast<unsigned int*>(eta_buf + kMaxGroup);
   int blocks_per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_adamw_persistent, kThreads, 0);
   blocks_per_sm = std::max(1, blocks_per_sm);
   for (const Group& g : groups) {
-    SB_CUDA_CHECK(op, cudaMemsetAsync(sync, 0, sizeof(unsigned int) * (g.count + 1), h->stream));
+    SB_CUDA_CHECK(op, cudaMemsetAsync(sync, 0, sizeof(unsigned int) * (2 * g.count + 1), h->stream));
     const int64_t grid = std::min<int64_t>(g.total_tasks, static_cast<int64_t>(h->num_sms) * blocks_per_sm);
     h->launches++;
     k_adamw_persistent<<<static_cast<unsigned>(grid), kThreads, 0, h->stream>>>(
-        g, c, hp->clipping == SB_CLIP_GRAD ? clip : nullptr, partials, sync, rms_out, eta_out);
+        g, c, hp->clipping == SB_CLIP_GRAD ? clip : nullptr, partials, sync, eta_buf, rms_out, eta_out);
   }
   SB_LAUNCH_CHECK(op);
   return SB_OK;
