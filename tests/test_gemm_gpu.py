@@ -165,3 +165,10 @@ def test_fp8_gemm(fa, fb, M, N, K, gemm_path):
     da = fp8_decode(host(qa.payload), fa).astype(np.float64) * host(qa.state)[:, None]
     db = fp8_decode(host(qb.payload), fb).astype(np.float64) * host(qb.state)[0]
     assert rel_err(y, da @ db.T) < 1e-5
+
+
+def test_gemm_path_option_rejects_bad_values():
+    h = A.handle()
+    with pytest.raises(A.InvalidArgument, match="sb_set_gemm_path: bad path"):
+        h.set_gemm_path(7)
+    h.set_gemm_path(A.SB_GEMM_AUTO)
