@@ -53,47 +53,94 @@ def peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
 
 
+_SAMPLER = r"""
+import sys, time, pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+bits = [pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+        pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap]
+mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+print("ready", flush=True)
+out = []
+import select
+while not select.select([sys.stdin], [], [], 0.002)[0]:
+    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+    out.append("%d %s" % (pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), "".join("1" if r & b else "0" for b in bits)))
+print(mx)
+print("\n".join(out), flush=True)
+"""
+
+
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled DURING the timed region: a separate NVML process
+    polling every 2 ms (no GIL contention with the launching thread); nvidia-smi every 200 ms
+    in a thread when NVML is unavailable."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, [hw, hw_thermal, sw_thermal, sw_power] bools)
+        self.source = None
+        self._proc = None
         self._stop = threading.Event()
         self._t = None
 
-    def _run(self):
+    def _sample_smi(self):
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+        f = [x.strip() for x in out.strip().split(",")]
+        if len(f) == 6:
+            self.samples.append((float(f[0]), float(f[1]), [x.lower() == "active" for x in f[2:]]))
+
+    def _run_smi(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
-                f = [s.strip() for s in out.strip().split(",")]
-                if len(f) == 6:
-                    self.samples.append(f)
+                self._sample_smi()
             except Exception:
                 pass
             self._stop.wait(0.2)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self._proc = subprocess.Popen([sys.executable, "-c", _SAMPLER, str(self.index)], stdin=subprocess.PIPE,
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            if self._proc.stdout.readline().strip() != "ready":
+                raise RuntimeError("sampler")
+            self.source = "nvml"
+        except Exception:
+            if self._proc:
+                self._proc.kill()
+            self._proc = None
+            self.source = "nvidia-smi"
+            self._t = threading.Thread(target=self._run_smi, daemon=True)
+            self._t.start()
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._proc:
+            try:
+                out, _ = self._proc.communicate("stop\n", timeout=10)
+                lines = out.strip().splitlines()
+                mx = float(lines[0])
+                for ln in lines[1:]:
+                    mhz, fl = ln.split()
+                    self.samples.append((float(mhz), mx, [c == "1" for c in fl]))
+            except Exception:
+                self._proc.kill()
+        else:
+            self._stop.set()
+            self._t.join(timeout=10)
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(float(s[0]) for s in self.samples)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(self.samples[0][1]), "reasons": reasons,
-                "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "source": self.source}
+        sm = sorted(s[0] for s in self.samples)
+        reasons = sorted({self.NAMES[i] for s in self.samples for i in range(4) if s[2][i]})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_min_mhz": sm[0], "sm_max_mhz": self.samples[0][1], "reasons": reasons,
+                "samples": len(self.samples), "source": self.source}
 
 
 # ----------------------------------------------------------------- CPU side
