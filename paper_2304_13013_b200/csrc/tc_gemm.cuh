@@ -96,6 +96,12 @@ struct KindTraits<KIND_BF16> {
 // Pipeline probe (tools/gemm_probe.cu only): per CTA {MMA waits on full, MMA waits on tempty,
 // MMA-loop cycles, producer waits on empty, epilogue waits on tfull, k-blocks}.
 extern __device__ unsigned long long g_probe[1024 * 6];  // defined in build/probe/probe_glue.cu
+extern __device__ long long g_trace[4096];               // CTA-pair 0 timeline (globaltimer ns)
+__device__ __forceinline__ long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 #define SB_PROBE_T0() const long long sb_t0_ = clock64()
 #define SB_PROBE_ADD(slot) atomicAdd(&g_probe[blockIdx.x * 6 + (slot)], (unsigned long long)(clock64() - sb_t0_))
 #else

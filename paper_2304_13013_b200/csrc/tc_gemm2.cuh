@@ -216,6 +216,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         if (rank == 0) sbptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * PP::STAGE);
         load2<A_MN, Kind2<KIND>::KATOM, PP::ATOMS>(&tmA, &full_bar[stage], smem_a + stage * PP::OPB, am0, kb);
         load2<B_MN, Kind2<KIND>::KATOM, PP::ATOMS>(&tmB, &full_bar[stage], smem_b + stage * PP::OPB, bn0, kb);
+#ifdef SB_GEMM_PROBE
+        if (pair == 0 && i < 512) g_trace[rank * 512 + i] = gtime();
+#endif
       }
     }
   } else if (warp == 1) {
@@ -230,6 +233,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       int it = 0;
 #ifdef SB_GEMM_PROBE
       const long long sb_loop0 = clock64();
+      int kidx = 0;
 #endif
       for (int u = pair; u < num_units; u += npairs, ++it) {
         const int acc = it & 1;
@@ -240,7 +244,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         int m0_, n0_, kb0, kb1;
         unit2(p, u, k_blocks, m0_, n0_, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
+#ifdef SB_GEMM_PROBE
+          const long long tw0 = gtime();
+#endif
           { SB_PROBE_T0(); sbptx::mbar_wait(&full_bar[stage], phase); SB_PROBE_ADD(0); }
+#ifdef SB_GEMM_PROBE
+          if (pair == 0 && kidx < 512) {
+            g_trace[1024 + kidx] = tw0;
+            g_trace[1536 + kidx] = gtime();
+          }
+          ++kidx;
+#endif
 #ifdef SB_GEMM_PROBE
           atomicAdd(&g_probe[blockIdx.x * 6 + 5], 1ull);
 #endif

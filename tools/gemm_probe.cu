@@ -22,6 +22,7 @@ __global__ void k_fill(uint8_t* p, size_t n, int bf16) {
   }
 }
 extern "C" void sb_probe_reset();
+extern "C" void sb_trace_read(long long* out);
 
 int main(int argc, char** argv) {
   const int64_t M = argc > 1 ? atoll(argv[1]) : 65792, N = argc > 2 ? atoll(argv[2]) : 5120,
@@ -72,6 +73,15 @@ int main(int argc, char** argv) {
   printf("per CTA avg (cycles): mma-loop %.0f | mma wait full %.0f | mma wait tempty %.0f | producer wait empty %.0f |"
          " epi(w4) wait tfull %.0f | k-blocks %.1f\n",
          sums[2] / 148, sums[0] / 148, sums[1] / 148, sums[3] / 148, sums[4] / 148, sums[5] / 148);
+  if (getenv("TRACE")) {
+    std::vector<long long> tr(4096);
+    sb_trace_read(tr.data());
+    const long long t0 = tr[1024];
+    printf("stage: leader-issue peer-issue | mma-wait-begin mma-wait-end (ns from first wait)\n");
+    for (int i = 0; i < 60; ++i)
+      printf("%3d: %7lld %7lld | %7lld %7lld  wait %5lld\n", i, tr[i] - t0, tr[512 + i] - t0, tr[1024 + i] - t0,
+             tr[1536 + i] - t0, tr[1536 + i] - tr[1024 + i]);
+  }
   printf("MMA busy fraction of loop ~ %.2f (ideal cycles = kblocks*4*128 = %.0f)\n",
          (sums[5] / 148 * 512) / (sums[2] / 148), sums[5] / 148 * 512);
   return 0;
