@@ -171,9 +171,13 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
 #pragma unroll 1
   for (int pr = 0; pr < 2; ++pr) {  // two 64-column pairs per warp
     uint32_t r0[32], r1[32];
+#ifdef SB_PROBE_SKIP_LD  // experiment only (tools/gemm_probe): epilogue without the TMEM drain
+    for (int j = 0; j < 32; ++j) r0[j] = r1[j] = t_row + j;
+#else
     sbptx::tmem_ld_32x32b_x32(t_row + pr * 64, r0);
     sbptx::tmem_ld_32x32b_x32(t_row + pr * 64 + 32, r1);
     sbptx::tmem_ld_wait();
+#endif
     if (pr == 1) {
       // accumulator fully drained into registers: hand TMEM back to the MMA warp
       sbptx::tc_fence_before();
