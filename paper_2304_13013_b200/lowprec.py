@@ -62,6 +62,16 @@ def _check_nonfinite(h: A.Handle, check: bool) -> None:
         h.synchronize()
 
 
+def check_error(device: int | None = None) -> None:
+    """Synchronise the handle's stream and raise InvalidArgument if any kernel since the last
+    check saw a non-finite input (the deferred form of the per-call check, for async /
+    CUDA-graph callers such as nn.SwitchBackLinear)."""
+    try:
+        A.handle(device).synchronize()
+    except InvalidArgument:
+        raise InvalidArgument(A.SB_ERR_NONFINITE, "switchback: non-finite input") from None
+
+
 @dataclass
 class QuantizedMatrix:
     """quantize.hpp:48-65. payload int8 (or uint8 fp8 bytes) row-major; state per axis."""

@@ -1,0 +1,67 @@
+"""PyTorch-facing SwitchBack layer: an ``autograd.Function`` over the C-ABI linear forward /
+backward (``sb_linear_forward`` / ``sb_linear_backward``, linear.cpp:113-278) and an
+``nn.Linear``-shaped module. This is a CALLER of the drop-in path (SURVEY.md §8b "PyTorch
+autograd.Function wrapper", §8f row 2 model-level caller), not part of the measured kernels.
+
+* Weights are fp32 master parameters; each forward feeds a bf16 (or fp32) copy to the kernels
+  and the weight gradient comes back in fp32 (the reference's dW precision, linear.cpp:245),
+  so no gradient precision is lost to a bf16 round trip.
+* No host synchronisation on the hot path (non-finite inputs still latch in the handle's
+  device error word; ``lowprec.check_error()`` / ``sb_synchronize`` report them), so the layer
+  is CUDA-graph capturable.
+* Inputs of any leading shape (..., in_features) are flattened to token rows.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _capi as A
+from . import lowprec as L
+
+_VARIANTS = {"switchback": A.SB_SWITCHBACK, "switchback_m": A.SB_SWITCHBACK_M, "switchback_q": A.SB_SWITCHBACK_Q,
+             "allquant": A.SB_ALLQUANT, "standard": A.SB_STANDARD}
+
+
+class _SwitchBackLinearFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x2d: torch.Tensor, weight: torch.Tensor, mode: L.LinearMode):
+        w = weight.detach().to(x2d.dtype).contiguous()
+        lctx = L.LinearContext()
+        y = L.linear_forward(mode, x2d.contiguous(), w, lctx, check=False)
+        ctx.lctx = lctx
+        ctx.mode = mode
+        ctx.keep_w = w  # the device context references it until the backward
+        return y
+
+    @staticmethod
+    def backward(ctx, g: torch.Tensor):
+        dx, dw = L.linear_backward(ctx.mode, ctx.lctx, g.contiguous(), check=False)
+        ctx.lctx = None
+        ctx.keep_w = None
+        return dx, dw, None
+
+
+class SwitchBackLinear(torch.nn.Module):
+    """y = x W^T (+ b) with the int8 SwitchBack forward / input gradient and the 16-bit weight
+    gradient (arXiv 2304.13013), on the B200 kernels of this package."""
+
+    def __init__(self, in_features: int, out_features: int, bias: bool = True, variant: str = "switchback",
+                 fmt: str = "int8", device=None):
+        super().__init__()
+        self.in_features, self.out_features = in_features, out_features
+        self.mode = L.LinearMode(_VARIANTS[variant], A.SB_INT8 if fmt == "int8" else A.SB_FP8)
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        # the reference's init (model.cpp:199-202): N(0, 1/n)
+        self.weight = torch.nn.Parameter(torch.randn(out_features, in_features, device=dev) * in_features ** -0.5)
+        self.bias = torch.nn.Parameter(torch.zeros(out_features, device=dev)) if bias else None
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        shape = x.shape
+        y = _SwitchBackLinearFn.apply(x.reshape(-1, self.in_features), self.weight, self.mode)
+        y = y.reshape(*shape[:-1], self.out_features)
+        if self.bias is not None:
+            y = y + self.bias.to(y.dtype)
+        return y
+
+    def extra_repr(self) -> str:
+        return f"in_features={self.in_features}, out_features={self.out_features}, bias={self.bias is not None}"
