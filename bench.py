@@ -245,12 +245,18 @@ def run_ours(args):
         A.check(h.lib.sb_linear_forward(h.h, C.byref(cmode), P(lay["x"]), P(lay["w"]), A.SB_BF16, T, lay["n"],
                                         lay["m"], P(lay["y"]), C.byref(lay["ctx"]), P(lay["ws"]), lay["ws"].numel()))
 
-    def bwd_dx(lay):
-        c = lay["ctx"]
+    def bwd_q(lay):
         A.check(h.lib.sb_quantize_rowwise(h.h, P(lay["g"]), A.SB_BF16, T, lay["m"], lay["m"], P(lay["gq"]), lay["m"],
                                           P(lay["gs"])))
+
+    def bwd_dx_gemm(lay):
+        c = lay["ctx"]
         A.check(h.lib.sb_gemm_i8(h.h, P(lay["gq"]), P(lay["gs"]), C.c_void_p(c.w_q_t), C.c_void_p(c.w_state),
                                  A.SB_SCALE_ROW_TENSOR, T, lay["n"], lay["m"], P(lay["dx"]), A.SB_BF16, 0))
+
+    def bwd_dx(lay):
+        bwd_q(lay)
+        bwd_dx_gemm(lay)
 
     def bwd_dw(lay):
         A.check(h.lib.sb_wgrad(h.h, P(lay["g"]), P(lay["x"]), A.SB_BF16, T, lay["m"], lay["n"], P(lay["dw"]), 0, 0))
@@ -260,36 +266,61 @@ def run_ours(args):
                                          P(lay["dw"]), 0))
 
     # Segments (one CUDA graph each): forwards of all layers then, last layer first, the
-    # input-gradient work and the weight gradient of each layer. seg_dw marks dW segments.
+    # input-gradient work and the weight gradient of each layer. seg_kind: "main" / "dw" run on
+    # the step stream; "q" (the row-wise quantize of G) runs on a side stream forked from the
+    # step stream and joined before the layer's dX GEMM ("dx"), so it fills the SMs the
+    # one-wave dW GEMM leaves idle (134 of 148 busy) instead of running after it. Both only
+    # read G: the overlap stays inside one linear's backward (linear.cpp:232-245).
     # The first layer's dW runs before its dX so that, under DP, the last dW all-reduce
     # overlaps that dX instead of being exposed at the end of the step.
-    segments, seg_dw = [], []
-    if plain:
+    segments, seg_kind = [], []
+    overlap = plain and not args.no_overlap
+    if plain and overlap:
+        segments.append(lambda: [fwd(l) for l in layers])
+        seg_kind.append("main")
+        for i in range(len(layers) - 1, -1, -1):
+            for fn, kind in ((bwd_q, "q"), (bwd_dw, "dw"), (bwd_dx_gemm, "dx")):
+                segments.append(lambda l=layers[i], fn=fn: fn(l))
+                seg_kind.append(kind)
+    elif plain:
         segments.append(lambda: ([fwd(l) for l in layers], bwd_dx(layers[-1])))
-        seg_dw.append(False)
+        seg_kind.append("main")
         for i in range(len(layers) - 1, -1, -1):
             segments.append(lambda l=layers[i]: bwd_dw(l))
-            seg_dw.append(True)
+            seg_kind.append("dw")
             if i > 1:
                 segments.append(lambda l=layers[i - 1]: bwd_dx(l))
-                seg_dw.append(False)
+                seg_kind.append("main")
         segments.append(lambda: bwd_dx(layers[0]))
-        seg_dw.append(False)
+        seg_kind.append("main")
     else:
         segments.append(lambda: [fwd(l) for l in layers])
-        seg_dw.append(False)
+        seg_kind.append("main")
         for i in range(len(layers) - 1, -1, -1):
             segments.append(lambda l=layers[i]: bwd_full(l))
-            seg_dw.append(False)
+            seg_kind.append("main")
+    seg_dw = [k == "dw" for k in seg_kind]
     stream = torch.cuda.current_stream(dev)
+    side = torch.cuda.Stream(dev)
     ar = dp.GradAllReduce()
+
+    def eager_step():
+        for seg, kind in zip(segments, seg_kind):
+            if kind == "q":
+                side.wait_stream(stream)
+                h.bind_stream(side.cuda_stream)
+                seg()
+                h.bind_stream(stream.cuda_stream)
+            else:
+                if kind == "dx":
+                    stream.wait_stream(side)
+                seg()
 
     # warmup (eager), counting launches of one step
     for i in range(max(1, args.warmup)):
         l0 = h.launches()
         h.bind_stream(stream.cuda_stream)
-        for seg in segments:
-            seg()
+        eager_step()
         launches_per_step = h.launches() - l0
     torch.cuda.synchronize()
     graphs = None
@@ -307,6 +338,9 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     run = [g.replay for g in graphs] if graphs else segments
+    if not graphs:  # eager launches follow the handle's stream binding
+        run = [(lambda seg=seg: (h.bind_stream(side.cuda_stream), seg(), h.bind_stream(stream.cuda_stream)))
+               if kind == "q" else seg for seg, kind in zip(segments, seg_kind)]
     ns = len(run)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(ns + 1)] for _ in range(args.steps)]
     # dW all-reduce issue points: after each layer's dW segment (or full backward)
@@ -320,7 +354,14 @@ def run_ours(args):
     def step(e):
         e[0].record(stream)
         for j in range(ns):
-            run[j]()
+            if seg_kind[j] == "q":
+                side.wait_stream(stream)
+                with torch.cuda.stream(side):
+                    run[j]()
+            else:
+                if seg_kind[j] == "dx":
+                    stream.wait_stream(side)
+                run[j]()
             e[j + 1].record(stream)
             if j in ar_after:
                 ar.launch(ar_after[j])
@@ -391,7 +432,7 @@ def run_ours(args):
                            "tokens_per_gpu": T, "global_tokens": T * world,
                            "layers": [f"{n}->{m}" for _, n, m in layers_cfg], "parallelism": f"dp{world} (token shards)",
                            "l2": "inputs larger than L2 (X, G operands 168-673 MB each)",
-                           "cuda_graphs": graphs is not None},
+                           "cuda_graphs": graphs is not None, "g_quantize_overlaps_dw": overlap},
                 "gpu_launches": launches,
                 "roofline": roof,
                 "int8_tops_per_step": int8_ops_step / 1e12,
@@ -644,6 +685,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true", help="quantize G after dW on one stream")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

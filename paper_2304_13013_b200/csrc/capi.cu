@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -605,8 +606,11 @@ sb_status sb_switchback_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, co
   // D2H of chunk i-1 run concurrently; Y of a chunk is copied out as soon as its forward GEMM
   // is done, dX after the backward. Small chunks keep the un-overlapped pipeline fill (first
   // H2D) and drain (last D2H, the dW copy) short; 4096 rows still fill the SM pairs.
-  constexpr int NS = 3;
-  const int64_t chunk = std::min<int64_t>(b, 4096);
+  // SB_HOST_CHUNK / SB_HOST_SLOTS override the defaults (measurement knobs).
+  const char* ce = std::getenv("SB_HOST_CHUNK");
+  const char* se = std::getenv("SB_HOST_SLOTS");
+  const int NS = se ? std::max(2, std::min(8, std::atoi(se))) : 3;
+  const int64_t chunk = std::min<int64_t>(b, ce ? std::max<int64_t>(128, std::atoll(ce)) : 4096);
   // device layout: W, W_q, W_qT, dW, states/words, NS x {x, g, y, dx, x_q, g_q, x states, g states}
   Carve c{nullptr};
   auto layout = [&](Carve& cv, void** P) {
@@ -627,7 +631,7 @@ sb_status sb_switchback_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, co
       P[6 + 8 * s + 7] = cv.take<float>(chunk);
     }
   };
-  void* P[6 + 8 * NS];
+  void* P[6 + 8 * 8];
   layout(c, P);
   const size_t need = c.off + 256;
   if (need > h->dev_pool_bytes) {

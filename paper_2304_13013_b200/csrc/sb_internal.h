@@ -20,7 +20,7 @@ struct sb_handle_s {
   int gemm_path = 0;  // sb_gemm_path
   // host-buffer pipeline (sb_switchback_fwd_bwd_host): copy streams + events, created once
   cudaStream_t s_in = nullptr, s_out = nullptr;
-  cudaEvent_t hp_ev[4][3] = {};  // [in, y, comp, out][slot]
+  cudaEvent_t hp_ev[4][8] = {};  // [in, y, comp, out][slot] (host pipeline, up to 8 slots)
   cudaEvent_t hp_start = nullptr;
   void* dev_pool = nullptr;
   size_t dev_pool_bytes = 0;
