@@ -530,6 +530,101 @@ def run_c5(args):
         torch.distributed.destroy_process_group()
 
 
+def run_vit_block(args):
+    """Model-level caller (model.cpp:287-408): one CLIP ViT-Huge
+    transformer block (pre-LN; qkv 1280->3840, 16-head attention, out 1280->1280, fc1
+    1280->5120, GELU, fc2 5120->1280; residuals), forward + backward at 256 x 257 tokens, with
+    the four linears as paper_2304_13013_b200.nn.SwitchBackLinear (fp32 master weights, int8
+    fwd/dX, bf16 dW) against the same block with torch bf16 linears under autocast (cuBLAS).
+    LayerNorm, GELU and attention (SDPA) are PyTorch's in both arms. Each arm is captured in
+    one CUDA graph; inputs and upstream gradients are synthetic and resident."""
+    import torch
+    import torch.nn.functional as F
+
+    from paper_2304_13013_b200 import _capi as A
+    from paper_2304_13013_b200.nn import SwitchBackLinear
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    B, S, D, H = 256, 257, 1280, 16
+    T = B * S
+
+    class Block(torch.nn.Module):
+        def __init__(self, sb):
+            super().__init__()
+            mk = (lambda i, o: SwitchBackLinear(i, o, device=dev)) if sb else \
+                (lambda i, o: torch.nn.Linear(i, o, device=dev))
+            self.ln1 = torch.nn.LayerNorm(D, device=dev)
+            self.ln2 = torch.nn.LayerNorm(D, device=dev)
+            self.qkv, self.out, self.fc1, self.fc2 = mk(D, 3 * D), mk(D, D), mk(D, 4 * D), mk(4 * D, D)
+
+        def forward(self, x):
+            h = self.ln1(x.float()).to(torch.bfloat16)
+            q, k, v = self.qkv(h).view(B, S, 3, H, D // H).permute(2, 0, 3, 1, 4).unbind(0)
+            a = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(B, S, D)
+            x = x + self.out(a)
+            h = self.ln2(x.float()).to(torch.bfloat16)
+            return x + self.fc2(F.gelu(self.fc1(h)))
+
+    gen = torch.Generator(device=dev).manual_seed(3)
+    x0 = torch.randn(B, S, D, device=dev, generator=gen).to(torch.bfloat16)
+    gy = torch.randn(B, S, D, device=dev, generator=gen).to(torch.bfloat16)
+    res = {}
+    launches = None
+    for arm in ("switchback", "bf16"):
+        blk = Block(arm == "switchback")
+        x = x0.clone().requires_grad_(True)
+
+        def step():
+            for p in blk.parameters():
+                p.grad = None
+            x.grad = None
+            with torch.autocast("cuda", dtype=torch.bfloat16, enabled=arm == "bf16"):
+                y = blk(x)
+            y.backward(gy)
+
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                step()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        h = A.handle(0)
+        l0 = h.launches()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step()
+        if arm == "switchback":
+            launches = h.launches() - l0
+        for _ in range(max(3, args.warmup)):
+            g.replay()
+        torch.cuda.synchronize()
+        s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(0) as clk:
+            s_ev.record()
+            for _ in range(args.steps):
+                g.replay()
+            e_ev.record()
+            torch.cuda.synchronize()
+        ms = s_ev.elapsed_time(e_ev) / args.steps
+        res[arm] = {"ms_per_step": ms, "value": T / (ms / 1000.0), "clocks": clk.summary()}
+        del g, blk
+        torch.cuda.empty_cache()
+    sbv, bfv = res["switchback"], res["bf16"]
+    line = {"metric": "ViT-H transformer block fwd+bwd tokens/s (model-level caller, SURVEY.md §8f row 2)",
+            "value": sbv["value"], "unit": "tokens/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": sbv["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int8 (linear fwd, dX) + bf16 (dW, attention, LN, GELU)", "data": "synthetic",
+            "config": {"workload": "CLIP ViT-Huge block (pre-LN, 16-head SDPA, MLP 5120, GELU), 256 images x 257 tokens",
+                       "config": "vit_block", "tokens": T, "cuda_graphs": True,
+                       "l2": "activations far larger than L2"},
+            "gpu_launches": launches * args.steps if launches is not None else None,
+            "clocks": sbv["clocks"],
+            "bf16_block": bfv, "speedup_vs_bf16_block": bfv["ms_per_step"] / sbv["ms_per_step"],
+            "e2e": None, "cpu_baseline": None, "roofline": None}
+    print(json.dumps(line), flush=True)
+
+
 def cpu_optimizer_rate(budget_s: float = 10.0):
     """The reference's optimizer_step (oracle/_ref, single-threaded as the reference) on a
     bounded sample of the C5 tensors; params/s."""
@@ -679,7 +774,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c5"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c5", "vit_block"])
     ap.add_argument("--tokens", type=int, default=T_PER_GPU)
     ap.add_argument("--ref-budget", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
@@ -691,6 +786,8 @@ def main():
         run_reference_arm(args)
     elif args.config == "c5":
         run_c5(args)
+    elif args.config == "vit_block":
+        run_vit_block(args)
     else:
         run_ours(args)
 

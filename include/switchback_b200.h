@@ -209,6 +209,13 @@ sb_status sb_linear_forward(sb_handle h, const sb_linear_mode* mode, const void*
                             int64_t b, int64_t n, int64_t m, void* y, sb_linear_ctx* ctx, void* workspace,
                             size_t workspace_bytes);
 
+/* sb_linear_forward plus an fp32 per-output-column bias (m values, NULL = none): y = X W^T + b.
+ * The reference applies biases outside linear_forward (model.cpp:303-333); here the add is
+ * fused into the int8 GEMM epilogue (one rounding to dt, no extra pass over y). */
+sb_status sb_linear_forward_bias(sb_handle h, const sb_linear_mode* mode, const void* x, const void* w,
+                                 const float* bias, sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y,
+                                 sb_linear_ctx* ctx, void* workspace, size_t workspace_bytes);
+
 /* linear_backward, linear.hpp:66-67 / linear.cpp:199-278: {dx [b x n] (dt), dw [m x n] (fp32)}.
  * dw_accumulate = 1 adds into dw (gradient accumulation / DP bucket). */
 sb_status sb_linear_backward(sb_handle h, const sb_linear_mode* mode, const sb_linear_ctx* ctx, const void* g,

@@ -398,8 +398,13 @@ static bool same_mode(const sb_linear_mode& a, const sb_linear_mode& b) {  // Li
   return a.fp8_forward == b.fp8_forward && a.fp8_gradient == b.fp8_gradient;
 }
 
-sb_status sb_linear_forward(sb_handle h, const sb_linear_mode* mode, const void* x, const void* w, sb_dtype dt, int64_t b,
-                            int64_t n, int64_t m, void* y, sb_linear_ctx* ctx, void* workspace, size_t ws_bytes) {
+}  // extern "C"
+
+// linear_forward (+ optional fp32 column bias, fused into the int8 GEMM epilogue on the
+// tensor-core path; added after the product on the others).
+static sb_status linear_forward_impl(sb_handle h, const sb_linear_mode* mode, const void* x, const void* w,
+                                     const float* bias, sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y,
+                                     sb_linear_ctx* ctx, void* workspace, size_t ws_bytes) {
   const char* op = "linear_forward";
   SB_TRY(check_h(h, op));
   if (!mode || !x || !w || !y || !float_dtype(dt)) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
@@ -431,6 +436,7 @@ sb_status sb_linear_forward(sb_handle h, const sb_linear_mode* mode, const void*
     } else {
       SB_TRY(gemm_bf16(h, x, false, w, false, b, m, n, y, out_dt));
     }
+    if (bias) SB_TRYC(op, sb::launch_add_bias(h, y, out_dt, b, m, bias));
     if (ctx) ctx->valid = 1;
     return SB_OK;
   }
@@ -439,11 +445,11 @@ sb_status sb_linear_forward(sb_handle h, const sb_linear_mode* mode, const void*
     if (md.variant == SB_SWITCHBACK_Q) {
       // dual row-wise: Y = qrow(X) . qrow(W)^T (linear.cpp:131-132)
       SB_TRYC(op, sb::launch_quantize_rowwise(h, w, dt, m, n, n, ws.w_q, n, ws.w_state));
-      SB_TRY(sb::gemm_i8(h, ws.x_q, ws.x_state, ws.w_q, ws.w_state, SB_SCALE_ROW_ROW, b, m, n, y, out_dt, md.exact));
+      SB_TRY(sb::gemm_i8(h, ws.x_q, ws.x_state, ws.w_q, ws.w_state, SB_SCALE_ROW_ROW, b, m, n, y, out_dt, md.exact, bias));
     } else {
       // tensor-wise W, both layouts from one read; W^T payload cached for the backward
       SB_TRY(q_tensorwise(h, w, dt, m, n, n, ws.w_q, n, ws.w_qt, m, ws.w_state, ws.words));
-      SB_TRY(sb::gemm_i8(h, ws.x_q, ws.x_state, ws.w_q, ws.w_state, SB_SCALE_ROW_TENSOR, b, m, n, y, out_dt, md.exact));
+      SB_TRY(sb::gemm_i8(h, ws.x_q, ws.x_state, ws.w_q, ws.w_state, SB_SCALE_ROW_TENSOR, b, m, n, y, out_dt, md.exact, bias));
     }
     if (ctx) {
       ctx->w_q_t = md.variant == SB_SWITCHBACK_Q ? nullptr : ws.w_qt;
@@ -474,6 +480,7 @@ sb_status sb_linear_forward(sb_handle h, const sb_linear_mode* mode, const void*
   } else {
     SB_TRY(sb::gemm_fp8(h, xq, ff, ws.x_state, ax, wq, ff, ws.w_state, wx, b, m, n, y, out_dt));
   }
+  if (bias) SB_TRYC(op, sb::launch_add_bias(h, y, out_dt, b, m, bias));
   if (ctx) {
     if (md.variant == SB_SWITCHBACK_M) {
       ctx->x_q = ws.x_q;
@@ -485,6 +492,19 @@ sb_status sb_linear_forward(sb_handle h, const sb_linear_mode* mode, const void*
     ctx->valid = 1;
   }
   return SB_OK;
+}
+
+extern "C" {
+
+sb_status sb_linear_forward(sb_handle h, const sb_linear_mode* mode, const void* x, const void* w, sb_dtype dt, int64_t b,
+                            int64_t n, int64_t m, void* y, sb_linear_ctx* ctx, void* workspace, size_t ws_bytes) {
+  return linear_forward_impl(h, mode, x, w, nullptr, dt, b, n, m, y, ctx, workspace, ws_bytes);
+}
+
+sb_status sb_linear_forward_bias(sb_handle h, const sb_linear_mode* mode, const void* x, const void* w,
+                                 const float* bias, sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y,
+                                 sb_linear_ctx* ctx, void* workspace, size_t ws_bytes) {
+  return linear_forward_impl(h, mode, x, w, bias, dt, b, n, m, y, ctx, workspace, ws_bytes);
 }
 
 sb_status sb_linear_backward(sb_handle h, const sb_linear_mode* mode, const sb_linear_ctx* ctx, const void* g, void* dx,

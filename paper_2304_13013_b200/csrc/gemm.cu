@@ -352,7 +352,7 @@ bool encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, 
 }
 
 sb_status gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* qb, const float* sbp, int scale_mode,
-                  int64_t M, int64_t N, int64_t K, void* out, sb_dtype out_dt, int exact) {
+                  int64_t M, int64_t N, int64_t K, void* out, sb_dtype out_dt, int exact, const float* bias) {
   const char* op = "int8 matmul";
   const bool raw = scale_mode == SB_SCALE_NONE;
   if (raw && out_dt != SB_I32 && out_dt != SB_I64) return fail(SB_ERR_INVALID_ARGUMENT, op, "raw output needs I32/I64");
@@ -385,6 +385,7 @@ sb_status gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* 
     p.sb_stride = sb_stride;
     p.post_scale = 1.0f / 16129.0f;
     p.splits = 1;
+    p.bias = (out_mode == sbtc::OUT_BF16 || out_mode == sbtc::OUT_F32) ? bias : nullptr;
     cudaError_t e;
     const bool col = sb_stride == 1;
     switch (out_mode) {
@@ -403,6 +404,10 @@ sb_status gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* 
       default: e = launch_tc<sbtc::KIND_I8, sbtc::OUT_I32>(h, A, B, td, p, 0); break;
     }
     if (e != cudaSuccess) return cuda_fail(op, e);
+    if (bias && !p.bias) {
+      const cudaError_t be = launch_add_bias(h, out, out_dt, M, N, bias);
+      if (be != cudaSuccess) return cuda_fail(op, be);
+    }
     return SB_OK;
   }
   // SIMT path (unaligned / tiny / int64 accumulation)
@@ -420,6 +425,7 @@ sb_status gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* 
   else
     k_gemm_i8_simt<sbtc::OUT_BF16><<<grid, 128, 0, h->stream>>>(qa, sa, sa_stride, qb, sbp, sb_stride, M, N, K, out);
   SB_LAUNCH_CHECK(op);
+  if (bias) SB_CUDA_CHECK(op, launch_add_bias(h, out, out_dt, M, N, bias));
   return SB_OK;
 }
 

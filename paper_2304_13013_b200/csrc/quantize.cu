@@ -1445,6 +1445,28 @@ cudaError_t launch_fp8_cast(sb_handle h, const float* x, int64_t n, int fmt, flo
   return cudaGetLastError();
 }
 
+template <typename T>
+__global__ void k_add_bias(T* __restrict__ y, int64_t rows, int64_t cols, const float* __restrict__ bias) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float v = static_cast<float>(y[i]);
+    y[i] = static_cast<T>(__fadd_rn(v, bias[i % cols]));
+  }
+}
+
+cudaError_t launch_add_bias(sb_handle h, void* y, sb_dtype dt, int64_t rows, int64_t cols, const float* bias) {
+  const unsigned grid = grid_for(rows * cols, 256 * 4, h->num_sms);
+  h->launches++;
+  if (dt == SB_F32)
+    k_add_bias<<<grid, 256, 0, h->stream>>>(static_cast<float*>(y), rows, cols, bias);
+  else if (dt == SB_BF16)
+    k_add_bias<<<grid, 256, 0, h->stream>>>(static_cast<__nv_bfloat16*>(y), rows, cols, bias);
+  else
+    return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_convert(sb_handle h, const void* x, sb_dtype xdt, void* y, sb_dtype ydt, int64_t n) {
   const unsigned grid = grid_for(n, 256 * 4, h->num_sms);
   h->launches++;

@@ -118,11 +118,15 @@ cudaError_t launch_absmax_rows(sb_handle h, const void* x, sb_dtype dt, int64_t 
 cudaError_t launch_dequantize_fp8(sb_handle h, const uint8_t* q, int64_t rows, int64_t cols, int64_t ldq, int fmt,
                                   const float* state, int axis, void* y, sb_dtype ydt, int64_t ldy);
 cudaError_t launch_convert(sb_handle h, const void* x, sb_dtype xdt, void* y, sb_dtype ydt, int64_t n);
+// y[r, c] += bias[c] in place (y is SB_F32 or SB_BF16, rows x cols contiguous)
+cudaError_t launch_add_bias(sb_handle h, void* y, sb_dtype dt, int64_t rows, int64_t cols, const float* bias);
 cudaError_t launch_fp8_cast(sb_handle h, const float* x, int64_t n, int fmt, float* y);
 
 // gemm_i8.cu
+// bias (optional, fp32 [N]): fused into the tensor-core epilogue for bf16 / fp32 outputs,
+// otherwise added by launch_add_bias after the product.
 sb_status gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* qb, const float* sb, int scale_mode,
-                  int64_t M, int64_t N, int64_t K, void* out, sb_dtype out_dt, int exact);
+                  int64_t M, int64_t N, int64_t K, void* out, sb_dtype out_dt, int exact, const float* bias = nullptr);
 // gemm_bf16.cu
 sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m, int64_t n, float* dw,
                 int exact, int accumulate);

@@ -62,7 +62,14 @@ struct Params {
   int tiles_m, tiles_n;
   int splits;              // split-K factor: work unit u = (tile u / splits, k-slice u % splits)
   int m_fast;              // raster: 1 = consecutive tiles walk M (B tile reused), 0 = walk N (A reused)
+  const float* bias;       // optional per-output-column bias (OUT_BF16 / OUT_F32): y = fl(acc * scale) + bias
 };
+
+// Column bias for the epilogue: 0 outside D or without a bias (warp-uniform address: one
+// broadcast load per column, served from L1 after the first tile).
+__device__ __forceinline__ float col_bias(const Params& p, int col) {
+  return (p.bias != nullptr && col < p.N) ? __ldg(p.bias + col) : 0.0f;
+}
 
 // Work unit -> (m0, n0, [kb0, kb1)).
 __device__ __forceinline__ void unit_coords(const Params& p, int u, int k_blocks, int& m0, int& n0, int& kb0, int& kb1) {
@@ -219,6 +226,12 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
           b0 *= fr;
           b1 *= fr;
         }
+        if (p.bias != nullptr) {  // fused bias add before the single bf16 rounding
+          a0 = __fadd_rn(a0, col_bias(p, col0 + 2 * j));
+          a1 = __fadd_rn(a1, col_bias(p, col0 + 2 * j + 1));
+          b0 = __fadd_rn(b0, col_bias(p, col0 + 32 + 2 * j));
+          b1 = __fadd_rn(b1, col_bias(p, col0 + 32 + 2 * j + 1));
+        }
         w[j] = pack_bf16x2(a0, a1);
         w[16 + j] = pack_bf16x2(b0, b1);
       }
@@ -253,7 +266,9 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
             w[j] = __float_as_uint(__double2float_rn(d));
           } else {
             const float v = KIND == KIND_I8 ? static_cast<float>(static_cast<int32_t>(r[j])) : __uint_as_float(r[j]);
-            w[j] = __float_as_uint(SB_COL ? v * (fr * cs[cc + j]) : v * fr);
+            const float y = SB_COL ? __fmul_rn(v, fr * cs[cc + j]) : __fmul_rn(v, fr);
+            // bias as a separate rounded add: identical bits to an unfused y + bias
+            w[j] = __float_as_uint(p.bias != nullptr ? __fadd_rn(y, col_bias(p, n0 + cc + j)) : y);
           }
         }
         if (lane == 0) sbptx::tma_store_wait_read<0>();

@@ -311,8 +311,10 @@ def _workspace(mode: LinearMode, b: int, n: int, m: int, device) -> torch.Tensor
 
 
 def linear_forward(mode: LinearMode, x: torch.Tensor, w: torch.Tensor, ctx: LinearContext | None = None,
-                   workspace: torch.Tensor | None = None, check: bool = True) -> torch.Tensor:
-    """linear.cpp:113-164: Y = X W^T through the variant's quantized path."""
+                   workspace: torch.Tensor | None = None, check: bool = True,
+                   bias: torch.Tensor | None = None) -> torch.Tensor:
+    """linear.cpp:113-164: Y = X W^T through the variant's quantized path. `bias` (fp32, m)
+    is optional and fused into the GEMM epilogue (sb_linear_forward_bias)."""
     _need_cuda(x, w)
     if x.dim() != 2 or w.dim() != 2 or x.numel() == 0 or w.numel() == 0:
         raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "linear_forward: empty operand")
@@ -328,8 +330,15 @@ def linear_forward(mode: LinearMode, x: torch.Tensor, w: torch.Tensor, ctx: Line
     y = torch.empty((b, m), dtype=x.dtype, device=x.device)
     h = A.handle(x.device.index)
     raw = A.LinearCtx()
-    st = h.lib.sb_linear_forward(h.h, C.byref(mode.c()), _p(x), _p(w), _dt(x), b, n, m, _p(y), C.byref(raw),
-                                 _p(workspace), workspace.numel())
+    if bias is None:
+        st = h.lib.sb_linear_forward(h.h, C.byref(mode.c()), _p(x), _p(w), _dt(x), b, n, m, _p(y), C.byref(raw),
+                                     _p(workspace), workspace.numel())
+    else:
+        if bias.dtype != torch.float32 or bias.shape != (m,) or not bias.is_cuda:
+            raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "linear_forward: bias must be fp32 of shape (m,)")
+        bias = bias.contiguous()
+        st = h.lib.sb_linear_forward_bias(h.h, C.byref(mode.c()), _p(x), _p(w), _p(bias), _dt(x), b, n, m, _p(y),
+                                          C.byref(raw), _p(workspace), workspace.numel())
     A.check(st)
     try:
         _check_nonfinite(h, check)

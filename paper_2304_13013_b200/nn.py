@@ -24,21 +24,25 @@ _VARIANTS = {"switchback": A.SB_SWITCHBACK, "switchback_m": A.SB_SWITCHBACK_M, "
 
 class _SwitchBackLinearFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x2d: torch.Tensor, weight: torch.Tensor, mode: L.LinearMode):
+    def forward(ctx, x2d: torch.Tensor, weight: torch.Tensor, bias, mode: L.LinearMode):
         w = weight.detach().to(x2d.dtype).contiguous()
         lctx = L.LinearContext()
-        y = L.linear_forward(mode, x2d.contiguous(), w, lctx, check=False)
+        b = bias.detach().float() if bias is not None else None
+        y = L.linear_forward(mode, x2d.contiguous(), w, lctx, check=False, bias=b)  # bias fused in the epilogue
         ctx.lctx = lctx
         ctx.mode = mode
+        ctx.has_bias = bias is not None
         ctx.keep_w = w  # the device context references it until the backward
         return y
 
     @staticmethod
     def backward(ctx, g: torch.Tensor):
-        dx, dw = L.linear_backward(ctx.mode, ctx.lctx, g.contiguous(), check=False)
+        g = g.contiguous()
+        dx, dw = L.linear_backward(ctx.mode, ctx.lctx, g, check=False)
+        db = g.sum(0, dtype=torch.float32) if ctx.has_bias and ctx.needs_input_grad[2] else None
         ctx.lctx = None
         ctx.keep_w = None
-        return dx, dw, None
+        return dx, dw, db, None
 
 
 class SwitchBackLinear(torch.nn.Module):
@@ -57,11 +61,8 @@ class SwitchBackLinear(torch.nn.Module):
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         shape = x.shape
-        y = _SwitchBackLinearFn.apply(x.reshape(-1, self.in_features), self.weight, self.mode)
-        y = y.reshape(*shape[:-1], self.out_features)
-        if self.bias is not None:
-            y = y + self.bias.to(y.dtype)
-        return y
+        y = _SwitchBackLinearFn.apply(x.reshape(-1, self.in_features), self.weight, self.bias, self.mode)
+        return y.reshape(*shape[:-1], self.out_features)
 
     def extra_repr(self) -> str:
         return f"in_features={self.in_features}, out_features={self.out_features}, bias={self.bias is not None}"
