@@ -542,11 +542,12 @@ def run_vit_block(args):
     import torch.nn.functional as F
 
     from paper_2304_13013_b200 import _capi as A
-    from paper_2304_13013_b200.nn import SwitchBackLinear
+    from paper_2304_13013_b200.nn import SwitchBackLinear, SwitchBackMLP
 
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     B, S, D, H = 256, 257, 1280, 16
+    fused = not args.no_overlap  # --no-overlap also turns the MLP producer fusion off (A/B)
     T = B * S
 
     class Block(torch.nn.Module):
@@ -556,7 +557,12 @@ def run_vit_block(args):
                 (lambda i, o: torch.nn.Linear(i, o, device=dev))
             self.ln1 = torch.nn.LayerNorm(D, device=dev)
             self.ln2 = torch.nn.LayerNorm(D, device=dev)
-            self.qkv, self.out, self.fc1, self.fc2 = mk(D, 3 * D), mk(D, D), mk(D, 4 * D), mk(4 * D, D)
+            self.qkv, self.out = mk(D, 3 * D), mk(D, D)
+            if sb and fused:  # GELU fused into the quantization of fc2's input / fc1's gradient
+                self.mlp = SwitchBackMLP(D, 4 * D, device=dev)
+            else:
+                fc1, fc2 = mk(D, 4 * D), mk(4 * D, D)
+                self.mlp = torch.nn.Sequential(fc1, torch.nn.GELU(), fc2)
 
         def forward(self, x):
             h = self.ln1(x.float()).to(torch.bfloat16)
@@ -564,7 +570,7 @@ def run_vit_block(args):
             a = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(B, S, D)
             x = x + self.out(a)
             h = self.ln2(x.float()).to(torch.bfloat16)
-            return x + self.fc2(F.gelu(self.fc1(h)))
+            return x + self.mlp(h)
 
     gen = torch.Generator(device=dev).manual_seed(3)
     x0 = torch.randn(B, S, D, device=dev, generator=gen).to(torch.bfloat16)
@@ -621,6 +627,7 @@ def run_vit_block(args):
             "gpu_launches": launches * args.steps if launches is not None else None,
             "clocks": sbv["clocks"],
             "bf16_block": bfv, "speedup_vs_bf16_block": bfv["ms_per_step"] / sbv["ms_per_step"],
+            "mlp_producer_fusion": fused,
             "e2e": None, "cpu_baseline": None, "roofline": None}
     print(json.dumps(line), flush=True)
 

@@ -221,6 +221,25 @@ sb_status sb_linear_forward_bias(sb_handle h, const sb_linear_mode* mode, const 
 sb_status sb_linear_backward(sb_handle h, const sb_linear_mode* mode, const sb_linear_ctx* ctx, const void* g,
                              void* dx, float* dw, int dw_accumulate);
 
+/* ---- producer fusion (no reference counterpart: the reference
+ * quantizes inside linear_forward / linear_backward, linear.cpp:130-134, 216-235) ----
+ * act = gelu(pre) (erf form) written as bf16 together with its row-wise int8 payload and
+ * states: the payload/states equal sb_quantize_rowwise(act) bit for bit. */
+sb_status sb_gelu_quantize_rowwise(sb_handle h, const void* pre, sb_dtype dt, int64_t rows, int64_t cols, void* act,
+                                   int8_t* q, float* state);
+/* g = dact * gelu'(pre) as bf16 plus its row-wise int8 payload and states. */
+sb_status sb_gelu_backward_quantize_rowwise(sb_handle h, const void* dact, const void* pre, sb_dtype dt, int64_t rows,
+                                            int64_t cols, void* g, int8_t* q, float* state);
+/* sb_linear_forward_bias with X already quantized row-wise by its producer (x_q b x n, x_state b):
+ * int8 SwitchBack / SwitchBackM / SwitchBackQ, non-exact. x stays referenced by ctx (dW). */
+sb_status sb_linear_forward_prequant(sb_handle h, const sb_linear_mode* mode, const void* x, const int8_t* x_q,
+                                     const float* x_state, const void* w, const float* bias, sb_dtype dt, int64_t b,
+                                     int64_t n, int64_t m, void* y, sb_linear_ctx* ctx, void* workspace,
+                                     size_t workspace_bytes);
+/* sb_linear_backward with G already quantized row-wise by its producer (g_q b x m, g_state b). */
+sb_status sb_linear_backward_prequant(sb_handle h, const sb_linear_mode* mode, const sb_linear_ctx* ctx, const void* g,
+                                      const int8_t* g_q, const float* g_state, void* dx, float* dw, int dw_accumulate);
+
 /* The reference bench's `switchback_fwd_bwd` unit (bench.cpp:75-81) over HOST buffers:
  * copies x (b x n), w (m x n), g (b x m) in, runs forward + backward, copies y, dx, dw
  * out. Token rows are pipelined in chunks across two streams so PCIe copies overlap

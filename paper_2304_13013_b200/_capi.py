@@ -30,6 +30,8 @@ EXPORTS = [
     "sb_last_error", "sb_launch_count", "sb_quantize_rowwise", "sb_quantize_columnwise",
     "sb_quantize_tensorwise", "sb_dequantize", "sb_quantize_fp8", "sb_dequantize_fp8", "sb_gemm_i8",
     "sb_matmul_f32", "sb_wgrad", "sb_gemm_fp8", "sb_linear_workspace_size", "sb_linear_forward", "sb_linear_forward_bias",
+    "sb_linear_forward_prequant", "sb_linear_backward_prequant", "sb_gelu_quantize_rowwise",
+    "sb_gelu_backward_quantize_rowwise",
     "sb_linear_backward", "sb_switchback_fwd_bwd_host", "sb_stableadamw_workspace_size", "sb_stableadamw_step",
     "sb_device_alloc", "sb_device_free", "sb_copy_to_device", "sb_copy_to_host", "sb_check_finite", "sb_fp8_cast",
     "sb_transpose_i8", "sb_compute_rms", "sb_grad_clip_global_norm", "sb_filter_nonfinite", "sb_dequantize_values",
@@ -115,6 +117,11 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             "sb_linear_forward_bias": ([v, C.POINTER(LinearMode), v, v, v, i32, i64, i64, i64, v, C.POINTER(LinearCtx), v,
                                         sz], i32),
             "sb_linear_backward": ([v, C.POINTER(LinearMode), C.POINTER(LinearCtx), v, v, v, i32], i32),
+            "sb_linear_forward_prequant": ([v, C.POINTER(LinearMode), v, v, v, v, v, i32, i64, i64, i64, v,
+                                            C.POINTER(LinearCtx), v, sz], i32),
+            "sb_linear_backward_prequant": ([v, C.POINTER(LinearMode), C.POINTER(LinearCtx), v, v, v, v, v, i32], i32),
+            "sb_gelu_quantize_rowwise": ([v, v, i32, i64, i64, v, v, v], i32),
+            "sb_gelu_backward_quantize_rowwise": ([v, v, v, i32, i64, i64, v, v, v], i32),
             "sb_switchback_fwd_bwd_host": ([v, C.POINTER(LinearMode), v, v, v, i32, i64, i64, i64, v, v, v], i32),
             "sb_stableadamw_workspace_size": ([C.POINTER(AdamwTensor), i32, C.POINTER(sz)], i32),
             "sb_stableadamw_step": ([v, C.POINTER(AdamwTensor), i32, C.POINTER(AdamwHparams), i64, v, v, v, sz],

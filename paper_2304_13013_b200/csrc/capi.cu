@@ -225,6 +225,11 @@ sb_status sb_create(int device, sb_handle* out) {
     return sb::fail(SB_ERR_CUDA, "sb_create", "allocation failed");
   }
   cudaMemset(h->d_err, 0, sizeof(uint32_t));
+  if (sb::build_gelu_lut(h) != cudaSuccess) {
+    cudaFree(h->d_err);
+    delete h;
+    return sb::fail(SB_ERR_CUDA, "sb_create", "GELU table build failed");
+  }
   cudaDeviceSynchronize();
   *out = h;
   return SB_OK;
@@ -235,6 +240,7 @@ sb_status sb_destroy(sb_handle h) {
   cudaSetDevice(h->device);
   cudaDeviceSynchronize();
   if (h->d_err) cudaFree(h->d_err);
+  if (h->gelu_lut) cudaFree(h->gelu_lut);
   if (h->d_scratch) cudaFree(h->d_scratch);
   if (h->dev_pool) cudaFree(h->dev_pool);
   if (h->s_in) {
@@ -404,7 +410,8 @@ static bool same_mode(const sb_linear_mode& a, const sb_linear_mode& b) {  // Li
 // tensor-core path; added after the product on the others).
 static sb_status linear_forward_impl(sb_handle h, const sb_linear_mode* mode, const void* x, const void* w,
                                      const float* bias, sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y,
-                                     sb_linear_ctx* ctx, void* workspace, size_t ws_bytes) {
+                                     sb_linear_ctx* ctx, void* workspace, size_t ws_bytes,
+                                     const int8_t* xq_in = nullptr, const float* xs_in = nullptr) {
   const char* op = "linear_forward";
   SB_TRY(check_h(h, op));
   if (!mode || !x || !w || !y || !float_dtype(dt)) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
@@ -441,22 +448,30 @@ static sb_status linear_forward_impl(sb_handle h, const sb_linear_mode* mode, co
     return SB_OK;
   }
   if (md.format == SB_INT8) {
-    SB_TRYC(op, sb::launch_quantize_rowwise(h, x, dt, b, n, n, ws.x_q, n, ws.x_state));
+    // X quantized row-wise here, or already by its producer (fused activation + quantize)
+    int8_t* xq = ws.x_q;
+    float* xs = ws.x_state;
+    if (xq_in) {
+      xq = const_cast<int8_t*>(xq_in);
+      xs = const_cast<float*>(xs_in);
+    } else {
+      SB_TRYC(op, sb::launch_quantize_rowwise(h, x, dt, b, n, n, xq, n, xs));
+    }
     if (md.variant == SB_SWITCHBACK_Q) {
       // dual row-wise: Y = qrow(X) . qrow(W)^T (linear.cpp:131-132)
       SB_TRYC(op, sb::launch_quantize_rowwise(h, w, dt, m, n, n, ws.w_q, n, ws.w_state));
-      SB_TRY(sb::gemm_i8(h, ws.x_q, ws.x_state, ws.w_q, ws.w_state, SB_SCALE_ROW_ROW, b, m, n, y, out_dt, md.exact, bias));
+      SB_TRY(sb::gemm_i8(h, xq, xs, ws.w_q, ws.w_state, SB_SCALE_ROW_ROW, b, m, n, y, out_dt, md.exact, bias));
     } else {
       // tensor-wise W, both layouts from one read; W^T payload cached for the backward
       SB_TRY(q_tensorwise(h, w, dt, m, n, n, ws.w_q, n, ws.w_qt, m, ws.w_state, ws.words));
-      SB_TRY(sb::gemm_i8(h, ws.x_q, ws.x_state, ws.w_q, ws.w_state, SB_SCALE_ROW_TENSOR, b, m, n, y, out_dt, md.exact, bias));
+      SB_TRY(sb::gemm_i8(h, xq, xs, ws.w_q, ws.w_state, SB_SCALE_ROW_TENSOR, b, m, n, y, out_dt, md.exact, bias));
     }
     if (ctx) {
       ctx->w_q_t = md.variant == SB_SWITCHBACK_Q ? nullptr : ws.w_qt;
       ctx->w_state = ws.w_state;
       if (md.variant == SB_SWITCHBACK_M) {  // linear.cpp:137-139: keep only the int8 tensors
-        ctx->x_q = ws.x_q;
-        ctx->x_state = ws.x_state;
+        ctx->x_q = xq;
+        ctx->x_state = xs;
         ctx->x = nullptr;
         ctx->w = nullptr;
       }
@@ -507,8 +522,21 @@ sb_status sb_linear_forward_bias(sb_handle h, const sb_linear_mode* mode, const 
   return linear_forward_impl(h, mode, x, w, bias, dt, b, n, m, y, ctx, workspace, ws_bytes);
 }
 
-sb_status sb_linear_backward(sb_handle h, const sb_linear_mode* mode, const sb_linear_ctx* ctx, const void* g, void* dx,
-                             float* dw, int dw_accumulate) {
+sb_status sb_linear_forward_prequant(sb_handle h, const sb_linear_mode* mode, const void* x, const int8_t* x_q,
+                                     const float* x_state, const void* w, const float* bias, sb_dtype dt, int64_t b,
+                                     int64_t n, int64_t m, void* y, sb_linear_ctx* ctx, void* workspace,
+                                     size_t ws_bytes) {
+  if (!mode || !x_q || !x_state || mode->format != SB_INT8 || mode->variant == SB_STANDARD ||
+      mode->variant == SB_ALLQUANT || mode->exact)
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, "linear_forward", "pre-quantized X needs an int8 row-wise variant");
+  return linear_forward_impl(h, mode, x, w, bias, dt, b, n, m, y, ctx, workspace, ws_bytes, x_q, x_state);
+}
+
+}  // extern "C"
+
+static sb_status linear_backward_impl(sb_handle h, const sb_linear_mode* mode, const sb_linear_ctx* ctx, const void* g,
+                                      void* dx, float* dw, int dw_accumulate, const int8_t* gq_in = nullptr,
+                                      const float* gs_in = nullptr) {
   const char* op = "linear_backward";
   SB_TRY(check_h(h, op));
   if (!mode || !ctx || !ctx->valid || !g || !dx || !dw) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
@@ -532,14 +560,22 @@ sb_status sb_linear_backward(sb_handle h, const sb_linear_mode* mode, const sb_l
   }
 
   if (md.format == SB_INT8) {
-    SB_TRYC(op, sb::launch_quantize_rowwise(h, g, dt, b, m, m, ws.g_q, m, ws.g_state));
+    // G quantized row-wise here, or already by its producer (fused GELU backward + quantize)
+    int8_t* gq = ws.g_q;
+    float* gs = ws.g_state;
+    if (gq_in) {
+      gq = const_cast<int8_t*>(gq_in);
+      gs = const_cast<float*>(gs_in);
+    } else {
+      SB_TRYC(op, sb::launch_quantize_rowwise(h, g, dt, b, m, m, gq, m, gs));
+    }
     if (md.variant == SB_SWITCHBACK_Q) {
       // column-wise quantize-transpose of W: per-row states of W^T (linear.cpp:226-229)
       SB_TRY(q_columnwise(h, ctx->w, dt, m, n, n, nullptr, 0, ws.w_qt, m, ws.wt_state, ws.words));
-      SB_TRY(sb::gemm_i8(h, ws.g_q, ws.g_state, ws.w_qt, ws.wt_state, SB_SCALE_ROW_ROW, b, n, m, dx, dt, exact));
+      SB_TRY(sb::gemm_i8(h, gq, gs, ws.w_qt, ws.wt_state, SB_SCALE_ROW_ROW, b, n, m, dx, dt, exact));
     } else {
       // W^T payload from the forward (== quantize_tensorwise_transpose(W), linear_test.cpp:252-264)
-      SB_TRY(sb::gemm_i8(h, ws.g_q, ws.g_state, ctx->w_q_t, ctx->w_state, SB_SCALE_ROW_TENSOR, b, n, m, dx, dt, exact));
+      SB_TRY(sb::gemm_i8(h, gq, gs, ctx->w_q_t, ctx->w_state, SB_SCALE_ROW_TENSOR, b, n, m, dx, dt, exact));
     }
     if (md.variant == SB_ALLQUANT) {
       // dW = dual_rowwise(qrow(G^T), qrow(X^T)) with K = b (linear.cpp:239-241)
@@ -605,6 +641,42 @@ sb_status sb_linear_backward(sb_handle h, const sb_linear_mode* mode, const sb_l
     return sb::wgrad(h, g, ws.deq, dt, b, m, n, dw, exact, dw_accumulate);
   }
   return sb::wgrad(h, g, ctx->x, dt, b, m, n, dw, exact, dw_accumulate);
+}
+
+extern "C" {
+
+sb_status sb_linear_backward(sb_handle h, const sb_linear_mode* mode, const sb_linear_ctx* ctx, const void* g, void* dx,
+                             float* dw, int dw_accumulate) {
+  return linear_backward_impl(h, mode, ctx, g, dx, dw, dw_accumulate);
+}
+
+sb_status sb_linear_backward_prequant(sb_handle h, const sb_linear_mode* mode, const sb_linear_ctx* ctx, const void* g,
+                                      const int8_t* g_q, const float* g_state, void* dx, float* dw, int dw_accumulate) {
+  if (!mode || !g_q || !g_state || mode->format != SB_INT8 || mode->variant == SB_STANDARD ||
+      mode->variant == SB_ALLQUANT || mode->exact)
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, "linear_backward", "pre-quantized G needs an int8 row-wise variant");
+  return linear_backward_impl(h, mode, ctx, g, dx, dw, dw_accumulate, g_q, g_state);
+}
+
+sb_status sb_gelu_quantize_rowwise(sb_handle h, const void* pre, sb_dtype dt, int64_t rows, int64_t cols, void* act,
+                                   int8_t* q, float* state) {
+  const char* op = "gelu_quantize_rowwise";
+  SB_TRY(check_h(h, op));
+  if (!pre || !act || !q || !state || dt != SB_BF16) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument (bf16 only)");
+  if (rows <= 0 || cols <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty matrix");
+  SB_TRYC(op, sb::launch_act_quantize_rowwise(h, 0, pre, nullptr, rows, cols, act, q, state));
+  return SB_OK;
+}
+
+sb_status sb_gelu_backward_quantize_rowwise(sb_handle h, const void* dact, const void* pre, sb_dtype dt, int64_t rows,
+                                            int64_t cols, void* g, int8_t* q, float* state) {
+  const char* op = "gelu_backward_quantize_rowwise";
+  SB_TRY(check_h(h, op));
+  if (!dact || !pre || !g || !q || !state || dt != SB_BF16)
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument (bf16 only)");
+  if (rows <= 0 || cols <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty matrix");
+  SB_TRYC(op, sb::launch_act_quantize_rowwise(h, 1, dact, pre, rows, cols, g, q, state));
+  return SB_OK;
 }
 
 // ------------------------------------------------- host-buffer pipeline --

@@ -501,6 +501,186 @@ bool rowwise_reg(sb_handle h, const T* x, int64_t rows, int nvec, int64_t ldx, i
   }
 }
 
+// ---- producer fusion: activation + row-wise quantize -------------
+// The MLP's GELU (forward) and GELU backward produce exactly the rows the next SwitchBack
+// GEMM quantizes row-wise. One kernel computes the activation row into registers, stores
+// it (bf16: the weight gradient needs it), and quantizes the SAME register values: one read
+// of the producer's input instead of write + re-read. The payload and states are those of
+// quantize_rowwise(act) bit for bit (identical qvec / state path on identical bf16 values).
+//   MODE 0: act = gelu(a)            (erf form, as torch.nn.functional.gelu)
+//   MODE 1: act = a * gelu'(b)       (a = upstream gradient, b = the GELU input)
+__device__ __forceinline__ float gelu_f(float x) {
+  return 0.5f * x * (1.0f + erff(x * 0.70710678118654752440f));
+}
+__device__ __forceinline__ float gelu_grad_f(float dy, float x) {
+  const float cdf = 0.5f * (1.0f + erff(x * 0.70710678118654752440f));
+  const float pdf = expf(-0.5f * x * x) * 0.39894228040143267794f;
+  return dy * (cdf + x * pdf);
+}
+// bf16 inputs take only 65536 values, so the GELU (and GELU') of every |x| < 8 is tabulated
+// once per handle with the formulas above (build_gelu_lut) and read from shared memory:
+// a lookup instead of ~40 instructions of erf/exp per element, bit-identical to the formula
+// (the table IS the formula's output). |x| >= 8, inf and NaN take the formula directly.
+constexpr uint32_t kLutHalf = 0x4100u;  // bf16 bits of 8.0: |x| < 8 <=> (bits & 0x7fff) < kLutHalf
+constexpr int kLutEntries = 2 * kLutHalf;
+__device__ __forceinline__ int lut_index(uint32_t bits16) {
+  const uint32_t mag = bits16 & 0x7fffu;
+  return mag < kLutHalf ? static_cast<int>((bits16 >> 15) * kLutHalf + mag) : -1;
+}
+__global__ void k_build_gelu_lut(__nv_bfloat16* fwd, float* grad_factor) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kLutEntries; i += gridDim.x * blockDim.x) {
+    const uint32_t bits = i < static_cast<int>(kLutHalf) ? static_cast<uint32_t>(i) : 0x8000u + (i - kLutHalf);
+    const float x = __bfloat162float(__ushort_as_bfloat16(static_cast<unsigned short>(bits)));
+    fwd[i] = __float2bfloat16_rn(gelu_f(x));
+    const float cdf = 0.5f * (1.0f + erff(x * 0.70710678118654752440f));
+    const float pdf = expf(-0.5f * x * x) * 0.39894228040143267794f;
+    grad_factor[i] = cdf + x * pdf;  // gelu_grad_f(dy, x) == dy * grad_factor (same ops, no fma)
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ uint4 act_vec(const uint4& a, const uint4& b, const void* lut) {
+  uint4 r;
+  const uint32_t* wa = reinterpret_cast<const uint32_t*>(&a);
+  const uint32_t* wb = reinterpret_cast<const uint32_t*>(&b);
+  uint32_t* wr = reinterpret_cast<uint32_t*>(&r);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint32_t out = 0;
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      const uint32_t xa = (wa[k] >> (16 * hf)) & 0xffffu;  // MODE 0: x; MODE 1: dy
+      uint32_t o;
+      if (MODE == 0) {
+        const int li = lut_index(xa);
+        o = li >= 0 ? static_cast<const unsigned short*>(lut)[li]
+                    : __bfloat16_as_ushort(__float2bfloat16_rn(
+                          gelu_f(__bfloat162float(__ushort_as_bfloat16(static_cast<unsigned short>(xa))))));
+      } else {
+        const uint32_t xb = (wb[k] >> (16 * hf)) & 0xffffu;  // x
+        const float dy = __bfloat162float(__ushort_as_bfloat16(static_cast<unsigned short>(xa)));
+        const int li = lut_index(xb);
+        const float gv = li >= 0 ? dy * static_cast<const float*>(lut)[li]
+                                 : gelu_grad_f(dy, __bfloat162float(__ushort_as_bfloat16(static_cast<unsigned short>(xb))));
+        o = __bfloat16_as_ushort(__float2bfloat16_rn(gv));
+      }
+      out |= o << (16 * hf);
+    }
+    wr[k] = out;
+  }
+  return r;
+}
+
+// One warp per row, in chunks of 4 vectors per lane: pass 1 computes the activation, stores
+// it and takes the absmax; pass 2 re-reads the just-written row (an L2 hit) and quantizes.
+// The GELU math is long (erf, exp), so the row is NOT held in registers across it: a
+// register-resident row (the plain quantizer's design) needs ~210 registers here and runs
+// 2-3x slower at 12% occupancy.
+constexpr int kActThreads = 1024;
+template <int MODE>
+__global__ void __launch_bounds__(kActThreads, 1) k_act_quantize_rows(const __nv_bfloat16* __restrict__ a,
+                                                                     const __nv_bfloat16* __restrict__ b, int64_t rows,
+                                                                     int nvec, __nv_bfloat16* __restrict__ act,
+                                                                     int8_t* __restrict__ q, float* __restrict__ state,
+                                                                     uint32_t* err, const uint4* __restrict__ lut_g) {
+  using T = __nv_bfloat16;
+  using Out = typename VecQ<T>::Out;
+  constexpr int CH = 4;
+  constexpr int LUT_VECS = kLutEntries * (MODE == 0 ? 2 : 4) / 16;
+  extern __shared__ uint4 lut_s[];
+  for (int i = threadIdx.x; i < LUT_VECS; i += blockDim.x) lut_s[i] = __ldg(lut_g + i);
+  __syncthreads();
+  const void* lut = lut_s;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+       row += warps) {
+    const int64_t off = row * static_cast<int64_t>(nvec);
+    const uint4* ar = reinterpret_cast<const uint4*>(a) + off;
+    const uint4* br = reinterpret_cast<const uint4*>(b) + off;
+    uint4* outr = reinterpret_cast<uint4*>(act) + off;
+    uint32_t amax = 0;
+    for (int c0 = 0; c0 < nvec; c0 += 32 * CH) {
+      uint4 v[CH], w[CH];
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const int i = c0 + j * 32 + lane;
+        v[j] = i < nvec ? ld_stream(ar + i) : make_uint4(0, 0, 0, 0);
+        if (MODE == 1) w[j] = i < nvec ? ld_stream(br + i) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const int i = c0 + j * 32 + lane;
+        const uint4 r = act_vec<MODE>(v[j], MODE == 1 ? w[j] : v[j], lut);
+        if (i < nvec) {
+          outr[i] = r;
+          amax = max(amax, vec_absmax_bits<T>(r));
+        }
+      }
+    }
+    amax = __reduce_max_sync(0xffffffffu, amax);
+    if (amax >= kNonFiniteBits) {
+      if (lane == 0) {
+        raise_nonfinite(err);
+        state[row] = __uint_as_float(amax);
+      }
+      continue;
+    }
+    const float st = state_from_bits(amax);
+    if (lane == 0) state[row] = st;
+    const Scale sc = make_scale(st);
+    const bool plain = sc.pre == 1.0f;
+    __syncwarp();  // this warp's act stores precede its re-reads
+    Out* qr = reinterpret_cast<Out*>(q + off * 8);
+    for (int c0 = 0; c0 < nvec; c0 += 32 * CH) {  // warp-uniform trip count (qvec votes)
+      uint4 v[CH];
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const int i = c0 + j * 32 + lane;
+        v[j] = i < nvec ? __ldcg(outr + i) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const int i = c0 + j * 32 + lane;
+        const Out o = qvec<T>(v[j], sc, plain);
+        if (i < nvec) qr[i] = o;
+      }
+    }
+  }
+}
+
+// Any shape: the activation elementwise (same formulas), then the row-wise quantizer.
+template <int MODE>
+__global__ void k_act_elementwise(const __nv_bfloat16* __restrict__ a, const __nv_bfloat16* __restrict__ b, int64_t n,
+                                  __nv_bfloat16* __restrict__ act) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float x = __bfloat162float(a[i]);
+    act[i] = __float2bfloat16_rn(MODE == 0 ? gelu_f(x) : gelu_grad_f(x, __bfloat162float(b[i])));
+  }
+}
+
+template <int MODE>
+cudaError_t launch_act_rows(sb_handle h, const __nv_bfloat16* a, const __nv_bfloat16* b, int64_t rows, int nvec,
+                            __nv_bfloat16* act, int8_t* q, float* state) {
+  const size_t smem = static_cast<size_t>(kLutEntries) * (MODE == 0 ? 2 : 4);
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(k_act_quantize_rows<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const uint4* lut = reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(h->gelu_lut) +
+                                                    (MODE == 0 ? 0 : static_cast<size_t>(kLutEntries) * 2));
+  const int64_t need = (rows + 31) / 32;
+  const int64_t blocks = std::min<int64_t>(need, static_cast<int64_t>(h->num_sms));
+  h->launches++;
+  k_act_quantize_rows<MODE><<<static_cast<unsigned>(blocks), kActThreads, smem, h->stream>>>(a, b, rows, nvec, act, q,
+                                                                                             state, h->d_err, lut);
+  return cudaGetLastError();
+}
+
 // SB_QUANT_KERNEL=tma selects the smem-ring kernel (A/B measurements); default: registers.
 bool prefer_tma_ring() {
   static int v = -1;
@@ -1465,6 +1645,46 @@ cudaError_t launch_add_bias(sb_handle h, void* y, sb_dtype dt, int64_t rows, int
   else
     return cudaErrorInvalidValue;
   return cudaGetLastError();
+}
+
+cudaError_t build_gelu_lut(sb_handle h) {
+  if (h->gelu_lut) return cudaSuccess;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, static_cast<size_t>(kLutEntries) * 6);
+  if (e != cudaSuccess) return e;
+  k_build_gelu_lut<<<64, 256>>>(static_cast<__nv_bfloat16*>(p),
+                               reinterpret_cast<float*>(static_cast<uint8_t*>(p) + static_cast<size_t>(kLutEntries) * 2));
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return e;
+  }
+  h->gelu_lut = p;
+  return cudaSuccess;
+}
+
+cudaError_t launch_act_quantize_rowwise(sb_handle h, int mode, const void* a, const void* b, int64_t rows, int64_t cols,
+                                        void* act, int8_t* q, float* state) {
+  using bf = __nv_bfloat16;
+  const bf* A = static_cast<const bf*>(a);
+  const bf* B = static_cast<const bf*>(b);
+  bf* O = static_cast<bf*>(act);
+  const bool vec_ok = h->gelu_lut && cols % 8 == 0 && sb::aligned(a, 16) && (mode == 0 || sb::aligned(b, 16)) &&
+                      sb::aligned(act, 16) && sb::aligned(q, 8) && cols / 8 < (1 << 30);
+  if (vec_ok) {
+    const int nvec = static_cast<int>(cols / 8);
+    return mode == 0 ? launch_act_rows<0>(h, A, B, rows, nvec, O, q, state)
+                     : launch_act_rows<1>(h, A, B, rows, nvec, O, q, state);
+  }
+  const unsigned grid = grid_for(rows * cols, 256 * 4, h->num_sms);
+  h->launches++;
+  if (mode == 0)
+    k_act_elementwise<0><<<grid, 256, 0, h->stream>>>(A, B, rows * cols, O);
+  else
+    k_act_elementwise<1><<<grid, 256, 0, h->stream>>>(A, B, rows * cols, O);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_quantize_rowwise(h, act, SB_BF16, rows, cols, cols, q, cols, state);
 }
 
 cudaError_t launch_convert(sb_handle h, const void* x, sb_dtype xdt, void* y, sb_dtype ydt, int64_t n) {

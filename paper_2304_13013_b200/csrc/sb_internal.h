@@ -24,6 +24,7 @@ struct sb_handle_s {
   cudaEvent_t hp_start = nullptr;
   void* dev_pool = nullptr;
   size_t dev_pool_bytes = 0;
+  void* gelu_lut = nullptr;  // GELU / GELU' tables for bf16 |x| < 8 (built at sb_create)
 };
 
 namespace sb {
@@ -118,6 +119,11 @@ cudaError_t launch_absmax_rows(sb_handle h, const void* x, sb_dtype dt, int64_t 
 cudaError_t launch_dequantize_fp8(sb_handle h, const uint8_t* q, int64_t rows, int64_t cols, int64_t ldq, int fmt,
                                   const float* state, int axis, void* y, sb_dtype ydt, int64_t ldy);
 cudaError_t launch_convert(sb_handle h, const void* x, sb_dtype xdt, void* y, sb_dtype ydt, int64_t n);
+cudaError_t build_gelu_lut(sb_handle h);
+// Fused activation + row-wise quantize (bf16, contiguous rows): mode 0 act = gelu(a),
+// mode 1 act = a * gelu'(b); writes act and the int8 payload / states of act.
+cudaError_t launch_act_quantize_rowwise(sb_handle h, int mode, const void* a, const void* b, int64_t rows, int64_t cols,
+                                        void* act, int8_t* q, float* state);
 // y[r, c] += bias[c] in place (y is SB_F32 or SB_BF16, rows x cols contiguous)
 cudaError_t launch_add_bias(sb_handle h, void* y, sb_dtype dt, int64_t rows, int64_t cols, const float* bias);
 cudaError_t launch_fp8_cast(sb_handle h, const float* x, int64_t n, int fmt, float* y);

@@ -107,6 +107,36 @@ def quantize_rowwise(x: torch.Tensor, check: bool = True) -> QuantizedMatrix:
     return QuantizedMatrix(q, st, ROW)
 
 
+def gelu_quantize_rowwise(pre: torch.Tensor, check: bool = True) -> tuple[torch.Tensor, QuantizedMatrix]:
+    """Producer fusion: act = gelu(pre) (bf16) and quantize_rowwise(act)
+    from one read of pre."""
+    _need_cuda(pre)
+    pre = pre.contiguous()
+    r, c = pre.shape
+    act = torch.empty_like(pre)
+    q = torch.empty((r, c), dtype=torch.int8, device=pre.device)
+    st = torch.empty(r, dtype=torch.float32, device=pre.device)
+    h = A.handle(pre.device.index)
+    A.check(h.lib.sb_gelu_quantize_rowwise(h.h, _p(pre), _dt(pre), r, c, _p(act), _p(q), _p(st)))
+    _check_nonfinite(h, check)
+    return act, QuantizedMatrix(q, st, ROW)
+
+
+def gelu_backward_quantize_rowwise(dact: torch.Tensor, pre: torch.Tensor,
+                                   check: bool = True) -> tuple[torch.Tensor, QuantizedMatrix]:
+    """g = dact * gelu'(pre) (bf16) and quantize_rowwise(g) from one read of dact and pre."""
+    _need_cuda(dact, pre)
+    dact, pre = dact.contiguous(), pre.contiguous()
+    r, c = pre.shape
+    g = torch.empty_like(pre)
+    q = torch.empty((r, c), dtype=torch.int8, device=pre.device)
+    st = torch.empty(r, dtype=torch.float32, device=pre.device)
+    h = A.handle(pre.device.index)
+    A.check(h.lib.sb_gelu_backward_quantize_rowwise(h.h, _p(dact), _p(pre), _dt(pre), r, c, _p(g), _p(q), _p(st)))
+    _check_nonfinite(h, check)
+    return g, QuantizedMatrix(q, st, ROW)
+
+
 def quantize_columnwise(x: torch.Tensor, check: bool = True, transposed: bool = False) -> QuantizedMatrix:
     """quantize.cpp:135-137. transposed=True returns quantize_rowwise(x^T) (linear.cpp:228-229)."""
     _need_cuda(x)
@@ -312,9 +342,10 @@ def _workspace(mode: LinearMode, b: int, n: int, m: int, device) -> torch.Tensor
 
 def linear_forward(mode: LinearMode, x: torch.Tensor, w: torch.Tensor, ctx: LinearContext | None = None,
                    workspace: torch.Tensor | None = None, check: bool = True,
-                   bias: torch.Tensor | None = None) -> torch.Tensor:
+                   bias: torch.Tensor | None = None, x_q: QuantizedMatrix | None = None) -> torch.Tensor:
     """linear.cpp:113-164: Y = X W^T through the variant's quantized path. `bias` (fp32, m)
-    is optional and fused into the GEMM epilogue (sb_linear_forward_bias)."""
+    is optional and fused into the GEMM epilogue (sb_linear_forward_bias). `x_q`: X already
+    quantized row-wise by its producer (gelu_quantize_rowwise), skipping that pass."""
     _need_cuda(x, w)
     if x.dim() != 2 or w.dim() != 2 or x.numel() == 0 or w.numel() == 0:
         raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "linear_forward: empty operand")
@@ -330,7 +361,16 @@ def linear_forward(mode: LinearMode, x: torch.Tensor, w: torch.Tensor, ctx: Line
     y = torch.empty((b, m), dtype=x.dtype, device=x.device)
     h = A.handle(x.device.index)
     raw = A.LinearCtx()
-    if bias is None:
+    if x_q is not None:
+        bp = None
+        if bias is not None:
+            if bias.dtype != torch.float32 or bias.shape != (m,) or not bias.is_cuda:
+                raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "linear_forward: bias must be fp32 of shape (m,)")
+            bias = bias.contiguous()
+            bp = bias
+        st = h.lib.sb_linear_forward_prequant(h.h, C.byref(mode.c()), _p(x), _p(x_q.payload), _p(x_q.state), _p(w), _p(bp),
+                                              _dt(x), b, n, m, _p(y), C.byref(raw), _p(workspace), workspace.numel())
+    elif bias is None:
         st = h.lib.sb_linear_forward(h.h, C.byref(mode.c()), _p(x), _p(w), _dt(x), b, n, m, _p(y), C.byref(raw),
                                      _p(workspace), workspace.numel())
     else:
@@ -347,14 +387,16 @@ def linear_forward(mode: LinearMode, x: torch.Tensor, w: torch.Tensor, ctx: Line
     if ctx is not None:
         ctx.mode = mode
         ctx.raw = raw
-        ctx.keep = (x, w) if mode.variant != A.SB_SWITCHBACK_M else ()
+        ctx.keep = ((x, w) if mode.variant != A.SB_SWITCHBACK_M else ()) + ((x_q,) if x_q is not None else ())
         ctx.workspace = workspace
     return y
 
 
 def linear_backward(mode: LinearMode, ctx: LinearContext, g: torch.Tensor, dw: torch.Tensor | None = None,
-                    dw_accumulate: bool = False, check: bool = True) -> tuple[torch.Tensor, torch.Tensor]:
-    """linear.cpp:199-278 -> (x_grad [b x n], w_grad [m x n] fp32)."""
+                    dw_accumulate: bool = False, check: bool = True,
+                    g_q: QuantizedMatrix | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """linear.cpp:199-278 -> (x_grad [b x n], w_grad [m x n] fp32). `g_q`: G already quantized
+    row-wise by its producer (gelu_backward_quantize_rowwise)."""
     if ctx.mode is None or not (mode == ctx.mode):
         raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT,
                               "linear_backward: context was produced by a different mode")
@@ -367,7 +409,12 @@ def linear_backward(mode: LinearMode, ctx: LinearContext, g: torch.Tensor, dw: t
     if dw is None:
         dw = torch.empty((r.m, r.n), dtype=torch.float32, device=g.device)
     h = A.handle(g.device.index)
-    A.check(h.lib.sb_linear_backward(h.h, C.byref(mode.c()), C.byref(r), _p(g), _p(dx), _p(dw), int(dw_accumulate)))
+    if g_q is not None:
+        A.check(h.lib.sb_linear_backward_prequant(h.h, C.byref(mode.c()), C.byref(r), _p(g), _p(g_q.payload), _p(g_q.state),
+                                                  _p(dx), _p(dw), int(dw_accumulate)))
+    else:
+        A.check(h.lib.sb_linear_backward(h.h, C.byref(mode.c()), C.byref(r), _p(g), _p(dx), _p(dw),
+                                         int(dw_accumulate)))
     try:
         _check_nonfinite(h, check)
     except InvalidArgument:

@@ -66,3 +66,59 @@ class SwitchBackLinear(torch.nn.Module):
 
     def extra_repr(self) -> str:
         return f"in_features={self.in_features}, out_features={self.out_features}, bias={self.bias is not None}"
+
+
+class _SwitchBackMLPFn(torch.autograd.Function):
+    """fc1 -> GELU -> fc2 with the producer fusions of SURVEY.md §8f row 1: GELU writes fc2's
+    row-wise int8 input in the same pass (sb_gelu_quantize_rowwise), and GELU's backward
+    writes fc1's quantized output gradient (sb_gelu_backward_quantize_rowwise), so neither
+    activation is re-read just to be quantized."""
+
+    @staticmethod
+    def forward(ctx, x2d, w1, b1, w2, b2, mode: L.LinearMode):
+        dt = x2d.dtype
+        w1b, w2b = w1.detach().to(dt).contiguous(), w2.detach().to(dt).contiguous()
+        c1, c2 = L.LinearContext(), L.LinearContext()
+        pre = L.linear_forward(mode, x2d.contiguous(), w1b, c1, check=False,
+                               bias=b1.detach().float() if b1 is not None else None)
+        act, act_q = L.gelu_quantize_rowwise(pre, check=False)
+        y = L.linear_forward(mode, act, w2b, c2, check=False, bias=b2.detach().float() if b2 is not None else None,
+                             x_q=act_q)
+        ctx.state = (c1, c2, pre, w1b, w2b)
+        ctx.mode = mode
+        ctx.bias = (b1 is not None, b2 is not None)
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        c1, c2, pre, _, _ = ctx.state
+        gy = gy.contiguous()
+        dact, dw2 = L.linear_backward(ctx.mode, c2, gy, check=False)
+        g1, g1_q = L.gelu_backward_quantize_rowwise(dact, pre, check=False)
+        dx, dw1 = L.linear_backward(ctx.mode, c1, g1, check=False, g_q=g1_q)
+        db1 = g1.sum(0, dtype=torch.float32) if ctx.bias[0] and ctx.needs_input_grad[2] else None
+        db2 = gy.sum(0, dtype=torch.float32) if ctx.bias[1] and ctx.needs_input_grad[4] else None
+        ctx.state = None
+        return dx, dw1, db1, dw2, db2, None
+
+
+class SwitchBackMLP(torch.nn.Module):
+    """Transformer MLP (fc1 -> GELU -> fc2) on SwitchBack linears with the activation fused into
+    the quantization of its consumer (forward) and producer-gradient (backward). bf16 inputs."""
+
+    def __init__(self, in_features: int, hidden_features: int, out_features: int | None = None, bias: bool = True,
+                 variant: str = "switchback", device=None):
+        super().__init__()
+        out_features = out_features or in_features
+        self.fc1 = SwitchBackLinear(in_features, hidden_features, bias=bias, variant=variant, device=device)
+        self.fc2 = SwitchBackLinear(hidden_features, out_features, bias=bias, variant=variant, device=device)
+        if variant not in ("switchback", "switchback_m", "switchback_q"):
+            raise ValueError("SwitchBackMLP needs an int8 row-wise variant")
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        if x.dtype != torch.bfloat16:
+            raise TypeError("SwitchBackMLP runs in bf16")
+        shape = x.shape
+        y = _SwitchBackMLPFn.apply(x.reshape(-1, self.fc1.in_features), self.fc1.weight, self.fc1.bias,
+                                   self.fc2.weight, self.fc2.bias, self.fc1.mode)
+        return y.reshape(*shape[:-1], self.fc2.out_features)

@@ -86,3 +86,66 @@ def test_cuda_graph_capture_replays_identically():
     torch.cuda.synchronize()
     assert torch.equal(out_y, ref_y) and torch.equal(out_dx, ref_dx)
     L.check_error()
+
+
+@pytest.mark.parametrize("rows,cols", [(1000, 5120), (37, 1280), (8, 8), (7, 100)])
+def test_gelu_quantize_fused_matches_composition(rows, cols):
+    """act == gelu(pre) within one bf16 ulp of torch's, and its payload / states are exactly
+    quantize_rowwise(act) (the fused kernel quantizes the values it stores)."""
+    torch.manual_seed(rows + cols)
+    pre = (torch.randn(rows, cols, device="cuda") * 2).bfloat16()
+    pre[0, :3] = 0
+    act, q = L.gelu_quantize_rowwise(pre)
+    ref = torch.nn.functional.gelu(pre.float())
+    assert ((act.float() - ref).abs() <= ref.abs() * 2 ** -7 + 1e-6).all()
+    q2 = L.quantize_rowwise(act)
+    assert torch.equal(q.payload, q2.payload) and torch.equal(q.state, q2.state)
+    dact = torch.randn(rows, cols, device="cuda").bfloat16()
+    g, gq = L.gelu_backward_quantize_rowwise(dact, pre)
+    x = pre.float().requires_grad_(True)
+    torch.nn.functional.gelu(x).backward(dact.float())
+    assert ((g.float() - x.grad).abs() <= x.grad.abs() * 2 ** -7 + 1e-5).all()
+    g2 = L.quantize_rowwise(g)
+    assert torch.equal(gq.payload, g2.payload) and torch.equal(gq.state, g2.state)
+
+
+def test_mlp_fused_module_matches_fp32():
+    from paper_2304_13013_b200.nn import SwitchBackMLP
+
+    torch.manual_seed(5)
+    mlp = SwitchBackMLP(256, 1024)
+    with torch.no_grad():
+        mlp.fc1.bias.normal_()
+        mlp.fc2.bias.normal_()
+    x = torch.randn(3, 333, 256, device="cuda").bfloat16().requires_grad_(True)
+    y = mlp(x)
+    g = torch.randn_like(y)
+    y.backward(g)
+    xr = x.detach().float().requires_grad_(True)
+    w1 = mlp.fc1.weight.detach().clone().requires_grad_(True)
+    w2 = mlp.fc2.weight.detach().clone().requires_grad_(True)
+    b1 = mlp.fc1.bias.detach().clone().requires_grad_(True)
+    b2 = mlp.fc2.bias.detach().clone().requires_grad_(True)
+    F = torch.nn.functional
+    yr = F.linear(F.gelu(F.linear(xr, w1, b1)), w2, b2)
+    yr.backward(g.float())
+    assert rel(y, yr) < 2e-2
+    assert rel(x.grad, xr.grad) < 3e-2
+    for p, r in ((mlp.fc1.weight, w1), (mlp.fc2.weight, w2), (mlp.fc1.bias, b1), (mlp.fc2.bias, b2)):
+        assert rel(p.grad, r.grad) < 2e-2
+
+
+def test_gelu_table_equals_formula_for_every_bf16():
+    """The fused kernels read GELU / GELU' from per-handle tables for |x| < 8; the (n x 1)
+    shape takes the elementwise formula path. Every one of the 65536 bf16 inputs must give
+    the same bits both ways (forward and backward)."""
+    allx = torch.arange(65536, dtype=torch.int32, device="cuda").to(torch.int16).view(torch.bfloat16)
+    a_vec, _ = L.gelu_quantize_rowwise(allx.view(8192, 8), check=False)
+    a_sc, _ = L.gelu_quantize_rowwise(allx.view(65536, 1), check=False)
+    assert torch.equal(a_vec.view(-1).view(torch.int16), a_sc.view(-1).view(torch.int16))
+    dy = torch.randn(65536, device="cuda").bfloat16()
+    g_vec, _ = L.gelu_backward_quantize_rowwise(dy.view(8192, 8), allx.view(8192, 8), check=False)
+    g_sc, _ = L.gelu_backward_quantize_rowwise(dy.view(65536, 1), allx.view(65536, 1), check=False)
+    assert torch.equal(g_vec.view(-1).view(torch.int16), g_sc.view(-1).view(torch.int16))
+    with pytest.raises(L.InvalidArgument):  # the inf / NaN inputs latched the error word: consume it
+        L.check_error()

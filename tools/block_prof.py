@@ -7,12 +7,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import torch.nn.functional as F
 
-from paper_2304_13013_b200.nn import SwitchBackLinear
+from paper_2304_13013_b200.nn import SwitchBackLinear, SwitchBackMLP
 
 dev = torch.device("cuda", 0)
 B, S, D, H = 256, 257, 1280, 16
-arm = os.environ.get("ARM", "switchback")
-mk = (lambda i, o: SwitchBackLinear(i, o, device=dev)) if arm == "switchback" else (lambda i, o: torch.nn.Linear(i, o, device=dev))
+arm = os.environ.get("ARM", "switchback")  # switchback | fused (SwitchBackMLP) | bf16
+mk = (lambda i, o: SwitchBackLinear(i, o, device=dev)) if arm != "bf16" else (lambda i, o: torch.nn.Linear(i, o, device=dev))
+mlp = SwitchBackMLP(D, 4 * D, device=dev) if arm == "fused" else None
 ln1, ln2 = torch.nn.LayerNorm(D, device=dev), torch.nn.LayerNorm(D, device=dev)
 qkv, out, fc1, fc2 = mk(D, 3 * D), mk(D, D), mk(D, 4 * D), mk(4 * D, D)
 x = torch.randn(B, S, D, device=dev).bfloat16().requires_grad_(True)
@@ -25,7 +26,7 @@ for it in range(2):
         a = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(B, S, D)
         x2 = x + out(a)
         h = ln2(x2.float()).to(torch.bfloat16)
-        y = x2 + fc2(F.gelu(fc1(h)))
+        y = x2 + (mlp(h) if mlp is not None else fc2(F.gelu(fc1(h))))
     y.backward(gy)
     torch.cuda.synchronize()
     torch.cuda.nvtx.range_pop()
