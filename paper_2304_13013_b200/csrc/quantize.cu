@@ -577,7 +577,7 @@ __device__ __forceinline__ uint4 act_vec(const uint4& a, const uint4& b, const v
 // register-resident row (the plain quantizer's design) needs ~210 registers here and runs
 // 2-3x slower at 12% occupancy.
 constexpr int kActThreads = 1024;
-template <int MODE>
+template <int MODE, int CH>
 __global__ void __launch_bounds__(kActThreads, 1) k_act_quantize_rows(const __nv_bfloat16* __restrict__ a,
                                                                      const __nv_bfloat16* __restrict__ b, int64_t rows,
                                                                      int nvec, __nv_bfloat16* __restrict__ act,
@@ -585,7 +585,6 @@ __global__ void __launch_bounds__(kActThreads, 1) k_act_quantize_rows(const __nv
                                                                      uint32_t* err, const uint4* __restrict__ lut_g) {
   using T = __nv_bfloat16;
   using Out = typename VecQ<T>::Out;
-  constexpr int CH = 4;
   constexpr int LUT_VECS = kLutEntries * (MODE == 0 ? 2 : 4) / 16;
   extern __shared__ uint4 lut_s[];
   for (int i = threadIdx.x; i < LUT_VECS; i += blockDim.x) lut_s[i] = __ldg(lut_g + i);
@@ -660,13 +659,13 @@ __global__ void k_act_elementwise(const __nv_bfloat16* __restrict__ a, const __n
   }
 }
 
-template <int MODE>
+template <int MODE, int CH>
 cudaError_t launch_act_rows(sb_handle h, const __nv_bfloat16* a, const __nv_bfloat16* b, int64_t rows, int nvec,
                             __nv_bfloat16* act, int8_t* q, float* state) {
   const size_t smem = static_cast<size_t>(kLutEntries) * (MODE == 0 ? 2 : 4);
   static bool attr = false;
   if (!attr) {
-    const cudaError_t e = cudaFuncSetAttribute(k_act_quantize_rows<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const cudaError_t e = cudaFuncSetAttribute(k_act_quantize_rows<MODE, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     attr = true;
@@ -676,8 +675,8 @@ cudaError_t launch_act_rows(sb_handle h, const __nv_bfloat16* a, const __nv_bflo
   const int64_t need = (rows + 31) / 32;
   const int64_t blocks = std::min<int64_t>(need, static_cast<int64_t>(h->num_sms));
   h->launches++;
-  k_act_quantize_rows<MODE><<<static_cast<unsigned>(blocks), kActThreads, smem, h->stream>>>(a, b, rows, nvec, act, q,
-                                                                                             state, h->d_err, lut);
+  k_act_quantize_rows<MODE, CH><<<static_cast<unsigned>(blocks), kActThreads, smem, h->stream>>>(a, b, rows, nvec, act,
+                                                                                                 q, state, h->d_err, lut);
   return cudaGetLastError();
 }
 
@@ -1673,8 +1672,15 @@ cudaError_t launch_act_quantize_rowwise(sb_handle h, int mode, const void* a, co
                       sb::aligned(act, 16) && sb::aligned(q, 8) && cols / 8 < (1 << 30);
   if (vec_ok) {
     const int nvec = static_cast<int>(cols / 8);
-    return mode == 0 ? launch_act_rows<0>(h, A, B, rows, nvec, O, q, state)
-                     : launch_act_rows<1>(h, A, B, rows, nvec, O, q, state);
+    const char* ce = getenv("SB_ACT_CH");  // measurement switch: vectors per lane per step
+    const int ch = ce ? atoi(ce) : 2;
+    if (mode == 0)
+      return ch == 4 ? launch_act_rows<0, 4>(h, A, B, rows, nvec, O, q, state)
+                     : ch == 1 ? launch_act_rows<0, 1>(h, A, B, rows, nvec, O, q, state)
+                               : launch_act_rows<0, 2>(h, A, B, rows, nvec, O, q, state);
+    return ch == 4 ? launch_act_rows<1, 4>(h, A, B, rows, nvec, O, q, state)
+                   : ch == 1 ? launch_act_rows<1, 1>(h, A, B, rows, nvec, O, q, state)
+                             : launch_act_rows<1, 2>(h, A, B, rows, nvec, O, q, state);
   }
   const unsigned grid = grid_for(rows * cols, 256 * 4, h->num_sms);
   h->launches++;
