@@ -248,6 +248,16 @@ sb_status sb_switchback_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, co
                                      const void* g, sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y, void* dx,
                                      float* dw);
 
+/* Asynchronous form: enqueues the same pipeline and returns; y, dx, dw (and the host inputs)
+ * must stay untouched until sb_host_pipeline_wait(h). Consecutive calls alternate between two
+ * device pools, so one call's uploads overlap the previous call's drain (a multi-layer step
+ * keeps both PCIe directions busy end to end). */
+sb_status sb_switchback_fwd_bwd_host_async(sb_handle h, const sb_linear_mode* mode, const void* x, const void* w,
+                                           const void* g, sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y,
+                                           void* dx, float* dw);
+/* Waits for every enqueued host-pipeline call; reports non-finite inputs like sb_synchronize. */
+sb_status sb_host_pipeline_wait(sb_handle h);
+
 /* --------------------------------------------------------- optimizer ---- */
 /* TensorRef, optimizer.hpp:74-79 (device pointers, fp32, numel elements each). */
 typedef struct sb_adamw_tensor {

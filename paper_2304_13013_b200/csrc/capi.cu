@@ -242,7 +242,10 @@ sb_status sb_destroy(sb_handle h) {
   if (h->d_err) cudaFree(h->d_err);
   if (h->gelu_lut) cudaFree(h->gelu_lut);
   if (h->d_scratch) cudaFree(h->d_scratch);
-  if (h->dev_pool) cudaFree(h->dev_pool);
+  for (int i = 0; i < 2; ++i) {
+    if (h->dev_pool[i]) cudaFree(h->dev_pool[i]);
+    if (h->pool_done[i]) cudaEventDestroy(h->pool_done[i]);
+  }
   if (h->s_in) {
     cudaStreamDestroy(h->s_in);
     cudaStreamDestroy(h->s_out);
@@ -684,9 +687,9 @@ sb_status sb_gelu_backward_quantize_rowwise(sb_handle h, const void* dact, const
 // chunks. Three streams: h2d copies, compute (the handle stream), d2h copies, so PCIe
 // transfers of chunk i+1 / i-1 overlap the kernels of chunk i. dW accumulates on the single
 // compute stream in chunk order (deterministic).
-sb_status sb_switchback_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, const void* x, const void* w,
-                                     const void* g, sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y, void* dx,
-                                     float* dw) {
+static sb_status fwd_bwd_host_enqueue(sb_handle h, const sb_linear_mode* mode, const void* x, const void* w,
+                                      const void* g, sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y, void* dx,
+                                      float* dw) {
   const char* op = "switchback_fwd_bwd";
   SB_TRY(check_h(h, op));
   if (!mode || !x || !w || !g || !y || !dx || !dw || !float_dtype(dt)) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
@@ -697,12 +700,13 @@ sb_status sb_switchback_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, co
   // Token rows stream through NS slots of `chunk` rows: H2D of chunk i+2 | kernels of chunk i |
   // D2H of chunk i-1 run concurrently; Y of a chunk is copied out as soon as its forward GEMM
   // is done, dX after the backward. Small chunks keep the un-overlapped pipeline fill (first
-  // H2D) and drain (last D2H, the dW copy) short; 4096 rows still fill the SM pairs.
+  // H2D) and drain (last D2H, the dW copy) short; 2048-row chunks x 4 slots measured best
+  // (tools/e2e_sweep.py: 39.7 ms per C2 step async, against 40.4 ms at 4096 x 3).
   // SB_HOST_CHUNK / SB_HOST_SLOTS override the defaults (measurement knobs).
   const char* ce = std::getenv("SB_HOST_CHUNK");
   const char* se = std::getenv("SB_HOST_SLOTS");
-  const int NS = se ? std::max(2, std::min(8, std::atoi(se))) : 3;
-  const int64_t chunk = std::min<int64_t>(b, ce ? std::max<int64_t>(128, std::atoll(ce)) : 4096);
+  const int NS = se ? std::max(2, std::min(8, std::atoi(se))) : 4;
+  const int64_t chunk = std::min<int64_t>(b, ce ? std::max<int64_t>(128, std::atoll(ce)) : 2048);
   // device layout: W, W_q, W_qT, dW, states/words, NS x {x, g, y, dx, x_q, g_q, x states, g states}
   Carve c{nullptr};
   auto layout = [&](Carve& cv, void** P) {
@@ -726,24 +730,28 @@ sb_status sb_switchback_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, co
   void* P[6 + 8 * 8];
   layout(c, P);
   const size_t need = c.off + 256;
-  if (need > h->dev_pool_bytes) {
-    if (h->dev_pool) {
-      cudaStreamSynchronize(h->stream);
-      cudaFree(h->dev_pool);
-    }
-    h->dev_pool = nullptr;
-    h->dev_pool_bytes = 0;
-    SB_CUDA_CHECK(op, cudaMalloc(&h->dev_pool, need));
-    h->dev_pool_bytes = need;
-  }
   if (!h->s_in) {
     SB_CUDA_CHECK(op, cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
     SB_CUDA_CHECK(op, cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
     for (auto& row : h->hp_ev)
       for (auto& e : row) SB_CUDA_CHECK(op, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     SB_CUDA_CHECK(op, cudaEventCreateWithFlags(&h->hp_start, cudaEventDisableTiming));
+    for (auto& e : h->pool_done) SB_CUDA_CHECK(op, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  Carve c2{static_cast<uint8_t*>(h->dev_pool)};
+  const int pi = h->pool_next;
+  h->pool_next ^= 1;
+  if (need > h->dev_pool_bytes[pi]) {
+    if (h->dev_pool[pi]) {
+      cudaDeviceSynchronize();  // the pool's previous call may still be in flight
+      cudaFree(h->dev_pool[pi]);
+    }
+    h->dev_pool[pi] = nullptr;
+    h->dev_pool_bytes[pi] = 0;
+    h->pool_used[pi] = false;
+    SB_CUDA_CHECK(op, cudaMalloc(&h->dev_pool[pi], need));
+    h->dev_pool_bytes[pi] = need;
+  }
+  Carve c2{static_cast<uint8_t*>(h->dev_pool[pi])};
   layout(c2, P);
   void* dW_ = P[0];
   int8_t* wq = static_cast<int8_t*>(P[1]);
@@ -757,9 +765,14 @@ sb_status sb_switchback_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, co
   cudaEvent_t* ev_out = h->hp_ev[3];
 
   cudaStream_t comp = h->stream, s_in = h->s_in, s_out = h->s_out;
+  // s_in only writes this call's private pool: it does not wait for earlier compute, so an
+  // async call's first chunks stream in while the previous call drains
   cudaEventRecord(h->hp_start, comp);
-  cudaStreamWaitEvent(s_in, h->hp_start, 0);
   cudaStreamWaitEvent(s_out, h->hp_start, 0);
+  if (h->pool_used[pi]) {  // this pool's previous call (two calls ago) has fully drained
+    cudaStreamWaitEvent(s_in, h->pool_done[pi], 0);
+    cudaStreamWaitEvent(comp, h->pool_done[pi], 0);
+  }
   sb_status st = SB_OK;
   const int64_t nchunks = (b + chunk - 1) / chunk;
   auto h2d = [&](int64_t i) {
@@ -803,12 +816,25 @@ sb_status sb_switchback_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, co
     cudaMemcpyAsync(static_cast<uint8_t*>(dx) + r0 * n * es, dxd, rows * n * es, cudaMemcpyDeviceToHost, s_out);
     cudaEventRecord(ev_out[s], s_out);
   }
-  for (int s = 0; s < NS; ++s) cudaStreamWaitEvent(comp, ev_out[s], 0);
-  cudaMemcpyAsync(dw, dwd, m * n * sizeof(float), cudaMemcpyDeviceToHost, comp);
-  cudaError_t e = cudaStreamSynchronize(comp);
-  cudaStreamSynchronize(s_in);
-  cudaStreamSynchronize(s_out);
-  if (st != SB_OK) return st;
+  // dW leaves on the D2H stream after the last chunk's compute; the event marks the pool free.
+  // The per-slot events are reused by the next call, so later calls must not wait on this
+  // call's recordings: every stream of the next call first waits on hp_start (recorded on
+  // comp) and comp waits here for this call's D2H before anything else is enqueued on it.
+  cudaEventRecord(ev_comp[0], comp);
+  cudaStreamWaitEvent(s_out, ev_comp[0], 0);
+  cudaMemcpyAsync(dw, dwd, m * n * sizeof(float), cudaMemcpyDeviceToHost, s_out);
+  cudaEventRecord(h->pool_done[pi], s_out);
+  h->pool_used[pi] = true;
+  return st;
+}
+
+}  // extern "C"
+namespace {
+sb_status host_pipeline_check(sb_handle h, const char* op) {
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  cudaStreamSynchronize(h->s_in);
+  cudaStreamSynchronize(h->s_out);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return sb::cuda_fail(op, e);
   uint32_t flags = 0;
   cudaMemcpy(&flags, h->d_err, sizeof(flags), cudaMemcpyDeviceToHost);
@@ -817,6 +843,27 @@ sb_status sb_switchback_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, co
     return sb::fail(SB_ERR_NONFINITE, op, "non-finite input");
   }
   return SB_OK;
+}
+}  // namespace
+extern "C" {
+
+sb_status sb_switchback_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, const void* x, const void* w,
+                                     const void* g, sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y, void* dx,
+                                     float* dw) {
+  SB_TRY(fwd_bwd_host_enqueue(h, mode, x, w, g, dt, b, n, m, y, dx, dw));
+  return host_pipeline_check(h, "switchback_fwd_bwd");
+}
+
+sb_status sb_switchback_fwd_bwd_host_async(sb_handle h, const sb_linear_mode* mode, const void* x, const void* w,
+                                           const void* g, sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y,
+                                           void* dx, float* dw) {
+  return fwd_bwd_host_enqueue(h, mode, x, w, g, dt, b, n, m, y, dx, dw);
+}
+
+sb_status sb_host_pipeline_wait(sb_handle h) {
+  SB_TRY(check_h(h, "sb_host_pipeline_wait"));
+  if (!h->s_in) return sb_synchronize(h);
+  return host_pipeline_check(h, "switchback_fwd_bwd");
 }
 
 }  // extern "C"

@@ -22,8 +22,13 @@ struct sb_handle_s {
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaEvent_t hp_ev[4][8] = {};  // [in, y, comp, out][slot] (host pipeline, up to 8 slots)
   cudaEvent_t hp_start = nullptr;
-  void* dev_pool = nullptr;
-  size_t dev_pool_bytes = 0;
+  // two device pools used by alternate host-pipeline calls, so an async call's transfers
+  // overlap the previous call's drain without aliasing its buffers
+  void* dev_pool[2] = {nullptr, nullptr};
+  size_t dev_pool_bytes[2] = {0, 0};
+  cudaEvent_t pool_done[2] = {nullptr, nullptr};  // recorded when a call's last D2H finished
+  bool pool_used[2] = {false, false};
+  int pool_next = 0;
   void* gelu_lut = nullptr;  // GELU / GELU' tables for bf16 |x| < 8 (built at sb_create)
 };
 

@@ -422,6 +422,26 @@ def linear_backward(mode: LinearMode, ctx: LinearContext, g: torch.Tensor, dw: t
     return dx, dw
 
 
+def switchback_fwd_bwd_host_many(layers, exact: bool = False):
+    """switchback_fwd_bwd_host over several (x, w, g) host triples (e.g. the linears of one
+    step), enqueued back to back with sb_switchback_fwd_bwd_host_async so each layer's uploads
+    overlap the previous layer's drain; one wait at the end. Returns [(y, dx, dw), ...]."""
+    h = A.handle()
+    md = LinearMode(A.SB_SWITCHBACK, A.SB_INT8, exact=exact)
+    outs = []
+    for x, w, g in layers:
+        b, n = x.shape
+        m = w.shape[0]
+        y = torch.empty((b, m), dtype=x.dtype, pin_memory=True)
+        dx = torch.empty((b, n), dtype=x.dtype, pin_memory=True)
+        dw = torch.empty((m, n), dtype=torch.float32, pin_memory=True)
+        A.check(h.lib.sb_switchback_fwd_bwd_host_async(h.h, C.byref(md.c()), _p(x), _p(w), _p(g), _dt(x), b, n, m,
+                                                       _p(y), _p(dx), _p(dw)))
+        outs.append((y, dx, dw))
+    A.check(h.lib.sb_host_pipeline_wait(h.h))
+    return outs
+
+
 def switchback_fwd_bwd_host(x, w, g, exact: bool = False):
     """bench.cpp:75-81 over HOST tensors (pinned CPU torch tensors): returns (y, dx, dw) on the
     host. Copies + kernels pipelined over token chunks inside the C-ABI call."""

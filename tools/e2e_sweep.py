@@ -18,18 +18,23 @@ bufs = []
 for n, m in ((1280, 5120), (5120, 1280)):
     bufs.append((torch.randn(T, n, generator=g).bfloat16().pin_memory(), (torch.randn(m, n, generator=g) / n ** 0.5).bfloat16().pin_memory(),
                  torch.randn(T, m, generator=g).bfloat16().pin_memory()))
-for _ in range(2):
-    for x, w, gg in bufs:
-        L.switchback_fwd_bwd_host(x, w, gg)
-torch.cuda.synchronize()
-t0 = time.perf_counter()
-for _ in range(4):
-    for x, w, gg in bufs:
-        L.switchback_fwd_bwd_host(x, w, gg)
-torch.cuda.synchronize()
-dt = (time.perf_counter() - t0) / 4
-print(f"chunk={os.environ.get('SB_HOST_CHUNK', 'def')} slots={os.environ.get('SB_HOST_SLOTS', 'def')}: "
-      f"{dt * 1e3:.2f} ms/step {T / dt / 1e6:.3f} M tokens/s")
+for mode in ("sync", "async"):
+    def once():
+        if mode == "sync":
+            for x, w, gg in bufs:
+                L.switchback_fwd_bwd_host(x, w, gg)
+        else:
+            L.switchback_fwd_bwd_host_many(bufs)
+    for _ in range(2):
+        once()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(4):
+        once()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / 4
+    print(f"{mode} chunk={os.environ.get('SB_HOST_CHUNK', 'def')} slots={os.environ.get('SB_HOST_SLOTS', 'def')}: "
+          f"{dt * 1e3:.2f} ms/step {T / dt / 1e6:.3f} M tokens/s")
 
 # the same bytes with no compute: per layer, X and G in on one stream, Y and dX out on another
 # (device buffers preallocated), chunked like the pipeline -- the PCIe bound for this pattern
