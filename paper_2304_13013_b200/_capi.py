@@ -11,7 +11,7 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libswitchback_b200.so")
+LIB_PATH = os.environ.get("SB_LIB_PATH") or os.path.join(PKG, "libswitchback_b200.so")  # override: A/B builds
 
 # enums (switchback_b200.h)
 SB_OK, SB_ERR_INVALID_ARGUMENT, SB_ERR_NONFINITE, SB_ERR_CUDA, SB_ERR_UNSUPPORTED = range(5)

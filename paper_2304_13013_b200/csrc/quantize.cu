@@ -527,14 +527,21 @@ __device__ __forceinline__ int lut_index(uint32_t bits16) {
   const uint32_t mag = bits16 & 0x7fffu;
   return mag < kLutHalf ? static_cast<int>((bits16 >> 15) * kLutHalf + mag) : -1;
 }
+// Forward: the full 65536-entry table (128 KB), indexed by the raw bf16 bits -- no range test,
+// inf / NaN included. Backward: fp32 factors only for |x| < 8 (a full fp32 table would not fit
+// in shared memory).
+constexpr int kFwdEntries = 65536;
 __global__ void k_build_gelu_lut(__nv_bfloat16* fwd, float* grad_factor) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kLutEntries; i += gridDim.x * blockDim.x) {
-    const uint32_t bits = i < static_cast<int>(kLutHalf) ? static_cast<uint32_t>(i) : 0x8000u + (i - kLutHalf);
-    const float x = __bfloat162float(__ushort_as_bfloat16(static_cast<unsigned short>(bits)));
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kFwdEntries; i += gridDim.x * blockDim.x) {
+    const float x = __bfloat162float(__ushort_as_bfloat16(static_cast<unsigned short>(i)));
     fwd[i] = __float2bfloat16_rn(gelu_f(x));
-    const float cdf = 0.5f * (1.0f + erff(x * 0.70710678118654752440f));
-    const float pdf = expf(-0.5f * x * x) * 0.39894228040143267794f;
-    grad_factor[i] = cdf + x * pdf;  // gelu_grad_f(dy, x) == dy * grad_factor (same ops, no fma)
+    if (i < kLutEntries) {
+      const uint32_t bits = i < static_cast<int>(kLutHalf) ? static_cast<uint32_t>(i) : 0x8000u + (i - kLutHalf);
+      const float xb = __bfloat162float(__ushort_as_bfloat16(static_cast<unsigned short>(bits)));
+      const float cdf = 0.5f * (1.0f + erff(xb * 0.70710678118654752440f));
+      const float pdf = expf(-0.5f * xb * xb) * 0.39894228040143267794f;
+      grad_factor[i] = cdf + xb * pdf;  // gelu_grad_f(dy, x) == dy * grad_factor (same ops, no fma)
+    }
   }
 }
 
@@ -552,10 +559,7 @@ __device__ __forceinline__ uint4 act_vec(const uint4& a, const uint4& b, const v
       const uint32_t xa = (wa[k] >> (16 * hf)) & 0xffffu;  // MODE 0: x; MODE 1: dy
       uint32_t o;
       if (MODE == 0) {
-        const int li = lut_index(xa);
-        o = li >= 0 ? static_cast<const unsigned short*>(lut)[li]
-                    : __bfloat16_as_ushort(__float2bfloat16_rn(
-                          gelu_f(__bfloat162float(__ushort_as_bfloat16(static_cast<unsigned short>(xa))))));
+        o = static_cast<const unsigned short*>(lut)[xa];
       } else {
         const uint32_t xb = (wb[k] >> (16 * hf)) & 0xffffu;  // x
         const float dy = __bfloat162float(__ushort_as_bfloat16(static_cast<unsigned short>(xa)));
@@ -585,7 +589,7 @@ __global__ void __launch_bounds__(kActThreads, 1) k_act_quantize_rows(const __nv
                                                                      uint32_t* err, const uint4* __restrict__ lut_g) {
   using T = __nv_bfloat16;
   using Out = typename VecQ<T>::Out;
-  constexpr int LUT_VECS = kLutEntries * (MODE == 0 ? 2 : 4) / 16;
+  constexpr int LUT_VECS = (MODE == 0 ? kFwdEntries * 2 : kLutEntries * 4) / 16;
   extern __shared__ uint4 lut_s[];
   for (int i = threadIdx.x; i < LUT_VECS; i += blockDim.x) lut_s[i] = __ldg(lut_g + i);
   __syncthreads();
@@ -662,7 +666,7 @@ __global__ void k_act_elementwise(const __nv_bfloat16* __restrict__ a, const __n
 template <int MODE, int CH>
 cudaError_t launch_act_rows(sb_handle h, const __nv_bfloat16* a, const __nv_bfloat16* b, int64_t rows, int nvec,
                             __nv_bfloat16* act, int8_t* q, float* state) {
-  const size_t smem = static_cast<size_t>(kLutEntries) * (MODE == 0 ? 2 : 4);
+  const size_t smem = MODE == 0 ? static_cast<size_t>(kFwdEntries) * 2 : static_cast<size_t>(kLutEntries) * 4;
   static bool attr = false;
   if (!attr) {
     const cudaError_t e = cudaFuncSetAttribute(k_act_quantize_rows<MODE, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -671,7 +675,7 @@ cudaError_t launch_act_rows(sb_handle h, const __nv_bfloat16* a, const __nv_bflo
     attr = true;
   }
   const uint4* lut = reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(h->gelu_lut) +
-                                                    (MODE == 0 ? 0 : static_cast<size_t>(kLutEntries) * 2));
+                                                    (MODE == 0 ? 0 : static_cast<size_t>(kFwdEntries) * 2));
   const int64_t need = (rows + 31) / 32;
   const int64_t blocks = std::min<int64_t>(need, static_cast<int64_t>(h->num_sms));
   h->launches++;
@@ -1649,10 +1653,10 @@ cudaError_t launch_add_bias(sb_handle h, void* y, sb_dtype dt, int64_t rows, int
 cudaError_t build_gelu_lut(sb_handle h) {
   if (h->gelu_lut) return cudaSuccess;
   void* p = nullptr;
-  cudaError_t e = cudaMalloc(&p, static_cast<size_t>(kLutEntries) * 6);
+  cudaError_t e = cudaMalloc(&p, static_cast<size_t>(kFwdEntries) * 2 + static_cast<size_t>(kLutEntries) * 4);
   if (e != cudaSuccess) return e;
   k_build_gelu_lut<<<64, 256>>>(static_cast<__nv_bfloat16*>(p),
-                               reinterpret_cast<float*>(static_cast<uint8_t*>(p) + static_cast<size_t>(kLutEntries) * 2));
+                               reinterpret_cast<float*>(static_cast<uint8_t*>(p) + static_cast<size_t>(kFwdEntries) * 2));
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     cudaFree(p);
