@@ -107,6 +107,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&tr, 8 * 2048);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  if (argc > 2) sms = atoi(argv[2]);  // CTAs launched (one per SM): per-SM vs aggregate limit
   cudaFuncSetAttribute(k_feed, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   struct Cfg { int stages, box_rows, boxes, mode, per_sm, wv; };
   const Cfg cfgs[] = {{8, 128, 1, 0, 1, 0}, {4, 128, 3, 0, 1, 0}};
