@@ -20,7 +20,9 @@
 
 namespace {
 
-constexpr int kThreads = 128;  // 128-thread blocks x 8 per SM: 6.44 ms vs 6.59 (256 x 4) / 6.80 (512 x 2) / 7.75 (64 x 16)
+// 128-thread blocks, 9 per SM (56 registers, a 24-byte spill): 6.27 ms per 1e9-param step vs
+// 6.44 (8 per SM, 64 regs), 6.59 (256 x 4), 6.80 (512 x 2), 7.0 (11-12 per SM: heavy spills)
+constexpr int kThreads = 128;
 constexpr int kPerThread = 16;
 constexpr int kChunk = kThreads * kPerThread;  // elements per block task
 constexpr int kMaxGroup = 256;                 // tensors per launch (kernel parameters <= 32 KB)
@@ -207,7 +209,7 @@ __device__ __forceinline__ void st_release(unsigned int* p, unsigned int v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads, 8) k_adamw_persistent(const __grid_constant__ Group grp, Coeffs c,
+__global__ void __launch_bounds__(kThreads, 9) k_adamw_persistent(const __grid_constant__ Group grp, Coeffs c,
                                                                const double* __restrict__ clip_ptr,
                                                                double* __restrict__ partials,
                                                                unsigned int* __restrict__ sync,
