@@ -22,6 +22,11 @@ def init_from_env(backend: str | None = None) -> tuple[int, int, int]:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # Test hooks for exercising the multi-rank path on a one-GPU box: SB_DP_SHARE_GPU=1 maps
+    # every rank to cuda:0, SB_DP_BACKEND=gloo replaces NCCL (which refuses two ranks on one GPU).
+    if os.environ.get("SB_DP_SHARE_GPU") == "1":
+        local = 0
+    backend = backend or os.environ.get("SB_DP_BACKEND") or None
     if world > 1 and not dist.is_initialized():
         if backend is None:
             backend = "nccl" if torch.cuda.is_available() else "gloo"
