@@ -517,19 +517,17 @@ __device__ __forceinline__ float gelu_grad_f(float dy, float x) {
   const float pdf = expf(-0.5f * x * x) * 0.39894228040143267794f;
   return dy * (cdf + x * pdf);
 }
-// bf16 inputs take only 65536 values, so the GELU (and GELU') of every |x| < 8 is tabulated
-// once per handle with the formulas above (build_gelu_lut) and read from shared memory:
-// a lookup instead of ~40 instructions of erf/exp per element, bit-identical to the formula
-// (the table IS the formula's output). |x| >= 8, inf and NaN take the formula directly.
-constexpr uint32_t kLutHalf = 0x4100u;  // bf16 bits of 8.0: |x| < 8 <=> (bits & 0x7fff) < kLutHalf
+// bf16 inputs take only 65536 values, so GELU and GELU' are tabulated once per handle with
+// the formulas above (build_gelu_lut) and read from shared memory: a lookup instead of ~40
+// instructions of erf/exp per element, bit-identical to the formula (the table IS the
+// formula's output; tests/test_nn_gpu.py checks every bf16 input).
+//   forward: all 65536 bf16 results (128 KB), indexed by the raw bits -- no range test.
+//   backward: the fp32 factor cdf + x*pdf for |x| < 16 (131 KB; a full fp32 table would not
+//   fit). Beyond it the formula saturates exactly in fp32: erf(+-x/sqrt2) = +-1 and
+//   exp(-x^2/2) underflows to 0, so the factor is 1 (x >= 16), +0 (x <= -16), NaN (inf/NaN:
+//   inf * 0): a select, no divergent branch.
+constexpr uint32_t kLutHalf = 0x4180u;  // bf16 bits of 16.0: |x| < 16 <=> (bits & 0x7fff) < kLutHalf
 constexpr int kLutEntries = 2 * kLutHalf;
-__device__ __forceinline__ int lut_index(uint32_t bits16) {
-  const uint32_t mag = bits16 & 0x7fffu;
-  return mag < kLutHalf ? static_cast<int>((bits16 >> 15) * kLutHalf + mag) : -1;
-}
-// Forward: the full 65536-entry table (128 KB), indexed by the raw bf16 bits -- no range test,
-// inf / NaN included. Backward: fp32 factors only for |x| < 8 (a full fp32 table would not fit
-// in shared memory).
 constexpr int kFwdEntries = 65536;
 __global__ void k_build_gelu_lut(__nv_bfloat16* fwd, float* grad_factor) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kFwdEntries; i += gridDim.x * blockDim.x) {
@@ -543,6 +541,14 @@ __global__ void k_build_gelu_lut(__nv_bfloat16* fwd, float* grad_factor) {
       grad_factor[i] = cdf + xb * pdf;  // gelu_grad_f(dy, x) == dy * grad_factor (same ops, no fma)
     }
   }
+}
+__device__ __forceinline__ float gelu_grad_factor(uint32_t xb, const float* lut) {
+  const uint32_t mag = xb & 0x7fffu;
+  const uint32_t neg = xb >> 15;
+  const bool in = mag < kLutHalf;
+  const float t = lut[in ? neg * kLutHalf + mag : 0u];
+  const float sat = mag >= 0x7f80u ? __int_as_float(0x7fffffff) : (neg ? 0.0f : 1.0f);
+  return in ? t : sat;
 }
 
 template <int MODE>
@@ -563,9 +569,7 @@ __device__ __forceinline__ uint4 act_vec(const uint4& a, const uint4& b, const v
       } else {
         const uint32_t xb = (wb[k] >> (16 * hf)) & 0xffffu;  // x
         const float dy = __bfloat162float(__ushort_as_bfloat16(static_cast<unsigned short>(xa)));
-        const int li = lut_index(xb);
-        const float gv = li >= 0 ? dy * static_cast<const float*>(lut)[li]
-                                 : gelu_grad_f(dy, __bfloat162float(__ushort_as_bfloat16(static_cast<unsigned short>(xb))));
+        const float gv = dy * gelu_grad_factor(xb, static_cast<const float*>(lut));
         o = __bfloat16_as_ushort(__float2bfloat16_rn(gv));
       }
       out |= o << (16 * hf);
