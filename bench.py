@@ -547,7 +547,7 @@ def run_vit_block(args):
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     B, S, D, H = 256, 257, 1280, 16
-    fused = not args.no_overlap  # --no-overlap also turns the MLP producer fusion off (A/B)
+    fused = not args.no_overlap  # --no-overlap also turns the LayerNorm / GELU producer fusions off (A/B)
     T = B * S
 
     class Block(torch.nn.Module):
@@ -557,19 +557,24 @@ def run_vit_block(args):
                 (lambda i, o: torch.nn.Linear(i, o, device=dev))
             self.ln1 = torch.nn.LayerNorm(D, device=dev)
             self.ln2 = torch.nn.LayerNorm(D, device=dev)
-            self.qkv, self.out = mk(D, 3 * D), mk(D, D)
-            if sb and fused:  # GELU fused into the quantization of fc2's input / fc1's gradient
-                self.mlp = SwitchBackMLP(D, 4 * D, device=dev)
+            self.fused = sb and fused
+            self.out = mk(D, D)
+            if self.fused:
+                # producer fusions: LayerNorm fused into the qkv / fc1 input quantization, GELU
+                # into fc2's input quantization and fc1's gradient quantization
+                self.qkv = SwitchBackLinear(D, 3 * D, device=dev, prenorm=True)
+                self.mlp = SwitchBackMLP(D, 4 * D, device=dev, prenorm=True)
             else:
+                self.qkv = mk(D, 3 * D)
                 fc1, fc2 = mk(D, 4 * D), mk(4 * D, D)
                 self.mlp = torch.nn.Sequential(fc1, torch.nn.GELU(), fc2)
 
         def forward(self, x):
-            h = self.ln1(x.float()).to(torch.bfloat16)
+            h = x if self.fused else self.ln1(x.float()).to(torch.bfloat16)
             q, k, v = self.qkv(h).view(B, S, 3, H, D // H).permute(2, 0, 3, 1, 4).unbind(0)
             a = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(B, S, D)
             x = x + self.out(a)
-            h = self.ln2(x.float()).to(torch.bfloat16)
+            h = x if self.fused else self.ln2(x.float()).to(torch.bfloat16)
             return x + self.mlp(h)
 
     gen = torch.Generator(device=dev).manual_seed(3)

@@ -230,6 +230,12 @@ sb_status sb_gelu_quantize_rowwise(sb_handle h, const void* pre, sb_dtype dt, in
 /* g = dact * gelu'(pre) as bf16 plus its row-wise int8 payload and states. */
 sb_status sb_gelu_backward_quantize_rowwise(sb_handle h, const void* dact, const void* pre, sb_dtype dt, int64_t rows,
                                             int64_t cols, void* g, int8_t* q, float* state);
+/* out = LayerNorm(x) (over each row of cols; fp32 gamma, beta; bf16 x and out) with its row-wise
+ * int8 payload and states, plus per-row mean and rstd (fp32) for the backward. Rows of up to
+ * 2048 columns (multiple of 8); SB_ERR_UNSUPPORTED otherwise. */
+sb_status sb_layernorm_quantize_rowwise(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols,
+                                        const float* gamma, const float* beta, float eps, void* out, int8_t* q,
+                                        float* state, float* mean, float* rstd);
 /* sb_linear_forward_bias with X already quantized row-wise by its producer (x_q b x n, x_state b):
  * int8 SwitchBack / SwitchBackM / SwitchBackQ, non-exact. x stays referenced by ctx (dW). */
 sb_status sb_linear_forward_prequant(sb_handle h, const sb_linear_mode* mode, const void* x, const int8_t* x_q,

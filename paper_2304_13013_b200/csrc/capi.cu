@@ -682,6 +682,21 @@ sb_status sb_gelu_backward_quantize_rowwise(sb_handle h, const void* dact, const
   return SB_OK;
 }
 
+sb_status sb_layernorm_quantize_rowwise(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols,
+                                        const float* gamma, const float* beta, float eps, void* out, int8_t* q,
+                                        float* state, float* mean, float* rstd) {
+  const char* op = "layernorm_quantize_rowwise";
+  SB_TRY(check_h(h, op));
+  if (!x || !gamma || !beta || !out || !q || !state || !mean || !rstd || dt != SB_BF16)
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument (bf16 only)");
+  if (rows <= 0 || cols <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty matrix");
+  const cudaError_t e = sb::launch_ln_quantize_rowwise(h, x, rows, cols, gamma, beta, eps, out, q, state, mean, rstd);
+  if (e == cudaErrorNotSupported)
+    return sb::fail(SB_ERR_UNSUPPORTED, op, "rows of <= 2048 columns, multiple of 8, 16-byte aligned");
+  SB_TRYC(op, e);
+  return SB_OK;
+}
+
 // ------------------------------------------------- host-buffer pipeline --
 // switchback_fwd_bwd over host memory: W is quantized once; token rows stream through in
 // chunks. Three streams: h2d copies, compute (the handle stream), d2h copies, so PCIe

@@ -688,6 +688,127 @@ cudaError_t launch_act_rows(sb_handle h, const __nv_bfloat16* a, const __nv_bflo
   return cudaGetLastError();
 }
 
+// ---- producer fusion: LayerNorm + row-wise quantize -----------------
+// A pre-norm block feeds LayerNorm(x) straight into a SwitchBack linear. One warp per row,
+// the row in registers: mean and variance (two passes over the registers, fp32), the affine
+// output rounded to bf16 and stored (the dW GEMM needs it), then the same register values
+// quantized row-wise; mean / rstd are written for the backward. Payload / states equal
+// quantize_rowwise(h) bit for bit.
+template <int VPL>
+__global__ void __launch_bounds__(256) k_ln_quantize_rows(const __nv_bfloat16* __restrict__ x, int64_t rows, int nvec,
+                                                          const float* __restrict__ gamma,
+                                                          const float* __restrict__ beta, float eps,
+                                                          __nv_bfloat16* __restrict__ h, int8_t* __restrict__ q,
+                                                          float* __restrict__ state, float* __restrict__ mean_out,
+                                                          float* __restrict__ rstd_out, uint32_t* err) {
+  using T = __nv_bfloat16;
+  using Out = typename VecQ<T>::Out;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const float inv_n = 1.0f / static_cast<float>(nvec * 8);
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+       row += warps) {
+    const int64_t off = row * static_cast<int64_t>(nvec);
+    const uint4* xr = reinterpret_cast<const uint4*>(x) + off;
+    uint4 v[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int i = j * 32 + lane;
+      v[j] = i < nvec ? ld_stream(xr + i) : make_uint4(0, 0, 0, 0);
+    }
+    float sum = 0.0f;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&v[j]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(p2[k]);
+        sum += f.x + f.y;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float mean = sum * inv_n;
+    float sq = 0.0f;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      if (j * 32 + lane >= nvec) continue;
+      const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&v[j]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(p2[k]);
+        const float a = f.x - mean, b = f.y - mean;
+        sq += a * a + b * b;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    const float rstd = rsqrtf(sq * inv_n + eps);
+    uint4* hr = reinterpret_cast<uint4*>(h) + off;
+    uint32_t amax = 0;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int i = j * 32 + lane;
+      if (i >= nvec) continue;
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma) + 2 * i);
+      const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma) + 2 * i + 1);
+      const float4 b0 = __ldg(reinterpret_cast<const float4*>(beta) + 2 * i);
+      const float4 b1 = __ldg(reinterpret_cast<const float4*>(beta) + 2 * i + 1);
+      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&v[j]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(p2[k]);
+        p2[k] = __float22bfloat162_rn(make_float2((f.x - mean) * rstd * gg[2 * k] + bb[2 * k],
+                                                  (f.y - mean) * rstd * gg[2 * k + 1] + bb[2 * k + 1]));
+      }
+      hr[i] = v[j];
+      amax = max(amax, vec_absmax_bits<T>(v[j]));
+    }
+    amax = __reduce_max_sync(0xffffffffu, amax);
+    if (lane == 0) {
+      mean_out[row] = mean;
+      rstd_out[row] = rstd;
+    }
+    if (amax >= kNonFiniteBits) {
+      if (lane == 0) {
+        raise_nonfinite(err);
+        state[row] = __uint_as_float(amax);
+      }
+      continue;
+    }
+    const float st = state_from_bits(amax);
+    if (lane == 0) state[row] = st;
+    const Scale sc = make_scale(st);
+    const bool plain = sc.pre == 1.0f;
+    Out* qr = reinterpret_cast<Out*>(q + off * 8);
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      if (j * 32 >= nvec) break;  // warp-uniform (qvec votes across the warp)
+      const int i = j * 32 + lane;
+      const Out o = qvec<T>(v[j], sc, plain);
+      if (i < nvec) qr[i] = o;
+    }
+  }
+}
+
+template <int VPL>
+void launch_ln_rows(sb_handle h, const __nv_bfloat16* x, int64_t rows, int nvec, const float* gamma, const float* beta,
+                    float eps, __nv_bfloat16* out, int8_t* q, float* state, float* mean, float* rstd) {
+  static int blocks_per_sm = 0;
+  if (blocks_per_sm == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_ln_quantize_rows<VPL>, 256, 0) != cudaSuccess ||
+        blocks_per_sm < 1)
+      blocks_per_sm = 1;
+  }
+  const int64_t need = (rows + 7) / 8;
+  const int64_t blocks = std::min<int64_t>(need, static_cast<int64_t>(h->num_sms) * blocks_per_sm);
+  h->launches++;
+  k_ln_quantize_rows<VPL><<<static_cast<unsigned>(blocks), 256, 0, h->stream>>>(x, rows, nvec, gamma, beta, eps, out, q,
+                                                                                state, mean, rstd, h->d_err);
+}
+
 // SB_QUANT_KERNEL=tma selects the smem-ring kernel (A/B measurements); default: registers.
 bool prefer_tma_ring() {
   static int v = -1;
@@ -1651,6 +1772,30 @@ cudaError_t launch_add_bias(sb_handle h, void* y, sb_dtype dt, int64_t rows, int
     k_add_bias<<<grid, 256, 0, h->stream>>>(static_cast<__nv_bfloat16*>(y), rows, cols, bias);
   else
     return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ln_quantize_rowwise(sb_handle h, const void* x, int64_t rows, int64_t cols, const float* gamma,
+                                       const float* beta, float eps, void* out, int8_t* q, float* state, float* mean,
+                                       float* rstd) {
+  using bf = __nv_bfloat16;
+  if (cols % 8 || !sb::aligned(x, 16) || !sb::aligned(out, 16) || !sb::aligned(q, 8) || !sb::aligned(gamma, 16) ||
+      !sb::aligned(beta, 16))
+    return cudaErrorNotSupported;
+  const int nvec = static_cast<int>(cols / 8);
+  const bf* X = static_cast<const bf*>(x);
+  bf* O = static_cast<bf*>(out);
+  switch ((nvec + 31) / 32) {
+    case 1: launch_ln_rows<1>(h, X, rows, nvec, gamma, beta, eps, O, q, state, mean, rstd); break;
+    case 2: launch_ln_rows<2>(h, X, rows, nvec, gamma, beta, eps, O, q, state, mean, rstd); break;
+    case 3: launch_ln_rows<3>(h, X, rows, nvec, gamma, beta, eps, O, q, state, mean, rstd); break;
+    case 4: launch_ln_rows<4>(h, X, rows, nvec, gamma, beta, eps, O, q, state, mean, rstd); break;
+    case 5: launch_ln_rows<5>(h, X, rows, nvec, gamma, beta, eps, O, q, state, mean, rstd); break;
+    case 6: launch_ln_rows<6>(h, X, rows, nvec, gamma, beta, eps, O, q, state, mean, rstd); break;
+    case 7:
+    case 8: launch_ln_rows<8>(h, X, rows, nvec, gamma, beta, eps, O, q, state, mean, rstd); break;
+    default: return cudaErrorNotSupported;  // rows longer than 2048: not fused
+  }
   return cudaGetLastError();
 }
 

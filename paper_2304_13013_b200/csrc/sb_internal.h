@@ -125,6 +125,11 @@ cudaError_t launch_dequantize_fp8(sb_handle h, const uint8_t* q, int64_t rows, i
                                   const float* state, int axis, void* y, sb_dtype ydt, int64_t ldy);
 cudaError_t launch_convert(sb_handle h, const void* x, sb_dtype xdt, void* y, sb_dtype ydt, int64_t n);
 cudaError_t build_gelu_lut(sb_handle h);
+// Fused LayerNorm (bf16 in, fp32 gamma/beta) + row-wise quantize of its bf16 output;
+// cudaErrorNotSupported for rows longer than 2048 or unaligned operands.
+cudaError_t launch_ln_quantize_rowwise(sb_handle h, const void* x, int64_t rows, int64_t cols, const float* gamma,
+                                       const float* beta, float eps, void* out, int8_t* q, float* state, float* mean,
+                                       float* rstd);
 // Fused activation + row-wise quantize (bf16, contiguous rows): mode 0 act = gelu(a),
 // mode 1 act = a * gelu'(b); writes act and the int8 payload / states of act.
 cudaError_t launch_act_quantize_rowwise(sb_handle h, int mode, const void* a, const void* b, int64_t rows, int64_t cols,

@@ -137,6 +137,26 @@ def gelu_backward_quantize_rowwise(dact: torch.Tensor, pre: torch.Tensor,
     return g, QuantizedMatrix(q, st, ROW)
 
 
+def layernorm_quantize_rowwise(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps: float = 1e-5,
+                               check: bool = True):
+    """Producer fusion: out = LayerNorm(x) (bf16, fp32 affine) and quantize_rowwise(out) from
+    one read of x; returns (out, QuantizedMatrix, mean, rstd) (mean / rstd fp32 per row)."""
+    _need_cuda(x, gamma, beta)
+    x = x.contiguous()
+    r, c = x.shape
+    gamma, beta = gamma.float().contiguous(), beta.float().contiguous()
+    out = torch.empty_like(x)
+    q = torch.empty((r, c), dtype=torch.int8, device=x.device)
+    st = torch.empty(r, dtype=torch.float32, device=x.device)
+    mean = torch.empty(r, dtype=torch.float32, device=x.device)
+    rstd = torch.empty(r, dtype=torch.float32, device=x.device)
+    h = A.handle(x.device.index)
+    A.check(h.lib.sb_layernorm_quantize_rowwise(h.h, _p(x), _dt(x), r, c, _p(gamma), _p(beta), C.c_float(eps),
+                                                _p(out), _p(q), _p(st), _p(mean), _p(rstd)))
+    _check_nonfinite(h, check)
+    return out, QuantizedMatrix(q, st, ROW), mean, rstd
+
+
 def quantize_columnwise(x: torch.Tensor, check: bool = True, transposed: bool = False) -> QuantizedMatrix:
     """quantize.cpp:135-137. transposed=True returns quantize_rowwise(x^T) (linear.cpp:228-229)."""
     _need_cuda(x)

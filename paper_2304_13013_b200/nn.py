@@ -50,9 +50,11 @@ class SwitchBackLinear(torch.nn.Module):
     gradient (arXiv 2304.13013), on the B200 kernels of this package."""
 
     def __init__(self, in_features: int, out_features: int, bias: bool = True, variant: str = "switchback",
-                 fmt: str = "int8", device=None):
+                 fmt: str = "int8", device=None, prenorm: bool = False, eps: float = 1e-5):
         super().__init__()
         self.in_features, self.out_features = in_features, out_features
+        # prenorm: y = linear(LayerNorm(x)) with the norm fused into the input quantization
+        self.norm = torch.nn.LayerNorm(in_features, eps=eps, device=device or "cuda") if prenorm else None
         self.mode = L.LinearMode(_VARIANTS[variant], A.SB_INT8 if fmt == "int8" else A.SB_FP8)
         dev = torch.device(device) if device is not None else torch.device("cuda")
         # the reference's init (model.cpp:199-202): N(0, 1/n)
@@ -61,11 +63,56 @@ class SwitchBackLinear(torch.nn.Module):
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         shape = x.shape
-        y = _SwitchBackLinearFn.apply(x.reshape(-1, self.in_features), self.weight, self.bias, self.mode)
+        x2d = x.reshape(-1, self.in_features)
+        if self.norm is not None:
+            if x.dtype != torch.bfloat16:
+                raise TypeError("prenorm SwitchBackLinear runs in bf16")
+            y = _LNLinearFn.apply(x2d, self.norm.weight, self.norm.bias, self.norm.eps, self.weight, self.bias,
+                                  self.mode)
+        else:
+            y = _SwitchBackLinearFn.apply(x2d, self.weight, self.bias, self.mode)
         return y.reshape(*shape[:-1], self.out_features)
 
     def extra_repr(self) -> str:
         return f"in_features={self.in_features}, out_features={self.out_features}, bias={self.bias is not None}"
+
+
+def _ln_backward(dh, x2d, mean, rstd, ln_w, ln_b, needs):
+    """LayerNorm backward with the forward's own mean / rstd, in fp32 (as a pre-norm block that
+    normalises x.float())."""
+    dx, dg, db = torch.ops.aten.native_layer_norm_backward(
+        dh.float(), x2d.float(), [x2d.shape[1]], mean.view(-1, 1), rstd.view(-1, 1), ln_w.detach().float(),
+        ln_b.detach().float(), list(needs))
+    return (dx.to(x2d.dtype) if dx is not None else None), dg, db
+
+
+class _LNLinearFn(torch.autograd.Function):
+    """y = SwitchBackLinear(LayerNorm(x)) with the normalisation fused into the row-wise
+    quantization of the linear's input (sb_layernorm_quantize_rowwise + prequantized forward)."""
+
+    @staticmethod
+    def forward(ctx, x2d, ln_w, ln_b, eps: float, weight, bias, mode: L.LinearMode):
+        x2d = x2d.contiguous()
+        h, hq, mean, rstd = L.layernorm_quantize_rowwise(x2d, ln_w.detach(), ln_b.detach(), eps, check=False)
+        w = weight.detach().to(x2d.dtype).contiguous()
+        lctx = L.LinearContext()
+        y = L.linear_forward(mode, h, w, lctx, check=False, bias=bias.detach().float() if bias is not None else None,
+                             x_q=hq)
+        ctx.state = (x2d, mean, rstd, lctx, w)
+        ctx.ln = (ln_w, ln_b)
+        ctx.mode = mode
+        ctx.has_bias = bias is not None
+        return y
+
+    @staticmethod
+    def backward(ctx, g):
+        x2d, mean, rstd, lctx, _ = ctx.state
+        g = g.contiguous()
+        dh, dw = L.linear_backward(ctx.mode, lctx, g, check=False)
+        db = g.sum(0, dtype=torch.float32) if ctx.has_bias and ctx.needs_input_grad[5] else None
+        dx, dg, dbeta = _ln_backward(dh, x2d, mean, rstd, *ctx.ln, ctx.needs_input_grad[:3])
+        ctx.state = None
+        return dx, dg, dbeta, None, dw, db, None
 
 
 class _SwitchBackMLPFn(torch.autograd.Function):
@@ -75,31 +122,43 @@ class _SwitchBackMLPFn(torch.autograd.Function):
     activation is re-read just to be quantized."""
 
     @staticmethod
-    def forward(ctx, x2d, w1, b1, w2, b2, mode: L.LinearMode):
+    def forward(ctx, x2d, ln_w, ln_b, eps, w1, b1, w2, b2, mode: L.LinearMode):
         dt = x2d.dtype
+        x2d = x2d.contiguous()
         w1b, w2b = w1.detach().to(dt).contiguous(), w2.detach().to(dt).contiguous()
         c1, c2 = L.LinearContext(), L.LinearContext()
-        pre = L.linear_forward(mode, x2d.contiguous(), w1b, c1, check=False,
-                               bias=b1.detach().float() if b1 is not None else None)
+        ln_state = None
+        if ln_w is not None:  # pre-norm: LayerNorm fused with fc1's input quantization
+            h, hq, mean, rstd = L.layernorm_quantize_rowwise(x2d, ln_w.detach(), ln_b.detach(), eps, check=False)
+            ln_state = (x2d, mean, rstd)
+        else:
+            h, hq = x2d, None
+        pre = L.linear_forward(mode, h, w1b, c1, check=False, bias=b1.detach().float() if b1 is not None else None,
+                               x_q=hq)
         act, act_q = L.gelu_quantize_rowwise(pre, check=False)
         y = L.linear_forward(mode, act, w2b, c2, check=False, bias=b2.detach().float() if b2 is not None else None,
                              x_q=act_q)
-        ctx.state = (c1, c2, pre, w1b, w2b)
+        ctx.state = (c1, c2, pre, w1b, w2b, h, hq, ln_state)
+        ctx.ln = (ln_w, ln_b)
         ctx.mode = mode
         ctx.bias = (b1 is not None, b2 is not None)
         return y
 
     @staticmethod
     def backward(ctx, gy):
-        c1, c2, pre, _, _ = ctx.state
+        c1, c2, pre, _, _, _, _, ln_state = ctx.state
         gy = gy.contiguous()
         dact, dw2 = L.linear_backward(ctx.mode, c2, gy, check=False)
         g1, g1_q = L.gelu_backward_quantize_rowwise(dact, pre, check=False)
         dx, dw1 = L.linear_backward(ctx.mode, c1, g1, check=False, g_q=g1_q)
-        db1 = g1.sum(0, dtype=torch.float32) if ctx.bias[0] and ctx.needs_input_grad[2] else None
-        db2 = gy.sum(0, dtype=torch.float32) if ctx.bias[1] and ctx.needs_input_grad[4] else None
+        db1 = g1.sum(0, dtype=torch.float32) if ctx.bias[0] and ctx.needs_input_grad[5] else None
+        db2 = gy.sum(0, dtype=torch.float32) if ctx.bias[1] and ctx.needs_input_grad[7] else None
+        dg = dbeta = None
+        if ln_state is not None:
+            x2d, mean, rstd = ln_state
+            dx, dg, dbeta = _ln_backward(dx, x2d, mean, rstd, *ctx.ln, ctx.needs_input_grad[:3])
         ctx.state = None
-        return dx, dw1, db1, dw2, db2, None
+        return dx, dg, dbeta, None, dw1, db1, dw2, db2, None
 
 
 class SwitchBackMLP(torch.nn.Module):
@@ -107,9 +166,11 @@ class SwitchBackMLP(torch.nn.Module):
     the quantization of its consumer (forward) and producer-gradient (backward). bf16 inputs."""
 
     def __init__(self, in_features: int, hidden_features: int, out_features: int | None = None, bias: bool = True,
-                 variant: str = "switchback", device=None):
+                 variant: str = "switchback", device=None, prenorm: bool = False, eps: float = 1e-5):
         super().__init__()
         out_features = out_features or in_features
+        # prenorm: LayerNorm fused into fc1's input quantization (sb_layernorm_quantize_rowwise)
+        self.norm = torch.nn.LayerNorm(in_features, eps=eps, device=device or "cuda") if prenorm else None
         self.fc1 = SwitchBackLinear(in_features, hidden_features, bias=bias, variant=variant, device=device)
         self.fc2 = SwitchBackLinear(hidden_features, out_features, bias=bias, variant=variant, device=device)
         if variant not in ("switchback", "switchback_m", "switchback_q"):
@@ -119,6 +180,8 @@ class SwitchBackMLP(torch.nn.Module):
         if x.dtype != torch.bfloat16:
             raise TypeError("SwitchBackMLP runs in bf16")
         shape = x.shape
-        y = _SwitchBackMLPFn.apply(x.reshape(-1, self.fc1.in_features), self.fc1.weight, self.fc1.bias,
-                                   self.fc2.weight, self.fc2.bias, self.fc1.mode)
+        n = self.norm
+        y = _SwitchBackMLPFn.apply(x.reshape(-1, self.fc1.in_features), n.weight if n is not None else None,
+                                   n.bias if n is not None else None, n.eps if n is not None else 0.0,
+                                   self.fc1.weight, self.fc1.bias, self.fc2.weight, self.fc2.bias, self.fc1.mode)
         return y.reshape(*shape[:-1], self.fc2.out_features)

@@ -149,3 +149,47 @@ def test_gelu_table_equals_formula_for_every_bf16():
     assert torch.equal(g_vec.view(-1).view(torch.int16), g_sc.view(-1).view(torch.int16))
     with pytest.raises(L.InvalidArgument):  # the inf / NaN inputs latched the error word: consume it
         L.check_error()
+
+
+@pytest.mark.parametrize("rows,cols", [(4000, 1280), (33, 256), (7, 2048)])
+def test_layernorm_quantize_fused(rows, cols):
+    """LayerNorm + row-wise quantize in one kernel: the output is torch's LayerNorm within bf16
+    rounding, and the payload / states are exactly quantize_rowwise(out)."""
+    torch.manual_seed(rows)
+    x = (torch.randn(rows, cols, device="cuda") * 3 + 0.5).bfloat16()
+    g = torch.randn(cols, device="cuda") * 0.5 + 1
+    b = torch.randn(cols, device="cuda") * 0.1
+    out, q, mean, rstd = L.layernorm_quantize_rowwise(x, g, b, 1e-5)
+    ref = torch.nn.functional.layer_norm(x.float(), (cols,), g, b, 1e-5)
+    assert ((out.float() - ref).abs() <= ref.abs() * 2 ** -7 + 2e-3).all()
+    q2 = L.quantize_rowwise(out)
+    assert torch.equal(q.payload, q2.payload) and torch.equal(q.state, q2.state)
+    assert torch.allclose(mean, x.float().mean(1), rtol=1e-5, atol=1e-5)
+
+
+def test_prenorm_modules_match_fp32():
+    from paper_2304_13013_b200.nn import SwitchBackLinear, SwitchBackMLP
+
+    torch.manual_seed(9)
+    F = torch.nn.functional
+    for mod in (SwitchBackLinear(256, 384, prenorm=True), SwitchBackMLP(256, 512, prenorm=True)):
+        with torch.no_grad():
+            mod.norm.weight.normal_(1.0, 0.2)
+            mod.norm.bias.normal_(0.0, 0.1)
+        x = torch.randn(2, 300, 256, device="cuda").bfloat16().requires_grad_(True)
+        y = mod(x)
+        g = torch.randn_like(y)
+        y.backward(g)
+        xr = x.detach().float().requires_grad_(True)
+        params = {n: p.detach().clone().requires_grad_(True) for n, p in mod.named_parameters()}
+        h = F.layer_norm(xr, (256,), params["norm.weight"], params["norm.bias"], mod.norm.eps)
+        if isinstance(mod, SwitchBackLinear):
+            yr = F.linear(h, params["weight"], params["bias"])
+        else:
+            yr = F.linear(F.gelu(F.linear(h, params["fc1.weight"], params["fc1.bias"])), params["fc2.weight"],
+                          params["fc2.bias"])
+        yr.backward(g.float())
+        assert rel(y, yr) < 3e-2  # int8 noise of one or two quantized GEMMs on top of bf16 LN rounding
+        assert rel(x.grad, xr.grad) < 3e-2
+        for n, p in mod.named_parameters():
+            assert rel(p.grad, params[n].grad) < 3e-2, n
