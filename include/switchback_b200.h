@@ -236,6 +236,13 @@ sb_status sb_gelu_backward_quantize_rowwise(sb_handle h, const void* dact, const
 sb_status sb_layernorm_quantize_rowwise(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols,
                                         const float* gamma, const float* beta, float eps, void* out, int8_t* q,
                                         float* state, float* mean, float* rstd);
+/* LayerNorm backward for the fused pre-norm path: dx (bf16), dgamma, dbeta (fp32, may be NULL)
+ * from dh, x (bf16) and the forward's mean / rstd; deterministic (fixed-order column sums).
+ * Rows of up to 1280 columns; workspace from sb_layernorm_backward_workspace_size. */
+sb_status sb_layernorm_backward_workspace_size(sb_handle h, int64_t cols, size_t* bytes);
+sb_status sb_layernorm_backward(sb_handle h, const void* dh, const void* x, sb_dtype dt, int64_t rows, int64_t cols,
+                                const float* mean, const float* rstd, const float* gamma, void* dx, float* dgamma,
+                                float* dbeta, void* workspace, size_t workspace_bytes);
 /* sb_linear_forward_bias with X already quantized row-wise by its producer (x_q b x n, x_state b):
  * int8 SwitchBack / SwitchBackM / SwitchBackQ, non-exact. x stays referenced by ctx (dW). */
 sb_status sb_linear_forward_prequant(sb_handle h, const sb_linear_mode* mode, const void* x, const int8_t* x_q,

@@ -31,7 +31,8 @@ EXPORTS = [
     "sb_quantize_tensorwise", "sb_dequantize", "sb_quantize_fp8", "sb_dequantize_fp8", "sb_gemm_i8",
     "sb_matmul_f32", "sb_wgrad", "sb_gemm_fp8", "sb_linear_workspace_size", "sb_linear_forward", "sb_linear_forward_bias",
     "sb_linear_forward_prequant", "sb_linear_backward_prequant", "sb_gelu_quantize_rowwise",
-    "sb_gelu_backward_quantize_rowwise", "sb_layernorm_quantize_rowwise",
+    "sb_gelu_backward_quantize_rowwise", "sb_layernorm_quantize_rowwise", "sb_layernorm_backward_workspace_size",
+    "sb_layernorm_backward",
     "sb_linear_backward", "sb_switchback_fwd_bwd_host", "sb_switchback_fwd_bwd_host_async",
     "sb_host_pipeline_wait", "sb_stableadamw_workspace_size", "sb_stableadamw_step",
     "sb_device_alloc", "sb_device_free", "sb_copy_to_device", "sb_copy_to_host", "sb_check_finite", "sb_fp8_cast",
@@ -124,6 +125,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             "sb_gelu_quantize_rowwise": ([v, v, i32, i64, i64, v, v, v], i32),
             "sb_gelu_backward_quantize_rowwise": ([v, v, v, i32, i64, i64, v, v, v], i32),
             "sb_layernorm_quantize_rowwise": ([v, v, i32, i64, i64, v, v, C.c_float, v, v, v, v, v], i32),
+            "sb_layernorm_backward_workspace_size": ([v, i64, C.POINTER(sz)], i32),
+            "sb_layernorm_backward": ([v, v, v, i32, i64, i64, v, v, v, v, v, v, v, sz], i32),
             "sb_switchback_fwd_bwd_host": ([v, C.POINTER(LinearMode), v, v, v, i32, i64, i64, i64, v, v, v], i32),
             "sb_switchback_fwd_bwd_host_async": ([v, C.POINTER(LinearMode), v, v, v, i32, i64, i64, i64, v, v, v], i32),
             "sb_host_pipeline_wait": ([v], i32),

@@ -697,6 +697,32 @@ sb_status sb_layernorm_quantize_rowwise(sb_handle h, const void* x, sb_dtype dt,
   return SB_OK;
 }
 
+sb_status sb_layernorm_backward_workspace_size(sb_handle h, int64_t cols, size_t* bytes) {
+  SB_TRY(check_h(h, "layernorm_backward"));
+  if (!bytes || cols <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, "layernorm_backward", "bad argument");
+  *bytes = static_cast<size_t>(sb::ln_backward_warps(h)) * 2 * static_cast<size_t>(cols) * sizeof(float);
+  return SB_OK;
+}
+
+sb_status sb_layernorm_backward(sb_handle h, const void* dh, const void* x, sb_dtype dt, int64_t rows, int64_t cols,
+                                const float* mean, const float* rstd, const float* gamma, void* dx, float* dgamma,
+                                float* dbeta, void* workspace, size_t workspace_bytes) {
+  const char* op = "layernorm_backward";
+  SB_TRY(check_h(h, op));
+  if (!dh || !x || !mean || !rstd || !gamma || !dx || !workspace || dt != SB_BF16)
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument (bf16 only)");
+  if (rows <= 0 || cols <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty matrix");
+  size_t need = 0;
+  SB_TRY(sb_layernorm_backward_workspace_size(h, cols, &need));
+  if (workspace_bytes < need) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "workspace too small");
+  const cudaError_t e = sb::launch_ln_backward(h, dh, x, rows, cols, mean, rstd, gamma, dx, dgamma, dbeta,
+                                               static_cast<float*>(workspace));
+  if (e == cudaErrorNotSupported)
+    return sb::fail(SB_ERR_UNSUPPORTED, op, "rows of <= 1280 columns, multiple of 8, 16-byte aligned");
+  SB_TRYC(op, e);
+  return SB_OK;
+}
+
 // ------------------------------------------------- host-buffer pipeline --
 // switchback_fwd_bwd over host memory: W is quantized once; token rows stream through in
 // chunks. Three streams: h2d copies, compute (the handle stream), d2h copies, so PCIe

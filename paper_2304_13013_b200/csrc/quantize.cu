@@ -809,6 +809,127 @@ void launch_ln_rows(sb_handle h, const __nv_bfloat16* x, int64_t rows, int nvec,
                                                                                 state, mean, rstd, h->d_err);
 }
 
+// LayerNorm backward for the fused pre-norm path (bf16 dh, x; fp32 mean, rstd, gamma):
+//   xhat = (x - mean) rstd, g = dh gamma, dx = rstd (g - mean(g) - xhat mean(g xhat)),
+//   dgamma = sum_rows dh xhat, dbeta = sum_rows dh.
+// One warp per row (rows of <= 1280 columns, held in registers with their per-column gamma /
+// beta-gradient accumulators); warp w owns rows w, w + W, ... and writes its column partials
+// to part[w][...]; k_ln_bwd_reduce sums them over w in a fixed order (deterministic).
+template <int VPL>
+__global__ void __launch_bounds__(256) k_ln_backward_rows(const __nv_bfloat16* __restrict__ dh,
+                                                          const __nv_bfloat16* __restrict__ x, int64_t rows, int nvec,
+                                                          const float* __restrict__ mean,
+                                                          const float* __restrict__ rstd,
+                                                          const float* __restrict__ gamma,
+                                                          __nv_bfloat16* __restrict__ dx, float* __restrict__ part) {
+  // shared: gamma[8][nvec] (k-major: lane-consecutive, conflict-free), then per warp its column
+  // accumulators dgamma[8][nvec], dbeta[8][nvec]
+  extern __shared__ float lnb_s[];
+  float* gs = lnb_s;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  float* accg = lnb_s + 8 * nvec * (1 + 2 * wib);
+  float* accb = accg + 8 * nvec;
+  for (int t = threadIdx.x; t < 8 * nvec; t += blockDim.x) gs[(t & 7) * nvec + (t >> 3)] = __ldg(gamma + t);
+  for (int t = lane; t < 8 * nvec; t += 32) {
+    accg[t] = 0.0f;
+    accb[t] = 0.0f;
+  }
+  __syncthreads();
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int cols = nvec * 8;
+  const float inv_n = 1.0f / static_cast<float>(cols);
+  for (int64_t row = gw; row < rows; row += warps) {
+    const int64_t off = row * static_cast<int64_t>(nvec);
+    uint4 vx[VPL], vd[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int i = j * 32 + lane;
+      vx[j] = i < nvec ? ld_stream(reinterpret_cast<const uint4*>(x) + off + i) : make_uint4(0, 0, 0, 0);
+      vd[j] = i < nvec ? ld_stream(reinterpret_cast<const uint4*>(dh) + off + i) : make_uint4(0, 0, 0, 0);
+    }
+    const float mu = __ldg(mean + row), rs = __ldg(rstd + row);
+    float s1 = 0.0f, s2 = 0.0f;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int i = j * 32 + lane;
+      if (i >= nvec) continue;
+      const __nv_bfloat162* px = reinterpret_cast<const __nv_bfloat162*>(&vx[j]);
+      const __nv_bfloat162* pd = reinterpret_cast<const __nv_bfloat162*>(&vd[j]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 fx = __bfloat1622float2(px[k]);
+        const float2 fd = __bfloat1622float2(pd[k]);
+        const float x0 = (fx.x - mu) * rs, x1 = (fx.y - mu) * rs;
+        const float g0 = fd.x * gs[(2 * k) * nvec + i], g1 = fd.y * gs[(2 * k + 1) * nvec + i];
+        s1 += g0 + g1;
+        s2 += g0 * x0 + g1 * x1;
+        accg[(2 * k) * nvec + i] += fd.x * x0;
+        accg[(2 * k + 1) * nvec + i] += fd.y * x1;
+        accb[(2 * k) * nvec + i] += fd.x;
+        accb[(2 * k + 1) * nvec + i] += fd.y;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    const float m1 = s1 * inv_n, m2 = s2 * inv_n;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int i = j * 32 + lane;
+      if (i >= nvec) continue;
+      const __nv_bfloat162* px = reinterpret_cast<const __nv_bfloat162*>(&vx[j]);
+      const __nv_bfloat162* pd = reinterpret_cast<const __nv_bfloat162*>(&vd[j]);
+      uint4 o;
+      __nv_bfloat162* po = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 fx = __bfloat1622float2(px[k]);
+        const float2 fd = __bfloat1622float2(pd[k]);
+        const float x0 = (fx.x - mu) * rs, x1 = (fx.y - mu) * rs;
+        const float g0 = fd.x * gs[(2 * k) * nvec + i], g1 = fd.y * gs[(2 * k + 1) * nvec + i];
+        po[k] = __float22bfloat162_rn(make_float2(rs * (g0 - m1 - x0 * m2), rs * (g1 - m1 - x1 * m2)));
+      }
+      reinterpret_cast<uint4*>(dx)[off + i] = o;
+    }
+  }
+  __syncwarp();
+  float* pg = part + gw * 2 * cols;
+  for (int t = lane; t < 8 * nvec; t += 32) {  // back to column order: c = i * 8 + k
+    const int k = t / nvec, i = t - k * nvec;
+    pg[i * 8 + k] = accg[t];
+    pg[cols + i * 8 + k] = accb[t];
+  }
+}
+
+template <int VPL>
+void launch_ln_bwd(sb_handle h, int64_t blocks, size_t smem, const __nv_bfloat16* D, const __nv_bfloat16* X,
+                   int64_t rows, int nvec, const float* mean, const float* rstd, const float* gamma, __nv_bfloat16* O,
+                   float* part) {
+  static bool attr = false;  // one flag per VPL instantiation
+  if (!attr) {
+    cudaFuncSetAttribute(k_ln_backward_rows<VPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  k_ln_backward_rows<VPL><<<static_cast<unsigned>(blocks), 256, smem, h->stream>>>(D, X, rows, nvec, mean, rstd, gamma,
+                                                                                   O, part);
+}
+
+__global__ void k_ln_bwd_reduce(const float* __restrict__ part, int64_t nparts, int cols, float* __restrict__ dgamma,
+                                float* __restrict__ dbeta) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= 2 * cols) return;
+  float s = 0.0f;
+  for (int64_t w = 0; w < nparts; ++w) s += part[w * 2 * cols + c];
+  if (c < cols) {
+    if (dgamma) dgamma[c] = s;
+  } else if (dbeta) {
+    dbeta[c - cols] = s;
+  }
+}
+
 // SB_QUANT_KERNEL=tma selects the smem-ring kernel (A/B measurements); default: registers.
 bool prefer_tma_ring() {
   static int v = -1;
@@ -1796,6 +1917,38 @@ cudaError_t launch_ln_quantize_rowwise(sb_handle h, const void* x, int64_t rows,
     case 8: launch_ln_rows<8>(h, X, rows, nvec, gamma, beta, eps, O, q, state, mean, rstd); break;
     default: return cudaErrorNotSupported;  // rows longer than 2048: not fused
   }
+  return cudaGetLastError();
+}
+
+// Warps the LayerNorm backward launches (its partial buffer holds 2 * cols floats per warp).
+int64_t ln_backward_warps(sb_handle h) { return static_cast<int64_t>(h->num_sms) * 2 * 8; }  // 2 blocks of 8 warps / SM
+
+cudaError_t launch_ln_backward(sb_handle h, const void* dh, const void* x, int64_t rows, int64_t cols,
+                               const float* mean, const float* rstd, const float* gamma, void* dx, float* dgamma,
+                               float* dbeta, float* part) {
+  using bf = __nv_bfloat16;
+  if (cols % 8 || cols > 1280 || !sb::aligned(dh, 16) || !sb::aligned(x, 16) || !sb::aligned(dx, 16) ||
+      !sb::aligned(part, 16))
+    return cudaErrorNotSupported;
+  const int nvec = static_cast<int>(cols / 8);
+  const int64_t blocks = ln_backward_warps(h) / 8;
+  const bf* D = static_cast<const bf*>(dh);
+  const bf* X = static_cast<const bf*>(x);
+  bf* O = static_cast<bf*>(dx);
+  const size_t smem = static_cast<size_t>(8) * nvec * (1 + 2 * 8) * sizeof(float);  // gamma + 8 warps x 2
+  h->launches++;
+  switch ((nvec + 31) / 32) {
+    case 1: launch_ln_bwd<1>(h, blocks, smem, D, X, rows, nvec, mean, rstd, gamma, O, part); break;
+    case 2: launch_ln_bwd<2>(h, blocks, smem, D, X, rows, nvec, mean, rstd, gamma, O, part); break;
+    case 3: launch_ln_bwd<3>(h, blocks, smem, D, X, rows, nvec, mean, rstd, gamma, O, part); break;
+    case 4: launch_ln_bwd<4>(h, blocks, smem, D, X, rows, nvec, mean, rstd, gamma, O, part); break;
+    default: launch_ln_bwd<5>(h, blocks, smem, D, X, rows, nvec, mean, rstd, gamma, O, part); break;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  h->launches++;
+  k_ln_bwd_reduce<<<static_cast<unsigned>((2 * cols + 255) / 256), 256, 0, h->stream>>>(part, ln_backward_warps(h),
+                                                                                          static_cast<int>(cols), dgamma, dbeta);
   return cudaGetLastError();
 }
 

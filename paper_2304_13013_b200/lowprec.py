@@ -157,6 +157,25 @@ def layernorm_quantize_rowwise(x: torch.Tensor, gamma: torch.Tensor, beta: torch
     return out, QuantizedMatrix(q, st, ROW), mean, rstd
 
 
+def layernorm_backward(dh: torch.Tensor, x: torch.Tensor, mean: torch.Tensor, rstd: torch.Tensor,
+                       gamma: torch.Tensor):
+    """Backward of layernorm_quantize_rowwise's LayerNorm: (dx bf16, dgamma fp32, dbeta fp32),
+    deterministic. Rows of up to 1280 columns."""
+    _need_cuda(dh, x, mean, rstd, gamma)
+    dh, x = dh.contiguous(), x.contiguous()
+    r, c = x.shape
+    h = A.handle(x.device.index)
+    nbytes = C.c_size_t()
+    A.check(h.lib.sb_layernorm_backward_workspace_size(h.h, c, C.byref(nbytes)))
+    ws = torch.empty(nbytes.value, dtype=torch.uint8, device=x.device)
+    dx = torch.empty_like(x)
+    dg = torch.empty(c, dtype=torch.float32, device=x.device)
+    db = torch.empty(c, dtype=torch.float32, device=x.device)
+    A.check(h.lib.sb_layernorm_backward(h.h, _p(dh), _p(x), _dt(x), r, c, _p(mean), _p(rstd),
+                                        _p(gamma.float().contiguous()), _p(dx), _p(dg), _p(db), _p(ws), ws.numel()))
+    return dx, dg, db
+
+
 def quantize_columnwise(x: torch.Tensor, check: bool = True, transposed: bool = False) -> QuantizedMatrix:
     """quantize.cpp:135-137. transposed=True returns quantize_rowwise(x^T) (linear.cpp:228-229)."""
     _need_cuda(x)

@@ -78,8 +78,12 @@ class SwitchBackLinear(torch.nn.Module):
 
 
 def _ln_backward(dh, x2d, mean, rstd, ln_w, ln_b, needs):
-    """LayerNorm backward with the forward's own mean / rstd, in fp32 (as a pre-norm block that
-    normalises x.float())."""
+    """LayerNorm backward with the forward's own mean / rstd: our bf16-in / bf16-out kernel
+    (sb_layernorm_backward, fp32 math, deterministic column sums) for rows of <= 1280 columns,
+    else torch's fp32 kernel."""
+    if x2d.shape[1] <= 1280 and x2d.shape[1] % 8 == 0:
+        dx, dg, db = L.layernorm_backward(dh, x2d, mean, rstd, ln_w.detach())
+        return (dx if needs[0] else None), (dg if needs[1] else None), (db if needs[2] else None)
     dx, dg, db = torch.ops.aten.native_layer_norm_backward(
         dh.float(), x2d.float(), [x2d.shape[1]], mean.view(-1, 1), rstd.view(-1, 1), ln_w.detach().float(),
         ln_b.detach().float(), list(needs))

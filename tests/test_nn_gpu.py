@@ -193,3 +193,23 @@ def test_prenorm_modules_match_fp32():
         assert rel(x.grad, xr.grad) < 3e-2
         for n, p in mod.named_parameters():
             assert rel(p.grad, params[n].grad) < 3e-2, n
+
+
+@pytest.mark.parametrize("rows,cols", [(5000, 1280), (37, 256), (300, 1000)])
+def test_layernorm_backward_kernel(rows, cols):
+    """sb_layernorm_backward against torch's LayerNorm backward (fp32) with the same mean /
+    rstd; dgamma / dbeta are fixed-order sums: bit-identical across runs."""
+    torch.manual_seed(cols)
+    x = (torch.randn(rows, cols, device="cuda") * 2 + 0.3).bfloat16()
+    g = torch.randn(cols, device="cuda") * 0.3 + 1
+    b = torch.randn(cols, device="cuda") * 0.1
+    _, _, mean, rstd = L.layernorm_quantize_rowwise(x, g, b)
+    dh = torch.randn(rows, cols, device="cuda").bfloat16()
+    dx, dg, db = L.layernorm_backward(dh, x, mean, rstd, g)
+    xr = x.float().requires_grad_(True)
+    gr, br = g.clone().requires_grad_(True), b.clone().requires_grad_(True)
+    torch.nn.functional.layer_norm(xr, (cols,), gr, br, 1e-5).backward(dh.float())
+    assert rel(dx, xr.grad) < 1e-2
+    assert rel(dg, gr.grad) < 1e-4 and rel(db, br.grad) < 1e-5
+    dx2, dg2, db2 = L.layernorm_backward(dh, x, mean, rstd, g)
+    assert torch.equal(dx, dx2) and torch.equal(dg, dg2) and torch.equal(db, db2)
