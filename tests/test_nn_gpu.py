@@ -213,3 +213,27 @@ def test_layernorm_backward_kernel(rows, cols):
     assert rel(dg, gr.grad) < 1e-4 and rel(db, br.grad) < 1e-5
     dx2, dg2, db2 = L.layernorm_backward(dh, x, mean, rstd, g)
     assert torch.equal(dx, dx2) and torch.equal(dg, dg2) and torch.equal(db, db2)
+
+
+def test_fused_producers_edge_rows():
+    """Constant rows (zero variance: out = beta, all-equal payload), all-zero rows (state
+    sentinel 1.0), and a non-finite row (latched, reported by check_error) through the fused
+    LayerNorm and GELU quantizers."""
+    cols = 1280
+    x = torch.randn(6, cols, device="cuda").bfloat16()
+    x[1] = 3.0
+    x[2] = 0.0
+    g = torch.ones(cols, device="cuda")
+    b = torch.zeros(cols, device="cuda")
+    out, q, mean, rstd = L.layernorm_quantize_rowwise(x, g, b)
+    assert (out[1] == 0).all() and (out[2] == 0).all()
+    assert float(q.state[1]) == 1.0 and float(q.state[2]) == 1.0  # zero rows: sentinel state
+    assert float(mean[1]) == 3.0
+    act, aq = L.gelu_quantize_rowwise(x)
+    assert float(aq.state[2]) == 1.0 and (aq.payload[2] == 0).all()
+    bad = x.clone()
+    bad[4, 7] = float("nan")
+    with pytest.raises(L.InvalidArgument):
+        L.gelu_quantize_rowwise(bad)
+    with pytest.raises(L.InvalidArgument):
+        L.layernorm_quantize_rowwise(bad, g, b)
