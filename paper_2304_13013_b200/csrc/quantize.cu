@@ -695,7 +695,7 @@ cudaError_t launch_act_rows(sb_handle h, const __nv_bfloat16* a, const __nv_bflo
 // quantized row-wise; mean / rstd are written for the backward. Payload / states equal
 // quantize_rowwise(h) bit for bit.
 template <int VPL>
-__global__ void __launch_bounds__(256) k_ln_quantize_rows(const __nv_bfloat16* __restrict__ x, int64_t rows, int nvec,
+__global__ void __launch_bounds__(256, 3) k_ln_quantize_rows(const __nv_bfloat16* __restrict__ x, int64_t rows, int nvec,
                                                           const float* __restrict__ gamma,
                                                           const float* __restrict__ beta, float eps,
                                                           __nv_bfloat16* __restrict__ h, int8_t* __restrict__ q,
@@ -895,12 +895,17 @@ __global__ void __launch_bounds__(256) k_ln_backward_rows(const __nv_bfloat16* _
       reinterpret_cast<uint4*>(dx)[off + i] = o;
     }
   }
-  __syncwarp();
-  float* pg = part + gw * 2 * cols;
-  for (int t = lane; t < 8 * nvec; t += 32) {  // back to column order: c = i * 8 + k
-    const int k = t / nvec, i = t - k * nvec;
-    pg[i * 8 + k] = accg[t];
-    pg[cols + i * 8 + k] = accb[t];
+  // the block sums its warps' column accumulators in warp order (deterministic) and writes one
+  // partial per block, in column order c = i * 8 + k
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  float* pg = part + static_cast<int64_t>(blockIdx.x) * 2 * cols;
+  for (int t = threadIdx.x; t < 16 * nvec; t += blockDim.x) {
+    const int which = t / (8 * nvec), tt = t - which * 8 * nvec;  // 0: dgamma, 1: dbeta
+    float acc = 0.0f;
+    for (int w = 0; w < nw; ++w) acc += lnb_s[8 * nvec * (1 + 2 * w + which) + tt];
+    const int k = tt / nvec, i = tt - k * nvec;
+    pg[which * cols + i * 8 + k] = acc;
   }
 }
 
@@ -917,16 +922,27 @@ void launch_ln_bwd(sb_handle h, int64_t blocks, size_t smem, const __nv_bfloat16
                                                                                    O, part);
 }
 
-__global__ void k_ln_bwd_reduce(const float* __restrict__ part, int64_t nparts, int cols, float* __restrict__ dgamma,
-                                float* __restrict__ dbeta) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= 2 * cols) return;
+// Column sums of the per-block partials [nparts][2 * cols]: block = 32 columns x 8 warps; warp w
+// sums partials w, w + 8, ... (coalesced 128-byte rows), then lane-wise over the 8 warps in
+// order: deterministic.
+__global__ void __launch_bounds__(256) k_ln_bwd_reduce(const float* __restrict__ part, int64_t nparts, int cols,
+                                                       float* __restrict__ dgamma, float* __restrict__ dbeta) {
+  __shared__ float red[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
   float s = 0.0f;
-  for (int64_t w = 0; w < nparts; ++w) s += part[w * 2 * cols + c];
-  if (c < cols) {
-    if (dgamma) dgamma[c] = s;
-  } else if (dbeta) {
-    dbeta[c - cols] = s;
+  if (c < 2 * cols)
+    for (int64_t p = w; p < nparts; p += 8) s += part[p * 2 * cols + c];
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && c < 2 * cols) {
+    float t = 0.0f;
+    for (int i = 0; i < 8; ++i) t += red[i][lane];
+    if (c < cols) {
+      if (dgamma) dgamma[c] = t;
+    } else if (dbeta) {
+      dbeta[c - cols] = t;
+    }
   }
 }
 
@@ -1947,8 +1963,8 @@ cudaError_t launch_ln_backward(sb_handle h, const void* dh, const void* x, int64
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   h->launches++;
-  k_ln_bwd_reduce<<<static_cast<unsigned>((2 * cols + 255) / 256), 256, 0, h->stream>>>(part, ln_backward_warps(h),
-                                                                                          static_cast<int>(cols), dgamma, dbeta);
+  k_ln_bwd_reduce<<<static_cast<unsigned>((2 * cols + 31) / 32), 256, 0, h->stream>>>(part, blocks, static_cast<int>(cols),
+                                                                                        dgamma, dbeta);
   return cudaGetLastError();
 }
 
