@@ -703,6 +703,13 @@ __global__ void __launch_bounds__(256, 3) k_ln_quantize_rows(const __nv_bfloat16
                                                           float* __restrict__ rstd_out, uint32_t* err) {
   using T = __nv_bfloat16;
   using Out = typename VecQ<T>::Out;
+  // gamma / beta staged once per block in shared memory (they are re-read for every row)
+  __shared__ float4 gb_s[2 * 2 * 32 * VPL];
+  for (int t = threadIdx.x; t < 2 * nvec; t += blockDim.x) {
+    gb_s[t] = __ldg(reinterpret_cast<const float4*>(gamma) + t);
+    gb_s[2 * 32 * VPL + t] = __ldg(reinterpret_cast<const float4*>(beta) + t);
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   const float inv_n = 1.0f / static_cast<float>(nvec * 8);
@@ -750,10 +757,8 @@ __global__ void __launch_bounds__(256, 3) k_ln_quantize_rows(const __nv_bfloat16
     for (int j = 0; j < VPL; ++j) {
       const int i = j * 32 + lane;
       if (i >= nvec) continue;
-      const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma) + 2 * i);
-      const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma) + 2 * i + 1);
-      const float4 b0 = __ldg(reinterpret_cast<const float4*>(beta) + 2 * i);
-      const float4 b1 = __ldg(reinterpret_cast<const float4*>(beta) + 2 * i + 1);
+      const float4 g0 = gb_s[2 * i], g1 = gb_s[2 * i + 1];
+      const float4 b0 = gb_s[2 * 32 * VPL + 2 * i], b1 = gb_s[2 * 32 * VPL + 2 * i + 1];
       const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
       const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
       __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&v[j]);
