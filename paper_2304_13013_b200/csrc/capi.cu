@@ -700,7 +700,7 @@ sb_status sb_layernorm_quantize_rowwise(sb_handle h, const void* x, sb_dtype dt,
 sb_status sb_layernorm_backward_workspace_size(sb_handle h, int64_t cols, size_t* bytes) {
   SB_TRY(check_h(h, "layernorm_backward"));
   if (!bytes || cols <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, "layernorm_backward", "bad argument");
-  *bytes = static_cast<size_t>(sb::ln_backward_warps(h)) * 2 * static_cast<size_t>(cols) * sizeof(float);
+  *bytes = static_cast<size_t>(sb::ln_backward_blocks(h)) * 2 * static_cast<size_t>(cols) * sizeof(float);
   return SB_OK;
 }
 

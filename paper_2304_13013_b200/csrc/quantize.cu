@@ -1941,8 +1941,8 @@ cudaError_t launch_ln_quantize_rowwise(sb_handle h, const void* x, int64_t rows,
   return cudaGetLastError();
 }
 
-// Warps the LayerNorm backward launches (its partial buffer holds 2 * cols floats per warp).
-int64_t ln_backward_warps(sb_handle h) { return static_cast<int64_t>(h->num_sms) * 2 * 8; }  // 2 blocks of 8 warps / SM
+// Blocks the LayerNorm backward launches (its partial buffer holds 2 * cols floats per block).
+int64_t ln_backward_blocks(sb_handle h) { return static_cast<int64_t>(h->num_sms) * 2; }  // 2 blocks of 8 warps / SM
 
 cudaError_t launch_ln_backward(sb_handle h, const void* dh, const void* x, int64_t rows, int64_t cols,
                                const float* mean, const float* rstd, const float* gamma, void* dx, float* dgamma,
@@ -1952,7 +1952,7 @@ cudaError_t launch_ln_backward(sb_handle h, const void* dh, const void* x, int64
       !sb::aligned(part, 16))
     return cudaErrorNotSupported;
   const int nvec = static_cast<int>(cols / 8);
-  const int64_t blocks = ln_backward_warps(h) / 8;
+  const int64_t blocks = ln_backward_blocks(h);
   const bf* D = static_cast<const bf*>(dh);
   const bf* X = static_cast<const bf*>(x);
   bf* O = static_cast<bf*>(dx);

@@ -125,9 +125,9 @@ cudaError_t launch_dequantize_fp8(sb_handle h, const uint8_t* q, int64_t rows, i
                                   const float* state, int axis, void* y, sb_dtype ydt, int64_t ldy);
 cudaError_t launch_convert(sb_handle h, const void* x, sb_dtype xdt, void* y, sb_dtype ydt, int64_t n);
 cudaError_t build_gelu_lut(sb_handle h);
-int64_t ln_backward_warps(sb_handle h);
+int64_t ln_backward_blocks(sb_handle h);
 // LayerNorm backward (bf16 dh / x / dx, fp32 mean / rstd / gamma / dgamma / dbeta) for rows of
-// <= 1280 columns; part = ln_backward_warps(h) * 2 * cols floats of scratch.
+// <= 1280 columns; part = ln_backward_blocks(h) * 2 * cols floats of scratch.
 cudaError_t launch_ln_backward(sb_handle h, const void* dh, const void* x, int64_t rows, int64_t cols,
                                const float* mean, const float* rstd, const float* gamma, void* dx, float* dgamma,
                                float* dbeta, float* part);
