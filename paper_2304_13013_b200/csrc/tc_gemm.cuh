@@ -62,6 +62,7 @@ struct Params {
   int tiles_m, tiles_n;
   int splits;              // split-K factor: work unit u = (tile u / splits, k-slice u % splits)
   int m_fast;              // raster: 1 = consecutive tiles walk M (B tile reused), 0 = walk N (A reused)
+  int tma3d;               // 2-CTA K-major operands as 3D maps (byte-in-atom, row, atom): bit 0 A, bit 1 B
   const float* bias;       // optional per-output-column bias (OUT_BF16 / OUT_F32): y = fl(acc * scale) + bias
 };
 

@@ -114,11 +114,25 @@ __device__ __forceinline__ void mma2(uint32_t d, uint64_t a, uint64_t b, uint32_
 // Load one operand's share of a stage: 128 rows (or MN columns) x ATOMS*128 bytes of K.
 // K-major: ATOMS boxes {KATOM elements, 128 rows} side by side along K.
 // MN-major: two boxes {64 MN elements, 64*ATOMS k-rows}, one per 64-wide MN chunk.
+// 3D form for K-major operands: the map views the operand as (byte-in-atom, row, K atom), so
+// one TMA lands all ATOMS atoms of a stage as consecutive 16 KB SW128 blocks (the same smem
+// layout as ATOMS 2D loads). Fewer bulk-tensor issues per stage shorten the single producer
+// thread's per-stage latency (tools/feed_bench.cu mode 2).
+__device__ __forceinline__ void tma_load_2sm_3d(const CUtensorMap* m, uint64_t* bar, void* dst, int32_t c0, int32_t c1,
+                                                int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          sbptx::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(sbptx::smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
 template <bool MN, int KATOM, int ATOMS>
-__device__ __forceinline__ void load2(const CUtensorMap* tm, uint64_t* bar, uint8_t* dst, int r0, int kb) {
+__device__ __forceinline__ void load2(const CUtensorMap* tm, uint64_t* bar, uint8_t* dst, int r0, int kb, bool three_d) {
   if (MN) {
     tma_load_2sm(tm, bar, dst, r0, kb * 64 * ATOMS);
     tma_load_2sm(tm, bar, dst + ATOMS * 8192, r0 + 64, kb * 64 * ATOMS);
+  } else if (three_d) {
+    tma_load_2sm_3d(tm, bar, dst, 0, r0, ATOMS * kb);
   } else {
 #pragma unroll
     for (int j = 0; j < ATOMS; ++j) tma_load_2sm(tm, bar, dst + j * ATOM_BYTES, (ATOMS * kb + j) * KATOM, r0);
@@ -214,8 +228,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const uint32_t phase = static_cast<uint32_t>(i / STAGES2) & 1u;
         { SB_PROBE_T0(); sbptx::mbar_wait(&empty_bar[stage], phase ^ 1u); SB_PROBE_ADD(3); }
         if (rank == 0) sbptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * PP::STAGE);
-        load2<A_MN, Kind2<KIND>::KATOM, PP::ATOMS>(&tmA, &full_bar[stage], smem_a + stage * PP::OPB, am0, kb);
-        load2<B_MN, Kind2<KIND>::KATOM, PP::ATOMS>(&tmB, &full_bar[stage], smem_b + stage * PP::OPB, bn0, kb);
+        load2<A_MN, Kind2<KIND>::KATOM, PP::ATOMS>(&tmA, &full_bar[stage], smem_a + stage * PP::OPB, am0, kb,
+                                                   p.tma3d & 1);
+        load2<B_MN, Kind2<KIND>::KATOM, PP::ATOMS>(&tmB, &full_bar[stage], smem_b + stage * PP::OPB, bn0, kb,
+                                                   p.tma3d & 2);
 #ifdef SB_GEMM_PROBE
         if (pair == 0 && i < 512) g_trace[rank * 512 + i] = gtime();
 #endif

@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(64, 1) k_feed(const __grid_constant__ CUtensor
     sbptx::fence_mbar_init();
   }
   __syncthreads();
-  const int tiles_r = rows_total / (box_rows * boxes);
+  const int tiles_r = rows_total / (mode == 2 ? box_rows : box_rows * boxes);
   long long t0 = clock64();
   if (warp == 0 && lane == 0) {
     int stage = 0;
@@ -64,6 +64,14 @@ __global__ void __launch_bounds__(64, 1) k_feed(const __grid_constant__ CUtensor
         for (int b = 0; b < boxes; ++b)
           sbptx::tma_load_2d(&tm, &full[stage], smem + stage * stage_bytes + b * box_rows * 128, kb * 128,
                              (tile * boxes + b) * box_rows);
+      } else if (mode == 2) {
+        // one 3D box {128 B, box_rows, boxes K-atoms} per stage: dims (byte-in-atom, row, atom)
+        const int atom0 = (kb * boxes) % (1280 / 128 - boxes + 1);
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+                sbptx::smem_u32(smem + stage * stage_bytes)),
+            "l"(reinterpret_cast<uint64_t>(&tm)), "r"(0), "r"(tile * box_rows), "r"(atom0), "r"(sbptx::smem_u32(&full[stage]))
+            : "memory");
       } else {
         for (int b = 0; b < boxes; ++b) {
           const int8_t* g = src1d + ((size_t)(tile * boxes + b) * box_rows * 1280 + (size_t)kb * box_rows * 128) % ((size_t)rows_total * 1280 - box_rows * 128);
@@ -110,10 +118,23 @@ int main(int argc, char** argv) {
   if (argc > 2) sms = atoi(argv[2]);  // CTAs launched (one per SM): per-SM vs aggregate limit
   cudaFuncSetAttribute(k_feed, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   struct Cfg { int stages, box_rows, boxes, mode, per_sm, wv; };
-  const Cfg cfgs[] = {{8, 128, 1, 0, 1, 0}, {4, 128, 3, 0, 1, 0}};
+  const Cfg cfgs[] = {{3, 128, 4, 0, 1, 0}, {3, 256, 2, 2, 1, 0}, {3, 128, 4, 2, 1, 0}, {6, 128, 2, 2, 1, 0}, {6, 128, 2, 0, 1, 0}};
   for (const Cfg& c : cfgs) {
     CUtensorMap tm;
-    if (!sb::encode_tmap_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, src, K, R, K, 128, c.box_rows,
+    if (c.mode == 2) {
+      // 3D view of the row-major [R x K] int8 matrix: (byte within a 128-B K atom, row, atom)
+      const cuuint64_t dims[3] = {128, (cuuint64_t)R, (cuuint64_t)(K / 128)};
+      const cuuint64_t strides[2] = {(cuuint64_t)K, 128};
+      const cuuint32_t box[3] = {128, (cuuint32_t)c.box_rows, (cuuint32_t)c.boxes};
+      const cuuint32_t estr[3] = {1, 1, 1};
+      CUresult r = cuTensorMapEncodeTiled(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, src, dims, strides, box, estr,
+                                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) {
+        printf("3D encode failed: %d\n", (int)r);
+        continue;
+      }
+    } else if (!sb::encode_tmap_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, src, K, R, K, 128, c.box_rows,
                             CU_TENSOR_MAP_SWIZZLE_128B)) {
       printf("encode failed\n");
       return 1;
