@@ -64,11 +64,16 @@ class SwitchBackLinear(torch.nn.Module):
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         shape = x.shape
         x2d = x.reshape(-1, self.in_features)
-        if self.norm is not None:
+        fusable = self.mode.format == A.SB_INT8 and self.mode.variant in (A.SB_SWITCHBACK, A.SB_SWITCHBACK_M,
+                                                                          A.SB_SWITCHBACK_Q)
+        if self.norm is not None and fusable:
             if x.dtype != torch.bfloat16:
                 raise TypeError("prenorm SwitchBackLinear runs in bf16")
             y = _LNLinearFn.apply(x2d, self.norm.weight, self.norm.bias, self.norm.eps, self.weight, self.bias,
                                   self.mode)
+        elif self.norm is not None:  # fp8 / tensor-wise X: LayerNorm unfused, then the layer
+            h = self.norm(x2d.float()).to(x2d.dtype)
+            y = _SwitchBackLinearFn.apply(h, self.weight, self.bias, self.mode)
         else:
             y = _SwitchBackLinearFn.apply(x2d, self.weight, self.bias, self.mode)
         return y.reshape(*shape[:-1], self.out_features)

@@ -237,3 +237,26 @@ def test_fused_producers_edge_rows():
         L.gelu_quantize_rowwise(bad)
     with pytest.raises(L.InvalidArgument):
         L.layernorm_quantize_rowwise(bad, g, b)
+
+
+@pytest.mark.parametrize("variant,fmt", [("switchback_q", "int8"), ("switchback_m", "int8"), ("switchback", "fp8"),
+                                         ("allquant", "int8")])
+def test_linear_module_variants(variant, fmt):
+    """SwitchBackLinear over the other reference variants / formats (prenorm fused where the
+    variant quantizes X row-wise in int8, unfused otherwise) against an fp32 reference."""
+    from paper_2304_13013_b200.nn import SwitchBackLinear
+
+    torch.manual_seed(4)
+    F = torch.nn.functional
+    mod = SwitchBackLinear(256, 320, variant=variant, fmt=fmt, prenorm=True)
+    x = torch.randn(600, 256, device="cuda").bfloat16().requires_grad_(True)
+    y = mod(x)
+    g = torch.randn_like(y)
+    y.backward(g)
+    xr = x.detach().float().requires_grad_(True)
+    ps = {n: p.detach().clone().requires_grad_(True) for n, p in mod.named_parameters()}
+    yr = F.linear(F.layer_norm(xr, (256,), ps["norm.weight"], ps["norm.bias"], mod.norm.eps), ps["weight"], ps["bias"])
+    yr.backward(g.float())
+    tol = 8e-2 if fmt == "fp8" else 3e-2
+    assert rel(y, yr) < tol and rel(x.grad, xr.grad) < tol
+    assert rel(mod.weight.grad, ps["weight"].grad) < tol
