@@ -550,6 +550,24 @@ def run_vit_block(args):
     fused = not args.no_overlap  # --no-overlap also turns the LayerNorm / GELU producer fusions off (A/B)
     T = B * S
 
+    class SplitQKV(torch.autograd.Function):
+        """q, k, v (B, H, S, Dh) views of the packed qkv output; the backward writes dq, dk, dv
+        straight into one packed (B, S, 3, H, Dh) gradient (three strided copies) instead of
+        autograd's stack + permute + contiguous (~1.9 ms of layout copies per step). Shared by
+        both arms: it is block plumbing, not part of the measured linears."""
+
+        @staticmethod
+        def forward(ctx, qkv):
+            t = qkv.view(B, S, 3, H, D // H)
+            return tuple(t[:, :, i].transpose(1, 2) for i in range(3))
+
+        @staticmethod
+        def backward(ctx, dq, dk, dv):
+            out = torch.empty(B, S, 3, H, D // H, dtype=dq.dtype, device=dq.device)
+            for i, g in enumerate((dq, dk, dv)):
+                out[:, :, i].copy_(g.transpose(1, 2))
+            return out.view(B, S, 3 * D)
+
     class Block(torch.nn.Module):
         def __init__(self, sb):
             super().__init__()
@@ -571,7 +589,7 @@ def run_vit_block(args):
 
         def forward(self, x):
             h = x if self.fused else self.ln1(x.float()).to(torch.bfloat16)
-            q, k, v = self.qkv(h).view(B, S, 3, H, D // H).permute(2, 0, 3, 1, 4).unbind(0)
+            q, k, v = SplitQKV.apply(self.qkv(h))
             a = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(B, S, D)
             x = x + self.out(a)
             h = x if self.fused else self.ln2(x.float()).to(torch.bfloat16)
