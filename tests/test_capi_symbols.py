@@ -61,3 +61,23 @@ def test_lowprec_shim_exports_reference_api():
                  "lowprec::linear_backward(", "lowprec::optimizer_step(", "lowprec::dequantize(",
                  "lowprec::quantize_fp8(", "lowprec::matmul("]:
         assert name in syms, name
+
+
+def test_pytorch_modules_have_no_cpu_fallback():
+    """The nn layer and the fused producer ops refuse CPU tensors instead of computing
+    anything on the host (the product path is the CUDA library or nothing)."""
+    import torch
+
+    from paper_2304_13013_b200 import lowprec as Lp
+    from paper_2304_13013_b200.nn import SwitchBackLinear
+
+    mod = SwitchBackLinear(16, 8, device="cpu")
+    with pytest.raises(Lp.InvalidArgument):
+        mod(torch.randn(4, 16).bfloat16())
+    x = torch.randn(4, 16).bfloat16()
+    with pytest.raises(Lp.InvalidArgument):
+        Lp.gelu_quantize_rowwise(x)
+    with pytest.raises(Lp.InvalidArgument):
+        Lp.layernorm_quantize_rowwise(x, torch.ones(16), torch.zeros(16))
+    with pytest.raises(Lp.InvalidArgument):
+        Lp.linear_forward(Lp.LinearMode(A.SB_SWITCHBACK, A.SB_INT8), x, torch.randn(8, 16).bfloat16())
