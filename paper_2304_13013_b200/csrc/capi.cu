@@ -156,7 +156,11 @@ sb_status check_h(sb_handle h, const char* op) {
 sb_status q_tensorwise(sb_handle h, const void* x, sb_dtype dt, int64_t r, int64_t c, int64_t ldx, int8_t* q,
                        int64_t ldq, int8_t* qt, int64_t ldqt, float* state, unsigned int* word) {
   cudaError_t fe = cudaSuccess;
-  if (sb::launch_quantize_tensorwise_fused(h, x, dt, r, c, ldx, q, ldq, qt, ldqt, state, word, &fe)) {
+  static const bool fused = [] {  // SB_TW_FUSED=0: two launches (absmax, then quantize) -- A/B switch
+    const char* e = std::getenv("SB_TW_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  if (fused && sb::launch_quantize_tensorwise_fused(h, x, dt, r, c, ldx, q, ldq, qt, ldqt, state, word, &fe)) {
     SB_TRYC("quantize_tensorwise", fe);
     return SB_OK;
   }
