@@ -39,7 +39,7 @@ def to_bytes(v, u):
 def main(tag):
     os.makedirs(PROF, exist_ok=True)
     summary = {}
-    for name in ("prof_dw", "prof_i8", "prof_q", "prof_k10", "prof_adamw"):
+    for name in ("prof_dw", "prof_i8", "prof_q", "prof_k10", "prof_ln", "prof_lnb", "prof_adamw"):
         rep = os.path.join(OUT, name + ".ncu-rep")
         if not os.path.exists(rep):
             continue
