@@ -695,34 +695,13 @@ cudaError_t launch_act_rows(sb_handle h, const __nv_bfloat16* a, const __nv_bflo
 // quantized row-wise; mean / rstd are written for the backward. Payload / states equal
 // quantize_rowwise(h) bit for bit.
 template <int VPL>
-__global__ void __launch_bounds__(256, 3) k_ln_quantize_rows(const __nv_bfloat16* __restrict__ x, int64_t rows, int nvec,
-                                                          const float* __restrict__ gamma,
-                                                          const float* __restrict__ beta, float eps,
-                                                          __nv_bfloat16* __restrict__ h, int8_t* __restrict__ q,
-                                                          float* __restrict__ state, float* __restrict__ mean_out,
-                                                          float* __restrict__ rstd_out, uint32_t* err) {
+__device__ __forceinline__ void ln_row(uint4 (&v)[VPL], int64_t row, int nvec, int lane, float inv_n, float eps,
+                                       const float4* gb_s, __nv_bfloat16* __restrict__ h, int8_t* __restrict__ q,
+                                       float* __restrict__ state, float* __restrict__ mean_out,
+                                       float* __restrict__ rstd_out, uint32_t* err) {
   using T = __nv_bfloat16;
   using Out = typename VecQ<T>::Out;
-  // gamma / beta staged once per block in shared memory (they are re-read for every row)
-  __shared__ float4 gb_s[2 * 2 * 32 * VPL];
-  for (int t = threadIdx.x; t < 2 * nvec; t += blockDim.x) {
-    gb_s[t] = __ldg(reinterpret_cast<const float4*>(gamma) + t);
-    gb_s[2 * 32 * VPL + t] = __ldg(reinterpret_cast<const float4*>(beta) + t);
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  const float inv_n = 1.0f / static_cast<float>(nvec * 8);
-  for (int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
-       row += warps) {
-    const int64_t off = row * static_cast<int64_t>(nvec);
-    const uint4* xr = reinterpret_cast<const uint4*>(x) + off;
-    uint4 v[VPL];
-#pragma unroll
-    for (int j = 0; j < VPL; ++j) {
-      const int i = j * 32 + lane;
-      v[j] = i < nvec ? ld_stream(xr + i) : make_uint4(0, 0, 0, 0);
-    }
+  const int64_t off = row * static_cast<int64_t>(nvec);
     float sum = 0.0f;
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
@@ -781,7 +760,7 @@ __global__ void __launch_bounds__(256, 3) k_ln_quantize_rows(const __nv_bfloat16
         raise_nonfinite(err);
         state[row] = __uint_as_float(amax);
       }
-      continue;
+      return;
     }
     const float st = state_from_bits(amax);
     if (lane == 0) state[row] = st;
@@ -795,6 +774,39 @@ __global__ void __launch_bounds__(256, 3) k_ln_quantize_rows(const __nv_bfloat16
       const Out o = qvec<T>(v[j], sc, plain);
       if (i < nvec) qr[i] = o;
     }
+}
+
+// Two rows per warp step: both rows' loads are issued before either row's math.
+template <int VPL>
+__global__ void __launch_bounds__(256, 2) k_ln_quantize_rows(const __nv_bfloat16* __restrict__ x, int64_t rows, int nvec,
+                                                          const float* __restrict__ gamma,
+                                                          const float* __restrict__ beta, float eps,
+                                                          __nv_bfloat16* __restrict__ h, int8_t* __restrict__ q,
+                                                          float* __restrict__ state, float* __restrict__ mean_out,
+                                                          float* __restrict__ rstd_out, uint32_t* err) {
+  // gamma / beta staged once per block in shared memory (they are re-read for every row)
+  __shared__ float4 gb_s[2 * 2 * 32 * VPL];
+  for (int t = threadIdx.x; t < 2 * nvec; t += blockDim.x) {
+    gb_s[t] = __ldg(reinterpret_cast<const float4*>(gamma) + t);
+    gb_s[2 * 32 * VPL + t] = __ldg(reinterpret_cast<const float4*>(beta) + t);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const float inv_n = 1.0f / static_cast<float>(nvec * 8);
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+       row += 2 * warps) {
+    const int64_t row2 = row + warps;
+    uint4 v[VPL], w[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int i = j * 32 + lane;
+      v[j] = i < nvec ? ld_stream(reinterpret_cast<const uint4*>(x) + row * nvec + i) : make_uint4(0, 0, 0, 0);
+      w[j] = (row2 < rows && i < nvec) ? ld_stream(reinterpret_cast<const uint4*>(x) + row2 * nvec + i)
+                                       : make_uint4(0, 0, 0, 0);
+    }
+    ln_row<VPL>(v, row, nvec, lane, inv_n, eps, gb_s, h, q, state, mean_out, rstd_out, err);
+    if (row2 < rows) ln_row<VPL>(w, row2, nvec, lane, inv_n, eps, gb_s, h, q, state, mean_out, rstd_out, err);
   }
 }
 
