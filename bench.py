@@ -188,8 +188,10 @@ def run_reference_arm(args):
     rates = []
     for _ in range(args.warmup):
         pass
+    # each step is a bounded sample; the whole arm stays around a minute whatever --steps is
+    budget = max(1.0, min(args.ref_budget, 60.0 / max(1, args.steps)))
     for _ in range(max(1, args.steps)):
-        r, cores, sample, kind = cpu_reference_rate(budget_s=args.ref_budget)
+        r, cores, sample, kind = cpu_reference_rate(budget_s=budget)
         rates.append(r)
     v = sum(rates) / len(rates)
     line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
