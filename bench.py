@@ -449,6 +449,17 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def adamw_traffic(n_params):
+    """DRAM bytes of one optimizer step over n_params, scaled from the ncu measurement in
+    profiles/adamw_traffic.json (None when absent)."""
+    prof = os.path.join(ROOT, "profiles", "adamw_traffic.json")
+    if not os.path.exists(prof):
+        return None
+    with open(prof) as f:
+        d = json.load(f)
+    return d["bytes_per_step"] / d["params"] * n_params
+
+
 def run_c5(args):
     """BASELINE.json configs[4]: one StableAdamW step (optimizer.cpp:102-172, update_clip,
     beta1 0.9, beta2 0.99, eps 1e-6, weight decay 0.2) over the ~1.0e9 fp32 parameters of 51
@@ -528,7 +539,7 @@ def run_c5(args):
                 "gpu_launches": launches,
                 "roofline": {"bound": "hbm", "kernel": "StableAdamW phase 1 + 2 (csrc/optim.cu)", "achieved": achieved,
                              "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
-                             "traffic": None, "bytes_per_param": 28},
+                             "traffic": adamw_traffic(n_mine), "bytes_per_param": 28},
                 "clocks": clk.summary(), "e2e": None, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
     if world > 1:
