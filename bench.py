@@ -564,6 +564,9 @@ def run_vit_block(args):
     torch.cuda.set_device(dev)
     B, S, D, H = 256, 257, 1280, 16
     fused = not args.no_overlap  # --no-overlap also turns the LayerNorm / GELU producer fusions off (A/B)
+    # residual adds in the GEMM epilogues: SB_BLOCK_RESID=1 (measured slower, 8.20 vs 7.95 ms: the
+    # epilogue reads the residual with per-row 4-byte loads; a TMA-staged residual tile is the fix)
+    resid_fused = os.environ.get("SB_BLOCK_RESID", "0") == "1"
     T = B * S
 
     class SplitQKV(torch.autograd.Function):
@@ -607,6 +610,9 @@ def run_vit_block(args):
             h = x if self.fused else self.ln1(x.float()).to(torch.bfloat16)
             q, k, v = SplitQKV.apply(self.qkv(h))
             a = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(B, S, D)
+            if self.fused and resid_fused:  # skip connections added in the out-proj / fc2 GEMM epilogues
+                x = self.out(a, residual=x)
+                return self.mlp(x, residual=x)
             x = x + self.out(a)
             h = x if self.fused else self.ln2(x.float()).to(torch.bfloat16)
             return x + self.mlp(h)

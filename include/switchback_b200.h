@@ -249,6 +249,13 @@ sb_status sb_linear_forward_prequant(sb_handle h, const sb_linear_mode* mode, co
                                      const float* x_state, const void* w, const float* bias, sb_dtype dt, int64_t b,
                                      int64_t n, int64_t m, void* y, sb_linear_ctx* ctx, void* workspace,
                                      size_t workspace_bytes);
+/* y = residual + (X W^T + bias): the residual (dt, b x m, contiguous) is added in the int8 GEMM
+ * epilogue before the single rounding to dt (the block's skip connection, model.cpp:327-333).
+ * x_q / x_state may be NULL (X quantized here) or a producer's payload as in _prequant. */
+sb_status sb_linear_forward_residual(sb_handle h, const sb_linear_mode* mode, const void* x, const int8_t* x_q,
+                                     const float* x_state, const void* w, const float* bias, const void* residual,
+                                     sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y, sb_linear_ctx* ctx,
+                                     void* workspace, size_t workspace_bytes);
 /* sb_linear_backward with G already quantized row-wise by its producer (g_q b x m, g_state b). */
 sb_status sb_linear_backward_prequant(sb_handle h, const sb_linear_mode* mode, const sb_linear_ctx* ctx, const void* g,
                                       const int8_t* g_q, const float* g_state, void* dx, float* dw, int dw_accumulate);

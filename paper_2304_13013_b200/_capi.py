@@ -30,7 +30,7 @@ EXPORTS = [
     "sb_last_error", "sb_launch_count", "sb_quantize_rowwise", "sb_quantize_columnwise",
     "sb_quantize_tensorwise", "sb_dequantize", "sb_quantize_fp8", "sb_dequantize_fp8", "sb_gemm_i8",
     "sb_matmul_f32", "sb_wgrad", "sb_gemm_fp8", "sb_linear_workspace_size", "sb_linear_forward", "sb_linear_forward_bias",
-    "sb_linear_forward_prequant", "sb_linear_backward_prequant", "sb_gelu_quantize_rowwise",
+    "sb_linear_forward_prequant", "sb_linear_backward_prequant", "sb_gelu_quantize_rowwise", "sb_linear_forward_residual",
     "sb_gelu_backward_quantize_rowwise", "sb_layernorm_quantize_rowwise", "sb_layernorm_backward_workspace_size",
     "sb_layernorm_backward",
     "sb_linear_backward", "sb_switchback_fwd_bwd_host", "sb_switchback_fwd_bwd_host_async",
@@ -122,6 +122,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             "sb_linear_forward_prequant": ([v, C.POINTER(LinearMode), v, v, v, v, v, i32, i64, i64, i64, v,
                                             C.POINTER(LinearCtx), v, sz], i32),
             "sb_linear_backward_prequant": ([v, C.POINTER(LinearMode), C.POINTER(LinearCtx), v, v, v, v, v, i32], i32),
+            "sb_linear_forward_residual": ([v, C.POINTER(LinearMode), v, v, v, v, v, v, i32, i64, i64, i64, v,
+                                            C.POINTER(LinearCtx), v, sz], i32),
             "sb_gelu_quantize_rowwise": ([v, v, i32, i64, i64, v, v, v], i32),
             "sb_gelu_backward_quantize_rowwise": ([v, v, v, i32, i64, i64, v, v, v], i32),
             "sb_layernorm_quantize_rowwise": ([v, v, i32, i64, i64, v, v, C.c_float, v, v, v, v, v], i32),
@@ -146,6 +148,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             "sb_dequantize_values": ([v, v, i64, i64, v, i32, v], i32),
         }
         for name, (args, res) in sig.items():
+            if os.environ.get("SB_LIB_PATH") and not hasattr(L, name):
+                continue  # A/B runs against an older build: bind what it exports
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = res

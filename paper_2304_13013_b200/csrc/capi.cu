@@ -418,7 +418,8 @@ static bool same_mode(const sb_linear_mode& a, const sb_linear_mode& b) {  // Li
 static sb_status linear_forward_impl(sb_handle h, const sb_linear_mode* mode, const void* x, const void* w,
                                      const float* bias, sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y,
                                      sb_linear_ctx* ctx, void* workspace, size_t ws_bytes,
-                                     const int8_t* xq_in = nullptr, const float* xs_in = nullptr) {
+                                     const int8_t* xq_in = nullptr, const float* xs_in = nullptr,
+                                     const void* resid = nullptr) {
   const char* op = "linear_forward";
   SB_TRY(check_h(h, op));
   if (!mode || !x || !w || !y || !float_dtype(dt)) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
@@ -451,6 +452,7 @@ static sb_status linear_forward_impl(sb_handle h, const sb_linear_mode* mode, co
       SB_TRY(gemm_bf16(h, x, false, w, false, b, m, n, y, out_dt));
     }
     if (bias) SB_TRYC(op, sb::launch_add_bias(h, y, out_dt, b, m, bias));
+    if (resid) SB_TRYC(op, sb::launch_add_residual(h, y, out_dt, b, m, resid));
     if (ctx) ctx->valid = 1;
     return SB_OK;
   }
@@ -467,11 +469,12 @@ static sb_status linear_forward_impl(sb_handle h, const sb_linear_mode* mode, co
     if (md.variant == SB_SWITCHBACK_Q) {
       // dual row-wise: Y = qrow(X) . qrow(W)^T (linear.cpp:131-132)
       SB_TRYC(op, sb::launch_quantize_rowwise(h, w, dt, m, n, n, ws.w_q, n, ws.w_state));
-      SB_TRY(sb::gemm_i8(h, xq, xs, ws.w_q, ws.w_state, SB_SCALE_ROW_ROW, b, m, n, y, out_dt, md.exact, bias));
+      SB_TRY(sb::gemm_i8(h, xq, xs, ws.w_q, ws.w_state, SB_SCALE_ROW_ROW, b, m, n, y, out_dt, md.exact, bias, resid, m));
     } else {
       // tensor-wise W, both layouts from one read; W^T payload cached for the backward
       SB_TRY(q_tensorwise(h, w, dt, m, n, n, ws.w_q, n, ws.w_qt, m, ws.w_state, ws.words));
-      SB_TRY(sb::gemm_i8(h, xq, xs, ws.w_q, ws.w_state, SB_SCALE_ROW_TENSOR, b, m, n, y, out_dt, md.exact, bias));
+      SB_TRY(sb::gemm_i8(h, xq, xs, ws.w_q, ws.w_state, SB_SCALE_ROW_TENSOR, b, m, n, y, out_dt, md.exact, bias, resid,
+                         m));
     }
     if (ctx) {
       ctx->w_q_t = md.variant == SB_SWITCHBACK_Q ? nullptr : ws.w_qt;
@@ -503,6 +506,7 @@ static sb_status linear_forward_impl(sb_handle h, const sb_linear_mode* mode, co
     SB_TRY(sb::gemm_fp8(h, xq, ff, ws.x_state, ax, wq, ff, ws.w_state, wx, b, m, n, y, out_dt));
   }
   if (bias) SB_TRYC(op, sb::launch_add_bias(h, y, out_dt, b, m, bias));
+  if (resid) SB_TRYC(op, sb::launch_add_residual(h, y, out_dt, b, m, resid));
   if (ctx) {
     if (md.variant == SB_SWITCHBACK_M) {
       ctx->x_q = ws.x_q;
@@ -537,6 +541,17 @@ sb_status sb_linear_forward_prequant(sb_handle h, const sb_linear_mode* mode, co
       mode->variant == SB_ALLQUANT || mode->exact)
     return sb::fail(SB_ERR_INVALID_ARGUMENT, "linear_forward", "pre-quantized X needs an int8 row-wise variant");
   return linear_forward_impl(h, mode, x, w, bias, dt, b, n, m, y, ctx, workspace, ws_bytes, x_q, x_state);
+}
+
+sb_status sb_linear_forward_residual(sb_handle h, const sb_linear_mode* mode, const void* x, const int8_t* x_q,
+                                     const float* x_state, const void* w, const float* bias, const void* residual,
+                                     sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y, sb_linear_ctx* ctx,
+                                     void* workspace, size_t ws_bytes) {
+  if (!residual) return sb::fail(SB_ERR_INVALID_ARGUMENT, "linear_forward", "null residual");
+  if (x_q && (!x_state || !mode || mode->format != SB_INT8 || mode->variant == SB_STANDARD ||
+              mode->variant == SB_ALLQUANT || mode->exact))
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, "linear_forward", "pre-quantized X needs an int8 row-wise variant");
+  return linear_forward_impl(h, mode, x, w, bias, dt, b, n, m, y, ctx, workspace, ws_bytes, x_q, x_state, residual);
 }
 
 }  // extern "C"

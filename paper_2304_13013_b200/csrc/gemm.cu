@@ -387,7 +387,8 @@ bool encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, 
 }
 
 sb_status gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* qb, const float* sbp, int scale_mode,
-                  int64_t M, int64_t N, int64_t K, void* out, sb_dtype out_dt, int exact, const float* bias) {
+                  int64_t M, int64_t N, int64_t K, void* out, sb_dtype out_dt, int exact, const float* bias,
+                  const void* resid, int64_t ld_resid) {
   const char* op = "int8 matmul";
   const bool raw = scale_mode == SB_SCALE_NONE;
   if (raw && out_dt != SB_I32 && out_dt != SB_I64) return fail(SB_ERR_INVALID_ARGUMENT, op, "raw output needs I32/I64");
@@ -421,12 +422,19 @@ sb_status gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* 
     p.post_scale = 1.0f / 16129.0f;
     p.splits = 1;
     p.bias = (out_mode == sbtc::OUT_BF16 || out_mode == sbtc::OUT_F32) ? bias : nullptr;
+    const bool fuse_resid = resid != nullptr && out_mode == sbtc::OUT_BF16 && aligned(resid, 4) && ld_resid % 2 == 0;
+    p.resid = fuse_resid ? static_cast<const __nv_bfloat16*>(resid) : nullptr;
+    p.ld_resid = ld_resid;
     cudaError_t e;
     const bool col = sb_stride == 1;
     switch (out_mode) {
       case sbtc::OUT_BF16:
-        e = col ? launch_tc<sbtc::KIND_I8, sbtc::OUT_BF16, false, false, true>(h, A, B, td, p, 0)
-                : launch_tc<sbtc::KIND_I8, sbtc::OUT_BF16>(h, A, B, td, p, 0);
+        if (fuse_resid)
+          e = col ? launch_tc<sbtc::KIND_I8, sbtc::OUT_BF16_RESID, false, false, true>(h, A, B, td, p, 0)
+                  : launch_tc<sbtc::KIND_I8, sbtc::OUT_BF16_RESID>(h, A, B, td, p, 0);
+        else
+          e = col ? launch_tc<sbtc::KIND_I8, sbtc::OUT_BF16, false, false, true>(h, A, B, td, p, 0)
+                  : launch_tc<sbtc::KIND_I8, sbtc::OUT_BF16>(h, A, B, td, p, 0);
         break;
       case sbtc::OUT_F32:
         e = col ? launch_tc<sbtc::KIND_I8, sbtc::OUT_F32, false, false, true>(h, A, B, td, p, 0)
@@ -442,6 +450,11 @@ sb_status gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* 
     if (bias && !p.bias) {
       const cudaError_t be = launch_add_bias(h, out, out_dt, M, N, bias);
       if (be != cudaSuccess) return cuda_fail(op, be);
+    }
+    if (resid && !fuse_resid) {
+      if (ld_resid != N) return fail(SB_ERR_UNSUPPORTED, op, "unfused residual must be contiguous");
+      const cudaError_t re = launch_add_residual(h, out, out_dt, M, N, resid);
+      if (re != cudaSuccess) return cuda_fail(op, re);
     }
     return SB_OK;
   }
@@ -461,6 +474,10 @@ sb_status gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* 
     k_gemm_i8_simt<sbtc::OUT_BF16><<<grid, 128, 0, h->stream>>>(qa, sa, sa_stride, qb, sbp, sb_stride, M, N, K, out);
   SB_LAUNCH_CHECK(op);
   if (bias) SB_CUDA_CHECK(op, launch_add_bias(h, out, out_dt, M, N, bias));
+  if (resid) {
+    if (ld_resid != N) return fail(SB_ERR_UNSUPPORTED, op, "unfused residual must be contiguous");
+    SB_CUDA_CHECK(op, launch_add_residual(h, out, out_dt, M, N, resid));
+  }
   return SB_OK;
 }
 

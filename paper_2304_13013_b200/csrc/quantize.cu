@@ -1917,6 +1917,27 @@ __global__ void k_add_bias(T* __restrict__ y, int64_t rows, int64_t cols, const 
   }
 }
 
+template <typename T>
+__global__ void k_add_residual(T* __restrict__ y, int64_t n, const T* __restrict__ r) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[i] = static_cast<T>(__fadd_rn(static_cast<float>(y[i]), static_cast<float>(r[i])));
+}
+
+cudaError_t launch_add_residual(sb_handle h, void* y, sb_dtype dt, int64_t rows, int64_t cols, const void* resid) {
+  const int64_t n = rows * cols;
+  const unsigned grid = grid_for(n, 256 * 4, h->num_sms);
+  h->launches++;
+  if (dt == SB_F32)
+    k_add_residual<<<grid, 256, 0, h->stream>>>(static_cast<float*>(y), n, static_cast<const float*>(resid));
+  else if (dt == SB_BF16)
+    k_add_residual<<<grid, 256, 0, h->stream>>>(static_cast<__nv_bfloat16*>(y), n,
+                                                static_cast<const __nv_bfloat16*>(resid));
+  else
+    return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_add_bias(sb_handle h, void* y, sb_dtype dt, int64_t rows, int64_t cols, const float* bias) {
   const unsigned grid = grid_for(rows * cols, 256 * 4, h->num_sms);
   h->launches++;

@@ -140,6 +140,8 @@ cudaError_t launch_ln_quantize_rowwise(sb_handle h, const void* x, int64_t rows,
 // mode 1 act = a * gelu'(b); writes act and the int8 payload / states of act.
 cudaError_t launch_act_quantize_rowwise(sb_handle h, int mode, const void* a, const void* b, int64_t rows, int64_t cols,
                                         void* act, int8_t* q, float* state);
+// y[r, c] += resid[r, c] in place (y, resid bf16 / fp32 of dt, rows x cols contiguous)
+cudaError_t launch_add_residual(sb_handle h, void* y, sb_dtype dt, int64_t rows, int64_t cols, const void* resid);
 // y[r, c] += bias[c] in place (y is SB_F32 or SB_BF16, rows x cols contiguous)
 cudaError_t launch_add_bias(sb_handle h, void* y, sb_dtype dt, int64_t rows, int64_t cols, const float* bias);
 cudaError_t launch_fp8_cast(sb_handle h, const float* x, int64_t n, int fmt, float* y);
@@ -147,8 +149,10 @@ cudaError_t launch_fp8_cast(sb_handle h, const float* x, int64_t n, int fmt, flo
 // gemm_i8.cu
 // bias (optional, fp32 [N]): fused into the tensor-core epilogue for bf16 / fp32 outputs,
 // otherwise added by launch_add_bias after the product.
+// resid (optional, bf16 [M x N], row stride ld_resid; bf16 output only): added in the epilogue.
 sb_status gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* qb, const float* sb, int scale_mode,
-                  int64_t M, int64_t N, int64_t K, void* out, sb_dtype out_dt, int exact, const float* bias = nullptr);
+                  int64_t M, int64_t N, int64_t K, void* out, sb_dtype out_dt, int exact, const float* bias = nullptr,
+                  const void* resid = nullptr, int64_t ld_resid = 0);
 // gemm_bf16.cu
 sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m, int64_t n, float* dw,
                 int exact, int accumulate);

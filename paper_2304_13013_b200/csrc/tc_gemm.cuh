@@ -35,7 +35,8 @@ enum Out {
   OUT_F32_EXACT = 2,  // float(double(acc) * sa_i * sb_j / 16129.0)  (linear.cpp:49), int8 only
   OUT_I32 = 3,        // raw s32 accumulators
   OUT_F32_RAW = 4,    // raw f32 accumulators (dW), TMA store
-  OUT_F32_RAW_ADD = 5 // raw f32 accumulators added into D (TMA reduce-add)
+  OUT_F32_RAW_ADD = 5, // raw f32 accumulators added into D (TMA reduce-add)
+  OUT_BF16_RESID = 6   // scaled, + bias, + a bf16 residual tile (p.resid), rounded once to bf16
 };
 
 constexpr int BM = 128;
@@ -64,6 +65,8 @@ struct Params {
   int m_fast;              // raster: 1 = consecutive tiles walk M (B tile reused), 0 = walk N (A reused)
   int tma3d;               // 2-CTA K-major operands as 3D maps (byte-in-atom, row, atom): bit 0 A, bit 1 B
   const float* bias;       // optional per-output-column bias (OUT_BF16 / OUT_F32): y = fl(acc * scale) + bias
+  const __nv_bfloat16* resid;  // OUT_BF16_RESID: residual [M x N] (row stride ld_resid) added in the epilogue
+  int64_t ld_resid;
 };
 
 // Column bias for the epilogue: 0 outside D or without a bias (warp-uniform address: one
@@ -200,8 +203,10 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
     const int cl = half * 128 + pr * 64;  // column within tile
     const int col0 = n0 + cl;
     if (col0 >= p.N || rm0 >= p.M) continue;  // whole pair outside D (warp-uniform)
-    if (OUT == OUT_BF16) {
+    if (OUT == OUT_BF16 || OUT == OUT_BF16_RESID) {
       uint32_t w[32];
+      const int64_t rrow = static_cast<int64_t>(rm0) + ew * 32 + lane;  // this lane's output row
+      const __nv_bfloat16* rp = (OUT == OUT_BF16_RESID && rrow < p.M) ? p.resid + rrow * p.ld_resid : nullptr;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         float a0, a1, b0, b1;
@@ -232,6 +237,18 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
           a1 = __fadd_rn(a1, col_bias(p, col0 + 2 * j + 1));
           b0 = __fadd_rn(b0, col_bias(p, col0 + 32 + 2 * j));
           b1 = __fadd_rn(b1, col_bias(p, col0 + 32 + 2 * j + 1));
+        }
+        if (OUT == OUT_BF16_RESID && rp != nullptr) {  // residual added before the single rounding
+          if (col0 + 2 * j < p.N) {
+            const float2 ra = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(rp + col0 + 2 * j));
+            a0 = __fadd_rn(a0, ra.x);
+            a1 = __fadd_rn(a1, ra.y);
+          }
+          if (col0 + 32 + 2 * j < p.N) {
+            const float2 rb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(rp + col0 + 32 + 2 * j));
+            b0 = __fadd_rn(b0, rb.x);
+            b1 = __fadd_rn(b1, rb.y);
+          }
         }
         w[j] = pack_bf16x2(a0, a1);
         w[16 + j] = pack_bf16x2(b0, b1);
@@ -421,7 +438,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
-    constexpr bool SCALED = OUT == OUT_BF16 || OUT == OUT_F32 || OUT == OUT_F32_EXACT;
+    constexpr bool SCALED = OUT == OUT_BF16 || OUT == OUT_BF16_RESID || OUT == OUT_F32 || OUT == OUT_F32_EXACT;
     const int ew = warp & 3;               // TMEM lane quarter this warp may access
     const int half = (warp - 4) >> 2;      // column half of the tile
     const int ei = threadIdx.x - 128;      // 0..255 within the epilogue group

@@ -295,7 +295,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue (both CTAs)
-    constexpr bool SCALED = OUT == OUT_BF16 || OUT == OUT_F32 || OUT == OUT_F32_EXACT;
+    constexpr bool SCALED = OUT == OUT_BF16 || OUT == OUT_BF16_RESID || OUT == OUT_F32 || OUT == OUT_F32_EXACT;
     const int ew = warp & 3;
     const int half = (warp - 4) >> 2;
     const int ei = threadIdx.x - 128;

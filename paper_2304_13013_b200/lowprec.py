@@ -381,7 +381,8 @@ def _workspace(mode: LinearMode, b: int, n: int, m: int, device) -> torch.Tensor
 
 def linear_forward(mode: LinearMode, x: torch.Tensor, w: torch.Tensor, ctx: LinearContext | None = None,
                    workspace: torch.Tensor | None = None, check: bool = True,
-                   bias: torch.Tensor | None = None, x_q: QuantizedMatrix | None = None) -> torch.Tensor:
+                   bias: torch.Tensor | None = None, x_q: QuantizedMatrix | None = None,
+                   residual: torch.Tensor | None = None) -> torch.Tensor:
     """linear.cpp:113-164: Y = X W^T through the variant's quantized path. `bias` (fp32, m)
     is optional and fused into the GEMM epilogue (sb_linear_forward_bias). `x_q`: X already
     quantized row-wise by its producer (gelu_quantize_rowwise), skipping that pass."""
@@ -400,7 +401,18 @@ def linear_forward(mode: LinearMode, x: torch.Tensor, w: torch.Tensor, ctx: Line
     y = torch.empty((b, m), dtype=x.dtype, device=x.device)
     h = A.handle(x.device.index)
     raw = A.LinearCtx()
-    if x_q is not None:
+    if residual is not None:
+        if residual.shape != (b, m) or residual.dtype != x.dtype or not residual.is_cuda:
+            raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "linear_forward: residual must be b x m of X's dtype")
+        residual = residual.contiguous()
+        if bias is not None:
+            if bias.dtype != torch.float32 or bias.shape != (m,) or not bias.is_cuda:
+                raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "linear_forward: bias must be fp32 of shape (m,)")
+            bias = bias.contiguous()
+        st = h.lib.sb_linear_forward_residual(h.h, C.byref(mode.c()), _p(x), _p(x_q.payload if x_q else None),
+                                              _p(x_q.state if x_q else None), _p(w), _p(bias), _p(residual), _dt(x),
+                                              b, n, m, _p(y), C.byref(raw), _p(workspace), workspace.numel())
+    elif x_q is not None:
         bp = None
         if bias is not None:
             if bias.dtype != torch.float32 or bias.shape != (m,) or not bias.is_cuda:

@@ -24,11 +24,13 @@ _VARIANTS = {"switchback": A.SB_SWITCHBACK, "switchback_m": A.SB_SWITCHBACK_M, "
 
 class _SwitchBackLinearFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x2d: torch.Tensor, weight: torch.Tensor, bias, mode: L.LinearMode):
+    def forward(ctx, x2d: torch.Tensor, weight: torch.Tensor, bias, mode: L.LinearMode, resid=None):
         w = weight.detach().to(x2d.dtype).contiguous()
         lctx = L.LinearContext()
         b = bias.detach().float() if bias is not None else None
-        y = L.linear_forward(mode, x2d.contiguous(), w, lctx, check=False, bias=b)  # bias fused in the epilogue
+        # bias (and the residual, if any) fused in the GEMM epilogue
+        y = L.linear_forward(mode, x2d.contiguous(), w, lctx, check=False, bias=b,
+                             residual=resid.detach() if resid is not None else None)
         ctx.lctx = lctx
         ctx.mode = mode
         ctx.has_bias = bias is not None
@@ -42,7 +44,7 @@ class _SwitchBackLinearFn(torch.autograd.Function):
         db = g.sum(0, dtype=torch.float32) if ctx.has_bias and ctx.needs_input_grad[2] else None
         ctx.lctx = None
         ctx.keep_w = None
-        return dx, dw, db, None
+        return dx, dw, db, None, (g if ctx.needs_input_grad[4] else None)
 
 
 class SwitchBackLinear(torch.nn.Module):
@@ -61,21 +63,23 @@ class SwitchBackLinear(torch.nn.Module):
         self.weight = torch.nn.Parameter(torch.randn(out_features, in_features, device=dev) * in_features ** -0.5)
         self.bias = torch.nn.Parameter(torch.zeros(out_features, device=dev)) if bias else None
 
-    def forward(self, x: torch.Tensor) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, residual: torch.Tensor | None = None) -> torch.Tensor:
+        """y = x W^T + b (+ residual, added in the GEMM epilogue: the block's skip connection)."""
         shape = x.shape
         x2d = x.reshape(-1, self.in_features)
+        r2d = residual.reshape(-1, self.out_features) if residual is not None else None
         fusable = self.mode.format == A.SB_INT8 and self.mode.variant in (A.SB_SWITCHBACK, A.SB_SWITCHBACK_M,
                                                                           A.SB_SWITCHBACK_Q)
         if self.norm is not None and fusable:
             if x.dtype != torch.bfloat16:
                 raise TypeError("prenorm SwitchBackLinear runs in bf16")
             y = _LNLinearFn.apply(x2d, self.norm.weight, self.norm.bias, self.norm.eps, self.weight, self.bias,
-                                  self.mode)
+                                  self.mode, r2d)
         elif self.norm is not None:  # fp8 / tensor-wise X: LayerNorm unfused, then the layer
             h = self.norm(x2d.float()).to(x2d.dtype)
-            y = _SwitchBackLinearFn.apply(h, self.weight, self.bias, self.mode)
+            y = _SwitchBackLinearFn.apply(h, self.weight, self.bias, self.mode, r2d)
         else:
-            y = _SwitchBackLinearFn.apply(x2d, self.weight, self.bias, self.mode)
+            y = _SwitchBackLinearFn.apply(x2d, self.weight, self.bias, self.mode, r2d)
         return y.reshape(*shape[:-1], self.out_features)
 
     def extra_repr(self) -> str:
@@ -100,13 +104,13 @@ class _LNLinearFn(torch.autograd.Function):
     quantization of the linear's input (sb_layernorm_quantize_rowwise + prequantized forward)."""
 
     @staticmethod
-    def forward(ctx, x2d, ln_w, ln_b, eps: float, weight, bias, mode: L.LinearMode):
+    def forward(ctx, x2d, ln_w, ln_b, eps: float, weight, bias, mode: L.LinearMode, resid=None):
         x2d = x2d.contiguous()
         h, hq, mean, rstd = L.layernorm_quantize_rowwise(x2d, ln_w.detach(), ln_b.detach(), eps, check=False)
         w = weight.detach().to(x2d.dtype).contiguous()
         lctx = L.LinearContext()
         y = L.linear_forward(mode, h, w, lctx, check=False, bias=bias.detach().float() if bias is not None else None,
-                             x_q=hq)
+                             x_q=hq, residual=resid.detach() if resid is not None else None)
         ctx.state = (x2d, mean, rstd, lctx, w)
         ctx.ln = (ln_w, ln_b)
         ctx.mode = mode
@@ -121,7 +125,7 @@ class _LNLinearFn(torch.autograd.Function):
         db = g.sum(0, dtype=torch.float32) if ctx.has_bias and ctx.needs_input_grad[5] else None
         dx, dg, dbeta = _ln_backward(dh, x2d, mean, rstd, *ctx.ln, ctx.needs_input_grad[:3])
         ctx.state = None
-        return dx, dg, dbeta, None, dw, db, None
+        return dx, dg, dbeta, None, dw, db, None, (g if ctx.needs_input_grad[7] else None)
 
 
 class _SwitchBackMLPFn(torch.autograd.Function):
@@ -131,7 +135,7 @@ class _SwitchBackMLPFn(torch.autograd.Function):
     activation is re-read just to be quantized."""
 
     @staticmethod
-    def forward(ctx, x2d, ln_w, ln_b, eps, w1, b1, w2, b2, mode: L.LinearMode):
+    def forward(ctx, x2d, ln_w, ln_b, eps, w1, b1, w2, b2, mode: L.LinearMode, resid=None):
         dt = x2d.dtype
         x2d = x2d.contiguous()
         w1b, w2b = w1.detach().to(dt).contiguous(), w2.detach().to(dt).contiguous()
@@ -146,7 +150,7 @@ class _SwitchBackMLPFn(torch.autograd.Function):
                                x_q=hq)
         act, act_q = L.gelu_quantize_rowwise(pre, check=False)
         y = L.linear_forward(mode, act, w2b, c2, check=False, bias=b2.detach().float() if b2 is not None else None,
-                             x_q=act_q)
+                             x_q=act_q, residual=resid.detach() if resid is not None else None)
         ctx.state = (c1, c2, pre, w1b, w2b, h, hq, ln_state)
         ctx.ln = (ln_w, ln_b)
         ctx.mode = mode
@@ -167,7 +171,7 @@ class _SwitchBackMLPFn(torch.autograd.Function):
             x2d, mean, rstd = ln_state
             dx, dg, dbeta = _ln_backward(dx, x2d, mean, rstd, *ctx.ln, ctx.needs_input_grad[:3])
         ctx.state = None
-        return dx, dg, dbeta, None, dw1, db1, dw2, db2, None
+        return dx, dg, dbeta, None, dw1, db1, dw2, db2, None, (gy if ctx.needs_input_grad[9] else None)
 
 
 class SwitchBackMLP(torch.nn.Module):
@@ -185,12 +189,14 @@ class SwitchBackMLP(torch.nn.Module):
         if variant not in ("switchback", "switchback_m", "switchback_q"):
             raise ValueError("SwitchBackMLP needs an int8 row-wise variant")
 
-    def forward(self, x: torch.Tensor) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, residual: torch.Tensor | None = None) -> torch.Tensor:
+        """fc2(gelu(fc1(norm(x)))) (+ residual, added in fc2's GEMM epilogue)."""
         if x.dtype != torch.bfloat16:
             raise TypeError("SwitchBackMLP runs in bf16")
         shape = x.shape
         n = self.norm
+        r2d = residual.reshape(-1, self.fc2.out_features) if residual is not None else None
         y = _SwitchBackMLPFn.apply(x.reshape(-1, self.fc1.in_features), n.weight if n is not None else None,
                                    n.bias if n is not None else None, n.eps if n is not None else 0.0,
-                                   self.fc1.weight, self.fc1.bias, self.fc2.weight, self.fc2.bias, self.fc1.mode)
+                                   self.fc1.weight, self.fc1.bias, self.fc2.weight, self.fc2.bias, self.fc1.mode, r2d)
         return y.reshape(*shape[:-1], self.fc2.out_features)

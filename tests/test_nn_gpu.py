@@ -260,3 +260,21 @@ def test_linear_module_variants(variant, fmt):
     tol = 8e-2 if fmt == "fp8" else 3e-2
     assert rel(y, yr) < tol and rel(x.grad, xr.grad) < tol
     assert rel(mod.weight.grad, ps["weight"].grad) < tol
+
+
+def test_residual_in_epilogue_modules():
+    """SwitchBackLinear / SwitchBackMLP with residual=: the skip connection added in the GEMM
+    epilogue, and its gradient passed straight through."""
+    from paper_2304_13013_b200.nn import SwitchBackLinear, SwitchBackMLP
+
+    torch.manual_seed(12)
+    F = torch.nn.functional
+    for mod in (SwitchBackLinear(256, 256), SwitchBackMLP(256, 512, prenorm=True)):
+        x = torch.randn(500, 256, device="cuda").bfloat16().requires_grad_(True)
+        r = torch.randn(500, 256, device="cuda").bfloat16().requires_grad_(True)
+        y = mod(x, residual=r)
+        y0 = mod(x) + r
+        assert rel(y, y0) < 1e-2
+        g = torch.randn_like(y)
+        y.backward(g)
+        assert torch.equal(r.grad, g)
