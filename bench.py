@@ -564,8 +564,8 @@ def run_vit_block(args):
     torch.cuda.set_device(dev)
     B, S, D, H = 256, 257, 1280, 16
     fused = not args.no_overlap  # --no-overlap also turns the LayerNorm / GELU producer fusions off (A/B)
-    # residual adds in the GEMM epilogues: SB_BLOCK_RESID=1 (measured slower, 8.20 vs 7.95 ms: the
-    # epilogue reads the residual with per-row 4-byte loads; a TMA-staged residual tile is the fix)
+    # residual adds in the GEMM epilogues: SB_BLOCK_RESID=1 (measured slightly slower, 8.10-8.16 vs
+    # 8.02-8.05 ms: the epilogue-heavy out-proj / fc2 GEMMs pay more for the extra reads)
     resid_fused = os.environ.get("SB_BLOCK_RESID", "0") == "1"
     T = B * S
 

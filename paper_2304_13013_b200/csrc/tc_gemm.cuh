@@ -205,8 +205,22 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
     if (col0 >= p.N || rm0 >= p.M) continue;  // whole pair outside D (warp-uniform)
     if (OUT == OUT_BF16 || OUT == OUT_BF16_RESID) {
       uint32_t w[32];
-      const int64_t rrow = static_cast<int64_t>(rm0) + ew * 32 + lane;  // this lane's output row
-      const __nv_bfloat16* rp = (OUT == OUT_BF16_RESID && rrow < p.M) ? p.resid + rrow * p.ld_resid : nullptr;
+      if (OUT == OUT_BF16_RESID) {
+        // stage the warp's 32 x 64 residual tile in buf with coalesced 16-byte loads (8 lanes per
+        // 128-byte row), in the same SW128 layout stage_row128 uses; each lane then reads its row
+        if (lane == 0) sbptx::tma_store_wait_read<0>();  // previous store done reading buf
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int rr = t * 4 + (lane >> 3), c = lane & 7;
+          const int64_t grow = static_cast<int64_t>(rm0) + ew * 32 + rr;
+          uint4 v = make_uint4(0, 0, 0, 0);
+          if (grow < p.M && col0 + 8 * c < p.N)
+            v = __ldg(reinterpret_cast<const uint4*>(p.resid + grow * p.ld_resid + col0 + 8 * c));
+          *reinterpret_cast<uint4*>(buf + rr * 128 + ((c ^ (rr & 7)) * 16)) = v;
+        }
+        __syncwarp();
+      }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         float a0, a1, b0, b1;
@@ -238,23 +252,26 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
           b0 = __fadd_rn(b0, col_bias(p, col0 + 32 + 2 * j));
           b1 = __fadd_rn(b1, col_bias(p, col0 + 32 + 2 * j + 1));
         }
-        if (OUT == OUT_BF16_RESID && rp != nullptr) {  // residual added before the single rounding
-          if (col0 + 2 * j < p.N) {
-            const float2 ra = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(rp + col0 + 2 * j));
-            a0 = __fadd_rn(a0, ra.x);
-            a1 = __fadd_rn(a1, ra.y);
-          }
-          if (col0 + 32 + 2 * j < p.N) {
-            const float2 rb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(rp + col0 + 32 + 2 * j));
-            b0 = __fadd_rn(b0, rb.x);
-            b1 = __fadd_rn(b1, rb.y);
-          }
+        if (OUT == OUT_BF16_RESID) {  // residual added before the single rounding
+          // columns 2j, 2j+1 live in chunk j/4 (a) and 4 + j/4 (b) of this lane's staged row
+          const uint32_t ra = *reinterpret_cast<const uint32_t*>(buf + lane * 128 + (((j >> 2) ^ (lane & 7)) * 16) +
+                                                                 (j & 3) * 4);
+          const uint32_t rb = *reinterpret_cast<const uint32_t*>(
+              buf + lane * 128 + (((4 + (j >> 2)) ^ (lane & 7)) * 16) + (j & 3) * 4);
+          const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ra));
+          const float2 fb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rb));
+          a0 = __fadd_rn(a0, fa.x);
+          a1 = __fadd_rn(a1, fa.y);
+          b0 = __fadd_rn(b0, fb.x);
+          b1 = __fadd_rn(b1, fb.y);
         }
         w[j] = pack_bf16x2(a0, a1);
         w[16 + j] = pack_bf16x2(b0, b1);
       }
-      if (lane == 0) sbptx::tma_store_wait_read<0>();  // previous store done reading buf
-      __syncwarp();
+      if (OUT != OUT_BF16_RESID) {
+        if (lane == 0) sbptx::tma_store_wait_read<0>();  // previous store done reading buf
+      }
+      __syncwarp();  // (RESID: every lane has read its residual row before buf is overwritten)
       stage_row128(buf, lane, w);  // 64 bf16 = 128 B per row
       sbptx::fence_proxy_async_smem();
       __syncwarp();
