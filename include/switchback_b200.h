@@ -203,6 +203,18 @@ typedef struct sb_linear_ctx {
 /* Workspace the forward+backward pair needs (caller allocates once, reuses). */
 sb_status sb_linear_workspace_size(const sb_linear_mode* mode, int64_t b, int64_t n, int64_t m, size_t* bytes);
 
+/* Byte offsets, inside a linear workspace, of the quantized operands the layer writes there
+ * (the reference's QuantizedMatrix temporaries, linear.cpp:134 / :234-235): X's row-wise
+ * payload [b x n] and states [b]; W's payload [m x n] (tensor-wise, or row-wise for
+ * SwitchBackQ) and its transpose [n x m]; W's state(s); G's row-wise payload [b x m] and
+ * states [b] (written by sb_linear_backward unless G came prequantized). Lets a caller (or a
+ * parity test) read the layer's own int8 operands without re-quantizing. */
+typedef struct sb_linear_ws_layout {
+  size_t x_q, x_state, w_q, w_q_t, w_state, g_q, g_state, total;
+} sb_linear_ws_layout;
+sb_status sb_linear_workspace_layout(const sb_linear_mode* mode, int64_t b, int64_t n, int64_t m,
+                                     sb_linear_ws_layout* out);
+
 /* linear_forward, linear.hpp:62-63 / linear.cpp:113-164: y[b x m] = X W^T through the
  * variant's quantized path. x/w/y are `dt` (SB_F32 or SB_BF16). ctx may be NULL. */
 sb_status sb_linear_forward(sb_handle h, const sb_linear_mode* mode, const void* x, const void* w, sb_dtype dt,

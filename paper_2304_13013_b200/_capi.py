@@ -29,7 +29,7 @@ EXPORTS = [
     "sb_abi_version", "sb_create", "sb_destroy", "sb_set_stream", "sb_synchronize", "sb_error_word",
     "sb_last_error", "sb_launch_count", "sb_quantize_rowwise", "sb_quantize_columnwise",
     "sb_quantize_tensorwise", "sb_dequantize", "sb_quantize_fp8", "sb_dequantize_fp8", "sb_gemm_i8",
-    "sb_matmul_f32", "sb_wgrad", "sb_gemm_fp8", "sb_linear_workspace_size", "sb_linear_forward", "sb_linear_forward_bias",
+    "sb_matmul_f32", "sb_wgrad", "sb_gemm_fp8", "sb_linear_workspace_size", "sb_linear_workspace_layout", "sb_linear_forward", "sb_linear_forward_bias",
     "sb_linear_forward_prequant", "sb_linear_backward_prequant", "sb_gelu_quantize_rowwise", "sb_linear_forward_residual",
     "sb_gelu_backward_quantize_rowwise", "sb_layernorm_quantize_rowwise", "sb_layernorm_backward_workspace_size",
     "sb_layernorm_backward",
@@ -63,6 +63,10 @@ class LinearCtx(C.Structure):
                 ("x", C.c_void_p), ("w", C.c_void_p), ("w_q_t", C.c_void_p), ("w_state", C.c_void_p),
                 ("x_q", C.c_void_p), ("x_state", C.c_void_p), ("workspace", C.c_void_p),
                 ("workspace_bytes", C.c_size_t), ("valid", C.c_int32)]
+
+
+class LinearWsLayout(C.Structure):
+    _fields_ = [(f, C.c_size_t) for f in ("x_q", "x_state", "w_q", "w_q_t", "w_state", "g_q", "g_state", "total")]
 
 
 class AdamwTensor(C.Structure):
@@ -114,6 +118,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             "sb_wgrad": ([v, v, v, i32, i64, i64, i64, v, i32, i32], i32),
             "sb_gemm_fp8": ([v, v, i32, v, i32, v, i32, v, i32, i64, i64, i64, v, i32], i32),
             "sb_linear_workspace_size": ([C.POINTER(LinearMode), i64, i64, i64, C.POINTER(sz)], i32),
+            "sb_linear_workspace_layout": ([C.POINTER(LinearMode), i64, i64, i64, C.POINTER(LinearWsLayout)], i32),
             "sb_linear_forward": ([v, C.POINTER(LinearMode), v, v, i32, i64, i64, i64, v, C.POINTER(LinearCtx), v, sz],
                                   i32),
             "sb_linear_forward_bias": ([v, C.POINTER(LinearMode), v, v, v, i32, i64, i64, i64, v, C.POINTER(LinearCtx), v,

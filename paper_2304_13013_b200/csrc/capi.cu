@@ -57,7 +57,8 @@ struct Carve {
   template <typename T>
   T* take(size_t count) {
     off = (off + 255) & ~size_t(255);
-    T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+    // a null base yields the offsets themselves (sb_linear_workspace_size / _layout)
+    T* p = reinterpret_cast<T*>(reinterpret_cast<uintptr_t>(base) + off);
     off += count * sizeof(T);
     return p;
   }
@@ -402,6 +403,24 @@ sb_status sb_linear_workspace_size(const sb_linear_mode* mode, int64_t b, int64_
   if (!mode || !bytes || b < 0 || n < 0 || m < 0)
     return sb::fail(SB_ERR_INVALID_ARGUMENT, "linear_forward", "bad argument");
   *bytes = carve(*mode, b, n, m, SB_F32, nullptr).total;
+  return SB_OK;
+}
+
+sb_status sb_linear_workspace_layout(const sb_linear_mode* mode, int64_t b, int64_t n, int64_t m,
+                                     sb_linear_ws_layout* out) {
+  if (!mode || !out || b < 0 || n < 0 || m < 0)
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, "linear_forward", "bad argument");
+  // the operand offsets do not depend on dt
+  const LinearWs w = carve(*mode, b, n, m, SB_F32, nullptr);
+  auto off = [](const void* p) { return static_cast<size_t>(reinterpret_cast<uintptr_t>(p)); };
+  out->x_q = off(w.x_q);
+  out->x_state = off(w.x_state);
+  out->w_q = off(w.w_q);
+  out->w_q_t = off(w.w_qt);
+  out->w_state = off(w.w_state);
+  out->g_q = off(w.g_q);
+  out->g_state = off(w.g_state);
+  out->total = w.total;
   return SB_OK;
 }
 

@@ -26,33 +26,95 @@ namespace {
 constexpr int64_t kInt32SafeInner = 2147483647LL / (127 * 127);  // 133144, linear.cpp:37
 
 // ----------------------------------------------------------- SIMT int8 ----
+// Fallback for operands the TMA path cannot take (K % 16 != 0, unaligned rows) and for
+// K > 133144, where the reference switches to an int64 accumulator (linear.cpp:62-65).
+// 64 x 64 outputs per block, 4 x 4 per thread; K tiles of 64 bytes staged in smem as packed
+// 4-byte words so each step is one dp4a per output. A tile's partial sum is at most
+// 64 * 127^2 < 2^31 in int32; tiles accumulate in int64, so the result is the exact integer
+// product for any K. Rows go on grid.y in steps of gridDim.y (no 65535-row limit).
+constexpr int kSimtTile = 64, kSimtKw = 16;  // 16 words = 64 bytes of K per tile
+
+__device__ __forceinline__ int load_word(const int8_t* __restrict__ row, int64_t k, int64_t K) {
+  uint32_t v = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+    if (k + b < K) v |= static_cast<uint32_t>(static_cast<uint8_t>(row[k + b])) << (8 * b);
+  return static_cast<int>(v);
+}
+
 template <int OUT>
-__global__ void k_gemm_i8_simt(const int8_t* __restrict__ qa, const float* __restrict__ sa, int sa_stride,
-                               const int8_t* __restrict__ qb, const float* __restrict__ sb, int sb_stride, int64_t M,
-                               int64_t N, int64_t K, void* __restrict__ out) {
-  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t i = blockIdx.y;
-  if (j >= N) return;
-  const int8_t* a = qa + i * K;
-  const int8_t* b = qb + j * K;
-  int64_t acc = 0;
-  for (int64_t p = 0; p < K; ++p) acc += static_cast<int64_t>(a[p]) * static_cast<int64_t>(b[p]);
-  const int64_t o = i * N + j;
-  if (OUT == 5) {  // raw int64
-    static_cast<int64_t*>(out)[o] = acc;
-  } else if (OUT == sbtc::OUT_I32) {
-    static_cast<int32_t*>(out)[o] = static_cast<int32_t>(acc);
-  } else {
-    const double d = __ddiv_rn(__dmul_rn(__dmul_rn(static_cast<double>(acc), static_cast<double>(sa[sa_stride ? i : 0])),
-                                         static_cast<double>(sb[sb_stride ? j : 0])),
-                               16129.0);
-    if (OUT == sbtc::OUT_F32_EXACT)
-      static_cast<float*>(out)[o] = __double2float_rn(d);
-    else if (OUT == sbtc::OUT_F32)
-      static_cast<float*>(out)[o] = static_cast<float>(acc) * (sa[sa_stride ? i : 0] / 16129.0f) * sb[sb_stride ? j : 0];
-    else
-      static_cast<__nv_bfloat16*>(out)[o] =
-          __float2bfloat16_rn(static_cast<float>(acc) * (sa[sa_stride ? i : 0] / 16129.0f) * sb[sb_stride ? j : 0]);
+__global__ void __launch_bounds__(256) k_gemm_i8_simt(const int8_t* __restrict__ qa, const float* __restrict__ sa,
+                                                      int sa_stride, const int8_t* __restrict__ qb,
+                                                      const float* __restrict__ sb, int sb_stride, int64_t M,
+                                                      int64_t N, int64_t K, void* __restrict__ out) {
+  __shared__ int As[kSimtKw][kSimtTile + 1];
+  __shared__ int Bs[kSimtKw][kSimtTile + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * kSimtTile;
+  for (int64_t i0 = static_cast<int64_t>(blockIdx.y) * kSimtTile; i0 < M; i0 += static_cast<int64_t>(gridDim.y) * kSimtTile) {
+    int64_t acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[u][v] = 0;
+    for (int64_t k0 = 0; k0 < K; k0 += 4 * kSimtKw) {
+      for (int e = threadIdx.x; e < kSimtKw * kSimtTile; e += 256) {
+        const int kw = e / kSimtTile, rr = e % kSimtTile;
+        const int64_t ia = i0 + rr, jb = j0 + rr, kg = k0 + 4 * kw;
+        As[kw][rr] = (ia < M && kg < K) ? load_word(qa + ia * K, kg, K) : 0;
+        Bs[kw][rr] = (jb < N && kg < K) ? load_word(qb + jb * K, kg, K) : 0;
+      }
+      __syncthreads();
+      int part[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) part[u][v] = 0;
+#pragma unroll 4
+      for (int kw = 0; kw < kSimtKw; ++kw) {
+        int av[4], bv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) av[u] = As[kw][ty * 4 + u];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) bv[v] = Bs[kw][tx * 4 + v];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) part[u][v] = __dp4a(av[u], bv[v], part[u][v]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] += part[u][v];
+      __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + ty * 4 + u;
+      if (i >= M) continue;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int64_t j = j0 + tx * 4 + v;
+        if (j >= N) continue;
+        const int64_t o = i * N + j;
+        const int64_t a = acc[u][v];
+        if (OUT == 5) {  // raw int64
+          static_cast<int64_t*>(out)[o] = a;
+        } else if (OUT == sbtc::OUT_I32) {
+          static_cast<int32_t*>(out)[o] = static_cast<int32_t>(a);
+        } else {
+          const float si = sa[sa_stride ? i : 0], sj = sb[sb_stride ? j : 0];
+          if (OUT == sbtc::OUT_F32_EXACT)  // linear.cpp:49, left to right in double
+            static_cast<float*>(out)[o] = __double2float_rn(
+                __ddiv_rn(__dmul_rn(__dmul_rn(static_cast<double>(a), static_cast<double>(si)), static_cast<double>(sj)),
+                          16129.0));
+          else if (OUT == sbtc::OUT_F32)
+            static_cast<float*>(out)[o] = static_cast<float>(a) * (si / 16129.0f) * sj;
+          else
+            static_cast<__nv_bfloat16*>(out)[o] = __float2bfloat16_rn(static_cast<float>(a) * (si / 16129.0f) * sj);
+        }
+      }
+    }
   }
 }
 
@@ -126,15 +188,16 @@ __global__ void k_gemm_fp8_simt(const uint8_t* __restrict__ qa, int fa, const fl
                                 const uint8_t* __restrict__ qb, int fb, const float* __restrict__ sb, int sb_stride,
                                 int64_t M, int64_t N, int64_t K, void* __restrict__ out, int out_bf16) {
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t i = blockIdx.y;
   if (j >= N) return;
-  float acc = 0.0f;
-  for (int64_t p = 0; p < K; ++p) acc = fmaf(dec_fp8(qa[i * K + p], fa), dec_fp8(qb[j * K + p], fb), acc);
-  const float y = acc * sa[sa_stride ? i : 0] * sb[sb_stride ? j : 0];
-  if (out_bf16)
-    static_cast<__nv_bfloat16*>(out)[i * N + j] = __float2bfloat16_rn(y);
-  else
-    static_cast<float*>(out)[i * N + j] = y;
+  for (int64_t i = blockIdx.y; i < M; i += gridDim.y) {  // no 65535-row grid limit
+    float acc = 0.0f;
+    for (int64_t p = 0; p < K; ++p) acc = fmaf(dec_fp8(qa[i * K + p], fa), dec_fp8(qb[j * K + p], fb), acc);
+    const float y = acc * sa[sa_stride ? i : 0] * sb[sb_stride ? j : 0];
+    if (out_bf16)
+      static_cast<__nv_bfloat16*>(out)[i * N + j] = __float2bfloat16_rn(y);
+    else
+      static_cast<float*>(out)[i * N + j] = y;
+  }
 }
 
 // ------------------------------------------------------------ TMA maps ----
@@ -374,6 +437,26 @@ bool out_tmap(CUtensorMap* m, sb_dtype dt, void* out, int64_t M, int64_t N) {
 
 namespace sb {
 
+// The tensor-core GEMMs need TMA-legal operands (K % 16 == 0 for int8 / fp8, 16-byte aligned
+// rows and bases). Anything else runs on the tiled SIMT kernels above, one to two orders of
+// magnitude slower: say so once per process on stderr, and refuse outright when
+// SB_STRICT_TC=1 (for callers that want a hard guarantee that the tcgen05 path ran).
+sb_status simt_fallback(sb_handle h, const char* op, int64_t M, int64_t N, int64_t K) {
+  static int strict = -1;
+  if (strict < 0) strict = getenv("SB_STRICT_TC") ? atoi(getenv("SB_STRICT_TC")) : 0;
+  if (strict)
+    return fail(SB_ERR_UNSUPPORTED, op, "operands are not TMA-legal (K % 16, alignment); SB_STRICT_TC=1 forbids the SIMT path");
+  static std::once_flag warned;
+  std::call_once(warned, [&] {
+    fprintf(stderr,
+            "switchback_b200: %s %lldx%lldx%lld is not TMA-legal (needs K %% 16 == 0 and 16-byte aligned rows): "
+            "running the SIMT fallback, much slower than tcgen05 (warned once; SB_STRICT_TC=1 makes it an error)\n",
+            op, static_cast<long long>(M), static_cast<long long>(N), static_cast<long long>(K));
+  });
+  (void)h;
+  return SB_OK;
+}
+
 bool encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer,
                     uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz) {
   EncodeFn fn = get_encode();
@@ -459,19 +542,24 @@ sb_status gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* 
     return SB_OK;
   }
   // SIMT path (unaligned / tiny / int64 accumulation)
-  const dim3 grid(static_cast<unsigned>((N + 127) / 128), static_cast<unsigned>(M));
+  if (K <= kInt32SafeInner) {
+    const sb_status fs = simt_fallback(h, op, M, N, K);
+    if (fs != SB_OK) return fs;
+  }
+  const dim3 grid(static_cast<unsigned>((N + kSimtTile - 1) / kSimtTile),
+                  static_cast<unsigned>(std::min<int64_t>((M + kSimtTile - 1) / kSimtTile, 65535)));
   h->launches++;
   if (out_dt == SB_I64)
-    k_gemm_i8_simt<5><<<grid, 128, 0, h->stream>>>(qa, sa, sa_stride, qb, sbp, sb_stride, M, N, K, out);
+    k_gemm_i8_simt<5><<<grid, 256, 0, h->stream>>>(qa, sa, sa_stride, qb, sbp, sb_stride, M, N, K, out);
   else if (out_mode == sbtc::OUT_I32)
-    k_gemm_i8_simt<sbtc::OUT_I32><<<grid, 128, 0, h->stream>>>(qa, sa, sa_stride, qb, sbp, sb_stride, M, N, K, out);
+    k_gemm_i8_simt<sbtc::OUT_I32><<<grid, 256, 0, h->stream>>>(qa, sa, sa_stride, qb, sbp, sb_stride, M, N, K, out);
   else if (out_mode == sbtc::OUT_F32_EXACT)
-    k_gemm_i8_simt<sbtc::OUT_F32_EXACT><<<grid, 128, 0, h->stream>>>(qa, sa, sa_stride, qb, sbp, sb_stride, M, N, K,
+    k_gemm_i8_simt<sbtc::OUT_F32_EXACT><<<grid, 256, 0, h->stream>>>(qa, sa, sa_stride, qb, sbp, sb_stride, M, N, K,
                                                                      out);
   else if (out_mode == sbtc::OUT_F32)
-    k_gemm_i8_simt<sbtc::OUT_F32><<<grid, 128, 0, h->stream>>>(qa, sa, sa_stride, qb, sbp, sb_stride, M, N, K, out);
+    k_gemm_i8_simt<sbtc::OUT_F32><<<grid, 256, 0, h->stream>>>(qa, sa, sa_stride, qb, sbp, sb_stride, M, N, K, out);
   else
-    k_gemm_i8_simt<sbtc::OUT_BF16><<<grid, 128, 0, h->stream>>>(qa, sa, sa_stride, qb, sbp, sb_stride, M, N, K, out);
+    k_gemm_i8_simt<sbtc::OUT_BF16><<<grid, 256, 0, h->stream>>>(qa, sa, sa_stride, qb, sbp, sb_stride, M, N, K, out);
   SB_LAUNCH_CHECK(op);
   if (bias) SB_CUDA_CHECK(op, launch_add_bias(h, out, out_dt, M, N, bias));
   if (resid) {
@@ -540,6 +628,10 @@ sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t 
     return SB_OK;
   }
   // exact sequential (or unaligned fallback): dW[i][j] = sum_t G[t][i] * X[t][j]
+  if (!exact) {
+    const sb_status fs = simt_fallback(h, op, m, n, b);
+    if (fs != SB_OK) return fs;
+  }
   const dim3 grid(static_cast<unsigned>((n + 63) / 64), static_cast<unsigned>((m + 63) / 64));
   h->launches++;
   if (dt == SB_BF16)
@@ -590,6 +682,10 @@ sb_status gemm_bf16_tc(sb_handle h, const void* a, bool a_mn, const void* b, boo
     return SB_OK;
   }
   // any shape: fp32-accumulating SIMT kernel over the same index maps
+  {
+    const sb_status fs = simt_fallback(h, op, M, N, K);
+    if (fs != SB_OK) return fs;
+  }
   const __nv_bfloat16* Ap = static_cast<const __nv_bfloat16*>(a);
   const __nv_bfloat16* Bp = static_cast<const __nv_bfloat16*>(b);
   const int64_t a_rs = a_mn ? 1 : K, a_ks = a_mn ? M : 1, b_rs = b_mn ? 1 : K, b_ks = b_mn ? N : 1;
@@ -640,7 +736,11 @@ sb_status gemm_fp8(sb_handle h, const uint8_t* qa, int fa, const float* sa, int 
     if (e != cudaSuccess) return cuda_fail(op, e);
     return SB_OK;
   }
-  const dim3 grid(static_cast<unsigned>((N + 127) / 128), static_cast<unsigned>(M));
+  {
+    const sb_status fs = simt_fallback(h, op, M, N, K);
+    if (fs != SB_OK) return fs;
+  }
+  const dim3 grid(static_cast<unsigned>((N + 127) / 128), static_cast<unsigned>(std::min<int64_t>(M, 65535)));
   h->launches++;
   k_gemm_fp8_simt<<<grid, 128, 0, h->stream>>>(qa, fa, sa, sa_stride, qb, fb, sbp, sb_stride, M, N, K, out,
                                                out_dt == SB_BF16);

@@ -313,6 +313,20 @@ __global__ void k_clip_factor(const double* __restrict__ partials, int64_t n, do
   }
 }
 
+// Empty tensors have no chunks: the reference still reports them, with rms = sqrt(0 / 0) = NaN
+// and eta = alpha / max(1, NaN) = alpha (std::max returns its first argument when the
+// comparison is false), optimizer.cpp:148-160.
+struct EmptyList {
+  int32_t index[64];
+  int count;
+};
+__global__ void k_empty_infos(const __grid_constant__ EmptyList e, double alpha, double* rms_out, double* eta_out) {
+  const int i = threadIdx.x;
+  if (i >= e.count) return;
+  if (rms_out) rms_out[e.index[i]] = __longlong_as_double(0x7ff8000000000000LL);
+  if (eta_out) eta_out[e.index[i]] = alpha;
+}
+
 double debias(double beta, int64_t t) {  // optimizer.cpp:63-68
   if (beta == 0.0) return 0.0;
   const double num = 1.0 - std::pow(beta, static_cast<double>(t - 1));
@@ -441,6 +455,22 @@ extern "C" sb_status sb_stableadamw_step(sb_handle h, const sb_adamw_tensor* ten
     h->launches++;
     k_adamw_persistent<<<static_cast<unsigned>(grid), kThreads, 0, h->stream>>>(
         g, c, hp->clipping == SB_CLIP_GRAD ? clip : nullptr, partials, sync, eta_buf, rms_out, eta_out);
+  }
+  if (rms_out || eta_out) {
+    EmptyList e{};
+    for (int i = 0; i < ntensors; ++i) {
+      if (tensors[i].numel != 0) continue;
+      e.index[e.count++] = i;
+      if (e.count == 64) {
+        h->launches++;
+        k_empty_infos<<<1, 64, 0, h->stream>>>(e, hp->alpha, rms_out, eta_out);
+        e.count = 0;
+      }
+    }
+    if (e.count > 0) {
+      h->launches++;
+      k_empty_infos<<<1, 64, 0, h->stream>>>(e, hp->alpha, rms_out, eta_out);
+    }
   }
   SB_LAUNCH_CHECK(op);
   return SB_OK;

@@ -379,6 +379,33 @@ def _workspace(mode: LinearMode, b: int, n: int, m: int, device) -> torch.Tensor
     return torch.empty(nbytes.value, dtype=torch.uint8, device=device)
 
 
+def workspace_views(ctx: LinearContext) -> dict:
+    """The int8 operands a linear wrote into its workspace (sb_linear_workspace_layout), as
+    QuantizedMatrix views: "x" (row-wise X), "w" (W; tensor-wise, or row-wise for SwitchBackQ),
+    "w_t" (W^T payload, tensor-wise state) and "g" (row-wise G, valid after linear_backward
+    unless G came prequantized). No copies: they alias ctx.workspace."""
+    r = ctx.raw
+    lay = A.LinearWsLayout()
+    A.check(A.load().sb_linear_workspace_layout(C.byref(ctx.mode.c()), r.b, r.n, r.m, C.byref(lay)))
+    ws = ctx.workspace
+
+    def view(off, count, dtype, shape):
+        es = torch.empty((), dtype=dtype).element_size()
+        return ws[off:off + count * es].view(dtype).view(*shape)
+
+    b, n, m = r.b, r.n, r.m
+    w_rows = ctx.mode.variant == A.SB_SWITCHBACK_Q
+    return {
+        "x": QuantizedMatrix(view(lay.x_q, b * n, torch.int8, (b, n)), view(lay.x_state, b, torch.float32, (b,)), ROW),
+        "w": QuantizedMatrix(view(lay.w_q, m * n, torch.int8, (m, n)),
+                             view(lay.w_state, m if w_rows else 1, torch.float32, (m if w_rows else 1,)),
+                             ROW if w_rows else TENSOR),
+        "w_t": QuantizedMatrix(view(lay.w_q_t, n * m, torch.int8, (n, m)), view(lay.w_state, 1, torch.float32, (1,)),
+                               TENSOR),
+        "g": QuantizedMatrix(view(lay.g_q, b * m, torch.int8, (b, m)), view(lay.g_state, b, torch.float32, (b,)), ROW),
+    }
+
+
 def linear_forward(mode: LinearMode, x: torch.Tensor, w: torch.Tensor, ctx: LinearContext | None = None,
                    workspace: torch.Tensor | None = None, check: bool = True,
                    bias: torch.Tensor | None = None, x_q: QuantizedMatrix | None = None,

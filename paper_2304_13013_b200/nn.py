@@ -68,14 +68,14 @@ class SwitchBackLinear(torch.nn.Module):
         shape = x.shape
         x2d = x.reshape(-1, self.in_features)
         r2d = residual.reshape(-1, self.out_features) if residual is not None else None
-        fusable = self.mode.format == A.SB_INT8 and self.mode.variant in (A.SB_SWITCHBACK, A.SB_SWITCHBACK_M,
-                                                                          A.SB_SWITCHBACK_Q)
+        # the fused LayerNorm + quantize kernel takes bf16 rows of <= 2048 columns, 8-aligned
+        # (sb_layernorm_quantize_rowwise); anything else normalises unfused, then quantizes
+        fusable = (self.mode.format == A.SB_INT8 and x.dtype == torch.bfloat16 and _ln_fusable(self.in_features)
+                   and self.mode.variant in (A.SB_SWITCHBACK, A.SB_SWITCHBACK_M, A.SB_SWITCHBACK_Q))
         if self.norm is not None and fusable:
-            if x.dtype != torch.bfloat16:
-                raise TypeError("prenorm SwitchBackLinear runs in bf16")
             y = _LNLinearFn.apply(x2d, self.norm.weight, self.norm.bias, self.norm.eps, self.weight, self.bias,
                                   self.mode, r2d)
-        elif self.norm is not None:  # fp8 / tensor-wise X: LayerNorm unfused, then the layer
+        elif self.norm is not None:  # fp8 / tensor-wise X / wide rows: LayerNorm unfused, then the layer
             h = self.norm(x2d.float()).to(x2d.dtype)
             y = _SwitchBackLinearFn.apply(h, self.weight, self.bias, self.mode, r2d)
         else:
@@ -84,6 +84,10 @@ class SwitchBackLinear(torch.nn.Module):
 
     def extra_repr(self) -> str:
         return f"in_features={self.in_features}, out_features={self.out_features}, bias={self.bias is not None}"
+
+
+def _ln_fusable(cols: int) -> bool:
+    return cols <= 2048 and cols % 8 == 0
 
 
 def _ln_backward(dh, x2d, mean, rstd, ln_w, ln_b, needs):
@@ -195,8 +199,11 @@ class SwitchBackMLP(torch.nn.Module):
             raise TypeError("SwitchBackMLP runs in bf16")
         shape = x.shape
         n = self.norm
+        x2d = x.reshape(-1, self.fc1.in_features)
+        if n is not None and not _ln_fusable(self.fc1.in_features):
+            x2d, n = n(x2d.float()).to(x.dtype), None  # rows the fused LayerNorm kernel cannot take
         r2d = residual.reshape(-1, self.fc2.out_features) if residual is not None else None
-        y = _SwitchBackMLPFn.apply(x.reshape(-1, self.fc1.in_features), n.weight if n is not None else None,
+        y = _SwitchBackMLPFn.apply(x2d, n.weight if n is not None else None,
                                    n.bias if n is not None else None, n.eps if n is not None else 0.0,
                                    self.fc1.weight, self.fc1.bias, self.fc2.weight, self.fc2.bias, self.fc1.mode, r2d)
         return y.reshape(*shape[:-1], self.fc2.out_features)

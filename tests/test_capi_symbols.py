@@ -81,3 +81,22 @@ def test_pytorch_modules_have_no_cpu_fallback():
         Lp.layernorm_quantize_rowwise(x, torch.ones(16), torch.zeros(16))
     with pytest.raises(Lp.InvalidArgument):
         Lp.linear_forward(Lp.LinearMode(A.SB_SWITCHBACK, A.SB_INT8), x, torch.randn(8, 16).bfloat16())
+
+
+def test_workspace_layout_offsets():
+    """sb_linear_workspace_layout (no device needed): operands are 256-byte aligned, in the
+    carve order, non-overlapping, and inside sb_linear_workspace_size."""
+    L = A.load()
+    mode = A.LinearMode(A.SB_SWITCHBACK, A.SB_INT8, 0, 1, 0)
+    b, n, m = 1000, 384, 520
+    lay = A.LinearWsLayout()
+    assert L.sb_linear_workspace_layout(C.byref(mode), b, n, m, C.byref(lay)) == 0
+    total = C.c_size_t()
+    assert L.sb_linear_workspace_size(C.byref(mode), b, n, m, C.byref(total)) == 0
+    assert lay.total == total.value
+    spans = [(lay.x_q, b * n), (lay.x_state, 4 * b), (lay.w_q, m * n), (lay.w_q_t, m * n), (lay.w_state, 4 * m),
+             (lay.g_q, b * m), (lay.g_state, 4 * b)]
+    assert lay.x_q == 0
+    for (o1, s1), (o2, _) in zip(spans, spans[1:]):
+        assert o1 % 256 == 0 and o1 + s1 <= o2
+    assert spans[-1][0] + spans[-1][1] <= lay.total

@@ -172,3 +172,25 @@ def test_gemm_path_option_rejects_bad_values():
     with pytest.raises(A.InvalidArgument, match="sb_set_gemm_path: bad path"):
         h.set_gemm_path(7)
     h.set_gemm_path(A.SB_GEMM_AUTO)
+
+
+@pytest.mark.parametrize("M,N,K", [(70000, 40, 1000), (3, 70, 140001), (65, 129, 37)])
+def test_int8_simt_fallback_large_m_and_int64(M, N, K):
+    """Operands the TMA path cannot take (K % 16 != 0) run on the tiled dp4a SIMT kernel:
+    exact integer products for any K (int64 tile sums past 133144, linear.cpp:62-65) and no
+    65535-row grid limit (M = 70000 token rows)."""
+    g = torch.Generator(device="cuda").manual_seed(M + K)
+    qa = torch.randint(-127, 128, (M, K), device="cuda", dtype=torch.int8, generator=g)
+    qb = torch.randint(-127, 128, (N, K), device="cuda", dtype=torch.int8, generator=g)
+    sa = torch.rand(M, device="cuda", generator=g) + 0.5
+    sb = torch.tensor([0.75], device="cuda")
+    A_ = L.QuantizedMatrix(qa, sa, L.ROW)
+    B_ = L.QuantizedMatrix(qb, sb, L.TENSOR)
+    want = qa.double() @ qb.double().T
+    y = L.int8_matmul_dequant(A_, B_, out_dtype=torch.float32, exact=True)
+    t = (want * sa.double()[:, None]) * 0.75
+    ref = (t / torch.full_like(t, 16129.0)).float()  # IEEE division (a Python-scalar divisor becomes a reciprocal)
+    assert torch.equal(y, ref)
+    if K <= 133144:
+        raw = L.int8_matmul_dequant(A_, B_, out_dtype="raw")
+        assert torch.equal(raw.double(), want)

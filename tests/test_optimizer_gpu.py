@@ -80,3 +80,13 @@ def test_update_clip_shrinks_eta():  # optimizer_test.cpp:143-159
     assert i1[0][1] == 0.1
     i2 = L.optimizer_step([L.TensorRef("w", p, dev([1000.0]), v, u)], hp, 2)
     assert i2[0][0] > 1.0 and i2[0][1] == pytest.approx(0.1 / i2[0][0], rel=1e-15) and i2[0][1] < 0.1
+
+
+def test_empty_tensor_reports_nan_rms_and_alpha():  # optimizer.cpp:148-160 with n = 0
+    p, g = dev([1.0, 2.0, 3.0, 4.0]), dev([0.5, -0.5, 0.25, 1.0])
+    v, u = torch.zeros(4, device="cuda"), torch.zeros(4, device="cuda")
+    e = [torch.zeros(0, device="cuda") for _ in range(4)]
+    hp = L.OptimizerHyperparams(lr_schedule=lambda t: 0.05, clipping=A.SB_CLIP_UPDATE)
+    info = L.optimizer_step([L.TensorRef("e", *e), L.TensorRef("w", p, g, v, u)], hp, 1)
+    assert np.isnan(info[0][0]) and info[0][1] == 0.05
+    assert info[1][1] == 0.05
