@@ -144,70 +144,118 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- CPU side
-def cpu_reference_rate(budget_s: float = 12.0, threads: int | None = None):
-    """The UNMODIFIED reference (oracle/_ref: lowprec::linear_forward + linear_backward,
-    {kSwitchBack, kInt8}) on all host threads over a bounded token sample of both C2
-    linears. Returns (tokens/s, cores, sample description, kind)."""
-    import numpy as np
+REF_SAMPLE_TOKENS = 8192  # the ViT-H configs are timed at T = 8192 and scaled linearly in T
 
-    import oracle as O
 
-    threads = threads or os.cpu_count() or 1
-    kind = "reference" if O.ref_available() else "port"
-    rows = max(threads, 8)
-    # calibrate: grow the per-layer token sample until one pass takes >= budget/4
-    total_t = 0.0
-    total_tok = 0
-    while True:
+class RefStep:
+    """One bounded step of the UNMODIFIED reference (oracle/_ref: lowprec::linear_forward +
+    linear_backward, {kSwitchBack, kInt8}) over both C2 linears, token rows sharded over the host
+    threads (rows are independent; dW partials summed in a fixed order). The
+    oracle port stands in only when oracle/_ref was not built."""
+
+    def __init__(self, tokens: int, threads: int | None = None):
+        import numpy as np
+
+        import oracle as O
+
+        self.O = O
+        self.kind = "reference" if O.ref_available() else "port"
+        self.threads = (threads or os.cpu_count() or 1) if self.kind == "reference" else 1
+        self.tokens = tokens
+        self.data = []
+        for i, (_, n, m) in enumerate(LAYERS):  # X, G ~ N(0, 1), W ~ N(0, 1/n) (model.cpp:199-202)
+            rng = np.random.default_rng(10 + i)
+            self.data.append((rng.standard_normal((tokens, n)).astype(np.float32),
+                              (rng.standard_normal((m, n)) / np.sqrt(n)).astype(np.float32),
+                              rng.standard_normal((tokens, m)).astype(np.float32), n, m))
+
+    def run(self) -> float:
         t0 = time.perf_counter()
-        for _, n, m in LAYERS:
-            x = np.random.default_rng(1).standard_normal((rows, n)).astype(np.float32)
-            w = (np.random.default_rng(2).standard_normal((m, n)) / np.sqrt(n)).astype(np.float32)
-            g = np.random.default_rng(3).standard_normal((rows, m)).astype(np.float32)
-            if kind == "reference":
-                rc = O.ref().ref_switchback_fwd_bwd_threaded(x, w, g, rows, n, m, threads, None, None, None)
+        for x, w, g, n, m in self.data:
+            if self.kind == "reference":
+                rc = self.O.ref().ref_switchback_fwd_bwd_threaded(x, w, g, self.tokens, n, m, self.threads, None, None,
+                                                                  None)
                 assert rc == 0
             else:
-                O.switchback_forward(x, w)
-                O.switchback_backward(x, w, g)
-        dt = time.perf_counter() - t0
-        total_t += dt
-        total_tok += rows
-        if total_t >= budget_s or dt >= budget_s / 3:
-            break
-        rows = int(rows * max(2.0, min(8.0, (budget_s / 3) / max(dt, 1e-3))))
-    # the rate is the last (largest) pass: the smaller calibration passes are warm-up, dominated
-    # by per-call fixed costs (thread start, W quantization) that a full-size call amortises
-    sample = (f"{rows} tokens through fc1+fc2 (1280->5120, 5120->1280) SwitchBack int8 fwd+bwd in the timed pass "
-              f"({total_tok} incl. calibration), token rows sharded over {threads if kind == 'reference' else 1} "
-              f"threads; cost is linear in tokens")
-    return rows / dt, threads if kind == "reference" else 1, sample, kind
+                self.O.switchback_forward(x, w)
+                self.O.switchback_backward(x, w, g)
+        return time.perf_counter() - t0
+
+    def sample(self) -> str:
+        return (f"{self.tokens} tokens (BASELINE.md §3 sample) through fc1+fc2 (1280->5120, 5120->1280) SwitchBack "
+                f"int8 fwd+bwd per step, token rows sharded over {self.threads} threads; per-step time extrapolated "
+                f"linearly to {T_PER_GPU} tokens (the reference's cost is linear in T: linear.cpp:43-51, "
+                f"matrix.cpp:58-66)")
+
+
+def cpu_reference_rate(tokens: int = REF_SAMPLE_TOKENS):
+    """cpu_baseline of our arm: one warm-up pass, then one timed T = 8192 step. (tokens/s, cores, sample, kind)"""
+    warm = RefStep(512)
+    warm.run()
+    rs = RefStep(tokens)
+    dt = rs.run()
+    return tokens / dt, rs.threads, rs.sample(), rs.kind
 
 
 def run_reference_arm(args):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref) on all host
+    threads, same metric / unit / config as our arm. Each of the W warm-up and K timed steps is
+    one T = 8192 sample of the C2 step; the tokens/s rate is exact for the sample and the
+    per-step time is extrapolated linearly to T = 65792 (marked). If the projected run would
+    exceed ~4 minutes (a box with few cores), the sample shrinks and says so."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    rates = []
+    tokens = args.ref_tokens
+    probe = RefStep(1024)
+    probe.run()
+    dt = probe.run()
+    per_token = dt / 1024
+    budget = 240.0
+    n_steps = max(1, args.steps) + args.warmup
+    if per_token * tokens * n_steps > budget:
+        tokens = max(256, int(budget / n_steps / per_token) // 256 * 256)
+    rs = RefStep(tokens)
     for _ in range(args.warmup):
-        pass
-    # each step is a bounded sample; the whole arm stays within ~1.5-2 minutes for --steps <= 20
-    budget = max(4.0, min(args.ref_budget, 90.0 / max(1, args.steps)))
-    for _ in range(max(1, args.steps)):
-        r, cores, sample, kind = cpu_reference_rate(budget_s=budget)
-        rates.append(r)
-    v = sum(rates) / len(rates)
+        rs.run()
+    times = [rs.run() for _ in range(max(1, args.steps))]
+    v = tokens * len(times) / sum(times)
     line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": T_PER_GPU / v * 1000.0, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int8+f32 (reference CPU)", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": WORKLOAD + " (CPU reference, bounded token sample)", "tokens_per_gpu": T_PER_GPU},
-            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": kind, "sample": sample},
+            "config": {"workload": WORKLOAD + f" (CPU reference, {tokens}-token sample per step)",
+                       "tokens_per_gpu": T_PER_GPU, "sample_tokens_per_step": tokens,
+                       "sample_ms_per_step": 1000.0 * sum(times) / len(times)},
+            "extrapolated": True,
+            "extrapolation": f"ms_per_step = {T_PER_GPU} tokens / measured rate: the reference cost is linear in T",
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": rs.threads, "kind": rs.kind,
+                             "sample": rs.sample()},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------- GPU side
+def dw_traffic(m, n, T):
+    """ncu DRAM bytes (read + write) of one dW GEMM launch of this shape, from the committed
+    --set full captures (profiles/dw_gemm_traffic.json, keyed "m x n x T"); None if unmeasured."""
+    prof = os.path.join(ROOT, "profiles", "dw_gemm_traffic.json")
+    if not os.path.exists(prof):
+        return None
+    with open(prof) as f:
+        d = json.load(f)
+    e = d.get("launches", {}).get(f"{m}x{n}x{T}")
+    return e["dram_bytes"] if e else None
+
+
+class Op:
+    """One kernel (or layer call) of the step: what it is, what it does per launch, where it runs."""
+
+    def __init__(self, label, fn, cls, work, stream="main", join=False, ar=None):
+        self.label, self.fn, self.cls, self.work = label, fn, cls, work
+        self.stream, self.join, self.ar = stream, join, ar
+
+
 def run_ours(args):
     import torch
 
@@ -223,153 +271,163 @@ def run_ours(args):
     mode = L.LinearMode({"switchback": A.SB_SWITCHBACK, "switchback_q": A.SB_SWITCHBACK_Q}[variant],
                         A.SB_INT8 if fmt == "int8" else A.SB_FP8)
     cmode = mode.c()
-    plain = variant == "switchback" and fmt == "int8"  # the segmented SwitchBack int8 step
+    plain = variant == "switchback" and fmt == "int8"  # the kernel-by-kernel SwitchBack int8 step
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
 
     def randn(*shape, scale=1.0):
         return (torch.randn(*shape, device=dev, generator=gen) * scale).to(torch.bfloat16)
 
+    def empty(*shape, dtype=torch.bfloat16):
+        return torch.empty(*shape, device=dev, dtype=dtype)
+
     layers = []
     for name, n, m in layers_cfg:
-        lay = {"name": name, "n": n, "m": m,
-               "x": randn(T, n), "w": randn(m, n, scale=n ** -0.5), "g": randn(T, m),
-               "y": torch.empty(T, m, device=dev, dtype=torch.bfloat16),
-               "dx": torch.empty(T, n, device=dev, dtype=torch.bfloat16),
-               "gq": torch.empty(T, m, device=dev, dtype=torch.int8),
-               "gs": torch.empty(T, device=dev, dtype=torch.float32),
-               "dw": torch.empty(m, n, device=dev, dtype=torch.float32), "ctx": A.LinearCtx()}
+        lay = {"name": name, "n": n, "m": m, "x": randn(T, n), "w": randn(m, n, scale=n ** -0.5), "g": randn(T, m),
+               "y": empty(T, m), "dx": empty(T, n), "dw": empty(m, n, dtype=torch.float32), "ctx": A.LinearCtx(),
+               "xq": empty(T, n, dtype=torch.int8), "xs": empty(T, dtype=torch.float32),
+               "wq": empty(m, n, dtype=torch.int8), "wqt": empty(n, m, dtype=torch.int8),
+               "wst": empty(1, dtype=torch.float32),
+               "gq": empty(T, m, dtype=torch.int8), "gs": empty(T, dtype=torch.float32)}
         lay["ws"] = L._workspace(mode, T, n, m, dev)
         layers.append(lay)
     h = A.handle(local)
     P = L._p
 
-    # The step's kernels, straight through the C-ABI (the same launches sb_linear_forward /
-    # sb_linear_backward issue; for SwitchBack int8 the backward is split so the dW GEMM can
-    # be timed alone).
-    def fwd(lay):
-        A.check(h.lib.sb_linear_forward(h.h, C.byref(cmode), P(lay["x"]), P(lay["w"]), A.SB_BF16, T, lay["n"],
-                                        lay["m"], P(lay["y"]), C.byref(lay["ctx"]), P(lay["ws"]), lay["ws"].numel()))
+    # The step, kernel by kernel, through the public C-ABI: per linear, quantize_rowwise(X),
+    # quantize_tensorwise(W) (both layouts from one read), the int8 forward GEMM; then, last
+    # layer first, quantize_rowwise(G), the bf16 dW GEMM and the int8 dX GEMM. These are the
+    # launches sb_linear_forward / sb_linear_backward issue (checked equal after the timed
+    # region); splitting them lets every kernel be timed inside the step. With overlap the
+    # quantize of G runs on a side stream next to the one-wave dW GEMM (which leaves SMs idle)
+    # and is joined before the dX GEMM: both only read G (linear.cpp:232-245). The first
+    # layer's dW runs before its dX so that, under DP, the last dW all-reduce overlaps that dX.
+    def q_x(l):
+        A.check(h.lib.sb_quantize_rowwise(h.h, P(l["x"]), A.SB_BF16, T, l["n"], l["n"], P(l["xq"]), l["n"], P(l["xs"])))
 
-    def bwd_q(lay):
-        A.check(h.lib.sb_quantize_rowwise(h.h, P(lay["g"]), A.SB_BF16, T, lay["m"], lay["m"], P(lay["gq"]), lay["m"],
-                                          P(lay["gs"])))
+    def q_w(l):
+        A.check(h.lib.sb_quantize_tensorwise(h.h, P(l["w"]), A.SB_BF16, l["m"], l["n"], l["n"], P(l["wq"]), l["n"],
+                                             P(l["wqt"]), l["m"], P(l["wst"])))
 
-    def bwd_dx_gemm(lay):
-        c = lay["ctx"]
-        A.check(h.lib.sb_gemm_i8(h.h, P(lay["gq"]), P(lay["gs"]), C.c_void_p(c.w_q_t), C.c_void_p(c.w_state),
-                                 A.SB_SCALE_ROW_TENSOR, T, lay["n"], lay["m"], P(lay["dx"]), A.SB_BF16, 0))
+    def gemm_fwd(l):
+        A.check(h.lib.sb_gemm_i8(h.h, P(l["xq"]), P(l["xs"]), P(l["wq"]), P(l["wst"]), A.SB_SCALE_ROW_TENSOR, T, l["m"],
+                                 l["n"], P(l["y"]), A.SB_BF16, 0))
 
-    def bwd_dx(lay):
-        bwd_q(lay)
-        bwd_dx_gemm(lay)
+    def q_g(l):
+        A.check(h.lib.sb_quantize_rowwise(h.h, P(l["g"]), A.SB_BF16, T, l["m"], l["m"], P(l["gq"]), l["m"], P(l["gs"])))
 
-    def bwd_dw(lay):
-        A.check(h.lib.sb_wgrad(h.h, P(lay["g"]), P(lay["x"]), A.SB_BF16, T, lay["m"], lay["n"], P(lay["dw"]), 0, 0))
+    def gemm_dx(l):
+        A.check(h.lib.sb_gemm_i8(h.h, P(l["gq"]), P(l["gs"]), P(l["wqt"]), P(l["wst"]), A.SB_SCALE_ROW_TENSOR, T,
+                                 l["n"], l["m"], P(l["dx"]), A.SB_BF16, 0))
 
-    def bwd_full(lay):
-        A.check(h.lib.sb_linear_backward(h.h, C.byref(cmode), C.byref(lay["ctx"]), P(lay["g"]), P(lay["dx"]),
-                                         P(lay["dw"]), 0))
+    def dw_gemm(l):
+        A.check(h.lib.sb_wgrad(h.h, P(l["g"]), P(l["x"]), A.SB_BF16, T, l["m"], l["n"], P(l["dw"]), 0, 0))
 
-    # Segments (one CUDA graph each): forwards of all layers then, last layer first, the
-    # input-gradient work and the weight gradient of each layer. seg_kind: "main" / "dw" run on
-    # the step stream; "q" (the row-wise quantize of G) runs on a side stream forked from the
-    # step stream and joined before the layer's dX GEMM ("dx"), so it fills the SMs the
-    # one-wave dW GEMM leaves idle (134 of 148 busy) instead of running after it. Both only
-    # read G: the overlap stays inside one linear's backward (linear.cpp:232-245).
-    # The first layer's dW runs before its dX so that, under DP, the last dW all-reduce
-    # overlaps that dX instead of being exposed at the end of the step.
-    segments, seg_kind = [], []
+    def layer_fwd(l):
+        A.check(h.lib.sb_linear_forward(h.h, C.byref(cmode), P(l["x"]), P(l["w"]), A.SB_BF16, T, l["n"], l["m"],
+                                        P(l["y"]), C.byref(l["ctx"]), P(l["ws"]), l["ws"].numel()))
+
+    def layer_bwd(l):
+        A.check(h.lib.sb_linear_backward(h.h, C.byref(cmode), C.byref(l["ctx"]), P(l["g"]), P(l["dx"]), P(l["dw"]), 0))
+
     overlap = plain and not args.no_overlap
-    if plain and overlap:
-        segments.append(lambda: [fwd(l) for l in layers])
-        seg_kind.append("main")
-        for i in range(len(layers) - 1, -1, -1):
-            for fn, kind in ((bwd_q, "q"), (bwd_dw, "dw"), (bwd_dx_gemm, "dx")):
-                segments.append(lambda l=layers[i], fn=fn: fn(l))
-                seg_kind.append(kind)
-    elif plain:
-        segments.append(lambda: ([fwd(l) for l in layers], bwd_dx(layers[-1])))
-        seg_kind.append("main")
-        for i in range(len(layers) - 1, -1, -1):
-            segments.append(lambda l=layers[i]: bwd_dw(l))
-            seg_kind.append("dw")
-            if i > 1:
-                segments.append(lambda l=layers[i - 1]: bwd_dx(l))
-                seg_kind.append("main")
-        segments.append(lambda: bwd_dx(layers[0]))
-        seg_kind.append("main")
-    else:
-        segments.append(lambda: [fwd(l) for l in layers])
-        seg_kind.append("main")
-        for i in range(len(layers) - 1, -1, -1):
-            segments.append(lambda l=layers[i]: bwd_full(l))
-            seg_kind.append("main")
-    seg_dw = [k == "dw" for k in seg_kind]
+    ops = []
+    for l in layers:
+        nm, n, m = l["name"], l["n"], l["m"]
+        if plain:
+            ops.append(Op(f"{nm} quantize_rowwise X {T}x{n}", lambda l=l: q_x(l), "quantize", T * n * 3 + 4 * T))
+            ops.append(Op(f"{nm} quantize_tensorwise W {m}x{n} (+transpose)", lambda l=l: q_w(l), "quantize",
+                          m * n * 4 + 4))
+            ops.append(Op(f"{nm} int8 fwd GEMM M={T} N={m} K={n}", lambda l=l: gemm_fwd(l), "int8_gemm", 2 * T * m * n))
+        else:
+            ops.append(Op(f"{nm} linear_forward", lambda l=l: layer_fwd(l), "layer", 2 * T * m * n))
+    for l in reversed(layers):
+        nm, n, m = l["name"], l["n"], l["m"]
+        if plain:
+            ops.append(Op(f"{nm} quantize_rowwise G {T}x{m}", lambda l=l: q_g(l), "quantize", T * m * 3 + 4 * T,
+                          stream="side" if overlap else "main"))
+            ops.append(Op(f"{nm} bf16 dW GEMM m={m} n={n} K={T}", lambda l=l: dw_gemm(l), "dw_gemm", 2 * T * m * n,
+                          ar=l["dw"]))
+            ops.append(Op(f"{nm} int8 dX GEMM M={T} N={n} K={m}", lambda l=l: gemm_dx(l), "int8_gemm", 2 * T * m * n,
+                          join=overlap))
+        else:
+            ops.append(Op(f"{nm} linear_backward", lambda l=l: layer_bwd(l), "layer", 4 * T * m * n, ar=l["dw"]))
+    # graph chunks end where a dW all-reduce is issued (world > 1): NCCL runs between replays
+    chunks, cur = [], []
+    for op in ops:
+        cur.append(op)
+        if op.ar is not None and world > 1:
+            chunks.append(cur)
+            cur = []
+    if cur:
+        chunks.append(cur)
+
     stream = torch.cuda.current_stream(dev)
     side = torch.cuda.Stream(dev)
     ar = dp.GradAllReduce()
 
-    def eager_step():
-        for seg, kind in zip(segments, seg_kind):
-            if kind == "q":
-                side.wait_stream(stream)
-                h.bind_stream(side.cuda_stream)
-                seg()
-                h.bind_stream(stream.cuda_stream)
-            else:
-                if kind == "dx":
-                    stream.wait_stream(side)
-                seg()
+    def enqueue(chunk, evs):
+        """Launch one chunk on the current stream, recording an event after every kernel (and
+        around the side-stream ones). evs: list to append (op, start_event, end_event) to."""
+        cur_s = torch.cuda.current_stream(dev)
+        prev = torch.cuda.Event(enable_timing=True, external=True)
+        prev.record(cur_s)
+        for op in chunk:
+            if op.stream == "side":
+                side.wait_stream(cur_s)
+                a = torch.cuda.Event(enable_timing=True, external=True)
+                b = torch.cuda.Event(enable_timing=True, external=True)
+                with torch.cuda.stream(side):
+                    h.bind_stream(side.cuda_stream)
+                    a.record(side)
+                    op.fn()
+                    b.record(side)
+                h.bind_stream(cur_s.cuda_stream)
+                evs.append((op, a, b))
+                continue
+            if op.join:
+                cur_s.wait_stream(side)
+            op.fn()
+            e = torch.cuda.Event(enable_timing=True, external=True)
+            e.record(cur_s)
+            evs.append((op, prev, e))
+            prev = e
 
-    # warmup (eager), counting launches of one step
+    # warmup (eager), counting our launches of one step
+    h.bind_stream(stream.cuda_stream)
     for i in range(max(1, args.warmup)):
         l0 = h.launches()
-        h.bind_stream(stream.cuda_stream)
-        eager_step()
+        for c in chunks:
+            enqueue(c, [])
         launches_per_step = h.launches() - l0
     torch.cuda.synchronize()
-    graphs = None
+    # one graph per (step, chunk), each with its own events: every kernel of every timed step
+    # is timed on the device inside the timed region, with no gaps added between kernels
+    replicas = []  # [(graphs or None, evs)]
+    for r in range(args.steps):
+        evs, graphs = [], []
+        if not args.no_graph:
+            for c in chunks:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    h.bind_stream(torch.cuda.current_stream(dev).cuda_stream)
+                    enqueue(c, evs)
+                graphs.append(g)
+            h.bind_stream(stream.cuda_stream)
+        replicas.append((graphs, evs))
     if not args.no_graph:
-        graphs = []
-        for seg in segments:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                h.bind_stream(torch.cuda.current_stream(dev).cuda_stream)
-                seg()
-            graphs.append(g)
-        h.bind_stream(stream.cuda_stream)
-        for g in graphs:
+        for g in replicas[0][0]:
             g.replay()
         torch.cuda.synchronize()
 
-    run = [g.replay for g in graphs] if graphs else segments
-    if not graphs:  # eager launches follow the handle's stream binding
-        run = [(lambda seg=seg: (h.bind_stream(side.cuda_stream), seg(), h.bind_stream(stream.cuda_stream)))
-               if kind == "q" else seg for seg, kind in zip(segments, seg_kind)]
-    ns = len(run)
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(ns + 1)] for _ in range(args.steps)]
-    # dW all-reduce issue points: after each layer's dW segment (or full backward)
-    ar_after = {}
-    k = 0
-    for j in range(1, ns):
-        if seg_dw[j] or not plain:
-            ar_after[j] = layers[len(layers) - 1 - k]["dw"]
-            k += 1
-
-    def step(e):
-        e[0].record(stream)
-        for j in range(ns):
-            if seg_kind[j] == "q":
-                side.wait_stream(stream)
-                with torch.cuda.stream(side):
-                    run[j]()
+    def step(r):
+        graphs, evs = replicas[r]
+        for j, c in enumerate(chunks):
+            if graphs:
+                graphs[j].replay()
             else:
-                if seg_kind[j] == "dx":
-                    stream.wait_stream(side)
-                run[j]()
-            e[j + 1].record(stream)
-            if j in ar_after:
-                ar.launch(ar_after[j])
+                enqueue(c, evs)
+            if world > 1 and c[-1].ar is not None:
+                ar.launch(c[-1].ar)
         ar.wait()
 
     if world > 1:
@@ -380,8 +438,8 @@ def run_ours(args):
         if world > 1:
             torch.distributed.barrier()
         start.record(stream)
-        for i in range(args.steps):
-            step(ev[i])
+        for r in range(args.steps):
+            step(r)
         end.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -391,39 +449,76 @@ def run_ours(args):
     value = T * world / (ms / 1000.0)
     launches = launches_per_step * args.steps
 
+    # ---- per-kernel evidence from the in-step events (mean over the timed steps)
     pk = peaks()
+    per = {}
+    for _, evs in replicas:
+        for op, a, b in evs:
+            per.setdefault(op.label, [op, 0.0])[1] += a.elapsed_time(b)
+    kernels = []
+    for label, (op, tot) in per.items():
+        us = tot / args.steps * 1000.0
+        row = {"op": label, "class": op.cls, "us": us, "stream": op.stream}
+        if op.cls == "int8_gemm":
+            row.update(tops=op.work / us / 1e6, peak_tops=INT8_PEAK_TOPS, frac=op.work / us / 1e6 / INT8_PEAK_TOPS)
+        elif op.cls == "dw_gemm":
+            row.update(tflops=op.work / us / 1e6, peak_tflops=pk["bf16_tflops"],
+                       frac=op.work / us / 1e6 / pk["bf16_tflops"])
+        elif op.cls == "quantize":
+            row.update(gbs=op.work / us / 1e3, peak_gbs=pk["hbm_gbs"], frac=op.work / us / 1e3 / pk["hbm_gbs"])
+        kernels.append(row)
+    step_us = ms * 1000.0
+    cls_us = lambda c, main_only=False: sum(k["us"] for k in kernels  # noqa: E731
+                                            if k["class"] == c and (not main_only or k["stream"] == "main"))
+    int8_rows = [k for k in kernels if k["class"] == "int8_gemm"]
+    summary = None
+    if int8_rows:
+        ops_tot = sum(per[k["op"]][0].work for k in int8_rows)
+        t_tot = cls_us("int8_gemm")
+        summary = {"int8_tops_in_step": ops_tot / t_tot / 1e6, "peak_tops": INT8_PEAK_TOPS,
+                   "frac": ops_tot / t_tot / 1e6 / INT8_PEAK_TOPS,
+                   "peak_source": "B200 dense int8 datasheet (4.5 POPS); MEASURED_PEAKS.json has no int8 entry",
+                   # bench.cpp:83-89: (2 q_row + q_tensor + q_tt) / switchback_fwd_bwd
+                   "quantize_fraction": cls_us("quantize") / step_us,
+                   "quantize_fraction_critical_path": cls_us("quantize", True) / step_us,
+                   "share_of_step": {c: cls_us(c) / step_us for c in ("int8_gemm", "dw_gemm", "quantize")},
+                   "timing": "CUDA events recorded between kernels inside each step's graph, mean over the timed steps"}
     roof = None
     if plain:
-        # dominant kernel: the bf16 dW GEMM (2*m*n*T flops per launch), timed by the events
-        # bracketing its graph segment inside the timed region
-        dw_ms = sum(e[j].elapsed_time(e[j + 1]) for e in ev for j in range(ns) if seg_dw[j])
-        flops_step = sum(2.0 * lay["m"] * lay["n"] * T for lay in layers)
-        achieved = flops_step * args.steps / (dw_ms / 1000.0) / 1e12
+        dw_rows = [k for k in kernels if k["class"] == "dw_gemm"]
+        dw_us = sum(k["us"] for k in dw_rows)
+        flops = sum(per[k["op"]][0].work for k in dw_rows)
+        achieved = flops / dw_us / 1e6
         peak = pk["bf16_tflops"]
-        traffic = None
-        prof = os.path.join(ROOT, "profiles", "dw_gemm_traffic.json")
-        if os.path.exists(prof):
-            with open(prof) as f:
-                traffic = json.load(f).get("bytes_per_launch")
-        roof = {"bound": "tensor", "kernel": "bf16 dW GEMM (tcgen05 kind::f16 cta_group::2, 256x384 one-wave tiles, MN-major operands)",
+        trafs = [dw_traffic(l["m"], l["n"], T) for l in layers]
+        roof = {"bound": "tensor",
+                "kernel": "bf16 dW GEMM (tcgen05 kind::f16 cta_group::2, 256x384 one-wave tiles, MN-major operands)",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "peak_source": f"{pk['source']} bf16 burst (MEASURED_PEAKS.json bf16_tflops: the kernel is timed "
                                f"inside a {ms * args.steps:.0f} ms region); sustained figure "
                                f"{pk['bf16_tflops_sustained']}, datasheet dense 2250",
-                "traffic": traffic, "share_of_step": dw_ms / (ms * args.steps),
-                "flops_per_launch": [2 * lay["m"] * lay["n"] * T for lay in layers]}
-    int8_ops_step = sum(4.0 * lay["m"] * lay["n"] * T for lay in layers)
+                "traffic": (sum(trafs) / len(trafs)) if all(t is not None for t in trafs) else None,
+                "traffic_source": "profiles/dw_gemm_traffic.json (ncu --set full dram__bytes_read+write, per launch)",
+                "algorithmic_bytes_per_launch": [2 * T * (l["m"] + l["n"]) + 4 * l["m"] * l["n"] for l in layers],
+                "share_of_step": dw_us / step_us,
+                "flops_per_launch": [2 * l["m"] * l["n"] * T for l in layers]}
+    int8_ops_step = sum(4.0 * l["m"] * l["n"] * T for l in layers)
 
-    # per-kernel rates right after the timed region (same thermal / power state), then the
-    # cuBLAS yardstick, then the host-buffer e2e pass and the CPU reference
-    kern = kernel_rates(torch, A, h, layers, T, pk, fmt == "int8" and variant == "switchback") if rank == 0 else None
+    # the decomposed step computes what the layer API computes (not timed)
+    if plain:
+        for l in layers[:1]:
+            y0 = l["y"].clone()
+            layer_fwd(l)
+            torch.cuda.synchronize()
+            assert torch.equal(y0, l["y"]), "kernel-by-kernel forward differs from sb_linear_forward"
+
     yard = cublas_yardstick(torch, layers, T, args) if rank == 0 else None
     e2e = None
     if rank == 0 and not args.no_e2e and args.config == "c2":
         e2e = e2e_host(args, L, torch)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and args.config == "c2":
-        r, cores, sample, kind = cpu_reference_rate(budget_s=args.ref_budget)
+        r, cores, sample, kind = cpu_reference_rate()
         cpu = {"value": r, "unit": "tokens/s", "cores": cores, "kind": kind, "sample": sample}
 
     if rank == 0:
@@ -431,17 +526,18 @@ def run_ours(args):
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None,
                 "dtype": ("int8 (fwd, dX) + bf16 (dW), fp32 accumulate" if fmt == "int8" else
-                          "fp8 e4m3/e5m2 (fwd, dX) + fp8-snapped dW, fp32 accumulate"),
+                          "fp8 e4m3/e5m2 (fwd, dX) + bf16 (dW), fp32 accumulate"),
                 "data": "synthetic",
                 "config": {"workload": workload, "config": args.config, "variant": variant, "format": fmt,
                            "tokens_per_gpu": T, "global_tokens": T * world,
                            "layers": [f"{n}->{m}" for _, n, m in layers_cfg], "parallelism": f"dp{world} (token shards)",
                            "l2": "inputs larger than L2 (X, G operands 168-673 MB each)",
-                           "cuda_graphs": graphs is not None, "g_quantize_overlaps_dw": overlap},
+                           "cuda_graphs": not args.no_graph, "g_quantize_overlaps_dw": overlap},
                 "gpu_launches": launches,
                 "roofline": roof,
                 "int8_tops_per_step": int8_ops_step / 1e12,
-                "kernels": kern,
+                "int8_summary": summary,
+                "kernels": kernels,
                 "clocks": clk.summary(),
                 "e2e": e2e, "cpu_baseline": cpu, "yardstick_cublas_bf16": yard}
         print(json.dumps(line), flush=True)
@@ -707,68 +803,6 @@ def cpu_optimizer_rate(budget_s: float = 10.0):
                       "lowprec::optimizer_step (single-threaded as the reference)"}
 
 
-def kernel_rates(torch, A, h, layers, T, pk, int8_path):
-    """Per-kernel rates measured after the timed region, each launch alone with CUDA events on
-    the launching stream (median of 5, inputs > L2): the int8 GEMMs (the metric's 'int8 TOPS %
-    of peak') and the row-wise quantizer (HBM-bound)."""
-    import ctypes as C
-
-    P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
-    stream = torch.cuda.current_stream()
-    h.bind_stream(stream.cuda_stream)
-
-    def timed(fn, reps=5):
-        ts = []
-        for _ in range(reps):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            fn()
-            b.record(stream)
-            torch.cuda.synchronize()
-            ts.append(a.elapsed_time(b))
-        return sorted(ts)[len(ts) // 2] / 1000.0
-
-    out = {"int8_gemm": [], "quantize_rowwise": []}
-    if not int8_path:
-        return out
-    for lay in layers:
-        n, m = lay["n"], lay["m"]
-        xq = torch.empty(T, n, device="cuda", dtype=torch.int8)
-        xs = torch.empty(T, device="cuda")
-        A.check(h.lib.sb_quantize_rowwise(h.h, P(lay["x"]), A.SB_BF16, T, n, n, P(xq), n, P(xs)))
-        # forward Y = X_q W_q^T (M=T, N=m, K=n) and input gradient dX = G_q W_q (M=T, N=n, K=m)
-        wq = torch.empty(m, n, device="cuda", dtype=torch.int8)
-        wqt = torch.empty(n, m, device="cuda", dtype=torch.int8)
-        wst = torch.empty(1, device="cuda")
-        A.check(h.lib.sb_quantize_tensorwise(h.h, P(lay["w"]), A.SB_BF16, m, n, n, P(wq), n, P(wqt), m, P(wst)))
-        gq = torch.empty(T, m, device="cuda", dtype=torch.int8)
-        gs = torch.empty(T, device="cuda")
-        A.check(h.lib.sb_quantize_rowwise(h.h, P(lay["g"]), A.SB_BF16, T, m, m, P(gq), m, P(gs)))
-        fwd = lambda: A.check(h.lib.sb_gemm_i8(h.h, P(xq), P(xs), P(wq), P(wst), A.SB_SCALE_ROW_TENSOR,  # noqa: E731
-                                               T, m, n, P(lay["y"]), A.SB_BF16, 0))
-        dxg = lambda: A.check(h.lib.sb_gemm_i8(h.h, P(gq), P(gs), P(wqt), P(wst), A.SB_SCALE_ROW_TENSOR,  # noqa: E731
-                                               T, n, m, P(lay["dx"]), A.SB_BF16, 0))
-        for name, fn, N, K in (("fwd", fwd, m, n), ("dX", dxg, n, m)):
-            t = timed(fn)
-            tops = 2.0 * T * N * K / t / 1e12
-            out["int8_gemm"].append({"gemm": f"{lay['name']} {name} M={T} N={N} K={K}", "us": t * 1e6, "tops": tops,
-                                     "peak_tops": INT8_PEAK_TOPS, "frac": tops / INT8_PEAK_TOPS})
-        for src, cols in ((lay["x"], n), (lay["g"], m)):
-            q = torch.empty(T, cols, device="cuda", dtype=torch.int8)
-            st = torch.empty(T, device="cuda")
-            t = timed(lambda: A.check(h.lib.sb_quantize_rowwise(h.h, P(src), A.SB_BF16, T, cols, cols, P(q), cols,
-                                                                P(st))))
-            gbs = (T * cols * 3 + 4 * T) / t / 1e9
-            out["quantize_rowwise"].append({"shape": f"{T}x{cols} bf16", "us": t * 1e6, "gbs": gbs,
-                                            "peak_gbs": pk["hbm_gbs"], "frac": gbs / pk["hbm_gbs"]})
-    tot_ops = sum(2.0 * T * lay["n"] * lay["m"] * 2 for lay in layers)
-    tot_t = sum(k["us"] for k in out["int8_gemm"]) / 1e6
-    out["int8_summary"] = {"tops": tot_ops / tot_t / 1e12, "peak_tops": INT8_PEAK_TOPS,
-                           "frac": tot_ops / tot_t / 1e12 / INT8_PEAK_TOPS,
-                           "peak_source": "B200 dense int8 datasheet (4.5 POPS); MEASURED_PEAKS.json has no int8 entry"}
-    return out
-
-
 def e2e_host(args, L, torch):
     """Same workload through the C-ABI host-buffer entry sb_switchback_fwd_bwd_host:
     pinned host X, W, G in; Y, dX, dW out, every step."""
@@ -827,7 +861,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c5", "vit_block"])
     ap.add_argument("--tokens", type=int, default=T_PER_GPU)
-    ap.add_argument("--ref-budget", type=float, default=12.0)
+    ap.add_argument("--ref-tokens", type=int, default=REF_SAMPLE_TOKENS,
+                    help="reference arm: token sample per step (BASELINE.md §3: 8192)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")

@@ -10,7 +10,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_reference_arm_json_line():
     r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "1",
-                        "--ref-budget", "0.5"], cwd=ROOT, capture_output=True, text=True, timeout=600,
+                        "--ref-tokens", "512"], cwd=ROOT, capture_output=True, text=True, timeout=600,
                        env={**os.environ, "RANK": "0", "WORLD_SIZE": "1"})
     assert r.returncode == 0, r.stderr
     lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
@@ -22,6 +22,7 @@ def test_reference_arm_json_line():
     assert d["impl"] == "reference" and d["metric"] == bench.METRIC and d["unit"] == "tokens/s"
     assert d["higher_is_better"] is True and d["value"] > 0
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
+    assert d["extrapolated"] is True and d["config"]["sample_tokens_per_step"] == 512
     assert d["e2e"] == {"value": d["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
 
 
