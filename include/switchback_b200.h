@@ -83,7 +83,9 @@ uint64_t sb_launch_count(sb_handle h);
 /* Tensor-core GEMM tiling for this handle (no reference counterpart: a B200 tuning knob).
  * SB_GEMM_AUTO: 2-CTA (cta_group::2) 256 x 256 tiles when the problem fills the SM pairs,
  * else 1-CTA 128 x 256; the other values force one form (results are identical). */
-typedef enum sb_gemm_path { SB_GEMM_AUTO = 0, SB_GEMM_1CTA = 1, SB_GEMM_2CTA = 2 } sb_gemm_path;
+/* AUTO picks per shape; 1CTA = 128 x 256 tiles; 2CTA = cta_group::2 256 x 256 tiles; WIDE = the
+ * transposed cta_group::2 256 x 384 int8 / fp8 kernel (tc_i8_wide.cuh) wherever it applies. */
+typedef enum sb_gemm_path { SB_GEMM_AUTO = 0, SB_GEMM_1CTA = 1, SB_GEMM_2CTA = 2, SB_GEMM_WIDE = 3 } sb_gemm_path;
 sb_status sb_set_gemm_path(sb_handle h, int path);
 
 /* Device memory + synchronous copies on the handle's stream (for FFI callers without a CUDA runtime). */

@@ -22,7 +22,7 @@ SB_STANDARD, SB_SWITCHBACK, SB_SWITCHBACK_M, SB_SWITCHBACK_Q, SB_ALLQUANT = rang
 SB_INT8, SB_FP8 = range(2)
 SB_SCALE_ROW_TENSOR, SB_SCALE_ROW_ROW, SB_SCALE_NONE = range(3)
 SB_CLIP_NONE, SB_CLIP_UPDATE, SB_CLIP_GRAD = range(3)
-SB_GEMM_AUTO, SB_GEMM_1CTA, SB_GEMM_2CTA = range(3)
+SB_GEMM_AUTO, SB_GEMM_1CTA, SB_GEMM_2CTA, SB_GEMM_WIDE = range(4)
 
 # every symbol include/switchback_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = [

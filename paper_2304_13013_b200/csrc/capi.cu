@@ -270,7 +270,7 @@ sb_status sb_set_stream(sb_handle h, void* s) {
 
 sb_status sb_set_gemm_path(sb_handle h, int path) {
   if (!h) return sb::fail(SB_ERR_INVALID_ARGUMENT, "sb_set_gemm_path", "null handle");
-  if (path < SB_GEMM_AUTO || path > SB_GEMM_2CTA) return sb::fail(SB_ERR_INVALID_ARGUMENT, "sb_set_gemm_path", "bad path");
+  if (path < SB_GEMM_AUTO || path > SB_GEMM_WIDE) return sb::fail(SB_ERR_INVALID_ARGUMENT, "sb_set_gemm_path", "bad path");
   h->gemm_path = path;
   return SB_OK;
 }

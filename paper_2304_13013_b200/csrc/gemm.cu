@@ -17,6 +17,7 @@
 #include "tc_gemm.cuh"
 #include "tc_gemm2.cuh"
 #include "tc_dw_wide.cuh"
+#include "tc_i8_wide.cuh"
 
 #include <cstdio>
 #include <cstdlib>
@@ -426,6 +427,113 @@ cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, cons
   return cudaGetLastError();
 }
 
+// Per-device cache of a cluster kernel's one-time setup (the max-dynamic-smem attribute is per
+// device context, and so is the co-resident pair count).
+struct PairCache {
+  std::once_flag once[16];
+  cudaError_t err[16] = {};
+  int pairs[16] = {};
+};
+template <typename Kern>
+int cluster_pairs(sb_handle h, PairCache& c, Kern kern, int smem, int threads, cudaError_t* err) {
+  const int d = h->device & 15;
+  std::call_once(c.once[d], [&] {
+    c.err[d] = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * (h->num_sms / 2));
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 2;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (c.err[d] != cudaSuccess || cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1)
+      n = h->num_sms / 2;
+    c.pairs[d] = n;
+    cudaGetLastError();
+  });
+  *err = c.err[d];
+  return c.pairs[d];
+}
+
+// The 256 x 384 int8 / fp8 kernel runs when forced (sb_set_gemm_path(h, SB_GEMM_WIDE)) or with
+// SB_GEMM_WIDE=1 in the environment; AUTO keeps the 256 x 256 kernel, which measured faster at
+// the C2 shapes (tools/gemm_probe.cu with the effective-clock readout: 256 x 256 is 95% MMA-busy
+// in its main loop at K = 5120 and 76% at K = 1280; 256 x 384 86% / 57%, its 16 epilogue warps
+// taking issue slots and shared-memory bandwidth from the MMA / TMA warps).
+bool wide_enabled(sb_handle h) {
+  static int env = -1;
+  if (env < 0) env = getenv("SB_GEMM_WIDE") ? atoi(getenv("SB_GEMM_WIDE")) : 0;
+  if (h->gemm_path == SB_GEMM_WIDE) return true;
+  return env != 0 && h->gemm_path == SB_GEMM_AUTO && h->num_sms >= 2;
+}
+
+// The transposed 256 x 384 GEMM (tc_i8_wide.cuh): D[M x N] = X[M x K] . W[N x K]^T computed as
+// W . X^T. W (weight rows) is the MMA's A operand, X (tokens) its B operand. Returns
+// cudaErrorNotSupported when the shape is better served by the 256 x 256 kernels (too few
+// tiles to fill the SM pairs).
+template <int KIND, int OUT, bool SB_COL>
+cudaError_t launch_wide_t(sb_handle h, const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap& tx2,
+                          const CUtensorMap& td, const sbwide::WideParams& p, uint32_t idesc) {
+  static PairCache cache;
+  auto kern = sbwide::k_gemm_wide<KIND, OUT, SB_COL>;
+  cudaError_t err;
+  const int pairs = cluster_pairs(h, cache, kern, sbwide::SMEM_BYTES, sbwide::THREADS, &err);
+  if (err != cudaSuccess) return err;
+  const int units = p.tiles_w * p.tiles_t;
+  const int grid = 2 * (units < pairs ? units : pairs);
+  h->launches++;
+  sb::launch_pdl(kern, dim3(grid), dim3(sbwide::THREADS), sbwide::SMEM_BYTES, h->stream, tw, tx, tx2, td, p, idesc);
+  return cudaGetLastError();
+}
+
+// w: N x K (weight rows), x: M x K (tokens), both K-major 8-bit; out: M x N (bf16 / f32 / s32).
+cudaError_t launch_wide(sb_handle h, int kind, int out_mode, bool sb_col, const void* x, const void* w, int64_t M,
+                        int64_t N, int64_t K, const float* sa, const float* sbp, float post, const float* bias,
+                        void* out, sb_dtype out_dt, uint32_t idesc) {
+  if (!wide_enabled(h)) return cudaErrorNotSupported;
+  const int64_t tiles_w = (N + sbwide::TW - 1) / sbwide::TW, tiles_t = (M + sbwide::TT - 1) / sbwide::TT;
+  // enough tiles for every SM pair to take several (the last partial wave costs little)
+  if (h->gemm_path != SB_GEMM_WIDE && tiles_w * tiles_t < 4 * (h->num_sms / 2)) return cudaErrorNotSupported;
+  const CUtensorMapDataType u8 = CU_TENSOR_MAP_DATA_TYPE_UINT8;
+  CUtensorMap tw, tx, tx2, td;
+  const bool ok =
+      sb::encode_tmap_2d(&tw, u8, w, K, N, K, sbwide::KB, 128, CU_TENSOR_MAP_SWIZZLE_128B) &&
+      sb::encode_tmap_2d(&tx, u8, x, K, M, K, sbwide::KB, 128, CU_TENSOR_MAP_SWIZZLE_128B) &&
+      sb::encode_tmap_2d(&tx2, u8, x, K, M, K, sbwide::KB, 64, CU_TENSOR_MAP_SWIZZLE_128B) &&
+      sb::encode_tmap_2d(&td,
+                         out_dt == SB_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                           : (out_dt == SB_I32 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32),
+                         out, N, M, N * sb::dt_size(out_dt), 32, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (!ok) return cudaErrorInvalidValue;
+  sbwide::WideParams p{};
+  p.M = static_cast<int>(M);
+  p.N = static_cast<int>(N);
+  p.K = static_cast<int>(K);
+  p.sa = sa;
+  p.sb = sbp;
+  p.post_scale = post;
+  p.bias = (out_mode == sbtc::OUT_BF16 || out_mode == sbtc::OUT_F32) ? bias : nullptr;
+  p.tiles_w = static_cast<int>(tiles_w);
+  p.tiles_t = static_cast<int>(tiles_t);
+#define SB_WIDE_CASE(KD, OM)                                                                    \
+  if (kind == KD && out_mode == OM)                                                             \
+    return sb_col ? launch_wide_t<KD, OM, true>(h, tw, tx, tx2, td, p, idesc)                   \
+                  : launch_wide_t<KD, OM, false>(h, tw, tx, tx2, td, p, idesc);
+  SB_WIDE_CASE(sbtc::KIND_I8, sbtc::OUT_BF16)
+  SB_WIDE_CASE(sbtc::KIND_I8, sbtc::OUT_F32)
+  SB_WIDE_CASE(sbtc::KIND_I8, sbtc::OUT_F32_EXACT)
+  SB_WIDE_CASE(sbtc::KIND_I8, sbtc::OUT_I32)
+  SB_WIDE_CASE(sbtc::KIND_F8, sbtc::OUT_BF16)
+  SB_WIDE_CASE(sbtc::KIND_F8, sbtc::OUT_F32)
+#undef SB_WIDE_CASE
+  return cudaErrorNotSupported;
+}
+
 bool out_tmap(CUtensorMap* m, sb_dtype dt, void* out, int64_t M, int64_t N) {
   if (dt == SB_BF16)
     return sb::encode_tmap_2d(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, out, N, M, N * 2, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -505,6 +613,12 @@ sb_status gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* 
     p.post_scale = 1.0f / 16129.0f;
     p.splits = 1;
     p.bias = (out_mode == sbtc::OUT_BF16 || out_mode == sbtc::OUT_F32) ? bias : nullptr;
+    if (resid == nullptr) {
+      const cudaError_t we = launch_wide(h, sbtc::KIND_I8, out_mode, sb_stride == 1, qa, qb, M, N, K, sa, sbp,
+                                         p.post_scale, bias, out, out_dt, 0);
+      if (we == cudaSuccess) return SB_OK;
+      if (we != cudaErrorNotSupported) return cuda_fail(op, we);
+    }
     const bool fuse_resid = resid != nullptr && out_mode == sbtc::OUT_BF16 && aligned(resid, 4) && ld_resid % 2 == 0;
     p.resid = fuse_resid ? static_cast<const __nv_bfloat16*>(resid) : nullptr;
     p.ld_resid = ld_resid;
@@ -726,6 +840,14 @@ sb_status gemm_fp8(sb_handle h, const uint8_t* qa, int fa, const float* sa, int 
     p.splits = 1;
     const uint32_t idesc = sbtc::KindTraits<sbtc::KIND_F8>::IDESC | (static_cast<uint32_t>(fa) << 7) |
                            (static_cast<uint32_t>(fb) << 10);
+    if (sa_stride == 1) {  // transposed wide kernel: W (format fb) is the MMA's A operand, X (fa) its B
+      const uint32_t idesc_t = sbtc::KindTraits<sbtc::KIND_F8>::IDESC | (static_cast<uint32_t>(fb) << 7) |
+                               (static_cast<uint32_t>(fa) << 10);
+      const cudaError_t we = launch_wide(h, sbtc::KIND_F8, out_dt == SB_BF16 ? sbtc::OUT_BF16 : sbtc::OUT_F32,
+                                         sb_stride == 1, qa, qb, M, N, K, sa, sbp, 1.0f, nullptr, out, out_dt, idesc_t);
+      if (we == cudaSuccess) return SB_OK;
+      if (we != cudaErrorNotSupported) return cuda_fail(op, we);
+    }
     cudaError_t e;
     if (sb_stride)
       e = out_dt == SB_BF16 ? launch_tc<sbtc::KIND_F8, sbtc::OUT_BF16, false, false, true>(h, A, B, td, p, idesc)

@@ -108,6 +108,7 @@ struct KindTraits<KIND_BF16> {
 // MMA-loop cycles, producer waits on empty, epilogue waits on tfull, k-blocks}.
 extern __device__ unsigned long long g_probe[1024 * 6];  // defined in build/probe/probe_glue.cu
 extern __device__ long long g_trace[4096];               // CTA-pair 0 timeline (globaltimer ns)
+extern __device__ unsigned long long g_probe_ns[1024];   // per CTA: MMA-loop wall time (ns), for the clock
 __device__ __forceinline__ long long gtime() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -248,7 +248,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       int it = 0;
 #ifdef SB_GEMM_PROBE
-      const long long sb_loop0 = clock64();
+      const long long sb_loop0 = clock64(), sb_ns0 = gtime();
       int kidx = 0;
 #endif
       for (int u = pair; u < num_units; u += npairs, ++it) {
@@ -291,6 +291,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
 #ifdef SB_GEMM_PROBE
       atomicAdd(&g_probe[blockIdx.x * 6 + 2], (unsigned long long)(clock64() - sb_loop0));
+      g_probe_ns[blockIdx.x] = (unsigned long long)(gtime() - sb_ns0);
 #endif
     }
   } else if (warp >= 4) {

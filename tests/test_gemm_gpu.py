@@ -12,9 +12,10 @@ from tests._util import bf16, dev, fp8_decode, host, rel_err
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=[A.SB_GEMM_1CTA, A.SB_GEMM_2CTA], ids=["1cta", "2cta"])
+@pytest.fixture(params=[A.SB_GEMM_1CTA, A.SB_GEMM_2CTA, A.SB_GEMM_WIDE], ids=["1cta", "2cta", "wide"])
 def gemm_path(request):
-    """Run the test on both tensor-core tilings (1-CTA 128x256 and cta_group::2 256x256)."""
+    """Run the test on every tensor-core tiling (1-CTA 128x256, cta_group::2 256x256, and the
+    transposed cta_group::2 256x384 int8 / fp8 kernel)."""
     h = A.handle()
     h.set_gemm_path(request.param)
     yield request.param

@@ -7,7 +7,8 @@ mkdir -p "$ROOT/build/probe"
 cat > "$ROOT/build/probe/probe_glue.cu" <<'EOG'
 #include <cuda_runtime.h>
 #include "tc_gemm.cuh"
-namespace sbtc { __device__ unsigned long long g_probe[1024 * 6]; __device__ long long g_trace[4096]; }
+namespace sbtc { __device__ unsigned long long g_probe[1024 * 6]; __device__ long long g_trace[4096]; __device__ unsigned long long g_probe_ns[1024]; }
+extern "C" void sb_probe_ns_read(unsigned long long* out, int n) { cudaMemcpyFromSymbol(out, sbtc::g_probe_ns, n * 8); }
 extern "C" void sb_trace_read(long long* out) { cudaMemcpyFromSymbol(out, sbtc::g_trace, 4096 * 8); }
 extern "C" void sb_probe_read(unsigned long long* out, int n) { cudaMemcpyFromSymbol(out, sbtc::g_probe, n * 8); }
 extern "C" void sb_probe_reset() { static unsigned long long z[1024 * 6] = {0}; cudaMemcpyToSymbol(sbtc::g_probe, z, sizeof(z)); }

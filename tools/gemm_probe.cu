@@ -22,6 +22,7 @@ __global__ void k_fill(uint8_t* p, size_t n, int bf16) {
   }
 }
 extern "C" void sb_probe_reset();
+extern "C" void sb_probe_ns_read(unsigned long long* out, int n);
 extern "C" void sb_trace_read(long long* out);
 
 int main(int argc, char** argv) {
@@ -82,6 +83,18 @@ int main(int argc, char** argv) {
       printf("%3d: %7lld %7lld | %7lld %7lld  wait %5lld\n", i, tr[i] - t0, tr[512 + i] - t0, tr[1024 + i] - t0,
              tr[1536 + i] - t0, tr[1536 + i] - tr[1024 + i]);
   }
+  {
+    std::vector<unsigned long long> ns(148);
+    sb_probe_ns_read(ns.data(), 148);
+    double cyc = 0, t = 0;
+    for (int c = 0; c < 148; c += 2) t += ns[c];
+    cyc = 2 * sums[2];
+    if (t > 0) printf("256x256 kernel: MMA-loop %.0f cycles in %.0f ns per leader CTA -> %.0f MHz effective SM clock\n",
+                      cyc / 74, t / 74, cyc / t * 1000.0);
+  }
+  if (getenv("SB_GEMM_WIDE") && atoi(getenv("SB_GEMM_WIDE")) == 1)
+    printf("wide kernel: MMA-loop %.0f cycles in %.0f ns per leader CTA -> %.0f MHz effective SM clock\n",
+           2 * sums[2] / 148, 2 * sums[5] / 148, sums[2] / sums[5] * 1000.0);
   printf("MMA busy fraction of loop ~ %.2f (ideal cycles = kblocks*4*128 = %.0f)\n",
          (sums[5] / 148 * 512) / (sums[2] / 148), sums[5] / 148 * 512);
   return 0;

@@ -1,5 +1,5 @@
 // mma_rate.cu — microbenchmark: back-to-back tcgen05.mma issue rate (operands resident in
-// smem, no TMA), 1-CTA M=128 vs 2-CTA M=256, kind::i8 and kind::f16, N=256.
+// smem, no TMA), 1-CTA M=128 vs 2-CTA M=256, kind::i8 and kind::f16, N=256 / 192 / 128.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/mma_rate.cu -o build/mma_rate
 #include <cstdio>
 
@@ -7,7 +7,7 @@
 
 using namespace sbtc;
 
-template <int KIND, bool TWO>
+template <int KIND, bool TWO, int NN = 256>
 __global__ void __launch_bounds__(128, 1) k_rate(int iters, long long* out) {
   extern __shared__ uint8_t sm_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(128, 1) k_rate(int iters, long long* out) {
   if (warp == 1 && leader && (threadIdx.x & 31) == 0) {
     uint32_t idesc = KIND == KIND_I8 ? KindTraits<KIND_I8>::IDESC : KindTraits<KIND_BF16>::IDESC;
     if (TWO) idesc = (idesc & ~(0x1Fu << 24)) | (16u << 24);
+    idesc = (idesc & ~(0x3Fu << 17)) | ((uint32_t)(NN >> 3) << 17);
     const uint32_t a = sbptx::smem_u32(smem), b = sbptx::smem_u32(smem + 16384);
     long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
@@ -71,13 +72,13 @@ __global__ void __launch_bounds__(128, 1) k_rate(int iters, long long* out) {
   }
 }
 
-template <int KIND, bool TWO>
+template <int KIND, bool TWO, int NN = 256>
 void run(const char* name, int blocks) {
   long long* d;
   cudaMalloc(&d, sizeof(long long) * 1024);
   cudaMemset(d, 0, sizeof(long long) * 1024);
   const int smem = 65536 + 2048;
-  cudaFuncSetAttribute(k_rate<KIND, TWO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_rate<KIND, TWO, NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 2000;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(blocks);
@@ -93,9 +94,9 @@ void run(const char* name, int blocks) {
   cudaEvent_t s, e;
   cudaEventCreate(&s);
   cudaEventCreate(&e);
-  cudaLaunchKernelEx(&cfg, k_rate<KIND, TWO>, iters, d);
+  cudaLaunchKernelEx(&cfg, k_rate<KIND, TWO, NN>, iters, d);
   cudaEventRecord(s);
-  cudaLaunchKernelEx(&cfg, k_rate<KIND, TWO>, iters, d);
+  cudaLaunchKernelEx(&cfg, k_rate<KIND, TWO, NN>, iters, d);
   cudaEventRecord(e);
   cudaError_t err = cudaDeviceSynchronize();
   float ms = 0;
@@ -103,7 +104,7 @@ void run(const char* name, int blocks) {
   long long h[1024];
   cudaMemcpy(h, d, sizeof(long long) * blocks, cudaMemcpyDeviceToHost);
   const double mmas = 4.0 * iters;
-  const double macs_per_mma = (TWO ? 256.0 : 128.0) * 256.0 * (KIND == KIND_I8 ? 32.0 : 16.0);
+  const double macs_per_mma = (TWO ? 256.0 : 128.0) * double(NN) * (KIND == KIND_I8 ? 32.0 : 16.0);
   const int issuers = TWO ? blocks / 2 : blocks;
   printf("%-22s blocks=%3d err=%d cyc/mma(leader0)=%.1f  chip=%.0f T%s/s\n", name, blocks, (int)err,
          double(h[0]) / mmas, issuers * mmas * macs_per_mma * 2.0 / (ms * 1e-3) / 1e12,
@@ -118,5 +119,8 @@ int main() {
   run<KIND_I8, true>("i8 2cta M256 N256", 148);
   run<KIND_BF16, false>("bf16 1cta M128 N256", 148);
   run<KIND_BF16, true>("bf16 2cta M256 N256", 148);
+  run<KIND_I8, true, 128>("i8 2cta M256 N128", 148);
+  run<KIND_BF16, true, 128>("bf16 2cta M256 N128", 148);
+  run<KIND_I8, true, 192>("i8 2cta M256 N192", 148);
   return 0;
 }
