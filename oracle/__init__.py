@@ -100,6 +100,8 @@ def ref():
                                          C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
         L.ref_switchback_fwd_bwd_threaded.argtypes = [_f32p, _f32p, _f32p, C.c_int64, C.c_int64, C.c_int64,
                                                       C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.ref_block_fwd_bwd.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_int,
+                                        C.POINTER(C.c_void_p), _f32p, _f32p, _f32p, _f32p, C.POINTER(C.c_void_p)]
         pp = C.POINTER(C.c_void_p)
         L.ref_optimizer_step.argtypes = [C.c_int, pp, pp, pp, pp, _i64p, C.c_double, C.c_double, C.c_double,
                                          C.c_double, C.c_double, C.c_double, C.c_int, C.c_double, C.c_int64,
@@ -259,3 +261,37 @@ def stableadamw_step(thetas, grads, vs, us, t, alpha, beta1=0.9, beta2=0.99, bet
             beta1, beta2, beta2_warmup_lambda, eps, weight_decay, clipping, max_grad_norm, t, rms, eta)
     _chk(rc, "optimizer_step")
     return rms, eta
+
+
+BLOCK_PARAMS = ["norm1.gain", "norm1.bias", "wq", "wk", "wv", "wo", "ls1", "ls2", "norm2.gain", "norm2.bias", "w1",
+                "w2"]
+
+
+def block_param_shapes(dim, hidden):
+    return {"norm1.gain": (1, dim), "norm1.bias": (1, dim), "wq": (dim, dim), "wk": (dim, dim), "wv": (dim, dim),
+            "wo": (dim, dim), "ls1": (1, dim), "ls2": (1, dim), "norm2.gain": (1, dim), "norm2.bias": (1, dim),
+            "w1": (hidden, dim), "w2": (dim, hidden)}
+
+
+def ref_block_fwd_bwd(variant, fmt, params, x, d_out, heads, mlp_ratio=4.0, layer_scale=True):
+    """The reference's transformer_block + block_backward (model.cpp:287-408, run through
+    model_forward / model_backward at depth 1 with identity embedding and head; oracle/_ref).
+    params: dict name -> float32 array (BLOCK_PARAMS). Returns (y, dx, grads dict)."""
+    x, d_out = _f32(x), _f32(d_out)
+    tokens, dim = x.shape
+    hidden = int(mlp_ratio * dim)
+    shapes = block_param_shapes(dim, hidden)
+    ps = [_f32(params[k]) if k in params else np.zeros(shapes[k], np.float32) for k in BLOCK_PARAMS]
+    grads = {k: np.zeros(shapes[k], np.float32) for k in BLOCK_PARAMS}
+    y = np.empty((tokens, dim), np.float32)
+    dx = np.empty((tokens, dim), np.float32)
+    pin = (C.c_void_p * 12)(*[a.ctypes.data for a in ps])
+    pout = (C.c_void_p * 12)(*[grads[k].ctypes.data for k in BLOCK_PARAMS])
+    rc = ref().ref_block_fwd_bwd(variant, fmt, tokens, dim, heads, mlp_ratio, int(layer_scale), pin, x, d_out, y, dx,
+                                 pout)
+    if rc != 0:
+        raise OracleError(f"block: {ref().ref_last_error().decode()}")
+    if not layer_scale:
+        grads.pop("ls1")
+        grads.pop("ls2")
+    return y, dx, grads

@@ -7,7 +7,10 @@
 // the repo. The library is used for three things only:
 //   1. generating tests/golden/ fixtures (tests/golden/make_golden.py),
 //   2. pinning oracle/oracle.c against the reference (tests/test_oracle_golden.py),
-//   3. bench.py's CPU baseline and `--impl reference` arm: lowprec::linear_forward
+//   3. the transformer-block parity test (tests/test_block_gpu.py): lowprec::model_forward /
+//      model_backward (model.cpp) at depth 1 with identity embedding / head, which is exactly
+//      transformer_block + block_backward (model.cpp:287-408) and exposes d(block input),
+//   4. bench.py's CPU baseline and `--impl reference` arm: lowprec::linear_forward
 //      + lowprec::linear_backward({kSwitchBack, kInt8}) — the reference's own
 //      switchback_fwd_bwd unit (bench.cpp:75-81) — on P host threads, each on a
 //      token-row shard (rows are independent).
@@ -20,6 +23,7 @@
 
 #include "lowprec/linear.hpp"
 #include "lowprec/matrix.hpp"
+#include "lowprec/model.hpp"
 #include "lowprec/optimizer.hpp"
 #include "lowprec/quantize.hpp"
 
@@ -226,6 +230,61 @@ int ref_optimizer_step(int nt, float** theta, const float** grad, float** v, flo
       if (out_rms) out_rms[i] = infos[size_t(i)].rms;
       if (out_eta) out_eta[i] = infos[size_t(i)].eta;
     }
+  });
+}
+
+// One pre-norm transformer block forward + backward (model.cpp:287-408) through the public
+// model API: depth 1, inputs = I (tokens x tokens) and embed = X^T so the block input is X
+// exactly (each output is one product with 1 plus zeros), head = I so logits = block output and
+// d(block output) = d_logits; the embed gradient is then d(block input)^T (model.cpp:442+).
+// params / grads: norm1.gain, norm1.bias, wq, wk, wv, wo, ls1, ls2, norm2.gain, norm2.bias,
+// w1, w2 (12 pointers; ls1 / ls2 ignored without layer scale). y: block output, dx: d(input).
+int ref_block_fwd_bwd(int variant, int format, int64_t tokens, int64_t dim, int64_t heads, double mlp_ratio,
+                      int layer_scale, const float* const* params, const float* x, const float* d_out, float* y,
+                      float* dx, float* const* grads) {
+  return guarded([&] {
+    ModelConfig cfg;
+    cfg.depth = 1;
+    cfg.dim = dim;
+    cfg.heads = heads;
+    cfg.mlp_ratio = mlp_ratio;
+    cfg.layer_scale_enabled = layer_scale != 0;
+    cfg.linear_mode = mode_of(variant, format);
+    cfg.embed_norm = false;
+    cfg.input_dim = tokens;
+    cfg.output_dim = dim;
+    const int64_t hid = cfg.mlp_hidden();
+    ModelParams p = zeros_like(cfg);
+    const Matrix xm = to_matrix(x, tokens, dim);
+    p.embed = xm.transposed();
+    for (int64_t i = 0; i < dim; ++i) p.head(i, i) = 1.0f;
+    BlockParams& b = p.blocks[0];
+    b.norm1.gain = to_matrix(params[0], 1, dim);
+    b.norm1.bias = to_matrix(params[1], 1, dim);
+    b.wq = to_matrix(params[2], dim, dim);
+    b.wk = to_matrix(params[3], dim, dim);
+    b.wv = to_matrix(params[4], dim, dim);
+    b.wo = to_matrix(params[5], dim, dim);
+    if (cfg.layer_scale_enabled) {
+      b.ls1 = to_matrix(params[6], 1, dim);
+      b.ls2 = to_matrix(params[7], 1, dim);
+    }
+    b.norm2.gain = to_matrix(params[8], 1, dim);
+    b.norm2.bias = to_matrix(params[9], 1, dim);
+    b.w1 = to_matrix(params[10], hid, dim);
+    b.w2 = to_matrix(params[11], dim, hid);
+    Matrix inputs(tokens, tokens);
+    for (int64_t i = 0; i < tokens; ++i) inputs(i, i) = 1.0f;
+    ModelTape tape;
+    const Matrix out = model_forward(cfg, p, inputs, &tape);
+    from_matrix(out, y);
+    const ModelParams g = model_backward(cfg, p, tape, to_matrix(d_out, tokens, dim));
+    from_matrix(g.embed.transposed(), dx);
+    const BlockParams& gb = g.blocks[0];
+    const Matrix* outs[12] = {&gb.norm1.gain, &gb.norm1.bias, &gb.wq, &gb.wk, &gb.wv, &gb.wo,
+                              &gb.ls1,        &gb.ls2,        &gb.norm2.gain, &gb.norm2.bias, &gb.w1, &gb.w2};
+    for (int k = 0; k < 12; ++k)
+      if (grads[k] && (cfg.layer_scale_enabled || (k != 6 && k != 7))) from_matrix(*outs[k], grads[k]);
   });
 }
 
