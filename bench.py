@@ -692,11 +692,19 @@ def run_vit_block(args):
             self.ln2 = torch.nn.LayerNorm(D, device=dev)
             self.fused = sb and fused
             self.out = mk(D, D)
+            # q / k / v: three projections with their own tensor-wise scales as in the reference
+            # block (model.cpp:303-305), run as one grouped GEMM; --qkv-packed quantizes the
+            # packed [3D x D] weight with ONE scale instead (a numerics deviation, kept for A/B)
+            groups = 1 if args.qkv_packed else 3
             if self.fused:
                 # producer fusions: LayerNorm fused into the qkv / fc1 input quantization, GELU
                 # into fc2's input quantization and fc1's gradient quantization
-                self.qkv = SwitchBackLinear(D, 3 * D, device=dev, prenorm=True)
+                self.qkv = SwitchBackLinear(D, 3 * D, device=dev, prenorm=True, groups=groups)
                 self.mlp = SwitchBackMLP(D, 4 * D, device=dev, prenorm=True)
+            elif sb:
+                self.qkv = SwitchBackLinear(D, 3 * D, device=dev, groups=groups)
+                fc1, fc2 = mk(D, 4 * D), mk(4 * D, D)
+                self.mlp = torch.nn.Sequential(fc1, torch.nn.GELU(), fc2)
             else:
                 self.qkv = mk(D, 3 * D)
                 fc1, fc2 = mk(D, 4 * D), mk(4 * D, D)
@@ -769,6 +777,8 @@ def run_vit_block(args):
             "clocks": sbv["clocks"],
             "bf16_block": bfv, "speedup_vs_bf16_block": bfv["ms_per_step"] / sbv["ms_per_step"],
             "mlp_producer_fusion": fused,
+            "qkv": "one packed weight, one tensor-wise scale (deviation)" if args.qkv_packed else
+                   "three projections, three tensor-wise scales (model.cpp:303-305), one grouped GEMM",
             "e2e": None, "cpu_baseline": None, "roofline": None}
     print(json.dumps(line), flush=True)
 
@@ -867,6 +877,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="quantize G after dW on one stream")
+    ap.add_argument("--qkv-packed", action="store_true", help="vit_block: one scale for the packed qkv weight")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

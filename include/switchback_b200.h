@@ -153,6 +153,15 @@ sb_status sb_transpose_i8(sb_handle h, const int8_t* in, int64_t rows, int64_t c
 sb_status sb_gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* qb, const float* sb,
                      sb_scale_mode mode, int64_t M, int64_t N, int64_t K, void* out, sb_dtype out_dt, int exact);
 
+/* sb_gemm_i8 with the layer epilogue: y = dequant(acc) (+ bias[N], fp32) (+ resid[M x N] of the
+ * output dtype, leading dim ld_resid), each added in fp32 before the single output rounding.
+ * bias / resid may be NULL. Serves grouped projections (model.cpp:303-305: q / k / v as one
+ * GEMM whose per-column W scale is its projection's, mode SB_SCALE_ROW_ROW) and the summed
+ * input gradients of such a group (dX = dX_q + dX_k + dX_v, the residual carrying the sum). */
+sb_status sb_gemm_i8_epilogue(sb_handle h, const int8_t* qa, const float* sa, const int8_t* qb, const float* sb,
+                              sb_scale_mode mode, int64_t M, int64_t N, int64_t K, const float* bias,
+                              const void* resid, int64_t ld_resid, void* out, sb_dtype out_dt, int exact);
+
 /* matmul, matrix.hpp:51 / matrix.cpp:53-68: y[r x c] = a[r x k] . bt[c x k]^T with a strictly
  * sequential fp32 reduction per output and no FMA — bit-identical to the reference. */
 sb_status sb_matmul_f32(sb_handle h, const float* a, const float* bt, int64_t r, int64_t c, int64_t k, float* y);

@@ -29,7 +29,7 @@ EXPORTS = [
     "sb_abi_version", "sb_create", "sb_destroy", "sb_set_stream", "sb_synchronize", "sb_error_word",
     "sb_last_error", "sb_launch_count", "sb_quantize_rowwise", "sb_quantize_columnwise",
     "sb_quantize_tensorwise", "sb_dequantize", "sb_quantize_fp8", "sb_dequantize_fp8", "sb_gemm_i8",
-    "sb_matmul_f32", "sb_wgrad", "sb_gemm_fp8", "sb_linear_workspace_size", "sb_linear_workspace_layout", "sb_linear_forward", "sb_linear_forward_bias",
+    "sb_gemm_i8_epilogue", "sb_matmul_f32", "sb_wgrad", "sb_gemm_fp8", "sb_linear_workspace_size", "sb_linear_workspace_layout", "sb_linear_forward", "sb_linear_forward_bias",
     "sb_linear_forward_prequant", "sb_linear_backward_prequant", "sb_gelu_quantize_rowwise", "sb_linear_forward_residual",
     "sb_gelu_backward_quantize_rowwise", "sb_layernorm_quantize_rowwise", "sb_layernorm_backward_workspace_size",
     "sb_layernorm_backward",
@@ -114,6 +114,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             "sb_quantize_fp8": ([v, v, i32, i64, i64, i64, i32, i32, v, i64, v], i32),
             "sb_dequantize_fp8": ([v, v, i64, i64, i64, i32, v, i32, v, i32, i64], i32),
             "sb_gemm_i8": ([v, v, v, v, v, i32, i64, i64, i64, v, i32, i32], i32),
+            "sb_gemm_i8_epilogue": ([v, v, v, v, v, i32, i64, i64, i64, v, v, i64, v, i32, i32], i32),
             "sb_matmul_f32": ([v, v, v, i64, i64, i64, v], i32),
             "sb_wgrad": ([v, v, v, i32, i64, i64, i64, v, i32, i32], i32),
             "sb_gemm_fp8": ([v, v, i32, v, i32, v, i32, v, i32, i64, i64, i64, v, i32], i32),

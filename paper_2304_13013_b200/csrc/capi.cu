@@ -371,6 +371,18 @@ sb_status sb_gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_
   return sb::gemm_i8(h, qa, sa, qb, sbp, mode, M, N, K, out, out_dt, exact);
 }
 
+sb_status sb_gemm_i8_epilogue(sb_handle h, const int8_t* qa, const float* sa, const int8_t* qb, const float* sbp,
+                              sb_scale_mode mode, int64_t M, int64_t N, int64_t K, const float* bias,
+                              const void* resid, int64_t ld_resid, void* out, sb_dtype out_dt, int exact) {
+  const char* op = mode == SB_SCALE_ROW_ROW ? "matmul_dequant_dual_rowwise" : "int8_matmul_dequant";
+  SB_TRY(check_h(h, op));
+  if (M < 0 || N < 0 || K < 0 || !qa || !qb || !out || !sa || !sbp || mode == SB_SCALE_NONE ||
+      (out_dt != SB_F32 && out_dt != SB_BF16) || (resid && ld_resid < N))
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  if (M == 0 || N == 0) return SB_OK;
+  return sb::gemm_i8(h, qa, sa, qb, sbp, mode, M, N, K, out, out_dt, exact, bias, resid, ld_resid);
+}
+
 sb_status sb_matmul_f32(sb_handle h, const float* a, const float* bt, int64_t r, int64_t c, int64_t k, float* y) {
   const char* op = "matmul";
   SB_TRY(check_h(h, op));

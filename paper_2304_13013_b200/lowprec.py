@@ -94,12 +94,13 @@ class QuantizedMatrix:
 def quantize_rowwise(x: torch.Tensor, check: bool = True) -> QuantizedMatrix:
     """quantize.cpp:131-133."""
     _need_cuda(x)
-    x = x.contiguous()
+    if x.dim() != 2 or x.stride(1) != 1 or x.stride(0) < x.shape[1]:
+        x = x.contiguous()  # row-strided views (a column slice of a wider tensor) are read in place
     r, c = x.shape
     q = torch.empty((r, c), dtype=torch.int8, device=x.device)
     st = torch.empty(r, dtype=torch.float32, device=x.device)
     h = A.handle(x.device.index)
-    A.check(h.lib.sb_quantize_rowwise(h.h, _p(x), _dt(x), r, c, c, _p(q), c, _p(st)))
+    A.check(h.lib.sb_quantize_rowwise(h.h, _p(x), _dt(x), r, c, x.stride(0), _p(q), c, _p(st)))
     try:
         _check_nonfinite(h, check)
     except InvalidArgument:
@@ -305,6 +306,28 @@ def matmul_dequant_dual_rowwise(qa: QuantizedMatrix, qb: QuantizedMatrix, out_dt
         raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT,
                               "matmul_dequant_dual_rowwise: both operands must be row-wise")
     return _int8_product(qa, qb, A.SB_SCALE_ROW_ROW, out_dtype, exact)
+
+
+def int8_gemm_epilogue(qa: QuantizedMatrix, qb: QuantizedMatrix, out_dtype=torch.bfloat16, bias=None, residual=None,
+                       exact: bool = False) -> torch.Tensor:
+    """sb_gemm_i8_epilogue: the row x tensor (qb tensor-wise) or row x row (qb row-wise: a
+    per-output-column scale) int8 product with an fp32 bias and a residual of the output dtype
+    added before the single output rounding."""
+    if qa.cols != qb.cols:
+        raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "int8 matmul: inner dimension mismatch")
+    M, K, N = qa.rows, qa.cols, qb.rows
+    dev = qa.payload.device
+    out = torch.empty((M, N), dtype=out_dtype, device=dev)
+    mode = A.SB_SCALE_ROW_ROW if qb.axis == ROW else A.SB_SCALE_ROW_TENSOR
+    ld = 0
+    if residual is not None:
+        if residual.dtype != out_dtype or residual.shape != (M, N) or residual.stride(1) != 1:
+            raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "int8 matmul: residual must be M x N of the output dtype")
+        ld = residual.stride(0)
+    h = A.handle(dev.index)
+    A.check(h.lib.sb_gemm_i8_epilogue(h.h, _p(qa.payload), _p(qa.state), _p(qb.payload), _p(qb.state), mode, M, N, K,
+                                      _p(bias), _p(residual), ld, _p(out), _dt(out), int(exact)))
+    return out
 
 
 def matmul(a: torch.Tensor, b_transposed: torch.Tensor) -> torch.Tensor:

@@ -52,9 +52,15 @@ class SwitchBackLinear(torch.nn.Module):
     gradient (arXiv 2304.13013), on the B200 kernels of this package."""
 
     def __init__(self, in_features: int, out_features: int, bias: bool = True, variant: str = "switchback",
-                 fmt: str = "int8", device=None, prenorm: bool = False, eps: float = 1e-5):
+                 fmt: str = "int8", device=None, prenorm: bool = False, eps: float = 1e-5, groups: int = 1):
         super().__init__()
         self.in_features, self.out_features = in_features, out_features
+        # groups > 1: out_features = groups projections of one shared input (q / k / v), each with
+        # its own tensor-wise weight scale as separate linears would have (model.cpp:303-305),
+        # computed as one GEMM (sb_gemm_i8_epilogue, per-column scales)
+        if groups > 1 and (out_features % groups or variant != "switchback" or fmt != "int8"):
+            raise ValueError("grouped SwitchBackLinear: int8 SwitchBack with out_features divisible by groups")
+        self.groups = groups
         # prenorm: y = linear(LayerNorm(x)) with the norm fused into the input quantization
         self.norm = torch.nn.LayerNorm(in_features, eps=eps, device=device or "cuda") if prenorm else None
         self.mode = L.LinearMode(_VARIANTS[variant], A.SB_INT8 if fmt == "int8" else A.SB_FP8)
@@ -72,7 +78,14 @@ class SwitchBackLinear(torch.nn.Module):
         # (sb_layernorm_quantize_rowwise); anything else normalises unfused, then quantizes
         fusable = (self.mode.format == A.SB_INT8 and x.dtype == torch.bfloat16 and _ln_fusable(self.in_features)
                    and self.mode.variant in (A.SB_SWITCHBACK, A.SB_SWITCHBACK_M, A.SB_SWITCHBACK_Q))
-        if self.norm is not None and fusable:
+        if self.groups > 1:
+            n = self.norm
+            ln_ok = n is not None and x.dtype == torch.bfloat16 and _ln_fusable(self.in_features)
+            if n is not None and not ln_ok:
+                x2d, n = n(x2d.float()).to(x2d.dtype), None
+            y = _GroupedLinearFn.apply(x2d, n.weight if n is not None else None, n.bias if n is not None else None,
+                                       n.eps if n is not None else 0.0, self.weight, self.bias, self.groups, r2d)
+        elif self.norm is not None and fusable:
             y = _LNLinearFn.apply(x2d, self.norm.weight, self.norm.bias, self.norm.eps, self.weight, self.bias,
                                   self.mode, r2d)
         elif self.norm is not None:  # fp8 / tensor-wise X / wide rows: LayerNorm unfused, then the layer
@@ -83,7 +96,8 @@ class SwitchBackLinear(torch.nn.Module):
         return y.reshape(*shape[:-1], self.out_features)
 
     def extra_repr(self) -> str:
-        return f"in_features={self.in_features}, out_features={self.out_features}, bias={self.bias is not None}"
+        return (f"in_features={self.in_features}, out_features={self.out_features}, bias={self.bias is not None}"
+                + (f", groups={self.groups}" if self.groups > 1 else ""))
 
 
 def _ln_fusable(cols: int) -> bool:
@@ -128,6 +142,61 @@ class _LNLinearFn(torch.autograd.Function):
         dh, dw = L.linear_backward(ctx.mode, lctx, g, check=False)
         db = g.sum(0, dtype=torch.float32) if ctx.has_bias and ctx.needs_input_grad[5] else None
         dx, dg, dbeta = _ln_backward(dh, x2d, mean, rstd, *ctx.ln, ctx.needs_input_grad[:3])
+        ctx.state = None
+        return dx, dg, dbeta, None, dw, db, None, (g if ctx.needs_input_grad[7] else None)
+
+
+class _GroupedLinearFn(torch.autograd.Function):
+    """`groups` SwitchBack int8 linears of one input, each with its own tensor-wise W scale
+    (model.cpp:303-305): the input's row-wise quantization once (fused with the LayerNorm when
+    prenorm), the groups' weights quantized into one packed payload, ONE GEMM with the
+    per-column scale of each group (row x row dequant mode, + bias fused). Backward: each
+    group's output gradient quantized row-wise on its own (a column slice, read in place), the
+    groups' dX products summed through the GEMM's residual epilogue, one dW GEMM for all groups."""
+
+    @staticmethod
+    def forward(ctx, x2d, ln_w, ln_b, eps, weight, bias, groups, resid=None):
+        x2d = x2d.contiguous()
+        dt = x2d.dtype
+        if ln_w is not None:
+            h, hq, mean, rstd = L.layernorm_quantize_rowwise(x2d, ln_w.detach(), ln_b.detach(), eps, check=False)
+            ln_state = (x2d, mean, rstd)
+        else:
+            h, hq, ln_state = x2d, L.quantize_rowwise(x2d, check=False), None
+        m, n = weight.shape
+        mg = m // groups
+        w = weight.detach().to(dt).contiguous()
+        wq = torch.empty((m, n), dtype=torch.int8, device=w.device)
+        scale = torch.empty(m, dtype=torch.float32, device=w.device)
+        wts = []
+        for i in range(groups):
+            q, qt = L.quantize_tensorwise(w[i * mg:(i + 1) * mg], check=False, with_transpose=True)
+            wq[i * mg:(i + 1) * mg] = q.payload
+            scale[i * mg:(i + 1) * mg] = q.state.expand(mg)
+            wts.append(qt)
+        y = L.int8_gemm_epilogue(hq, L.QuantizedMatrix(wq, scale, L.ROW), out_dtype=dt,
+                                 bias=bias.detach().float().contiguous() if bias is not None else None,
+                                 residual=resid.detach() if resid is not None else None)
+        ctx.state = (h, wts, ln_state, groups)
+        ctx.ln = (ln_w, ln_b)
+        ctx.has_bias = bias is not None
+        return y
+
+    @staticmethod
+    def backward(ctx, g):
+        h, wts, ln_state, groups = ctx.state
+        g = g.contiguous()
+        mg = g.shape[1] // groups
+        dx = None
+        for i, wt in enumerate(wts):
+            gq = L.quantize_rowwise(g[:, i * mg:(i + 1) * mg], check=False)  # the group's own row scales
+            dx = L.int8_gemm_epilogue(gq, wt, out_dtype=g.dtype, residual=dx)  # dX_0 + dX_1 + ... in order
+        dw = L.wgrad(g, h, exact=False)
+        db = g.sum(0, dtype=torch.float32) if ctx.has_bias and ctx.needs_input_grad[5] else None
+        dg = dbeta = None
+        if ln_state is not None:
+            x2d, mean, rstd = ln_state
+            dx, dg, dbeta = _ln_backward(dx, x2d, mean, rstd, *ctx.ln, ctx.needs_input_grad[:3])
         ctx.state = None
         return dx, dg, dbeta, None, dw, db, None, (g if ctx.needs_input_grad[7] else None)
 

@@ -278,3 +278,35 @@ def test_residual_in_epilogue_modules():
         g = torch.randn_like(y)
         y.backward(g)
         assert torch.equal(r.grad, g)
+
+
+@pytest.mark.parametrize("prenorm", [False, True])
+def test_grouped_qkv_module_equals_three_linears(prenorm):
+    """SwitchBackLinear(groups=3): q / k / v with three tensor-wise scales (model.cpp:303-305) as
+    one GEMM. Forward: bit-identical to three separate SwitchBackLinear layers (same per-element
+    arithmetic); dW / db: equal to the separate layers' to fp32 accumulation order; dX: the sum
+    of the three layers' input gradients within bf16 rounding."""
+    torch.manual_seed(3)
+    T, D = 4096, 256
+    grp = SwitchBackLinear(D, 3 * D, groups=3, prenorm=prenorm)
+    sep = [SwitchBackLinear(D, D, prenorm=prenorm) for _ in range(3)]
+    with torch.no_grad():
+        for i, s in enumerate(sep):
+            s.weight.copy_(grp.weight[i * D:(i + 1) * D])
+            s.bias.copy_(torch.randn(D, device="cuda"))
+            grp.bias[i * D:(i + 1) * D] = s.bias
+            if prenorm:
+                s.norm.load_state_dict(grp.norm.state_dict())
+    x = torch.randn(T, D, device="cuda").bfloat16()
+    gy = torch.randn(T, 3 * D, device="cuda").bfloat16()
+    xg = x.clone().requires_grad_(True)
+    yg = grp(xg)
+    yg.backward(gy)
+    xs = x.clone().requires_grad_(True)
+    ys = torch.cat([s(xs) for s in sep], 1)
+    ys.backward(gy)
+    assert torch.equal(yg, ys)
+    for i, s in enumerate(sep):
+        assert rel(grp.weight.grad[i * D:(i + 1) * D], s.weight.grad) < 1e-5
+        assert rel(grp.bias.grad[i * D:(i + 1) * D], s.bias.grad) < 1e-6
+    assert rel(xg.grad.float(), xs.grad.float()) < 1e-2
