@@ -279,6 +279,18 @@ sb_status sb_linear_forward_residual(sb_handle h, const sb_linear_mode* mode, co
                                      const float* x_state, const void* w, const float* bias, const void* residual,
                                      sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y, sb_linear_ctx* ctx,
                                      void* workspace, size_t workspace_bytes);
+/* linear_forward with every optional producer-side input at once (each may be NULL):
+ *   x_q / x_state  X already quantized row-wise by its producer (LayerNorm / GELU fusion);
+ *   w_absmax       W's tensor-wise absmax as an fp32-bit-pattern word, as sb_stableadamw_step_ex
+ *                  writes it next to the bf16 shadow weight: W is quantized in one pass;
+ *   bias, residual as sb_linear_forward_bias / _residual.
+ * Prequantized X needs a row-wise int8 variant (SwitchBack, SwitchBackM, SwitchBackQ); w_absmax
+ * a tensor-wise one (SwitchBack, SwitchBackM). */
+sb_status sb_linear_forward_ex(sb_handle h, const sb_linear_mode* mode, const void* x, const int8_t* x_q,
+                               const float* x_state, const void* w, const unsigned int* w_absmax, const float* bias,
+                               const void* residual, sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y,
+                               sb_linear_ctx* ctx, void* workspace, size_t workspace_bytes);
+
 /* sb_linear_backward with G already quantized row-wise by its producer (g_q b x m, g_state b). */
 sb_status sb_linear_backward_prequant(sb_handle h, const sb_linear_mode* mode, const sb_linear_ctx* ctx, const void* g,
                                       const int8_t* g_q, const float* g_state, void* dx, float* dw, int dw_accumulate);
@@ -331,6 +343,38 @@ sb_status sb_stableadamw_workspace_size(const sb_adamw_tensor* tensors, int nten
  * may be NULL. Element math in fp64 mirroring optimizer.cpp:142-146,162-167. */
 sb_status sb_stableadamw_step(sb_handle h, const sb_adamw_tensor* tensors, int ntensors, const sb_adamw_hparams* hp,
                               int64_t t, double* rms_out, double* eta_out, void* workspace, size_t workspace_bytes);
+
+/* The trainer's gradient-to-update path (trainer.cpp:127-155) in the optimizer's own passes:
+ *   filter_nonfinite (optimizer.cpp:83-100): g' = f32(double(g) / loss_scale) formed on the fly
+ *     (the gradient buffers are not rewritten); a tensor with a non-finite g' is skipped — its
+ *     theta / v / u stay untouched, rms = NaN, eta = 0 — and with per_tensor_skip = 0 one bad
+ *     tensor skips them all;
+ *   grad_absmax (trainer.cpp:138): max |g'| per tensor (NaN ignored, as Matrix::abs_max);
+ *   the in-step global-norm clip (optimizer.cpp:121-131) over the tensors that are applied;
+ * and, for the NEXT step's forward, the weight's bf16 shadow copy and its tensor-wise absmax
+ * (the quantize_tensorwise state, quantize.cpp:139-141) written by the theta update itself
+ * (optimizer.cpp:162-167), so the next forward quantizes W without its own absmax pass
+ * (sb_quantize_tensorwise_from_absmax, sb_linear_forward_ex). One read-only statistics pass
+ * over g runs first when skipping, telemetry or the global-norm clip needs it (the skip
+ * decision must precede any state update); every other pass is the plain step's. */
+typedef struct sb_adamw_extras {
+  double loss_scale;              /* LossScaler::scale (> 0); 1 = no unscaling */
+  int32_t per_tensor_skip;        /* LossScaler::per_tensor_skip */
+  int32_t* skipped;               /* DEVICE [ntensors] out: 1 = skipped this step (or NULL) */
+  float* grad_absmax;             /* DEVICE [ntensors] out (or NULL) */
+  void* const* shadow_bf16;       /* HOST [ntensors] of DEVICE bf16 pointers (entries may be NULL) */
+  unsigned int* const* absmax_word; /* HOST [ntensors] of DEVICE words: max |bf16(theta')| as fp32 bits */
+} sb_adamw_extras;
+
+sb_status sb_stableadamw_step_ex(sb_handle h, const sb_adamw_tensor* tensors, int ntensors,
+                                 const sb_adamw_hparams* hp, int64_t t, const sb_adamw_extras* extras,
+                                 double* rms_out, double* eta_out, void* workspace, size_t workspace_bytes);
+
+/* quantize_tensorwise (+ transpose) of x with its absmax already known (an fp32-bit-pattern word
+ * as sb_stableadamw_step_ex writes it): one pass, payloads bit-identical to sb_quantize_tensorwise. */
+sb_status sb_quantize_tensorwise_from_absmax(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols,
+                                             int64_t ldx, const unsigned int* absmax_word, int8_t* q, int64_t ldq,
+                                             int8_t* q_t, int64_t ldqt, float* state);
 
 /* compute_rms, optimizer.hpp:54 / optimizer.cpp:31-42: *out (DEVICE double) =
  * sqrt(mean(g^2 / max(u, eps^2))), fp64, fixed-order reduction. */

@@ -30,7 +30,8 @@ EXPORTS = [
     "sb_last_error", "sb_launch_count", "sb_quantize_rowwise", "sb_quantize_columnwise",
     "sb_quantize_tensorwise", "sb_dequantize", "sb_quantize_fp8", "sb_dequantize_fp8", "sb_gemm_i8",
     "sb_gemm_i8_epilogue", "sb_matmul_f32", "sb_wgrad", "sb_gemm_fp8", "sb_linear_workspace_size", "sb_linear_workspace_layout", "sb_linear_forward", "sb_linear_forward_bias",
-    "sb_linear_forward_prequant", "sb_linear_backward_prequant", "sb_gelu_quantize_rowwise", "sb_linear_forward_residual",
+    "sb_linear_forward_prequant", "sb_linear_backward_prequant", "sb_linear_forward_ex", "sb_quantize_tensorwise_from_absmax",
+    "sb_stableadamw_step_ex", "sb_gelu_quantize_rowwise", "sb_linear_forward_residual",
     "sb_gelu_backward_quantize_rowwise", "sb_layernorm_quantize_rowwise", "sb_layernorm_backward_workspace_size",
     "sb_layernorm_backward",
     "sb_linear_backward", "sb_switchback_fwd_bwd_host", "sb_switchback_fwd_bwd_host_async",
@@ -72,6 +73,12 @@ class LinearWsLayout(C.Structure):
 class AdamwTensor(C.Structure):
     _fields_ = [("theta", C.c_void_p), ("grad", C.c_void_p), ("v", C.c_void_p), ("u", C.c_void_p),
                 ("numel", C.c_int64)]
+
+
+class AdamwExtras(C.Structure):
+    _fields_ = [("loss_scale", C.c_double), ("per_tensor_skip", C.c_int32), ("skipped", C.c_void_p),
+                ("grad_absmax", C.c_void_p), ("shadow_bf16", C.POINTER(C.c_void_p)),
+                ("absmax_word", C.POINTER(C.c_void_p))]
 
 
 class AdamwHparams(C.Structure):
@@ -127,6 +134,11 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             "sb_linear_backward": ([v, C.POINTER(LinearMode), C.POINTER(LinearCtx), v, v, v, i32], i32),
             "sb_linear_forward_prequant": ([v, C.POINTER(LinearMode), v, v, v, v, v, i32, i64, i64, i64, v,
                                             C.POINTER(LinearCtx), v, sz], i32),
+            "sb_linear_forward_ex": ([v, C.POINTER(LinearMode), v, v, v, v, v, v, v, i32, i64, i64, i64, v,
+                                      C.POINTER(LinearCtx), v, sz], i32),
+            "sb_quantize_tensorwise_from_absmax": ([v, v, i32, i64, i64, i64, v, v, i64, v, i64, v], i32),
+            "sb_stableadamw_step_ex": ([v, C.POINTER(AdamwTensor), i32, C.POINTER(AdamwHparams), i64,
+                                        C.POINTER(AdamwExtras), v, v, v, sz], i32),
             "sb_linear_backward_prequant": ([v, C.POINTER(LinearMode), C.POINTER(LinearCtx), v, v, v, v, v, i32], i32),
             "sb_linear_forward_residual": ([v, C.POINTER(LinearMode), v, v, v, v, v, v, i32, i64, i64, i64, v,
                                             C.POINTER(LinearCtx), v, sz], i32),

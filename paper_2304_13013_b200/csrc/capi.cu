@@ -327,6 +327,18 @@ sb_status sb_quantize_tensorwise(sb_handle h, const void* x, sb_dtype dt, int64_
   return q_tensorwise(h, x, dt, rows, cols, ldx, q, ldq, q_t, ldqt, state, words);
 }
 
+sb_status sb_quantize_tensorwise_from_absmax(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols,
+                                             int64_t ldx, const unsigned int* absmax_word, int8_t* q, int64_t ldq,
+                                             int8_t* q_t, int64_t ldqt, float* state) {
+  const char* op = "quantize_tensorwise";
+  SB_TRY(check_h(h, op));
+  if (rows <= 0 || cols <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty matrix");
+  if (!float_dtype(dt) || !x || !absmax_word || (!q && !q_t) || !state || ldx < cols)
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  SB_TRYC(op, sb::launch_quantize_from_words(h, x, dt, rows, cols, ldx, absmax_word, 0, q, ldq, q_t, ldqt, state));
+  return SB_OK;
+}
+
 sb_status sb_dequantize(sb_handle h, const int8_t* q, int64_t rows, int64_t cols, int64_t ldq, const float* state,
                         sb_axis axis, void* y, sb_dtype ydt, int64_t ldy) {
   const char* op = "dequantize";
@@ -450,7 +462,7 @@ static sb_status linear_forward_impl(sb_handle h, const sb_linear_mode* mode, co
                                      const float* bias, sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y,
                                      sb_linear_ctx* ctx, void* workspace, size_t ws_bytes,
                                      const int8_t* xq_in = nullptr, const float* xs_in = nullptr,
-                                     const void* resid = nullptr) {
+                                     const void* resid = nullptr, const unsigned int* w_absmax = nullptr) {
   const char* op = "linear_forward";
   SB_TRY(check_h(h, op));
   if (!mode || !x || !w || !y || !float_dtype(dt)) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
@@ -502,8 +514,13 @@ static sb_status linear_forward_impl(sb_handle h, const sb_linear_mode* mode, co
       SB_TRYC(op, sb::launch_quantize_rowwise(h, w, dt, m, n, n, ws.w_q, n, ws.w_state));
       SB_TRY(sb::gemm_i8(h, xq, xs, ws.w_q, ws.w_state, SB_SCALE_ROW_ROW, b, m, n, y, out_dt, md.exact, bias, resid, m));
     } else {
-      // tensor-wise W, both layouts from one read; W^T payload cached for the backward
-      SB_TRY(q_tensorwise(h, w, dt, m, n, n, ws.w_q, n, ws.w_qt, m, ws.w_state, ws.words));
+      // tensor-wise W, both layouts from one read; W^T payload cached for the backward. With
+      // W's absmax already known (written by the optimizer step with the bf16 shadow), a single
+      // quantize pass without the absmax pass.
+      if (w_absmax)
+        SB_TRYC(op, sb::launch_quantize_from_words(h, w, dt, m, n, n, w_absmax, 0, ws.w_q, n, ws.w_qt, m, ws.w_state));
+      else
+        SB_TRY(q_tensorwise(h, w, dt, m, n, n, ws.w_q, n, ws.w_qt, m, ws.w_state, ws.words));
       SB_TRY(sb::gemm_i8(h, xq, xs, ws.w_q, ws.w_state, SB_SCALE_ROW_TENSOR, b, m, n, y, out_dt, md.exact, bias, resid,
                          m));
     }
@@ -552,6 +569,21 @@ static sb_status linear_forward_impl(sb_handle h, const sb_linear_mode* mode, co
 }
 
 extern "C" {
+
+sb_status sb_linear_forward_ex(sb_handle h, const sb_linear_mode* mode, const void* x, const int8_t* x_q,
+                               const float* x_state, const void* w, const unsigned int* w_absmax, const float* bias,
+                               const void* residual, sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y,
+                               sb_linear_ctx* ctx, void* workspace, size_t ws_bytes) {
+  if ((x_q == nullptr) != (x_state == nullptr))
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, "linear_forward", "x_q and x_state go together");
+  if ((x_q || w_absmax) && mode &&
+      !(mode->format == SB_INT8 && (mode->variant == SB_SWITCHBACK || mode->variant == SB_SWITCHBACK_M ||
+                                    (mode->variant == SB_SWITCHBACK_Q && !w_absmax))))
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, "linear_forward",
+                    "prequantized X needs a row-wise int8 variant; a W absmax needs tensor-wise W");
+  return linear_forward_impl(h, mode, x, w, bias, dt, b, n, m, y, ctx, workspace, ws_bytes, x_q, x_state, residual,
+                             w_absmax);
+}
 
 sb_status sb_linear_forward(sb_handle h, const sb_linear_mode* mode, const void* x, const void* w, sb_dtype dt, int64_t b,
                             int64_t n, int64_t m, void* y, sb_linear_ctx* ctx, void* workspace, size_t ws_bytes) {

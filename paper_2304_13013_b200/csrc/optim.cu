@@ -16,6 +16,8 @@
 #include <cmath>
 #include <vector>
 
+#include <cuda_bf16.h>
+
 #include "sb_internal.h"
 
 namespace {
@@ -40,6 +42,8 @@ struct TensorDesc {
   int64_t task2;   // first phase-2 task
   int32_t index;   // position in the caller's tensor list (rms/eta outputs)
   int32_t vec;     // all four arrays 16-byte aligned and numel % 4 == 0: float4 path
+  __nv_bfloat16* shadow;  // optional: bf16(theta') for the next forward (sb_adamw_extras)
+  unsigned int* word;     // optional: max |bf16(theta')| as fp32 bits
 };
 
 struct Group {
@@ -58,7 +62,25 @@ struct Coeffs {
   double floor_;              // eps^2
   double eps, alpha, wd;
   int32_t update_clip;
+  // filter_nonfinite's unscaling (optimizer.cpp:91-92), g' = f32(double(g) / scale):
+  // 0 none, 1 scale is a power of two (then g' = g * fl(1/scale) in fp32, exact and identical),
+  // 2 general (fp64 division)
+  int32_t scale_mode;
+  float inv_scale_f;
+  double scale;
+  const int32_t* skipped;  // per caller tensor index: 1 = leave this tensor untouched (or null)
 };
+
+// The gradient the update sees: unscaled (EX), then the in-step clip factor.
+template <bool EX>
+__device__ __forceinline__ double grad_in(const Coeffs& c, float g, double clip) {
+  if (EX && c.scale_mode == 1) g = __fmul_rn(g, c.inv_scale_f);
+  if (EX && c.scale_mode == 2) g = __double2float_rn(__ddiv_rn(static_cast<double>(g), c.scale));
+  return clip == 1.0 ? static_cast<double>(g) : __dmul_rn(static_cast<double>(g), clip);
+}
+__device__ __forceinline__ uint32_t bf16_abs_bits(__nv_bfloat16 b) {  // as fp32 bits (quantize.cu abs_bits)
+  return (static_cast<uint32_t>(__bfloat16_as_ushort(b)) & 0x7fffu) << 16;
+}
 
 template <typename F>
 __device__ __forceinline__ int find_by(const Group& g, F key, int64_t x) {
@@ -127,6 +149,7 @@ __device__ __forceinline__ float update(const Coeffs& c, double eta, double eta_
 }
 
 // Phase-1 work on chunk `blk` of tensor d: moments + partial RMS sum (fixed order).
+template <bool EX>
 __device__ __forceinline__ double phase1_chunk(const TensorDesc& d, const Coeffs& c, double clip, int64_t blk) {
   const int64_t base = blk * kChunk;
   double acc = 0.0;
@@ -154,8 +177,7 @@ __device__ __forceinline__ double phase1_chunk(const TensorDesc& d, const Coeffs
           float ua[4] = {uv[e].x, uv[e].y, uv[e].z, uv[e].w};
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const double g = clip == 1.0 ? static_cast<double>(ga[k]) : __dmul_rn(static_cast<double>(ga[k]), clip);
-            acc = __dadd_rn(acc, moments(c, g, va[k], ua[k]));
+            acc = __dadd_rn(acc, moments(c, grad_in<EX>(c, ga[k], clip), va[k], ua[k]));
           }
           *reinterpret_cast<float4*>(d.v + i) = make_float4(va[0], va[1], va[2], va[3]);
           *reinterpret_cast<float4*>(d.u + i) = make_float4(ua[0], ua[1], ua[2], ua[3]);
@@ -166,9 +188,8 @@ __device__ __forceinline__ double phase1_chunk(const TensorDesc& d, const Coeffs
     for (int e = 0; e < kPerThread; ++e) {
       const int64_t i = base + e * kThreads + threadIdx.x;
       if (i < d.numel) {
-        const double g = __dmul_rn(static_cast<double>(d.grad[i]), clip);
         float v = d.v[i], u = d.u[i];
-        acc = __dadd_rn(acc, moments(c, g, v, u));
+        acc = __dadd_rn(acc, moments(c, grad_in<EX>(c, d.grad[i], clip), v, u));
         d.v[i] = v;
         d.u[i] = u;
       }
@@ -177,9 +198,14 @@ __device__ __forceinline__ double phase1_chunk(const TensorDesc& d, const Coeffs
   return acc;
 }
 
-__device__ __forceinline__ void phase2_chunk(const TensorDesc& d, const Coeffs& c, double eta, int64_t blk) {
+// Phase-2 work on chunk `blk`: theta update (kept as is when `keep`: a skipped tensor), plus with
+// EX the bf16 shadow copy; returns this thread's max |bf16(theta')| as fp32 bits (0 without EX).
+template <bool EX>
+__device__ __forceinline__ uint32_t phase2_chunk(const TensorDesc& d, const Coeffs& c, double eta, int64_t blk,
+                                                 bool keep) {
   const double eta_wd = __dmul_rn(eta, c.wd);
   const int64_t base = blk * kChunk;
+  uint32_t amax = 0;
   if (d.vec) {
 #pragma unroll
     for (int hh = 0; hh < kPerThread / 4 / kVecPerIter; ++hh) {
@@ -189,29 +215,51 @@ __device__ __forceinline__ void phase2_chunk(const TensorDesc& d, const Coeffs& 
         const int64_t i = base + (static_cast<int64_t>(kVecPerIter * hh + e) * kThreads + threadIdx.x) * 4;
         if (i < d.numel) {
           tv[e] = __ldcs(reinterpret_cast<const float4*>(d.theta + i));
-          vv[e] = __ldcs(reinterpret_cast<const float4*>(d.v + i));
-          uv[e] = __ldcs(reinterpret_cast<const float4*>(d.u + i));
+          if (!EX || !keep) {
+            vv[e] = __ldcs(reinterpret_cast<const float4*>(d.v + i));
+            uv[e] = __ldcs(reinterpret_cast<const float4*>(d.u + i));
+          }
         }
       }
 #pragma unroll
       for (int e = 0; e < kVecPerIter; ++e) {
         const int64_t i = base + (static_cast<int64_t>(kVecPerIter * hh + e) * kThreads + threadIdx.x) * 4;
         if (i < d.numel) {
-          float4 o;
-          o.x = update(c, eta, eta_wd, tv[e].x, vv[e].x, uv[e].x);
-          o.y = update(c, eta, eta_wd, tv[e].y, vv[e].y, uv[e].y);
-          o.z = update(c, eta, eta_wd, tv[e].z, vv[e].z, uv[e].z);
-          o.w = update(c, eta, eta_wd, tv[e].w, vv[e].w, uv[e].w);
-          __stcs(reinterpret_cast<float4*>(d.theta + i), o);
+          float4 o = tv[e];
+          if (!EX || !keep) {
+            o.x = update(c, eta, eta_wd, tv[e].x, vv[e].x, uv[e].x);
+            o.y = update(c, eta, eta_wd, tv[e].y, vv[e].y, uv[e].y);
+            o.z = update(c, eta, eta_wd, tv[e].z, vv[e].z, uv[e].z);
+            o.w = update(c, eta, eta_wd, tv[e].w, vv[e].w, uv[e].w);
+            __stcs(reinterpret_cast<float4*>(d.theta + i), o);
+          }
+          if (EX && d.shadow != nullptr) {
+            const __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+            amax = max(max(amax, max(bf16_abs_bits(lo.x), bf16_abs_bits(lo.y))),
+                       max(bf16_abs_bits(hi.x), bf16_abs_bits(hi.y)));
+            uint2 pk;
+            pk.x = *reinterpret_cast<const uint32_t*>(&lo);
+            pk.y = *reinterpret_cast<const uint32_t*>(&hi);
+            *reinterpret_cast<uint2*>(d.shadow + i) = pk;
+          }
         }
       }
     }
   } else {
     for (int e = 0; e < kPerThread; ++e) {
       const int64_t i = base + e * kThreads + threadIdx.x;
-      if (i < d.numel) d.theta[i] = update(c, eta, eta_wd, d.theta[i], d.v[i], d.u[i]);
+      if (i < d.numel) {
+        const float o = (EX && keep) ? d.theta[i] : update(c, eta, eta_wd, d.theta[i], d.v[i], d.u[i]);
+        if (!EX || !keep) d.theta[i] = o;
+        if (EX && d.shadow != nullptr) {
+          const __nv_bfloat16 b = __float2bfloat16_rn(o);
+          d.shadow[i] = b;
+          amax = max(amax, bf16_abs_bits(b));
+        }
+      }
     }
   }
+  return amax;
 }
 
 // Persistent multi-tensor StableAdamW. Tasks, fetched in order from an atomic counter:
@@ -227,7 +275,8 @@ __device__ __forceinline__ void st_release(unsigned int* p, unsigned int v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads, 9) k_adamw_persistent(const __grid_constant__ Group grp, Coeffs c,
+template <bool EX>
+__global__ void __launch_bounds__(kThreads, EX ? 8 : 9) k_adamw_persistent(const __grid_constant__ Group grp, Coeffs c,
                                                                const double* __restrict__ clip_ptr,
                                                                double* __restrict__ partials,
                                                                unsigned int* __restrict__ sync,
@@ -262,8 +311,9 @@ __global__ void __launch_bounds__(kThreads, 9) k_adamw_persistent(const __grid_c
     const int ti = seg >> 1;
     const TensorDesc& d = grp.t[ti];
     const int64_t local = (seg & 1) ? d.nblocks + (task - d.task2) : task - d.task0;
+    const bool skip = EX && c.skipped != nullptr && c.skipped[d.index] != 0;
     if (local < d.nblocks) {
-      const double s = block_sum(phase1_chunk(d, c, clip, local), red);
+      const double s = block_sum(skip ? 0.0 : phase1_chunk<EX>(d, c, clip, local), red);
       if (threadIdx.x == 0) {
         partials[d.block0 + local] = s;
         __threadfence();
@@ -279,8 +329,13 @@ __global__ void __launch_bounds__(kThreads, 9) k_adamw_persistent(const __grid_c
         for (int64_t j = threadIdx.x; j < d.nblocks; j += kThreads) sum = __dadd_rn(sum, __ldcg(partials + d.block0 + j));
         const double tot = block_sum(sum, red);
         if (threadIdx.x == 0) {
-          const double rms = __dsqrt_rn(__ddiv_rn(tot, static_cast<double>(d.numel)));
-          const double eta = c.update_clip ? __ddiv_rn(c.alpha, rms > 1.0 ? rms : 1.0) : c.alpha;
+          double rms = __dsqrt_rn(__ddiv_rn(tot, static_cast<double>(d.numel)));
+          double eta = c.update_clip ? __ddiv_rn(c.alpha, rms > 1.0 ? rms : 1.0) : c.alpha;
+          if (skip) {  // trainer.cpp:140-143: a skipped tensor reports rms = NaN
+            rms = __longlong_as_double(0x7ff8000000000000LL);
+            eta = 0.0;
+          }
+          if (EX && d.word != nullptr) *d.word = 0u;  // the phase-2 chunks max into it after the flag
           eta_buf[ti] = eta;
           if (rms_out) rms_out[d.index] = rms;
           if (eta_out) eta_out[d.index] = eta;
@@ -294,40 +349,14 @@ __global__ void __launch_bounds__(kThreads, 9) k_adamw_persistent(const __grid_c
         s_eta = __ldcg(eta_buf + ti);
       }
       __syncthreads();
-      phase2_chunk(d, c, s_eta, local - d.nblocks);
+      const uint32_t m = phase2_chunk<EX>(d, c, s_eta, local - d.nblocks, skip);
+      if (EX && d.word != nullptr) {
+        const uint32_t wm = __reduce_max_sync(0xffffffffu, m);
+        if ((threadIdx.x & 31) == 0 && wm != 0u) atomicMax(d.word, wm);
+      }
     }
     if (threadIdx.x == 0) s_task = next;
     __syncthreads();
-  }
-}
-
-// kGradClip (optimizer.cpp:121-131): global sum of squares -> clip factor on device.
-__global__ void __launch_bounds__(kThreads) k_sumsq(const __grid_constant__ Group grp, double* __restrict__ partials,
-                                                    int64_t offset) {
-  __shared__ double red[kThreads / 32];
-  const int64_t gblk = offset + blockIdx.x;  // global chunk index (partials slot)
-  const TensorDesc& d = grp.t[find_tensor(grp, gblk)];
-  const int64_t base = (gblk - d.block0) * kChunk;
-  double acc = 0.0;
-  for (int e = 0; e < kPerThread; ++e) {
-    const int64_t i = base + e * kThreads + threadIdx.x;
-    if (i < d.numel) {
-      const double g = static_cast<double>(d.grad[i]);
-      acc = __dadd_rn(acc, __dmul_rn(g, g));
-    }
-  }
-  const double s = block_sum(acc, red);
-  if (threadIdx.x == 0) partials[gblk] = s;
-}
-
-__global__ void k_clip_factor(const double* __restrict__ partials, int64_t n, double max_norm, double* clip) {
-  __shared__ double red[kThreads / 32];
-  double s = 0.0;
-  for (int64_t j = threadIdx.x; j < n; j += kThreads) s = __dadd_rn(s, partials[j]);
-  const double tot = block_sum(s, red);
-  if (threadIdx.x == 0) {
-    const double norm = __dsqrt_rn(tot);
-    *clip = norm > max_norm ? __ddiv_rn(max_norm, norm) : 1.0;
   }
 }
 
@@ -345,6 +374,79 @@ __global__ void k_empty_infos(const __grid_constant__ EmptyList e, double alpha,
   if (eta_out) eta_out[e.index[i]] = alpha;
 }
 
+// Statistics pass of sb_stableadamw_step_ex (one read of g, before any state changes): per
+// chunk the unscaled gradient's non-finite flag, |g'| max and sum of g'^2; the block that
+// finishes a tensor's last chunk sums the tensor's partials in a fixed order into tensor_ss.
+// counts[k] (zeroed) counts finished chunks of group tensor k.
+__global__ void __launch_bounds__(kThreads) k_gradstats(const __grid_constant__ Group grp, Coeffs c,
+                                                        double* __restrict__ partials, int64_t offset,
+                                                        unsigned int* __restrict__ counts, double* __restrict__ tensor_ss,
+                                                        int32_t* __restrict__ skipped, unsigned int* __restrict__ amax_bits) {
+  __shared__ double red[kThreads / 32];
+  __shared__ int s_last;
+  const int64_t gblk = offset + blockIdx.x;
+  const int ti = find_tensor(grp, gblk);
+  const TensorDesc& d = grp.t[ti];
+  const int64_t base = (gblk - d.block0) * kChunk;
+  double acc = 0.0;
+  uint32_t amax = 0, bad = 0;
+  for (int e = 0; e < kPerThread; ++e) {
+    const int64_t i = base + e * kThreads + threadIdx.x;
+    if (i < d.numel) {
+      const double gd = grad_in<true>(c, d.grad[i], 1.0);
+      const uint32_t ab = __float_as_uint(static_cast<float>(gd)) & 0x7fffffffu;
+      bad |= ab >= 0x7f800000u;                 // inf or NaN (optimizer.cpp:94)
+      if (ab <= 0x7f800000u) amax = max(amax, ab);  // NaN never wins (Matrix::abs_max, matrix.cpp:31-35)
+      acc = __dadd_rn(acc, __dmul_rn(gd, gd));
+    }
+  }
+  amax = __reduce_max_sync(0xffffffffu, amax);
+  bad = __reduce_or_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0) {
+    if (amax_bits != nullptr && amax != 0u) atomicMax(amax_bits + d.index, amax);
+    if (bad) atomicOr(reinterpret_cast<unsigned int*>(skipped) + d.index, 1u);
+  }
+  const double sblk = block_sum(acc, red);
+  if (threadIdx.x == 0) {
+    partials[gblk] = sblk;
+    __threadfence();
+    s_last = atomicAdd(counts + ti, 1u) == static_cast<unsigned int>(d.nblocks - 1);
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    double sum = 0.0;
+    for (int64_t j = threadIdx.x; j < d.nblocks; j += kThreads) sum = __dadd_rn(sum, __ldcg(partials + d.block0 + j));
+    const double tot = block_sum(sum, red);
+    if (threadIdx.x == 0) tensor_ss[d.index] = tot;
+  }
+}
+
+// After the statistics pass: LossScaler::per_tensor_skip == 0 turns one skip into all
+// (optimizer.cpp:96-99); kGradClip's factor from the applied tensors' sums, in tensor order
+// (optimizer.cpp:121-131).
+__global__ void k_gradstats_final(int n, int per_tensor_skip, const double* __restrict__ tensor_ss,
+                                  int32_t* __restrict__ skipped, int grad_clip, double max_norm, double* clip) {
+  __shared__ double red[kThreads / 32];
+  __shared__ int s_any;
+  if (threadIdx.x == 0) s_any = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += kThreads)
+    if (skipped[i]) s_any = 1;
+  __syncthreads();
+  if (!per_tensor_skip && s_any)
+    for (int i = threadIdx.x; i < n; i += kThreads) skipped[i] = 1;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += kThreads)
+    if (!skipped[i]) s = __dadd_rn(s, tensor_ss[i]);
+  const double tot = block_sum(s, red);
+  if (threadIdx.x == 0 && clip != nullptr) {
+    const double norm = __dsqrt_rn(tot);
+    *clip = (grad_clip && norm > max_norm) ? __ddiv_rn(max_norm, norm) : 1.0;
+  }
+}
+
 double debias(double beta, int64_t t) {  // optimizer.cpp:63-68
   if (beta == 0.0) return 0.0;
   const double num = 1.0 - std::pow(beta, static_cast<double>(t - 1));
@@ -357,7 +459,7 @@ double beta2_warmup(int64_t t, double lambda) {  // optimizer.cpp:44-49
   return std::min(b, std::nextafter(1.0, 0.0));
 }
 
-std::vector<Group> make_groups(const sb_adamw_tensor* ts, int n, int64_t* total_blocks) {
+std::vector<Group> make_groups(const sb_adamw_tensor* ts, int n, int64_t* total_blocks, const sb_adamw_extras* ex) {
   std::vector<Group> groups;
   Group cur{};
   int64_t blocks_all = 0;
@@ -378,7 +480,10 @@ std::vector<Group> make_groups(const sb_adamw_tensor* ts, int n, int64_t* total_
     d.block0 = blocks_all;  // partials are global across groups (the grad-clip pass shares them)
     d.nblocks = nb;
     d.index = i;
-    d.vec = a16(d.theta) && a16(d.grad) && a16(d.v) && a16(d.u) && (d.numel % 4 == 0);
+    d.shadow = ex && ex->shadow_bf16 ? static_cast<__nv_bfloat16*>(ex->shadow_bf16[i]) : nullptr;
+    d.word = ex && ex->absmax_word ? ex->absmax_word[i] : nullptr;
+    d.vec = a16(d.theta) && a16(d.grad) && a16(d.v) && a16(d.u) && (d.numel % 4 == 0) &&
+            (d.shadow == nullptr || (reinterpret_cast<uintptr_t>(d.shadow) & 7u) == 0);
     cur.total_blocks += nb;
     blocks_all += nb;
   }
@@ -411,30 +516,33 @@ extern "C" sb_status sb_stableadamw_workspace_size(const sb_adamw_tensor* tensor
   if (!bytes || (ntensors > 0 && !tensors)) return sb::fail(SB_ERR_INVALID_ARGUMENT, "optimizer_step", "null argument");
   int64_t total = 0;
   for (int i = 0; i < ntensors; ++i) total += (tensors[i].numel + kChunk - 1) / kChunk;
-  // partials (one double per chunk), the grad-clip factor, eta per group tensor, sync words
-  // (task counter + per group tensor: finished phase-1 chunks, eta-ready flag)
-  *bytes = static_cast<size_t>(total + 2 + kMaxGroup) * sizeof(double) + (2 * kMaxGroup + 2) * sizeof(unsigned int) + 64;
+  // partials (one double per chunk), the grad-clip factor, eta per group tensor, per caller
+  // tensor the statistics pass's sum of squares (double), skip flag and |g'| max word, sync
+  // words (task counter + per group tensor: finished phase-1 chunks, eta-ready flag)
+  *bytes = static_cast<size_t>(total + 2 + kMaxGroup + ntensors) * sizeof(double) +
+           static_cast<size_t>(2 * ntensors + 2 * kMaxGroup + 2) * sizeof(unsigned int) + 64;
   return SB_OK;
 }
 
-extern "C" sb_status sb_stableadamw_step(sb_handle h, const sb_adamw_tensor* tensors, int ntensors,
-                                         const sb_adamw_hparams* hp, int64_t t, double* rms_out, double* eta_out,
-                                         void* workspace, size_t workspace_bytes) {
+extern "C" sb_status sb_stableadamw_step_ex(sb_handle h, const sb_adamw_tensor* tensors, int ntensors,
+                                            const sb_adamw_hparams* hp, int64_t t, const sb_adamw_extras* ex,
+                                            double* rms_out, double* eta_out, void* workspace, size_t workspace_bytes) {
   const char* op = "optimizer_step";
-  if (!h || !hp) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "null argument");
+  if (!h || !hp || (ntensors > 0 && !tensors)) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "null argument");
   if (t < 1) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "t must be >= 1");  // optimizer.cpp:104
   for (int i = 0; i < ntensors; ++i)  // empty tensors may come with null data pointers
     if ((tensors[i].numel != 0 && (!tensors[i].theta || !tensors[i].grad || !tensors[i].v || !tensors[i].u)) ||
         tensors[i].numel < 0)
       return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "null tensor reference");  // :107-108
   if (hp->clipping == SB_CLIP_GRAD && !(hp->max_grad_norm > 0))
-    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "max_grad_norm must be > 0");
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, "grad_clip", "max_norm must be > 0");
+  if (ex && !(ex->loss_scale > 0)) return sb::fail(SB_ERR_INVALID_ARGUMENT, "loss scaler", "scale must be > 0");
   size_t need = 0;
   sb_stableadamw_workspace_size(tensors, ntensors, &need);
   if (!workspace || workspace_bytes < need) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "workspace too small");
   cudaSetDevice(h->device);
 
-  Coeffs c;
+  Coeffs c{};
   c.b1 = debias(hp->beta1, t);
   c.b2 = hp->beta2_warmup_lambda > 0 ? beta2_warmup(t, hp->beta2_warmup_lambda) : debias(hp->beta2, t);
   c.omb1 = 1.0 - c.b1;
@@ -444,36 +552,66 @@ extern "C" sb_status sb_stableadamw_step(sb_handle h, const sb_adamw_tensor* ten
   c.alpha = hp->alpha;
   c.wd = hp->weight_decay;
   c.update_clip = hp->clipping == SB_CLIP_UPDATE;
+  if (ex && ex->loss_scale != 1.0) {
+    int e2 = 0;
+    const double m = std::frexp(ex->loss_scale, &e2);
+    const bool pow2 = m == 0.5 && e2 - 1 >= -126 && e2 - 1 <= 126;  // 1/scale exact in fp32
+    c.scale_mode = pow2 ? 1 : 2;
+    c.inv_scale_f = pow2 ? static_cast<float>(1.0 / ex->loss_scale) : 0.0f;
+    c.scale = ex->loss_scale;
+  }
 
   int64_t total_blocks = 0;
-  const std::vector<Group> groups = make_groups(tensors, ntensors, &total_blocks);
+  const std::vector<Group> groups = make_groups(tensors, ntensors, &total_blocks, ex);
   double* partials = static_cast<double*>(workspace);
   double* clip = partials + total_blocks;
+  double* eta_buf = clip + 1;
+  double* tensor_ss = eta_buf + kMaxGroup;
+  unsigned int* skip_int = reinterpret_cast<unsigned int*>(tensor_ss + ntensors);
+  unsigned int* amax_int = skip_int + ntensors;
+  unsigned int* sync = amax_int + ntensors;
 
-  if (hp->clipping == SB_CLIP_GRAD) {
+  // statistics pass: needed by the skip decision, the telemetry and the global-norm clip
+  const bool stats = hp->clipping == SB_CLIP_GRAD ||
+                     (ex && (ex->skipped || ex->grad_absmax || ex->loss_scale != 1.0));
+  int32_t* skipped = ex && ex->skipped ? ex->skipped : reinterpret_cast<int32_t*>(skip_int);
+  unsigned int* amax = ex && ex->grad_absmax ? reinterpret_cast<unsigned int*>(ex->grad_absmax) : nullptr;
+  if (stats && ntensors > 0) {
+    SB_CUDA_CHECK(op, cudaMemsetAsync(tensor_ss, 0, sizeof(double) * ntensors, h->stream));
+    SB_CUDA_CHECK(op, cudaMemsetAsync(skipped, 0, sizeof(int32_t) * ntensors, h->stream));
+    if (amax) SB_CUDA_CHECK(op, cudaMemsetAsync(amax, 0, sizeof(unsigned int) * ntensors, h->stream));
     int64_t off = 0;
     for (const Group& g : groups) {
+      SB_CUDA_CHECK(op, cudaMemsetAsync(sync, 0, sizeof(unsigned int) * g.count, h->stream));
       h->launches++;
-      k_sumsq<<<static_cast<unsigned>(g.total_blocks), kThreads, 0, h->stream>>>(g, partials, off);
+      k_gradstats<<<static_cast<unsigned>(g.total_blocks), kThreads, 0, h->stream>>>(g, c, partials, off, sync,
+                                                                                       tensor_ss, skipped, amax);
       off += g.total_blocks;
     }
     h->launches++;
-    k_clip_factor<<<1, kThreads, 0, h->stream>>>(partials, off, hp->max_grad_norm, clip);
+    k_gradstats_final<<<1, kThreads, 0, h->stream>>>(ntensors, ex ? ex->per_tensor_skip : 1, tensor_ss, skipped,
+                                                     hp->clipping == SB_CLIP_GRAD, hp->max_grad_norm, clip);
     SB_LAUNCH_CHECK(op);
+    c.skipped = ex ? skipped : nullptr;
   }
   // persistent task-list kernel per group; sync words (task counter + per-tensor phase-1
-  // counts) zeroed once per step
-  double* eta_buf = clip + 1;
-  unsigned int* sync = reinterpret_cast<unsigned int*>(eta_buf + kMaxGroup);
+  // counts) zeroed once per group
+  const bool extra = ex != nullptr;
   int blocks_per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_adamw_persistent, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, extra ? k_adamw_persistent<true> : k_adamw_persistent<false>,
+                                                kThreads, 0);
   blocks_per_sm = std::max(1, blocks_per_sm);
   for (const Group& g : groups) {
     SB_CUDA_CHECK(op, cudaMemsetAsync(sync, 0, sizeof(unsigned int) * (2 * g.count + 1), h->stream));
     const int64_t grid = std::min<int64_t>(g.total_tasks, static_cast<int64_t>(h->num_sms) * blocks_per_sm);
     h->launches++;
-    k_adamw_persistent<<<static_cast<unsigned>(grid), kThreads, 0, h->stream>>>(
-        g, c, hp->clipping == SB_CLIP_GRAD ? clip : nullptr, partials, sync, eta_buf, rms_out, eta_out);
+    const double* cp = hp->clipping == SB_CLIP_GRAD ? clip : nullptr;
+    if (extra)
+      k_adamw_persistent<true><<<static_cast<unsigned>(grid), kThreads, 0, h->stream>>>(g, c, cp, partials, sync, eta_buf,
+                                                                                       rms_out, eta_out);
+    else
+      k_adamw_persistent<false><<<static_cast<unsigned>(grid), kThreads, 0, h->stream>>>(g, c, cp, partials, sync,
+                                                                                        eta_buf, rms_out, eta_out);
   }
   if (rms_out || eta_out) {
     EmptyList e{};
@@ -493,4 +631,10 @@ extern "C" sb_status sb_stableadamw_step(sb_handle h, const sb_adamw_tensor* ten
   }
   SB_LAUNCH_CHECK(op);
   return SB_OK;
+}
+
+extern "C" sb_status sb_stableadamw_step(sb_handle h, const sb_adamw_tensor* tensors, int ntensors,
+                                         const sb_adamw_hparams* hp, int64_t t, double* rms_out, double* eta_out,
+                                         void* workspace, size_t workspace_bytes) {
+  return sb_stableadamw_step_ex(h, tensors, ntensors, hp, t, nullptr, rms_out, eta_out, workspace, workspace_bytes);
 }

@@ -235,6 +235,28 @@ def quantize_tensorwise_transpose(x: torch.Tensor, check: bool = True) -> Quanti
     return QuantizedMatrix(qt, st, TENSOR)
 
 
+def quantize_tensorwise_from_absmax(x: torch.Tensor, absmax_word: torch.Tensor, check: bool = True,
+                                    with_transpose: bool = False):
+    """quantize_tensorwise with the absmax already known (the word optimizer_step_ex writes with
+    the bf16 shadow weight): one pass, payloads bit-identical to quantize_tensorwise(x)."""
+    _need_cuda(x, absmax_word)
+    x = x.contiguous()
+    r, c = x.shape
+    q = torch.empty((r, c), dtype=torch.int8, device=x.device)
+    qt = torch.empty((c, r), dtype=torch.int8, device=x.device) if with_transpose else None
+    st = torch.empty(1, dtype=torch.float32, device=x.device)
+    h = A.handle(x.device.index)
+    A.check(h.lib.sb_quantize_tensorwise_from_absmax(h.h, _p(x), _dt(x), r, c, c, _p(absmax_word), _p(q), c, _p(qt),
+                                                      r, _p(st)))
+    try:
+        _check_nonfinite(h, check)
+    except InvalidArgument:
+        raise InvalidArgument(A.SB_ERR_NONFINITE, "quantize_tensorwise: non-finite input") from None
+    if with_transpose:
+        return QuantizedMatrix(q, st, TENSOR), QuantizedMatrix(qt, st, TENSOR)
+    return QuantizedMatrix(q, st, TENSOR)
+
+
 def quantize_fp8(x: torch.Tensor, fmt: int, axis: int, check: bool = True) -> QuantizedMatrix:
     """quantize.cpp:161-176; payload stored as e4m3/e5m2 bytes (uint8)."""
     _need_cuda(x)
@@ -432,7 +454,7 @@ def workspace_views(ctx: LinearContext) -> dict:
 def linear_forward(mode: LinearMode, x: torch.Tensor, w: torch.Tensor, ctx: LinearContext | None = None,
                    workspace: torch.Tensor | None = None, check: bool = True,
                    bias: torch.Tensor | None = None, x_q: QuantizedMatrix | None = None,
-                   residual: torch.Tensor | None = None) -> torch.Tensor:
+                   residual: torch.Tensor | None = None, w_absmax: torch.Tensor | None = None) -> torch.Tensor:
     """linear.cpp:113-164: Y = X W^T through the variant's quantized path. `bias` (fp32, m)
     is optional and fused into the GEMM epilogue (sb_linear_forward_bias). `x_q`: X already
     quantized row-wise by its producer (gelu_quantize_rowwise), skipping that pass."""
@@ -451,7 +473,21 @@ def linear_forward(mode: LinearMode, x: torch.Tensor, w: torch.Tensor, ctx: Line
     y = torch.empty((b, m), dtype=x.dtype, device=x.device)
     h = A.handle(x.device.index)
     raw = A.LinearCtx()
-    if residual is not None:
+    if w_absmax is not None:  # W's tensor-wise absmax word from optimizer_step_ex: sb_linear_forward_ex
+        if w_absmax.dtype != torch.int32 or w_absmax.numel() != 1 or not w_absmax.is_cuda:
+            raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "linear_forward: w_absmax must be one int32 device word")
+        if bias is not None:
+            if bias.dtype != torch.float32 or bias.shape != (m,) or not bias.is_cuda:
+                raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "linear_forward: bias must be fp32 of shape (m,)")
+            bias = bias.contiguous()
+        if residual is not None:
+            if residual.shape != (b, m) or residual.dtype != x.dtype or not residual.is_cuda:
+                raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "linear_forward: residual must be b x m of X's dtype")
+            residual = residual.contiguous()
+        st = h.lib.sb_linear_forward_ex(h.h, C.byref(mode.c()), _p(x), _p(x_q.payload if x_q else None),
+                                        _p(x_q.state if x_q else None), _p(w), _p(w_absmax), _p(bias), _p(residual),
+                                        _dt(x), b, n, m, _p(y), C.byref(raw), _p(workspace), workspace.numel())
+    elif residual is not None:
         if residual.shape != (b, m) or residual.dtype != x.dtype or not residual.is_cuda:
             raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "linear_forward: residual must be b x m of X's dtype")
         residual = residual.contiguous()
@@ -617,3 +653,56 @@ def optimizer_step(tensors: list[TensorRef], hp: OptimizerHyperparams, t: int,
         return out
     o = out.cpu()
     return [(float(o[0, i]), float(o[1, i])) for i in range(n)]
+
+
+@dataclass
+class LossScaler:
+    """optimizer.hpp:45-48."""
+    scale: float = 1.0
+    per_tensor_skip: bool = True
+
+
+def optimizer_step_ex(tensors: list[TensorRef], hp: OptimizerHyperparams, t: int, scaler: LossScaler | None = None,
+                      shadows: list | None = None, workspace: torch.Tensor | None = None):
+    """The trainer's update path (trainer.cpp:127-155) fused into the optimizer's passes
+    (sb_stableadamw_step_ex): filter_nonfinite's unscaling and per-tensor skip, grad_absmax
+    telemetry, the in-step clip over the applied tensors, and — for tensors given a
+    shadow = (bf16 tensor of the param's shape, int32 word) — the next forward's bf16 weight
+    and its tensor-wise absmax. Returns a dict of device tensors: rms, eta (float64 [n]),
+    skipped (int32 [n]), grad_absmax (float32 [n]); no host synchronisation."""
+    if t < 1:
+        raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "optimizer_step: t must be >= 1")
+    if hp.lr_schedule is None:
+        raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "optimizer_step: lr_schedule not set")
+    scaler = scaler or LossScaler()
+    n = len(tensors)
+    arr = (A.AdamwTensor * max(n, 1))()
+    for i, r in enumerate(tensors):
+        if not (r.param.shape == r.grad.shape == r.v.shape == r.u.shape):
+            raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, f"optimizer_step: shape mismatch for {r.name}")
+        arr[i] = A.AdamwTensor(r.param.data_ptr(), r.grad.data_ptr(), r.v.data_ptr(), r.u.data_ptr(), r.param.numel())
+    dev = tensors[0].param.device if n else torch.device("cuda")
+    if workspace is None:
+        nbytes = C.c_size_t()
+        A.check(A.load().sb_stableadamw_workspace_size(arr, n, C.byref(nbytes)))
+        workspace = torch.empty(nbytes.value, dtype=torch.uint8, device=dev)
+    out = {"rms": torch.empty(max(n, 1), dtype=torch.float64, device=dev),
+           "eta": torch.empty(max(n, 1), dtype=torch.float64, device=dev),
+           "skipped": torch.empty(max(n, 1), dtype=torch.int32, device=dev),
+           "grad_absmax": torch.empty(max(n, 1), dtype=torch.float32, device=dev)}
+    sh = (C.c_void_p * max(n, 1))()
+    wd = (C.c_void_p * max(n, 1))()
+    for i in range(n):
+        s_ = shadows[i] if shadows else None
+        if s_ is not None:
+            if s_[0].dtype != torch.bfloat16 or s_[0].numel() != tensors[i].param.numel() or s_[1].dtype != torch.int32:
+                raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "optimizer_step: shadow must be (bf16 like param, int32 word)")
+            sh[i], wd[i] = s_[0].data_ptr(), s_[1].data_ptr()
+    ex = A.AdamwExtras(float(scaler.scale), int(scaler.per_tensor_skip), out["skipped"].data_ptr(),
+                       out["grad_absmax"].data_ptr(), sh, wd)
+    hpc = A.AdamwHparams(float(hp.lr_schedule(t)), hp.beta1, hp.beta2, hp.beta2_warmup_lambda, hp.eps,
+                         hp.weight_decay, hp.max_grad_norm, int(hp.clipping))
+    h = A.handle(dev.index)
+    A.check(h.lib.sb_stableadamw_step_ex(h.h, arr, n, C.byref(hpc), t, C.byref(ex), _p(out["rms"]), _p(out["eta"]),
+                                         _p(workspace), workspace.numel()))
+    return {k: v[:n] for k, v in out.items()}
