@@ -363,7 +363,12 @@ def run_ours(args):
 
     stream = torch.cuda.current_stream(dev)
     side = torch.cuda.Stream(dev)
-    ar = dp.GradAllReduce()
+    # the dW all-reduce: the library's own NCCL communicator (sb_dp_init, csrc/dp.cu) when the
+    # ranks run NCCL; torch.distributed only for the gloo test hook
+    comm = None
+    if world > 1 and torch.distributed.get_backend() == "nccl":
+        comm = dp.NcclComm(h, rank, world)
+    ar = dp.GradAllReduce(comm=comm)
 
     def enqueue(chunk, evs):
         """Launch one chunk on the current stream, recording an event after every kernel (and
@@ -560,7 +565,8 @@ def run_c5(args):
     """BASELINE.json configs[4]: one StableAdamW step (optimizer.cpp:102-172, update_clip,
     beta1 0.9, beta2 0.99, eps 1e-6, weight decay 0.2) over the ~1.0e9 fp32 parameters of 51
     ViT-H blocks {3840x1280, 1280x1280, 5120x1280, 1280x5120}, whole
-    tensors sharded round-robin over the ranks (strong scaling: total parameters fixed).
+    tensors sharded over the ranks by size (dp.lpt_partition; strong scaling: total parameters
+    fixed).
     HBM-bound: 28 B/param (read theta, g, v, u; write theta, v, u)."""
     import torch
 
@@ -571,7 +577,9 @@ def run_c5(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     shapes = [(3840, 1280), (1280, 1280), (5120, 1280), (1280, 5120)] * 51
-    mine = [s for i, s in enumerate(shapes) if i % world == rank]
+    # whole tensors per rank, size-balanced (LPT: max / mean 1.0065 at 8 ranks; round-robin by
+    # index was 1.36)
+    mine = [shapes[i] for i in dp.lpt_partition([a * b for a, b in shapes], world)[rank]]
     total_params = sum(a * b for a, b in shapes)
     n_mine = sum(a * b for a, b in mine)
     # one flat allocation per state array, tensors are views (as a trainer's flat buffers)
@@ -630,7 +638,7 @@ def run_c5(args):
                 "vs_baseline": None, "dtype": "f64 math / f32 storage", "data": "synthetic",
                 "config": {"workload": "StableAdamW (update_clip) over 51 ViT-H blocks x 4 weight tensors",
                            "config": "c5", "params_total": total_params, "params_per_rank": n_mine,
-                           "tensors_per_rank": len(mine), "parallelism": f"{world} ranks, whole tensors round-robin",
+                           "tensors_per_rank": len(mine), "parallelism": f"{world} ranks, whole tensors, size-balanced (LPT)",
                            "l2": "state (16 GB) far larger than L2"},
                 "gpu_launches": launches,
                 "roofline": {"bound": "hbm", "kernel": "StableAdamW phase 1 + 2 (csrc/optim.cu)", "achieved": achieved,

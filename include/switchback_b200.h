@@ -391,6 +391,25 @@ sb_status sb_grad_clip_global_norm(sb_handle h, float* const* grads, const int64
 sb_status sb_filter_nonfinite(sb_handle h, const float* const* grads, float* const* out, const int64_t* numel, int n,
                               double scale, int per_tensor_skip, int32_t* skipped);
 
+/* ------------------------------------------------- data parallelism (dp.cu) -- */
+/* Token-dimension data parallelism, one process per GPU. The library opens
+ * libnccl.so.2 at run time. Setup as NCCL's own: rank 0 gets a 128-byte id, every rank receives
+ * it out of band and calls sb_dp_init on its handle. */
+sb_status sb_dp_available(int* nccl_version); /* SB_ERR_UNSUPPORTED without libnccl.so.2 */
+sb_status sb_dp_unique_id(uint8_t* id_out /* 128 bytes */);
+sb_status sb_dp_init(sb_handle h, const uint8_t* id, int rank, int world);
+sb_status sb_dp_rank(sb_handle h, int* rank, int* world);
+/* dW all-reduce (sum, in place) of n device fp32 buffers, on the handle's communication stream
+ * after the work already enqueued on its stream; returns at once (overlaps the next layer's
+ * backward). `bufs` / `numel` are HOST arrays. sb_dp_wait joins it back into the stream. */
+sb_status sb_dp_allreduce_grads_async(sb_handle h, float* const* bufs, const int64_t* numel, int n);
+sb_status sb_dp_wait(sb_handle h);
+/* Stream-ordered small all-reduces: max of uint32 absmax words (AllQuant's token-dimension
+ * scales across ranks, linear.cpp:239-241) and sum of doubles (a sharded optimizer's RMS sums). */
+sb_status sb_dp_allreduce_max_u32(sb_handle h, unsigned int* words, int64_t n);
+sb_status sb_dp_allreduce_sum_f64(sb_handle h, double* vals, int64_t n);
+sb_status sb_dp_destroy(sb_handle h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -295,3 +295,17 @@ def ref_block_fwd_bwd(variant, fmt, params, x, d_out, heads, mlp_ratio=4.0, laye
         grads.pop("ls1")
         grads.pop("ls2")
     return y, dx, grads
+
+
+def ref_linear(variant, fmt, x, w, g):
+    """The reference's linear_forward + linear_backward (oracle/_ref): (y, dx, dw)."""
+    x, w, g = _f32(x), _f32(w), _f32(g)
+    b, n = x.shape
+    m = w.shape[0]
+    y = np.empty((b, m), np.float32)
+    dx = np.empty((b, n), np.float32)
+    dw = np.empty((m, n), np.float32)
+    rc = ref().ref_linear_fwd_bwd(variant, fmt, x, w, _ptr(g), b, n, m, _ptr(y), _ptr(dx), _ptr(dw))
+    if rc != 0:
+        raise OracleError(f"linear: {ref().ref_last_error().decode()}")
+    return y, dx, dw

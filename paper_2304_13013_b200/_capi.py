@@ -38,7 +38,9 @@ EXPORTS = [
     "sb_host_pipeline_wait", "sb_stableadamw_workspace_size", "sb_stableadamw_step",
     "sb_device_alloc", "sb_device_free", "sb_copy_to_device", "sb_copy_to_host", "sb_check_finite", "sb_fp8_cast",
     "sb_transpose_i8", "sb_compute_rms", "sb_grad_clip_global_norm", "sb_filter_nonfinite", "sb_dequantize_values",
-    "sb_set_gemm_path",
+    "sb_set_gemm_path", "sb_dp_available", "sb_dp_unique_id", "sb_dp_init", "sb_dp_rank",
+    "sb_dp_allreduce_grads_async", "sb_dp_wait", "sb_dp_allreduce_max_u32", "sb_dp_allreduce_sum_f64",
+    "sb_dp_destroy",
 ]
 
 
@@ -139,6 +141,15 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             "sb_quantize_tensorwise_from_absmax": ([v, v, i32, i64, i64, i64, v, v, i64, v, i64, v], i32),
             "sb_stableadamw_step_ex": ([v, C.POINTER(AdamwTensor), i32, C.POINTER(AdamwHparams), i64,
                                         C.POINTER(AdamwExtras), v, v, v, sz], i32),
+            "sb_dp_available": ([C.POINTER(i32)], i32),
+            "sb_dp_unique_id": ([v], i32),
+            "sb_dp_init": ([v, v, i32, i32], i32),
+            "sb_dp_rank": ([v, C.POINTER(i32), C.POINTER(i32)], i32),
+            "sb_dp_allreduce_grads_async": ([v, C.POINTER(v), C.POINTER(i64), i32], i32),
+            "sb_dp_wait": ([v], i32),
+            "sb_dp_allreduce_max_u32": ([v, v, i64], i32),
+            "sb_dp_allreduce_sum_f64": ([v, v, i64], i32),
+            "sb_dp_destroy": ([v], i32),
             "sb_linear_backward_prequant": ([v, C.POINTER(LinearMode), C.POINTER(LinearCtx), v, v, v, v, v, i32], i32),
             "sb_linear_forward_residual": ([v, C.POINTER(LinearMode), v, v, v, v, v, v, i32, i64, i64, i64, v,
                                             C.POINTER(LinearCtx), v, sz], i32),

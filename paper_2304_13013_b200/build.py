@@ -22,7 +22,7 @@ BUILD = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libswitchback_b200.so")
 SHIM = os.path.join(PKG, "liblowprec_b200.so")
 
-CU_SOURCES = ["quantize.cu", "gemm.cu", "optim.cu", "capi.cu", "util.cu"]
+CU_SOURCES = ["quantize.cu", "gemm.cu", "optim.cu", "capi.cu", "util.cu", "dp.cu"]
 HEADERS = ["sb_ptx.cuh", "sb_internal.h", "tc_gemm.cuh", "tc_gemm2.cuh", "tc_dw_wide.cuh", "tc_i8_wide.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -63,7 +63,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for f in [ex.submit(_run, c, l) for c, l in jobs]:
             f.result()
     if force or jobs or _newer(LIB, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda" if False else "-lrt"])
+        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lrt", "-ldl"])
     shim_src = os.path.join(CSRC, "lowprec_shim.cpp")
     if os.path.exists(shim_src) and (force or _newer(SHIM, [shim_src, LIB, os.path.join(CSRC, "lowprec_shim.hpp")])):
         _run(["g++", "-O2", "-std=c++20", "-ffp-contract=off", "-fPIC", "-shared", "-I" + os.path.join(ROOT, "include"),

@@ -82,6 +82,7 @@ struct LinearWs {
   float* gt_state;
   int8_t* xt_q;    // AllQuant int8: quantize_rowwise(X^T)  n x b
   float* xt_state;
+  int64_t* raw64;  // AllQuant int8 under data parallelism: dW accumulators summed over ranks  m x n
   size_t total;
 };
 
@@ -109,6 +110,7 @@ LinearWs carve(const sb_linear_mode& md, int64_t b, int64_t n, int64_t m, sb_dty
     w.gt_state = c.take<float>(m);
     w.xt_q = c.take<int8_t>(n * b);
     w.xt_state = c.take<float>(n);
+    w.raw64 = c.take<int64_t>(m * n);
   }
   w.total = c.off + 256;
   return w;
@@ -244,6 +246,7 @@ sb_status sb_destroy(sb_handle h) {
   if (!h) return SB_OK;
   cudaSetDevice(h->device);
   cudaDeviceSynchronize();
+  sb_dp_destroy(h);
   if (h->d_err) cudaFree(h->d_err);
   if (h->gelu_lut) cudaFree(h->gelu_lut);
   if (h->d_scratch) cudaFree(h->d_scratch);
@@ -664,9 +667,16 @@ static sb_status linear_backward_impl(sb_handle h, const sb_linear_mode* mode, c
     }
     if (md.variant == SB_ALLQUANT) {
       // dW = dual_rowwise(qrow(G^T), qrow(X^T)) with K = b (linear.cpp:239-241)
+      if (dw_accumulate) return sb::fail(SB_ERR_UNSUPPORTED, op, "AllQuant dW does not accumulate");
+      if (sb::dp_active(h)) {
+        // token-sharded: the rows of G^T / X^T span every rank's tokens, so the per-feature
+        // absmax is a max over ranks, and dW's integer accumulators are summed over ranks
+        // before the one dequantization (bit-identical to the single-GPU product)
+        return sb::dp_allquant_dw(h, g, ctx->x, dt, b, n, m, ws.gt_q, ws.gt_state, ws.xt_q, ws.xt_state, ws.words,
+                                  ws.raw64, dw);
+      }
       SB_TRY(q_columnwise(h, g, dt, b, m, m, nullptr, 0, ws.gt_q, b, ws.gt_state, ws.words));
       SB_TRY(q_columnwise(h, ctx->x, dt, b, n, n, nullptr, 0, ws.xt_q, b, ws.xt_state, ws.words));
-      if (dw_accumulate) return sb::fail(SB_ERR_UNSUPPORTED, op, "AllQuant dW does not accumulate");
       return sb::gemm_i8(h, ws.gt_q, ws.gt_state, ws.xt_q, ws.xt_state, SB_SCALE_ROW_ROW, m, n, b, dw, SB_F32, exact);
     }
     if (md.variant == SB_SWITCHBACK_M) {

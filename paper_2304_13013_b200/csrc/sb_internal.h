@@ -30,6 +30,12 @@ struct sb_handle_s {
   bool pool_used[2] = {false, false};
   int pool_next = 0;
   void* gelu_lut = nullptr;  // GELU / GELU' tables for bf16 |x| < 8 (built at sb_create)
+  // data parallelism (dp.cu): NCCL communicator, its stream and the fork / join events
+  void* dp_comm = nullptr;
+  int dp_rank = 0, dp_world = 1;
+  cudaStream_t dp_stream = nullptr;
+  cudaEvent_t dp_ready = nullptr, dp_done = nullptr;
+  bool dp_pending = false;
 };
 
 namespace sb {
@@ -163,5 +169,16 @@ sb_status gemm_bf16_tc(sb_handle h, const void* a, bool a_mn, const void* b, boo
 // gemm_fp8
 sb_status gemm_fp8(sb_handle h, const uint8_t* qa, int fa, const float* sa, int axa, const uint8_t* qb, int fb,
                    const float* sb, int axb, int64_t M, int64_t N, int64_t K, void* out, sb_dtype out_dt);
+
+// dp.cu
+// True when the handle has a communicator of more than one rank (or SB_DP_FORCE=1 with one rank,
+// which runs the multi-rank code paths against the identity collectives).
+bool dp_active(sb_handle h);
+// AllQuant int8 dW under token sharding (linear.cpp:239-241): per-feature absmax of G and X maxed
+// over ranks, column-wise quantization, raw int32 product summed over ranks as int64, one exact
+// dequantization float(double(acc) * s_g * s_x / 16129) into dw (also the int32 scratch).
+sb_status dp_allquant_dw(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t n, int64_t m,
+                         int8_t* gt_q, float* gt_state, int8_t* xt_q, float* xt_state, unsigned int* words,
+                         int64_t* raw64, float* dw);
 
 }  // namespace sb

@@ -91,3 +91,68 @@ def test_shard_rows_cover_exactly():
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             sizes = [b - a for a, b in spans]
             assert max(sizes) - min(sizes) <= 1
+
+
+def _allquant_worker(rank, world, port, T, n, m, out_dir):
+    """AllQuant int8 dW under token sharding, as csrc/dp.cu runs it: per-feature absmax maxed
+    over ranks, column-wise quantization of the local rows, the local raw integer product,
+    summed over ranks as int64, one dequantization (linear.cpp:239-241, :49)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import oracle as O
+    from paper_2304_13013_b200 import dp
+
+    dp.init_from_env(backend="gloo")
+    x, _, g = _inputs(T, n, m)
+    r0, r1 = dp.shard_rows(T, rank, world)
+    gl, xl = g[r0:r1], x[r0:r1]
+    sg = torch.from_numpy(np.abs(gl).max(0, initial=0.0))   # absmax per feature, this rank's tokens
+    sx = torch.from_numpy(np.abs(xl).max(0, initial=0.0))
+    dist.all_reduce(sg, op=dist.ReduceOp.MAX)                # sb_dp_allreduce_max_u32
+    dist.all_reduce(sx, op=dist.ReduceOp.MAX)
+    sg = np.where(sg.numpy() == 0, 1.0, sg.numpy()).astype(np.float32)  # zero-slice sentinel
+    sx = np.where(sx.numpy() == 0, 1.0, sx.numpy()).astype(np.float32)
+    # lround(127 x / s): half away from zero (quantize.cpp:17-20)
+    qg = (np.sign(gl) * np.floor(np.abs(127.0 * gl.astype(np.float64) / sg) + 0.5)).astype(np.int8).T.copy()
+    qx = (np.sign(xl) * np.floor(np.abs(127.0 * xl.astype(np.float64) / sx) + 0.5)).astype(np.int8).T.copy()
+    raw = torch.from_numpy(qg.astype(np.int64) @ qx.astype(np.int64).T)  # local int product [m x n]
+    dist.all_reduce(raw, op=dist.ReduceOp.SUM)               # the int64 sum over ranks
+    dw = ((raw.numpy().astype(np.float64) * sg.astype(np.float64)[:, None]) * sx.astype(np.float64)[None, :]
+          / 16129.0).astype(np.float32)
+    np.savez(os.path.join(out_dir, f"aq{rank}.npz"), dw=dw)
+    dist.destroy_process_group()
+
+
+def test_allquant_token_sharded_dw_is_bit_exact(tmp_path):
+    """The data-parallel AllQuant dW (max-reduced feature scales, int64-summed accumulators) is
+    bit-identical to the single-process reference (oracle/_ref when built, else the oracle)."""
+    import oracle as O
+
+    T, n, m, world = 50, 24, 40, 2
+    mp.spawn(_allquant_worker, args=(world, _free_port(), T, n, m, str(tmp_path)), nprocs=world, join=True)
+    x, w, g = _inputs(T, n, m)
+    qgt, sgt = O.quantize(np.ascontiguousarray(g.T), O.ROW)
+    qxt, sxt = O.quantize(np.ascontiguousarray(x.T), O.ROW)
+    want = O.int8_gemm(qgt, sgt, qxt, sxt, want_raw=False)   # matmul_dequant_dual_rowwise, K = T
+    if O.ref_available():
+        _, _, dw_ref = O.ref_linear(4, 0, x, w, g)            # AllQuant int8 through the reference
+        assert np.array_equal(want, dw_ref)
+    for rank in range(world):
+        assert np.array_equal(np.load(tmp_path / f"aq{rank}.npz")["dw"], want)
+
+
+def test_lpt_partition_balances_c5():
+    """C5 (BASELINE configs[4]): 51 ViT-H blocks x 4 weight tensors over 2 / 4 / 8 ranks, whole
+    tensors per rank: max / mean <= 1.02 (round-robin by index: 1.17 / 1.33 / 1.36)."""
+    from paper_2304_13013_b200 import dp
+
+    sizes = [3840 * 1280, 1280 * 1280, 5120 * 1280, 1280 * 5120] * 51
+    for world in (1, 2, 4, 8):
+        parts = dp.lpt_partition(sizes, world)
+        assert sorted(i for p in parts for i in p) == list(range(len(sizes)))
+        loads = [sum(sizes[i] for i in p) for p in parts]
+        assert max(loads) / (sum(loads) / world) <= 1.02
