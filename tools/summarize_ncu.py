@@ -69,7 +69,7 @@ def main(tag):
         json.dump({"captures": summary, "launches": launches}, f, indent=1)
     # human-readable launch list of one bench step (ours) next to the cuBLAS yardstick
     with open(os.path.join(PROF, f"{tag}_launches.md"), "w") as f:
-        f.write(f"# {tag}: ncu launch list of `python tools/prof_step.py` (2 bench steps)\n\n")
+        f.write(f"# {tag}: ncu launch list of `{os.environ.get('LAUNCH_CMD', 'python tools/prof_step.py')}`\n\n")
         f.write("`ncu --metrics gpu__time_duration.sum --clock-control none` — cold-cache, serialised: compare shares.\n\n")
         f.write("| id | kernel | grid | us |\n|---|---|---|---|\n")
         for l in launches:
