@@ -236,15 +236,16 @@ def run_reference_arm(args):
 
 
 # ----------------------------------------------------------------- GPU side
-def dw_traffic(m, n, T):
+def dw_traffic(m, n, T, fused=False):
     """ncu DRAM bytes (read + write) of one dW GEMM launch of this shape, from the committed
-    --set full captures (profiles/dw_gemm_traffic.json, keyed "m x n x T"); None if unmeasured."""
+    --set full captures (profiles/dw_gemm_traffic.json, keyed "m x n x T", "+gq" for the launch
+    that also quantizes G); None if unmeasured."""
     prof = os.path.join(ROOT, "profiles", "dw_gemm_traffic.json")
     if not os.path.exists(prof):
         return None
     with open(prof) as f:
         d = json.load(f)
-    e = d.get("launches", {}).get(f"{m}x{n}x{T}")
+    e = d.get("launches", {}).get(f"{m}x{n}x{T}" + ("+gq" if fused else ""))
     return e["dram_bytes"] if e else None
 
 
@@ -322,6 +323,10 @@ def run_ours(args):
     def dw_gemm(l):
         A.check(h.lib.sb_wgrad(h.h, P(l["g"]), P(l["x"]), A.SB_BF16, T, l["m"], l["n"], P(l["dw"]), 0, 0))
 
+    def dw_gemm_gq(l):  # dW GEMM with quantize_rowwise(G) in the same launch
+        A.check(h.lib.sb_wgrad_quantize_rowwise(h.h, P(l["g"]), P(l["x"]), A.SB_BF16, T, l["m"], l["n"], P(l["dw"]),
+                                                P(l["gq"]), l["m"], P(l["gs"])))
+
     def layer_fwd(l):
         A.check(h.lib.sb_linear_forward(h.h, C.byref(cmode), P(l["x"]), P(l["w"]), A.SB_BF16, T, l["n"], l["m"],
                                         P(l["y"]), C.byref(l["ctx"]), P(l["ws"]), l["ws"].numel()))
@@ -329,7 +334,11 @@ def run_ours(args):
     def layer_bwd(l):
         A.check(h.lib.sb_linear_backward(h.h, C.byref(cmode), C.byref(l["ctx"]), P(l["g"]), P(l["dx"]), P(l["dw"]), 0))
 
-    overlap = plain and not args.no_overlap
+    # G's row-wise quantize: inside the dW launch (default: the dW kernel's idle warps do it while
+    # the tensor cores stream the GEMM), or as its own kernel on a side stream (--unfused-gq), or
+    # serially (--unfused-gq --no-overlap)
+    fused_gq = plain and not args.unfused_gq
+    overlap = plain and not args.no_overlap and not fused_gq
     ops = []
     for l in layers:
         nm, n, m = l["name"], l["n"], l["m"]
@@ -342,7 +351,11 @@ def run_ours(args):
             ops.append(Op(f"{nm} linear_forward", lambda l=l: layer_fwd(l), "layer", 2 * T * m * n))
     for l in reversed(layers):
         nm, n, m = l["name"], l["n"], l["m"]
-        if plain:
+        if fused_gq:
+            ops.append(Op(f"{nm} bf16 dW GEMM m={m} n={n} K={T} + quantize_rowwise G {T}x{m}",
+                          lambda l=l: dw_gemm_gq(l), "dw_gemm", 2 * T * m * n, ar=l["dw"]))
+            ops.append(Op(f"{nm} int8 dX GEMM M={T} N={n} K={m}", lambda l=l: gemm_dx(l), "int8_gemm", 2 * T * m * n))
+        elif plain:
             ops.append(Op(f"{nm} quantize_rowwise G {T}x{m}", lambda l=l: q_g(l), "quantize", T * m * 3 + 4 * T,
                           stream="side" if overlap else "main"))
             ops.append(Op(f"{nm} bf16 dW GEMM m={m} n={n} K={T}", lambda l=l: dw_gemm(l), "dw_gemm", 2 * T * m * n,
@@ -486,6 +499,8 @@ def run_ours(args):
                    # bench.cpp:83-89: (2 q_row + q_tensor + q_tt) / switchback_fwd_bwd
                    "quantize_fraction": cls_us("quantize") / step_us,
                    "quantize_fraction_critical_path": cls_us("quantize", True) / step_us,
+                   "quantize_note": ("standalone quantize kernels only: G's row-wise quantize runs inside the dW "
+                                     "GEMM launches (dw_gemm rows)") if fused_gq else "all quantize kernels",
                    "share_of_step": {c: cls_us(c) / step_us for c in ("int8_gemm", "dw_gemm", "quantize")},
                    "timing": "CUDA events recorded between kernels inside each step's graph, mean over the timed steps"}
     roof = None
@@ -495,16 +510,19 @@ def run_ours(args):
         flops = sum(per[k["op"]][0].work for k in dw_rows)
         achieved = flops / dw_us / 1e6
         peak = pk["bf16_tflops"]
-        trafs = [dw_traffic(l["m"], l["n"], T) for l in layers]
+        trafs = [dw_traffic(l["m"], l["n"], T, fused_gq) for l in layers]
         roof = {"bound": "tensor",
-                "kernel": "bf16 dW GEMM (tcgen05 kind::f16 cta_group::2, 256x384 one-wave tiles, MN-major operands)",
+                "kernel": "bf16 dW GEMM (tcgen05 kind::f16 cta_group::2, 256x384 one-wave tiles, MN-major operands)" +
+                          (" with quantize_rowwise(G) in its idle warps (the launch's time includes it)"
+                           if fused_gq else ""),
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "peak_source": f"{pk['source']} bf16 burst (MEASURED_PEAKS.json bf16_tflops: the kernel is timed "
                                f"inside a {ms * args.steps:.0f} ms region); sustained figure "
                                f"{pk['bf16_tflops_sustained']}, datasheet dense 2250",
                 "traffic": (sum(trafs) / len(trafs)) if all(t is not None for t in trafs) else None,
                 "traffic_source": "profiles/dw_gemm_traffic.json (ncu --set full dram__bytes_read+write, per launch)",
-                "algorithmic_bytes_per_launch": [2 * T * (l["m"] + l["n"]) + 4 * l["m"] * l["n"] for l in layers],
+                "algorithmic_bytes_per_launch": [2 * T * (l["m"] + l["n"]) + 4 * l["m"] * l["n"] +
+                                                 ((T * l["m"] * 3 + 4 * T) if fused_gq else 0) for l in layers],
                 "share_of_step": dw_us / step_us,
                 "flops_per_launch": [2 * l["m"] * l["n"] * T for l in layers]}
     int8_ops_step = sum(4.0 * l["m"] * l["n"] * T for l in layers)
@@ -537,7 +555,10 @@ def run_ours(args):
                            "tokens_per_gpu": T, "global_tokens": T * world,
                            "layers": [f"{n}->{m}" for _, n, m in layers_cfg], "parallelism": f"dp{world} (token shards)",
                            "l2": "inputs larger than L2 (X, G operands 168-673 MB each)",
-                           "cuda_graphs": not args.no_graph, "g_quantize_overlaps_dw": overlap},
+                           "cuda_graphs": not args.no_graph,
+                           "g_quantize": ("fused into the dW GEMM launch (sb_wgrad_quantize_rowwise)" if fused_gq else
+                                          "own kernel on a side stream next to the dW GEMM" if overlap else
+                                          "own kernel, serial") if plain else "inside sb_linear_backward"},
                 "gpu_launches": launches,
                 "roofline": roof,
                 "int8_tops_per_step": int8_ops_step / 1e12,
@@ -885,6 +906,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="quantize G after dW on one stream")
+    ap.add_argument("--unfused-gq", action="store_true",
+                    help="quantize G in its own kernel instead of inside the dW GEMM launch (A/B)")
     ap.add_argument("--qkv-packed", action="store_true", help="vit_block: one scale for the packed qkv weight")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -84,8 +84,16 @@ uint64_t sb_launch_count(sb_handle h);
  * SB_GEMM_AUTO: 2-CTA (cta_group::2) 256 x 256 tiles when the problem fills the SM pairs,
  * else 1-CTA 128 x 256; the other values force one form (results are identical). */
 /* AUTO picks per shape; 1CTA = 128 x 256 tiles; 2CTA = cta_group::2 256 x 256 tiles; WIDE = the
- * transposed cta_group::2 256 x 384 int8 / fp8 kernel (tc_i8_wide.cuh) wherever it applies. */
-typedef enum sb_gemm_path { SB_GEMM_AUTO = 0, SB_GEMM_1CTA = 1, SB_GEMM_2CTA = 2, SB_GEMM_WIDE = 3 } sb_gemm_path;
+ * transposed cta_group::2 256 x 384 int8 / fp8 kernel (tc_i8_wide.cuh) wherever it applies;
+ * 2CTA_MC = the 256 x 256 kernel in clusters of two CTA pairs that share (TMA-multicast) the
+ * B operand of vertically adjacent tiles (tc_gemm2.cuh Pipe2<2>). */
+typedef enum sb_gemm_path {
+  SB_GEMM_AUTO = 0,
+  SB_GEMM_1CTA = 1,
+  SB_GEMM_2CTA = 2,
+  SB_GEMM_WIDE = 3,
+  SB_GEMM_2CTA_MC = 4
+} sb_gemm_path;
 sb_status sb_set_gemm_path(sb_handle h, int path);
 
 /* Device memory + synchronous copies on the handle's stream (for FFI callers without a CUDA runtime). */
@@ -172,6 +180,15 @@ sb_status sb_matmul_f32(sb_handle h, const float* a, const float* bt, int64_t r,
  * accumulate=1 adds into dw (fp32) instead of overwriting. */
 sb_status sb_wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m, int64_t n,
                    float* dw, int exact, int accumulate);
+/* The SwitchBack backward's two consumers of G in one launch (linear.cpp:232-245 reads G for
+ * quantize_rowwise(G) -> dX and for wgrad_full_precision(G, X) -> dW): dw[m x n] = g^T x as
+ * sb_wgrad (exact=0, no accumulate), and g_q[b x m] (row stride ldq bytes) / g_state[b] =
+ * sb_quantize_rowwise(g), bit for bit. On the one-wave bf16 dW kernel the quantize runs in its
+ * otherwise idle warps while the tensor cores stream the GEMM; elsewhere it is a separate launch
+ * before the GEMM. Replaces the pair quantize_rowwise(grad_output) + wgrad_full_precision
+ * issued by linear_backward (linear.cpp:232, :245). */
+sb_status sb_wgrad_quantize_rowwise(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m,
+                                    int64_t n, float* dw, int8_t* g_q, int64_t ldq, float* g_state);
 
 /* fp8 GEMM (the SwitchBack fp8 simulation, linear.cpp:148-153 / :250-266): out = (qa . qb^T)
  * * sa_i * sb_j with qa/qb e4m3|e5m2 bytes, K-major; states per row (row axis) or broadcast

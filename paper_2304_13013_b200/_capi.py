@@ -22,14 +22,14 @@ SB_STANDARD, SB_SWITCHBACK, SB_SWITCHBACK_M, SB_SWITCHBACK_Q, SB_ALLQUANT = rang
 SB_INT8, SB_FP8 = range(2)
 SB_SCALE_ROW_TENSOR, SB_SCALE_ROW_ROW, SB_SCALE_NONE = range(3)
 SB_CLIP_NONE, SB_CLIP_UPDATE, SB_CLIP_GRAD = range(3)
-SB_GEMM_AUTO, SB_GEMM_1CTA, SB_GEMM_2CTA, SB_GEMM_WIDE = range(4)
+SB_GEMM_AUTO, SB_GEMM_1CTA, SB_GEMM_2CTA, SB_GEMM_WIDE, SB_GEMM_2CTA_MC = range(5)
 
 # every symbol include/switchback_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = [
     "sb_abi_version", "sb_create", "sb_destroy", "sb_set_stream", "sb_synchronize", "sb_error_word",
     "sb_last_error", "sb_launch_count", "sb_quantize_rowwise", "sb_quantize_columnwise",
     "sb_quantize_tensorwise", "sb_dequantize", "sb_quantize_fp8", "sb_dequantize_fp8", "sb_gemm_i8",
-    "sb_gemm_i8_epilogue", "sb_matmul_f32", "sb_wgrad", "sb_gemm_fp8", "sb_linear_workspace_size", "sb_linear_workspace_layout", "sb_linear_forward", "sb_linear_forward_bias",
+    "sb_gemm_i8_epilogue", "sb_matmul_f32", "sb_wgrad", "sb_wgrad_quantize_rowwise", "sb_gemm_fp8", "sb_linear_workspace_size", "sb_linear_workspace_layout", "sb_linear_forward", "sb_linear_forward_bias",
     "sb_linear_forward_prequant", "sb_linear_backward_prequant", "sb_linear_forward_ex", "sb_quantize_tensorwise_from_absmax",
     "sb_stableadamw_step_ex", "sb_gelu_quantize_rowwise", "sb_linear_forward_residual",
     "sb_gelu_backward_quantize_rowwise", "sb_layernorm_quantize_rowwise", "sb_layernorm_backward_workspace_size",
@@ -126,6 +126,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             "sb_gemm_i8_epilogue": ([v, v, v, v, v, i32, i64, i64, i64, v, v, i64, v, i32, i32], i32),
             "sb_matmul_f32": ([v, v, v, i64, i64, i64, v], i32),
             "sb_wgrad": ([v, v, v, i32, i64, i64, i64, v, i32, i32], i32),
+            "sb_wgrad_quantize_rowwise": ([v, v, v, i32, i64, i64, i64, v, v, i64, v], i32),
             "sb_gemm_fp8": ([v, v, i32, v, i32, v, i32, v, i32, i64, i64, i64, v, i32], i32),
             "sb_linear_workspace_size": ([C.POINTER(LinearMode), i64, i64, i64, C.POINTER(sz)], i32),
             "sb_linear_workspace_layout": ([C.POINTER(LinearMode), i64, i64, i64, C.POINTER(LinearWsLayout)], i32),

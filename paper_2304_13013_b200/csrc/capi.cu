@@ -273,7 +273,7 @@ sb_status sb_set_stream(sb_handle h, void* s) {
 
 sb_status sb_set_gemm_path(sb_handle h, int path) {
   if (!h) return sb::fail(SB_ERR_INVALID_ARGUMENT, "sb_set_gemm_path", "null handle");
-  if (path < SB_GEMM_AUTO || path > SB_GEMM_WIDE) return sb::fail(SB_ERR_INVALID_ARGUMENT, "sb_set_gemm_path", "bad path");
+  if (path < SB_GEMM_AUTO || path > SB_GEMM_2CTA_MC) return sb::fail(SB_ERR_INVALID_ARGUMENT, "sb_set_gemm_path", "bad path");
   h->gemm_path = path;
   return SB_OK;
 }
@@ -413,6 +413,22 @@ sb_status sb_wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64
   if (!g || !x || !dw || !float_dtype(dt) || b < 0 || m < 0 || n < 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
   if (m == 0 || n == 0) return SB_OK;
   return sb::wgrad(h, g, x, dt, b, m, n, dw, exact, accumulate);
+}
+
+sb_status sb_wgrad_quantize_rowwise(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m,
+                                    int64_t n, float* dw, int8_t* g_q, int64_t ldq, float* g_state) {
+  const char* op = "linear_backward";
+  SB_TRY(check_h(h, op));
+  // an empty G is rejected as quantize_rowwise rejects it (require_quantizable, quantize.cpp:11-14)
+  if (b <= 0 || m <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, "quantize_rowwise", "empty matrix");
+  if (!float_dtype(dt) || n < 0 || ldq < m || !g || !g_q || !g_state || (n > 0 && (!x || !dw)))
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  const sb::RowQuant rq{g_q, ldq, g_state};
+  if (n == 0) {
+    SB_TRYC(op, sb::launch_quantize_rowwise(h, g, dt, b, m, m, g_q, ldq, g_state));
+    return SB_OK;
+  }
+  return sb::wgrad(h, g, x, dt, b, m, n, dw, 0, 0, &rq);
 }
 
 sb_status sb_gemm_fp8(sb_handle h, const uint8_t* qa, sb_fp8_format fa, const float* sa, sb_axis axa, const uint8_t* qb,
@@ -651,9 +667,17 @@ static sb_status linear_backward_impl(sb_handle h, const sb_linear_mode* mode, c
     // G quantized row-wise here, or already by its producer (fused GELU backward + quantize)
     int8_t* gq = ws.g_q;
     float* gs = ws.g_state;
+    bool dw_done = false;
     if (gq_in) {
       gq = const_cast<int8_t*>(gq_in);
       gs = const_cast<float*>(gs_in);
+    } else if (md.variant == SB_SWITCHBACK) {
+      // dW = G^T X first, with the row-wise quantize of G riding in the same launch (the dW
+      // kernel's idle warps, tc_dw_wide.cuh); dX below consumes G_q. Both only read G
+      // (linear.cpp:232-245), so the order does not change any result.
+      const sb::RowQuant rq{gq, m, gs};
+      SB_TRY(sb::wgrad(h, g, ctx->x, dt, b, m, n, dw, exact, dw_accumulate, &rq));
+      dw_done = true;
     } else {
       SB_TRYC(op, sb::launch_quantize_rowwise(h, g, dt, b, m, m, gq, m, gs));
     }
@@ -684,6 +708,7 @@ static sb_status linear_backward_impl(sb_handle h, const sb_linear_mode* mode, c
       SB_TRYC(op, sb::launch_dequantize(h, ctx->x_q, b, n, n, ctx->x_state, SB_AXIS_ROW, ws.deq, dt, n));
       return sb::wgrad(h, g, ws.deq, dt, b, m, n, dw, exact, dw_accumulate);
     }
+    if (dw_done) return SB_OK;
     return sb::wgrad(h, g, ctx->x, dt, b, m, n, dw, exact, dw_accumulate);  // linear.cpp:245
   }
 

@@ -263,7 +263,7 @@ bool encode_operand(CUtensorMap* m, const Operand& o, uint32_t rows, uint32_t mn
 // SB_GEMM_2CTA=0/1 in the environment overrides the AUTO choice; sb_set_gemm_path overrides both.
 bool use_2cta(sb_handle h, int64_t M, int64_t units256) {
   if (h->gemm_path == SB_GEMM_1CTA || h->num_sms < 2) return false;
-  if (h->gemm_path == SB_GEMM_2CTA) return true;
+  if (h->gemm_path == SB_GEMM_2CTA || h->gemm_path == SB_GEMM_2CTA_MC) return true;
   static int env = -2;
   if (env == -2) {
     const char* e = getenv("SB_GEMM_2CTA");
@@ -273,54 +273,82 @@ bool use_2cta(sb_handle h, int64_t M, int64_t units256) {
   return M > 128 && units256 >= h->num_sms / 2;
 }
 
-// 2-CTA launch of pipeline shape CFG (tc_gemm2.cuh Pipe2).
-template <int KIND, int OUT, bool A_MN, bool B_MN, bool SB_COL, int CFG>
-cudaError_t launch_2cta_cfg(sb_handle h, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& d,
-                            const sbtc::Params& p, uint32_t idesc, int units) {
-  auto kern = sbtc2::k_tc_gemm2<KIND, A_MN, B_MN, OUT, SB_COL, CFG>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  static int max_pairs = 0;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sbtc2::SMEM2_BYTES);
-    // persistent grid: only as many CTA pairs as can be co-resident (a pair needs two SMs of
-    // one TPC); launching more would run the surplus as a second wave
+// Per-device cache of a cluster kernel's one-time setup (the max-dynamic-smem attribute is per
+// device context, and so is the co-resident cluster count).
+struct PairCache {
+  std::once_flag once[16];
+  cudaError_t err[16] = {};
+  int pairs[16] = {};
+};
+template <typename Kern>
+int cluster_pairs(sb_handle h, PairCache& c, Kern kern, int smem, int threads, cudaError_t* err, int csize = 2) {
+  const int d = h->device & 15;
+  std::call_once(c.once[d], [&] {
+    c.err[d] = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2 * (h->num_sms / 2));
-    cfg.blockDim = dim3(sbtc::NUM_THREADS);
-    cfg.dynamicSmemBytes = sbtc2::SMEM2_BYTES;
+    cfg.gridDim = dim3(csize * (h->num_sms / csize));
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute attr;
     attr.id = cudaLaunchAttributeClusterDimension;
-    attr.val.clusterDim.x = 2;
+    attr.val.clusterDim.x = csize;
     attr.val.clusterDim.y = 1;
     attr.val.clusterDim.z = 1;
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     int n = 0;
-    if (attr_err != cudaSuccess || cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1)
-      n = h->num_sms / 2;
-    max_pairs = n;
+    if (c.err[d] != cudaSuccess || cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1)
+      n = h->num_sms / csize;
+    c.pairs[d] = n;
     cudaGetLastError();
-    if (getenv("SB_DEBUG")) fprintf(stderr, "[sb] 2-CTA GEMM (cfg %d): %d co-resident pairs\n", CFG, n);
   });
-  if (attr_err != cudaSuccess) return attr_err;
-  const int grid = 2 * (units < max_pairs ? units : max_pairs);
+  *err = c.err[d];
+  return c.pairs[d];
+}
+
+// 2-CTA launch of pipeline shape CFG (tc_gemm2.cuh Pipe2); `units` = pair tiles (CFG 0 / 1)
+// or cluster-of-4 units (CFG 2). Persistent grid: only as many clusters as can be co-resident
+// (a pair needs two SMs of one TPC); launching more would run the surplus as a second wave.
+template <int KIND, int OUT, bool A_MN, bool B_MN, bool SB_COL, int CFG>
+cudaError_t launch_2cta_cfg(sb_handle h, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& d,
+                            const sbtc::Params& p, uint32_t idesc, int units) {
+  auto kern = sbtc2::k_tc_gemm2<KIND, A_MN, B_MN, OUT, SB_COL, CFG>;
+  constexpr int CL = sbtc2::Pipe2<CFG>::CL;
+  static PairCache cache;
+  cudaError_t err = cudaSuccess;
+  const int max_clusters = cluster_pairs(h, cache, kern, sbtc2::SMEM2_BYTES, sbtc::NUM_THREADS, &err, CL);
+  if (err != cudaSuccess) return err;
+  if (getenv("SB_DEBUG")) fprintf(stderr, "[sb] 2-CTA GEMM (cfg %d): %d co-resident clusters of %d\n", CFG, max_clusters, CL);
+  const int grid = CL * (units < max_clusters ? units : max_clusters);
   sb::launch_pdl(kern, dim3(grid), dim3(sbtc::NUM_THREADS), sbtc2::SMEM2_BYTES, h->stream, ta, tb, d, p, idesc);
   return cudaGetLastError();
 }
 
-// SB_GEMM_CFG=0|1 picks the 2-CTA pipeline shape (default 0).
+// SB_GEMM_CFG=0|1|2 picks the 2-CTA pipeline shape (tc_gemm2.cuh Pipe2; default 0).
 int gemm2_cfg() {
   static int c = -1;
   if (c < 0) c = getenv("SB_GEMM_CFG") ? atoi(getenv("SB_GEMM_CFG")) : 0;
   return c;
 }
-constexpr int kCfgMnKrows[2] = {64 * sbtc2::Pipe2<0>::ATOMS, 64 * sbtc2::Pipe2<1>::ATOMS};
+// Pipeline shape for one 2-CTA launch: SB_GEMM_2CTA_MC forces the cluster-of-4 multicast form,
+// SB_GEMM_CFG in the environment overrides AUTO, and AUTO takes the multicast form for the
+// 8-bit GEMMs when there is at least one cluster unit per co-resident cluster.
+int gemm2_cfg_for(sb_handle h, const sbtc::Params& p) {
+  if (h->gemm_path == SB_GEMM_2CTA_MC) return 2;
+  if (getenv("SB_GEMM_CFG")) return gemm2_cfg();
+  (void)p;
+  return 0;
+}
+constexpr int kCfgMnKrows[3] = {64 * sbtc2::Pipe2<0>::ATOMS, 64 * sbtc2::Pipe2<1>::ATOMS, 64 * sbtc2::Pipe2<2>::ATOMS};
 
 template <int KIND, int OUT, bool A_MN, bool B_MN, bool SB_COL>
 cudaError_t launch_2cta(sb_handle h, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& d,
-                        const sbtc::Params& p, uint32_t idesc, int units) {
-  if (gemm2_cfg() == 1) return launch_2cta_cfg<KIND, OUT, A_MN, B_MN, SB_COL, 1>(h, ta, tb, d, p, idesc, units);
+                        const sbtc::Params& p, uint32_t idesc, int units, int cfg) {
+  if (cfg == 1) return launch_2cta_cfg<KIND, OUT, A_MN, B_MN, SB_COL, 1>(h, ta, tb, d, p, idesc, units);
+  if (cfg == 2) {
+    const int units4 = ((p.tiles_m + 1) / 2) * p.tiles_n * p.splits;
+    return launch_2cta_cfg<KIND, OUT, A_MN, B_MN, SB_COL, 2>(h, ta, tb, d, p, idesc, units4);
+  }
   return launch_2cta_cfg<KIND, OUT, A_MN, B_MN, SB_COL, 0>(h, ta, tb, d, p, idesc, units);
 }
 
@@ -330,20 +358,23 @@ cudaError_t launch_tc(sb_handle h, const Operand& A, const Operand& B, const CUt
   const int64_t units256 = ((p.M + 255) / 256) * ((p.N + sbtc::BN - 1) / sbtc::BN) * (p.splits < 1 ? 1 : p.splits);
   const bool two = use_2cta(h, p.M, units256);
   CUtensorMap ta, tb;
-  const int mnk = two ? kCfgMnKrows[gemm2_cfg() == 1 ? 1 : 0] : 64;
+  const int cfg = two ? gemm2_cfg_for(h, p) : 0;
+  const int mnk = two ? kCfgMnKrows[cfg] : 64;
   if (!encode_operand(&ta, A, 128, mnk) || !encode_operand(&tb, B, two ? 128 : 256, mnk))
     return cudaErrorInvalidValue;
   p.tma3d = 0;
   if (two && tma3d_enabled()) {
-    const int atoms = gemm2_cfg() == 1 ? sbtc2::Pipe2<1>::ATOMS : sbtc2::Pipe2<0>::ATOMS;
+    const int atoms = cfg == 1 ? sbtc2::Pipe2<1>::ATOMS : sbtc2::Pipe2<0>::ATOMS;
     CUtensorMap t3;
     if (!A.mn && encode_operand3d(&t3, A, 128, atoms)) {
       ta = t3;
       p.tma3d |= 1;
     }
     if (!B.mn && encode_operand3d(&t3, B, 128, atoms)) {
-      tb = t3;
-      p.tma3d |= 2;
+      if (cfg != 2) {  // the cluster-of-4 form multicasts B atom by atom (2D boxes)
+        tb = t3;
+        p.tma3d |= 2;
+      }
     }
   }
   p.tiles_m = static_cast<int>((p.M + (two ? sbtc2::BM2 : sbtc::BM) - 1) / (two ? sbtc2::BM2 : sbtc::BM));
@@ -351,7 +382,7 @@ cudaError_t launch_tc(sb_handle h, const Operand& A, const Operand& B, const CUt
   if (p.splits < 1) p.splits = 1;
   const int units = p.tiles_m * p.tiles_n * p.splits;
   h->launches++;
-  if (two) return launch_2cta<KIND, OUT, A_MN, B_MN, SB_COL>(h, ta, tb, d, p, idesc, units);
+  if (two) return launch_2cta<KIND, OUT, A_MN, B_MN, SB_COL>(h, ta, tb, d, p, idesc, units, cfg);
   static std::once_flag once1;
   static cudaError_t attr_err1 = cudaSuccess;
   std::call_once(once1, [] {
@@ -368,8 +399,9 @@ cudaError_t launch_tc(sb_handle h, const Operand& A, const Operand& B, const CUt
 // One-wave 256 x 384 dW (tc_dw_wide.cuh) when one orientation fits the SM pairs in a single
 // wave; cudaErrorNotSupported = use the 256 x 256 split-K path. G: A operand (MN-major, m
 // wide), X: B operand (n wide); TRANS runs C = X^T G and stores C^T.
+// rq (optional): also quantize G row-wise inside the same launch (tc_dw_wide.cuh QV).
 cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, const CUtensorMap& td, int64_t m, int64_t n,
-                           int64_t T) {
+                           int64_t T, const sb::RowQuant* rq) {
   static int env = -1;
   if (env < 0) env = getenv("SB_DW_WIDE") ? atoi(getenv("SB_DW_WIDE")) : 1;
   if (!env || h->gemm_path == SB_GEMM_1CTA || h->num_sms < 2) return cudaErrorNotSupported;
@@ -377,7 +409,9 @@ cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, cons
   static cudaError_t attr_err = cudaSuccess;
   static std::once_flag once;
   std::call_once(once, [&] {
-    for (auto kern : {sbdw::k_dw_wide<false>, sbdw::k_dw_wide<true>}) {
+    for (auto kern : {sbdw::k_dw_wide<false, 0>, sbdw::k_dw_wide<true, 0>, sbdw::k_dw_wide<false, 1>,
+                      sbdw::k_dw_wide<true, 1>, sbdw::k_dw_wide<false, 5>, sbdw::k_dw_wide<true, 5>,
+                      sbdw::k_dw_wide<false, 20>, sbdw::k_dw_wide<true, 20>}) {
       const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sbdw::SMEM_BYTES);
       if (e != cudaSuccess) attr_err = e;
     }
@@ -393,7 +427,7 @@ cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, cons
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     int n_ = 0;
-    if (attr_err != cudaSuccess || cudaOccupancyMaxActiveClusters(&n_, sbdw::k_dw_wide<false>, &cfg) != cudaSuccess ||
+    if (attr_err != cudaSuccess || cudaOccupancyMaxActiveClusters(&n_, sbdw::k_dw_wide<false, 0>, &cfg) != cudaSuccess ||
         n_ < 1)
       n_ = h->num_sms / 2;
     max_pairs = n_;
@@ -418,46 +452,40 @@ cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, cons
   p.tiles_m = static_cast<int>((p.M + sbdw::WM - 1) / sbdw::WM);
   p.tiles_n = static_cast<int>((p.N + sbdw::WN - 1) / sbdw::WN);
   const int units = p.tiles_m * p.tiles_n;
-  const int grid = 2 * (units < max_pairs ? units : max_pairs);
+  int qv = 0;
+  if (rq) {
+    // G [T x m] row-major bf16 (its MN-major operand view), rows of m / 8 16-byte vectors
+    const int nvec = static_cast<int>(m / 8);
+    qv = nvec == 160 ? 5 : (nvec == 640 ? 20 : 1);  // the ViT-H widths held in registers, else two-pass
+    p.qg = static_cast<const __nv_bfloat16*>(G.ptr);
+    p.q_rows = T;
+    p.q_ld = m;
+    p.q_nvec = nvec;
+    p.q_out = rq->q;
+    p.q_ldq = rq->ldq;
+    p.q_state = rq->state;
+    p.q_err = h->d_err;
+    static int qw = -1;  // SB_DWQ_WARPS: quantizing warps per CTA (measurement knob)
+    if (qw < 0) qw = getenv("SB_DWQ_WARPS") ? std::max(1, std::min(10, atoi(getenv("SB_DWQ_WARPS")))) : 10;
+    p.q_warps = qw;
+  }
+  // with a fused quantize every co-resident pair takes part (pairs without a tile only quantize)
+  const int grid = 2 * (rq ? max_pairs : (units < max_pairs ? units : max_pairs));
   h->launches++;
-  if (trans)
-    sb::launch_pdl(sbdw::k_dw_wide<true>, dim3(grid), dim3(sbtc::NUM_THREADS), sbdw::SMEM_BYTES, h->stream, ta, tb, td, p);
-  else
-    sb::launch_pdl(sbdw::k_dw_wide<false>, dim3(grid), dim3(sbtc::NUM_THREADS), sbdw::SMEM_BYTES, h->stream, ta, tb, td, p);
+  auto go = [&](auto kern) {
+    sb::launch_pdl(kern, dim3(grid), dim3(sbtc::NUM_THREADS), sbdw::SMEM_BYTES, h->stream, ta, tb, td, p);
+  };
+  switch (qv * 2 + (trans ? 1 : 0)) {
+    case 0: go(sbdw::k_dw_wide<false, 0>); break;
+    case 1: go(sbdw::k_dw_wide<true, 0>); break;
+    case 2: go(sbdw::k_dw_wide<false, 1>); break;
+    case 3: go(sbdw::k_dw_wide<true, 1>); break;
+    case 10: go(sbdw::k_dw_wide<false, 5>); break;
+    case 11: go(sbdw::k_dw_wide<true, 5>); break;
+    case 40: go(sbdw::k_dw_wide<false, 20>); break;
+    default: go(sbdw::k_dw_wide<true, 20>); break;
+  }
   return cudaGetLastError();
-}
-
-// Per-device cache of a cluster kernel's one-time setup (the max-dynamic-smem attribute is per
-// device context, and so is the co-resident pair count).
-struct PairCache {
-  std::once_flag once[16];
-  cudaError_t err[16] = {};
-  int pairs[16] = {};
-};
-template <typename Kern>
-int cluster_pairs(sb_handle h, PairCache& c, Kern kern, int smem, int threads, cudaError_t* err) {
-  const int d = h->device & 15;
-  std::call_once(c.once[d], [&] {
-    c.err[d] = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2 * (h->num_sms / 2));
-    cfg.blockDim = dim3(threads);
-    cfg.dynamicSmemBytes = smem;
-    cudaLaunchAttribute attr;
-    attr.id = cudaLaunchAttributeClusterDimension;
-    attr.val.clusterDim.x = 2;
-    attr.val.clusterDim.y = 1;
-    attr.val.clusterDim.z = 1;
-    cfg.attrs = &attr;
-    cfg.numAttrs = 1;
-    int n = 0;
-    if (c.err[d] != cudaSuccess || cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1)
-      n = h->num_sms / 2;
-    c.pairs[d] = n;
-    cudaGetLastError();
-  });
-  *err = c.err[d];
-  return c.pairs[d];
 }
 
 // The 256 x 384 int8 / fp8 kernel runs when forced (sb_set_gemm_path(h, SB_GEMM_WIDE)) or with
@@ -693,9 +721,18 @@ sb_status matmul_f32_seq(sb_handle h, const float* a, int64_t a_rs, int64_t a_ks
 }
 
 sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m, int64_t n, float* dw,
-                int exact, int accumulate) {
+                int exact, int accumulate, const RowQuant* rq) {
   const char* op = "linear_backward";
   CUtensorMap td;
+  // a fused row-wise quantize of G rides in the one-wave dW kernel (bf16 G, 16-byte rows);
+  // anywhere else it is the standalone quantizer, launched first
+  const bool fuse_q = rq && dt == SB_BF16 && !exact && !accumulate && m % 8 == 0 && aligned(g, 16) &&
+                      aligned(rq->q, 16) && rq->ldq % 16 == 0;
+  if (rq && !fuse_q) {
+    const cudaError_t qe = launch_quantize_rowwise(h, g, dt, b, m, m, rq->q, rq->ldq, rq->state);
+    if (qe != cudaSuccess) return cuda_fail(op, qe);
+    rq = nullptr;
+  }
   if (dt == SB_BF16 && !exact && (m % 8 == 0) && (n % 8 == 0) && aligned(g, 16) && aligned(x, 16) && aligned(dw, 16) &&
       b < (1LL << 31) && get_encode() != nullptr && out_tmap(&td, SB_F32, dw, m, n)) {
     // A = G[T x m] and B = X[T x n] read in place as MN-major operands; K = T tokens
@@ -704,9 +741,14 @@ sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t 
     const Operand B{x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, static_cast<uint64_t>(n), static_cast<uint64_t>(b),
                     static_cast<uint64_t>(n * 2), true, 64};
     if (!accumulate) {
-      const cudaError_t we = launch_dw_wide(h, A, B, td, m, n, b);
+      const cudaError_t we = launch_dw_wide(h, A, B, td, m, n, b, rq);
       if (we == cudaSuccess) return SB_OK;
       if (we != cudaErrorNotSupported) return cuda_fail(op, we);
+    }
+    if (rq) {  // the one-wave kernel does not apply to this shape: quantize separately
+      const cudaError_t qe = launch_quantize_rowwise(h, g, dt, b, m, m, rq->q, rq->ldq, rq->state);
+      if (qe != cudaSuccess) return cuda_fail(op, qe);
+      rq = nullptr;
     }
     sbtc::Params p{};
     p.M = static_cast<int>(m);
@@ -742,6 +784,10 @@ sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t 
     return SB_OK;
   }
   // exact sequential (or unaligned fallback): dW[i][j] = sum_t G[t][i] * X[t][j]
+  if (rq) {
+    const cudaError_t qe = launch_quantize_rowwise(h, g, dt, b, m, m, rq->q, rq->ldq, rq->state);
+    if (qe != cudaSuccess) return cuda_fail(op, qe);
+  }
   if (!exact) {
     const sb_status fs = simt_fallback(h, op, m, n, b);
     if (fs != SB_OK) return fs;

@@ -160,8 +160,17 @@ sb_status gemm_i8(sb_handle h, const int8_t* qa, const float* sa, const int8_t* 
                   int64_t M, int64_t N, int64_t K, void* out, sb_dtype out_dt, int exact, const float* bias = nullptr,
                   const void* resid = nullptr, int64_t ld_resid = 0);
 // gemm_bf16.cu
+// Row-wise int8 quantize of G riding along with the dW GEMM (payload q [b x m], row stride ldq
+// bytes, states [b]); identical to launch_quantize_rowwise(G).
+struct RowQuant {
+  int8_t* q;
+  int64_t ldq;
+  float* state;
+};
+// rq (optional): also quantize G row-wise — inside the one-wave dW kernel when it applies,
+// otherwise as a separate launch before the GEMM.
 sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m, int64_t n, float* dw,
-                int exact, int accumulate);
+                int exact, int accumulate, const RowQuant* rq = nullptr);
 sb_status matmul_f32_seq(sb_handle h, const float* a, int64_t a_rs, int64_t a_ks, const float* bt, int64_t b_rs,
                          int64_t b_ks, int64_t r, int64_t c, int64_t k, float* y, int accumulate);
 sb_status gemm_bf16_tc(sb_handle h, const void* a, bool a_mn, const void* b, bool b_mn, int64_t M, int64_t N, int64_t K,

@@ -15,7 +15,17 @@
 // Stages hold 64 tokens: A 128 MN x 64 k (2 SW128 boxes), B 192 MN x 64 k (3 boxes) = 40 KB
 // per CTA, 4 stages. Synchronisation as tc_gemm2.cuh (leader-only full barrier with both
 // CTAs' bytes, multicast commits to both CTAs' empty barriers).
+//
+// Fused row-wise quantize of G (QV != 0). In SwitchBack's backward, G feeds both this GEMM (bf16)
+// and the int8 dX GEMM (row-wise int8 G_q, linear.cpp:232-235). The dW kernel's epilogue warps
+// sit idle through the whole main loop (one tile per pair, K = T tokens), and warps 2-3 always
+// do; these 10 warps per CTA quantize G's rows (one warp per row, the standalone K1 row body,
+// quant_core.cuh) while the producer / MMA threads stream the GEMM, so the quantize's HBM
+// traffic overlaps tensor-core work inside one launch instead of competing for SMs from a
+// second stream. QV = VPL (16-byte vectors per lane held in registers), or 1 = two-pass rows
+// of any length. The payload and states are those of sb_quantize_rowwise(G), bit for bit.
 #pragma once
+#include "quant_core.cuh"
 #include "tc_gemm2.cuh"
 
 namespace sbdw {
@@ -41,7 +51,46 @@ static_assert(SMEM_BYTES <= MAX_DYN_SMEM, "shared memory budget");
 struct WParams {
   int M, N, K;  // GEMM shape (TRANS: M = n, N = m)
   int tiles_m, tiles_n;
+  // fused row-wise quantize of G [q_rows x 8 q_nvec] (QV != 0)
+  const __nv_bfloat16* qg;
+  int64_t q_rows, q_ld, q_ldq;  // rows, G row stride (elements), payload row stride (bytes)
+  int q_nvec;                   // 16-byte vectors per row
+  int8_t* q_out;
+  float* q_state;
+  uint32_t* q_err;
+  int q_warps;  // quantizing warps per CTA: warps 2 .. 2 + q_warps - 1 (<= 2 + EPI_WARPS)
 };
+
+// The quantize trails the GEMM through G: the GEMM streams G's rows (tokens) from HBM in
+// k-blocks of 64 tokens, all pairs at about the same pace, and the quantize of a k-block's 64
+// rows waits until this CTA's producer has issued the loads of k-block + kLag, so the rows are
+// read from L2 (just brought in by the GEMM's TMA) instead of a second HBM stream racing the
+// GEMM's own (measured: an unpaced quantize saturated HBM for its first ~150 us and stalled
+// the GEMM). k-block kb belongs to working CTA kb mod (working CTAs); `prog` is the producer's
+// progress (k-blocks issued), in shared memory.
+constexpr int kLag = 6;
+template <int QV>
+__device__ __forceinline__ void quantize_g_rows(const WParams& p, int qwarp, int lane, const volatile int* prog,
+                                                int k_blocks, int num_units) {
+  if (qwarp >= p.q_warps) return;
+  const int working = 2 * min(num_units, static_cast<int>(gridDim.x >> 1));  // CTAs whose pair has a tile
+  const int c = static_cast<int>(blockIdx.x);
+  if (c >= working) return;
+  const int qkb = static_cast<int>((p.q_rows + KROWS - 1) / KROWS);
+  for (int kb = c; kb < qkb; kb += working) {
+    const int need = min(kb + kLag, k_blocks);
+    while (*prog < need) __nanosleep(256);
+    const int64_t r1 = min(static_cast<int64_t>(kb + 1) * KROWS, p.q_rows);
+    for (int64_t r = static_cast<int64_t>(kb) * KROWS + qwarp; r < r1; r += p.q_warps) {
+      const uint4* xr = reinterpret_cast<const uint4*>(p.qg + r * p.q_ld);
+      if (QV == 1)
+        sbq::quantize_row_stream<__nv_bfloat16>(xr, p.q_nvec, p.q_out + r * p.q_ldq, p.q_state + r, p.q_err, lane);
+      else
+        sbq::quantize_row_reg<__nv_bfloat16, (QV > 1 ? QV : 1)>(xr, p.q_nvec, p.q_out + r * p.q_ldq, p.q_state + r,
+                                                                 p.q_err, lane);
+    }
+  }
+}
 
 __device__ __forceinline__ void mma_f16_2(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -54,7 +103,7 @@ __device__ __forceinline__ void mma_f16_2(uint32_t d, uint64_t a, uint64_t b, ui
 // written to D[m][n] through a transposed staging tile: lane t (row t) stores its 32 values
 // down column t of a [32 m][32 n] fp32 tile (SW128 layout of the D tensor map; for a fixed
 // register index the 32 lanes fill one 128-byte row, so the stores are bank-conflict free).
-template <bool TRANS>
+template <bool TRANS, int QV>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     k_dw_wide(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmD, const WParams p) {
@@ -68,6 +117,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull_bar = empty_bar + NSTAGES;
   uint64_t* tempty_bar = tfull_bar + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 1);
+  volatile int* prog = reinterpret_cast<volatile int*>(tmem_slot + 1);  // producer progress (k-blocks issued)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -86,6 +136,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
     sbptx::mbar_init(tfull_bar, 1);
     sbptx::mbar_init(tempty_bar, 2 * EPI_WARPS);
+    *prog = 0;
     sbptx::fence_mbar_init();
   }
   if (warp == 1) {
@@ -122,6 +173,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         tma_load_2sm(&tmB, &full_bar[stage], sb, bn_a, k0);
         tma_load_2sm(&tmB, &full_bar[stage], sb + BOX, bn_a + 64, k0);
         tma_load_2sm(&tmB, &full_bar[stage], sb + 2 * BOX, bn_b, k0);
+        if (QV != 0 && u == pair) *prog = kb + 1;  // first tile only: prog never goes back (no wait on a later tile)
         if (++stage == NSTAGES) {
           stage = 0;
           phase ^= 1u;
@@ -162,7 +214,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         commit_mc(tfull_bar);
       }
     }
+  } else if (warp == 2 || warp == 3) {
+    if (QV != 0) quantize_g_rows<QV>(p, warp - 2, lane, prog, k_blocks, num_units);
   } else if (warp >= 4) {
+    if (QV != 0) quantize_g_rows<QV>(p, warp - 2, lane, prog, k_blocks, num_units);
     // --------------------------------------------------------------- epilogue (both CTAs)
     const int ew = warp & 3;             // TMEM lane quarter
     const int half = (warp - 4) >> 2;    // column half: [192 half, 192 half + 192)

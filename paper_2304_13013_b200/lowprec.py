@@ -380,6 +380,26 @@ def wgrad(g: torch.Tensor, x: torch.Tensor, exact: bool | None = None, out: torc
     return out
 
 
+def wgrad_quantize_rowwise(g: torch.Tensor, x: torch.Tensor, check: bool = True) -> tuple[torch.Tensor, QuantizedMatrix]:
+    """The backward's two uses of G in one launch: (wgrad_full_precision(G, X), quantize_rowwise(G))
+    (linear.cpp:232, :245). dW as wgrad(exact=False); the payload / states equal
+    quantize_rowwise(G) bit for bit."""
+    _need_cuda(g, x)
+    g, x = g.contiguous(), x.contiguous()
+    b, m = g.shape
+    n = x.shape[1]
+    dw = torch.empty((m, n), dtype=torch.float32, device=g.device)
+    q = torch.empty((b, m), dtype=torch.int8, device=g.device)
+    st = torch.empty(b, dtype=torch.float32, device=g.device)
+    h = A.handle(g.device.index)
+    A.check(h.lib.sb_wgrad_quantize_rowwise(h.h, _p(g), _p(x), _dt(g), b, m, n, _p(dw), _p(q), m, _p(st)))
+    try:
+        _check_nonfinite(h, check)
+    except InvalidArgument:
+        raise InvalidArgument(A.SB_ERR_NONFINITE, "quantize_rowwise: non-finite input") from None
+    return dw, QuantizedMatrix(q, st, ROW)
+
+
 def gemm_fp8(qa: QuantizedMatrix, qb: QuantizedMatrix, out_dtype=torch.float32) -> torch.Tensor:
     """fp8 SwitchBack product (linear.cpp:151-153): snapped operands, tensor-core accumulation."""
     M, K, N = qa.rows, qa.cols, qb.rows

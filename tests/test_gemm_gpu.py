@@ -12,10 +12,12 @@ from tests._util import bf16, dev, fp8_decode, host, rel_err
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=[A.SB_GEMM_1CTA, A.SB_GEMM_2CTA, A.SB_GEMM_WIDE], ids=["1cta", "2cta", "wide"])
+@pytest.fixture(params=[A.SB_GEMM_1CTA, A.SB_GEMM_2CTA, A.SB_GEMM_WIDE, A.SB_GEMM_2CTA_MC],
+                ids=["1cta", "2cta", "wide", "2cta_mc"])
 def gemm_path(request):
-    """Run the test on every tensor-core tiling (1-CTA 128x256, cta_group::2 256x256, and the
-    transposed cta_group::2 256x384 int8 / fp8 kernel)."""
+    """Run the test on every tensor-core tiling (1-CTA 128x256, cta_group::2 256x256, the
+    transposed cta_group::2 256x384 int8 / fp8 kernel, and the 256x256 kernel in clusters of two
+    pairs sharing B by TMA multicast)."""
     h = A.handle()
     h.set_gemm_path(request.param)
     yield request.param
