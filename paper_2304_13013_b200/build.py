@@ -23,7 +23,7 @@ LIB = os.path.join(PKG, "libswitchback_b200.so")
 SHIM = os.path.join(PKG, "liblowprec_b200.so")
 
 CU_SOURCES = ["quantize.cu", "gemm.cu", "optim.cu", "capi.cu", "util.cu", "dp.cu"]
-HEADERS = ["sb_ptx.cuh", "sb_internal.h", "tc_gemm.cuh", "tc_gemm2.cuh", "tc_dw_wide.cuh", "tc_i8_wide.cuh"]
+HEADERS = ["sb_ptx.cuh", "sb_internal.h", "quant_core.cuh", "tc_gemm.cuh", "tc_gemm2.cuh", "tc_dw_wide.cuh", "tc_i8_wide.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # --fmad=false: no FMA contraction anywhere (the reference's -ffp-contract=off numeric

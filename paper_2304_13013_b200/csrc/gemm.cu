@@ -409,9 +409,8 @@ cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, cons
   static cudaError_t attr_err = cudaSuccess;
   static std::once_flag once;
   std::call_once(once, [&] {
-    for (auto kern : {sbdw::k_dw_wide<false, 0>, sbdw::k_dw_wide<true, 0>, sbdw::k_dw_wide<false, 1>,
-                      sbdw::k_dw_wide<true, 1>, sbdw::k_dw_wide<false, 5>, sbdw::k_dw_wide<true, 5>,
-                      sbdw::k_dw_wide<false, 20>, sbdw::k_dw_wide<true, 20>}) {
+    for (auto kern : {sbdw::k_dw_wide<false, 0>, sbdw::k_dw_wide<true, 0>, sbdw::k_dw_wide<false, sbdw::kQV>,
+                      sbdw::k_dw_wide<true, sbdw::kQV>}) {
       const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sbdw::SMEM_BYTES);
       if (e != cudaSuccess) attr_err = e;
     }
@@ -456,7 +455,7 @@ cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, cons
   if (rq) {
     // G [T x m] row-major bf16 (its MN-major operand view), rows of m / 8 16-byte vectors
     const int nvec = static_cast<int>(m / 8);
-    qv = nvec == 160 ? 5 : (nvec == 640 ? 20 : 1);  // the ViT-H widths held in registers, else two-pass
+    qv = sbdw::kQV;
     p.qg = static_cast<const __nv_bfloat16*>(G.ptr);
     p.q_rows = T;
     p.q_ld = m;
@@ -475,16 +474,10 @@ cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, cons
   auto go = [&](auto kern) {
     sb::launch_pdl(kern, dim3(grid), dim3(sbtc::NUM_THREADS), sbdw::SMEM_BYTES, h->stream, ta, tb, td, p);
   };
-  switch (qv * 2 + (trans ? 1 : 0)) {
-    case 0: go(sbdw::k_dw_wide<false, 0>); break;
-    case 1: go(sbdw::k_dw_wide<true, 0>); break;
-    case 2: go(sbdw::k_dw_wide<false, 1>); break;
-    case 3: go(sbdw::k_dw_wide<true, 1>); break;
-    case 10: go(sbdw::k_dw_wide<false, 5>); break;
-    case 11: go(sbdw::k_dw_wide<true, 5>); break;
-    case 40: go(sbdw::k_dw_wide<false, 20>); break;
-    default: go(sbdw::k_dw_wide<true, 20>); break;
-  }
+  if (qv)
+    trans ? go(sbdw::k_dw_wide<true, sbdw::kQV>) : go(sbdw::k_dw_wide<false, sbdw::kQV>);
+  else
+    trans ? go(sbdw::k_dw_wide<true, 0>) : go(sbdw::k_dw_wide<false, 0>);
   return cudaGetLastError();
 }
 

@@ -297,4 +297,60 @@ __device__ __forceinline__ void quantize_row_stream(const uint4* __restrict__ xr
   }
 }
 
+// Compact bf16 row quantizer for kernels that carry it as a side task (the dW GEMM): the same
+// payload / states as quantize_row_reg, but two passes over the row (absmax, then payload; the
+// second read is an L2 hit) with U vectors per lane in flight per step, and the exact fallback
+// out of line, so the side task adds a few hundred instructions to the host kernel instead of
+// a fully unrolled row (a 64 KB kernel thrashed the instruction cache of the GEMM's issuing
+// threads: ncu showed instruction-fetch requests at 65% of peak and the tensor pipe losing 12%).
+static __device__ __noinline__ uint2 qvec_bf16_slow(uint4 v, Scale sc, bool plain) {
+  return qvec<__nv_bfloat16>(v, sc, plain);
+}
+template <int U>
+__device__ __forceinline__ void quantize_row_bf16_2pass(const uint4* __restrict__ xr, int nvec, int8_t* __restrict__ qrow,
+                                                        float* __restrict__ state_row, uint32_t* err, int lane) {
+  uint32_t amax = 0;
+#pragma unroll 1
+  for (int b = 0; b < nvec; b += 32 * U) {
+    uint4 v[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int i = b + j * 32 + lane;
+      v[j] = i < nvec ? ld_stream(xr + i) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) amax = max(amax, vec_absmax_bits<__nv_bfloat16>(v[j]));
+  }
+  amax = __reduce_max_sync(0xffffffffu, amax);
+  if (amax >= kNonFiniteBits) {
+    if (lane == 0) {
+      raise_nonfinite(err);
+      *state_row = __uint_as_float(amax);
+    }
+    return;
+  }
+  const float st = state_from_bits(amax);
+  if (lane == 0) *state_row = st;
+  const Scale sc = make_scale(st);
+  const bool plain = sc.pre == 1.0f;
+  const bool fast = __all_sync(0xffffffffu, plain);
+  uint2* qr = reinterpret_cast<uint2*>(qrow);
+#pragma unroll 1
+  for (int b = 0; b < nvec; b += 32 * U) {
+    uint4 v[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int i = b + j * 32 + lane;
+      v[j] = i < nvec ? ld_stream(xr + i) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int i = b + j * 32 + lane;
+      if (b + j * 32 >= nvec) break;  // warp-uniform
+      const uint2 o = fast ? qvec_bf16_fast(v[j], sc.inv2) : qvec_bf16_slow(v[j], sc, plain);
+      if (i < nvec) qr[i] = o;
+    }
+  }
+}
+
 }  // namespace sbq

@@ -22,8 +22,8 @@
 // do; these 10 warps per CTA quantize G's rows (one warp per row, the standalone K1 row body,
 // quant_core.cuh) while the producer / MMA threads stream the GEMM, so the quantize's HBM
 // traffic overlaps tensor-core work inside one launch instead of competing for SMs from a
-// second stream. QV = VPL (16-byte vectors per lane held in registers), or 1 = two-pass rows
-// of any length. The payload and states are those of sb_quantize_rowwise(G), bit for bit.
+// second stream. QV = 16-byte vectors per lane in flight per step of the two-pass row quantizer
+// (quant_core.cuh). The payload and states are those of sb_quantize_rowwise(G), bit for bit.
 #pragma once
 #include "quant_core.cuh"
 #include "tc_gemm2.cuh"
@@ -69,6 +69,7 @@ struct WParams {
 // the GEMM). k-block kb belongs to working CTA kb mod (working CTAs); `prog` is the producer's
 // progress (k-blocks issued), in shared memory.
 constexpr int kLag = 6;
+constexpr int kQV = 8;  // vectors per lane in flight per step of the fused row quantizer
 template <int QV>
 __device__ __forceinline__ void quantize_g_rows(const WParams& p, int qwarp, int lane, const volatile int* prog,
                                                 int k_blocks, int num_units) {
@@ -79,15 +80,12 @@ __device__ __forceinline__ void quantize_g_rows(const WParams& p, int qwarp, int
   const int qkb = static_cast<int>((p.q_rows + KROWS - 1) / KROWS);
   for (int kb = c; kb < qkb; kb += working) {
     const int need = min(kb + kLag, k_blocks);
-    while (*prog < need) __nanosleep(256);
+    while (*prog < need) __nanosleep(2000);
     const int64_t r1 = min(static_cast<int64_t>(kb + 1) * KROWS, p.q_rows);
+#pragma unroll 1
     for (int64_t r = static_cast<int64_t>(kb) * KROWS + qwarp; r < r1; r += p.q_warps) {
       const uint4* xr = reinterpret_cast<const uint4*>(p.qg + r * p.q_ld);
-      if (QV == 1)
-        sbq::quantize_row_stream<__nv_bfloat16>(xr, p.q_nvec, p.q_out + r * p.q_ldq, p.q_state + r, p.q_err, lane);
-      else
-        sbq::quantize_row_reg<__nv_bfloat16, (QV > 1 ? QV : 1)>(xr, p.q_nvec, p.q_out + r * p.q_ldq, p.q_state + r,
-                                                                 p.q_err, lane);
+      sbq::quantize_row_bf16_2pass<(QV > 0 ? QV : 1)>(xr, p.q_nvec, p.q_out + r * p.q_ldq, p.q_state + r, p.q_err, lane);
     }
   }
 }
