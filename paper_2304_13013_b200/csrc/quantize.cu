@@ -942,9 +942,19 @@ __global__ void __launch_bounds__(256) k_quantize_tensorwise_fused(const T* __re
       const int64_t r0 = task * slab;
       const int nr = static_cast<int>(rows - r0 < slab ? rows - r0 : slab);
       uint32_t m = 0;
-      for (int i = threadIdx.x; i < nr * vpr; i += blockDim.x) {
-        const int r = i / vpr, v = i - r * vpr;
-        m = max(m, vec_absmax_bits<T>(ld_stream(reinterpret_cast<const uint4*>(x + (r0 + r) * ldx) + v)));
+      const int cnt = nr * vpr;
+      // all of a step's loads in flight before the first use (ld_stream is volatile asm, so a
+      // load-then-max loop would serialise one L2/HBM round trip per vector)
+      for (int base = 0; base < cnt; base += 8 * 256) {
+        uint4 v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int i = base + j * 256 + static_cast<int>(threadIdx.x);
+          const int r = i / vpr, c = i - r * vpr;
+          v[j] = i < cnt ? ld_stream(reinterpret_cast<const uint4*>(x + (r0 + r) * ldx) + c) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m = max(m, vec_absmax_bits<T>(v[j]));
       }
       m = __reduce_max_sync(0xffffffffu, m);
       if (lane == 0) red[warp] = m;
@@ -988,13 +998,21 @@ __global__ void __launch_bounds__(256) k_quantize_tensorwise_fused(const T* __re
     constexpr int GPR = 64 / VEC;          // vector groups per tile row
     constexpr int RPP = 256 / GPR;         // rows per pass
     const int g = threadIdx.x % GPR, lr0 = threadIdx.x / GPR;
+    constexpr int NP = 64 / RPP;
+    uint4 vin[NP];
 #pragma unroll
-    for (int pass = 0; pass < 64 / RPP; ++pass) {
+    for (int pass = 0; pass < NP; ++pass) {  // both passes' loads in flight first
+      const int64_t r = r0 + pass * RPP + lr0, c = c0 + g * VEC;
+      vin[pass] = (r < rows && c < cols) ? ld_stream(reinterpret_cast<const uint4*>(x + r * ldx + c))
+                                         : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int pass = 0; pass < NP; ++pass) {
       const int lr = pass * RPP + lr0;
       const int64_t r = r0 + lr, c = c0 + g * VEC;
       uint32_t w0 = 0, w1 = 0;  // payload bytes of this vector (VEC <= 8)
       if (r < rows && c < cols) {
-        const uint4 v = ld_stream(reinterpret_cast<const uint4*>(x + r * ldx + c));
+        const uint4 v = vin[pass];
         if constexpr (sizeof(T) == 2) {
           const uint2 o = fast ? qvec_bf16_fast(v, sc.inv2) : VecQ<T>::run(v, sc);
           w0 = o.x;
@@ -1039,6 +1057,156 @@ __global__ void __launch_bounds__(256) k_quantize_tensorwise_fused(const T* __re
     }
     __syncthreads();
   }
+}
+
+// ------------------------------------------------------- K2+K3 one pass ----
+// Tensor-wise quantize (+ transposed payload) for weights that fit on the chip at once: one
+// 128-row tile per block (bf16: 128 x 128, fp32: 128 x 64; 2048 16-byte vectors, 8 per thread)
+// held in registers across a grid-wide absmax: each block loads its tile with all loads in
+// flight, max-reduces it into sync[0] and counts itself done in sync[2]; once every block has
+// arrived it quantizes the registers (one HBM read of W in total) and writes q row-major and
+// q_t through a shared-memory transpose. The launch is cooperative (the runtime guarantees the
+// blocks are co-resident, or refuses the launch and the task-list kernel above runs instead).
+// ~2 HBM round trips + one grid barrier instead of the task list's serial atomics / barriers
+// per 8 KB task (22 us -> a few us for the ViT-H weights).
+constexpr int kTwRows = 128;
+template <typename T>
+__global__ void __launch_bounds__(256) k_quantize_tensorwise_coop(const T* __restrict__ x, int64_t rows, int64_t cols,
+                                                                   int64_t ldx, int8_t* __restrict__ q, int64_t ldq,
+                                                                   int8_t* __restrict__ qt, int64_t ldqt,
+                                                                   float* __restrict__ state, unsigned int* sync,
+                                                                   uint32_t* err) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int TC = 16 * VEC;  // tile columns: 16 vectors per tile row
+  __shared__ uint32_t red[8];
+  __shared__ __align__(16) int8_t tile[kTwRows][TC + 16];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t tc = (cols + TC - 1) / TC;
+  const int64_t r0 = (blockIdx.x / tc) * kTwRows, c0 = (blockIdx.x % tc) * TC;
+  const int vc = threadIdx.x & 15, lr0 = threadIdx.x >> 4;  // vector column, first tile row (+16 j)
+  const int64_t c = c0 + vc * VEC;
+  sbptx::pdl_trigger();
+  sbptx::pdl_wait();
+  uint4 v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int64_t r = r0 + lr0 + 16 * j;
+    v[j] = (r < rows && c < cols) ? ld_stream(reinterpret_cast<const uint4*>(x + r * ldx + c)) : make_uint4(0, 0, 0, 0);
+  }
+  uint32_t m = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) m = max(m, vec_absmax_bits<T>(v[j]));
+  m = __reduce_max_sync(0xffffffffu, m);
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < 8; ++i) m = max(m, red[i]);
+    if (m) atomicMax(sync, m);
+    __threadfence();
+    atomicAdd(sync + 2, 1u);
+    while (ld_acquire_gpu(sync + 2) < gridDim.x) __nanosleep(32);
+    red[0] = ld_acquire_gpu(sync);
+  }
+  __syncthreads();
+  const uint32_t wb = red[0];
+  if (wb >= kNonFiniteBits) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      raise_nonfinite(err);
+      state[0] = __uint_as_float(wb);
+    }
+    return;
+  }
+  const float st = state_from_bits(wb);
+  if (blockIdx.x == 0 && threadIdx.x == 0) state[0] = st;
+  const Scale sc = make_scale(st);
+  const bool fast = sizeof(T) == 2 && sc.pre == 1.0f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int lr = lr0 + 16 * j;
+    const int64_t r = r0 + lr;
+    uint32_t w0 = 0, w1 = 0;
+    if constexpr (sizeof(T) == 2) {
+      const uint2 o = fast ? qvec_bf16_fast(v[j], sc.inv2) : VecQ<T>::run(v[j], sc);
+      w0 = o.x;
+      w1 = o.y;
+    } else {
+      w0 = VecQ<T>::run(v[j], sc);
+    }
+    if (q && r < rows && c < cols) {
+      if constexpr (VEC == 8)
+        *reinterpret_cast<uint2*>(q + r * ldq + c) = make_uint2(w0, w1);
+      else
+        *reinterpret_cast<uint32_t*>(q + r * ldq + c) = w0;
+    }
+    if constexpr (VEC == 8)
+      *reinterpret_cast<uint2*>(&tile[lr][vc * 8]) = make_uint2(w0, w1);
+    else
+      *reinterpret_cast<uint32_t*>(&tile[lr][vc * 4]) = w0;
+  }
+  if (!qt) return;
+  __syncthreads();
+  // q_t[c][r0 .. r0 + 127]: 256 / TC threads per tile column, 16 rows (one uint4) per step
+  constexpr int TPC = 256 / TC;            // threads per tile column (2 bf16, 4 fp32)
+  constexpr int RPT = kTwRows / TPC;       // rows per thread (64 / 32)
+  const int lc = threadIdx.x / TPC, rq0 = (threadIdx.x % TPC) * RPT;
+  const int64_t cc = c0 + lc;
+  if (cc >= cols) return;
+#pragma unroll
+  for (int k0 = 0; k0 < RPT; k0 += 16) {
+    uint32_t wv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t pk = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) pk |= static_cast<uint32_t>(static_cast<uint8_t>(tile[rq0 + k0 + 4 * k + i][lc])) << (8 * i);
+      wv[k] = pk;
+    }
+    const int64_t r = r0 + rq0 + k0;
+    int8_t* dst = qt + cc * ldqt + r;
+    if (r + 15 < rows && sb::aligned(dst, 16)) {
+      *reinterpret_cast<uint4*>(dst) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+    } else {
+      for (int i = 0; i < 16 && r + i < rows; ++i) dst[i] = static_cast<int8_t>((wv[i >> 2] >> (8 * (i & 3))) & 0xff);
+    }
+  }
+}
+
+template <typename T>
+bool launch_tensorwise_coop(sb_handle h, const T* x, int64_t rows, int64_t cols, int64_t ldx, int8_t* q, int64_t ldq,
+                            int8_t* qt, int64_t ldqt, float* state, unsigned int* sync, cudaError_t* err) {
+  constexpr int TC = 16 * (16 / sizeof(T));
+  static int cap[16] = {};  // co-resident blocks per device
+  const int d = h->device & 15;
+  if (cap[d] == 0) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_quantize_tensorwise_coop<T>, 256, 0) != cudaSuccess || b < 1)
+      b = 0;
+    cudaGetLastError();
+    cap[d] = b > 0 ? b * h->num_sms : -1;
+  }
+  const int64_t tiles = ((rows + kTwRows - 1) / kTwRows) * ((cols + TC - 1) / TC);
+  if (cap[d] < 0 || tiles > cap[d]) return false;
+  *err = cudaMemsetAsync(sync, 0, 4 * sizeof(unsigned int), h->stream);
+  if (*err != cudaSuccess) return true;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(tiles));
+  cfg.blockDim = dim3(256);
+  cfg.stream = h->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  h->launches++;
+  *err = cudaLaunchKernelEx(&cfg, k_quantize_tensorwise_coop<T>, x, rows, cols, ldx, q, ldq, qt, ldqt, state, sync,
+                            h->d_err);
+  if (*err == cudaErrorCooperativeLaunchTooLarge || *err == cudaErrorNotSupported) {
+    cudaGetLastError();
+    h->launches--;
+    cap[d] = -1;  // never again on this device: the task-list kernel runs
+    return false;
+  }
+  return true;
 }
 
 // ----------------------------------------------------------------- K10 ----
@@ -1489,6 +1657,13 @@ bool launch_quantize_tensorwise_fused(sb_handle h, const void* x, sb_dtype dt, i
   const int vec = dt == SB_BF16 ? 8 : 4;
   if (cols % vec || ldx % vec || !sb::aligned(x, 16) || rows <= 0 || cols <= 0) return false;
   if (q && (ldq % vec || !sb::aligned(q, 8))) return false;
+  if (!getenv("SB_TW_TASKLIST")) {  // one pass with the tile in registers when the grid fits the chip
+    const bool done = dt == SB_BF16 ? launch_tensorwise_coop(h, static_cast<const __nv_bfloat16*>(x), rows, cols, ldx, q,
+                                                             ldq, q_t, ldqt, state, sync, err)
+                                    : launch_tensorwise_coop(h, static_cast<const float*>(x), rows, cols, ldx, q, ldq,
+                                                             q_t, ldqt, state, sync, err);
+    if (done) return true;
+  }
   static int cap_bf16 = 0, cap_f32 = 0;
   int& cap = dt == SB_BF16 ? cap_bf16 : cap_f32;
   if (cap == 0) {
