@@ -121,6 +121,22 @@ __device__ __forceinline__ long long gtime() {
 #define SB_PROBE_ADD(slot)
 #endif
 
+// float(acc) for an s32 accumulator (the epilogue's int8 dequant input). Default: I2F.F32.S32
+// (XU pipe). Built with -DSB_I2F_FMA: the same correctly rounded value on the FMA / ALU pipes
+// (acc = hi 2^16 + lo, both halves exact in fp32 via the 2^23 magic number, one FMA rounding
+// hi 2^16 + lo once; checked against (float)acc on the host for every |acc| < 1e8 and a stride
+// beyond). ncu shows the XU pipe ~80% busy in the K = 1280 GEMMs, but the 6-instruction form
+// measured slower in the C2 step (fc1 fwd 303 -> 330 us): issue slots, not XU, pace it.
+__device__ __forceinline__ float i2f_exact(uint32_t acc) {
+#ifndef SB_I2F_FMA
+  return static_cast<float>(static_cast<int32_t>(acc));
+#else
+  const float lo = __fsub_rn(__uint_as_float((acc & 0xffffu) | 0x4b000000u), 8388608.0f);  // 2^23 + lo - 2^23
+  const float hi = __fsub_rn(__int_as_float((static_cast<int32_t>(acc) >> 16) + 0x4b400000), 12582912.0f);
+  return __fmaf_rn(hi, 65536.0f, lo);
+#endif
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -226,10 +242,10 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
       for (int j = 0; j < 16; ++j) {
         float a0, a1, b0, b1;
         if (KIND == KIND_I8) {
-          a0 = static_cast<float>(static_cast<int32_t>(r0[2 * j]));
-          a1 = static_cast<float>(static_cast<int32_t>(r0[2 * j + 1]));
-          b0 = static_cast<float>(static_cast<int32_t>(r1[2 * j]));
-          b1 = static_cast<float>(static_cast<int32_t>(r1[2 * j + 1]));
+          a0 = i2f_exact(r0[2 * j]);
+          a1 = i2f_exact(r0[2 * j + 1]);
+          b0 = i2f_exact(r1[2 * j]);
+          b1 = i2f_exact(r1[2 * j + 1]);
         } else {
           a0 = __uint_as_float(r0[2 * j]);
           a1 = __uint_as_float(r0[2 * j + 1]);
@@ -301,7 +317,7 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
                 16129.0);
             w[j] = __float_as_uint(__double2float_rn(d));
           } else {
-            const float v = KIND == KIND_I8 ? static_cast<float>(static_cast<int32_t>(r[j])) : __uint_as_float(r[j]);
+            const float v = KIND == KIND_I8 ? i2f_exact(r[j]) : __uint_as_float(r[j]);
             const float y = SB_COL ? __fmul_rn(v, fr * cs[cc + j]) : __fmul_rn(v, fr);
             // bias as a separate rounded add: identical bits to an unfused y + bias
             w[j] = __float_as_uint(p.bias != nullptr ? __fadd_rn(y, col_bias(p, n0 + cc + j)) : y);

@@ -105,7 +105,7 @@ __device__ __forceinline__ void store_chunk(const WideParams& p, const CUtensorM
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
       const float fk = __shfl_sync(0xffffffffu, fr, k);
-      float v = KIND == KIND_I8 ? static_cast<float>(static_cast<int32_t>(r[k])) : __uint_as_float(r[k]);
+      float v = KIND == KIND_I8 ? i2f_exact(r[k]) : __uint_as_float(r[k]);
       v = SB_COL ? v * (fk * sbj) : v * fk;
       if (p.bias != nullptr) v = __fadd_rn(v, bias_j);
       r[k] = __float_as_uint(v);
@@ -145,7 +145,7 @@ __device__ __forceinline__ void store_chunk(const WideParams& p, const CUtensorM
             16129.0)));
       } else {
         const float fk = __shfl_sync(0xffffffffu, fr, k);
-        const float v = KIND == KIND_I8 ? static_cast<float>(static_cast<int32_t>(r[k])) : __uint_as_float(r[k]);
+        const float v = KIND == KIND_I8 ? i2f_exact(r[k]) : __uint_as_float(r[k]);
         const float y = SB_COL ? __fmul_rn(v, fk * sbj) : __fmul_rn(v, fk);
         w = __float_as_uint(p.bias != nullptr ? __fadd_rn(y, bias_j) : y);
       }
