@@ -383,13 +383,15 @@ cudaError_t launch_tc(sb_handle h, const Operand& A, const Operand& B, const CUt
   const int units = p.tiles_m * p.tiles_n * p.splits;
   h->launches++;
   if (two) return launch_2cta<KIND, OUT, A_MN, B_MN, SB_COL>(h, ta, tb, d, p, idesc, units, cfg);
-  static std::once_flag once1;
-  static cudaError_t attr_err1 = cudaSuccess;
-  std::call_once(once1, [] {
-    attr_err1 = cudaFuncSetAttribute(sbtc::k_tc_gemm<KIND, A_MN, B_MN, OUT, SB_COL>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, sbtc::SMEM_BYTES);
+  // the max-dynamic-smem attribute is per device context: set once per device
+  static std::once_flag once1[16];
+  static cudaError_t attr_err1[16] = {};
+  const int dv = h->device & 15;
+  std::call_once(once1[dv], [dv] {
+    attr_err1[dv] = cudaFuncSetAttribute(sbtc::k_tc_gemm<KIND, A_MN, B_MN, OUT, SB_COL>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, sbtc::SMEM_BYTES);
   });
-  if (attr_err1 != cudaSuccess) return attr_err1;
+  if (attr_err1[dv] != cudaSuccess) return attr_err1[dv];
   const int grid = units < h->num_sms ? units : h->num_sms;
   sbtc::k_tc_gemm<KIND, A_MN, B_MN, OUT, SB_COL><<<grid, sbtc::NUM_THREADS, sbtc::SMEM_BYTES, h->stream>>>(
       ta, tb, d, p, idesc);
@@ -405,10 +407,14 @@ cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, cons
   static int env = -1;
   if (env < 0) env = getenv("SB_DW_WIDE") ? atoi(getenv("SB_DW_WIDE")) : 1;
   if (!env || h->gemm_path == SB_GEMM_1CTA || h->num_sms < 2) return cudaErrorNotSupported;
-  static int max_pairs = 0;
-  static cudaError_t attr_err = cudaSuccess;
-  static std::once_flag once;
-  std::call_once(once, [&] {
+  // per device: the smem attribute and the co-resident pair count belong to the device context
+  static int max_pairs_d[16] = {};
+  static cudaError_t attr_err_d[16] = {};
+  static std::once_flag once_d[16];
+  const int dv = h->device & 15;
+  int& max_pairs = max_pairs_d[dv];
+  cudaError_t& attr_err = attr_err_d[dv];
+  std::call_once(once_d[dv], [&] {
     for (auto kern : {sbdw::k_dw_wide<false, 0>, sbdw::k_dw_wide<true, 0>, sbdw::k_dw_wide<false, sbdw::kQV>,
                       sbdw::k_dw_wide<true, sbdw::kQV>}) {
       const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sbdw::SMEM_BYTES);

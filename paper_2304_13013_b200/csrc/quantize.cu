@@ -401,12 +401,12 @@ template <int MODE, int CH>
 cudaError_t launch_act_rows(sb_handle h, const __nv_bfloat16* a, const __nv_bfloat16* b, int64_t rows, int nvec,
                             __nv_bfloat16* act, int8_t* q, float* state) {
   const size_t smem = MODE == 0 ? static_cast<size_t>(kFwdEntries) * 2 : static_cast<size_t>(kLutEntries) * 4;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[16] = {};  // the smem attribute is per device context
+  if (!attr[h->device & 15]) {
     const cudaError_t e = cudaFuncSetAttribute(k_act_quantize_rows<MODE, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr[h->device & 15] = true;
   }
   const uint4* lut = reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(h->gelu_lut) +
                                                     (MODE == 0 ? 0 : static_cast<size_t>(kFwdEntries) * 2));
@@ -660,10 +660,10 @@ template <int VPL>
 void launch_ln_bwd(sb_handle h, int64_t blocks, size_t smem, const __nv_bfloat16* D, const __nv_bfloat16* X,
                    int64_t rows, int nvec, const float* mean, const float* rstd, const float* gamma, __nv_bfloat16* O,
                    float* part) {
-  static bool attr = false;  // one flag per VPL instantiation
-  if (!attr) {
+  static bool attr[16] = {};  // one flag per VPL instantiation and device
+  if (!attr[h->device & 15]) {
     cudaFuncSetAttribute(k_ln_backward_rows<VPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
+    attr[h->device & 15] = true;
   }
   k_ln_backward_rows<VPL><<<static_cast<unsigned>(blocks), 256, smem, h->stream>>>(D, X, rows, nvec, mean, rstd, gamma,
                                                                                    O, part);
@@ -724,11 +724,11 @@ cudaError_t rowwise_impl(sb_handle h, const T* x, int64_t rows, int64_t cols, in
   int stages = static_cast<int>(std::min<int64_t>(32, kQRingBytes / std::max(slot, 1)));
   if (stages > kQWarps) stages -= stages % kQWarps;  // slot ownership: see k_quantize_rowwise_tma
   if (stages >= 4) {
-    static bool attr = false;
+    static bool attr[16] = {};  // per device context
     const int smem = stages * slot + 2 * stages * 8;
-    if (!attr) {
+    if (!attr[h->device & 15]) {
       cudaFuncSetAttribute(k_quantize_rowwise_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kQRingBytes + 1024);
-      attr = true;
+      attr[h->device & 15] = true;
     }
     int64_t blocks = std::min<int64_t>(rows, static_cast<int64_t>(h->num_sms) * 2);
     k_quantize_rowwise_tma<T><<<static_cast<unsigned>(blocks), kQThreads, smem, h->stream>>>(
