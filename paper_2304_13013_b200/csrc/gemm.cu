@@ -476,6 +476,13 @@ cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, cons
   }
   // with a fused quantize every co-resident pair takes part (pairs without a tile only quantize)
   const int grid = 2 * (rq ? max_pairs : (units < max_pairs ? units : max_pairs));
+  if (rq && units < max_pairs) {
+    // the tile-less pairs' share of G's k-blocks (SB_DWQ_IDLE: fraction of all k-blocks)
+    static double frac = -1.0;
+    if (frac < 0) frac = getenv("SB_DWQ_IDLE") ? atof(getenv("SB_DWQ_IDLE")) : 0.0;
+    const int64_t qkb = (T + sbdw::KROWS - 1) / sbdw::KROWS;
+    p.q_idle_kb = static_cast<int>(std::min<double>(static_cast<double>(qkb), frac * static_cast<double>(qkb)));
+  }
   h->launches++;
   auto go = [&](auto kern) {
     sb::launch_pdl(kern, dim3(grid), dim3(sbtc::NUM_THREADS), sbdw::SMEM_BYTES, h->stream, ta, tb, td, p);

@@ -59,6 +59,7 @@ struct WParams {
   float* q_state;
   uint32_t* q_err;
   int q_warps;  // quantizing warps per CTA: warps 2 .. 2 + q_warps - 1 (<= 2 + EPI_WARPS)
+  int q_idle_kb;  // leading k-blocks of G quantized by the CTAs whose pair has no tile (unpaced)
 };
 
 // The quantize trails the GEMM through G: the GEMM streams G's rows (tokens) from HBM in
@@ -76,11 +77,16 @@ __device__ __forceinline__ void quantize_g_rows(const WParams& p, int qwarp, int
   if (qwarp >= p.q_warps) return;
   const int working = 2 * min(num_units, static_cast<int>(gridDim.x >> 1));  // CTAs whose pair has a tile
   const int c = static_cast<int>(blockIdx.x);
-  if (c >= working) return;
   const int qkb = static_cast<int>((p.q_rows + KROWS - 1) / KROWS);
-  for (int kb = c; kb < qkb; kb += working) {
+  const bool idle = c >= working;
+  // idle CTAs (no GEMM tile: every SM cycle is theirs) take the first q_idle_kb k-blocks at full
+  // speed; the working CTAs take the rest, paced behind their own producer
+  const int kb0 = idle ? c - working : p.q_idle_kb + c;
+  const int kb_end = idle ? min(p.q_idle_kb, qkb) : qkb;
+  const int kb_step = idle ? static_cast<int>(gridDim.x) - working : working;
+  for (int kb = kb0; kb < kb_end; kb += kb_step) {
     const int need = min(kb + kLag, k_blocks);
-    while (*prog < need) __nanosleep(2000);
+    while (!idle && *prog < need) __nanosleep(2000);
     const int64_t r1 = min(static_cast<int64_t>(kb + 1) * KROWS, p.q_rows);
 #pragma unroll 1
     for (int64_t r = static_cast<int64_t>(kb) * KROWS + qwarp; r < r1; r += p.q_warps) {
