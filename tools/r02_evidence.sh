@@ -23,6 +23,8 @@ case "${PART:-1}" in
 3)
   timeout 600 $N $F -k regex:k_tc_gemm2 -c 2 -o gpurun_out/prof_i8 -f python tools/gprof.py > /dev/null 2>&1
   timeout 600 $N $F -k regex:tensorwise_coop -s 2 -c 1 -o gpurun_out/prof_tw -f python tools/twbench.py > /dev/null 2>&1
+  ;;
+4)
   timeout 600 $N $F -k regex:act_quantize_rows -s 2 -c 2 -o gpurun_out/prof_k10 -f python tools/prof_k10.py > /dev/null 2>&1
   timeout 600 $N $F -k regex:k_ln_ -s 2 -c 2 -o gpurun_out/prof_ln -f python tools/prof_ln.py > /dev/null 2>&1
   NBLK=4 timeout 600 $N $F -k regex:adamw -s 2 -c 1 -o gpurun_out/prof_adamw -f python tools/oprof.py > /dev/null 2>&1
