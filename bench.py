@@ -4,9 +4,11 @@ Default workload = config 2 (BASELINE.json configs[1]): the CLIP ViT-Huge MLP bl
 fc1 1280->5120 and fc2 5120->1280, 256 images x 257 tokens = 65792 tokens per GPU,
 SwitchBack int8 (row-wise X/G, tensor-wise W) forward + input gradient on tcgen05
 kind::i8, bf16 weight gradient on tcgen05 kind::f16. One step = forward + backward of
-both linears (the reference's switchback_fwd_bwd unit, bench.cpp:75-81), each with its
-own synthetic bf16 input and output gradient. N > 1: weak scaling, each rank owns 65792
-tokens; dW all-reduce (NCCL) is the only collective.
+the two chained linears (the reference's switchback_fwd_bwd unit, bench.cpp:75-81, applied
+to the MLP block of model.cpp:324-329 / 351-360 without its GELU): fc2 consumes fc1's
+output, fc1's output gradient is fc2's input gradient; synthetic bf16 X and block-output
+gradient G. N > 1: weak scaling, each rank owns 65792 tokens; dW all-reduce (NCCL) is the
+only collective.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...
@@ -30,7 +32,8 @@ sys.path.insert(0, ROOT)
 T_PER_GPU = 256 * 257
 LAYERS = [("fc1", 1280, 5120), ("fc2", 5120, 1280)]  # (name, n = in_features, m = out_features)
 METRIC = "SwitchBack fwd+bwd tokens/s at ViT-H shapes (1/2/4/8 GPU); int8 TOPS % of peak"
-WORKLOAD = "CLIP ViT-Huge MLP block 1280->5120->1280, 256 images x 257 tokens, int8 fwd/dX + bf16 dW"
+WORKLOAD = ("CLIP ViT-Huge MLP block 1280->5120->1280 (fc1 -> fc2 chained), 256 images x 257 tokens, "
+            "int8 fwd/dX + bf16 dW")
 # BASELINE.json configs as bench modes (--config); c2 is the headline line the driver runs.
 CONFIGS = {
     "c2": (LAYERS, WORKLOAD, "switchback", "int8"),
@@ -149,9 +152,10 @@ REF_SAMPLE_TOKENS = 8192  # the ViT-H configs are timed at T = 
 
 class RefStep:
     """One bounded step of the UNMODIFIED reference (oracle/_ref: lowprec::linear_forward +
-    linear_backward, {kSwitchBack, kInt8}) over both C2 linears, token rows sharded over the host
-    threads (rows are independent; dW partials summed in a fixed order). The
-    oracle port stands in only when oracle/_ref was not built."""
+    linear_backward, {kSwitchBack, kInt8}) over the chained C2 linears (fc1 -> fc2 forward,
+    fc2 -> fc1 backward), token rows sharded over the host threads (rows are independent,
+    SPEC.md:301-302; dW partials summed in a fixed order). The oracle port stands in only when
+    oracle/_ref was not built."""
 
     def __init__(self, tokens: int, threads: int | None = None):
         import numpy as np
@@ -162,28 +166,31 @@ class RefStep:
         self.kind = "reference" if O.ref_available() else "port"
         self.threads = (threads or os.cpu_count() or 1) if self.kind == "reference" else 1
         self.tokens = tokens
-        self.data = []
-        for i, (_, n, m) in enumerate(LAYERS):  # X, G ~ N(0, 1), W ~ N(0, 1/n) (model.cpp:199-202)
-            rng = np.random.default_rng(10 + i)
-            self.data.append((rng.standard_normal((tokens, n)).astype(np.float32),
-                              (rng.standard_normal((m, n)) / np.sqrt(n)).astype(np.float32),
-                              rng.standard_normal((tokens, m)).astype(np.float32), n, m))
+        (_, n, hd), (_, _, m) = LAYERS
+        rng = np.random.default_rng(10)  # X, G ~ N(0, 1), W ~ N(0, 1/fan_in) (model.cpp:199-202)
+        self.dims = (n, hd, m)
+        self.x = rng.standard_normal((tokens, n)).astype(np.float32)
+        self.w1 = (rng.standard_normal((hd, n)) / np.sqrt(n)).astype(np.float32)
+        self.w2 = (rng.standard_normal((m, hd)) / np.sqrt(hd)).astype(np.float32)
+        self.g = rng.standard_normal((tokens, m)).astype(np.float32)
 
     def run(self) -> float:
+        n, hd, m = self.dims
         t0 = time.perf_counter()
-        for x, w, g, n, m in self.data:
-            if self.kind == "reference":
-                rc = self.O.ref().ref_switchback_fwd_bwd_threaded(x, w, g, self.tokens, n, m, self.threads, None, None,
-                                                                  None)
-                assert rc == 0
-            else:
-                self.O.switchback_forward(x, w)
-                self.O.switchback_backward(x, w, g)
+        if self.kind == "reference":
+            rc = self.O.ref().ref_switchback_mlp_fwd_bwd_threaded(self.x, self.w1, self.w2, self.g, self.tokens, n, hd,
+                                                                  m, self.threads, None, None, None, None)
+            assert rc == 0
+        else:
+            h = self.O.switchback_forward(self.x, self.w1)
+            self.O.switchback_forward(h, self.w2)
+            dh, _ = self.O.switchback_backward(h, self.w2, self.g)
+            self.O.switchback_backward(self.x, self.w1, dh)
         return time.perf_counter() - t0
 
     def sample(self) -> str:
-        return (f"{self.tokens} tokens (BASELINE.md §3 sample) through fc1+fc2 (1280->5120, 5120->1280) SwitchBack "
-                f"int8 fwd+bwd per step, token rows sharded over {self.threads} threads; per-step time extrapolated "
+        return (f"{self.tokens} tokens (BASELINE.md §3 sample) through fc1 -> fc2 chained (1280->5120->1280) "
+                f"SwitchBack int8 fwd+bwd per step, token rows sharded over {self.threads} threads; per-step time extrapolated "
                 f"linearly to {T_PER_GPU} tokens (the reference's cost is linear in T: linear.cpp:43-51, "
                 f"matrix.cpp:58-66)")
 
@@ -291,6 +298,10 @@ def run_ours(args):
                "gq": empty(T, m, dtype=torch.int8), "gs": empty(T, dtype=torch.float32)}
         lay["ws"] = L._workspace(mode, T, n, m, dev)
         layers.append(lay)
+    chained = layers_cfg is LAYERS  # the MLP block: fc2 reads fc1's Y, fc1's G is fc2's dX
+    if chained:
+        layers[1]["x"] = layers[0]["y"]
+        layers[0]["g"] = layers[1]["dx"]
     h = A.handle(local)
     P = L._p
 
@@ -539,6 +550,7 @@ def run_ours(args):
     e2e = None
     if rank == 0 and not args.no_e2e and args.config == "c2":
         e2e = e2e_host(args, L, torch)
+        e2e["per_linear_entry"] = e2e_host_per_linear(args, L, torch)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and args.config == "c2":
         r, cores, sample, kind = cpu_reference_rate()
@@ -843,8 +855,40 @@ def cpu_optimizer_rate(budget_s: float = 10.0):
 
 
 def e2e_host(args, L, torch):
-    """Same workload through the C-ABI host-buffer entry sb_switchback_fwd_bwd_host:
-    pinned host X, W, G in; Y, dX, dW out, every step."""
+    """Same workload (the chained C2 MLP block) through the C-ABI host-buffer entry
+    sb_switchback_mlp_fwd_bwd_host: pinned host X, W1, W2, G in; Y, dX, dW1, dW2 out, every
+    step; the hidden activation and its gradient stay on the device (as in the device step)."""
+    from paper_2304_13013_b200 import _capi as A
+
+    T = args.tokens
+    (_, n, hd), (_, _, m) = LAYERS
+    g = torch.Generator().manual_seed(7)
+    x = torch.randn(T, n, generator=g).to(torch.bfloat16).pin_memory()
+    w1 = (torch.randn(hd, n, generator=g) / n ** 0.5).to(torch.bfloat16).pin_memory()
+    w2 = (torch.randn(m, hd, generator=g) / hd ** 0.5).to(torch.bfloat16).pin_memory()
+    gg = torch.randn(T, m, generator=g).to(torch.bfloat16).pin_memory()
+    h2d = (x.numel() + w1.numel() + w2.numel() + gg.numel()) * 2
+    d2h = (T * m + T * n) * 2 + (w1.numel() + w2.numel()) * 4
+    for _ in range(max(1, args.warmup // 2)):
+        L.switchback_mlp_fwd_bwd_host(x, w1, w2, gg, A.SB_ACT_NONE)
+    steps = max(1, min(args.steps, 10))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        L.switchback_mlp_fwd_bwd_host(x, w1, w2, gg, A.SB_ACT_NONE)  # returns after Y, dX, dW1, dW2 are on the host
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": T / dt, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "path": "sb_switchback_mlp_fwd_bwd_host (C-ABI, pinned host buffers, 8192-token chunks: H2D / kernels / "
+                    "D2H overlapped on three streams, hidden activation kept in HBM), one synchronous call per step",
+            "pcie_note": "H2D and D2H share the link: ~93 GB/s combined measured (tools/pcie_bw.py), so the "
+                         "752 MB of host traffic per step has an ~8.1 ms floor",
+            "steps": steps}
+
+
+def e2e_host_per_linear(args, L, torch):
+    """The per-linear host entry sb_switchback_fwd_bwd_host over both linears (X, W, G of each
+    linear in; Y, dX, dW out): the hidden activation crosses PCIe four times. Secondary."""
     T = args.tokens
     bufs = []
     g = torch.Generator().manual_seed(7)

@@ -327,6 +327,28 @@ sb_status sb_switchback_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, co
 sb_status sb_switchback_fwd_bwd_host_async(sb_handle h, const sb_linear_mode* mode, const void* x, const void* w,
                                            const void* g, sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y,
                                            void* dx, float* dw);
+/* Activation between the two linears of sb_switchback_mlp_fwd_bwd_host. */
+typedef enum sb_activation { SB_ACT_NONE = 0, SB_ACT_GELU = 1 } sb_activation;
+
+/* The MLP block of the reference's transformer_block (model.cpp:324-329) and its backward
+ * (model.cpp:351-360) over HOST buffers: two chained SwitchBack int8 linears
+ *   h_pre = linear_forward(x, w1) (b x hd), h = act(h_pre), y = linear_forward(h, w2) (b x m);
+ *   (d_h, dw2) = linear_backward(w2_ctx, g), d_hpre = d_h * act'(h_pre),
+ *   (dx, dw1) = linear_backward(w1_ctx, d_hpre).
+ * x (b x n), w1 (hd x n), w2 (m x hd), g (b x m) in; y (b x m), dx (b x n) out in dt, dw1 / dw2
+ * fp32. The hidden activation and its gradient never leave the device: token chunks stream
+ * through (H2D | kernels | D2H overlapped), so PCIe carries only the block's inputs and outputs.
+ * activation: SB_ACT_NONE (the two linears back to back) or SB_ACT_GELU (bf16, not exact;
+ * gelu(double) rounded to float as model.cpp:327, fused into the quantize kernels). Y and dX
+ * are per-row and bit-identical to the device-resident path; dw1 / dw2 sum the chunks in order. */
+sb_status sb_switchback_mlp_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, int activation, const void* x,
+                                         const void* w1, const void* w2, const void* g, sb_dtype dt, int64_t b,
+                                         int64_t n, int64_t hd, int64_t m, void* y, void* dx, float* dw1, float* dw2);
+/* Asynchronous form (same pools / rules as sb_switchback_fwd_bwd_host_async). */
+sb_status sb_switchback_mlp_fwd_bwd_host_async(sb_handle h, const sb_linear_mode* mode, int activation, const void* x,
+                                               const void* w1, const void* w2, const void* g, sb_dtype dt, int64_t b,
+                                               int64_t n, int64_t hd, int64_t m, void* y, void* dx, float* dw1,
+                                               float* dw2);
 /* Waits for every enqueued host-pipeline call; reports non-finite inputs like sb_synchronize. */
 sb_status sb_host_pipeline_wait(sb_handle h);
 

@@ -100,6 +100,9 @@ def ref():
                                          C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
         L.ref_switchback_fwd_bwd_threaded.argtypes = [_f32p, _f32p, _f32p, C.c_int64, C.c_int64, C.c_int64,
                                                       C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.ref_switchback_mlp_fwd_bwd_threaded.argtypes = [_f32p, _f32p, _f32p, _f32p, C.c_int64, C.c_int64,
+                                                          C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_void_p,
+                                                          C.c_void_p, C.c_void_p]
         L.ref_block_fwd_bwd.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_int,
                                         C.POINTER(C.c_void_p), _f32p, _f32p, _f32p, _f32p, C.POINTER(C.c_void_p)]
         pp = C.POINTER(C.c_void_p)

@@ -188,6 +188,54 @@ int ref_switchback_fwd_bwd_threaded(const float* x, const float* w, const float*
   });
 }
 
+// Two chained SwitchBack int8 linears (the MLP block of model.cpp:324-329 with no activation,
+// and its backward, model.cpp:351-360): h = linear_forward(x, w1), y = linear_forward(h, w2),
+// (dh, dw2) = linear_backward(ctx2, g), (dx, dw1) = linear_backward(ctx1, dh), with token rows
+// sharded over `threads` (every op is per row except the W quantize and the dW sums, whose
+// per-thread partials are added in thread order). Outputs may be null.
+int ref_switchback_mlp_fwd_bwd_threaded(const float* x, const float* w1, const float* w2, const float* g,
+                                        int64_t b, int64_t n, int64_t hd, int64_t m, int threads, float* y,
+                                        float* dx, float* dw1, float* dw2) {
+  return guarded([&] {
+    if (threads < 1) threads = 1;
+    if (threads > b) threads = int(b);
+    const LinearMode mode = mode_of(1, 0);
+    const Matrix w1m = to_matrix(w1, hd, n), w2m = to_matrix(w2, m, hd);
+    std::vector<Matrix> p1{size_t(threads)}, p2{size_t(threads)};
+    std::vector<std::exception_ptr> errs{size_t(threads)};
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) {
+      pool.emplace_back([&, t] {
+        try {
+          const int64_t r0 = b * t / threads, r1 = b * (t + 1) / threads;
+          LinearContext c1, c2;
+          const Matrix hs = linear_forward(mode, to_matrix(x + r0 * n, r1 - r0, n), w1m, &c1);
+          const Matrix ys = linear_forward(mode, hs, w2m, &c2);
+          auto g2 = linear_backward(mode, c2, to_matrix(g + r0 * m, r1 - r0, m));
+          auto g1 = linear_backward(mode, c1, g2.first);
+          if (y) std::memcpy(y + r0 * m, ys.data(), size_t(ys.size()) * sizeof(float));
+          if (dx) std::memcpy(dx + r0 * n, g1.first.data(), size_t(g1.first.size()) * sizeof(float));
+          p1[size_t(t)] = std::move(g1.second);
+          p2[size_t(t)] = std::move(g2.second);
+        } catch (...) {
+          errs[size_t(t)] = std::current_exception();
+        }
+      });
+    }
+    for (auto& th : pool) th.join();
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
+    auto sum = [&](float* dst, const std::vector<Matrix>& parts, int64_t count) {
+      if (!dst) return;
+      std::memset(dst, 0, size_t(count) * sizeof(float));
+      for (const Matrix& p : parts)
+        for (int64_t i = 0; i < count; ++i) dst[i] += p.data()[i];
+    };
+    sum(dw1, p1, hd * n);
+    sum(dw2, p2, m * hd);
+  });
+}
+
 // optimizer_step over `nt` tensors (flat views of shape 1 x numel).
 // clipping: 0 none, 1 update_clip, 2 grad_clip. alpha is the (constant) lr_schedule value.
 int ref_optimizer_step(int nt, float** theta, const float** grad, float** v, float** u,

@@ -23,6 +23,7 @@ SB_INT8, SB_FP8 = range(2)
 SB_SCALE_ROW_TENSOR, SB_SCALE_ROW_ROW, SB_SCALE_NONE = range(3)
 SB_CLIP_NONE, SB_CLIP_UPDATE, SB_CLIP_GRAD = range(3)
 SB_GEMM_AUTO, SB_GEMM_1CTA, SB_GEMM_2CTA, SB_GEMM_WIDE, SB_GEMM_2CTA_MC = range(5)
+SB_ACT_NONE, SB_ACT_GELU = range(2)
 
 # every symbol include/switchback_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = [
@@ -35,6 +36,7 @@ EXPORTS = [
     "sb_gelu_backward_quantize_rowwise", "sb_layernorm_quantize_rowwise", "sb_layernorm_backward_workspace_size",
     "sb_layernorm_backward",
     "sb_linear_backward", "sb_switchback_fwd_bwd_host", "sb_switchback_fwd_bwd_host_async",
+    "sb_switchback_mlp_fwd_bwd_host", "sb_switchback_mlp_fwd_bwd_host_async",
     "sb_host_pipeline_wait", "sb_stableadamw_workspace_size", "sb_stableadamw_step",
     "sb_device_alloc", "sb_device_free", "sb_copy_to_device", "sb_copy_to_host", "sb_check_finite", "sb_fp8_cast",
     "sb_transpose_i8", "sb_compute_rms", "sb_grad_clip_global_norm", "sb_filter_nonfinite", "sb_dequantize_values",
@@ -161,6 +163,10 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             "sb_layernorm_backward": ([v, v, v, i32, i64, i64, v, v, v, v, v, v, v, sz], i32),
             "sb_switchback_fwd_bwd_host": ([v, C.POINTER(LinearMode), v, v, v, i32, i64, i64, i64, v, v, v], i32),
             "sb_switchback_fwd_bwd_host_async": ([v, C.POINTER(LinearMode), v, v, v, i32, i64, i64, i64, v, v, v], i32),
+            "sb_switchback_mlp_fwd_bwd_host": ([v, C.POINTER(LinearMode), i32, v, v, v, v, i32, i64, i64, i64, i64,
+                                                v, v, v, v], i32),
+            "sb_switchback_mlp_fwd_bwd_host_async": ([v, C.POINTER(LinearMode), i32, v, v, v, v, i32, i64, i64, i64,
+                                                      i64, v, v, v, v], i32),
             "sb_host_pipeline_wait": ([v], i32),
             "sb_stableadamw_workspace_size": ([C.POINTER(AdamwTensor), i32, C.POINTER(sz)], i32),
             "sb_stableadamw_step": ([v, C.POINTER(AdamwTensor), i32, C.POINTER(AdamwHparams), i64, v, v, v, sz],

@@ -30,18 +30,23 @@ sb_status cuda_fail(const char* op, cudaError_t e) {
 
 unsigned int* scratch(sb_handle h, size_t words) {
   const size_t bytes = words * sizeof(unsigned int);
-  if (bytes > h->scratch_bytes) {
-    if (h->d_scratch) {
+  auto& e = h->scratch[h->stream];
+  if (bytes > e.second) {
+    // growing frees the old buffer: not allowed while the stream is being captured into a graph
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(h->stream, &cs);
+    if (cs != cudaStreamCaptureStatusNone) return nullptr;
+    if (e.first) {
       cudaStreamSynchronize(h->stream);
-      cudaFree(h->d_scratch);
+      cudaFree(e.first);
     }
-    h->d_scratch = nullptr;
-    h->scratch_bytes = 0;
-    size_t want = std::max<size_t>(bytes, 4096);
-    if (cudaMalloc(&h->d_scratch, want) != cudaSuccess) return nullptr;
-    h->scratch_bytes = want;
+    e = {nullptr, 0};
+    const size_t want = std::max<size_t>(bytes, 65536);
+    unsigned int* p = nullptr;
+    if (cudaMalloc(&p, want) != cudaSuccess) return nullptr;
+    e = {p, want};
   }
-  return h->d_scratch;
+  return e.first;
 }
 
 }  // namespace sb
@@ -249,7 +254,8 @@ sb_status sb_destroy(sb_handle h) {
   sb_dp_destroy(h);
   if (h->d_err) cudaFree(h->d_err);
   if (h->gelu_lut) cudaFree(h->gelu_lut);
-  if (h->d_scratch) cudaFree(h->d_scratch);
+  for (auto& kv : h->scratch)
+    if (kv.second.first) cudaFree(kv.second.first);
   for (int i = 0; i < 2; ++i) {
     if (h->dev_pool[i]) cudaFree(h->dev_pool[i]);
     if (h->pool_done[i]) cudaEventDestroy(h->pool_done[i]);
@@ -260,6 +266,7 @@ sb_status sb_destroy(sb_handle h) {
     for (auto& row : h->hp_ev)
       for (auto& e : row) cudaEventDestroy(e);
     cudaEventDestroy(h->hp_start);
+    cudaEventDestroy(h->hp_wready);
   }
   delete h;
   return SB_OK;
@@ -315,7 +322,7 @@ sb_status sb_quantize_columnwise(sb_handle h, const void* x, sb_dtype dt, int64_
   if (rows <= 0 || cols <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty matrix");
   if (!float_dtype(dt) || !x || (!q && !q_t) || !state || ldx < cols) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
   unsigned int* words = sb::scratch(h, cols + 1);
-  if (!words) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed");
+  if (!words) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed (or would grow inside a graph capture: run the op once on this stream first)");
   return q_columnwise(h, x, dt, rows, cols, ldx, q, ldq, q_t, ldqt, state, words);
 }
 
@@ -326,7 +333,7 @@ sb_status sb_quantize_tensorwise(sb_handle h, const void* x, sb_dtype dt, int64_
   if (rows <= 0 || cols <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty matrix");
   if (!float_dtype(dt) || !x || (!q && !q_t) || !state || ldx < cols) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
   unsigned int* words = sb::scratch(h, 4);
-  if (!words) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed");
+  if (!words) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed (or would grow inside a graph capture: run the op once on this stream first)");
   return q_tensorwise(h, x, dt, rows, cols, ldx, q, ldq, q_t, ldqt, state, words);
 }
 
@@ -361,7 +368,7 @@ sb_status sb_quantize_fp8(sb_handle h, const void* x, sb_dtype dt, int64_t rows,
   if (!float_dtype(dt) || !x || !q || !state || (fmt != SB_E4M3 && fmt != SB_E5M2) || axis < 0 || axis > 2)
     return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
   unsigned int* words = sb::scratch(h, std::max(rows, cols) + 1);
-  if (!words) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed");
+  if (!words) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed (or would grow inside a graph capture: run the op once on this stream first)");
   return q_fp8(h, x, dt, rows, cols, ldx, fmt, axis, q, ldq, state, words);
 }
 
@@ -841,6 +848,55 @@ sb_status sb_layernorm_backward(sb_handle h, const void* dh, const void* x, sb_d
 }
 
 // ------------------------------------------------- host-buffer pipeline --
+// Copy streams, per-slot events and the two alternating device pools of the host-buffer
+// entries; created on first use. *pi = the pool this call owns (big enough for `need`).
+static sb_status host_pool_acquire(sb_handle h, const char* op, size_t need, int* pi_out) {
+  if (!h->s_in) {
+    SB_CUDA_CHECK(op, cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
+    SB_CUDA_CHECK(op, cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
+    for (auto& row : h->hp_ev)
+      for (auto& e : row) SB_CUDA_CHECK(op, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    SB_CUDA_CHECK(op, cudaEventCreateWithFlags(&h->hp_start, cudaEventDisableTiming));
+    SB_CUDA_CHECK(op, cudaEventCreateWithFlags(&h->hp_wready, cudaEventDisableTiming));
+    for (auto& e : h->pool_done) SB_CUDA_CHECK(op, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  const int pi = h->pool_next;
+  h->pool_next ^= 1;
+  if (need > h->dev_pool_bytes[pi]) {
+    if (h->dev_pool[pi]) {
+      cudaDeviceSynchronize();  // the pool's previous call may still be in flight
+      cudaFree(h->dev_pool[pi]);
+    }
+    h->dev_pool[pi] = nullptr;
+    h->dev_pool_bytes[pi] = 0;
+    h->pool_used[pi] = false;
+    SB_CUDA_CHECK(op, cudaMalloc(&h->dev_pool[pi], need));
+    h->dev_pool_bytes[pi] = need;
+  }
+  *pi_out = pi;
+  return SB_OK;
+}
+
+// Stream order at the start of a host-pipeline call. s_in only writes this call's private
+// pool: it does not wait for earlier compute, so an async call's first chunks stream in while
+// the previous call drains.
+static void host_pool_begin(sb_handle h, int pi) {
+  cudaEventRecord(h->hp_start, h->stream);
+  cudaStreamWaitEvent(h->s_out, h->hp_start, 0);
+  if (h->pool_used[pi]) {  // this pool's previous call (two calls ago) has fully drained
+    cudaStreamWaitEvent(h->s_in, h->pool_done[pi], 0);
+    cudaStreamWaitEvent(h->stream, h->pool_done[pi], 0);
+  }
+}
+
+// Slot count / chunk rows of the host pipelines (SB_HOST_SLOTS / SB_HOST_CHUNK override).
+static void host_chunking(int64_t b, int64_t def_chunk, int* ns, int64_t* chunk) {
+  const char* ce = std::getenv("SB_HOST_CHUNK");
+  const char* se = std::getenv("SB_HOST_SLOTS");
+  *ns = se ? std::max(2, std::min(8, std::atoi(se))) : 4;
+  *chunk = std::min<int64_t>(b, ce ? std::max<int64_t>(128, std::atoll(ce)) : def_chunk);
+}
+
 // switchback_fwd_bwd over host memory: W is quantized once; token rows stream through in
 // chunks. Three streams: h2d copies, compute (the handle stream), d2h copies, so PCIe
 // transfers of chunk i+1 / i-1 overlap the kernels of chunk i. dW accumulates on the single
@@ -861,10 +917,9 @@ static sb_status fwd_bwd_host_enqueue(sb_handle h, const sb_linear_mode* mode, c
   // H2D) and drain (last D2H, the dW copy) short; 2048-row chunks x 4 slots measured best
   // (tools/e2e_sweep.py: 39.7 ms per C2 step async, against 40.4 ms at 4096 x 3).
   // SB_HOST_CHUNK / SB_HOST_SLOTS override the defaults (measurement knobs).
-  const char* ce = std::getenv("SB_HOST_CHUNK");
-  const char* se = std::getenv("SB_HOST_SLOTS");
-  const int NS = se ? std::max(2, std::min(8, std::atoi(se))) : 4;
-  const int64_t chunk = std::min<int64_t>(b, ce ? std::max<int64_t>(128, std::atoll(ce)) : 2048);
+  int NS = 4;
+  int64_t chunk = 2048;
+  host_chunking(b, 2048, &NS, &chunk);
   // device layout: W, W_q, W_qT, dW, states/words, NS x {x, g, y, dx, x_q, g_q, x states, g states}
   Carve c{nullptr};
   auto layout = [&](Carve& cv, void** P) {
@@ -888,27 +943,8 @@ static sb_status fwd_bwd_host_enqueue(sb_handle h, const sb_linear_mode* mode, c
   void* P[6 + 8 * 8];
   layout(c, P);
   const size_t need = c.off + 256;
-  if (!h->s_in) {
-    SB_CUDA_CHECK(op, cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
-    SB_CUDA_CHECK(op, cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
-    for (auto& row : h->hp_ev)
-      for (auto& e : row) SB_CUDA_CHECK(op, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    SB_CUDA_CHECK(op, cudaEventCreateWithFlags(&h->hp_start, cudaEventDisableTiming));
-    for (auto& e : h->pool_done) SB_CUDA_CHECK(op, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
-  const int pi = h->pool_next;
-  h->pool_next ^= 1;
-  if (need > h->dev_pool_bytes[pi]) {
-    if (h->dev_pool[pi]) {
-      cudaDeviceSynchronize();  // the pool's previous call may still be in flight
-      cudaFree(h->dev_pool[pi]);
-    }
-    h->dev_pool[pi] = nullptr;
-    h->dev_pool_bytes[pi] = 0;
-    h->pool_used[pi] = false;
-    SB_CUDA_CHECK(op, cudaMalloc(&h->dev_pool[pi], need));
-    h->dev_pool_bytes[pi] = need;
-  }
+  int pi = 0;
+  SB_TRY(host_pool_acquire(h, op, need, &pi));
   Carve c2{static_cast<uint8_t*>(h->dev_pool[pi])};
   layout(c2, P);
   void* dW_ = P[0];
@@ -923,14 +959,7 @@ static sb_status fwd_bwd_host_enqueue(sb_handle h, const sb_linear_mode* mode, c
   cudaEvent_t* ev_out = h->hp_ev[3];
 
   cudaStream_t comp = h->stream, s_in = h->s_in, s_out = h->s_out;
-  // s_in only writes this call's private pool: it does not wait for earlier compute, so an
-  // async call's first chunks stream in while the previous call drains
-  cudaEventRecord(h->hp_start, comp);
-  cudaStreamWaitEvent(s_out, h->hp_start, 0);
-  if (h->pool_used[pi]) {  // this pool's previous call (two calls ago) has fully drained
-    cudaStreamWaitEvent(s_in, h->pool_done[pi], 0);
-    cudaStreamWaitEvent(comp, h->pool_done[pi], 0);
-  }
+  host_pool_begin(h, pi);
   sb_status st = SB_OK;
   const int64_t nchunks = (b + chunk - 1) / chunk;
   auto h2d = [&](int64_t i) {
@@ -986,6 +1015,178 @@ static sb_status fwd_bwd_host_enqueue(sb_handle h, const sb_linear_mode* mode, c
   return st;
 }
 
+
+// Two chained SwitchBack int8 linears over host memory — the MLP block of model.cpp:324-329
+// (fc1: n -> hd, optional GELU, fc2: hd -> m) and its backward (model.cpp:351-360) — with the
+// hidden activation and its gradient kept on the device. Per token chunk (rows are
+// independent in every op but the W quantize and the dW sums):
+//   X_c -> q -> fc1 GEMM -> P_c [-> GELU] = A_c -> q -> fc2 GEMM -> Y_c            (Y_c out)
+//   G_c -> dW2 += G_c^T A_c (G_c's quantize in the same launch) -> dX2 GEMM -> dA_c
+//   [dA_c * GELU'(P_c)] = G1_c -> dW1 += G1_c^T X_c (+ quantize G1_c) -> dX GEMM -> dX_c (out)
+// dW1 / dW2 accumulate in chunk order on the compute stream (deterministic) and leave last.
+static sb_status mlp_host_enqueue(sb_handle h, const sb_linear_mode* mode, int activation, const void* x,
+                                  const void* w1, const void* w2, const void* g, sb_dtype dt, int64_t b, int64_t n,
+                                  int64_t hd, int64_t m, void* y, void* dx, float* dw1, float* dw2) {
+  const char* op = "switchback_mlp_fwd_bwd";
+  SB_TRY(check_h(h, op));
+  if (!mode || !x || !w1 || !w2 || !g || !y || !dx || !dw1 || !dw2 || !float_dtype(dt))
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  if (b <= 0 || n <= 0 || hd <= 0 || m <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty operand");
+  if (mode->variant != SB_SWITCHBACK || mode->format != SB_INT8)
+    return sb::fail(SB_ERR_UNSUPPORTED, op, "host pipeline implements SwitchBack int8");
+  if (activation != SB_ACT_NONE && activation != SB_ACT_GELU)
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "unknown activation");
+  if (activation == SB_ACT_GELU && (dt != SB_BF16 || mode->exact))
+    return sb::fail(SB_ERR_UNSUPPORTED, op, "GELU runs on the bf16 performance path");
+  const size_t es = sb::dt_size(dt);
+  const bool gelu = activation == SB_ACT_GELU;
+  // 8192-row chunks after a 2048-row first chunk measured best at the C2 shape (9.6 ms per call,
+  // 84% of the bidirectional PCIe floor; tools/mlp_e2e_sweep.py): the kernels of a chunk take
+  // half its copies, so fewer, larger chunks waste less on launch gaps and small GEMM waves
+  int NS = 4;
+  int64_t chunk = 8192;
+  host_chunking(b, 8192, &NS, &chunk);
+  // pool layout: weights {W1, W2, payloads (both layouts), states, words}, dW1, dW2; the
+  // compute-only chunk buffers once (one compute stream); NS copy slots {x, g, y, dx}
+  enum { W1, W2, W1Q, W1QT, W2Q, W2QT, WST1, WST2, WRD1, WRD2, DW1, DW2, XQ, XS, PRE, ACT, HQ, HS, GQ, GS, DA,
+         G1, G1Q, G1S, NFIX };
+  Carve c{nullptr};
+  auto layout = [&](Carve& cv, void** P) {
+    P[W1] = cv.take<uint8_t>(hd * n * es);
+    P[W2] = cv.take<uint8_t>(m * hd * es);
+    P[W1Q] = cv.take<int8_t>(hd * n);
+    P[W1QT] = cv.take<int8_t>(hd * n);
+    P[W2Q] = cv.take<int8_t>(m * hd);
+    P[W2QT] = cv.take<int8_t>(m * hd);
+    P[WST1] = cv.take<float>(8);
+    P[WST2] = cv.take<float>(8);
+    P[WRD1] = cv.take<unsigned int>(8);
+    P[WRD2] = cv.take<unsigned int>(8);
+    P[DW1] = cv.take<float>(hd * n);
+    P[DW2] = cv.take<float>(m * hd);
+    P[XQ] = cv.take<int8_t>(chunk * n);
+    P[XS] = cv.take<float>(chunk);
+    P[PRE] = cv.take<uint8_t>(chunk * hd * es);
+    P[ACT] = gelu ? cv.take<uint8_t>(chunk * hd * es) : P[PRE];
+    P[HQ] = cv.take<int8_t>(chunk * hd);
+    P[HS] = cv.take<float>(chunk);
+    P[GQ] = cv.take<int8_t>(chunk * m);
+    P[GS] = cv.take<float>(chunk);
+    P[DA] = cv.take<uint8_t>(chunk * hd * es);
+    P[G1] = gelu ? cv.take<uint8_t>(chunk * hd * es) : P[DA];
+    P[G1Q] = cv.take<int8_t>(chunk * hd);
+    P[G1S] = cv.take<float>(chunk);
+    for (int s = 0; s < NS; ++s) {
+      P[NFIX + 4 * s + 0] = cv.take<uint8_t>(chunk * n * es);
+      P[NFIX + 4 * s + 1] = cv.take<uint8_t>(chunk * m * es);
+      P[NFIX + 4 * s + 2] = cv.take<uint8_t>(chunk * m * es);
+      P[NFIX + 4 * s + 3] = cv.take<uint8_t>(chunk * n * es);
+    }
+  };
+  void* P[NFIX + 4 * 8];
+  layout(c, P);
+  int pi = 0;
+  SB_TRY(host_pool_acquire(h, op, c.off + 256, &pi));
+  Carve c2{static_cast<uint8_t*>(h->dev_pool[pi])};
+  layout(c2, P);
+  auto I8 = [&](int k) { return static_cast<int8_t*>(P[k]); };
+  auto F = [&](int k) { return static_cast<float*>(P[k]); };
+  cudaEvent_t* ev_in = h->hp_ev[0];
+  cudaEvent_t* ev_y = h->hp_ev[1];
+  cudaEvent_t* ev_comp = h->hp_ev[2];
+  cudaEvent_t* ev_out = h->hp_ev[3];
+  cudaStream_t comp = h->stream, s_in = h->s_in, s_out = h->s_out;
+  host_pool_begin(h, pi);
+  // chunk i covers rows [r0(i), r0(i) + rows(i)); the first chunk is a quarter chunk so the
+  // first Y leaves (and the D2H direction starts) sooner (SB_HOST_FIRST overrides)
+  const char* fe = std::getenv("SB_HOST_FIRST");
+  const int64_t first = std::min<int64_t>(b, fe ? std::max<int64_t>(128, std::atoll(fe)) : std::max<int64_t>(128, chunk / 4));
+  const int64_t nchunks = 1 + (b - first + chunk - 1) / chunk;
+  auto r0_of = [&](int64_t i) { return i == 0 ? int64_t(0) : first + (i - 1) * chunk; };
+  auto rows_of = [&](int64_t i) { return i == 0 ? first : std::min(chunk, b - r0_of(i)); };
+  auto h2d = [&](int64_t i) {
+    const int s = static_cast<int>(i % NS);
+    const int64_t r0 = r0_of(i), rows = rows_of(i);
+    if (i >= NS) cudaStreamWaitEvent(s_in, ev_comp[s], 0);  // slot's x, g consumed by chunk i-NS
+    cudaMemcpyAsync(P[NFIX + 4 * s + 0], static_cast<const uint8_t*>(x) + r0 * n * es, rows * n * es,
+                    cudaMemcpyHostToDevice, s_in);
+    cudaMemcpyAsync(P[NFIX + 4 * s + 1], static_cast<const uint8_t*>(g) + r0 * m * es, rows * m * es,
+                    cudaMemcpyHostToDevice, s_in);
+    cudaEventRecord(ev_in[s], s_in);
+  };
+  sb_status st = SB_OK;
+  // W1, then the first chunk, then W2 on the upload stream (in the order the first chunk's
+  // kernels need them); both weights quantized once (both layouts)
+  cudaMemcpyAsync(P[W1], w1, hd * n * es, cudaMemcpyHostToDevice, s_in);
+  h2d(0);
+  cudaMemcpyAsync(P[W2], w2, m * hd * es, cudaMemcpyHostToDevice, s_in);
+  cudaEventRecord(h->hp_wready, s_in);
+  cudaStreamWaitEvent(comp, h->hp_wready, 0);
+  st = q_tensorwise(h, P[W1], dt, hd, n, n, I8(W1Q), n, I8(W1QT), hd, F(WST1), static_cast<unsigned int*>(P[WRD1]));
+  if (st == SB_OK)
+    st = q_tensorwise(h, P[W2], dt, m, hd, hd, I8(W2Q), hd, I8(W2QT), m, F(WST2), static_cast<unsigned int*>(P[WRD2]));
+  for (int64_t i = 1; i < std::min<int64_t>(NS - 1, nchunks); ++i) h2d(i);
+  auto qrow = [&](const void* src, int64_t rows, int64_t cols, int8_t* q, float* s) {
+    if (st == SB_OK && sb::launch_quantize_rowwise(h, src, dt, rows, cols, cols, q, cols, s) != cudaSuccess)
+      st = sb::cuda_fail(op, cudaGetLastError());
+  };
+  auto act = [&](int md, const void* a, const void* bb, int64_t rows, void* out, int8_t* q, float* s) {
+    if (st == SB_OK && sb::launch_act_quantize_rowwise(h, md, a, bb, rows, hd, out, q, s) != cudaSuccess)
+      st = sb::cuda_fail(op, cudaGetLastError());
+  };
+  for (int64_t i = 0; i < nchunks && st == SB_OK; ++i) {
+    const int s = static_cast<int>(i % NS);
+    const int64_t r0 = r0_of(i), rows = rows_of(i);
+    if (i + NS - 1 < nchunks) h2d(i + NS - 1);
+    cudaStreamWaitEvent(comp, ev_in[s], 0);
+    if (i >= NS) cudaStreamWaitEvent(comp, ev_out[s], 0);  // slot's y, dx copied out
+    void* xd = P[NFIX + 4 * s + 0];
+    void* gd = P[NFIX + 4 * s + 1];
+    void* yd = P[NFIX + 4 * s + 2];
+    void* dxd = P[NFIX + 4 * s + 3];
+    // forward
+    qrow(xd, rows, n, I8(XQ), F(XS));
+    if (st == SB_OK) st = sb::gemm_i8(h, I8(XQ), F(XS), I8(W1Q), F(WST1), SB_SCALE_ROW_TENSOR, rows, hd, n, P[PRE], dt, mode->exact);
+    if (gelu)
+      act(0, P[PRE], nullptr, rows, P[ACT], I8(HQ), F(HS));
+    else
+      qrow(P[PRE], rows, hd, I8(HQ), F(HS));
+    if (st == SB_OK) st = sb::gemm_i8(h, I8(HQ), F(HS), I8(W2Q), F(WST2), SB_SCALE_ROW_TENSOR, rows, m, hd, yd, dt, mode->exact);
+    cudaEventRecord(ev_y[s], comp);
+    // backward: fc2 (dW2 with G's quantize in the launch, then dA), then fc1
+    const sb::RowQuant rq2{I8(GQ), m, F(GS)};
+    if (st == SB_OK) st = sb::wgrad(h, gd, P[ACT], dt, rows, m, hd, F(DW2), mode->exact, i > 0, &rq2);
+    const bool last = i == nchunks - 1;
+    if (last) cudaEventRecord(ev_comp[(s + 1) % NS], comp);  // dW2 complete (that slot's event is not waited on again)
+    if (st == SB_OK) st = sb::gemm_i8(h, I8(GQ), F(GS), I8(W2QT), F(WST2), SB_SCALE_ROW_TENSOR, rows, hd, m, P[DA], dt, mode->exact);
+    if (gelu) {
+      act(1, P[DA], P[PRE], rows, P[G1], I8(G1Q), F(G1S));
+      if (st == SB_OK) st = sb::wgrad(h, P[G1], xd, dt, rows, hd, n, F(DW1), mode->exact, i > 0);
+    } else {
+      const sb::RowQuant rq1{I8(G1Q), hd, F(G1S)};
+      if (st == SB_OK) st = sb::wgrad(h, P[G1], xd, dt, rows, hd, n, F(DW1), mode->exact, i > 0, &rq1);
+    }
+    if (st == SB_OK) st = sb::gemm_i8(h, I8(G1Q), F(G1S), I8(W1QT), F(WST1), SB_SCALE_ROW_TENSOR, rows, n, hd, dxd, dt, mode->exact);
+    cudaEventRecord(ev_comp[s], comp);
+    cudaStreamWaitEvent(s_out, ev_y[s], 0);
+    cudaMemcpyAsync(static_cast<uint8_t*>(y) + r0 * m * es, yd, rows * m * es, cudaMemcpyDeviceToHost, s_out);
+    if (last) {  // dW2 leaves while the last chunk's fc1 backward runs
+      cudaStreamWaitEvent(s_out, ev_comp[(s + 1) % NS], 0);
+      cudaMemcpyAsync(dw2, P[DW2], m * hd * sizeof(float), cudaMemcpyDeviceToHost, s_out);
+    }
+    cudaStreamWaitEvent(s_out, ev_comp[s], 0);
+    cudaMemcpyAsync(static_cast<uint8_t*>(dx) + r0 * n * es, dxd, rows * n * es, cudaMemcpyDeviceToHost, s_out);
+    cudaEventRecord(ev_out[s], s_out);
+  }
+  // as fwd_bwd_host_enqueue: dW1 leaves after the last chunk; the event frees the pool
+  cudaEventRecord(ev_comp[0], comp);
+  cudaStreamWaitEvent(s_out, ev_comp[0], 0);
+  cudaMemcpyAsync(dw1, P[DW1], hd * n * sizeof(float), cudaMemcpyDeviceToHost, s_out);
+  cudaEventRecord(h->pool_done[pi], s_out);
+  h->pool_used[pi] = true;
+  return st;
+}
+
 }  // extern "C"
 namespace {
 sb_status host_pipeline_check(sb_handle h, const char* op) {
@@ -1016,6 +1217,20 @@ sb_status sb_switchback_fwd_bwd_host_async(sb_handle h, const sb_linear_mode* mo
                                            const void* g, sb_dtype dt, int64_t b, int64_t n, int64_t m, void* y,
                                            void* dx, float* dw) {
   return fwd_bwd_host_enqueue(h, mode, x, w, g, dt, b, n, m, y, dx, dw);
+}
+
+sb_status sb_switchback_mlp_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, int activation, const void* x,
+                                         const void* w1, const void* w2, const void* g, sb_dtype dt, int64_t b,
+                                         int64_t n, int64_t hd, int64_t m, void* y, void* dx, float* dw1, float* dw2) {
+  SB_TRY(mlp_host_enqueue(h, mode, activation, x, w1, w2, g, dt, b, n, hd, m, y, dx, dw1, dw2));
+  return host_pipeline_check(h, "switchback_mlp_fwd_bwd");
+}
+
+sb_status sb_switchback_mlp_fwd_bwd_host_async(sb_handle h, const sb_linear_mode* mode, int activation, const void* x,
+                                               const void* w1, const void* w2, const void* g, sb_dtype dt, int64_t b,
+                                               int64_t n, int64_t hd, int64_t m, void* y, void* dx, float* dw1,
+                                               float* dw2) {
+  return mlp_host_enqueue(h, mode, activation, x, w1, w2, g, dt, b, n, hd, m, y, dx, dw1, dw2);
 }
 
 sb_status sb_host_pipeline_wait(sb_handle h) {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
 #include <string>
 #include <utility>
 
@@ -14,14 +15,17 @@ struct sb_handle_s {
   cudaStream_t stream = nullptr;
   int num_sms = 148;
   uint32_t* d_err = nullptr;       // device error latch (bit 0: non-finite input seen)
-  unsigned int* d_scratch = nullptr;  // small scratch (tensor absmax words etc.)
-  size_t scratch_bytes = 0;
+  // small per-stream scratch (tensor absmax words etc.) for the standalone ops that have no
+  // caller workspace: one buffer per CUDA stream the handle has been bound to, so ops enqueued
+  // on two streams never share words; grown only outside stream capture
+  std::map<cudaStream_t, std::pair<unsigned int*, size_t>> scratch;
   uint64_t launches = 0;
   int gemm_path = 0;  // sb_gemm_path
   // host-buffer pipeline (sb_switchback_fwd_bwd_host): copy streams + events, created once
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaEvent_t hp_ev[4][8] = {};  // [in, y, comp, out][slot] (host pipeline, up to 8 slots)
   cudaEvent_t hp_start = nullptr;
+  cudaEvent_t hp_wready = nullptr;  // MLP host pipeline: both weights uploaded
   // two device pools used by alternate host-pipeline calls, so an async call's transfers
   // overlap the previous call's drain without aliasing its buffers
   void* dev_pool[2] = {nullptr, nullptr};

@@ -221,7 +221,7 @@ sb_status sb_compute_rms(sb_handle h, const float* g, const float* u, int64_t n,
   if (n <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty input");
   const int np = static_cast<int>(grid_of(n, h->num_sms));
   double* partial = reinterpret_cast<double*>(sb::scratch(h, 2 * static_cast<size_t>(np) + 2));
-  if (!partial) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed");
+  if (!partial) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed (or would grow inside a graph capture: run the op once on this stream first)");
   h->launches += 2;
   k_partial<<<np, kT, 0, h->stream>>>(g, u, n, eps * eps, 0, partial);
   k_finish<<<1, kT, 0, h->stream>>>(partial, np, static_cast<double>(n), 0, 0.0, out);
@@ -241,7 +241,7 @@ sb_status sb_grad_clip_global_norm(sb_handle h, float* const* grads, const int64
     total += np[static_cast<size_t>(i)];
   }
   double* partial = reinterpret_cast<double*>(sb::scratch(h, 2 * static_cast<size_t>(total) + 4));
-  if (!partial) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed");
+  if (!partial) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed (or would grow inside a graph capture: run the op once on this stream first)");
   double* clip = partial + total;
   int off = 0;
   for (int i = 0; i < n; ++i) {

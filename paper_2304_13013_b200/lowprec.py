@@ -614,6 +614,34 @@ def switchback_fwd_bwd_host(x, w, g, exact: bool = False):
     return y, dx, dw
 
 
+def switchback_mlp_fwd_bwd_host(x, w1, w2, g, activation: int = A.SB_ACT_NONE, exact: bool = False,
+                                wait: bool = True):
+    """The MLP block of transformer_block / block_backward (model.cpp:324-329, 351-360) over
+    HOST tensors: y = fc2(act(fc1(x))) and its backward for the block-output gradient g, the
+    hidden activation kept on the device. x (b, n), w1 (hd, n), w2 (m, hd), g (b, m) pinned CPU
+    tensors; returns (y, dx, dw1, dw2) on the host. wait=False enqueues only
+    (sb_switchback_mlp_fwd_bwd_host_async; call host_pipeline_wait() before reading)."""
+    b, n = x.shape
+    hd, m = w1.shape[0], w2.shape[0]
+    if w1.shape[1] != n or w2.shape[1] != hd or tuple(g.shape) != (b, m):
+        raise ValueError("switchback_mlp_fwd_bwd: shape mismatch")
+    y = torch.empty((b, m), dtype=x.dtype, pin_memory=True)
+    dx = torch.empty((b, n), dtype=x.dtype, pin_memory=True)
+    dw1 = torch.empty((hd, n), dtype=torch.float32, pin_memory=True)
+    dw2 = torch.empty((m, hd), dtype=torch.float32, pin_memory=True)
+    h = A.handle()
+    md = LinearMode(A.SB_SWITCHBACK, A.SB_INT8, exact=exact)
+    fn = h.lib.sb_switchback_mlp_fwd_bwd_host if wait else h.lib.sb_switchback_mlp_fwd_bwd_host_async
+    A.check(fn(h.h, C.byref(md.c()), activation, _p(x), _p(w1), _p(w2), _p(g), _dt(x), b, n, hd, m, _p(y), _p(dx),
+               _p(dw1), _p(dw2)))
+    return y, dx, dw1, dw2
+
+
+def host_pipeline_wait():
+    h = A.handle()
+    A.check(h.lib.sb_host_pipeline_wait(h.h))
+
+
 # ---------------------------------------------------------------- optimizer
 @dataclass
 class OptimizerHyperparams:
