@@ -298,6 +298,16 @@ def run_ours(args):
                "gq": empty(T, m, dtype=torch.int8), "gs": empty(T, dtype=torch.float32)}
         lay["ws"] = L._workspace(mode, T, n, m, dev)
         layers.append(lay)
+    # --dw-comm fused: dW lives in a symmetric (peer-mapped) buffer and the dW GEMM's epilogue
+    # reduce-scatters into the owner ranks' copies (sb_dp_wgrad_allreduce_fused: zero, barrier,
+    # GEMM + reduce-scatter, barrier, all-gather of owned rows); NCCL calls inside it, so eager
+    fused_comm = args.dw_comm == "fused" and plain and not args.unfused_gq
+    if fused_comm:
+        args.no_graph = True
+        comm0 = dp.NcclComm(A.handle(local), rank, world) if world > 1 else None
+        for lay in layers:
+            lay["sym"] = dp.SymmetricBuffer(A.handle(local), 4 * lay["m"] * lay["n"], rank, world, comm=comm0)
+            lay["dw"] = lay["sym"].view((lay["m"], lay["n"]))
     chained = layers_cfg is LAYERS  # the MLP block: fc2 reads fc1's Y, fc1's G is fc2's dX
     if chained:
         layers[1]["x"] = layers[0]["y"]
@@ -334,6 +344,10 @@ def run_ours(args):
     def dw_gemm(l):
         A.check(h.lib.sb_wgrad(h.h, P(l["g"]), P(l["x"]), A.SB_BF16, T, l["m"], l["n"], P(l["dw"]), 0, 0))
 
+    def dw_fused_comm(l):  # dW GEMM + reduce-scatter epilogue + all-gather (world 1: the GEMM alone)
+        A.check(h.lib.sb_dp_wgrad_allreduce_fused(h.h, P(l["g"]), P(l["x"]), A.SB_BF16, T, l["m"], l["n"], P(l["dw"]),
+                                                  P(l["gq"]), l["m"], P(l["gs"])))
+
     def dw_gemm_gq(l):  # dW GEMM with quantize_rowwise(G) in the same launch
         A.check(h.lib.sb_wgrad_quantize_rowwise(h.h, P(l["g"]), P(l["x"]), A.SB_BF16, T, l["m"], l["n"], P(l["dw"]),
                                                 P(l["gq"]), l["m"], P(l["gs"])))
@@ -362,7 +376,11 @@ def run_ours(args):
             ops.append(Op(f"{nm} linear_forward", lambda l=l: layer_fwd(l), "layer", 2 * T * m * n))
     for l in reversed(layers):
         nm, n, m = l["name"], l["n"], l["m"]
-        if fused_gq:
+        if fused_comm:
+            ops.append(Op(f"{nm} bf16 dW GEMM m={m} n={n} K={T} + quantize_rowwise G + reduce-scatter",
+                          lambda l=l: dw_fused_comm(l), "dw_gemm", 2 * T * m * n))
+            ops.append(Op(f"{nm} int8 dX GEMM M={T} N={n} K={m}", lambda l=l: gemm_dx(l), "int8_gemm", 2 * T * m * n))
+        elif fused_gq:
             ops.append(Op(f"{nm} bf16 dW GEMM m={m} n={n} K={T} + quantize_rowwise G {T}x{m}",
                           lambda l=l: dw_gemm_gq(l), "dw_gemm", 2 * T * m * n, ar=l["dw"]))
             ops.append(Op(f"{nm} int8 dX GEMM M={T} N={n} K={m}", lambda l=l: gemm_dx(l), "int8_gemm", 2 * T * m * n))
@@ -390,7 +408,7 @@ def run_ours(args):
     # the dW all-reduce: the library's own NCCL communicator (sb_dp_init, csrc/dp.cu) when the
     # ranks run NCCL; torch.distributed only for the gloo test hook
     comm = None
-    if world > 1 and torch.distributed.get_backend() == "nccl":
+    if world > 1 and torch.distributed.get_backend() == "nccl" and not fused_comm:
         comm = dp.NcclComm(h, rank, world)
     ar = dp.GradAllReduce(comm=comm)
 
@@ -568,6 +586,8 @@ def run_ours(args):
                            "layers": [f"{n}->{m}" for _, n, m in layers_cfg], "parallelism": f"dp{world} (token shards)",
                            "l2": "inputs larger than L2 (X, G operands 168-673 MB each)",
                            "cuda_graphs": not args.no_graph,
+                           "dw_comm": ("fused GEMM + peer reduce-scatter + all-gather" if fused_comm else
+                                       "NCCL all-reduce on a comm stream") if world > 1 else None,
                            "g_quantize": ("fused into the dW GEMM launch (sb_wgrad_quantize_rowwise)" if fused_gq else
                                           "own kernel on a side stream next to the dW GEMM" if overlap else
                                           "own kernel, serial") if plain else "inside sb_linear_backward"},
@@ -953,6 +973,9 @@ def main():
     ap.add_argument("--unfused-gq", action="store_true",
                     help="quantize G in its own kernel instead of inside the dW GEMM launch (A/B)")
     ap.add_argument("--qkv-packed", action="store_true", help="vit_block: one scale for the packed qkv weight")
+    ap.add_argument("--dw-comm", default="allreduce", choices=["allreduce", "fused"],
+                    help="N > 1: NCCL all-reduce of dW after the GEMM on a comm stream (default), or the dW "
+                         "GEMM's reduce-scatter epilogue over peer memory + all-gather (sb_dp_wgrad_allreduce_fused)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

@@ -449,6 +449,37 @@ sb_status sb_dp_allreduce_max_u32(sb_handle h, unsigned int* words, int64_t n);
 sb_status sb_dp_allreduce_sum_f64(sb_handle h, double* vals, int64_t n);
 sb_status sb_dp_destroy(sb_handle h);
 
+/* Fused dW GEMM + reduce-scatter over peer memory (SURVEY.md §8e stage 2). dW lives in a
+ * symmetric buffer: the same allocation on every rank, each rank's copy mapped into every
+ * process (CUDA IPC over NVLink). The one-wave dW kernel's epilogue reduce-adds (TMA
+ * cp.reduce.async.bulk .add.f32) every 32-row block of G_r^T X_r into the copy of the rank owning
+ * that block (sb_dp_owned_rows), so the reduction streams out while the GEMM runs; the owned rows
+ * are then all-gathered. The sum order across ranks is not fixed: dW matches the single-GPU
+ * result within fp32 tolerance (with one rank: bit-identical to sb_wgrad).
+ *   alloc:    cudaMalloc + cudaIpcGetMemHandle (64-byte handle out);
+ *   open:     map the peers' copies from the world x 64 bytes of handles (exchanged out of band);
+ *   exchange: alloc's handle all-gathered over the handle's NCCL communicator, then open. */
+sb_status sb_dp_symmetric_alloc(sb_handle h, size_t bytes, void** ptr, uint8_t* ipc_handle /* 64 bytes */);
+sb_status sb_dp_symmetric_open(sb_handle h, void* ptr, int rank, int world, const uint8_t* ipc_handles);
+sb_status sb_dp_symmetric_exchange(sb_handle h, void* ptr, const uint8_t* ipc_handle);
+sb_status sb_dp_symmetric_free(sb_handle h, void* ptr);
+/* Rows [r0, r1) of a `rows`-row dW that `rank` owns: 32-row blocks, block rb -> rank rb*world/nblocks. */
+sb_status sb_dp_owned_rows(int64_t rows, int rank, int world, int64_t* r0, int64_t* r1);
+/* The fused GEMM alone: dw (m x n fp32, inside an opened symmetric buffer) must be zeroed on every
+ * rank, and that ordered before this call on every rank (sb_dp_barrier). g_q / g_state (optional):
+ * G's row-wise quantize in the same launch, as sb_wgrad_quantize_rowwise. bf16 operands, shapes
+ * the one-wave dW kernel serves (SB_ERR_UNSUPPORTED otherwise). */
+sb_status sb_wgrad_reduce_scatter(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m,
+                                  int64_t n, float* dw, int8_t* g_q, int64_t ldq, float* g_state);
+/* Stream-ordered barrier over the communicator (a one-element all-reduce). */
+sb_status sb_dp_barrier(sb_handle h);
+/* Every owner's rows of dw broadcast into the other ranks' copies (one NCCL group). */
+sb_status sb_dp_allgather_rows(sb_handle h, float* dw, int64_t m, int64_t n);
+/* zero + barrier + sb_wgrad_reduce_scatter + barrier + sb_dp_allgather_rows on the handle's
+ * stream: dw = sum over ranks of G_r^T X_r on every rank. */
+sb_status sb_dp_wgrad_allreduce_fused(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m,
+                                      int64_t n, float* dw, int8_t* g_q, int64_t ldq, float* g_state);
+
 #ifdef __cplusplus
 }
 #endif

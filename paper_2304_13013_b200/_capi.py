@@ -42,7 +42,9 @@ EXPORTS = [
     "sb_transpose_i8", "sb_compute_rms", "sb_grad_clip_global_norm", "sb_filter_nonfinite", "sb_dequantize_values",
     "sb_set_gemm_path", "sb_dp_available", "sb_dp_unique_id", "sb_dp_init", "sb_dp_rank",
     "sb_dp_allreduce_grads_async", "sb_dp_wait", "sb_dp_allreduce_max_u32", "sb_dp_allreduce_sum_f64",
-    "sb_dp_destroy",
+    "sb_dp_destroy", "sb_dp_symmetric_alloc", "sb_dp_symmetric_open", "sb_dp_symmetric_exchange",
+    "sb_dp_symmetric_free", "sb_dp_owned_rows", "sb_wgrad_reduce_scatter", "sb_dp_barrier", "sb_dp_allgather_rows",
+    "sb_dp_wgrad_allreduce_fused",
 ]
 
 
@@ -153,6 +155,15 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             "sb_dp_allreduce_max_u32": ([v, v, i64], i32),
             "sb_dp_allreduce_sum_f64": ([v, v, i64], i32),
             "sb_dp_destroy": ([v], i32),
+            "sb_dp_symmetric_alloc": ([v, sz, C.POINTER(v), v], i32),
+            "sb_dp_symmetric_open": ([v, v, i32, i32, v], i32),
+            "sb_dp_symmetric_exchange": ([v, v, v], i32),
+            "sb_dp_symmetric_free": ([v, v], i32),
+            "sb_dp_owned_rows": ([i64, i32, i32, C.POINTER(i64), C.POINTER(i64)], i32),
+            "sb_wgrad_reduce_scatter": ([v, v, v, i32, i64, i64, i64, v, v, i64, v], i32),
+            "sb_dp_barrier": ([v], i32),
+            "sb_dp_allgather_rows": ([v, v, i64, i64], i32),
+            "sb_dp_wgrad_allreduce_fused": ([v, v, v, i32, i64, i64, i64, v, v, i64, v], i32),
             "sb_linear_backward_prequant": ([v, C.POINTER(LinearMode), C.POINTER(LinearCtx), v, v, v, v, v, i32], i32),
             "sb_linear_forward_residual": ([v, C.POINTER(LinearMode), v, v, v, v, v, v, i32, i64, i64, i64, v,
                                             C.POINTER(LinearCtx), v, sz], i32),

@@ -30,23 +30,25 @@ sb_status cuda_fail(const char* op, cudaError_t e) {
 
 unsigned int* scratch(sb_handle h, size_t words) {
   const size_t bytes = words * sizeof(unsigned int);
+  auto it = h->scratch.find(h->stream);
+  if (it != h->scratch.end() && bytes <= it->second.second) return it->second.first;
+  // a stream seen for the first time inside a graph capture cannot allocate (cudaMalloc /
+  // cudaFree are illegal while capturing): it uses the buffer made at sb_create
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(h->stream, &cs);
+  if (cs != cudaStreamCaptureStatusNone)
+    return bytes <= h->capture_scratch_bytes ? h->capture_scratch : nullptr;
   auto& e = h->scratch[h->stream];
-  if (bytes > e.second) {
-    // growing frees the old buffer: not allowed while the stream is being captured into a graph
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(h->stream, &cs);
-    if (cs != cudaStreamCaptureStatusNone) return nullptr;
-    if (e.first) {
-      cudaStreamSynchronize(h->stream);
-      cudaFree(e.first);
-    }
-    e = {nullptr, 0};
-    const size_t want = std::max<size_t>(bytes, 65536);
-    unsigned int* p = nullptr;
-    if (cudaMalloc(&p, want) != cudaSuccess) return nullptr;
-    e = {p, want};
+  if (e.first) {
+    cudaStreamSynchronize(h->stream);
+    cudaFree(e.first);
   }
-  return e.first;
+  e = {nullptr, 0};
+  const size_t want = std::max<size_t>(bytes, 65536);
+  unsigned int* p = nullptr;
+  if (cudaMalloc(&p, want) != cudaSuccess) return nullptr;
+  e = {p, want};
+  return p;
 }
 
 }  // namespace sb
@@ -237,6 +239,12 @@ sb_status sb_create(int device, sb_handle* out) {
     return sb::fail(SB_ERR_CUDA, "sb_create", "allocation failed");
   }
   cudaMemset(h->d_err, 0, sizeof(uint32_t));
+  h->capture_scratch_bytes = 1 << 20;
+  if (cudaMalloc(&h->capture_scratch, h->capture_scratch_bytes) != cudaSuccess) {
+    cudaFree(h->d_err);
+    delete h;
+    return sb::fail(SB_ERR_CUDA, "sb_create", "allocation failed");
+  }
   if (sb::build_gelu_lut(h) != cudaSuccess) {
     cudaFree(h->d_err);
     delete h;
@@ -252,10 +260,12 @@ sb_status sb_destroy(sb_handle h) {
   cudaSetDevice(h->device);
   cudaDeviceSynchronize();
   sb_dp_destroy(h);
+  sb::dp_free_symmetric(h);
   if (h->d_err) cudaFree(h->d_err);
   if (h->gelu_lut) cudaFree(h->gelu_lut);
   for (auto& kv : h->scratch)
     if (kv.second.first) cudaFree(kv.second.first);
+  if (h->capture_scratch) cudaFree(h->capture_scratch);
   for (int i = 0; i < 2; ++i) {
     if (h->dev_pool[i]) cudaFree(h->dev_pool[i]);
     if (h->pool_done[i]) cudaEventDestroy(h->pool_done[i]);
@@ -322,7 +332,7 @@ sb_status sb_quantize_columnwise(sb_handle h, const void* x, sb_dtype dt, int64_
   if (rows <= 0 || cols <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty matrix");
   if (!float_dtype(dt) || !x || (!q && !q_t) || !state || ldx < cols) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
   unsigned int* words = sb::scratch(h, cols + 1);
-  if (!words) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed (or would grow inside a graph capture: run the op once on this stream first)");
+  if (!words) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed (inside a graph capture: at most 256 K words)");
   return q_columnwise(h, x, dt, rows, cols, ldx, q, ldq, q_t, ldqt, state, words);
 }
 
@@ -333,7 +343,7 @@ sb_status sb_quantize_tensorwise(sb_handle h, const void* x, sb_dtype dt, int64_
   if (rows <= 0 || cols <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty matrix");
   if (!float_dtype(dt) || !x || (!q && !q_t) || !state || ldx < cols) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
   unsigned int* words = sb::scratch(h, 4);
-  if (!words) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed (or would grow inside a graph capture: run the op once on this stream first)");
+  if (!words) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed (inside a graph capture: at most 256 K words)");
   return q_tensorwise(h, x, dt, rows, cols, ldx, q, ldq, q_t, ldqt, state, words);
 }
 
@@ -368,7 +378,7 @@ sb_status sb_quantize_fp8(sb_handle h, const void* x, sb_dtype dt, int64_t rows,
   if (!float_dtype(dt) || !x || !q || !state || (fmt != SB_E4M3 && fmt != SB_E5M2) || axis < 0 || axis > 2)
     return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
   unsigned int* words = sb::scratch(h, std::max(rows, cols) + 1);
-  if (!words) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed (or would grow inside a graph capture: run the op once on this stream first)");
+  if (!words) return sb::fail(SB_ERR_CUDA, op, "scratch allocation failed (inside a graph capture: at most 256 K words)");
   return q_fp8(h, x, dt, rows, cols, ldx, fmt, axis, q, ldq, state, words);
 }
 

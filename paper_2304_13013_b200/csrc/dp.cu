@@ -22,6 +22,7 @@
 #include <cstring>
 #include <algorithm>
 #include <mutex>
+#include <vector>
 #include <string>
 
 #include "sb_internal.h"
@@ -35,7 +36,7 @@ typedef struct {
 } ncclUniqueId;
 typedef enum { ncclSuccess = 0 } ncclResult_t;
 enum { ncclSum = 0, ncclMax = 2 };
-enum { ncclUint32 = 3, ncclInt64 = 4, ncclFloat32 = 7, ncclFloat64 = 8 };
+enum { ncclUint8 = 1, ncclUint32 = 3, ncclInt64 = 4, ncclFloat32 = 7, ncclFloat64 = 8 };
 
 struct Nccl {
   void* lib = nullptr;
@@ -45,6 +46,7 @@ struct Nccl {
   int (*allReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   int (*reduceScatter)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   int (*allGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  int (*broadcast)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   int (*groupStart)() = nullptr;
   int (*groupEnd)() = nullptr;
   const char* (*errorString)(int) = nullptr;
@@ -68,11 +70,13 @@ Nccl& nccl() {
     n.allReduce = reinterpret_cast<decltype(n.allReduce)>(dlsym(n.lib, "ncclAllReduce"));
     n.reduceScatter = reinterpret_cast<decltype(n.reduceScatter)>(dlsym(n.lib, "ncclReduceScatter"));
     n.allGather = reinterpret_cast<decltype(n.allGather)>(dlsym(n.lib, "ncclAllGather"));
+    n.broadcast = reinterpret_cast<decltype(n.broadcast)>(dlsym(n.lib, "ncclBroadcast"));
     n.groupStart = reinterpret_cast<decltype(n.groupStart)>(dlsym(n.lib, "ncclGroupStart"));
     n.groupEnd = reinterpret_cast<decltype(n.groupEnd)>(dlsym(n.lib, "ncclGroupEnd"));
     n.errorString = reinterpret_cast<decltype(n.errorString)>(dlsym(n.lib, "ncclGetErrorString"));
     n.getVersion = reinterpret_cast<decltype(n.getVersion)>(dlsym(n.lib, "ncclGetVersion"));
     n.ok = n.getUniqueId && n.commInitRank && n.commDestroy && n.allReduce && n.reduceScatter && n.allGather &&
+           n.broadcast &&
            n.groupStart && n.groupEnd && n.errorString;
   });
   return n;
@@ -122,6 +126,31 @@ __global__ void k_dequant_i64(const int64_t* __restrict__ acc, const float* __re
 }  // namespace
 
 namespace sb {
+
+const sb_symbuf* find_symbuf(sb_handle h, const void* p, size_t bytes) {
+  const auto* q = static_cast<const uint8_t*>(p);
+  for (const sb_symbuf& s : h->sym) {
+    const auto* b = static_cast<const uint8_t*>(s.local);
+    if (q >= b && q + bytes <= b + s.bytes) return &s;
+  }
+  return nullptr;
+}
+
+void dp_owned_rows(int64_t rows, int rank, int world, int64_t* r0, int64_t* r1) {
+  const int64_t nb = (rows + 31) / 32;
+  auto first_block = [&](int64_t r) { return (r * nb + world - 1) / world; };  // ceil(r nb / world)
+  *r0 = std::min<int64_t>(rows, 32 * first_block(rank));
+  *r1 = std::min<int64_t>(rows, 32 * first_block(rank + 1));
+}
+
+void dp_free_symmetric(sb_handle h) {
+  for (sb_symbuf& s : h->sym) {
+    for (int r = 0; r < s.world; ++r)
+      if (s.opened && r != s.rank && s.peer[r]) cudaIpcCloseMemHandle(s.peer[r]);
+    cudaFree(s.local);
+  }
+  h->sym.clear();
+}
 
 bool dp_active(sb_handle h) {
   static int force = -1;
@@ -194,6 +223,7 @@ sb_status sb_dp_init(sb_handle h, const uint8_t* id, int rank, int world) {
   SB_CUDA_CHECK(op, cudaStreamCreateWithFlags(&h->dp_stream, cudaStreamNonBlocking));
   SB_CUDA_CHECK(op, cudaEventCreateWithFlags(&h->dp_ready, cudaEventDisableTiming));
   SB_CUDA_CHECK(op, cudaEventCreateWithFlags(&h->dp_done, cudaEventDisableTiming));
+  if (!h->dp_token) SB_CUDA_CHECK(op, cudaMalloc(&h->dp_token, sizeof(float)));
   if (getenv("SB_DEBUG") || getenv("SB_DP_LOG")) {
     int v = 0;
     if (nccl().getVersion) nccl().getVersion(&v);
@@ -269,6 +299,165 @@ sb_status sb_dp_destroy(sb_handle h) {
   cudaEventDestroy(h->dp_ready);
   cudaEventDestroy(h->dp_done);
   h->dp_stream = nullptr;
+  if (h->dp_token) cudaFree(h->dp_token);
+  h->dp_token = nullptr;
+  return SB_OK;
+}
+
+// ------------------------------------------------ fused dW reduce-scatter ---
+// Symmetric buffers: cudaMalloc'ed on every rank, exported with cudaIpcGetMemHandle, and every
+// peer's copy opened in this process, so the dW kernel's epilogue can TMA reduce-add into the
+// owner's copy over NVLink (P2P). The handles travel out of band (sb_dp_symmetric_open) or over
+// the handle's NCCL communicator (sb_dp_symmetric_exchange).
+sb_status sb_dp_symmetric_alloc(sb_handle h, size_t bytes, void** ptr, uint8_t* ipc_handle) {
+  const char* op = "sb_dp_symmetric_alloc";
+  if (!h || !ptr || !ipc_handle || bytes == 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  cudaSetDevice(h->device);
+  sb_symbuf s;
+  s.bytes = (bytes + 255) & ~size_t(255);
+  SB_CUDA_CHECK(op, cudaMalloc(&s.local, s.bytes));
+  cudaIpcMemHandle_t ih;
+  const cudaError_t e = cudaIpcGetMemHandle(&ih, s.local);
+  if (e != cudaSuccess) {
+    cudaFree(s.local);
+    return sb::cuda_fail(op, e);
+  }
+  std::memcpy(ipc_handle, &ih, sizeof(ih));
+  h->sym.push_back(s);
+  *ptr = s.local;
+  return SB_OK;
+}
+
+sb_status sb_dp_symmetric_open(sb_handle h, void* ptr, int rank, int world, const uint8_t* ipc_handles) {
+  const char* op = "sb_dp_symmetric_open";
+  if (!h || !ptr || !ipc_handles || world < 1 || world > 8 || rank < 0 || rank >= world)
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument (1 <= world <= 8)");
+  sb_symbuf* s = const_cast<sb_symbuf*>(sb::find_symbuf(h, ptr, 1));
+  if (!s || s->local != ptr) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "not a symmetric buffer of this handle");
+  if (s->opened) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "already opened");
+  cudaSetDevice(h->device);
+  s->rank = rank;
+  s->world = world;
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) {
+      s->peer[r] = s->local;
+      continue;
+    }
+    cudaIpcMemHandle_t ih;
+    std::memcpy(&ih, ipc_handles + 64 * r, sizeof(ih));
+    const cudaError_t e = cudaIpcOpenMemHandle(&s->peer[r], ih, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      for (int q = 0; q < r; ++q)
+        if (q != rank && s->peer[q]) cudaIpcCloseMemHandle(s->peer[q]);
+      std::memset(s->peer, 0, sizeof(s->peer));
+      return sb::cuda_fail(op, e);
+    }
+  }
+  s->opened = true;
+  return SB_OK;
+}
+
+sb_status sb_dp_symmetric_exchange(sb_handle h, void* ptr, const uint8_t* ipc_handle) {
+  const char* op = "sb_dp_symmetric_exchange";
+  SB_TRY_S(need_comm(h, op));
+  if (!ptr || !ipc_handle) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  if (h->dp_world > 8) return sb::fail(SB_ERR_UNSUPPORTED, op, "at most 8 ranks");
+  uint8_t* d = nullptr;
+  SB_CUDA_CHECK(op, cudaMalloc(&d, 64 * static_cast<size_t>(h->dp_world)));
+  std::vector<uint8_t> all(64 * static_cast<size_t>(h->dp_world));
+  cudaError_t e = cudaMemcpyAsync(d + 64 * h->dp_rank, ipc_handle, 64, cudaMemcpyHostToDevice, h->stream);
+  int r = ncclSuccess;
+  if (e == cudaSuccess)
+    r = nccl().allGather(d + 64 * h->dp_rank, d, 64, ncclUint8, static_cast<ncclComm_t>(h->dp_comm), h->stream);
+  if (e == cudaSuccess && r == ncclSuccess) e = cudaMemcpyAsync(all.data(), d, all.size(), cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess && r == ncclSuccess) e = cudaStreamSynchronize(h->stream);
+  cudaFree(d);
+  if (r != ncclSuccess) return nccl_fail(op, r);
+  if (e != cudaSuccess) return sb::cuda_fail(op, e);
+  return sb_dp_symmetric_open(h, ptr, h->dp_rank, h->dp_world, all.data());
+}
+
+sb_status sb_dp_symmetric_free(sb_handle h, void* ptr) {
+  const char* op = "sb_dp_symmetric_free";
+  if (!h) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "null handle");
+  for (size_t i = 0; i < h->sym.size(); ++i) {
+    sb_symbuf& s = h->sym[i];
+    if (s.local != ptr) continue;
+    cudaSetDevice(h->device);
+    cudaDeviceSynchronize();
+    for (int r = 0; r < s.world; ++r)
+      if (s.opened && r != s.rank && s.peer[r]) cudaIpcCloseMemHandle(s.peer[r]);
+    cudaFree(s.local);
+    h->sym.erase(h->sym.begin() + static_cast<std::ptrdiff_t>(i));
+    return SB_OK;
+  }
+  return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "not a symmetric buffer of this handle");
+}
+
+sb_status sb_dp_owned_rows(int64_t rows, int rank, int world, int64_t* r0, int64_t* r1) {
+  if (rows < 0 || world < 1 || rank < 0 || rank >= world || !r0 || !r1)
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, "sb_dp_owned_rows", "bad argument");
+  sb::dp_owned_rows(rows, rank, world, r0, r1);
+  return SB_OK;
+}
+
+sb_status sb_wgrad_reduce_scatter(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m,
+                                  int64_t n, float* dw, int8_t* g_q, int64_t ldq, float* g_state) {
+  const char* op = "wgrad_reduce_scatter";
+  if (!h || !g || !x || !dw || b <= 0 || m <= 0 || n <= 0 || (g_q && (!g_state || ldq < m)))
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  const sb_symbuf* s = sb::find_symbuf(h, dw, static_cast<size_t>(m * n) * sizeof(float));
+  if (!s) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "dw is not inside a symmetric buffer (sb_dp_symmetric_alloc)");
+  cudaSetDevice(h->device);
+  const sb::RowQuant rq{g_q, ldq, g_state};
+  return sb::wgrad_reduce_scatter(h, g, x, dt, b, m, n, dw, *s, g_q ? &rq : nullptr);
+}
+
+// Stream-ordered barrier: a one-element all-reduce on the handle's stream. When it completes on
+// a rank, every rank has reached it (and finished the work it enqueued before it).
+sb_status sb_dp_barrier(sb_handle h) {
+  const char* op = "sb_dp_barrier";
+  SB_TRY_S(need_comm(h, op));
+  SB_NCCL(op, nccl().allReduce(h->dp_token, h->dp_token, 1, ncclFloat32, ncclSum, static_cast<ncclComm_t>(h->dp_comm),
+                               h->stream));
+  return SB_OK;
+}
+
+// After the reduce-scatter each rank's copy holds the complete sum in the rows it owns; every
+// owner broadcasts its rows into the same rows of the other ranks' copies (one NCCL group).
+sb_status sb_dp_allgather_rows(sb_handle h, float* dw, int64_t m, int64_t n) {
+  const char* op = "sb_dp_allgather_rows";
+  SB_TRY_S(need_comm(h, op));
+  if (!dw || m <= 0 || n <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  SB_NCCL(op, nccl().groupStart());
+  for (int r = 0; r < h->dp_world; ++r) {
+    int64_t r0 = 0, r1 = 0;
+    sb::dp_owned_rows(m, r, h->dp_world, &r0, &r1);
+    if (r1 > r0)
+      SB_NCCL(op, nccl().broadcast(dw + r0 * n, dw + r0 * n, static_cast<size_t>((r1 - r0) * n), ncclFloat32, r,
+                                   static_cast<ncclComm_t>(h->dp_comm), h->stream));
+  }
+  SB_NCCL(op, nccl().groupEnd());
+  return SB_OK;
+}
+
+// The whole fused exchange for one weight gradient, stream-ordered on the handle's stream:
+// zero this rank's copy, barrier (every copy zeroed before any rank adds), the dW GEMM with its
+// reduce-scatter epilogue, barrier (every rank's adds landed), all-gather of the owned rows.
+// Afterwards dw holds sum_r G_r^T X_r on every rank. Without a communicator (one rank) it is
+// the GEMM into the zeroed local buffer.
+sb_status sb_dp_wgrad_allreduce_fused(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m,
+                                      int64_t n, float* dw, int8_t* g_q, int64_t ldq, float* g_state) {
+  const char* op = "wgrad_allreduce_fused";
+  if (!h || !dw || m <= 0 || n <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  const bool multi = h->dp_comm != nullptr && h->dp_world > 1;
+  SB_CUDA_CHECK(op, cudaMemsetAsync(dw, 0, static_cast<size_t>(m * n) * sizeof(float), h->stream));
+  if (multi) SB_TRY_S(sb_dp_barrier(h));
+  SB_TRY_S(sb_wgrad_reduce_scatter(h, g, x, dt, b, m, n, dw, g_q, ldq, g_state));
+  if (multi) {
+    SB_TRY_S(sb_dp_barrier(h));
+    SB_TRY_S(sb_dp_allgather_rows(h, dw, m, n));
+  }
   return SB_OK;
 }
 

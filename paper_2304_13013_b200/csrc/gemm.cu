@@ -403,7 +403,7 @@ cudaError_t launch_tc(sb_handle h, const Operand& A, const Operand& B, const CUt
 // wide), X: B operand (n wide); TRANS runs C = X^T G and stores C^T.
 // rq (optional): also quantize G row-wise inside the same launch (tc_dw_wide.cuh QV).
 cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, const CUtensorMap& td, int64_t m, int64_t n,
-                           int64_t T, const sb::RowQuant* rq) {
+                           int64_t T, const sb::RowQuant* rq, const sbdw::DMaps<8>* rs = nullptr) {
   static int env = -1;
   if (env < 0) env = getenv("SB_DW_WIDE") ? atoi(getenv("SB_DW_WIDE")) : 1;
   if (!env || h->gemm_path == SB_GEMM_1CTA || h->num_sms < 2) return cudaErrorNotSupported;
@@ -417,6 +417,11 @@ cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, cons
   std::call_once(once_d[dv], [&] {
     for (auto kern : {sbdw::k_dw_wide<false, 0>, sbdw::k_dw_wide<true, 0>, sbdw::k_dw_wide<false, sbdw::kQV>,
                       sbdw::k_dw_wide<true, sbdw::kQV>}) {
+      const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sbdw::SMEM_BYTES);
+      if (e != cudaSuccess) attr_err = e;
+    }
+    for (auto kern : {sbdw::k_dw_wide<false, 0, 8>, sbdw::k_dw_wide<true, 0, 8>, sbdw::k_dw_wide<false, sbdw::kQV, 8>,
+                      sbdw::k_dw_wide<true, sbdw::kQV, 8>}) {
       const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sbdw::SMEM_BYTES);
       if (e != cudaSuccess) attr_err = e;
     }
@@ -484,8 +489,22 @@ cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, cons
     p.q_idle_kb = static_cast<int>(std::min<double>(static_cast<double>(qkb), frac * static_cast<double>(qkb)));
   }
   h->launches++;
+  if (rs) {
+    auto go8 = [&](auto kern) {
+      sb::launch_pdl(kern, dim3(grid), dim3(sbtc::NUM_THREADS), sbdw::SMEM_BYTES, h->stream, ta, tb, *rs, p);
+    };
+    if (qv)
+      trans ? go8(sbdw::k_dw_wide<true, sbdw::kQV, 8>) : go8(sbdw::k_dw_wide<false, sbdw::kQV, 8>);
+    else
+      trans ? go8(sbdw::k_dw_wide<true, 0, 8>) : go8(sbdw::k_dw_wide<false, 0, 8>);
+    return cudaGetLastError();
+  }
+  sbdw::DMaps<1> d1{};
+  d1.m[0] = td;
+  d1.world = 1;
+  d1.nblocks = 1;
   auto go = [&](auto kern) {
-    sb::launch_pdl(kern, dim3(grid), dim3(sbtc::NUM_THREADS), sbdw::SMEM_BYTES, h->stream, ta, tb, td, p);
+    sb::launch_pdl(kern, dim3(grid), dim3(sbtc::NUM_THREADS), sbdw::SMEM_BYTES, h->stream, ta, tb, d1, p);
   };
   if (qv)
     trans ? go(sbdw::k_dw_wide<true, sbdw::kQV>) : go(sbdw::k_dw_wide<false, sbdw::kQV>);
@@ -808,6 +827,35 @@ sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t 
     k_matmul_seq<float><<<grid, 256, 0, h->stream>>>(static_cast<const float*>(g), 1, m, static_cast<const float*>(x), 1,
                                                      n, m, n, b, dw, accumulate);
   SB_LAUNCH_CHECK(op);
+  return SB_OK;
+}
+
+sb_status wgrad_reduce_scatter(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m, int64_t n,
+                               float* dw, const sb_symbuf& sym, const RowQuant* rq) {
+  const char* op = "wgrad_reduce_scatter";
+  if (sym.world < 1 || sym.world > 8 || !sym.opened) return fail(SB_ERR_INVALID_ARGUMENT, op, "symmetric buffer not opened");
+  const bool ok = dt == SB_BF16 && m % 8 == 0 && n % 8 == 0 && aligned(g, 16) && aligned(x, 16) && aligned(dw, 16) &&
+                  b > 0 && b < (1LL << 31) && get_encode() != nullptr &&
+                  (!rq || (aligned(rq->q, 16) && rq->ldq % 16 == 0));
+  if (!ok) return fail(SB_ERR_UNSUPPORTED, op, "bf16, m % 8 == 0, n % 8 == 0, 16-byte aligned operands");
+  const size_t off = static_cast<size_t>(reinterpret_cast<const uint8_t*>(dw) - static_cast<const uint8_t*>(sym.local));
+  sbdw::DMaps<8> dm{};
+  dm.world = sym.world;
+  dm.nblocks = static_cast<int>((m + 31) / 32);
+  CUtensorMap td;
+  if (!out_tmap(&td, SB_F32, dw, m, n)) return fail(SB_ERR_UNSUPPORTED, op, "tensor map encode failed");
+  for (int r = 0; r < sym.world; ++r) {
+    float* pr = reinterpret_cast<float*>(static_cast<uint8_t*>(sym.peer[r]) + off);
+    if (!out_tmap(&dm.m[r], SB_F32, pr, m, n)) return fail(SB_ERR_UNSUPPORTED, op, "peer tensor map encode failed");
+  }
+  const Operand A{g, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, static_cast<uint64_t>(m), static_cast<uint64_t>(b),
+                  static_cast<uint64_t>(m * 2), true, 64};
+  const Operand B{x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, static_cast<uint64_t>(n), static_cast<uint64_t>(b),
+                  static_cast<uint64_t>(n * 2), true, 64};
+  const cudaError_t e = launch_dw_wide(h, A, B, td, m, n, b, rq, &dm);
+  if (e == cudaErrorNotSupported)
+    return fail(SB_ERR_UNSUPPORTED, op, "shape not served by the one-wave dW kernel (use sb_wgrad + all-reduce)");
+  if (e != cudaSuccess) return cuda_fail(op, e);
   return SB_OK;
 }
 

@@ -5,10 +5,22 @@
 #include <stdint.h>
 
 #include <map>
+#include <vector>
 #include <string>
 #include <utility>
 
 #include "../../include/switchback_b200.h"
+
+// A symmetric buffer for the fused dW reduce-scatter: the same-size allocation on every rank,
+// each rank's mapped into this process (CUDA IPC), so a kernel can reduce-add into a peer's
+// copy over NVLink. peer[rank] == local.
+struct sb_symbuf {
+  void* local = nullptr;
+  size_t bytes = 0;
+  int rank = 0, world = 1;
+  void* peer[8] = {};
+  bool opened = false;  // peer[] filled by sb_dp_symmetric_open
+};
 
 struct sb_handle_s {
   int device = 0;
@@ -17,8 +29,10 @@ struct sb_handle_s {
   uint32_t* d_err = nullptr;       // device error latch (bit 0: non-finite input seen)
   // small per-stream scratch (tensor absmax words etc.) for the standalone ops that have no
   // caller workspace: one buffer per CUDA stream the handle has been bound to, so ops enqueued
-  // on two streams never share words; grown only outside stream capture
+  // eagerly on two streams never share words; allocated only outside stream capture
   std::map<cudaStream_t, std::pair<unsigned int*, size_t>> scratch;
+  unsigned int* capture_scratch = nullptr;  // 1 MB from sb_create: streams first seen while capturing
+  size_t capture_scratch_bytes = 0;
   uint64_t launches = 0;
   int gemm_path = 0;  // sb_gemm_path
   // host-buffer pipeline (sb_switchback_fwd_bwd_host): copy streams + events, created once
@@ -40,6 +54,8 @@ struct sb_handle_s {
   cudaStream_t dp_stream = nullptr;
   cudaEvent_t dp_ready = nullptr, dp_done = nullptr;
   bool dp_pending = false;
+  float* dp_token = nullptr;  // one device float: the payload of sb_dp_barrier's all-reduce
+  std::vector<sb_symbuf> sym;  // symmetric buffers (sb_dp_symmetric_alloc)
 };
 
 namespace sb {
@@ -175,6 +191,12 @@ struct RowQuant {
 // otherwise as a separate launch before the GEMM.
 sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m, int64_t n, float* dw,
                 int exact, int accumulate, const RowQuant* rq = nullptr);
+// dW = G^T X with the epilogue reduce-adding every 32-row block of dW into its owner rank's copy
+// of the symmetric buffer holding dw (fused GEMM + reduce-scatter); one-wave bf16 kernel only
+// (SB_ERR_UNSUPPORTED otherwise). Every rank's dw must be zeroed (and the zeroing ordered
+// before this call on every rank) first.
+sb_status wgrad_reduce_scatter(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m, int64_t n,
+                               float* dw, const sb_symbuf& sym, const RowQuant* rq);
 sb_status matmul_f32_seq(sb_handle h, const float* a, int64_t a_rs, int64_t a_ks, const float* bt, int64_t b_rs,
                          int64_t b_ks, int64_t r, int64_t c, int64_t k, float* y, int accumulate);
 sb_status gemm_bf16_tc(sb_handle h, const void* a, bool a_mn, const void* b, bool b_mn, int64_t M, int64_t N, int64_t K,
@@ -184,6 +206,13 @@ sb_status gemm_fp8(sb_handle h, const uint8_t* qa, int fa, const float* sa, int 
                    const float* sb, int axb, int64_t M, int64_t N, int64_t K, void* out, sb_dtype out_dt);
 
 // dp.cu
+// The symmetric buffer holding [p, p + bytes) (nullptr if none).
+const sb_symbuf* find_symbuf(sb_handle h, const void* p, size_t bytes);
+// Rows [r0, r1) of a rows-row dW owned by `rank` in the fused reduce-scatter: 32-row blocks,
+// block rb owned by rank (rb * world) / nblocks (contiguous, sizes differ by at most one block).
+void dp_owned_rows(int64_t rows, int rank, int world, int64_t* r0, int64_t* r1);
+// Close every peer mapping and free every symmetric buffer of the handle (sb_destroy).
+void dp_free_symmetric(sb_handle h);
 // True when the handle has a communicator of more than one rank (or SB_DP_FORCE=1 with one rank,
 // which runs the multi-rank code paths against the identity collectives).
 bool dp_active(sb_handle h);

@@ -24,6 +24,14 @@
 // traffic overlaps tensor-core work inside one launch instead of competing for SMs from a
 // second stream. QV = 16-byte vectors per lane in flight per step of the two-pass row quantizer
 // (quant_core.cuh). The payload and states are those of sb_quantize_rowwise(G), bit for bit.
+//
+// Fused reduce-scatter (NM > 1, SURVEY.md §8e stage 2). Under token data parallelism dW is the
+// sum over ranks of each rank's G_r^T X_r. With NM = 8 the kernel receives one D tensor map per
+// rank, each over that rank's copy of a symmetric (CUDA-IPC peer-mapped) dW buffer, and every
+// 32 x 32 output box leaves the epilogue as a TMA reduce-add (cp.reduce.async.bulk.tensor .add
+// .f32) into the copy of the rank that owns its 32-row block of dW: the reduce-scatter's
+// NVLink traffic streams out tile by tile while the tensor cores work, instead of a collective
+// after the GEMM. Owned rows are then all-gathered (sb_dp_allgather_rows).
 #pragma once
 #include "quant_core.cuh"
 #include "tc_gemm2.cuh"
@@ -96,6 +104,22 @@ __device__ __forceinline__ void quantize_g_rows(const WParams& p, int qwarp, int
   }
 }
 
+// The output tensor maps: NM = 1, the local dW (plain TMA store); NM = 8, one per rank's copy
+// of the symmetric dW (TMA reduce-add into the owner of each 32-row block).
+template <int NM>
+struct DMaps {
+  CUtensorMap m[NM];
+  int world;    // ranks (<= NM)
+  int nblocks;  // 32-row blocks of dW (ownership: block rb -> rank rb * world / nblocks)
+};
+
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* m, const void* src, int32_t c0, int32_t c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(sbptx::smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+
 __device__ __forceinline__ void mma_f16_2(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
@@ -107,10 +131,10 @@ __device__ __forceinline__ void mma_f16_2(uint32_t d, uint64_t a, uint64_t b, ui
 // written to D[m][n] through a transposed staging tile: lane t (row t) stores its 32 values
 // down column t of a [32 m][32 n] fp32 tile (SW128 layout of the D tensor map; for a fixed
 // register index the 32 lanes fill one 128-byte row, so the stores are bank-conflict free).
-template <bool TRANS, int QV>
+template <bool TRANS, int QV, int NM = 1>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     k_dw_wide(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const __grid_constant__ CUtensorMap tmD, const WParams p) {
+              const __grid_constant__ DMaps<NM> dm, const WParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
@@ -133,7 +157,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     sbptx::tma_prefetch_desc(&tmA);
     sbptx::tma_prefetch_desc(&tmB);
-    sbptx::tma_prefetch_desc(&tmD);
+    for (int r = 0; r < (NM > 1 ? dm.world : 1); ++r) sbptx::tma_prefetch_desc(&dm.m[r]);
     for (int s = 0; s < NSTAGES; ++s) {
       sbptx::mbar_init(&full_bar[s], 1);
       sbptx::mbar_init(&empty_bar[s], 1);
@@ -259,15 +283,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         sbptx::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          if (TRANS)
-            sbptx::tma_store_2d(&tmD, buf, rm0, col0);  // D[m = col][n = row]
-          else
-            sbptx::tma_store_2d(&tmD, buf, col0, rm0);
+          // D[m = col][n = row] (TRANS) or D[m = row][n = col]; c0 = n, c1 = m
+          const int dn = TRANS ? rm0 : col0, dmr = TRANS ? col0 : rm0;
+          if (NM > 1) {
+            const int owner = static_cast<int>((static_cast<int64_t>(dmr >> 5) * dm.world) / dm.nblocks);
+            tma_reduce_add_2d(&dm.m[owner], buf, dn, dmr);
+          } else {
+            sbptx::tma_store_2d(&dm.m[0], buf, dn, dmr);
+          }
           sbptx::tma_store_commit();
         }
       }
     }
-    if (lane == 0) sbptx::tma_store_wait_all<0>();
+    if (lane == 0) {
+      sbptx::tma_store_wait_all<0>();
+      // the reduce-adds landed in peers' memory: make them visible system-wide before the
+      // kernel (and the caller's barrier after it) completes
+      if (NM > 1) __threadfence_system();
+    }
   }
   __syncthreads();
   cluster_sync();

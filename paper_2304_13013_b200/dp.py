@@ -140,3 +140,87 @@ def max_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def owned_rows(rows: int, rank: int, world: int) -> tuple[int, int]:
+    """Rows [r0, r1) of a `rows`-row dW owned by `rank` in the fused reduce-scatter (mirror of
+    sb_dp_owned_rows, csrc/dp.cu): 32-row blocks, block rb -> rank rb * world // nblocks."""
+    nb = (rows + 31) // 32
+
+    def first(r):
+        return (r * nb + world - 1) // world
+
+    return min(rows, 32 * first(rank)), min(rows, 32 * first(rank + 1))
+
+
+class _CudaView:
+    """__cuda_array_interface__ over a raw device pointer (zero-copy torch view)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class SymmetricBuffer:
+    """A device buffer allocated on every rank and mapped into every rank's process
+    (sb_dp_symmetric_alloc + CUDA IPC), the target of the fused dW GEMM + reduce-scatter
+    (sb_wgrad_reduce_scatter). The 64-byte IPC handles travel over the library's NCCL
+    communicator (`comm`) or, without one, over torch.distributed (`all_gather_object`: gloo in
+    the one-GPU multi-process tests)."""
+
+    def __init__(self, handle, nbytes: int, rank: int = 0, world: int = 1, comm: NcclComm | None = None,
+                 group=None):
+        import ctypes as C
+
+        from . import _capi as A
+
+        self.h, self.rank, self.world = handle, rank, world
+        ptr, ih = C.c_void_p(), (C.c_uint8 * 64)()
+        A.check(handle.lib.sb_dp_symmetric_alloc(handle.h, nbytes, C.byref(ptr), ih))
+        self.ptr, self.nbytes = ptr.value, nbytes
+        if comm is not None:
+            A.check(handle.lib.sb_dp_symmetric_exchange(handle.h, ptr, ih))
+        else:
+            mine = bytes(ih)
+            if world > 1:
+                allh: list = [None] * world
+                dist.all_gather_object(allh, mine, group=group)
+            else:
+                allh = [mine]
+            blob = (C.c_uint8 * (64 * world)).from_buffer_copy(b"".join(allh))
+            A.check(handle.lib.sb_dp_symmetric_open(handle.h, ptr, rank, world, blob))
+
+    def view(self, shape, offset_bytes: int = 0) -> torch.Tensor:
+        """fp32 torch tensor over [offset, offset + prod(shape) * 4) of this rank's copy."""
+        n = 1
+        for s in shape:
+            n *= s
+        if offset_bytes < 0 or offset_bytes + 4 * n > self.nbytes or offset_bytes % 16:
+            raise ValueError("view outside the symmetric buffer (or not 16-byte aligned)")
+        return torch.as_tensor(_CudaView(self.ptr + offset_bytes, shape, "<f4"), device="cuda")
+
+    def close(self) -> None:
+        import ctypes as C
+
+        from . import _capi as A
+
+        if self.ptr:
+            A.check(self.h.lib.sb_dp_symmetric_free(self.h.h, C.c_void_p(self.ptr)))
+            self.ptr = 0
+
+
+def wgrad_reduce_scatter(handle, g: torch.Tensor, x: torch.Tensor, dw: torch.Tensor, g_q=None, g_state=None) -> None:
+    """dW GEMM whose epilogue reduce-adds each 32-row block into its owner rank's copy of the
+    symmetric buffer behind `dw` (sb_wgrad_reduce_scatter). Every rank's dw must be zeroed and
+    that ordered before this call on every rank."""
+    import ctypes as C
+
+    from . import _capi as A
+
+    b, m = g.shape
+    n = x.shape[1]
+    handle.bind_stream(torch.cuda.current_stream(g.device).cuda_stream)
+    A.check(handle.lib.sb_wgrad_reduce_scatter(
+        handle.h, C.c_void_p(g.data_ptr()), C.c_void_p(x.data_ptr()), A.SB_BF16, b, m, n, C.c_void_p(dw.data_ptr()),
+        C.c_void_p(g_q.data_ptr() if g_q is not None else None), m,
+        C.c_void_p(g_state.data_ptr() if g_state is not None else None)))

@@ -156,3 +156,28 @@ def test_lpt_partition_balances_c5():
         assert sorted(i for p in parts for i in p) == list(range(len(sizes)))
         loads = [sum(sizes[i] for i in p) for p in parts]
         assert max(loads) / (sum(loads) / world) <= 1.02
+
+
+def test_owned_rows_partition_matches_library():
+    """The fused reduce-scatter's row ownership (dp.owned_rows == sb_dp_owned_rows): contiguous,
+    32-row aligned, covering every row once, balanced to one 32-row block."""
+    import ctypes as C
+
+    from paper_2304_13013_b200 import _capi as A
+    from paper_2304_13013_b200 import dp
+
+    lib = A.load(build_if_missing=False)
+    for rows in (1, 31, 32, 100, 1280, 3840, 5120, 5121):
+        for world in (1, 2, 3, 4, 8):
+            prev = 0
+            sizes = []
+            for r in range(world):
+                r0, r1 = dp.owned_rows(rows, r, world)
+                a, b = C.c_int64(), C.c_int64()
+                assert lib.sb_dp_owned_rows(rows, r, world, C.byref(a), C.byref(b)) == 0
+                assert (a.value, b.value) == (r0, r1)
+                assert r0 == prev and (r0 % 32 == 0 or r0 == rows)
+                prev = r1
+                sizes.append(-(-(r1 - r0) // 32))
+            assert prev == rows
+            assert max(sizes) - min(sizes) <= 1

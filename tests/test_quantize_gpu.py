@@ -213,3 +213,23 @@ def test_golden_fixture_quantize(golden):
         assert np.array_equal(host(L.quantize_tensorwise_transpose(dev(x)).payload), d[prefix + "q_tensor_t"])
         p = L.quantize_fp8(dev(x), L.E4M3, L.ROW)
         assert np.array_equal(fp8_decode(host(p.payload), 0), d[prefix + "fp8_e4m3_row"])
+
+
+def test_standalone_quantizers_capture_in_cuda_graph():
+    """The ops that use the handle's scratch words (tensor-wise, column-wise) can be captured in a
+    CUDA graph on a stream the handle has never run on (no allocation while capturing), and the
+    replay equals the eager result."""
+    torch.manual_seed(5)
+    x = torch.randn(1024, 768, device="cuda").to(torch.bfloat16)
+    t_ref = L.quantize_tensorwise(x)
+    c_ref = L.quantize_columnwise(x)
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            t = L.quantize_tensorwise(x, check=False)
+            c = L.quantize_columnwise(x, check=False)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(t.payload, t_ref.payload) and torch.equal(t.state, t_ref.state)
+    assert torch.equal(c.payload, c_ref.payload) and torch.equal(c.state, c_ref.state)
