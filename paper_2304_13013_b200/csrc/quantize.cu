@@ -1340,22 +1340,49 @@ __global__ void k_quantize_fp8(const T* __restrict__ x, int64_t rows, int64_t co
 // tools/fp8_div_check.cu, ~1.07e9 pairs); rows outside it and fp32 input use __fdiv_rn.
 // bf16 fast path on magnitudes: the quotient of |x| (abs is a free operand modifier), the
 // magnitude code, and the 8 sign bits OR-ed in from the raw bf16 words at the end.
+// fp8_code_unit_abs for two magnitudes at once, the float steps on the packed fp32x2 pipe
+// (FFMA2 / FADD2: per lane the same IEEE operations, so the codes are identical):
+//   normal:    ((|a| + half - 1) >> drop) - (127 - BIAS) << MB, folded into one add;
+//   subnormal: round-half-down(n), n = |a| 2^(BIAS+MB-1) < 2^MB, as ceil(n - 1/2): n - 1/2 is
+//              exact (one FFMA), ceil by the magic-number add rounded toward +inf.
+template <int MB, int BIAS>
+__device__ __forceinline__ void fp8_code2_abs(float2 a, uint32_t& c0, uint32_t& c1) {
+  constexpr uint32_t drop = 23 - MB;
+  constexpr uint32_t K = (1u << (drop - 1)) - 1u - (static_cast<uint32_t>(127 - BIAS) << 23);  // mod 2^32
+  constexpr uint32_t thr = static_cast<uint32_t>(128 - BIAS) << 23;
+  const float P = __uint_as_float(static_cast<uint32_t>(127 + BIAS + MB - 1) << 23);
+  const float2 t = __ffma2_rn(a, make_float2(P, P), make_float2(-0.5f, -0.5f));
+  const float2 m = __fadd2_ru(t, make_float2(12582912.0f, 12582912.0f));
+  const uint32_t ab0 = __float_as_uint(a.x), ab1 = __float_as_uint(a.y);
+  c0 = ab0 < thr ? __float_as_uint(m.x) - 0x4B400000u : (ab0 + K) >> drop;
+  c1 = ab1 < thr ? __float_as_uint(m.y) - 0x4B400000u : (ab1 + K) >> drop;
+}
+
+// bf16 fast path on magnitudes, two elements per packed fp32x2 operation: |x| is the bf16 word
+// with its sign bits cleared, the quotient |x| / s by q0 = |x| r and one Markstein correction,
+// the magnitude codes packed with byte permutes and the 8 sign bits OR-ed in from the raw words.
 template <int FMT>
 __device__ __forceinline__ uint2 fp8_vec_bf16_fast(const uint4& v, float s, float r) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  const float2 r2 = make_float2(r, r), ns2 = make_float2(-s, -s);
   uint32_t c[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const float ax = fabsf(__uint_as_float((i & 1) ? (w[i >> 1] & 0xffff0000u) : (w[i >> 1] << 16)));
-    const float q0 = __fmul_rn(ax, r);
-    const float a = __fmaf_rn(__fmaf_rn(-s, q0, ax), r, q0);
-    c[i] = FMT == 0 ? fp8_code_unit_abs<3, 7>(a) : fp8_code_unit_abs<2, 15>(a);
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t wa = w[i] & 0x7fff7fffu;
+    const float2 ax = make_float2(__uint_as_float(wa << 16), __uint_as_float(wa & 0xffff0000u));
+    const float2 q0 = __fmul2_rn(ax, r2);
+    const float2 a = __ffma2_rn(__ffma2_rn(ns2, q0, ax), r2, q0);
+    if (FMT == 0)
+      fp8_code2_abs<3, 7>(a, c[2 * i], c[2 * i + 1]);
+    else
+      fp8_code2_abs<2, 15>(a, c[2 * i], c[2 * i + 1]);
   }
-  // sign of element 2k is bit 15 of w[k], of element 2k+1 bit 31
-  const uint32_t s0 = ((w[0] >> 8) & 0x80u) | ((w[0] >> 16) & 0x8000u) | ((w[1] << 8) & 0x800000u) | (w[1] & 0x80000000u);
-  const uint32_t s1 = ((w[2] >> 8) & 0x80u) | ((w[2] >> 16) & 0x8000u) | ((w[3] << 8) & 0x800000u) | (w[3] & 0x80000000u);
-  return make_uint2((c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24)) | s0,
-                    (c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24)) | s1);
+  // sign of element 2k is bit 15 of w[k] (bit 7 of byte 1), of element 2k+1 bit 31 (byte 3)
+  const uint32_t s0 = __byte_perm(w[0], w[1], 0x7531) & 0x80808080u;
+  const uint32_t s1 = __byte_perm(w[2], w[3], 0x7531) & 0x80808080u;
+  const uint32_t p0 = __byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410);
+  const uint32_t p1 = __byte_perm(__byte_perm(c[4], c[5], 0x0040), __byte_perm(c[6], c[7], 0x0040), 0x5410);
+  return make_uint2(p0 | s0, p1 | s1);
 }
 
 template <bool FAST, int FMT, typename T>
