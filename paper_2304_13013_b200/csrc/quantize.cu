@@ -432,34 +432,36 @@ __device__ __forceinline__ void ln_row(uint4 (&v)[VPL], int64_t row, int nvec, i
   using T = __nv_bfloat16;
   using Out = typename VecQ<T>::Out;
   const int64_t off = row * static_cast<int64_t>(nvec);
-    float sum = 0.0f;
+  // the element math runs on the packed fp32x2 pipe (FADD2 / FFMA2 / FMUL2): two columns per
+  // instruction, half the issue slots of the scalar form
+  float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
-    for (int j = 0; j < VPL; ++j) {
-      const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&v[j]);
+  for (int j = 0; j < VPL; ++j) {
+    const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&v[j]);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 f = __bfloat1622float2(p2[k]);
-        sum += f.x + f.y;
-      }
+    for (int k = 0; k < 4; ++k) acc = __fadd2_rn(acc, __bfloat1622float2(p2[k]));
+  }
+  float sum = acc.x + acc.y;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float mean = sum * inv_n;
+  const float2 nmean = make_float2(-mean, -mean);
+  float2 acc2 = make_float2(0.0f, 0.0f);
+#pragma unroll
+  for (int j = 0; j < VPL; ++j) {
+    if (j * 32 + lane >= nvec) continue;
+    const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&v[j]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 d = __fadd2_rn(__bfloat1622float2(p2[k]), nmean);
+      acc2 = __ffma2_rn(d, d, acc2);
     }
+  }
+  float sq = acc2.x + acc2.y;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    const float mean = sum * inv_n;
-    float sq = 0.0f;
-#pragma unroll
-    for (int j = 0; j < VPL; ++j) {
-      if (j * 32 + lane >= nvec) continue;
-      const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&v[j]);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 f = __bfloat1622float2(p2[k]);
-        const float a = f.x - mean, b = f.y - mean;
-        sq += a * a + b * b;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
     const float rstd = rsqrtf(sq * inv_n + eps);
+    const float2 rs2 = make_float2(rstd, rstd);
     uint4* hr = reinterpret_cast<uint4*>(h) + off;
     uint32_t amax = 0;
 #pragma unroll
@@ -468,14 +470,15 @@ __device__ __forceinline__ void ln_row(uint4 (&v)[VPL], int64_t row, int nvec, i
       if (i >= nvec) continue;
       const float4 g0 = gb_s[2 * i], g1 = gb_s[2 * i + 1];
       const float4 b0 = gb_s[2 * 32 * VPL + 2 * i], b1 = gb_s[2 * 32 * VPL + 2 * i + 1];
-      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      const float2 gg[4] = {make_float2(g0.x, g0.y), make_float2(g0.z, g0.w), make_float2(g1.x, g1.y),
+                            make_float2(g1.z, g1.w)};
+      const float2 bb[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                            make_float2(b1.z, b1.w)};
       __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&v[j]);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const float2 f = __bfloat1622float2(p2[k]);
-        p2[k] = __float22bfloat162_rn(make_float2((f.x - mean) * rstd * gg[2 * k] + bb[2 * k],
-                                                  (f.y - mean) * rstd * gg[2 * k + 1] + bb[2 * k + 1]));
+        const float2 xh = __fmul2_rn(__fadd2_rn(__bfloat1622float2(p2[k]), nmean), rs2);
+        p2[k] = __float22bfloat162_rn(__ffma2_rn(xh, gg[k], bb[k]));
       }
       hr[i] = v[j];
       amax = max(amax, vec_absmax_bits<T>(v[j]));
@@ -569,17 +572,19 @@ __global__ void __launch_bounds__(256) k_ln_backward_rows(const __nv_bfloat16* _
                                                           const float* __restrict__ rstd,
                                                           const float* __restrict__ gamma,
                                                           __nv_bfloat16* __restrict__ dx, float* __restrict__ part) {
-  // shared: gamma[8][nvec] (k-major: lane-consecutive, conflict-free), then per warp its column
-  // accumulators dgamma[8][nvec], dbeta[8][nvec]
+  // shared: gamma as float2 [4][nvec] (column pair kk of vector i at kk * nvec + i: lane-consecutive,
+  // conflict-free 8-byte accesses), then per warp its column accumulators dgamma, dbeta in the same
+  // layout. The element math runs on the packed fp32x2 pipe (FADD2 / FMUL2 / FFMA2).
   extern __shared__ float lnb_s[];
-  float* gs = lnb_s;
+  float2* gs = reinterpret_cast<float2*>(lnb_s);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  float* accg = lnb_s + 8 * nvec * (1 + 2 * wib);
-  float* accb = accg + 8 * nvec;
-  for (int t = threadIdx.x; t < 8 * nvec; t += blockDim.x) gs[(t & 7) * nvec + (t >> 3)] = __ldg(gamma + t);
-  for (int t = lane; t < 8 * nvec; t += 32) {
-    accg[t] = 0.0f;
-    accb[t] = 0.0f;
+  float2* accg = reinterpret_cast<float2*>(lnb_s + 8 * nvec * (1 + 2 * wib));
+  float2* accb = accg + 4 * nvec;
+  for (int t = threadIdx.x; t < 8 * nvec; t += blockDim.x)  // column t = 8 i + k
+    lnb_s[2 * (((t & 7) >> 1) * nvec + (t >> 3)) + (t & 1)] = __ldg(gamma + t);
+  for (int t = lane; t < 4 * nvec; t += 32) {
+    accg[t] = make_float2(0.0f, 0.0f);
+    accb[t] = make_float2(0.0f, 0.0f);
   }
   __syncthreads();
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib;
@@ -596,7 +601,8 @@ __global__ void __launch_bounds__(256) k_ln_backward_rows(const __nv_bfloat16* _
       vd[j] = i < nvec ? ld_stream(reinterpret_cast<const uint4*>(dh) + off + i) : make_uint4(0, 0, 0, 0);
     }
     const float mu = __ldg(mean + row), rs = __ldg(rstd + row);
-    float s1 = 0.0f, s2 = 0.0f;
+    const float2 nmu = make_float2(-mu, -mu), rs2 = make_float2(rs, rs);
+    float2 s1 = make_float2(0.0f, 0.0f), s2 = make_float2(0.0f, 0.0f);
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
       const int i = j * 32 + lane;
@@ -605,24 +611,22 @@ __global__ void __launch_bounds__(256) k_ln_backward_rows(const __nv_bfloat16* _
       const __nv_bfloat162* pd = reinterpret_cast<const __nv_bfloat162*>(&vd[j]);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const float2 fx = __bfloat1622float2(px[k]);
         const float2 fd = __bfloat1622float2(pd[k]);
-        const float x0 = (fx.x - mu) * rs, x1 = (fx.y - mu) * rs;
-        const float g0 = fd.x * gs[(2 * k) * nvec + i], g1 = fd.y * gs[(2 * k + 1) * nvec + i];
-        s1 += g0 + g1;
-        s2 += g0 * x0 + g1 * x1;
-        accg[(2 * k) * nvec + i] += fd.x * x0;
-        accg[(2 * k + 1) * nvec + i] += fd.y * x1;
-        accb[(2 * k) * nvec + i] += fd.x;
-        accb[(2 * k + 1) * nvec + i] += fd.y;
+        const float2 xh = __fmul2_rn(__fadd2_rn(__bfloat1622float2(px[k]), nmu), rs2);
+        const float2 g = __fmul2_rn(fd, gs[k * nvec + i]);
+        s1 = __fadd2_rn(s1, g);
+        s2 = __ffma2_rn(g, xh, s2);
+        accg[k * nvec + i] = __ffma2_rn(fd, xh, accg[k * nvec + i]);
+        accb[k * nvec + i] = __fadd2_rn(accb[k * nvec + i], fd);
       }
     }
+    float t1 = s1.x + s1.y, t2 = s2.x + s2.y;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+      t2 += __shfl_xor_sync(0xffffffffu, t2, o);
     }
-    const float m1 = s1 * inv_n, m2 = s2 * inv_n;
+    const float2 nm1 = make_float2(-t1 * inv_n, -t1 * inv_n), nm2 = make_float2(-t2 * inv_n, -t2 * inv_n);
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
       const int i = j * 32 + lane;
@@ -633,11 +637,10 @@ __global__ void __launch_bounds__(256) k_ln_backward_rows(const __nv_bfloat16* _
       __nv_bfloat162* po = reinterpret_cast<__nv_bfloat162*>(&o);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const float2 fx = __bfloat1622float2(px[k]);
-        const float2 fd = __bfloat1622float2(pd[k]);
-        const float x0 = (fx.x - mu) * rs, x1 = (fx.y - mu) * rs;
-        const float g0 = fd.x * gs[(2 * k) * nvec + i], g1 = fd.y * gs[(2 * k + 1) * nvec + i];
-        po[k] = __float22bfloat162_rn(make_float2(rs * (g0 - m1 - x0 * m2), rs * (g1 - m1 - x1 * m2)));
+        const float2 xh = __fmul2_rn(__fadd2_rn(__bfloat1622float2(px[k]), nmu), rs2);
+        const float2 g = __fmul2_rn(__bfloat1622float2(pd[k]), gs[k * nvec + i]);
+        // rs (g - mean(g) - xhat mean(g xhat))
+        po[k] = __float22bfloat162_rn(__fmul2_rn(__ffma2_rn(xh, nm2, __fadd2_rn(g, nm1)), rs2));
       }
       reinterpret_cast<uint4*>(dx)[off + i] = o;
     }
@@ -651,8 +654,9 @@ __global__ void __launch_bounds__(256) k_ln_backward_rows(const __nv_bfloat16* _
     const int which = t / (8 * nvec), tt = t - which * 8 * nvec;  // 0: dgamma, 1: dbeta
     float acc = 0.0f;
     for (int w = 0; w < nw; ++w) acc += lnb_s[8 * nvec * (1 + 2 * w + which) + tt];
-    const int k = tt / nvec, i = tt - k * nvec;
-    pg[which * cols + i * 8 + k] = acc;
+    // float tt = 2 (kk nvec + i) + e holds column 8 i + 2 kk + e
+    const int kk = tt / (2 * nvec), rem = tt - kk * 2 * nvec;
+    pg[which * cols + (rem >> 1) * 8 + 2 * kk + (rem & 1)] = acc;
   }
 }
 
