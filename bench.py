@@ -303,6 +303,8 @@ def run_ours(args):
     # GEMM + reduce-scatter, barrier, all-gather of owned rows); NCCL calls inside it, so eager
     fused_comm = args.dw_comm == "fused" and plain and not args.unfused_gq
     if fused_comm:
+        if world > 1 and torch.distributed.get_backend() != "nccl":
+            raise SystemExit("--dw-comm fused needs the NCCL backend (its barriers and all-gather are NCCL)")
         args.no_graph = True
         comm0 = dp.NcclComm(A.handle(local), rank, world) if world > 1 else None
         for lay in layers:
