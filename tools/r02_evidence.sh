@@ -13,6 +13,10 @@ case "${PART:-1}" in
   done
   timeout 400 python bench.py --config vit_block --no-overlap --no-cpu > gpurun_out/bench_vit_block_unfused.json 2>/dev/null
   timeout 400 python bench.py --unfused-gq --no-overlap --no-e2e --no-cpu > gpurun_out/bench_c2_unfused_gq.json 2>/dev/null
+  timeout 400 python bench.py --dw-comm fused --no-e2e --no-cpu > gpurun_out/bench_c2_dw_comm_fused.json 2>/dev/null
+  timeout 300 python tools/hbm_kernels.py > gpurun_out/hbm_kernels.txt 2>&1
+  timeout 300 python tools/mlp_e2e_sweep.py 4096:1024,8192:2048,8192:0 > gpurun_out/mlp_e2e_sweep.txt 2>&1
+  timeout 300 python tools/pcie_bw.py > gpurun_out/pcie_bw.txt 2>&1
   timeout 600 python bench.py --impl reference > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
   timeout 600 $N --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python tools/prof_step.py > /dev/null 2>&1
   ;;
@@ -28,6 +32,7 @@ case "${PART:-1}" in
   timeout 600 $N $F -k regex:act_quantize_rows -s 2 -c 2 -o gpurun_out/prof_k10 -f python tools/prof_k10.py > /dev/null 2>&1
   timeout 600 $N $F -k regex:k_ln_ -s 2 -c 2 -o gpurun_out/prof_ln -f python tools/prof_ln.py > /dev/null 2>&1
   NBLK=4 timeout 600 $N $F -k regex:adamw -s 2 -c 1 -o gpurun_out/prof_adamw -f python tools/oprof.py > /dev/null 2>&1
+  timeout 600 $N $F -k regex:fp8_rows_reg -s 1 -c 2 -o gpurun_out/prof_fp8 -f python tools/prof_fp8.py > /dev/null 2>&1
   ;;
 esac
 ls -la gpurun_out/
