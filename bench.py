@@ -632,9 +632,16 @@ def run_c5(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     shapes = [(3840, 1280), (1280, 1280), (5120, 1280), (1280, 5120)] * 51
-    # whole tensors per rank, size-balanced (LPT: max / mean 1.0065 at 8 ranks; round-robin by
-    # index was 1.36)
-    mine = [shapes[i] for i in dp.lpt_partition([a * b for a, b in shapes], world)[rank]]
+    zero1 = args.zero1
+    if zero1:
+        # ZeRO-1: every tensor row-sharded by the fused reduce-scatter's ownership (dp.owned_rows),
+        # one fp64 all-reduce of the 204 per-tensor RMS sums between the two phases
+        rows = [dp.owned_rows(a, rank, world) for a, _ in shapes]
+        mine = [(r1 - r0, b) for (r0, r1), (_, b) in zip(rows, shapes)]
+    else:
+        # whole tensors per rank, size-balanced (LPT: max / mean 1.0065 at 8 ranks; round-robin by
+        # index was 1.36)
+        mine = [shapes[i] for i in dp.lpt_partition([a * b for a, b in shapes], world)[rank]]
     total_params = sum(a * b for a, b in shapes)
     n_mine = sum(a * b for a, b in mine)
     # one flat allocation per state array, tensors are views (as a trainer's flat buffers)
@@ -652,7 +659,15 @@ def run_c5(args):
         off += n
     lib = A.load()
     nbytes = C.c_size_t()
-    A.check(lib.sb_stableadamw_workspace_size(arr, len(mine), C.byref(nbytes)))
+    if zero1:
+        A.check(lib.sb_stableadamw_sharded_workspace_size(arr, len(mine), C.byref(nbytes)))
+        tot = (C.c_int64 * len(shapes))(*[a * b for a, b in shapes])
+        comm = dp.NcclComm(A.handle(local), rank, world) if world > 1 and \
+            torch.distributed.get_backend() == "nccl" else None
+        if world > 1 and comm is None:
+            raise SystemExit("--zero1 under N > 1 needs the NCCL backend (the library's fp64 all-reduce)")
+    else:
+        A.check(lib.sb_stableadamw_workspace_size(arr, len(mine), C.byref(nbytes)))
     ws = torch.empty(max(1, nbytes.value), dtype=torch.uint8, device=dev)
     out = torch.empty((2, len(mine)), dtype=torch.float64, device=dev)
     hp = A.AdamwHparams(1e-3, 0.9, 0.99, 0.0, 1e-6, 0.2, 1.0, A.SB_CLIP_UPDATE)
@@ -663,6 +678,11 @@ def run_c5(args):
 
     def step():
         t[0] += 1
+        if zero1:
+            A.check(h.lib.sb_stableadamw_step_sharded(h.h, arr, tot, len(mine), C.byref(hp), t[0], None, None,
+                                                      C.c_void_p(out[0].data_ptr()), C.c_void_p(out[1].data_ptr()),
+                                                      C.c_void_p(ws.data_ptr()), ws.numel()))
+            return
         A.check(h.lib.sb_stableadamw_step(h.h, arr, len(mine), C.byref(hp), t[0], C.c_void_p(out[0].data_ptr()),
                                           C.c_void_p(out[1].data_ptr()), C.c_void_p(ws.data_ptr()), ws.numel()))
 
@@ -693,12 +713,17 @@ def run_c5(args):
                 "vs_baseline": None, "dtype": "f64 math / f32 storage", "data": "synthetic",
                 "config": {"workload": "StableAdamW (update_clip) over 51 ViT-H blocks x 4 weight tensors",
                            "config": "c5", "params_total": total_params, "params_per_rank": n_mine,
-                           "tensors_per_rank": len(mine), "parallelism": f"{world} ranks, whole tensors, size-balanced (LPT)",
+                           "tensors_per_rank": len(mine),
+                           "parallelism": (f"{world} ranks, ZeRO-1: every tensor row-sharded, phase 1 / fp64 "
+                                           "all-reduce of the per-tensor RMS sums / phase 2") if zero1 else
+                                          f"{world} ranks, whole tensors, size-balanced (LPT)",
                            "l2": "state (16 GB) far larger than L2"},
                 "gpu_launches": launches,
                 "roofline": {"bound": "hbm", "kernel": "StableAdamW phase 1 + 2 (csrc/optim.cu)", "achieved": achieved,
                              "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
-                             "traffic": adamw_traffic(n_mine), "bytes_per_param": 28},
+                             "traffic": None if zero1 else adamw_traffic(n_mine), "bytes_per_param": 28,
+                             "note": ("ZeRO-1 splits the step at the RMS: phase 2 re-reads v, u from HBM (36 B/param "
+                                      "moved, 28 counted)") if zero1 else None},
                 "clocks": clk.summary(), "e2e": None, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -975,6 +1000,8 @@ def main():
     ap.add_argument("--unfused-gq", action="store_true",
                     help="quantize G in its own kernel instead of inside the dW GEMM launch (A/B)")
     ap.add_argument("--qkv-packed", action="store_true", help="vit_block: one scale for the packed qkv weight")
+    ap.add_argument("--zero1", action="store_true", help="c5: ZeRO-1 row-sharded optimizer (phase split + fp64 "
+                    "all-reduce of the per-tensor RMS sums) instead of whole tensors per rank")
     ap.add_argument("--dw-comm", default="allreduce", choices=["allreduce", "fused"],
                     help="N > 1: NCCL all-reduce of dW after the GEMM on a comm stream (default), or the dW "
                          "GEMM's reduce-scatter epilogue over peer memory + all-gather (sb_dp_wgrad_allreduce_fused)")

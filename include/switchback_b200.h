@@ -409,6 +409,34 @@ sb_status sb_stableadamw_step_ex(sb_handle h, const sb_adamw_tensor* tensors, in
                                  const sb_adamw_hparams* hp, int64_t t, const sb_adamw_extras* extras,
                                  double* rms_out, double* eta_out, void* workspace, size_t workspace_bytes);
 
+/* ZeRO-1 StableAdamW: `tensors[i]` is this rank's contiguous shard of tensor i
+ * (e.g. the dW rows it owns after sb_wgrad_reduce_scatter, with theta / v / u rows to match) and
+ * numel_total[i] the whole tensor's element count. RMS couples a whole tensor
+ * (optimizer.cpp:148-157), so the step splits there:
+ *   phase 1: v, u of the shard, and per tensor the shard's sum of g^2 / max(u, eps^2) (fp64,
+ *            fixed order) into shard_sums (DEVICE [ntensors]);
+ *   (the caller sums shard_sums over ranks: one fp64 all-reduce of ntensors values)
+ *   phase 2: RMS = sqrt(total / numel_total), eta, the theta update of the shard; optional bf16
+ *            shadow rows + tensor-wise absmax words for the next forward, as sb_stableadamw_step_ex.
+ * sb_stableadamw_step_sharded runs both with sb_dp_allreduce_sum_f64 between them (the handle's
+ * communicator; one rank: no collective). v, u are bitwise the unsharded step's; RMS differs only by
+ * the cross-rank summation order (theta bitwise when eta does not depend on it, e.g. RMS <= 1
+ * under update clipping). Plain steps: kGradClip is refused (it needs the global norm).
+ * Workspace: sb_stableadamw_sharded_workspace_size. HOST arrays: tensors, numel_total,
+ * shadow_bf16, absmax_word (may be NULL). */
+sb_status sb_stableadamw_sharded_workspace_size(const sb_adamw_tensor* tensors, int ntensors, size_t* bytes);
+sb_status sb_stableadamw_shard_phase1(sb_handle h, const sb_adamw_tensor* tensors, const int64_t* numel_total,
+                                      int ntensors, const sb_adamw_hparams* hp, int64_t t, double* shard_sums,
+                                      void* workspace, size_t workspace_bytes);
+sb_status sb_stableadamw_shard_phase2(sb_handle h, const sb_adamw_tensor* tensors, const int64_t* numel_total,
+                                      int ntensors, const sb_adamw_hparams* hp, int64_t t, const double* total_sums,
+                                      void* const* shadow_bf16, unsigned int* const* absmax_word, double* rms_out,
+                                      double* eta_out, void* workspace, size_t workspace_bytes);
+sb_status sb_stableadamw_step_sharded(sb_handle h, const sb_adamw_tensor* tensors, const int64_t* numel_total,
+                                      int ntensors, const sb_adamw_hparams* hp, int64_t t, void* const* shadow_bf16,
+                                      unsigned int* const* absmax_word, double* rms_out, double* eta_out,
+                                      void* workspace, size_t workspace_bytes);
+
 /* quantize_tensorwise (+ transpose) of x with its absmax already known (an fp32-bit-pattern word
  * as sb_stableadamw_step_ex writes it): one pass, payloads bit-identical to sb_quantize_tensorwise. */
 sb_status sb_quantize_tensorwise_from_absmax(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols,

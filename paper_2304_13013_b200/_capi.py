@@ -44,7 +44,8 @@ EXPORTS = [
     "sb_dp_allreduce_grads_async", "sb_dp_wait", "sb_dp_allreduce_max_u32", "sb_dp_allreduce_sum_f64",
     "sb_dp_destroy", "sb_dp_symmetric_alloc", "sb_dp_symmetric_open", "sb_dp_symmetric_exchange",
     "sb_dp_symmetric_free", "sb_dp_owned_rows", "sb_wgrad_reduce_scatter", "sb_dp_barrier", "sb_dp_allgather_rows",
-    "sb_dp_wgrad_allreduce_fused",
+    "sb_dp_wgrad_allreduce_fused", "sb_stableadamw_sharded_workspace_size", "sb_stableadamw_shard_phase1",
+    "sb_stableadamw_shard_phase2", "sb_stableadamw_step_sharded",
 ]
 
 
@@ -162,6 +163,13 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             "sb_dp_owned_rows": ([i64, i32, i32, C.POINTER(i64), C.POINTER(i64)], i32),
             "sb_wgrad_reduce_scatter": ([v, v, v, i32, i64, i64, i64, v, v, i64, v], i32),
             "sb_dp_barrier": ([v], i32),
+            "sb_stableadamw_sharded_workspace_size": ([C.POINTER(AdamwTensor), i32, C.POINTER(sz)], i32),
+            "sb_stableadamw_shard_phase1": ([v, C.POINTER(AdamwTensor), v, i32, C.POINTER(AdamwHparams), i64, v, v,
+                                             sz], i32),
+            "sb_stableadamw_shard_phase2": ([v, C.POINTER(AdamwTensor), v, i32, C.POINTER(AdamwHparams), i64, v, v, v,
+                                             v, v, v, sz], i32),
+            "sb_stableadamw_step_sharded": ([v, C.POINTER(AdamwTensor), v, i32, C.POINTER(AdamwHparams), i64, v, v, v,
+                                             v, v, sz], i32),
             "sb_dp_allgather_rows": ([v, v, i64, i64], i32),
             "sb_dp_wgrad_allreduce_fused": ([v, v, v, i32, i64, i64, i64, v, v, i64, v], i32),
             "sb_linear_backward_prequant": ([v, C.POINTER(LinearMode), C.POINTER(LinearCtx), v, v, v, v, v, i32], i32),

@@ -1110,7 +1110,9 @@ static sb_status mlp_host_enqueue(sb_handle h, const sb_linear_mode* mode, int a
   // chunk i covers rows [r0(i), r0(i) + rows(i)); the first chunk is a quarter chunk so the
   // first Y leaves (and the D2H direction starts) sooner (SB_HOST_FIRST overrides)
   const char* fe = std::getenv("SB_HOST_FIRST");
-  const int64_t first = std::min<int64_t>(b, fe ? std::max<int64_t>(128, std::atoll(fe)) : std::max<int64_t>(128, chunk / 4));
+  // (a batch that fits one chunk stays one chunk)
+  const int64_t first = b <= chunk ? b : std::min<int64_t>(b, fe ? std::max<int64_t>(128, std::atoll(fe))
+                                                                 : std::max<int64_t>(128, chunk / 4));
   const int64_t nchunks = 1 + (b - first + chunk - 1) / chunk;
   auto r0_of = [&](int64_t i) { return i == 0 ? int64_t(0) : first + (i - 1) * chunk; };
   auto rows_of = [&](int64_t i) { return i == 0 ? first : std::min(chunk, b - r0_of(i)); };

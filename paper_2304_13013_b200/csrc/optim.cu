@@ -44,6 +44,8 @@ struct TensorDesc {
   int32_t vec;     // all four arrays 16-byte aligned and numel % 4 == 0: float4 path
   __nv_bfloat16* shadow;  // optional: bf16(theta') for the next forward (sb_adamw_extras)
   unsigned int* word;     // optional: max |bf16(theta')| as fp32 bits
+  double numel_total;     // elements of the whole tensor (RMS denominator): numel, or the
+                          // full tensor's count when this is one rank's shard (ZeRO-1)
 };
 
 struct Group {
@@ -53,6 +55,7 @@ struct Group {
   int64_t seg_start[2 * kMaxGroup];
   int16_t seg_id[2 * kMaxGroup];
   int count;
+  int nseg;  // segments in seg_start / seg_id (2 * count fused, count per ZeRO-1 phase)
   int64_t total_blocks;
   int64_t total_tasks;
 };
@@ -275,7 +278,11 @@ __device__ __forceinline__ void st_release(unsigned int* p, unsigned int v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <bool EX>
+// MODE 0: the fused step above. MODE 1 (ZeRO-1 phase 1): phase-1 tasks only; the tensor's fixed-
+// order sum of g^2 / max(u, eps^2) over this rank's shard goes to eta_buf[index] (the caller sums
+// it over ranks). MODE 2 (ZeRO-1 phase 2): phase-2 tasks only; eta_buf[index] holds the sum over
+// every rank's shard, from which each task forms RMS over the whole tensor (numel_total) and eta.
+template <bool EX, int MODE = 0>
 __global__ void __launch_bounds__(kThreads, EX ? 8 : 9) k_adamw_persistent(const __grid_constant__ Group grp, Coeffs c,
                                                                const double* __restrict__ clip_ptr,
                                                                double* __restrict__ partials,
@@ -301,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, EX ? 8 : 9) k_adamw_persistent(const
     if (task >= grp.total_tasks) break;
     unsigned int next = 0;
     if (threadIdx.x == 0) next = atomicAdd(sync, 1u);
-    int lo = 0, hi = 2 * grp.count - 1;  // segment containing `task`
+    int lo = 0, hi = grp.nseg - 1;  // segment containing `task`
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
       if (grp.seg_start[mid] <= task) lo = mid;
@@ -312,7 +319,23 @@ __global__ void __launch_bounds__(kThreads, EX ? 8 : 9) k_adamw_persistent(const
     const TensorDesc& d = grp.t[ti];
     const int64_t local = (seg & 1) ? d.nblocks + (task - d.task2) : task - d.task0;
     const bool skip = EX && c.skipped != nullptr && c.skipped[d.index] != 0;
-    if (local < d.nblocks) {
+    if (MODE == 2) {
+      if (threadIdx.x == 0) {
+        const double rms = __dsqrt_rn(__ddiv_rn(__ldcg(eta_buf + d.index), d.numel_total));
+        const double eta = c.update_clip ? __ddiv_rn(c.alpha, rms > 1.0 ? rms : 1.0) : c.alpha;
+        s_eta = eta;
+        if (local == d.nblocks) {
+          if (rms_out) rms_out[d.index] = rms;
+          if (eta_out) eta_out[d.index] = eta;
+        }
+      }
+      __syncthreads();
+      const uint32_t m = phase2_chunk<EX>(d, c, s_eta, local - d.nblocks, false);
+      if (EX && d.word != nullptr) {
+        const uint32_t wm = __reduce_max_sync(0xffffffffu, m);
+        if ((threadIdx.x & 31) == 0 && wm != 0u) atomicMax(d.word, wm);
+      }
+    } else if (local < d.nblocks) {
       const double s = block_sum(skip ? 0.0 : phase1_chunk<EX>(d, c, clip, local), red);
       if (threadIdx.x == 0) {
         partials[d.block0 + local] = s;
@@ -328,7 +351,9 @@ __global__ void __launch_bounds__(kThreads, EX ? 8 : 9) k_adamw_persistent(const
         double sum = 0.0;
         for (int64_t j = threadIdx.x; j < d.nblocks; j += kThreads) sum = __dadd_rn(sum, __ldcg(partials + d.block0 + j));
         const double tot = block_sum(sum, red);
-        if (threadIdx.x == 0) {
+        if (MODE == 1) {
+          if (threadIdx.x == 0) eta_buf[d.index] = tot;
+        } else if (threadIdx.x == 0) {
           double rms = __dsqrt_rn(__ddiv_rn(tot, static_cast<double>(d.numel)));
           double eta = c.update_clip ? __ddiv_rn(c.alpha, rms > 1.0 ? rms : 1.0) : c.alpha;
           if (skip) {  // trainer.cpp:140-143: a skipped tensor reports rms = NaN
@@ -459,7 +484,8 @@ double beta2_warmup(int64_t t, double lambda) {  // optimizer.cpp:44-49
   return std::min(b, std::nextafter(1.0, 0.0));
 }
 
-std::vector<Group> make_groups(const sb_adamw_tensor* ts, int n, int64_t* total_blocks, const sb_adamw_extras* ex) {
+std::vector<Group> make_groups(const sb_adamw_tensor* ts, int n, int64_t* total_blocks, const sb_adamw_extras* ex,
+                               int mode = 0, const int64_t* numel_total = nullptr) {
   std::vector<Group> groups;
   Group cur{};
   int64_t blocks_all = 0;
@@ -477,6 +503,7 @@ std::vector<Group> make_groups(const sb_adamw_tensor* ts, int n, int64_t* total_
     d.v = ts[i].v;
     d.u = ts[i].u;
     d.numel = ts[i].numel;
+    d.numel_total = static_cast<double>(numel_total ? numel_total[i] : ts[i].numel);
     d.block0 = blocks_all;  // partials are global across groups (the grad-clip pass shares them)
     d.nblocks = nb;
     d.index = i;
@@ -499,12 +526,17 @@ std::vector<Group> make_groups(const sb_adamw_tensor* ts, int n, int64_t* total_
       else g.t[k].task0 = tk;
       tk += g.t[k].nblocks;
     };
-    for (int k = 0; k < g.count; ++k) {
-      seg(k, 0);
-      if (k > 0) seg(k - 1, 1);
+    if (mode == 0) {
+      for (int k = 0; k < g.count; ++k) {
+        seg(k, 0);
+        if (k > 0) seg(k - 1, 1);
+      }
+      if (g.count > 0) seg(g.count - 1, 1);
+    } else {  // ZeRO-1: one phase per launch
+      for (int k = 0; k < g.count; ++k) seg(k, mode == 1 ? 0 : 1);
     }
-    if (g.count > 0) seg(g.count - 1, 1);
     g.total_tasks = tk;
+    g.nseg = ns;
   }
   *total_blocks = blocks_all;
   return groups;
@@ -637,4 +669,170 @@ extern "C" sb_status sb_stableadamw_step(sb_handle h, const sb_adamw_tensor* ten
                                          const sb_adamw_hparams* hp, int64_t t, double* rms_out, double* eta_out,
                                          void* workspace, size_t workspace_bytes) {
   return sb_stableadamw_step_ex(h, tensors, ntensors, hp, t, nullptr, rms_out, eta_out, workspace, workspace_bytes);
+}
+
+// ------------------------------------------------------------------ ZeRO-1 ----
+#define SB_TRY_O(expr)           \
+  do {                           \
+    const sb_status _s = (expr); \
+    if (_s != SB_OK) return _s;  \
+  } while (0)
+__global__ void k_shard_info(const double* sum, double numel_total, double alpha, int update_clip, double* rms_out,
+                             double* eta_out) {
+  const double rms = __dsqrt_rn(__ddiv_rn(*sum, numel_total));
+  if (rms_out) *rms_out = rms;
+  if (eta_out) *eta_out = update_clip ? __ddiv_rn(alpha, rms > 1.0 ? rms : 1.0) : alpha;
+}
+// StableAdamW on one rank's shard of every tensor ("C5 ZeRO-1 adds reduce-scatter
+// (dW) -> local StableAdamW on the shard -> all-gather(theta), plus one fp64 scalar per tensor
+// (sum g^2 / max(u, eps^2)) allreduced before eta"). The RMS couples every element of a tensor
+// (optimizer.cpp:148-157), so the step splits at that point: phase 1 updates v, u of the shard and
+// returns the shard's sum per tensor; the caller (or sb_stableadamw_step_sharded, over the
+// handle's NCCL communicator) sums them over ranks; phase 2 forms RMS over the whole tensor and
+// updates theta (and, with shadow_bf16 / absmax_word, the next forward's bf16 weight rows).
+// v, u are bitwise those of the unsharded step; RMS differs from it only by the order of the
+// cross-rank sum (so theta is bitwise whenever eta does not depend on it, e.g. RMS <= 1 under
+// update clipping). Plain steps only: no loss-scale unscaling, skipping or global-norm clip.
+namespace {
+sb_status shard_check(const char* op, sb_handle h, const sb_adamw_tensor* tensors, const int64_t* numel_total,
+                      int ntensors, const sb_adamw_hparams* hp, int64_t t, void* workspace, size_t workspace_bytes) {
+  if (!h || !hp || (ntensors > 0 && (!tensors || !numel_total)))
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "null argument");
+  if (t < 1) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "t must be >= 1");
+  if (hp->clipping == SB_CLIP_GRAD)
+    return sb::fail(SB_ERR_UNSUPPORTED, op, "grad_clip needs the global norm: use the unsharded step");
+  for (int i = 0; i < ntensors; ++i)
+    if (tensors[i].numel < 0 || numel_total[i] < tensors[i].numel ||
+        (tensors[i].numel != 0 && (!tensors[i].theta || !tensors[i].grad || !tensors[i].v || !tensors[i].u)))
+      return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad tensor shard");
+  size_t need = 0;
+  sb_stableadamw_workspace_size(tensors, ntensors, &need);
+  need += static_cast<size_t>(ntensors) * sizeof(double);
+  if (!workspace || workspace_bytes < need) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "workspace too small");
+  return SB_OK;
+}
+Coeffs shard_coeffs(const sb_adamw_hparams* hp, int64_t t) {
+  Coeffs c{};
+  c.b1 = debias(hp->beta1, t);
+  c.b2 = hp->beta2_warmup_lambda > 0 ? beta2_warmup(t, hp->beta2_warmup_lambda) : debias(hp->beta2, t);
+  c.omb1 = 1.0 - c.b1;
+  c.omb2 = 1.0 - c.b2;
+  c.floor_ = hp->eps * hp->eps;
+  c.eps = hp->eps;
+  c.alpha = hp->alpha;
+  c.wd = hp->weight_decay;
+  c.update_clip = hp->clipping == SB_CLIP_UPDATE;
+  return c;
+}
+}  // namespace
+
+extern "C" sb_status sb_stableadamw_sharded_workspace_size(const sb_adamw_tensor* tensors, int ntensors,
+                                                           size_t* bytes) {
+  SB_TRY_O(sb_stableadamw_workspace_size(tensors, ntensors, bytes));
+  *bytes = ((*bytes + 15) & ~size_t(15)) + static_cast<size_t>(ntensors) * sizeof(double);
+  return SB_OK;
+}
+
+extern "C" sb_status sb_stableadamw_shard_phase1(sb_handle h, const sb_adamw_tensor* tensors,
+                                                 const int64_t* numel_total, int ntensors,
+                                                 const sb_adamw_hparams* hp, int64_t t, double* shard_sums,
+                                                 void* workspace, size_t workspace_bytes) {
+  const char* op = "optimizer_step_sharded";
+  SB_TRY_O(shard_check(op, h, tensors, numel_total, ntensors, hp, t, workspace, workspace_bytes));
+  if (ntensors > 0 && !shard_sums) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "null shard_sums");
+  cudaSetDevice(h->device);
+  const Coeffs c = shard_coeffs(hp, t);
+  int64_t total_blocks = 0;
+  const std::vector<Group> groups = make_groups(tensors, ntensors, &total_blocks, nullptr, 1, numel_total);
+  double* partials = static_cast<double*>(workspace);
+  unsigned int* sync = reinterpret_cast<unsigned int*>(partials + total_blocks + 2 + kMaxGroup + ntensors);
+  // an empty shard contributes 0 to its tensor's sum
+  if (ntensors > 0) SB_CUDA_CHECK(op, cudaMemsetAsync(shard_sums, 0, sizeof(double) * ntensors, h->stream));
+  int blocks_per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_adamw_persistent<false, 1>, kThreads, 0);
+  blocks_per_sm = std::max(1, blocks_per_sm);
+  for (const Group& g : groups) {
+    SB_CUDA_CHECK(op, cudaMemsetAsync(sync, 0, sizeof(unsigned int) * (2 * g.count + 1), h->stream));
+    const int64_t grid = std::min<int64_t>(g.total_tasks, static_cast<int64_t>(h->num_sms) * blocks_per_sm);
+    h->launches++;
+    k_adamw_persistent<false, 1><<<static_cast<unsigned>(grid), kThreads, 0, h->stream>>>(
+        g, c, nullptr, partials, sync, shard_sums, nullptr, nullptr);
+  }
+  SB_LAUNCH_CHECK(op);
+  return SB_OK;
+}
+
+extern "C" sb_status sb_stableadamw_shard_phase2(sb_handle h, const sb_adamw_tensor* tensors,
+                                                 const int64_t* numel_total, int ntensors,
+                                                 const sb_adamw_hparams* hp, int64_t t, const double* total_sums,
+                                                 void* const* shadow_bf16, unsigned int* const* absmax_word,
+                                                 double* rms_out, double* eta_out, void* workspace,
+                                                 size_t workspace_bytes) {
+  const char* op = "optimizer_step_sharded";
+  SB_TRY_O(shard_check(op, h, tensors, numel_total, ntensors, hp, t, workspace, workspace_bytes));
+  if (ntensors > 0 && !total_sums) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "null total_sums");
+  cudaSetDevice(h->device);
+  const Coeffs c = shard_coeffs(hp, t);
+  sb_adamw_extras ex{};
+  ex.loss_scale = 1.0;
+  ex.shadow_bf16 = shadow_bf16;
+  ex.absmax_word = absmax_word;
+  const bool extra = shadow_bf16 != nullptr || absmax_word != nullptr;
+  int64_t total_blocks = 0;
+  const std::vector<Group> groups =
+      make_groups(tensors, ntensors, &total_blocks, extra ? &ex : nullptr, 2, numel_total);
+  double* partials = static_cast<double*>(workspace);
+  unsigned int* sync = reinterpret_cast<unsigned int*>(partials + total_blocks + 2 + kMaxGroup + ntensors);
+  if (absmax_word)
+    for (int i = 0; i < ntensors; ++i)
+      if (absmax_word[i]) SB_CUDA_CHECK(op, cudaMemsetAsync(absmax_word[i], 0, sizeof(unsigned int), h->stream));
+  int blocks_per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, extra ? k_adamw_persistent<true, 2> : k_adamw_persistent<false, 2>,
+                                                kThreads, 0);
+  blocks_per_sm = std::max(1, blocks_per_sm);
+  for (const Group& g : groups) {
+    SB_CUDA_CHECK(op, cudaMemsetAsync(sync, 0, sizeof(unsigned int), h->stream));
+    const int64_t grid = std::min<int64_t>(g.total_tasks, static_cast<int64_t>(h->num_sms) * blocks_per_sm);
+    h->launches++;
+    // eta_buf = the summed RMS terms, indexed by caller tensor (read only in MODE 2)
+    double* sums = const_cast<double*>(total_sums);
+    if (extra)
+      k_adamw_persistent<true, 2><<<static_cast<unsigned>(grid), kThreads, 0, h->stream>>>(g, c, nullptr, partials, sync,
+                                                                                          sums, rms_out, eta_out);
+    else
+      k_adamw_persistent<false, 2><<<static_cast<unsigned>(grid), kThreads, 0, h->stream>>>(g, c, nullptr, partials, sync,
+                                                                                           sums, rms_out, eta_out);
+  }
+  // a rank whose shard of a tensor is empty still reports the tensor's rms / eta
+  if (rms_out || eta_out) {
+    for (int i = 0; i < ntensors; ++i) {
+      if (tensors[i].numel != 0) continue;
+      h->launches++;
+      k_shard_info<<<1, 1, 0, h->stream>>>(total_sums + i, static_cast<double>(numel_total[i]), c.alpha,
+                                           c.update_clip, rms_out ? rms_out + i : nullptr, eta_out ? eta_out + i : nullptr);
+    }
+  }
+  SB_LAUNCH_CHECK(op);
+  return SB_OK;
+}
+
+extern "C" sb_status sb_stableadamw_step_sharded(sb_handle h, const sb_adamw_tensor* tensors,
+                                                 const int64_t* numel_total, int ntensors,
+                                                 const sb_adamw_hparams* hp, int64_t t,
+                                                 void* const* shadow_bf16, unsigned int* const* absmax_word,
+                                                 double* rms_out, double* eta_out, void* workspace,
+                                                 size_t workspace_bytes) {
+  const char* op = "optimizer_step_sharded";
+  SB_TRY_O(shard_check(op, h, tensors, numel_total, ntensors, hp, t, workspace, workspace_bytes));
+  size_t base = 0, need = 0;
+  sb_stableadamw_workspace_size(tensors, ntensors, &base);
+  sb_stableadamw_sharded_workspace_size(tensors, ntensors, &need);
+  if (workspace_bytes < need) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "workspace too small");
+  double* sums = reinterpret_cast<double*>(static_cast<uint8_t*>(workspace) + ((base + 15) & ~size_t(15)));
+  SB_TRY_O(sb_stableadamw_shard_phase1(h, tensors, numel_total, ntensors, hp, t, sums, workspace, base + ntensors * 8));
+  int rank = 0, world = 1;
+  sb_dp_rank(h, &rank, &world);
+  if (world > 1 && ntensors > 0) SB_TRY_O(sb_dp_allreduce_sum_f64(h, sums, ntensors));
+  return sb_stableadamw_shard_phase2(h, tensors, numel_total, ntensors, hp, t, sums, shadow_bf16, absmax_word,
+                                     rms_out, eta_out, workspace, base + ntensors * 8);
 }

@@ -703,6 +703,57 @@ def optimizer_step(tensors: list[TensorRef], hp: OptimizerHyperparams, t: int,
     return [(float(o[0, i]), float(o[1, i])) for i in range(n)]
 
 
+def optimizer_step_sharded(shards: list[TensorRef], numel_total: list[int], hp: OptimizerHyperparams, t: int,
+                           allreduce=None, shadows: list | None = None, workspace: torch.Tensor | None = None):
+    """ZeRO-1 StableAdamW (sb_stableadamw_shard_phase1 / _phase2): `shards[i]` holds this rank's
+    contiguous slice of tensor i (param / grad / v / u views of the same elements), numel_total[i]
+    the whole tensor's size. Between the phases the per-tensor fp64 sums of g^2 / max(u, eps^2)
+    are summed over ranks by `allreduce(sums)` (in place on the float64 device tensor: e.g. a
+    torch.distributed all_reduce; None = one rank, or the library's own NCCL communicator via
+    sb_stableadamw_step_sharded when `allreduce == "nccl"`). shadows[i] = (bf16 view of the shard,
+    int32 word) or None, as optimizer_step_ex. Returns {rms, eta} float64 device tensors."""
+    if t < 1:
+        raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "optimizer_step: t must be >= 1")
+    n = len(shards)
+    arr = (A.AdamwTensor * max(n, 1))()
+    tot = (C.c_int64 * max(n, 1))(*numel_total)
+    for i, r in enumerate(shards):
+        if not (r.param.numel() == r.grad.numel() == r.v.numel() == r.u.numel()):
+            raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, f"optimizer_step: shape mismatch for {r.name}")
+        arr[i] = A.AdamwTensor(r.param.data_ptr(), r.grad.data_ptr(), r.v.data_ptr(), r.u.data_ptr(), r.param.numel())
+    dev = shards[0].param.device if n else torch.device("cuda")
+    if workspace is None:
+        nbytes = C.c_size_t()
+        A.check(A.load().sb_stableadamw_sharded_workspace_size(arr, n, C.byref(nbytes)))
+        workspace = torch.empty(nbytes.value, dtype=torch.uint8, device=dev)
+    sh = (C.c_void_p * max(n, 1))()
+    wd = (C.c_void_p * max(n, 1))()
+    for i in range(n):
+        s_ = shadows[i] if shadows else None
+        if s_ is not None:
+            sh[i], wd[i] = s_[0].data_ptr(), s_[1].data_ptr()
+    shp = sh if shadows else None
+    wdp = wd if shadows else None
+    hpc = A.AdamwHparams(float(hp.lr_schedule(t)), hp.beta1, hp.beta2, hp.beta2_warmup_lambda, hp.eps,
+                         hp.weight_decay, hp.max_grad_norm, int(hp.clipping))
+    out = {"rms": torch.empty(max(n, 1), dtype=torch.float64, device=dev),
+           "eta": torch.empty(max(n, 1), dtype=torch.float64, device=dev)}
+    h = A.handle(dev.index)
+    if allreduce == "nccl":
+        A.check(h.lib.sb_stableadamw_step_sharded(h.h, arr, tot, n, C.byref(hpc), t, shp, wdp, _p(out["rms"]),
+                                                  _p(out["eta"]), _p(workspace), workspace.numel()))
+        return {k: v[:n] for k, v in out.items()}
+    sums = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    A.check(h.lib.sb_stableadamw_shard_phase1(h.h, arr, tot, n, C.byref(hpc), t, _p(sums), _p(workspace),
+                                              workspace.numel()))
+    if allreduce is not None:
+        allreduce(sums)
+    h.bind_stream(torch.cuda.current_stream(dev).cuda_stream)
+    A.check(h.lib.sb_stableadamw_shard_phase2(h.h, arr, tot, n, C.byref(hpc), t, _p(sums), shp, wdp, _p(out["rms"]),
+                                              _p(out["eta"]), _p(workspace), workspace.numel()))
+    return {k: v[:n] for k, v in out.items()}
+
+
 @dataclass
 class LossScaler:
     """optimizer.hpp:45-48."""
