@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "sb_internal.h"
 
@@ -1107,15 +1108,30 @@ static sb_status mlp_host_enqueue(sb_handle h, const sb_linear_mode* mode, int a
   cudaEvent_t* ev_out = h->hp_ev[3];
   cudaStream_t comp = h->stream, s_in = h->s_in, s_out = h->s_out;
   host_pool_begin(h, pi);
-  // chunk i covers rows [r0(i), r0(i) + rows(i)); the first chunk is a quarter chunk so the
-  // first Y leaves (and the D2H direction starts) sooner (SB_HOST_FIRST overrides)
+  // chunk i covers rows [cuts[i], cuts[i + 1]). Tapered at both ends: a quarter chunk first, so
+  // the first Y leaves (and the D2H direction starts) sooner, and a quarter chunk last, so less
+  // compute and fewer bytes are left for the un-overlapped drain after the last upload.
+  // SB_HOST_FIRST sets the taper rows, SB_HOST_TAPER=0 turns it off (measurement knobs).
   const char* fe = std::getenv("SB_HOST_FIRST");
-  // (a batch that fits one chunk stays one chunk)
-  const int64_t first = b <= chunk ? b : std::min<int64_t>(b, fe ? std::max<int64_t>(128, std::atoll(fe))
-                                                                 : std::max<int64_t>(128, chunk / 4));
-  const int64_t nchunks = 1 + (b - first + chunk - 1) / chunk;
-  auto r0_of = [&](int64_t i) { return i == 0 ? int64_t(0) : first + (i - 1) * chunk; };
-  auto rows_of = [&](int64_t i) { return i == 0 ? first : std::min(chunk, b - r0_of(i)); };
+  const char* te = std::getenv("SB_HOST_TAPER");
+  const bool taper = !(te && te[0] == '0');
+  std::vector<int64_t> cuts{0};
+  if (b <= chunk) {  // a batch that fits one chunk stays one chunk
+    cuts.push_back(b);
+  } else {
+    const int64_t q = std::min<int64_t>(chunk, fe ? std::max<int64_t>(128, std::atoll(fe)) : std::max<int64_t>(128, chunk / 4));
+    int64_t r = taper ? q : chunk;
+    cuts.push_back(r);
+    while (r < b) {
+      const int64_t rem = b - r;
+      const int64_t step = !taper ? std::min(rem, chunk) : rem <= q ? rem : rem <= chunk + q ? rem - q : chunk;
+      r += step;
+      cuts.push_back(r);
+    }
+  }
+  const int64_t nchunks = static_cast<int64_t>(cuts.size()) - 1;
+  auto r0_of = [&](int64_t i) { return cuts[i]; };
+  auto rows_of = [&](int64_t i) { return cuts[i + 1] - cuts[i]; };
   auto h2d = [&](int64_t i) {
     const int s = static_cast<int>(i % NS);
     const int64_t r0 = r0_of(i), rows = rows_of(i);
