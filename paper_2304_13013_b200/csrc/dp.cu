@@ -451,6 +451,11 @@ sb_status sb_dp_wgrad_allreduce_fused(sb_handle h, const void* g, const void* x,
   const char* op = "wgrad_allreduce_fused";
   if (!h || !dw || m <= 0 || n <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
   const bool multi = h->dp_comm != nullptr && h->dp_world > 1;
+  const sb_symbuf* sym = sb::find_symbuf(h, dw, static_cast<size_t>(m * n) * sizeof(float));
+  if (sym && sym->world > 1 && !multi)
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op,
+                    "a multi-rank symmetric buffer needs the handle's communicator for the barriers and all-gather "
+                    "(or call sb_wgrad_reduce_scatter with your own barriers)");
   SB_CUDA_CHECK(op, cudaMemsetAsync(dw, 0, static_cast<size_t>(m * n) * sizeof(float), h->stream));
   if (multi) SB_TRY_S(sb_dp_barrier(h));
   SB_TRY_S(sb_wgrad_reduce_scatter(h, g, x, dt, b, m, n, dw, g_q, ldq, g_state));

@@ -34,7 +34,7 @@ case "${PART:-1}" in
   timeout 600 $N $F -k regex:act_quantize_rows -s 2 -c 2 -o gpurun_out/prof_k10 -f python tools/prof_k10.py > /dev/null 2>&1
   timeout 600 $N $F -k regex:k_ln_ -s 2 -c 2 -o gpurun_out/prof_ln -f python tools/prof_ln.py > /dev/null 2>&1
   NBLK=4 timeout 600 $N $F -k regex:adamw -s 2 -c 1 -o gpurun_out/prof_adamw -f python tools/oprof.py > /dev/null 2>&1
-  timeout 600 $N $F -k regex:fp8_rows_reg -s 1 -c 2 -o gpurun_out/prof_fp8 -f python tools/prof_fp8.py > /dev/null 2>&1
+  timeout 600 $N $F -k regex:fp8_rows -s 1 -c 2 -o gpurun_out/prof_fp8 -f python tools/prof_fp8.py > /dev/null 2>&1
   ;;
 esac
 ls -la gpurun_out/
