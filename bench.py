@@ -851,6 +851,14 @@ def run_vit_block(args):
             torch.cuda.synchronize()
         ms = s_ev.elapsed_time(e_ev) / args.steps
         res[arm] = {"ms_per_step": ms, "value": T / (ms / 1000.0), "clocks": clk.summary()}
+        if os.environ.get("SB_VIT_PROFILE"):  # kernel-time table of one replay on stderr (A/B aid, not the bench)
+            from torch.profiler import ProfilerActivity, profile
+            with profile(activities=[ProfilerActivity.CUDA]) as prof:
+                g.replay()
+                torch.cuda.synchronize()
+            print(f"--- {arm} arm: one replay", file=sys.stderr)
+            print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=40, max_name_column_width=90),
+                  file=sys.stderr)
         del g, blk
         torch.cuda.empty_cache()
     sbv, bfv = res["switchback"], res["bf16"]

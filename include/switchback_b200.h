@@ -419,7 +419,9 @@ sb_status sb_stableadamw_step_ex(sb_handle h, const sb_adamw_tensor* tensors, in
  *   phase 2: RMS = sqrt(total / numel_total), eta, the theta update of the shard; optional bf16
  *            shadow rows + tensor-wise absmax words for the next forward, as sb_stableadamw_step_ex.
  * sb_stableadamw_step_sharded runs both with sb_dp_allreduce_sum_f64 between them (the handle's
- * communicator; one rank: no collective). v, u are bitwise the unsharded step's; RMS differs only by
+ * communicator; one rank: no collective) and max-reduces the absmax words over ranks afterwards
+ * (sb_dp_allreduce_max_words: a shard's word covers its rows only; with the split entries the
+ * caller does that max). v, u are bitwise the unsharded step's; RMS differs only by
  * the cross-rank summation order (theta bitwise when eta does not depend on it, e.g. RMS <= 1
  * under update clipping). Plain steps: kGradClip is refused (it needs the global norm).
  * Workspace: sb_stableadamw_sharded_workspace_size. HOST arrays: tensors, numel_total,
@@ -475,6 +477,9 @@ sb_status sb_dp_wait(sb_handle h);
  * scales across ranks, linear.cpp:239-241) and sum of doubles (a sharded optimizer's RMS sums). */
 sb_status sb_dp_allreduce_max_u32(sb_handle h, unsigned int* words, int64_t n);
 sb_status sb_dp_allreduce_sum_f64(sb_handle h, double* vals, int64_t n);
+/* Max all-reduce of n separate device uint32 words (`words` is a HOST array of device pointers,
+ * entries may be NULL), one NCCL group. */
+sb_status sb_dp_allreduce_max_words(sb_handle h, unsigned int* const* words, int n);
 sb_status sb_dp_destroy(sb_handle h);
 
 /* Fused dW GEMM + reduce-scatter over peer memory (SURVEY.md §8e stage 2). dW lives in a

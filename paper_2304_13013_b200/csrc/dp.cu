@@ -279,6 +279,21 @@ sb_status sb_dp_allreduce_max_u32(sb_handle h, unsigned int* words, int64_t n) {
   return SB_OK;
 }
 
+// Max all-reduce of n separate device words in one NCCL group (the ZeRO-1 step's per-tensor bf16
+// shadow absmax words: each rank saw only its rows).
+sb_status sb_dp_allreduce_max_words(sb_handle h, unsigned int* const* words, int n) {
+  const char* op = "sb_dp_allreduce_max";
+  SB_TRY_S(need_comm(h, op));
+  if (n < 0 || (n > 0 && !words)) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  SB_NCCL(op, nccl().groupStart());
+  for (int i = 0; i < n; ++i)
+    if (words[i])
+      SB_NCCL(op, nccl().allReduce(words[i], words[i], 1, ncclUint32, ncclMax, static_cast<ncclComm_t>(h->dp_comm),
+                                   h->stream));
+  SB_NCCL(op, nccl().groupEnd());
+  return SB_OK;
+}
+
 sb_status sb_dp_allreduce_sum_f64(sb_handle h, double* vals, int64_t n) {
   const char* op = "sb_dp_allreduce_sum";
   SB_TRY_S(need_comm(h, op));

@@ -833,6 +833,9 @@ extern "C" sb_status sb_stableadamw_step_sharded(sb_handle h, const sb_adamw_ten
   int rank = 0, world = 1;
   sb_dp_rank(h, &rank, &world);
   if (world > 1 && ntensors > 0) SB_TRY_O(sb_dp_allreduce_sum_f64(h, sums, ntensors));
-  return sb_stableadamw_shard_phase2(h, tensors, numel_total, ntensors, hp, t, sums, shadow_bf16, absmax_word,
-                                     rms_out, eta_out, workspace, base + ntensors * 8);
+  SB_TRY_O(sb_stableadamw_shard_phase2(h, tensors, numel_total, ntensors, hp, t, sums, shadow_bf16, absmax_word,
+                                       rms_out, eta_out, workspace, base + ntensors * 8));
+  // each rank's absmax words cover its rows only: the next forward's tensor-wise scale is their max
+  if (world > 1 && absmax_word) SB_TRY_O(sb_dp_allreduce_max_words(h, absmax_word, ntensors));
+  return SB_OK;
 }

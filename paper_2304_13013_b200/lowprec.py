@@ -704,7 +704,8 @@ def optimizer_step(tensors: list[TensorRef], hp: OptimizerHyperparams, t: int,
 
 
 def optimizer_step_sharded(shards: list[TensorRef], numel_total: list[int], hp: OptimizerHyperparams, t: int,
-                           allreduce=None, shadows: list | None = None, workspace: torch.Tensor | None = None):
+                           allreduce=None, shadows: list | None = None, workspace: torch.Tensor | None = None,
+                           allreduce_max=None):
     """ZeRO-1 StableAdamW (sb_stableadamw_shard_phase1 / _phase2): `shards[i]` holds this rank's
     contiguous slice of tensor i (param / grad / v / u views of the same elements), numel_total[i]
     the whole tensor's size. Between the phases the per-tensor fp64 sums of g^2 / max(u, eps^2)
@@ -751,6 +752,10 @@ def optimizer_step_sharded(shards: list[TensorRef], numel_total: list[int], hp: 
     h.bind_stream(torch.cuda.current_stream(dev).cuda_stream)
     A.check(h.lib.sb_stableadamw_shard_phase2(h.h, arr, tot, n, C.byref(hpc), t, _p(sums), shp, wdp, _p(out["rms"]),
                                               _p(out["eta"]), _p(workspace), workspace.numel()))
+    if shadows and allreduce_max is not None:
+        for s_ in shadows:
+            if s_ is not None:
+                allreduce_max(s_[1])
     return {k: v[:n] for k, v in out.items()}
 
 
