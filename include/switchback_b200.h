@@ -509,7 +509,9 @@ sb_status sb_dp_barrier(sb_handle h);
 /* Every owner's rows of dw broadcast into the other ranks' copies (one NCCL group). */
 sb_status sb_dp_allgather_rows(sb_handle h, float* dw, int64_t m, int64_t n);
 /* zero + barrier + sb_wgrad_reduce_scatter + barrier + sb_dp_allgather_rows on the handle's
- * stream: dw = sum over ranks of G_r^T X_r on every rank. */
+ * stream: dw = sum over ranks of G_r^T X_r on every rank. Shapes the one-wave dW kernel does not
+ * serve (e.g. a 1280 x 1280 out-projection) take the local dW GEMM + a NCCL sum all-reduce instead,
+ * with the same result contract; dw must still lie in a symmetric buffer. */
 sb_status sb_dp_wgrad_allreduce_fused(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m,
                                       int64_t n, float* dw, int8_t* g_q, int64_t ldq, float* g_state);
 

@@ -471,6 +471,18 @@ sb_status sb_dp_wgrad_allreduce_fused(sb_handle h, const void* g, const void* x,
     return sb::fail(SB_ERR_INVALID_ARGUMENT, op,
                     "a multi-rank symmetric buffer needs the handle's communicator for the barriers and all-gather "
                     "(or call sb_wgrad_reduce_scatter with your own barriers)");
+  if (!sym) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "dw is not inside a symmetric buffer (sb_dp_symmetric_alloc)");
+  // shapes the one-wave dW kernel does not serve (e.g. a 1280 x 1280 out-projection): the local
+  // GEMM (with G's quantize) and a NCCL sum all-reduce, same result contract
+  const sb::RowQuant rq{g_q, ldq, g_state};
+  if (!sb::dw_wide_serves(h, m, n, b) || dt != SB_BF16) {
+    cudaSetDevice(h->device);
+    SB_TRY_S(sb::wgrad(h, g, x, dt, b, m, n, dw, 0, 0, g_q ? &rq : nullptr));
+    if (multi)
+      SB_NCCL(op, nccl().allReduce(dw, dw, static_cast<size_t>(m * n), ncclFloat32, ncclSum,
+                                   static_cast<ncclComm_t>(h->dp_comm), h->stream));
+    return SB_OK;
+  }
   SB_CUDA_CHECK(op, cudaMemsetAsync(dw, 0, static_cast<size_t>(m * n) * sizeof(float), h->stream));
   if (multi) SB_TRY_S(sb_dp_barrier(h));
   SB_TRY_S(sb_wgrad_reduce_scatter(h, g, x, dt, b, m, n, dw, g_q, ldq, g_state));

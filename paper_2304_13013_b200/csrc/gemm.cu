@@ -402,12 +402,12 @@ cudaError_t launch_tc(sb_handle h, const Operand& A, const Operand& B, const CUt
 // wave; cudaErrorNotSupported = use the 256 x 256 split-K path. G: A operand (MN-major, m
 // wide), X: B operand (n wide); TRANS runs C = X^T G and stores C^T.
 // rq (optional): also quantize G row-wise inside the same launch (tc_dw_wide.cuh QV).
-cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, const CUtensorMap& td, int64_t m, int64_t n,
-                           int64_t T, const sb::RowQuant* rq, const sbdw::DMaps<8>* rs = nullptr) {
+// Co-resident pairs of the one-wave dW kernel on h's device (its smem attributes set once per
+// device context); <= 0 when the kernel is off (SB_DW_WIDE=0, 1-CTA path) or cannot launch.
+int dw_wide_pairs(sb_handle h) {
   static int env = -1;
   if (env < 0) env = getenv("SB_DW_WIDE") ? atoi(getenv("SB_DW_WIDE")) : 1;
-  if (!env || h->gemm_path == SB_GEMM_1CTA || h->num_sms < 2) return cudaErrorNotSupported;
-  // per device: the smem attribute and the co-resident pair count belong to the device context
+  if (!env || h->gemm_path == SB_GEMM_1CTA || h->num_sms < 2) return 0;
   static int max_pairs_d[16] = {};
   static cudaError_t attr_err_d[16] = {};
   static std::once_flag once_d[16];
@@ -443,7 +443,13 @@ cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, cons
     max_pairs = n_;
     cudaGetLastError();
   });
-  if (attr_err != cudaSuccess) return cudaErrorNotSupported;
+  return attr_err != cudaSuccess ? 0 : max_pairs;
+}
+
+cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, const CUtensorMap& td, int64_t m, int64_t n,
+                           int64_t T, const sb::RowQuant* rq, const sbdw::DMaps<8>* rs = nullptr) {
+  const int max_pairs = dw_wide_pairs(h);
+  if (max_pairs <= 0) return cudaErrorNotSupported;
   const int64_t u_direct = ((m + sbdw::WM - 1) / sbdw::WM) * ((n + sbdw::WN - 1) / sbdw::WN);
   const int64_t u_trans = ((n + sbdw::WM - 1) / sbdw::WM) * ((m + sbdw::WN - 1) / sbdw::WN);
   const bool trans = u_direct > max_pairs;
@@ -828,6 +834,20 @@ sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t 
                                                      n, m, n, b, dw, accumulate);
   SB_LAUNCH_CHECK(op);
   return SB_OK;
+}
+
+bool dw_wide_serves(sb_handle h, int64_t m, int64_t n, int64_t b) {
+  // the shape rule of launch_dw_wide (one orientation fits the co-resident pairs in one wave, and
+  // the 256 x 256 tiling would leave a partial wave), with the device's co-resident pair count
+  if (b <= 0 || b >= (1LL << 31) || m % 8 || n % 8) return false;
+  const int max_pairs = dw_wide_pairs(h);
+  if (max_pairs <= 0) return false;
+  const int64_t u_direct = ((m + sbdw::WM - 1) / sbdw::WM) * ((n + sbdw::WN - 1) / sbdw::WN);
+  const int64_t u_trans = ((n + sbdw::WM - 1) / sbdw::WM) * ((m + sbdw::WN - 1) / sbdw::WN);
+  const bool trans = u_direct > max_pairs;
+  if (trans && u_trans > max_pairs) return false;
+  const int64_t u256 = ((m + 255) / 256) * ((n + 255) / 256);
+  return !(u256 % max_pairs == 0 || (trans ? u_trans : u_direct) * 4 < max_pairs * 3);
 }
 
 sb_status wgrad_reduce_scatter(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m, int64_t n,

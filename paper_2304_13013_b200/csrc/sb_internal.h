@@ -197,6 +197,8 @@ sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t 
 // before this call on every rank) first.
 sb_status wgrad_reduce_scatter(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m, int64_t n,
                                float* dw, const sb_symbuf& sym, const RowQuant* rq);
+// True when the one-wave dW kernel (and so wgrad_reduce_scatter) serves an m x n dW over b tokens.
+bool dw_wide_serves(sb_handle h, int64_t m, int64_t n, int64_t b);
 sb_status matmul_f32_seq(sb_handle h, const float* a, int64_t a_rs, int64_t a_ks, const float* bt, int64_t b_rs,
                          int64_t b_ks, int64_t r, int64_t c, int64_t k, float* y, int accumulate);
 sb_status gemm_bf16_tc(sb_handle h, const void* a, bool a_mn, const void* b, bool b_mn, int64_t M, int64_t N, int64_t K,

@@ -112,3 +112,30 @@ def test_two_processes_one_gpu_reduce_scatter(tmp_path, m, n):
         outs.append((p.returncode, out))
     for rc, out in outs:
         assert rc == 0, out[-3000:]
+
+
+@pytest.mark.parametrize("m,n", [(1280, 1280), (3840, 1280)])
+def test_fused_allreduce_every_layer_shape(m, n):
+    """sb_dp_wgrad_allreduce_fused serves every ViT-H dW shape: the out-projection (1280 x 1280) is
+    not a one-wave shape and takes the local GEMM + all-reduce form, qkv (3840 x 1280) the fused
+    reduce-scatter epilogue; both equal the plain dW (one rank), G's payload equal to
+    quantize_rowwise(G)."""
+    T = 16384
+    torch.manual_seed(m)
+    g = torch.randn(T, m, device="cuda").bfloat16()
+    x = torch.randn(T, n, device="cuda").bfloat16()
+    h = A.handle(0)
+    buf = dp.SymmetricBuffer(h, 4 * m * n)
+    try:
+        dw = buf.view((m, n))
+        gq = torch.empty(T, m, dtype=torch.int8, device="cuda")
+        gs = torch.empty(T, dtype=torch.float32, device="cuda")
+        A.check(h.lib.sb_dp_wgrad_allreduce_fused(h.h, L._p(g), L._p(x), A.SB_BF16, T, m, n, L._p(dw), L._p(gq), m,
+                                                  L._p(gs)))
+        ref = L.wgrad(g, x)
+        q = L.quantize_rowwise(g)
+        torch.cuda.synchronize()
+        assert torch.equal(dw, ref)
+        assert torch.equal(gq, q.payload) and torch.equal(gs, q.state)
+    finally:
+        buf.close()
