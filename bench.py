@@ -568,9 +568,12 @@ def run_ours(args):
 
     yard = cublas_yardstick(torch, layers, T, args) if rank == 0 else None
     e2e = None
-    if rank == 0 and not args.no_e2e and args.config == "c2":
-        e2e = e2e_host(args, L, torch)
-        e2e["per_linear_entry"] = e2e_host_per_linear(args, L, torch)
+    if not args.no_e2e and args.config == "c2":
+        # every rank drives its own shard through the host entry (dW summed over ranks inside it
+        # when the library communicator is up); whole-job rate = all tokens / slowest rank
+        e2e = e2e_host(args, L, torch, world=world, dev=dev)
+        if rank == 0 and world == 1:
+            e2e["per_linear_entry"] = e2e_host_per_linear(args, L, torch)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and args.config == "c2":
         r, cores, sample, kind = cpu_reference_rate()
@@ -909,11 +912,14 @@ def cpu_optimizer_rate(budget_s: float = 10.0):
                       "lowprec::optimizer_step (single-threaded as the reference)"}
 
 
-def e2e_host(args, L, torch):
+def e2e_host(args, L, torch, world=1, dev=None):
     """Same workload (the chained C2 MLP block) through the C-ABI host-buffer entry
     sb_switchback_mlp_fwd_bwd_host: pinned host X, W1, W2, G in; Y, dX, dW1, dW2 out, every
-    step; the hidden activation and its gradient stay on the device (as in the device step)."""
+    step; the hidden activation and its gradient stay on the device (as in the device step).
+    N > 1: every rank runs its shard concurrently (its own GPU and PCIe link), dW summed over the
+    ranks inside the call; the time is the max over ranks."""
     from paper_2304_13013_b200 import _capi as A
+    from paper_2304_13013_b200 import dp
 
     T = args.tokens
     (_, n, hd), (_, _, m) = LAYERS
@@ -928,17 +934,20 @@ def e2e_host(args, L, torch):
         L.switchback_mlp_fwd_bwd_host(x, w1, w2, gg, A.SB_ACT_NONE)
     steps = max(1, min(args.steps, 10))
     torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         L.switchback_mlp_fwd_bwd_host(x, w1, w2, gg, A.SB_ACT_NONE)  # returns after Y, dX, dW1, dW2 are on the host
     torch.cuda.synchronize()
-    dt = (time.perf_counter() - t0) / steps
-    return {"value": T / dt, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+    dt = dp.max_over_ranks((time.perf_counter() - t0) / steps, dev)
+    return {"value": T * world / dt, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ranks": world,
             "path": "sb_switchback_mlp_fwd_bwd_host (C-ABI, pinned host buffers, 8192-token chunks: H2D / kernels / "
                     "D2H overlapped on three streams, hidden activation kept in HBM), one synchronous call per step",
             "pcie_note": "H2D and D2H share the link: ~93 GB/s combined measured (tools/pcie_bw.py), so the "
                          "752 MB of host traffic per step has an ~8.1 ms floor",
-            "steps": steps}
+            "bytes_note": "h2d / d2h bytes are per rank and step", "steps": steps}
 
 
 def e2e_host_per_linear(args, L, torch):

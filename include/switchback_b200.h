@@ -340,7 +340,9 @@ typedef enum sb_activation { SB_ACT_NONE = 0, SB_ACT_GELU = 1 } sb_activation;
  * through (H2D | kernels | D2H overlapped), so PCIe carries only the block's inputs and outputs.
  * activation: SB_ACT_NONE (the two linears back to back) or SB_ACT_GELU (bf16, not exact;
  * gelu(double) rounded to float as model.cpp:327, fused into the quantize kernels). Y and dX
- * are per-row and bit-identical to the device-resident path; dw1 / dw2 sum the chunks in order. */
+ * are per-row and bit-identical to the device-resident path; dw1 / dw2 sum the chunks in order.
+ * With a communicator on the handle (sb_dp_init, world > 1) each rank passes its own token shard
+ * and dw1 / dw2 come back summed over the ranks (NCCL all-reduce on the device before the copy). */
 sb_status sb_switchback_mlp_fwd_bwd_host(sb_handle h, const sb_linear_mode* mode, int activation, const void* x,
                                          const void* w1, const void* w2, const void* g, sb_dtype dt, int64_t b,
                                          int64_t n, int64_t hd, int64_t m, void* y, void* dx, float* dw1, float* dw2);

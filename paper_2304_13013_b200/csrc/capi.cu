@@ -1185,6 +1185,8 @@ static sb_status mlp_host_enqueue(sb_handle h, const sb_linear_mode* mode, int a
     const sb::RowQuant rq2{I8(GQ), m, F(GS)};
     if (st == SB_OK) st = sb::wgrad(h, gd, P[ACT], dt, rows, m, hd, F(DW2), mode->exact, i > 0, &rq2);
     const bool last = i == nchunks - 1;
+    // under data parallelism (a communicator on the handle) dW is summed over ranks before it leaves
+    if (last && st == SB_OK) st = sb::dp_allreduce_sum_f32(h, F(DW2), m * hd, comp);
     if (last) cudaEventRecord(ev_comp[(s + 1) % NS], comp);  // dW2 complete (that slot's event is not waited on again)
     if (st == SB_OK) st = sb::gemm_i8(h, I8(GQ), F(GS), I8(W2QT), F(WST2), SB_SCALE_ROW_TENSOR, rows, hd, m, P[DA], dt, mode->exact);
     if (gelu) {
@@ -1207,6 +1209,7 @@ static sb_status mlp_host_enqueue(sb_handle h, const sb_linear_mode* mode, int a
     cudaEventRecord(ev_out[s], s_out);
   }
   // as fwd_bwd_host_enqueue: dW1 leaves after the last chunk; the event frees the pool
+  if (st == SB_OK) st = sb::dp_allreduce_sum_f32(h, F(DW1), hd * n, comp);
   cudaEventRecord(ev_comp[0], comp);
   cudaStreamWaitEvent(s_out, ev_comp[0], 0);
   cudaMemcpyAsync(dw1, P[DW1], hd * n * sizeof(float), cudaMemcpyDeviceToHost, s_out);

@@ -143,6 +143,14 @@ void dp_owned_rows(int64_t rows, int rank, int world, int64_t* r0, int64_t* r1) 
   *r1 = std::min<int64_t>(rows, 32 * first_block(rank + 1));
 }
 
+sb_status dp_allreduce_sum_f32(sb_handle h, float* buf, int64_t n, cudaStream_t stream) {
+  const char* op = "dp_allreduce";
+  if (!h->dp_comm || h->dp_world <= 1 || n <= 0) return SB_OK;
+  SB_NCCL(op, nccl().allReduce(buf, buf, static_cast<size_t>(n), ncclFloat32, ncclSum,
+                               static_cast<ncclComm_t>(h->dp_comm), stream));
+  return SB_OK;
+}
+
 void dp_free_symmetric(sb_handle h) {
   for (sb_symbuf& s : h->sym) {
     for (int r = 0; r < s.world; ++r)

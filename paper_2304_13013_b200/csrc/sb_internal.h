@@ -213,6 +213,9 @@ const sb_symbuf* find_symbuf(sb_handle h, const void* p, size_t bytes);
 // Rows [r0, r1) of a rows-row dW owned by `rank` in the fused reduce-scatter: 32-row blocks,
 // block rb owned by rank (rb * world) / nblocks (contiguous, sizes differ by at most one block).
 void dp_owned_rows(int64_t rows, int rank, int world, int64_t* r0, int64_t* r1);
+// Sum all-reduce of n fp32 values in place on `stream` over the handle's communicator (no-op
+// without one, or with one rank).
+sb_status dp_allreduce_sum_f32(sb_handle h, float* buf, int64_t n, cudaStream_t stream);
 // Close every peer mapping and free every symmetric buffer of the handle (sb_destroy).
 void dp_free_symmetric(sb_handle h);
 // True when the handle has a communicator of more than one rank (or SB_DP_FORCE=1 with one rank,
