@@ -13,7 +13,7 @@ extern "C" void sb_trace_read(long long* out) { cudaMemcpyFromSymbol(out, sbtc::
 extern "C" void sb_probe_read(unsigned long long* out, int n) { cudaMemcpyFromSymbol(out, sbtc::g_probe, n * 8); }
 extern "C" void sb_probe_reset() { static unsigned long long z[1024 * 6] = {0}; cudaMemcpyToSymbol(sbtc::g_probe, z, sizeof(z)); }
 EOG
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -rdc=true --fmad=false -DSB_GEMM_PROBE -I "$ROOT/include" -I "$C" \
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -rdc=true --fmad=false -DSB_GEMM_PROBE $EXTRA -I "$ROOT/include" -I "$C" \
   "$C/quantize.cu" "$C/gemm.cu" "$C/optim.cu" "$C/capi.cu" "$C/util.cu" "$C/dp.cu" "$ROOT/build/probe/probe_glue.cu" \
-  "$ROOT/tools/gemm_probe.cu" -o "$ROOT/build/gemm_probe" -ldl -lcuda
+  "$ROOT/tools/gemm_probe.cu" -o "$ROOT/build/gemm_probe$SUFFIX" -ldl -lcuda
 echo built build/gemm_probe
