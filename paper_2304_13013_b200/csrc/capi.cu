@@ -267,6 +267,7 @@ sb_status sb_destroy(sb_handle h) {
   for (auto& kv : h->scratch)
     if (kv.second.first) cudaFree(kv.second.first);
   if (h->capture_scratch) cudaFree(h->capture_scratch);
+  if (h->cast_buf) cudaFree(h->cast_buf);
   for (int i = 0; i < 2; ++i) {
     if (h->dev_pool[i]) cudaFree(h->dev_pool[i]);
     if (h->pool_done[i]) cudaEventDestroy(h->pool_done[i]);

@@ -55,6 +55,8 @@ struct sb_handle_s {
   cudaEvent_t dp_ready = nullptr, dp_done = nullptr;
   bool dp_pending = false;
   float* dp_token = nullptr;  // one device float: the payload of sb_dp_barrier's all-reduce
+  void* cast_buf = nullptr;   // bf16 copies of fp32 G / X for the 16-bit dW (grown outside capture)
+  size_t cast_bytes = 0;
   std::vector<sb_symbuf> sym;  // symmetric buffers (sb_dp_symmetric_alloc)
 };
 
@@ -171,6 +173,8 @@ cudaError_t launch_add_residual(sb_handle h, void* y, sb_dtype dt, int64_t rows,
 // y[r, c] += bias[c] in place (y is SB_F32 or SB_BF16, rows x cols contiguous)
 cudaError_t launch_add_bias(sb_handle h, void* y, sb_dtype dt, int64_t rows, int64_t cols, const float* bias);
 cudaError_t launch_fp8_cast(sb_handle h, const float* x, int64_t n, int fmt, float* y);
+// b[i] = bf16(a[i]) (RNE), contiguous n elements (a 16-byte aligned for the vector path)
+cudaError_t launch_f32_to_bf16(sb_handle h, const float* a, int64_t n, void* b);
 
 // gemm_i8.cu
 // bias (optional, fp32 [N]): fused into the tensor-core epilogue for bf16 / fp32 outputs,
