@@ -131,3 +131,16 @@ def test_argument_errors():
     with pytest.raises(A.SBError):  # GELU is the bf16 performance path only
         L.switchback_mlp_fwd_bwd_host(x.float().pin_memory(), w1.float().pin_memory(), w2.float().pin_memory(),
                                       g.float().pin_memory(), activation=A.SB_ACT_GELU, exact=True)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_unaligned_widths_take_the_fallback_kernels(dtype, chunk_env):
+    """Widths that are not TMA-legal (n, hidden, m not multiples of 16) run the SIMT fallbacks inside
+    the pipeline (several ragged chunks): Y / dX still equal the device-resident layer API."""
+    b, n, hd, m = 3000, 100, 72, 40
+    chunk_env(1024)
+    x, w1, w2, g = _inputs(b, n, hd, m, 8, dtype)
+    y, dx, dw1, dw2 = L.switchback_mlp_fwd_bwd_host(x, w1, w2, g)
+    yd, dxd, dw1d, dw2d = _device_mlp(x, w1, w2, g, False)
+    assert torch.equal(y, yd) and torch.equal(dx, dxd)
+    assert rel_err(dw1.numpy(), dw1d.numpy()) < 1e-4 and rel_err(dw2.numpy(), dw2d.numpy()) < 1e-4
