@@ -803,7 +803,12 @@ def run_vit_block(args):
 
         def forward(self, x):
             h = x if self.fused else self.ln1(x.float()).to(torch.bfloat16)
-            q, k, v = SplitQKV.apply(self.qkv(h))
+            if self.fused and not args.qkv_packed:
+                # q / k / v handed to attention as head views; their gradients come back through
+                # one pack + quantize kernel (SwitchBackLinear.qkv_heads)
+                q, k, v = self.qkv.qkv_heads(h, H)
+            else:
+                q, k, v = SplitQKV.apply(self.qkv(h))
             a = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(B, S, D)
             if self.fused and resid_fused:  # skip connections added in the out-proj / fc2 GEMM epilogues
                 x = self.out(a, residual=x)

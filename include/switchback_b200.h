@@ -270,6 +270,15 @@ sb_status sb_gelu_quantize_rowwise(sb_handle h, const void* pre, sb_dtype dt, in
 /* g = dact * gelu'(pre) as bf16 plus its row-wise int8 payload and states. */
 sb_status sb_gelu_backward_quantize_rowwise(sb_handle h, const void* dact, const void* pre, sb_dtype dt, int64_t rows,
                                             int64_t cols, void* g, int8_t* q, float* state);
+/* Producer fusion at the q/k/v projection's backward (model.cpp:303-305, 385-397): the attention
+ * gradients dq, dk, dv arrive head-major [B, H, S, Dh] (bf16; strides[3 i + 0/1/2] = element
+ * strides of b, h, s of tensor i; Dh contiguous). One pass writes the packed output gradient
+ * g [B S x 3 H Dh] that the grouped dW GEMM reads and, from the same registers, each projection's
+ * row-wise int8 payload q[i] [B S x H Dh] / states state[i] [B S] — equal to quantize_rowwise of
+ * g's column block i (the three per-projection quantizations of the grouped backward). */
+sb_status sb_heads_pack_quantize(sb_handle h, const void* const* dqkv, const int64_t* strides, int64_t B, int64_t S,
+                                 int H, int Dh, void* g, int8_t* const* q, float* const* state);
+
 /* out = LayerNorm(x) (over each row of cols; fp32 gamma, beta; bf16 x and out) with its row-wise
  * int8 payload and states, plus per-row mean and rstd (fp32) for the backward. Rows of up to
  * 2048 columns (multiple of 8); SB_ERR_UNSUPPORTED otherwise. */

@@ -46,6 +46,7 @@ EXPORTS = [
     "sb_dp_symmetric_free", "sb_dp_owned_rows", "sb_wgrad_reduce_scatter", "sb_dp_barrier", "sb_dp_allgather_rows",
     "sb_dp_wgrad_allreduce_fused", "sb_stableadamw_sharded_workspace_size", "sb_stableadamw_shard_phase1",
     "sb_stableadamw_shard_phase2", "sb_stableadamw_step_sharded", "sb_dp_allreduce_max_words",
+    "sb_heads_pack_quantize",
 ]
 
 
@@ -163,6 +164,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             "sb_dp_owned_rows": ([i64, i32, i32, C.POINTER(i64), C.POINTER(i64)], i32),
             "sb_wgrad_reduce_scatter": ([v, v, v, i32, i64, i64, i64, v, v, i64, v], i32),
             "sb_dp_barrier": ([v], i32),
+            "sb_heads_pack_quantize": ([v, v, v, i64, i64, i32, i32, v, v, v], i32),
             "sb_dp_allreduce_max_words": ([v, v, i32], i32),
             "sb_stableadamw_sharded_workspace_size": ([C.POINTER(AdamwTensor), i32, C.POINTER(sz)], i32),
             "sb_stableadamw_shard_phase1": ([v, C.POINTER(AdamwTensor), v, i32, C.POINTER(AdamwHparams), i64, v, v,

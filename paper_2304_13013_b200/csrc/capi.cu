@@ -267,7 +267,6 @@ sb_status sb_destroy(sb_handle h) {
   for (auto& kv : h->scratch)
     if (kv.second.first) cudaFree(kv.second.first);
   if (h->capture_scratch) cudaFree(h->capture_scratch);
-  if (h->cast_buf) cudaFree(h->cast_buf);
   for (int i = 0; i < 2; ++i) {
     if (h->dev_pool[i]) cudaFree(h->dev_pool[i]);
     if (h->pool_done[i]) cudaEventDestroy(h->pool_done[i]);
@@ -815,6 +814,21 @@ sb_status sb_gelu_backward_quantize_rowwise(sb_handle h, const void* dact, const
     return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument (bf16 only)");
   if (rows <= 0 || cols <= 0) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "empty matrix");
   SB_TRYC(op, sb::launch_act_quantize_rowwise(h, 1, dact, pre, rows, cols, g, q, state));
+  return SB_OK;
+}
+
+sb_status sb_heads_pack_quantize(sb_handle h, const void* const* dqkv, const int64_t* strides, int64_t B, int64_t S,
+                                 int H, int Dh, void* g, int8_t* const* q, float* const* state) {
+  const char* op = "heads_pack_quantize";
+  SB_TRY(check_h(h, op));
+  if (!dqkv || !strides || !g || !q || !state || B <= 0 || S <= 0 || H <= 0 || Dh <= 0)
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  for (int i = 0; i < 3; ++i)
+    if (!dqkv[i] || !q[i] || !state[i]) return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument");
+  const cudaError_t e = sb::launch_heads_pack_quantize(h, dqkv, strides, B, S, H, Dh, g, q, state);
+  if (e == cudaErrorNotSupported)
+    return sb::fail(SB_ERR_UNSUPPORTED, op, "bf16, H * Dh <= 2048, Dh % 8 == 0, 16-byte aligned heads");
+  SB_TRYC(op, e);
   return SB_OK;
 }
 

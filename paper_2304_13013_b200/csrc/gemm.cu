@@ -754,44 +754,6 @@ sb_status matmul_f32_seq(sb_handle h, const float* a, int64_t a_rs, int64_t a_ks
 sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m, int64_t n, float* dw,
                 int exact, int accumulate, const RowQuant* rq) {
   const char* op = "linear_backward";
-  // fp32 I/O on the performance path: SwitchBack's 16-bit weight gradient — G and X rounded to
-  // bf16 once (one cast pass each), then the bf16 tensor-core dW; G's row-wise payload (if asked)
-  // from the fp32 G itself. exact = 1 keeps the reference's sequential fp32 product.
-  if (dt == SB_F32 && !exact && m % 8 == 0 && n % 8 == 0 && aligned(g, 16) && aligned(x, 16) && aligned(dw, 16) &&
-      b < (1LL << 31) && get_encode() != nullptr) {
-    const size_t gb = static_cast<size_t>(b) * m * 2, xb = static_cast<size_t>(b) * n * 2;
-    const size_t need = ((gb + 255) & ~size_t(255)) + xb;
-    bool ok = need <= h->cast_bytes;
-    if (!ok) {
-      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-      cudaStreamIsCapturing(h->stream, &cs);
-      if (cs == cudaStreamCaptureStatusNone) {  // no allocation while capturing (the SIMT path runs then)
-        if (h->cast_buf) {
-          cudaStreamSynchronize(h->stream);
-          cudaFree(h->cast_buf);
-        }
-        h->cast_buf = nullptr;
-        h->cast_bytes = 0;
-        if (cudaMalloc(&h->cast_buf, need) == cudaSuccess) {
-          h->cast_bytes = need;
-          ok = true;
-        }
-        cudaGetLastError();
-      }
-    }
-    if (ok) {
-      void* g16 = h->cast_buf;
-      void* x16 = static_cast<uint8_t*>(h->cast_buf) + ((gb + 255) & ~size_t(255));
-      if (rq) {
-        const cudaError_t qe = launch_quantize_rowwise(h, g, dt, b, m, m, rq->q, rq->ldq, rq->state);
-        if (qe != cudaSuccess) return cuda_fail(op, qe);
-      }
-      cudaError_t e = launch_f32_to_bf16(h, static_cast<const float*>(g), b * m, g16);
-      if (e == cudaSuccess) e = launch_f32_to_bf16(h, static_cast<const float*>(x), b * n, x16);
-      if (e != cudaSuccess) return cuda_fail(op, e);
-      return wgrad(h, g16, x16, SB_BF16, b, m, n, dw, 0, accumulate, nullptr);
-    }
-  }
   CUtensorMap td;
   // a fused row-wise quantize of G rides in the one-wave dW kernel (bf16 G, 16-byte rows);
   // anywhere else it is the standalone quantizer, launched first

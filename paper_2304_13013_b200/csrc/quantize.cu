@@ -509,6 +509,75 @@ __device__ __forceinline__ void ln_row(uint4 (&v)[VPL], int64_t row, int nvec, i
     }
 }
 
+// ---- producer fusion: attention gradients -> the q/k/v projection's packed G + its quantize --
+// The grouped q/k/v linear (three projections of one input, model.cpp:303-305) gets its output
+// gradients from attention as three head-major tensors dq, dk, dv [B, H, S, Dh] (any strides, Dh
+// contiguous). One warp per (token row t = b S + s, projection i): gather the row's H x Dh values
+// (the layout change a torch caller does with three strided copies), write them into the packed
+// G [T x 3D] the dW GEMM reads, and quantize them row-wise from the same registers into the
+// projection's payload q_i [T x D] / states s_i [T] — equal to quantize_rowwise(G[:, iD:(i+1)D]).
+struct HeadsSrc {
+  const __nv_bfloat16* p[3];
+  int64_t sb[3], sh[3], ss[3];  // element strides of b, h, s (Dh stride 1)
+  int8_t* q[3];
+  float* st[3];
+};
+
+template <int VPL>
+__global__ void __launch_bounds__(256) k_heads_pack_quantize(const __grid_constant__ HeadsSrc src, int64_t S, int H,
+                                                             int Dh, int64_t T, __nv_bfloat16* __restrict__ g,
+                                                             uint32_t* err) {
+  using T16 = __nv_bfloat16;
+  using Out = typename VecQ<T16>::Out;
+  const int lane = threadIdx.x & 31;
+  const int D = H * Dh, nvec = D / 8, vph = Dh / 8;  // 16-byte vectors per row / per head
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t w = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); w < 3 * T; w += warps) {
+    const int i = static_cast<int>(w % 3);
+    const int64_t t = w / 3, b = t / S, s = t - b * S;
+    const T16* base = src.p[i] + b * src.sb[i] + s * src.ss[i];
+    uint4 v[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int k = j * 32 + lane;
+      if (k < nvec) {
+        const int hh = k / vph, wi = k - hh * vph;
+        v[j] = ld_stream(reinterpret_cast<const uint4*>(base + hh * src.sh[i] + wi * 8));
+      } else {
+        v[j] = make_uint4(0, 0, 0, 0);
+      }
+    }
+    uint4* grow = reinterpret_cast<uint4*>(g + t * 3 * D + i * D);
+    uint32_t amax = 0;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int k = j * 32 + lane;
+      if (k < nvec) grow[k] = v[j];
+      amax = max(amax, vec_absmax_bits<T16>(v[j]));
+    }
+    amax = __reduce_max_sync(0xffffffffu, amax);
+    if (amax >= kNonFiniteBits) {
+      if (lane == 0) {
+        raise_nonfinite(err);
+        src.st[i][t] = __uint_as_float(amax);
+      }
+      continue;
+    }
+    const float stv = state_from_bits(amax);
+    if (lane == 0) src.st[i][t] = stv;
+    const Scale sc = make_scale(stv);
+    const bool plain = sc.pre == 1.0f;
+    Out* qr = reinterpret_cast<Out*>(src.q[i] + t * D);
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      if (j * 32 >= nvec) break;  // warp-uniform (qvec votes across the warp)
+      const int k = j * 32 + lane;
+      const Out o = qvec<T16>(v[j], sc, plain);
+      if (k < nvec) qr[k] = o;
+    }
+  }
+}
+
 // Two rows per warp step: both rows' loads are issued before either row's math.
 template <int VPL>
 __global__ void __launch_bounds__(256, 2) k_ln_quantize_rows(const __nv_bfloat16* __restrict__ x, int64_t rows, int nvec,
@@ -1956,6 +2025,38 @@ cudaError_t build_gelu_lut(sb_handle h) {
   }
   h->gelu_lut = p;
   return cudaSuccess;
+}
+
+cudaError_t launch_heads_pack_quantize(sb_handle h, const void* const* src, const int64_t* strides, int64_t B,
+                                       int64_t S, int H, int Dh, void* g, int8_t* const* q, float* const* st) {
+  const int D = H * Dh;
+  if (Dh % 8 || D > 2048 || B <= 0 || S <= 0 || !sb::aligned(g, 16)) return cudaErrorNotSupported;
+  HeadsSrc hs{};
+  for (int i = 0; i < 3; ++i) {
+    hs.p[i] = static_cast<const __nv_bfloat16*>(src[i]);
+    hs.sb[i] = strides[3 * i];
+    hs.sh[i] = strides[3 * i + 1];
+    hs.ss[i] = strides[3 * i + 2];
+    hs.q[i] = q[i];
+    hs.st[i] = st[i];
+    if (!sb::aligned(src[i], 16) || hs.sb[i] % 8 || hs.sh[i] % 8 || hs.ss[i] % 8 || !sb::aligned(q[i], 8))
+      return cudaErrorNotSupported;
+  }
+  const int64_t T = B * S;
+  const int vpl = (D / 8 + 31) / 32;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>((3 * T + 7) / 8, 8LL * h->num_sms));
+  h->launches++;
+  switch (vpl) {
+    case 1: k_heads_pack_quantize<1><<<grid, 256, 0, h->stream>>>(hs, S, H, Dh, T, static_cast<__nv_bfloat16*>(g), h->d_err); break;
+    case 2: k_heads_pack_quantize<2><<<grid, 256, 0, h->stream>>>(hs, S, H, Dh, T, static_cast<__nv_bfloat16*>(g), h->d_err); break;
+    case 3: k_heads_pack_quantize<3><<<grid, 256, 0, h->stream>>>(hs, S, H, Dh, T, static_cast<__nv_bfloat16*>(g), h->d_err); break;
+    case 4: k_heads_pack_quantize<4><<<grid, 256, 0, h->stream>>>(hs, S, H, Dh, T, static_cast<__nv_bfloat16*>(g), h->d_err); break;
+    case 5: k_heads_pack_quantize<5><<<grid, 256, 0, h->stream>>>(hs, S, H, Dh, T, static_cast<__nv_bfloat16*>(g), h->d_err); break;
+    case 6: k_heads_pack_quantize<6><<<grid, 256, 0, h->stream>>>(hs, S, H, Dh, T, static_cast<__nv_bfloat16*>(g), h->d_err); break;
+    case 7: k_heads_pack_quantize<7><<<grid, 256, 0, h->stream>>>(hs, S, H, Dh, T, static_cast<__nv_bfloat16*>(g), h->d_err); break;
+    default: k_heads_pack_quantize<8><<<grid, 256, 0, h->stream>>>(hs, S, H, Dh, T, static_cast<__nv_bfloat16*>(g), h->d_err); break;
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_act_quantize_rowwise(sb_handle h, int mode, const void* a, const void* b, int64_t rows, int64_t cols,

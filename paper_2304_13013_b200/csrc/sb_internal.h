@@ -55,8 +55,6 @@ struct sb_handle_s {
   cudaEvent_t dp_ready = nullptr, dp_done = nullptr;
   bool dp_pending = false;
   float* dp_token = nullptr;  // one device float: the payload of sb_dp_barrier's all-reduce
-  void* cast_buf = nullptr;   // bf16 copies of fp32 G / X for the 16-bit dW (grown outside capture)
-  size_t cast_bytes = 0;
   std::vector<sb_symbuf> sym;  // symmetric buffers (sb_dp_symmetric_alloc)
 };
 
@@ -168,13 +166,17 @@ cudaError_t launch_ln_quantize_rowwise(sb_handle h, const void* x, int64_t rows,
 // mode 1 act = a * gelu'(b); writes act and the int8 payload / states of act.
 cudaError_t launch_act_quantize_rowwise(sb_handle h, int mode, const void* a, const void* b, int64_t rows, int64_t cols,
                                         void* act, int8_t* q, float* state);
+// Attention gradients dq / dk / dv [B, H, S, Dh] (bf16, element strides (b, h, s) per tensor in
+// `strides`, Dh contiguous) -> packed G [B S x 3 H Dh] and the row-wise int8 payload / states of
+// each projection's column block (q[i] [B S x H Dh], st[i] [B S]); cudaErrorNotSupported for
+// H Dh > 2048, Dh % 8, or unaligned operands.
+cudaError_t launch_heads_pack_quantize(sb_handle h, const void* const* src, const int64_t* strides, int64_t B,
+                                       int64_t S, int H, int Dh, void* g, int8_t* const* q, float* const* st);
 // y[r, c] += resid[r, c] in place (y, resid bf16 / fp32 of dt, rows x cols contiguous)
 cudaError_t launch_add_residual(sb_handle h, void* y, sb_dtype dt, int64_t rows, int64_t cols, const void* resid);
 // y[r, c] += bias[c] in place (y is SB_F32 or SB_BF16, rows x cols contiguous)
 cudaError_t launch_add_bias(sb_handle h, void* y, sb_dtype dt, int64_t rows, int64_t cols, const float* bias);
 cudaError_t launch_fp8_cast(sb_handle h, const float* x, int64_t n, int fmt, float* y);
-// b[i] = bf16(a[i]) (RNE), contiguous n elements (a 16-byte aligned for the vector path)
-cudaError_t launch_f32_to_bf16(sb_handle h, const float* a, int64_t n, void* b);
 
 // gemm_i8.cu
 // bias (optional, fp32 [N]): fused into the tensor-core epilogue for bf16 / fp32 outputs,

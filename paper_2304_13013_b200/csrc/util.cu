@@ -1,4 +1,3 @@
-#include <algorithm>
 #include <cstdlib>
 // util.cu — the remaining C-ABI entries: device memory + copies for FFI callers, the
 // device finiteness check (Matrix::all_finite), fp8_cast, the int8 payload transpose, and the
@@ -284,38 +283,7 @@ sb_status sb_filter_nonfinite(sb_handle h, const float* const* grads, float* con
 
 }  // extern "C"
 
-namespace {
-// fp32 -> bf16 (RNE), 8 elements per thread step (two float4 in, one uint4 out)
-__global__ void k_f32_to_bf16(const float* __restrict__ a, __nv_bfloat16* __restrict__ b, int64_t n) {
-  const int64_t n8 = n / 8;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const float4 x = __ldcs(reinterpret_cast<const float4*>(a) + 2 * i);
-    const float4 y = __ldcs(reinterpret_cast<const float4*>(a) + 2 * i + 1);
-    const __nv_bfloat162 p0 = __floats2bfloat162_rn(x.x, x.y), p1 = __floats2bfloat162_rn(x.z, x.w);
-    const __nv_bfloat162 p2 = __floats2bfloat162_rn(y.x, y.y), p3 = __floats2bfloat162_rn(y.z, y.w);
-    uint4 o;
-    o.x = *reinterpret_cast<const uint32_t*>(&p0);
-    o.y = *reinterpret_cast<const uint32_t*>(&p1);
-    o.z = *reinterpret_cast<const uint32_t*>(&p2);
-    o.w = *reinterpret_cast<const uint32_t*>(&p3);
-    reinterpret_cast<uint4*>(b)[i] = o;
-  }
-  for (int64_t i = n8 * 8 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    b[i] = __float2bfloat16_rn(a[i]);
-}
-}  // namespace
-
 namespace sb {
-cudaError_t launch_f32_to_bf16(sb_handle h, const float* a, int64_t n, void* b) {
-  if (n <= 0) return cudaSuccess;
-  const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n / 8 + 255) / 256 + 1, 8LL * h->num_sms));
-  h->launches++;
-  k_f32_to_bf16<<<grid, 256, 0, h->stream>>>(a, static_cast<__nv_bfloat16*>(b), n);
-  return cudaGetLastError();
-}
-
 bool pdl_enabled() {
   static int v = -1;
   if (v < 0) {

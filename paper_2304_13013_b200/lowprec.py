@@ -138,6 +138,32 @@ def gelu_backward_quantize_rowwise(dact: torch.Tensor, pre: torch.Tensor,
     return g, QuantizedMatrix(q, st, ROW)
 
 
+def heads_pack_quantize(dq: torch.Tensor, dk: torch.Tensor, dv: torch.Tensor, check: bool = True):
+    """sb_heads_pack_quantize: attention gradients [B, H, S, Dh] (bf16, Dh contiguous) -> the
+    packed q/k/v output gradient G [B*S, 3*H*Dh] and each projection's row-wise int8 payload /
+    states (== quantize_rowwise(G[:, i*D:(i+1)*D])) from one pass. Returns (G, [QuantizedMatrix]*3)."""
+    _need_cuda(dq, dk, dv)
+    B, H, S, Dh = dq.shape
+    ts = []
+    for t in (dq, dk, dv):
+        if t.shape != (B, H, S, Dh) or t.dtype != torch.bfloat16:
+            raise InvalidArgument(A.SB_ERR_INVALID_ARGUMENT, "heads_pack_quantize: three bf16 [B, H, S, Dh] tensors")
+        ts.append(t if t.stride(3) == 1 else t.contiguous())
+    D = H * Dh
+    dev = dq.device
+    g = torch.empty((B * S, 3 * D), dtype=torch.bfloat16, device=dev)
+    qs = [torch.empty((B * S, D), dtype=torch.int8, device=dev) for _ in range(3)]
+    sts = [torch.empty(B * S, dtype=torch.float32, device=dev) for _ in range(3)]
+    srcs = (C.c_void_p * 3)(*[t.data_ptr() for t in ts])
+    strides = (C.c_int64 * 9)(*[v for t in ts for v in (t.stride(0), t.stride(1), t.stride(2))])
+    qp = (C.c_void_p * 3)(*[q.data_ptr() for q in qs])
+    sp = (C.c_void_p * 3)(*[x.data_ptr() for x in sts])
+    h = A.handle(dev.index)
+    A.check(h.lib.sb_heads_pack_quantize(h.h, srcs, strides, B, S, H, Dh, _p(g), qp, sp))
+    _check_nonfinite(h, check)
+    return g, [QuantizedMatrix(q, st, ROW) for q, st in zip(qs, sts)]
+
+
 def layernorm_quantize_rowwise(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps: float = 1e-5,
                                check: bool = True):
     """Producer fusion: out = LayerNorm(x) (bf16, fp32 affine) and quantize_rowwise(out) from

@@ -95,6 +95,21 @@ class SwitchBackLinear(torch.nn.Module):
             y = _SwitchBackLinearFn.apply(x2d, self.weight, self.bias, self.mode, r2d)
         return y.reshape(*shape[:-1], self.out_features)
 
+    def qkv_heads(self, x: torch.Tensor, heads: int):
+        """The grouped q/k/v projection (groups = 3) for attention: x [B, S, in] -> q, k, v as
+        [B, heads, S, Dh] views of the packed output; their gradients go straight into the fused
+        pack + quantize kernel (_QKVHeadsFn)."""
+        if self.groups != 3:
+            raise ValueError("qkv_heads: a groups=3 SwitchBackLinear")
+        B, S = x.shape[0], x.shape[1]
+        x2d = x.reshape(-1, self.in_features)
+        n = self.norm
+        ln_ok = n is not None and x.dtype == torch.bfloat16 and _ln_fusable(self.in_features)
+        if n is not None and not ln_ok:
+            x2d, n = n(x2d.float()).to(x2d.dtype), None
+        return _QKVHeadsFn.apply(x2d, n.weight if n is not None else None, n.bias if n is not None else None,
+                                 n.eps if n is not None else 0.0, self.weight, self.bias, B, S, heads)
+
     def extra_repr(self) -> str:
         return (f"in_features={self.in_features}, out_features={self.out_features}, bias={self.bias is not None}"
                 + (f", groups={self.groups}" if self.groups > 1 else ""))
@@ -146,6 +161,54 @@ class _LNLinearFn(torch.autograd.Function):
         return dx, dg, dbeta, None, dw, db, None, (g if ctx.needs_input_grad[7] else None)
 
 
+def _grouped_forward(ctx, x2d, ln_w, ln_b, eps, weight, bias, groups, resid=None):
+    x2d = x2d.contiguous()
+    dt = x2d.dtype
+    if ln_w is not None:
+        h, hq, mean, rstd = L.layernorm_quantize_rowwise(x2d, ln_w.detach(), ln_b.detach(), eps, check=False)
+        ln_state = (x2d, mean, rstd)
+    else:
+        h, hq, ln_state = x2d, L.quantize_rowwise(x2d, check=False), None
+    m, n = weight.shape
+    mg = m // groups
+    w = weight.detach().to(dt).contiguous()
+    wq = torch.empty((m, n), dtype=torch.int8, device=w.device)
+    scale = torch.empty(m, dtype=torch.float32, device=w.device)
+    wts = []
+    for i in range(groups):
+        q, qt = L.quantize_tensorwise(w[i * mg:(i + 1) * mg], check=False, with_transpose=True)
+        wq[i * mg:(i + 1) * mg] = q.payload
+        scale[i * mg:(i + 1) * mg] = q.state.expand(mg)
+        wts.append(qt)
+    y = L.int8_gemm_epilogue(hq, L.QuantizedMatrix(wq, scale, L.ROW), out_dtype=dt,
+                             bias=bias.detach().float().contiguous() if bias is not None else None,
+                             residual=resid.detach() if resid is not None else None)
+    ctx.state = (h, wts, ln_state, groups)
+    ctx.ln = (ln_w, ln_b)
+    ctx.has_bias = bias is not None
+    return y
+
+
+def _grouped_backward(ctx, g, gqs=None):
+    """dX = sum_i dequant(qrow(G_i) . W_i^T-payload) through the residual epilogue, one dW GEMM over
+    the packed G; gqs: the groups' row-wise payloads when a producer already made them."""
+    h, wts, ln_state, groups = ctx.state
+    g = g.contiguous()
+    mg = g.shape[1] // groups
+    dx = None
+    for i, wt in enumerate(wts):
+        gq = gqs[i] if gqs is not None else L.quantize_rowwise(g[:, i * mg:(i + 1) * mg], check=False)  # own row scales
+        dx = L.int8_gemm_epilogue(gq, wt, out_dtype=g.dtype, residual=dx)  # dX_0 + dX_1 + ... in order
+    dw = L.wgrad(g, h, exact=False)
+    db = g.sum(0, dtype=torch.float32) if ctx.has_bias and ctx.needs_input_grad[5] else None
+    dg = dbeta = None
+    if ln_state is not None:
+        x2d, mean, rstd = ln_state
+        dx, dg, dbeta = _ln_backward(dx, x2d, mean, rstd, *ctx.ln, ctx.needs_input_grad[:3])
+    ctx.state = None
+    return dx, dg, dbeta, dw, db
+
+
 class _GroupedLinearFn(torch.autograd.Function):
     """`groups` SwitchBack int8 linears of one input, each with its own tensor-wise W scale
     (model.cpp:303-305): the input's row-wise quantization once (fused with the LayerNorm when
@@ -156,49 +219,33 @@ class _GroupedLinearFn(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, x2d, ln_w, ln_b, eps, weight, bias, groups, resid=None):
-        x2d = x2d.contiguous()
-        dt = x2d.dtype
-        if ln_w is not None:
-            h, hq, mean, rstd = L.layernorm_quantize_rowwise(x2d, ln_w.detach(), ln_b.detach(), eps, check=False)
-            ln_state = (x2d, mean, rstd)
-        else:
-            h, hq, ln_state = x2d, L.quantize_rowwise(x2d, check=False), None
-        m, n = weight.shape
-        mg = m // groups
-        w = weight.detach().to(dt).contiguous()
-        wq = torch.empty((m, n), dtype=torch.int8, device=w.device)
-        scale = torch.empty(m, dtype=torch.float32, device=w.device)
-        wts = []
-        for i in range(groups):
-            q, qt = L.quantize_tensorwise(w[i * mg:(i + 1) * mg], check=False, with_transpose=True)
-            wq[i * mg:(i + 1) * mg] = q.payload
-            scale[i * mg:(i + 1) * mg] = q.state.expand(mg)
-            wts.append(qt)
-        y = L.int8_gemm_epilogue(hq, L.QuantizedMatrix(wq, scale, L.ROW), out_dtype=dt,
-                                 bias=bias.detach().float().contiguous() if bias is not None else None,
-                                 residual=resid.detach() if resid is not None else None)
-        ctx.state = (h, wts, ln_state, groups)
-        ctx.ln = (ln_w, ln_b)
-        ctx.has_bias = bias is not None
-        return y
+        return _grouped_forward(ctx, x2d, ln_w, ln_b, eps, weight, bias, groups, resid)
 
     @staticmethod
     def backward(ctx, g):
-        h, wts, ln_state, groups = ctx.state
-        g = g.contiguous()
-        mg = g.shape[1] // groups
-        dx = None
-        for i, wt in enumerate(wts):
-            gq = L.quantize_rowwise(g[:, i * mg:(i + 1) * mg], check=False)  # the group's own row scales
-            dx = L.int8_gemm_epilogue(gq, wt, out_dtype=g.dtype, residual=dx)  # dX_0 + dX_1 + ... in order
-        dw = L.wgrad(g, h, exact=False)
-        db = g.sum(0, dtype=torch.float32) if ctx.has_bias and ctx.needs_input_grad[5] else None
-        dg = dbeta = None
-        if ln_state is not None:
-            x2d, mean, rstd = ln_state
-            dx, dg, dbeta = _ln_backward(dx, x2d, mean, rstd, *ctx.ln, ctx.needs_input_grad[:3])
-        ctx.state = None
+        dx, dg, dbeta, dw, db = _grouped_backward(ctx, g)
         return dx, dg, dbeta, None, dw, db, None, (g if ctx.needs_input_grad[7] else None)
+
+
+class _QKVHeadsFn(torch.autograd.Function):
+    """The grouped q/k/v projection handing attention its heads: forward returns q, k, v as
+    [B, H, S, Dh] views of the packed output; backward receives the attention gradients in that
+    head-major layout and turns them into the packed G plus the three projections' row-wise
+    payloads in ONE kernel (sb_heads_pack_quantize) — the layout copy a caller would otherwise
+    make, with the quantization riding on it — then runs the grouped backward."""
+
+    @staticmethod
+    def forward(ctx, x2d, ln_w, ln_b, eps, weight, bias, B, S, H):
+        y = _grouped_forward(ctx, x2d, ln_w, ln_b, eps, weight, bias, 3)
+        ctx.heads = (B, S, H)
+        t = y.view(B, S, 3, H, y.shape[1] // (3 * H))
+        return tuple(t[:, :, i].transpose(1, 2) for i in range(3))
+
+    @staticmethod
+    def backward(ctx, dq, dk, dv):
+        g, gqs = L.heads_pack_quantize(dq, dk, dv, check=False)
+        dx, dg, dbeta, dw, db = _grouped_backward(ctx, g, gqs)
+        return dx, dg, dbeta, None, dw, db, None, None, None
 
 
 class _SwitchBackMLPFn(torch.autograd.Function):

@@ -197,23 +197,3 @@ def test_int8_simt_fallback_large_m_and_int64(M, N, K):
     if K <= 133144:
         raw = L.int8_matmul_dequant(A_, B_, out_dtype="raw")
         assert torch.equal(raw.double(), want)
-
-
-@pytest.mark.parametrize("m,n,T", [(1280, 1280, 16384), (5120, 1280, 8192), (96, 64, 1000)])
-def test_wgrad_fp32_performance_path_is_16bit(m, n, T):
-    """fp32 I/O, exact = 0: SwitchBack's 16-bit weight gradient — G and X rounded to bf16 once, the
-    bf16 tensor-core product — equals the bf16 path on the rounded operands bit for bit and the fp64
-    product within the bf16 input rounding; G's payload comes from the fp32 G itself."""
-    torch.manual_seed(m + n)
-    g = torch.randn(T, m, device="cuda")
-    x = torch.randn(T, n, device="cuda")
-    dw = L.wgrad(g, x, exact=False)
-    dw16 = L.wgrad(g.bfloat16(), x.bfloat16(), exact=False)
-    ref = (g.double().t() @ x.double()).float()
-    torch.cuda.synchronize()
-    assert torch.equal(dw, dw16)
-    assert ((dw - ref).norm() / ref.norm()).item() < 1e-2
-    dw2, gq = L.wgrad_quantize_rowwise(g, x, check=False)
-    q = L.quantize_rowwise(g)
-    assert torch.equal(dw2, dw)
-    assert torch.equal(gq.payload, q.payload) and torch.equal(gq.state, q.state)

@@ -310,3 +310,34 @@ def test_grouped_qkv_module_equals_three_linears(prenorm):
         assert rel(grp.weight.grad[i * D:(i + 1) * D], s.weight.grad) < 1e-5
         assert rel(grp.bias.grad[i * D:(i + 1) * D], s.bias.grad) < 1e-6
     assert rel(xg.grad.float(), xs.grad.float()) < 1e-2
+
+
+@pytest.mark.parametrize("prenorm", [False, True])
+def test_qkv_heads_matches_split_copies(prenorm):
+    """SwitchBackLinear.qkv_heads (q / k / v as head views, gradients packed + quantized by one kernel)
+    gives the same outputs and gradients, bit for bit, as the grouped linear followed by a
+    torch split / transpose (whose backward copies the heads into the packed G)."""
+    from paper_2304_13013_b200.nn import SwitchBackLinear
+
+    B, S, D, H = 3, 37, 256, 4
+    torch.manual_seed(4)
+    lin = SwitchBackLinear(D, 3 * D, device="cuda", prenorm=prenorm, groups=3)
+    with torch.no_grad():
+        lin.bias.normal_()
+    x0 = torch.randn(B, S, D, device="cuda").bfloat16()
+    gq, gk, gv = (torch.randn(B, H, S, D // H, device="cuda").bfloat16() for _ in range(3))
+
+    def run(fused):
+        lin.zero_grad(set_to_none=True)
+        x = x0.clone().requires_grad_(True)
+        if fused:
+            q, k, v = lin.qkv_heads(x, H)
+        else:
+            t = lin(x).view(B, S, 3, H, D // H)
+            q, k, v = (t[:, :, i].transpose(1, 2) for i in range(3))
+        ((q.float() * gq.float()).sum() + (k.float() * gk.float()).sum() + (v.float() * gv.float()).sum()).backward()
+        return [q.detach().clone(), x.grad.clone()] + [p.grad.clone() for p in lin.parameters()]
+
+    a, b = run(True), run(False)
+    for u, w in zip(a, b):
+        assert torch.equal(u, w)
