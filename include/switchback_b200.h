@@ -150,6 +150,12 @@ sb_status sb_dequantize_values(sb_handle h, const float* p, int64_t rows, int64_
 /* transpose_tensorwise's payload move (linear.cpp:170-189): out[cols x rows] = in[rows x cols]^T. */
 sb_status sb_transpose_i8(sb_handle h, const int8_t* in, int64_t rows, int64_t cols, int8_t* out);
 
+/* Bias gradient of the nn module's linears (no reference counterpart: the reference's linears
+ * carry no bias, model.cpp:324-329): out[c] = sum over rows of x[r, c] in fp32, x bf16 or fp32
+ * with leading dim ld >= cols. Deterministic (fixed split and summation order for a given shape
+ * and device); rows == 0 writes zeros. Uses the stream's internal scratch (<= 1 MB). */
+sb_status sb_column_sums(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ld, float* out);
+
 /* --------------------------------------------------------------- GEMM -- */
 /* int8_matmul_dequant / matmul_dequant_dual_rowwise, linear.hpp:54-58 / linear.cpp:39-83.
  * out[M x N] (ld N) = (qa[M x K] . qb[N x K]^T) with the state epilogue of `mode`.

@@ -39,7 +39,7 @@ EXPORTS = [
     "sb_switchback_mlp_fwd_bwd_host", "sb_switchback_mlp_fwd_bwd_host_async",
     "sb_host_pipeline_wait", "sb_stableadamw_workspace_size", "sb_stableadamw_step",
     "sb_device_alloc", "sb_device_free", "sb_copy_to_device", "sb_copy_to_host", "sb_check_finite", "sb_fp8_cast",
-    "sb_transpose_i8", "sb_compute_rms", "sb_grad_clip_global_norm", "sb_filter_nonfinite", "sb_dequantize_values",
+    "sb_transpose_i8", "sb_column_sums", "sb_compute_rms", "sb_grad_clip_global_norm", "sb_filter_nonfinite", "sb_dequantize_values",
     "sb_set_gemm_path", "sb_dp_available", "sb_dp_unique_id", "sb_dp_init", "sb_dp_rank",
     "sb_dp_allreduce_grads_async", "sb_dp_wait", "sb_dp_allreduce_max_u32", "sb_dp_allreduce_sum_f64",
     "sb_dp_destroy", "sb_dp_symmetric_alloc", "sb_dp_symmetric_open", "sb_dp_symmetric_exchange",
@@ -200,6 +200,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             "sb_check_finite": ([v, v, i32, i64], i32),
             "sb_fp8_cast": ([v, v, i64, i32, v], i32),
             "sb_transpose_i8": ([v, v, i64, i64, v], i32),
+            "sb_column_sums": ([v, v, i32, i64, i64, i64, v], i32),
             "sb_compute_rms": ([v, v, v, i64, C.c_double, v], i32),
             "sb_grad_clip_global_norm": ([v, C.POINTER(v), C.POINTER(i64), i32, C.c_double], i32),
             "sb_filter_nonfinite": ([v, C.POINTER(v), C.POINTER(v), C.POINTER(i64), i32, C.c_double, i32, v], i32),

@@ -5,6 +5,7 @@
 // (optimizer.cpp:31-42, :72-100). Reductions are fp64 in a fixed tree order (deterministic).
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "sb_internal.h"
@@ -135,6 +136,114 @@ sb_status ck(sb_handle h, const char* op) {
   return SB_OK;
 }
 
+
+// Column sums of a [rows x cols] matrix (leading dim ld) into fp32: the bias gradient of the nn
+// module's linears (sum over tokens of G). Block = 8 warps over one strip of 32 * VEC columns
+// (16-byte loads, one coalesced 512-byte row segment per warp), rows [r0, r1) of split
+// blockIdx.y; warp w takes rows r0 + w, r0 + w + 8, ... (4 loads in flight per thread), the 8
+// warps are then summed in order into part[blockIdx.y][...] (or straight into out when there
+// is one split), and k_colsum_finish adds the splits in order: deterministic for a given shape.
+template <typename T, int VEC>
+__global__ void __launch_bounds__(kT) k_colsum(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ld,
+                                               int64_t rows_per_split, float* __restrict__ part) {
+  __shared__ float red[kT / 32][32 * VEC];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 32 * VEC + lane * VEC;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_split;
+  const int64_t r1 = r0 + rows_per_split < rows ? r0 + rows_per_split : rows;
+  float acc[VEC];
+#pragma unroll
+  for (int k = 0; k < VEC; ++k) acc[k] = 0.0f;
+  const bool full = c0 + VEC <= cols;
+  int64_t r = r0 + w;
+  if (VEC > 1 && full) {
+    using V = uint4;
+    auto add = [&](const V& v) {
+      const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) acc[k] += static_cast<float>(e[k]);
+    };
+    for (; r + 24 < r1; r += 32) {
+      V v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const V*>(x + (r + 8 * u) * ld + c0));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) add(v[u]);
+    }
+    for (; r < r1; r += 8) add(__ldg(reinterpret_cast<const V*>(x + r * ld + c0)));
+  } else {
+    for (; r < r1; r += 8)
+#pragma unroll
+      for (int k = 0; k < VEC; ++k)
+        if (c0 + k < cols) acc[k] += static_cast<float>(x[r * ld + c0 + k]);
+  }
+#pragma unroll
+  for (int k = 0; k < VEC; ++k) red[w][lane * VEC + k] = acc[k];
+  __syncthreads();
+  for (int t = threadIdx.x; t < 32 * VEC; t += kT) {
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 * VEC + t;
+    if (c >= cols) continue;
+    float s = 0.0f;
+#pragma unroll
+    for (int i = 0; i < kT / 32; ++i) s += red[i][t];
+    part[static_cast<int64_t>(blockIdx.y) * cols + c] = s;
+  }
+}
+
+// out[c] = sum over splits of part[i][c]: block = 32 columns x 8 warps, warp w adds splits
+// w, w + 8, ... (coalesced 128-byte rows), then the 8 warp sums in order.
+__global__ void __launch_bounds__(kT) k_colsum_finish(const float* __restrict__ part, int splits, int64_t cols,
+                                                      float* __restrict__ out) {
+  __shared__ float red[kT / 32][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 + lane;
+  float s = 0.0f;
+  if (c < cols)
+    for (int i = w; i < splits; i += kT / 32) s += part[static_cast<int64_t>(i) * cols + c];
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && c < cols) {
+    float t = 0.0f;
+#pragma unroll
+    for (int i = 0; i < kT / 32; ++i) t += red[i][lane];
+    out[c] = t;
+  }
+}
+
+template <typename T>
+sb_status colsum_launch(sb_handle h, const T* x, int64_t rows, int64_t cols, int64_t ld, float* out) {
+  constexpr int VEC = 16 / sizeof(T);
+  const bool vec = cols % VEC == 0 && ld % VEC == 0 && sb::aligned(x, 16);
+  const int per = vec ? 32 * VEC : 32;
+  const int64_t strips = (cols + per - 1) / per;
+  // ~8 resident blocks per SM; the split partials live in the stream's scratch (<= 1 MB, the
+  // capture-time buffer's size)
+  int64_t splits = (static_cast<int64_t>(h->num_sms) * 8 + strips - 1) / strips;
+  splits = std::min<int64_t>(splits, std::max<int64_t>(1, rows / 64));
+  splits = std::min<int64_t>(splits, std::max<int64_t>(1, (1 << 20) / (cols * 4)));
+  splits = std::max<int64_t>(splits, 1);
+  const int64_t rps = (rows + splits - 1) / splits;
+  splits = (rows + rps - 1) / rps;
+  float* part = out;
+  if (splits > 1) {
+    part = reinterpret_cast<float*>(sb::scratch(h, static_cast<size_t>(splits * cols)));
+    if (!part) return sb::fail(SB_ERR_CUDA, "column_sums", "scratch allocation failed (or would grow inside a graph capture: run the op once on this stream first)");
+  }
+  const dim3 grid(static_cast<unsigned>(strips), static_cast<unsigned>(splits));
+  h->launches++;
+  if (vec)
+    k_colsum<T, VEC><<<grid, kT, 0, h->stream>>>(x, rows, cols, ld, rps, part);
+  else
+    k_colsum<T, 1><<<grid, kT, 0, h->stream>>>(x, rows, cols, ld, rps, part);
+  if (splits > 1) {
+    h->launches++;
+    k_colsum_finish<<<static_cast<unsigned>((cols + 31) / 32), kT, 0, h->stream>>>(part, static_cast<int>(splits), cols,
+                                                                                   out);
+  }
+  SB_LAUNCH_CHECK("column_sums");
+  return SB_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -213,6 +322,19 @@ sb_status sb_transpose_i8(sb_handle h, const int8_t* in, int64_t rows, int64_t c
                    h->stream>>>(in, rows, cols, out);
   SB_LAUNCH_CHECK("transpose");
   return SB_OK;
+}
+
+sb_status sb_column_sums(sb_handle h, const void* x, sb_dtype dt, int64_t rows, int64_t cols, int64_t ld, float* out) {
+  const char* op = "column_sums";
+  if (ck(h, op) != SB_OK || (!x && rows > 0) || !out || cols <= 0 || rows < 0 || ld < cols || (dt != SB_BF16 && dt != SB_F32))
+    return sb::fail(SB_ERR_INVALID_ARGUMENT, op, "bad argument (bf16 / fp32, ld >= cols > 0)");
+  if (rows == 0) {
+    cudaMemsetAsync(out, 0, static_cast<size_t>(cols) * sizeof(float), h->stream);
+    SB_LAUNCH_CHECK(op);
+    return SB_OK;
+  }
+  return dt == SB_BF16 ? colsum_launch(h, static_cast<const __nv_bfloat16*>(x), rows, cols, ld, out)
+                       : colsum_launch(h, static_cast<const float*>(x), rows, cols, ld, out);
 }
 
 sb_status sb_compute_rms(sb_handle h, const float* g, const float* u, int64_t n, double eps, double* out) {

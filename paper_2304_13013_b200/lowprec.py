@@ -184,6 +184,19 @@ def layernorm_quantize_rowwise(x: torch.Tensor, gamma: torch.Tensor, beta: torch
     return out, QuantizedMatrix(q, st, ROW), mean, rstd
 
 
+def column_sums(x: torch.Tensor) -> torch.Tensor:
+    """fp32 column sums of a 2-D bf16 / fp32 matrix (row stride may exceed the width): the nn
+    module's bias gradient, deterministic (sb_column_sums)."""
+    _need_cuda(x)
+    if x.dim() != 2 or x.stride(1) != 1 or x.stride(0) < x.shape[1]:
+        x = x.reshape(-1, x.shape[-1]).contiguous()
+    r, c = x.shape
+    out = torch.empty(c, dtype=torch.float32, device=x.device)
+    h = A.handle(x.device.index)
+    A.check(h.lib.sb_column_sums(h.h, _p(x), _dt(x), r, c, x.stride(0), _p(out)))
+    return out
+
+
 def layernorm_backward(dh: torch.Tensor, x: torch.Tensor, mean: torch.Tensor, rstd: torch.Tensor,
                        gamma: torch.Tensor):
     """Backward of layernorm_quantize_rowwise's LayerNorm: (dx bf16, dgamma fp32, dbeta fp32),

@@ -41,7 +41,7 @@ class _SwitchBackLinearFn(torch.autograd.Function):
     def backward(ctx, g: torch.Tensor):
         g = g.contiguous()
         dx, dw = L.linear_backward(ctx.mode, ctx.lctx, g, check=False)
-        db = g.sum(0, dtype=torch.float32) if ctx.has_bias and ctx.needs_input_grad[2] else None
+        db = L.column_sums(g) if ctx.has_bias and ctx.needs_input_grad[2] else None
         ctx.lctx = None
         ctx.keep_w = None
         return dx, dw, db, None, (g if ctx.needs_input_grad[4] else None)
@@ -155,7 +155,7 @@ class _LNLinearFn(torch.autograd.Function):
         x2d, mean, rstd, lctx, _ = ctx.state
         g = g.contiguous()
         dh, dw = L.linear_backward(ctx.mode, lctx, g, check=False)
-        db = g.sum(0, dtype=torch.float32) if ctx.has_bias and ctx.needs_input_grad[5] else None
+        db = L.column_sums(g) if ctx.has_bias and ctx.needs_input_grad[5] else None
         dx, dg, dbeta = _ln_backward(dh, x2d, mean, rstd, *ctx.ln, ctx.needs_input_grad[:3])
         ctx.state = None
         return dx, dg, dbeta, None, dw, db, None, (g if ctx.needs_input_grad[7] else None)
@@ -200,7 +200,7 @@ def _grouped_backward(ctx, g, gqs=None):
         gq = gqs[i] if gqs is not None else L.quantize_rowwise(g[:, i * mg:(i + 1) * mg], check=False)  # own row scales
         dx = L.int8_gemm_epilogue(gq, wt, out_dtype=g.dtype, residual=dx)  # dX_0 + dX_1 + ... in order
     dw = L.wgrad(g, h, exact=False)
-    db = g.sum(0, dtype=torch.float32) if ctx.has_bias and ctx.needs_input_grad[5] else None
+    db = L.column_sums(g) if ctx.has_bias and ctx.needs_input_grad[5] else None
     dg = dbeta = None
     if ln_state is not None:
         x2d, mean, rstd = ln_state
@@ -284,8 +284,8 @@ class _SwitchBackMLPFn(torch.autograd.Function):
         dact, dw2 = L.linear_backward(ctx.mode, c2, gy, check=False)
         g1, g1_q = L.gelu_backward_quantize_rowwise(dact, pre, check=False)
         dx, dw1 = L.linear_backward(ctx.mode, c1, g1, check=False, g_q=g1_q)
-        db1 = g1.sum(0, dtype=torch.float32) if ctx.bias[0] and ctx.needs_input_grad[5] else None
-        db2 = gy.sum(0, dtype=torch.float32) if ctx.bias[1] and ctx.needs_input_grad[7] else None
+        db1 = L.column_sums(g1) if ctx.bias[0] and ctx.needs_input_grad[5] else None
+        db2 = L.column_sums(gy) if ctx.bias[1] and ctx.needs_input_grad[7] else None
         dg = dbeta = None
         if ln_state is not None:
             x2d, mean, rstd = ln_state

@@ -59,6 +59,9 @@ pre = torch.randn(T, 5120, device="cuda").bfloat16()
 report("gelu_quantize_rowwise 65792x5120", timeit(lambda: L.gelu_quantize_rowwise(pre, check=False)), T * 5120 * 5 + 4 * T)
 report("gelu_backward_quantize 65792x5120",
        timeit(lambda: L.gelu_backward_quantize_rowwise(x5, pre, check=False)), T * 5120 * 7 + 4 * T)
+report("column_sums (bias grad) 65792x5120", timeit(lambda: L.column_sums(x5)), T * 5120 * 2)
+report("column_sums (bias grad) 65792x1280", timeit(lambda: L.column_sums(x1)), T * 1280 * 2)
+report("torch .sum(0) fp32 65792x5120 (yardstick)", timeit(lambda: x5.sum(0, dtype=torch.float32)), T * 5120 * 2)
 w = torch.randn(5120, 1280, device="cuda").bfloat16()
 report("quantize_tensorwise (+T) 5120x1280", timeit(lambda: L.quantize_tensorwise(w, check=False, with_transpose=True)),
        5120 * 1280 * 4 + 4)
