@@ -1764,8 +1764,8 @@ bool launch_quantize_tensorwise_fused(sb_handle h, const void* x, sb_dtype dt, i
                                                              q_t, ldqt, state, sync, err);
     if (done) return true;
   }
-  static int cap_bf16 = 0, cap_f32 = 0;
-  int& cap = dt == SB_BF16 ? cap_bf16 : cap_f32;
+  static int cap_bf16[16] = {}, cap_f32[16] = {};  // co-resident blocks per device
+  int& cap = (dt == SB_BF16 ? cap_bf16 : cap_f32)[h->device & 15];
   if (cap == 0) {
     int b = 0;
     if (dt == SB_BF16)
