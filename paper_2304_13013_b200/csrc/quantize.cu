@@ -578,14 +578,15 @@ __global__ void __launch_bounds__(256) k_heads_pack_quantize(const __grid_consta
   }
 }
 
-// Two rows per warp step: both rows' loads are issued before either row's math.
-template <int VPL>
-__global__ void __launch_bounds__(256, 2) k_ln_quantize_rows(const __nv_bfloat16* __restrict__ x, int64_t rows, int nvec,
-                                                          const float* __restrict__ gamma,
-                                                          const float* __restrict__ beta, float eps,
-                                                          __nv_bfloat16* __restrict__ h, int8_t* __restrict__ q,
-                                                          float* __restrict__ state, float* __restrict__ mean_out,
-                                                          float* __restrict__ rstd_out, uint32_t* err) {
+// NR rows per warp step: all NR rows' loads are issued before the first row's math. MINB =
+// the launch-bounds residency target (registers per thread <= 64K / (256 MINB)).
+template <int VPL, int NR, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_ln_quantize_rows(const __nv_bfloat16* __restrict__ x, int64_t rows,
+                                                             int nvec, const float* __restrict__ gamma,
+                                                             const float* __restrict__ beta, float eps,
+                                                             __nv_bfloat16* __restrict__ h, int8_t* __restrict__ q,
+                                                             float* __restrict__ state, float* __restrict__ mean_out,
+                                                             float* __restrict__ rstd_out, uint32_t* err) {
   // gamma / beta staged once per block in shared memory (they are re-read for every row)
   __shared__ float4 gb_s[2 * 2 * 32 * VPL];
   for (int t = threadIdx.x; t < 2 * nvec; t += blockDim.x) {
@@ -597,35 +598,49 @@ __global__ void __launch_bounds__(256, 2) k_ln_quantize_rows(const __nv_bfloat16
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   const float inv_n = 1.0f / static_cast<float>(nvec * 8);
   for (int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
-       row += 2 * warps) {
-    const int64_t row2 = row + warps;
-    uint4 v[VPL], w[VPL];
+       row += NR * warps) {
+    uint4 v[NR][VPL];
 #pragma unroll
-    for (int j = 0; j < VPL; ++j) {
-      const int i = j * 32 + lane;
-      v[j] = i < nvec ? ld_stream(reinterpret_cast<const uint4*>(x) + row * nvec + i) : make_uint4(0, 0, 0, 0);
-      w[j] = (row2 < rows && i < nvec) ? ld_stream(reinterpret_cast<const uint4*>(x) + row2 * nvec + i)
-                                       : make_uint4(0, 0, 0, 0);
-    }
-    ln_row<VPL>(v, row, nvec, lane, inv_n, eps, gb_s, h, q, state, mean_out, rstd_out, err);
-    if (row2 < rows) ln_row<VPL>(w, row2, nvec, lane, inv_n, eps, gb_s, h, q, state, mean_out, rstd_out, err);
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+        const int i = j * 32 + lane;
+        const int64_t rr = row + r * warps;
+        v[r][j] = (rr < rows && i < nvec) ? ld_stream(reinterpret_cast<const uint4*>(x) + rr * nvec + i)
+                                          : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+      if (row + r * warps < rows)
+        ln_row<VPL>(v[r], row + r * warps, nvec, lane, inv_n, eps, gb_s, h, q, state, mean_out, rstd_out, err);
   }
 }
 
+template <int VPL, int NR, int MINB>
+void launch_ln_rows_v(sb_handle h, const __nv_bfloat16* x, int64_t rows, int nvec, const float* gamma,
+                      const float* beta, float eps, __nv_bfloat16* out, int8_t* q, float* state, float* mean,
+                      float* rstd) {
+  static int blocks_per_sm[16] = {};
+  int& bps = blocks_per_sm[h->device & 15];
+  if (bps == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_ln_quantize_rows<VPL, NR, MINB>, 256, 0) != cudaSuccess ||
+        bps < 1)
+      bps = 1;
+  }
+  const int64_t need = (rows + 8 * NR - 1) / (8 * NR);
+  const int64_t blocks = std::min<int64_t>(need, static_cast<int64_t>(h->num_sms) * bps);
+  h->launches++;
+  k_ln_quantize_rows<VPL, NR, MINB><<<static_cast<unsigned>(blocks), 256, 0, h->stream>>>(
+      x, rows, nvec, gamma, beta, eps, out, q, state, mean, rstd, h->d_err);
+}
+
+// 2 rows per warp step at 2 blocks / SM measured best at 65792 x 1280 (89-90 us, 72% of HBM);
+// 3 rows at 2 blocks: 91 us; 2 rows at 3 blocks (80 registers, spills): 94 us; 1 row at 3 or 4
+// blocks: 115-117 us; 3-4 rows at 1 block: 122-125 us.
 template <int VPL>
 void launch_ln_rows(sb_handle h, const __nv_bfloat16* x, int64_t rows, int nvec, const float* gamma, const float* beta,
                     float eps, __nv_bfloat16* out, int8_t* q, float* state, float* mean, float* rstd) {
-  static int blocks_per_sm = 0;
-  if (blocks_per_sm == 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_ln_quantize_rows<VPL>, 256, 0) != cudaSuccess ||
-        blocks_per_sm < 1)
-      blocks_per_sm = 1;
-  }
-  const int64_t need = (rows + 7) / 8;
-  const int64_t blocks = std::min<int64_t>(need, static_cast<int64_t>(h->num_sms) * blocks_per_sm);
-  h->launches++;
-  k_ln_quantize_rows<VPL><<<static_cast<unsigned>(blocks), 256, 0, h->stream>>>(x, rows, nvec, gamma, beta, eps, out, q,
-                                                                                state, mean, rstd, h->d_err);
+  launch_ln_rows_v<VPL, 2, 2>(h, x, rows, nvec, gamma, beta, eps, out, q, state, mean, rstd);
 }
 
 // LayerNorm backward for the fused pre-norm path (bf16 dh, x; fp32 mean, rstd, gamma):
@@ -635,6 +650,58 @@ void launch_ln_rows(sb_handle h, const __nv_bfloat16* x, int64_t rows, int nvec,
 // beta-gradient accumulators); warp w owns rows w, w + W, ... and writes its column partials
 // to part[w][...]; k_ln_bwd_reduce sums them over w in a fixed order (deterministic).
 template <int VPL>
+__device__ __forceinline__ void ln_bwd_row(const uint4 (&vx)[VPL], const uint4 (&vd)[VPL], int64_t row, int nvec,
+                                           int lane, float inv_n, const float* __restrict__ mean,
+                                           const float* __restrict__ rstd, const float2* gs, float2* accg,
+                                           float2* accb, __nv_bfloat16* __restrict__ dx) {
+  const int64_t off = row * static_cast<int64_t>(nvec);
+  const float mu = __ldg(mean + row), rs = __ldg(rstd + row);
+  const float2 nmu = make_float2(-mu, -mu), rs2 = make_float2(rs, rs);
+  float2 s1 = make_float2(0.0f, 0.0f), s2 = make_float2(0.0f, 0.0f);
+#pragma unroll
+  for (int j = 0; j < VPL; ++j) {
+    const int i = j * 32 + lane;
+    if (i >= nvec) continue;
+    const __nv_bfloat162* px = reinterpret_cast<const __nv_bfloat162*>(&vx[j]);
+    const __nv_bfloat162* pd = reinterpret_cast<const __nv_bfloat162*>(&vd[j]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 fd = __bfloat1622float2(pd[k]);
+      const float2 xh = __fmul2_rn(__fadd2_rn(__bfloat1622float2(px[k]), nmu), rs2);
+      const float2 g = __fmul2_rn(fd, gs[k * nvec + i]);
+      s1 = __fadd2_rn(s1, g);
+      s2 = __ffma2_rn(g, xh, s2);
+      accg[k * nvec + i] = __ffma2_rn(fd, xh, accg[k * nvec + i]);
+      accb[k * nvec + i] = __fadd2_rn(accb[k * nvec + i], fd);
+    }
+  }
+  float t1 = s1.x + s1.y, t2 = s2.x + s2.y;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+    t2 += __shfl_xor_sync(0xffffffffu, t2, o);
+  }
+  const float2 nm1 = make_float2(-t1 * inv_n, -t1 * inv_n), nm2 = make_float2(-t2 * inv_n, -t2 * inv_n);
+#pragma unroll
+  for (int j = 0; j < VPL; ++j) {
+    const int i = j * 32 + lane;
+    if (i >= nvec) continue;
+    const __nv_bfloat162* px = reinterpret_cast<const __nv_bfloat162*>(&vx[j]);
+    const __nv_bfloat162* pd = reinterpret_cast<const __nv_bfloat162*>(&vd[j]);
+    uint4 o;
+    __nv_bfloat162* po = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 xh = __fmul2_rn(__fadd2_rn(__bfloat1622float2(px[k]), nmu), rs2);
+      const float2 g = __fmul2_rn(__bfloat1622float2(pd[k]), gs[k * nvec + i]);
+      // rs (g - mean(g) - xhat mean(g xhat))
+      po[k] = __float22bfloat162_rn(__fmul2_rn(__ffma2_rn(xh, nm2, __fadd2_rn(g, nm1)), rs2));
+    }
+    reinterpret_cast<uint4*>(dx)[off + i] = o;
+  }
+}
+
+template <int VPL, int NR>
 __global__ void __launch_bounds__(256) k_ln_backward_rows(const __nv_bfloat16* __restrict__ dh,
                                                           const __nv_bfloat16* __restrict__ x, int64_t rows, int nvec,
                                                           const float* __restrict__ mean,
@@ -660,59 +727,22 @@ __global__ void __launch_bounds__(256) k_ln_backward_rows(const __nv_bfloat16* _
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   const int cols = nvec * 8;
   const float inv_n = 1.0f / static_cast<float>(cols);
-  for (int64_t row = gw; row < rows; row += warps) {
-    const int64_t off = row * static_cast<int64_t>(nvec);
-    uint4 vx[VPL], vd[VPL];
+  for (int64_t row = gw; row < rows; row += NR * warps) {
+    uint4 vx[NR][VPL], vd[NR][VPL];
 #pragma unroll
-    for (int j = 0; j < VPL; ++j) {
-      const int i = j * 32 + lane;
-      vx[j] = i < nvec ? ld_stream(reinterpret_cast<const uint4*>(x) + off + i) : make_uint4(0, 0, 0, 0);
-      vd[j] = i < nvec ? ld_stream(reinterpret_cast<const uint4*>(dh) + off + i) : make_uint4(0, 0, 0, 0);
-    }
-    const float mu = __ldg(mean + row), rs = __ldg(rstd + row);
-    const float2 nmu = make_float2(-mu, -mu), rs2 = make_float2(rs, rs);
-    float2 s1 = make_float2(0.0f, 0.0f), s2 = make_float2(0.0f, 0.0f);
+    for (int r = 0; r < NR; ++r)
 #pragma unroll
-    for (int j = 0; j < VPL; ++j) {
-      const int i = j * 32 + lane;
-      if (i >= nvec) continue;
-      const __nv_bfloat162* px = reinterpret_cast<const __nv_bfloat162*>(&vx[j]);
-      const __nv_bfloat162* pd = reinterpret_cast<const __nv_bfloat162*>(&vd[j]);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 fd = __bfloat1622float2(pd[k]);
-        const float2 xh = __fmul2_rn(__fadd2_rn(__bfloat1622float2(px[k]), nmu), rs2);
-        const float2 g = __fmul2_rn(fd, gs[k * nvec + i]);
-        s1 = __fadd2_rn(s1, g);
-        s2 = __ffma2_rn(g, xh, s2);
-        accg[k * nvec + i] = __ffma2_rn(fd, xh, accg[k * nvec + i]);
-        accb[k * nvec + i] = __fadd2_rn(accb[k * nvec + i], fd);
+      for (int j = 0; j < VPL; ++j) {
+        const int i = j * 32 + lane;
+        const int64_t rr = row + r * warps;
+        const bool ok = rr < rows && i < nvec;
+        vx[r][j] = ok ? ld_stream(reinterpret_cast<const uint4*>(x) + rr * nvec + i) : make_uint4(0, 0, 0, 0);
+        vd[r][j] = ok ? ld_stream(reinterpret_cast<const uint4*>(dh) + rr * nvec + i) : make_uint4(0, 0, 0, 0);
       }
-    }
-    float t1 = s1.x + s1.y, t2 = s2.x + s2.y;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      t1 += __shfl_xor_sync(0xffffffffu, t1, o);
-      t2 += __shfl_xor_sync(0xffffffffu, t2, o);
-    }
-    const float2 nm1 = make_float2(-t1 * inv_n, -t1 * inv_n), nm2 = make_float2(-t2 * inv_n, -t2 * inv_n);
-#pragma unroll
-    for (int j = 0; j < VPL; ++j) {
-      const int i = j * 32 + lane;
-      if (i >= nvec) continue;
-      const __nv_bfloat162* px = reinterpret_cast<const __nv_bfloat162*>(&vx[j]);
-      const __nv_bfloat162* pd = reinterpret_cast<const __nv_bfloat162*>(&vd[j]);
-      uint4 o;
-      __nv_bfloat162* po = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 xh = __fmul2_rn(__fadd2_rn(__bfloat1622float2(px[k]), nmu), rs2);
-        const float2 g = __fmul2_rn(__bfloat1622float2(pd[k]), gs[k * nvec + i]);
-        // rs (g - mean(g) - xhat mean(g xhat))
-        po[k] = __float22bfloat162_rn(__fmul2_rn(__ffma2_rn(xh, nm2, __fadd2_rn(g, nm1)), rs2));
-      }
-      reinterpret_cast<uint4*>(dx)[off + i] = o;
-    }
+    for (int r = 0; r < NR; ++r)
+      if (row + r * warps < rows)
+        ln_bwd_row<VPL>(vx[r], vd[r], row + r * warps, nvec, lane, inv_n, mean, rstd, gs, accg, accb, dx);
   }
   // the block sums its warps' column accumulators in warp order (deterministic) and writes one
   // partial per block, in column order c = i * 8 + k
@@ -729,17 +759,26 @@ __global__ void __launch_bounds__(256) k_ln_backward_rows(const __nv_bfloat16* _
   }
 }
 
+template <int VPL, int NR>
+void launch_ln_bwd_v(sb_handle h, int64_t blocks, size_t smem, const __nv_bfloat16* D, const __nv_bfloat16* X,
+                     int64_t rows, int nvec, const float* mean, const float* rstd, const float* gamma, __nv_bfloat16* O,
+                     float* part) {
+  static bool attr[16] = {};  // one flag per instantiation and device
+  if (!attr[h->device & 15]) {
+    cudaFuncSetAttribute(k_ln_backward_rows<VPL, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr[h->device & 15] = true;
+  }
+  k_ln_backward_rows<VPL, NR><<<static_cast<unsigned>(blocks), 256, smem, h->stream>>>(D, X, rows, nvec, mean, rstd,
+                                                                                       gamma, O, part);
+}
+
+// one row per warp step: loading two rows ahead measured slower (121.7 vs 113.5 us at
+// 65792 x 1280; 128 registers, same 2 blocks / SM as the shared-memory accumulators allow)
 template <int VPL>
 void launch_ln_bwd(sb_handle h, int64_t blocks, size_t smem, const __nv_bfloat16* D, const __nv_bfloat16* X,
                    int64_t rows, int nvec, const float* mean, const float* rstd, const float* gamma, __nv_bfloat16* O,
                    float* part) {
-  static bool attr[16] = {};  // one flag per VPL instantiation and device
-  if (!attr[h->device & 15]) {
-    cudaFuncSetAttribute(k_ln_backward_rows<VPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr[h->device & 15] = true;
-  }
-  k_ln_backward_rows<VPL><<<static_cast<unsigned>(blocks), 256, smem, h->stream>>>(D, X, rows, nvec, mean, rstd, gamma,
-                                                                                   O, part);
+  launch_ln_bwd_v<VPL, 1>(h, blocks, smem, D, X, rows, nvec, mean, rstd, gamma, O, part);
 }
 
 // Column sums of the per-block partials [nparts][2 * cols]: block = 32 columns x 8 warps; warp w
