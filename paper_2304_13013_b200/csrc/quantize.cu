@@ -772,8 +772,9 @@ void launch_ln_bwd_v(sb_handle h, int64_t blocks, size_t smem, const __nv_bfloat
                                                                                        gamma, O, part);
 }
 
-// one row per warp step: loading two rows ahead measured slower (121.7 vs 113.5 us at
-// 65792 x 1280; 128 registers, same 2 blocks / SM as the shared-memory accumulators allow)
+// one row per warp step, 8-warp blocks, 2 per SM: loading two rows ahead measured slower (121.7
+// vs 113.5 us at 65792 x 1280; 128 registers), and so did smaller blocks with more of them per
+// SM (4 warps x 4 blocks: 119.7 us; 3 warps x 6 blocks: 139 us)
 template <int VPL>
 void launch_ln_bwd(sb_handle h, int64_t blocks, size_t smem, const __nv_bfloat16* D, const __nv_bfloat16* X,
                    int64_t rows, int nvec, const float* mean, const float* rstd, const float* gamma, __nv_bfloat16* O,
