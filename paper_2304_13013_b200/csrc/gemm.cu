@@ -484,6 +484,9 @@ cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, cons
     static int qw = -1;  // SB_DWQ_WARPS: quantizing warps per CTA (measurement knob)
     if (qw < 0) qw = getenv("SB_DWQ_WARPS") ? std::max(1, std::min(10, atoi(getenv("SB_DWQ_WARPS")))) : 10;
     p.q_warps = qw;
+    static int lag = INT32_MIN;  // SB_DWQ_LAG: pacing distance behind the producer, k-blocks (measurement knob)
+    if (lag == INT32_MIN) lag = getenv("SB_DWQ_LAG") ? atoi(getenv("SB_DWQ_LAG")) : sbdw::kLag;
+    p.q_lag = lag;
   }
   // with a fused quantize every co-resident pair takes part (pairs without a tile only quantize)
   const int grid = 2 * (rq ? max_pairs : (units < max_pairs ? units : max_pairs));

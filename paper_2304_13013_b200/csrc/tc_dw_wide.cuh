@@ -68,6 +68,7 @@ struct WParams {
   uint32_t* q_err;
   int q_warps;  // quantizing warps per CTA: warps 2 .. 2 + q_warps - 1 (<= 2 + EPI_WARPS)
   int q_idle_kb;  // leading k-blocks of G quantized by the CTAs whose pair has no tile (unpaced)
+  int q_lag;      // a working CTA quantizes k-block kb once its producer has issued kb + q_lag
 };
 
 // The quantize trails the GEMM through G: the GEMM streams G's rows (tokens) from HBM in
@@ -76,8 +77,10 @@ struct WParams {
 // read from L2 (just brought in by the GEMM's TMA) instead of a second HBM stream racing the
 // GEMM's own (measured: an unpaced quantize saturated HBM for its first ~150 us and stalled
 // the GEMM). k-block kb belongs to working CTA kb mod (working CTAs); `prog` is the producer's
-// progress (k-blocks issued), in shared memory.
-constexpr int kLag = 6;
+// progress (k-blocks issued), in shared memory. Lag sweep (C2 step, SB_DWQ_LAG): 48 / 24 / 12 /
+// 6 / 2 / 0 k-blocks -> fc1 dW 717 / 702 / 694 / 691 / 689 / 685 us; -2 .. -16 (the quantize
+// ahead of the producer) the same as 0 within noise; unpaced 847 us.
+constexpr int kLag = 0;
 constexpr int kQV = 8;  // vectors per lane in flight per step of the fused row quantizer
 template <int QV>
 __device__ __forceinline__ void quantize_g_rows(const WParams& p, int qwarp, int lane, const volatile int* prog,
@@ -93,7 +96,7 @@ __device__ __forceinline__ void quantize_g_rows(const WParams& p, int qwarp, int
   const int kb_end = idle ? min(p.q_idle_kb, qkb) : qkb;
   const int kb_step = idle ? static_cast<int>(gridDim.x) - working : working;
   for (int kb = kb0; kb < kb_end; kb += kb_step) {
-    const int need = min(kb + kLag, k_blocks);
+    const int need = min(kb + p.q_lag, k_blocks);
     while (!idle && *prog < need) __nanosleep(2000);
     const int64_t r1 = min(static_cast<int64_t>(kb + 1) * KROWS, p.q_rows);
 #pragma unroll 1
