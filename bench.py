@@ -366,14 +366,23 @@ def run_ours(args):
     # serially (--unfused-gq --no-overlap)
     fused_gq = plain and not args.unfused_gq
     overlap = plain and not args.no_overlap and not fused_gq
+    # W's tensor-wise quantizes depend on no activation: with overlap both run on the side stream
+    # at the start of the step, under the first layer's X quantize, and the first GEMM joins them
+    w_side = plain and not args.no_overlap
     ops = []
-    for l in layers:
+    if w_side:
+        for l in layers:
+            ops.append(Op(f"{l['name']} quantize_tensorwise W {l['m']}x{l['n']} (+transpose)", lambda l=l: q_w(l),
+                          "quantize", l["m"] * l["n"] * 4 + 4, stream="side"))
+    for i, l in enumerate(layers):
         nm, n, m = l["name"], l["n"], l["m"]
         if plain:
             ops.append(Op(f"{nm} quantize_rowwise X {T}x{n}", lambda l=l: q_x(l), "quantize", T * n * 3 + 4 * T))
-            ops.append(Op(f"{nm} quantize_tensorwise W {m}x{n} (+transpose)", lambda l=l: q_w(l), "quantize",
-                          m * n * 4 + 4))
-            ops.append(Op(f"{nm} int8 fwd GEMM M={T} N={m} K={n}", lambda l=l: gemm_fwd(l), "int8_gemm", 2 * T * m * n))
+            if not w_side:
+                ops.append(Op(f"{nm} quantize_tensorwise W {m}x{n} (+transpose)", lambda l=l: q_w(l), "quantize",
+                              m * n * 4 + 4))
+            ops.append(Op(f"{nm} int8 fwd GEMM M={T} N={m} K={n}", lambda l=l: gemm_fwd(l), "int8_gemm", 2 * T * m * n,
+                          join=w_side and i == 0))
         else:
             ops.append(Op(f"{nm} linear_forward", lambda l=l: layer_fwd(l), "layer", 2 * T * m * n))
     for l in reversed(layers):
@@ -1018,7 +1027,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--no-overlap", action="store_true", help="quantize G after dW on one stream")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="one stream: W quantizes in line, G quantize after dW (with --unfused-gq)")
     ap.add_argument("--unfused-gq", action="store_true",
                     help="quantize G in its own kernel instead of inside the dW GEMM launch (A/B)")
     ap.add_argument("--qkv-packed", action="store_true", help="vit_block: one scale for the packed qkv weight")
