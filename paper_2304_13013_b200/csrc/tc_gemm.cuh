@@ -188,6 +188,22 @@ __device__ __forceinline__ void arrive_leader(uint64_t* bar) {
                : "memory");
 }
 
+// OUT_BF16_RESID: the warp's 32 x 64 residual tile of a column pair, fetched into registers with
+// coalesced 16-byte loads (8 lanes per 128-byte row) one step ahead of its use — pair 0's by the
+// caller before it waits for the accumulator, pair 1's right after pair 0's is staged — so the
+// HBM latency overlaps the MMAs, the TMEM drain and the previous store instead of stalling the
+// epilogue (and, through TMEM, the MMAs).
+__device__ __forceinline__ void resid_fetch_pair(const Params& p, uint4 (&rv)[8], int rm0, int ew, int lane, int c0) {
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int rr = t * 4 + (lane >> 3), c = lane & 7;
+    const int64_t grow = static_cast<int64_t>(rm0) + ew * 32 + rr;
+    rv[t] = make_uint4(0, 0, 0, 0);
+    if (grow < p.M && c0 + 8 * c < p.N)
+      rv[t] = __ldg(reinterpret_cast<const uint4*>(p.resid + grow * p.ld_resid + c0 + 8 * c));
+  }
+}
+
 // Drain this CTA's 128 x 256 accumulator (TMEM lane quarter `ew`, column half `half`) to D:
 // tcgen05.ld -> scale / convert in registers -> SW128 smem staging -> TMA store (or reduce-add).
 // Rows [rm0, rm0 + 128) of D; the TMEM buffer is handed back (`tempty`, on the leader CTA's
@@ -195,7 +211,8 @@ __device__ __forceinline__ void arrive_leader(uint64_t* bar) {
 template <int KIND, int OUT, bool SB_COL, bool TWO>
 __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap* tmD, uint32_t t_row, uint64_t* tempty,
                                               int rm0, int n0, int ew, int half, int lane, uint8_t* buf, const float* cs,
-                                              float fr, double sa_d, float sb_tensor) {
+                                              float fr, double sa_d, float sb_tensor, uint4 (&rv)[8]) {
+  auto resid_fetch = [&](int c0) { resid_fetch_pair(p, rv, rm0, ew, lane, c0); };
 #pragma unroll 1
   for (int pr = 0; pr < 2; ++pr) {  // two 64-column pairs per warp
     uint32_t r0[32], r1[32];
@@ -223,20 +240,17 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
     if (OUT == OUT_BF16 || OUT == OUT_BF16_RESID) {
       uint32_t w[32];
       if (OUT == OUT_BF16_RESID) {
-        // stage the warp's 32 x 64 residual tile in buf with coalesced 16-byte loads (8 lanes per
-        // 128-byte row), in the same SW128 layout stage_row128 uses; each lane then reads its row
+        // stage the prefetched residual tile in buf in the SW128 layout stage_row128 uses; each
+        // lane then reads its own row
         if (lane == 0) sbptx::tma_store_wait_read<0>();  // previous store done reading buf
         __syncwarp();
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
           const int rr = t * 4 + (lane >> 3), c = lane & 7;
-          const int64_t grow = static_cast<int64_t>(rm0) + ew * 32 + rr;
-          uint4 v = make_uint4(0, 0, 0, 0);
-          if (grow < p.M && col0 + 8 * c < p.N)
-            v = __ldg(reinterpret_cast<const uint4*>(p.resid + grow * p.ld_resid + col0 + 8 * c));
-          *reinterpret_cast<uint4*>(buf + rr * 128 + ((c ^ (rr & 7)) * 16)) = v;
+          *reinterpret_cast<uint4*>(buf + rr * 128 + ((c ^ (rr & 7)) * 16)) = rv[t];
         }
         __syncwarp();
+        if (pr == 0 && col0 + 64 < p.N) resid_fetch(col0 + 64);  // the next pair's tile
       }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
@@ -503,6 +517,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         sa_d = static_cast<double>(s);
         fr = SB_COL ? s * p.post_scale : s * p.post_scale * sb_tensor;
       }
+      uint4 rv[8];
+      if (OUT == OUT_BF16_RESID && m0 < p.M) resid_fetch_pair(p, rv, m0, ew, lane, n0 + half * 128);
       {
         SB_PROBE_T0();
         sbptx::mbar_wait(&tfull_bar[acc], acc_phase);
@@ -511,7 +527,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       sbptx::tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + half * 128;
       epilogue_tile<KIND, OUT, SB_COL, false>(p, &tmD, t_row, &tempty_bar[acc], m0, n0, ew, half, lane, buf, cs, fr,
-                                             sa_d, sb_tensor);
+                                             sa_d, sb_tensor, rv);
     }
     if (lane == 0) sbptx::tma_store_wait_all<0>();
   }

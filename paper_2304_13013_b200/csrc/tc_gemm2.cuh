@@ -395,11 +395,13 @@ __global__ void __cluster_dims__(Pipe2<CFG>::CL, 1, 1) __launch_bounds__(NUM_THR
         sa_d = static_cast<double>(s);
         fr = SB_COL ? s * p.post_scale : s * p.post_scale * sb_tensor;
       }
+      uint4 rv[8];
+      if (OUT == OUT_BF16_RESID && rm0 < p.M) sbtc::resid_fetch_pair(p, rv, rm0, ew, lane, n0 + half * 128);
       { SB_PROBE_T0(); sbptx::mbar_wait(&tfull_bar[acc], acc_phase); if (lane == 0 && warp == 4) SB_PROBE_ADD(4); }
       sbptx::tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + half * 128;
       epilogue_tile<KIND, OUT, SB_COL, true>(p, &tmD, t_row, &tempty_bar[acc], rm0, n0, ew, half, lane, buf, cs, fr,
-                                            sa_d, sb_tensor);
+                                            sa_d, sb_tensor, rv);
     }
     if (lane == 0) sbptx::tma_store_wait_all<0>();
   }
