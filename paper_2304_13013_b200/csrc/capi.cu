@@ -278,6 +278,7 @@ sb_status sb_destroy(sb_handle h) {
       for (auto& e : row) cudaEventDestroy(e);
     cudaEventDestroy(h->hp_start);
     cudaEventDestroy(h->hp_wready);
+    cudaEventDestroy(h->hp_w1ready);
   }
   delete h;
   return SB_OK;
@@ -884,6 +885,7 @@ static sb_status host_pool_acquire(sb_handle h, const char* op, size_t need, int
       for (auto& e : row) SB_CUDA_CHECK(op, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     SB_CUDA_CHECK(op, cudaEventCreateWithFlags(&h->hp_start, cudaEventDisableTiming));
     SB_CUDA_CHECK(op, cudaEventCreateWithFlags(&h->hp_wready, cudaEventDisableTiming));
+    SB_CUDA_CHECK(op, cudaEventCreateWithFlags(&h->hp_w1ready, cudaEventDisableTiming));
     for (auto& e : h->pool_done) SB_CUDA_CHECK(op, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   const int pi = h->pool_next;
@@ -1120,16 +1122,20 @@ static sb_status mlp_host_enqueue(sb_handle h, const sb_linear_mode* mode, int a
   cudaEvent_t* ev_in = h->hp_ev[0];
   cudaEvent_t* ev_y = h->hp_ev[1];
   cudaEvent_t* ev_comp = h->hp_ev[2];
+  cudaEvent_t* ev_x = h->hp_ev[4];
   cudaEvent_t* ev_out = h->hp_ev[3];
   cudaStream_t comp = h->stream, s_in = h->s_in, s_out = h->s_out;
   host_pool_begin(h, pi);
-  // chunk i covers rows [cuts[i], cuts[i + 1]). Tapered at both ends: a quarter chunk first, so
-  // the first Y leaves (and the D2H direction starts) sooner, and a quarter chunk last, so less
-  // compute and fewer bytes are left for the un-overlapped drain after the last upload.
-  // SB_HOST_FIRST sets the taper rows, SB_HOST_TAPER=0 turns it off (measurement knobs).
+  // chunk i covers rows [cuts[i], cuts[i + 1]). Tapered at both ends: a quarter chunk q first, so
+  // the first Y leaves (and the D2H direction starts) sooner, and chunks halving down to q at
+  // the end, so less compute and fewer bytes (the D2H backlog) are left for the un-overlapped
+  // drain after the last upload (9.53 vs 9.58 ms per C2 step with one q chunk last).
+  // SB_HOST_FIRST sets q, SB_HOST_TAPER=1 ends with one q chunk, =0 turns the taper off
+  // (measurement knobs).
   const char* fe = std::getenv("SB_HOST_FIRST");
   const char* te = std::getenv("SB_HOST_TAPER");
   const bool taper = !(te && te[0] == '0');
+  const bool geo = !(te && te[0] == '1');  // end taper: halving toward q (SB_HOST_TAPER=1: one q chunk)
   std::vector<int64_t> cuts{0};
   if (b <= chunk) {  // a batch that fits one chunk stays one chunk
     cuts.push_back(b);
@@ -1139,7 +1145,11 @@ static sb_status mlp_host_enqueue(sb_handle h, const sb_linear_mode* mode, int a
     cuts.push_back(r);
     while (r < b) {
       const int64_t rem = b - r;
-      const int64_t step = !taper ? std::min(rem, chunk) : rem <= q ? rem : rem <= chunk + q ? rem - q : chunk;
+      const int64_t step = !taper ? std::min(rem, chunk)
+                           : geo   ? (rem <= q ? rem : std::min(chunk, std::max(q, rem / 2)))
+                           : rem <= q ? rem
+                           : rem <= chunk + q ? rem - q
+                                              : chunk;
       r += step;
       cuts.push_back(r);
     }
@@ -1147,26 +1157,40 @@ static sb_status mlp_host_enqueue(sb_handle h, const sb_linear_mode* mode, int a
   const int64_t nchunks = static_cast<int64_t>(cuts.size()) - 1;
   auto r0_of = [&](int64_t i) { return cuts[i]; };
   auto rows_of = [&](int64_t i) { return cuts[i + 1] - cuts[i]; };
-  auto h2d = [&](int64_t i) {
+  // a chunk's x (ev_x: its forward may start) then its g (ev_in: its backward may start)
+  auto h2d_x = [&](int64_t i) {
     const int s = static_cast<int>(i % NS);
     const int64_t r0 = r0_of(i), rows = rows_of(i);
     if (i >= NS) cudaStreamWaitEvent(s_in, ev_comp[s], 0);  // slot's x, g consumed by chunk i-NS
     cudaMemcpyAsync(P[NFIX + 4 * s + 0], static_cast<const uint8_t*>(x) + r0 * n * es, rows * n * es,
                     cudaMemcpyHostToDevice, s_in);
+    cudaEventRecord(ev_x[s], s_in);
+  };
+  auto h2d_g = [&](int64_t i) {
+    const int s = static_cast<int>(i % NS);
+    const int64_t r0 = r0_of(i), rows = rows_of(i);
     cudaMemcpyAsync(P[NFIX + 4 * s + 1], static_cast<const uint8_t*>(g) + r0 * m * es, rows * m * es,
                     cudaMemcpyHostToDevice, s_in);
     cudaEventRecord(ev_in[s], s_in);
   };
+  auto h2d = [&](int64_t i) {
+    h2d_x(i);
+    h2d_g(i);
+  };
   sb_status st = SB_OK;
-  // W1, then the first chunk, then W2 on the upload stream (in the order the first chunk's
-  // kernels need them); both weights quantized once (both layouts)
+  // upload order = the order the first chunk's kernels need them: W1, x_0, W2 (the forward),
+  // then g_0 (the backward); each weight quantized once (both layouts) as soon as it is in
   cudaMemcpyAsync(P[W1], w1, hd * n * es, cudaMemcpyHostToDevice, s_in);
-  h2d(0);
+  cudaEventRecord(h->hp_w1ready, s_in);
+  h2d_x(0);
   cudaMemcpyAsync(P[W2], w2, m * hd * es, cudaMemcpyHostToDevice, s_in);
   cudaEventRecord(h->hp_wready, s_in);
-  cudaStreamWaitEvent(comp, h->hp_wready, 0);
+  h2d_g(0);
+  const char* wl = std::getenv("SB_HOST_W2LATE");
+  const bool w2late = !(wl && wl[0] == '0');
+  cudaStreamWaitEvent(comp, w2late ? h->hp_w1ready : h->hp_wready, 0);
   st = q_tensorwise(h, P[W1], dt, hd, n, n, I8(W1Q), n, I8(W1QT), hd, F(WST1), static_cast<unsigned int*>(P[WRD1]));
-  if (st == SB_OK)
+  if (!w2late && st == SB_OK)
     st = q_tensorwise(h, P[W2], dt, m, hd, hd, I8(W2Q), hd, I8(W2QT), m, F(WST2), static_cast<unsigned int*>(P[WRD2]));
   for (int64_t i = 1; i < std::min<int64_t>(NS - 1, nchunks); ++i) h2d(i);
   auto qrow = [&](const void* src, int64_t rows, int64_t cols, int8_t* q, float* s) {
@@ -1181,7 +1205,7 @@ static sb_status mlp_host_enqueue(sb_handle h, const sb_linear_mode* mode, int a
     const int s = static_cast<int>(i % NS);
     const int64_t r0 = r0_of(i), rows = rows_of(i);
     if (i + NS - 1 < nchunks) h2d(i + NS - 1);
-    cudaStreamWaitEvent(comp, ev_in[s], 0);
+    cudaStreamWaitEvent(comp, ev_x[s], 0);
     if (i >= NS) cudaStreamWaitEvent(comp, ev_out[s], 0);  // slot's y, dx copied out
     void* xd = P[NFIX + 4 * s + 0];
     void* gd = P[NFIX + 4 * s + 1];
@@ -1194,9 +1218,16 @@ static sb_status mlp_host_enqueue(sb_handle h, const sb_linear_mode* mode, int a
       act(0, P[PRE], nullptr, rows, P[ACT], I8(HQ), F(HS));
     else
       qrow(P[PRE], rows, hd, I8(HQ), F(HS));
+    if (i == 0 && w2late) {  // W2 arrives after x_0: its quantize runs after fc1's first chunk
+      cudaStreamWaitEvent(comp, h->hp_wready, 0);
+      if (st == SB_OK)
+        st = q_tensorwise(h, P[W2], dt, m, hd, hd, I8(W2Q), hd, I8(W2QT), m, F(WST2),
+                          static_cast<unsigned int*>(P[WRD2]));
+    }
     if (st == SB_OK) st = sb::gemm_i8(h, I8(HQ), F(HS), I8(W2Q), F(WST2), SB_SCALE_ROW_TENSOR, rows, m, hd, yd, dt, mode->exact);
     cudaEventRecord(ev_y[s], comp);
     // backward: fc2 (dW2 with G's quantize in the launch, then dA), then fc1
+    cudaStreamWaitEvent(comp, ev_in[s], 0);
     const sb::RowQuant rq2{I8(GQ), m, F(GS)};
     if (st == SB_OK) st = sb::wgrad(h, gd, P[ACT], dt, rows, m, hd, F(DW2), mode->exact, i > 0, &rq2);
     const bool last = i == nchunks - 1;

@@ -37,9 +37,10 @@ struct sb_handle_s {
   int gemm_path = 0;  // sb_gemm_path
   // host-buffer pipeline (sb_switchback_fwd_bwd_host): copy streams + events, created once
   cudaStream_t s_in = nullptr, s_out = nullptr;
-  cudaEvent_t hp_ev[4][8] = {};  // [in, y, comp, out][slot] (host pipeline, up to 8 slots)
+  cudaEvent_t hp_ev[5][8] = {};  // [in, y, comp, out, x in][slot] (host pipeline, up to 8 slots)
   cudaEvent_t hp_start = nullptr;
-  cudaEvent_t hp_wready = nullptr;  // MLP host pipeline: both weights uploaded
+  cudaEvent_t hp_wready = nullptr;   // MLP host pipeline: both weights uploaded
+  cudaEvent_t hp_w1ready = nullptr;  // MLP host pipeline: W1 uploaded
   // two device pools used by alternate host-pipeline calls, so an async call's transfers
   // overlap the previous call's drain without aliasing its buffers
   void* dev_pool[2] = {nullptr, nullptr};
