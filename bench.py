@@ -944,7 +944,8 @@ def e2e_host(args, L, torch, world=1, dev=None):
     gg = torch.randn(T, m, generator=g).to(torch.bfloat16).pin_memory()
     h2d = (x.numel() + w1.numel() + w2.numel() + gg.numel()) * 2
     d2h = (T * m + T * n) * 2 + (w1.numel() + w2.numel()) * 4
-    for _ in range(max(1, args.warmup // 2)):
+    # >= 2 warm-up calls: the entry alternates two device pools, each allocated on first use
+    for _ in range(max(3, args.warmup)):
         L.switchback_mlp_fwd_bwd_host(x, w1, w2, gg, A.SB_ACT_NONE)
     steps = max(1, min(args.steps, 10))
     torch.cuda.synchronize()
@@ -957,7 +958,7 @@ def e2e_host(args, L, torch, world=1, dev=None):
     dt = dp.max_over_ranks((time.perf_counter() - t0) / steps, dev)
     return {"value": T * world / dt, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ranks": world,
-            "path": "sb_switchback_mlp_fwd_bwd_host (C-ABI, pinned host buffers, 8192-token chunks: H2D / kernels / "
+            "path": "sb_switchback_mlp_fwd_bwd_host (C-ABI, pinned host buffers, 4096-token chunks: H2D / kernels / "
                     "D2H overlapped on three streams, hidden activation kept in HBM), one synchronous call per step",
             "pcie_note": "H2D and D2H share the link: ~93 GB/s combined measured (tools/pcie_bw.py), so the "
                          "752 MB of host traffic per step has an ~8.1 ms floor",
@@ -977,7 +978,7 @@ def e2e_host_per_linear(args, L, torch):
         bufs.append((x, w, gg))
     h2d = sum(x.numel() * 2 + w.numel() * 2 + gg.numel() * 2 for x, w, gg in bufs)
     d2h = sum(x.shape[0] * w.shape[0] * 2 + x.numel() * 2 + w.numel() * 4 for x, w, gg in bufs)
-    for _ in range(max(1, args.warmup // 2)):
+    for _ in range(max(3, args.warmup)):  # both device pools allocated before the timed calls
         L.switchback_fwd_bwd_host_many(bufs)
     steps = max(1, min(args.steps, 5))
     torch.cuda.synchronize()

@@ -1068,12 +1068,13 @@ static sb_status mlp_host_enqueue(sb_handle h, const sb_linear_mode* mode, int a
     return sb::fail(SB_ERR_UNSUPPORTED, op, "GELU runs on the bf16 performance path");
   const size_t es = sb::dt_size(dt);
   const bool gelu = activation == SB_ACT_GELU;
-  // 8192-row chunks after a 2048-row first chunk measured best at the C2 shape (9.6 ms per call,
-  // 84% of the bidirectional PCIe floor; tools/mlp_e2e_sweep.py): the kernels of a chunk take
-  // half its copies, so fewer, larger chunks waste less on launch gaps and small GEMM waves
+  // 4096-row chunks (1024-row first chunk, halving end taper) measured best at the C2 shape once
+  // a chunk's forward waits only for its x (tools/mlp_e2e_sweep.py, one box, alternating runs):
+  // 8.87 ms per call against 9.03 / 9.27 / 9.39 / 9.45 ms at 3584 / 4608 / 5120 / 8192 rows and
+  // 9.82 ms at 2048 (with both x and g awaited, 8192 had been best)
   int NS = 4;
-  int64_t chunk = 8192;
-  host_chunking(b, 8192, &NS, &chunk);
+  int64_t chunk = 4096;
+  host_chunking(b, 4096, &NS, &chunk);
   // pool layout: weights {W1, W2, payloads (both layouts), states, words}, dW1, dW2; the
   // compute-only chunk buffers once (one compute stream); NS copy slots {x, g, y, dx}
   enum { W1, W2, W1Q, W1QT, W2Q, W2QT, WST1, WST2, WRD1, WRD2, DW1, DW2, XQ, XS, PRE, ACT, HQ, HS, GQ, GS, DA,

@@ -16,7 +16,7 @@ case "${PART:-1}" in
   timeout 400 python bench.py --dw-comm fused --no-e2e --no-cpu > gpurun_out/bench_c2_dw_comm_fused.json 2>/dev/null
   timeout 400 python bench.py --config c5 --zero1 --no-cpu > gpurun_out/bench_c5_zero1.json 2>/dev/null
   timeout 300 python tools/hbm_kernels.py > gpurun_out/hbm_kernels.txt 2>&1
-  timeout 300 python tools/mlp_e2e_sweep.py 8192:0:1,8192:0:0,4096:0:1,16384:0:1 > gpurun_out/mlp_e2e_sweep.txt 2>&1
+  timeout 300 python tools/mlp_e2e_sweep.py 4096:0:2,4096:0:1,4096:0:0,8192:0:2,3072:0:2,6144:0:2 > gpurun_out/mlp_e2e_sweep.txt 2>&1
   timeout 300 python tools/e2e_timeline.py > gpurun_out/e2e_timeline.txt 2>&1
   timeout 300 python tools/pcie_bw.py > gpurun_out/pcie_bw.txt 2>&1
   timeout 600 python bench.py --impl reference > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
