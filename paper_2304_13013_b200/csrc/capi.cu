@@ -985,16 +985,19 @@ static sb_status fwd_bwd_host_enqueue(sb_handle h, const sb_linear_mode* mode, c
   cudaEvent_t* ev_y = h->hp_ev[1];
   cudaEvent_t* ev_comp = h->hp_ev[2];
   cudaEvent_t* ev_out = h->hp_ev[3];
+  cudaEvent_t* ev_x = h->hp_ev[4];
 
   cudaStream_t comp = h->stream, s_in = h->s_in, s_out = h->s_out;
   host_pool_begin(h, pi);
   sb_status st = SB_OK;
   const int64_t nchunks = (b + chunk - 1) / chunk;
+  // a chunk's x (ev_x: its forward may start), then its g (ev_in: its backward may start)
   auto h2d = [&](int64_t i) {
     const int s = static_cast<int>(i % NS);
     const int64_t r0 = i * chunk, rows = std::min(chunk, b - r0);
     if (i >= NS) cudaStreamWaitEvent(s_in, ev_comp[s], 0);  // slot's x, g consumed by chunk i-NS
     cudaMemcpyAsync(P[6 + 8 * s + 0], static_cast<const uint8_t*>(x) + r0 * n * es, rows * n * es, cudaMemcpyHostToDevice, s_in);
+    cudaEventRecord(ev_x[s], s_in);
     cudaMemcpyAsync(P[6 + 8 * s + 1], static_cast<const uint8_t*>(g) + r0 * m * es, rows * m * es, cudaMemcpyHostToDevice, s_in);
     cudaEventRecord(ev_in[s], s_in);
   };
@@ -1007,7 +1010,7 @@ static sb_status fwd_bwd_host_enqueue(sb_handle h, const sb_linear_mode* mode, c
     const int s = static_cast<int>(i % NS);
     const int64_t r0 = i * chunk, rows = std::min(chunk, b - r0);
     if (i + NS - 1 < nchunks) h2d(i + NS - 1);
-    cudaStreamWaitEvent(comp, ev_in[s], 0);
+    cudaStreamWaitEvent(comp, ev_x[s], 0);
     if (i >= NS) cudaStreamWaitEvent(comp, ev_out[s], 0);  // slot's y, dx copied out
     void* xd = P[6 + 8 * s + 0];
     void* gd = P[6 + 8 * s + 1];
@@ -1020,10 +1023,11 @@ static sb_status fwd_bwd_host_enqueue(sb_handle h, const sb_linear_mode* mode, c
     if (sb::launch_quantize_rowwise(h, xd, dt, rows, n, n, xq, n, xs) != cudaSuccess) st = sb::cuda_fail(op, cudaGetLastError());
     if (st == SB_OK) st = sb::gemm_i8(h, xq, xs, wq, wstate, SB_SCALE_ROW_TENSOR, rows, m, n, yd, dt, mode->exact);
     cudaEventRecord(ev_y[s], comp);
-    if (st == SB_OK && sb::launch_quantize_rowwise(h, gd, dt, rows, m, m, gq, m, gs) != cudaSuccess)
-      st = sb::cuda_fail(op, cudaGetLastError());
+    // backward: dW += G^T X with G's row-wise quantize in the same launch, then the dX GEMM
+    cudaStreamWaitEvent(comp, ev_in[s], 0);
+    const sb::RowQuant rq{gq, m, gs};
+    if (st == SB_OK) st = sb::wgrad(h, gd, xd, dt, rows, m, n, dwd, mode->exact, i > 0, &rq);
     if (st == SB_OK) st = sb::gemm_i8(h, gq, gs, wqt, wstate, SB_SCALE_ROW_TENSOR, rows, n, m, dxd, dt, mode->exact);
-    if (st == SB_OK) st = sb::wgrad(h, gd, xd, dt, rows, m, n, dwd, mode->exact, i > 0);
     cudaEventRecord(ev_comp[s], comp);
     cudaStreamWaitEvent(s_out, ev_y[s], 0);
     cudaMemcpyAsync(static_cast<uint8_t*>(y) + r0 * m * es, yd, rows * m * es, cudaMemcpyDeviceToHost, s_out);
