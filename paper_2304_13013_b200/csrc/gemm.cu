@@ -446,17 +446,27 @@ int dw_wide_pairs(sb_handle h) {
   return attr_err != cudaSuccess ? 0 : max_pairs;
 }
 
+// The one-wave dW tiling plan for an m x n dW on max_pairs co-resident pairs: false = use the
+// 256 x 256 path. Both orientations are tried; with one wave in either, the one with fewer tiles
+// (e.g. 3840 x 1280: 50 full 256 x 384 tiles transposed against 60 with 15 of them a third wide,
+// 489 vs 510 us). Worth it only when the 256 x 256 tiling would leave a partial wave and the
+// one-wave tiling keeps most pairs busy.
+bool dw_wide_plan(int max_pairs, int64_t m, int64_t n, bool* trans) {
+  const int64_t u_direct = ((m + sbdw::WM - 1) / sbdw::WM) * ((n + sbdw::WN - 1) / sbdw::WN);
+  const int64_t u_trans = ((n + sbdw::WM - 1) / sbdw::WM) * ((m + sbdw::WN - 1) / sbdw::WN);
+  const bool d_ok = u_direct <= max_pairs, t_ok = u_trans <= max_pairs;
+  if (!d_ok && !t_ok) return false;
+  *trans = !d_ok || (t_ok && u_trans < u_direct);
+  const int64_t u256 = ((m + 255) / 256) * ((n + 255) / 256);
+  return !(u256 % max_pairs == 0 || std::max(d_ok ? u_direct : 0, t_ok ? u_trans : 0) * 4 < max_pairs * 3);
+}
+
 cudaError_t launch_dw_wide(sb_handle h, const Operand& G, const Operand& X, const CUtensorMap& td, int64_t m, int64_t n,
                            int64_t T, const sb::RowQuant* rq, const sbdw::DMaps<8>* rs = nullptr) {
   const int max_pairs = dw_wide_pairs(h);
   if (max_pairs <= 0) return cudaErrorNotSupported;
-  const int64_t u_direct = ((m + sbdw::WM - 1) / sbdw::WM) * ((n + sbdw::WN - 1) / sbdw::WN);
-  const int64_t u_trans = ((n + sbdw::WM - 1) / sbdw::WM) * ((m + sbdw::WN - 1) / sbdw::WN);
-  const bool trans = u_direct > max_pairs;
-  if (trans && u_trans > max_pairs) return cudaErrorNotSupported;
-  // worth it only when the 256 x 256 tiling would leave a partial wave
-  const int64_t u256 = ((m + 255) / 256) * ((n + 255) / 256);
-  if (u256 % max_pairs == 0 || (trans ? u_trans : u_direct) * 4 < max_pairs * 3) return cudaErrorNotSupported;
+  bool trans = false;
+  if (!dw_wide_plan(max_pairs, m, n, &trans)) return cudaErrorNotSupported;
   const Operand& Aop = trans ? X : G;
   const Operand& Bop = trans ? G : X;
   CUtensorMap ta, tb;
@@ -840,17 +850,12 @@ sb_status wgrad(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t 
 }
 
 bool dw_wide_serves(sb_handle h, int64_t m, int64_t n, int64_t b) {
-  // the shape rule of launch_dw_wide (one orientation fits the co-resident pairs in one wave, and
-  // the 256 x 256 tiling would leave a partial wave), with the device's co-resident pair count
+  // the shape rule of launch_dw_wide (dw_wide_plan) with the device's co-resident pair count
   if (b <= 0 || b >= (1LL << 31) || m % 8 || n % 8) return false;
   const int max_pairs = dw_wide_pairs(h);
   if (max_pairs <= 0) return false;
-  const int64_t u_direct = ((m + sbdw::WM - 1) / sbdw::WM) * ((n + sbdw::WN - 1) / sbdw::WN);
-  const int64_t u_trans = ((n + sbdw::WM - 1) / sbdw::WM) * ((m + sbdw::WN - 1) / sbdw::WN);
-  const bool trans = u_direct > max_pairs;
-  if (trans && u_trans > max_pairs) return false;
-  const int64_t u256 = ((m + 255) / 256) * ((n + 255) / 256);
-  return !(u256 % max_pairs == 0 || (trans ? u_trans : u_direct) * 4 < max_pairs * 3);
+  bool trans = false;
+  return dw_wide_plan(max_pairs, m, n, &trans);
 }
 
 sb_status wgrad_reduce_scatter(sb_handle h, const void* g, const void* x, sb_dtype dt, int64_t b, int64_t m, int64_t n,
