@@ -144,3 +144,33 @@ def test_unaligned_widths_take_the_fallback_kernels(dtype, chunk_env):
     yd, dxd, dw1d, dw2d = _device_mlp(x, w1, w2, g, False)
     assert torch.equal(y, yd) and torch.equal(dx, dxd)
     assert rel_err(dw1.numpy(), dw1d.numpy()) < 1e-4 and rel_err(dw2.numpy(), dw2d.numpy()) < 1e-4
+
+
+@pytest.mark.parametrize("taper,first,w2late", [("0", None, "1"), ("1", "512", "1"), ("2", "300", "0"), ("2", None, "1")])
+def test_chunk_schedules_agree(taper, first, w2late, chunk_env):
+    """Every chunk schedule of the pipeline (no taper, one short last chunk, chunks halving at the
+    end, odd first-chunk sizes, W2 quantized up front or after the first chunk) gives Y / dX
+    bit-identical to the device-resident layer API; dW differs only by the chunked fp32 sum order."""
+    b, n, hd, m = 9000, 256, 512, 256
+    chunk_env(2048)
+    keys = ("SB_HOST_TAPER", "SB_HOST_FIRST", "SB_HOST_W2LATE")
+    old = {k: os.environ.get(k) for k in keys}
+    try:
+        os.environ["SB_HOST_TAPER"] = taper
+        os.environ["SB_HOST_W2LATE"] = w2late
+        if first:
+            os.environ["SB_HOST_FIRST"] = first
+        else:
+            os.environ.pop("SB_HOST_FIRST", None)
+        x, w1, w2, g = _inputs(b, n, hd, m, 11, torch.bfloat16)
+        for act in (A.SB_ACT_NONE, A.SB_ACT_GELU):
+            y, dx, dw1, dw2 = L.switchback_mlp_fwd_bwd_host(x, w1, w2, g, activation=act)
+            yd, dxd, dw1d, dw2d = _device_mlp(x, w1, w2, g, act == A.SB_ACT_GELU)
+            assert torch.equal(y, yd) and torch.equal(dx, dxd)
+            assert rel_err(dw1.numpy(), dw1d.numpy()) < 1e-4 and rel_err(dw2.numpy(), dw2d.numpy()) < 1e-4
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
