@@ -960,8 +960,8 @@ def e2e_host(args, L, torch, world=1, dev=None):
             "ranks": world,
             "path": "sb_switchback_mlp_fwd_bwd_host (C-ABI, pinned host buffers, 4096-token chunks: H2D / kernels / "
                     "D2H overlapped on three streams, hidden activation kept in HBM), one synchronous call per step",
-            "pcie_note": "H2D and D2H share the link: ~93 GB/s combined measured (tools/pcie_bw.py), so the "
-                         "752 MB of host traffic per step has an ~8.1 ms floor",
+            "pcie_note": "H2D and D2H share the link: 91-100 GB/s combined measured (tools/pcie_bw.py), so "
+                         "the 752 MB of host traffic per step has a ~7.5-8.2 ms floor",
             "bytes_note": "h2d / d2h bytes are per rank and step", "steps": steps}
 
 
