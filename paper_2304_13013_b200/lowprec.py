@@ -654,20 +654,30 @@ def switchback_fwd_bwd_host(x, w, g, exact: bool = False):
 
 
 def switchback_mlp_fwd_bwd_host(x, w1, w2, g, activation: int = A.SB_ACT_NONE, exact: bool = False,
-                                wait: bool = True):
+                                wait: bool = True, out=None):
     """The MLP block of transformer_block / block_backward (model.cpp:324-329, 351-360) over
     HOST tensors: y = fc2(act(fc1(x))) and its backward for the block-output gradient g, the
     hidden activation kept on the device. x (b, n), w1 (hd, n), w2 (m, hd), g (b, m) pinned CPU
     tensors; returns (y, dx, dw1, dw2) on the host. wait=False enqueues only
-    (sb_switchback_mlp_fwd_bwd_host_async; call host_pipeline_wait() before reading)."""
+    (sb_switchback_mlp_fwd_bwd_host_async; call host_pipeline_wait() before reading).
+    out: optional preallocated pinned (y, dx, dw1, dw2) to write into (e.g. alternating sets
+    for back-to-back async calls)."""
     b, n = x.shape
     hd, m = w1.shape[0], w2.shape[0]
     if w1.shape[1] != n or w2.shape[1] != hd or tuple(g.shape) != (b, m):
         raise ValueError("switchback_mlp_fwd_bwd: shape mismatch")
-    y = torch.empty((b, m), dtype=x.dtype, pin_memory=True)
-    dx = torch.empty((b, n), dtype=x.dtype, pin_memory=True)
-    dw1 = torch.empty((hd, n), dtype=torch.float32, pin_memory=True)
-    dw2 = torch.empty((m, hd), dtype=torch.float32, pin_memory=True)
+    if out is not None:
+        y, dx, dw1, dw2 = out
+        want = (((b, m), x.dtype), ((b, n), x.dtype), ((hd, n), torch.float32), ((m, hd), torch.float32))
+        for t, (shape, dtype) in zip(out, want):
+            if tuple(t.shape) != shape or t.dtype != dtype or not t.is_contiguous() or t.is_cuda:
+                raise ValueError("switchback_mlp_fwd_bwd: out buffers must be contiguous host tensors "
+                                 "(y, dx in x's dtype; dw1, dw2 fp32) of the output shapes")
+    else:
+        y = torch.empty((b, m), dtype=x.dtype, pin_memory=True)
+        dx = torch.empty((b, n), dtype=x.dtype, pin_memory=True)
+        dw1 = torch.empty((hd, n), dtype=torch.float32, pin_memory=True)
+        dw2 = torch.empty((m, hd), dtype=torch.float32, pin_memory=True)
     h = A.handle()
     md = LinearMode(A.SB_SWITCHBACK, A.SB_INT8, exact=exact)
     fn = h.lib.sb_switchback_mlp_fwd_bwd_host if wait else h.lib.sb_switchback_mlp_fwd_bwd_host_async
