@@ -174,3 +174,20 @@ def test_chunk_schedules_agree(taper, first, w2late, chunk_env):
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
+
+
+def test_async_into_alternating_out_buffers():
+    """Back-to-back async calls writing into two alternating preallocated output sets (the
+    pipelined use): every call's outputs equal the synchronous call's."""
+    b, n, hd, m = 10000, 256, 768, 256
+    x, w1, w2, g = _inputs(b, n, hd, m, 12, torch.bfloat16)
+    ref = L.switchback_mlp_fwd_bwd_host(x, w1, w2, g)
+    outs = [tuple(torch.empty_like(t).pin_memory() for t in ref) for _ in range(2)]
+    for i in range(5):
+        L.switchback_mlp_fwd_bwd_host(x, w1, w2, g, wait=False, out=outs[i % 2])
+    L.host_pipeline_wait()
+    for o in outs:
+        for a, r in zip(o, ref):
+            assert torch.equal(a, r)
+    with pytest.raises(ValueError):
+        L.switchback_mlp_fwd_bwd_host(x, w1, w2, g, out=(outs[0][0], outs[0][1], outs[0][3], outs[0][2]))  # dw1 / dw2 swapped
